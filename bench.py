@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""bench.py — B200 benchmark of the LiLAC harness path (BASELINE.json metric).
+
+Workload (N=1 default): NPB CG class C (configs[1] of BASELINE.json): n=150000,
+nonzer=15, shift=110, fp64 CSR, matrix resident in HBM, synthetic input from
+NPB's own generator (makea). One *step* = one NPB outer iteration = conj_grad
+(25 CG steps: fused SpMV+dot, z/r update+dot, p update) + residual SpMV +
+norms/x update = 26 SpMVs, captured as one CUDA graph.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). `value` = NPB iterations/s over the whole job,
+device-resident; `e2e` = the same metric through the C-ABI harness entry points
+(b200_spmv_csr / b200_dot / b200_axpy / b200_xpay) from pinned host buffers,
+i.e. the LiLAC model where the host program keeps its CG loop; `roofline`
+= the SpMV kernel's achieved HBM GB/s vs the measured copy peak; `cpu_baseline`
+= the reference's own CPU harness (oracle/_ref, interp.cpp:330-389) on a
+bounded sample, timed on this box's host cores.
+N>1 (torchrun): weak-scaling replicas — each rank runs its own class-C
+solve on its GPU (no data-path collective); value = sum of iterations / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMV GFLOP/s & HBM GB/s (% of roofline); NPB-CG iters/sec at 1/2/4/8 B200"
+UNIT = "NPB-CG iters/s"
+NPB = {  # na, nonzer, niter, shift, zeta_verify (NPB 3.x)
+    "S": (1400, 7, 15, 10.0, 8.5971775078648),
+    "A": (14000, 11, 15, 20.0, 17.130235054029),
+    "B": (75000, 13, 75, 60.0, 22.712745482631),
+    "C": (150000, 15, 75, 110.0, 28.973605592845),
+}
+CGITMAX = 25
+SPMV_PER_STEP = CGITMAX + 1
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--npb-class", default="C", choices=sorted(NPB))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--spmv-reps", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_info():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def cpu_desc():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+# ------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ------------------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "utilization.gpu"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return self
+
+        def pump():
+            for line in self.proc.stdout:
+                self.rows.append([c.strip() for c in line.split(",")])
+
+        self.thread = threading.Thread(target=pump, daemon=True)
+        self.thread.start()
+        return self
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=1)
+        rows = [r for r in self.rows if len(r) == len(self.FIELDS)]
+        sm = []
+        reasons = set()
+        sm_max = None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        loaded = [r for r in rows if _num(r[7]) and _num(r[7]) > 0] or rows
+        for r in loaded:
+            if _num(r[0]):
+                sm.append(_num(r[0]))
+            if _num(r[1]):
+                sm_max = _num(r[1])
+            for k, nm in enumerate(names):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": sm_max,
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+def _num(s):
+    try:
+        return float(s)
+    except (TypeError, ValueError):
+        return None
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_substr: str):
+    """Per-launch DRAM bytes of the SpMV kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        for k, v in d.get("kernels", {}).items():
+            if kernel_substr in k:
+                return v.get("dram_bytes")
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+# ------------------------------------------------------------------------------------
+# reference CPU harness (oracle/_ref) — the baseline arm
+# ------------------------------------------------------------------------------------
+
+def reference_sample(rp, ci, val, n, reps=1, row_frac=8):
+    """Times the reference's own HarnessFn ("lilac.spmv_csr", interp.cpp:330-389)
+    on the first rows/row_frac rows (a bounded sample of the SpMV) and
+    "lilac.dotproduct" on full-length vectors. Returns (seconds per NPB
+    iteration extrapolated, kind, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    rows_s = max(1, n // row_frac)
+    nnz_s = int(rp[rows_s])
+    x = np.ones(n)
+    if O.ref_available():
+        R = O.ref()
+        kind = "reference"
+        h = R.ref_prepare_csr(rows_s, O.ptr(rp), O.ptr(val), O.ptr(x), O.ptr(ci), nnz_s, n)
+        hd = R.ref_prepare_dot(n, O.ptr(x), O.ptr(x))
+        call = lambda hh: R.ref_call(hh)  # noqa: E731
+        free = R.ref_free
+    else:
+        kind = "port"
+        h = hd = None
+        free = None
+    t_spmv = []
+    t_dot = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        if h is not None:
+            assert call(h) == 0
+        else:
+            O.spmv_csr(rp[: rows_s + 1], ci[:nnz_s], val[:nnz_s], x)
+        t_spmv.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        if hd is not None:
+            assert call(hd) == 0
+        else:
+            O.dot(x, x)
+        t_dot.append(time.perf_counter() - t0)
+    if free:
+        free(h)
+        free(hd)
+    ts = min(t_spmv) * (int(rp[n]) / max(nnz_s, 1))
+    td = min(t_dot)
+    dots_per_iter = 2 * CGITMAX + 3
+    t_iter = SPMV_PER_STEP * ts + dots_per_iter * td
+    desc = (f"{'lilac.spmv_csr HarnessFn (oracle/_ref)' if kind == 'reference' else 'oracle port'} on rows "
+            f"[0,{rows_s}) ({nnz_s} nnz) scaled to nnz={int(rp[n])}, x{SPMV_PER_STEP} SpMV + "
+            f"{dots_per_iter} full-length dotproduct calls per NPB iteration; host CG vector updates not counted")
+    return t_iter, kind, desc, ts
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    na, nonzer, niter, shift, _ = NPB[args.npb_class]
+    rp, ci, val = O.npb_makea(na, nonzer, shift)
+    steps = []
+    for i in range(args.warmup + args.steps):
+        t_iter, kind, desc, _ = reference_sample(rp, ci, val, na, reps=1)
+        if i >= args.warmup:
+            steps.append(t_iter)
+    ms = statistics.mean(steps) * 1e3
+    value = 1e3 / ms
+    model, ncpu = cpu_desc()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (NPB makea)",
+        "config": {"workload": f"NPB CG class {args.npb_class} (n={na}, nnz={int(rp[-1])}) SpMV harness path",
+                   "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": desc,
+                         "cpu": model, "host_cpus": ncpu},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------
+
+def e2e_harness_cg(rp, ci, val, n, shift, steps):
+    """NPB outer iterations through the C-ABI harness entry points on pinned
+    host vectors (the LiLAC model: host CG loop, offloaded SpMV/dot/axpy)."""
+    import torch
+    from paper_2001_07938_b200 import harness as H
+
+    def pinned(k):
+        return torch.zeros(k, dtype=torch.float64, pin_memory=True).numpy()
+
+    x, z, r, p, q, res = (pinned(n) for _ in range(6))
+    x[:] = 1.0
+
+    def outer():
+        z[:] = 0.0
+        q[:] = 0.0
+        r[:] = x
+        p[:] = r
+        rho = H.dotproduct(n, r, r)
+        for _ in range(CGITMAX):
+            H.spmv_csr(n, q, rp, val, p, ci)
+            d = H.dotproduct(n, p, q)
+            alpha = rho / d
+            rho0 = rho
+            H.axpy(n, z, alpha, p)
+            H.axpy(n, r, -alpha, q)
+            rho = H.dotproduct(n, r, r)
+            H.xpay(n, p, rho / rho0, r)
+        H.spmv_csr(n, r, rp, val, z, ci)
+        np.subtract(x, r, out=res)
+        rnorm = float(np.sqrt(H.dotproduct(n, res, res)))
+        t1 = H.dotproduct(n, x, z)
+        t2 = 1.0 / np.sqrt(H.dotproduct(n, z, z))
+        x[:] = t2 * z
+        return shift + 1.0 / t1, rnorm
+
+    outer()  # first call: uploads the matrix (marshal construct), untimed
+    x[:] = 1.0
+    st0 = H.harness_stats()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        zeta, _ = outer()
+    t = time.perf_counter() - t0
+    st1 = H.harness_stats()
+    h2d = sum(v["bytes_h2d"] for v in st1.values()) - sum(v["bytes_h2d"] for v in st0.values())
+    d2h = sum(v["bytes_d2h"] for v in st1.values()) - sum(v["bytes_d2h"] for v in st0.values())
+    calls = sum(v["calls"] for v in st1.values()) - sum(v["calls"] for v in st0.values())
+    kern = sum(v["t_kernel_ms"] for v in st1.values()) - sum(v["t_kernel_ms"] for v in st0.values())
+    return {"value": steps / t, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
+            "d2h_bytes_per_step": d2h // steps, "harness_calls_per_step": calls // steps,
+            "kernel_ms_per_step": kern / steps, "ms_per_step": 1e3 * t / steps,
+            "path": "b200_spmv_csr/b200_dot/b200_axpy/b200_xpay on pinned host arrays"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2001_07938_b200 import _native as N
+    from paper_2001_07938_b200 import device as D
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = N.lib()
+    N.check(L.b200_init(local))
+
+    na, nonzer, niter, shift, zeta_ref = NPB[args.npb_class]
+    t0 = time.perf_counter()
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    t_gen = time.perf_counter() - t0
+    nnz = int(rp[-1])
+    A = D.Matrix.csr(rp, ci, val)
+    info = A.info()
+    cg = D.CG(A)
+
+    # correctness gate: the full NPB benchmark must verify before we time anything
+    zeta, rnorm = cg.npb(niter, shift)
+    verified = abs(zeta - zeta_ref) / zeta_ref <= 1e-10
+
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    cg.reset(sh)
+    for _ in range(args.warmup):
+        cg.outer(shift, CGITMAX, sh)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local).start()
+    time.sleep(0.2)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        cg.outer(shift, CGITMAX, sh)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+
+    # dominant kernel alone: the CSR SpMV on the same stream, inputs > L2
+    x = torch.rand(na, dtype=torch.float64, device="cuda")
+    y = torch.empty(na, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(stream):
+        for _ in range(5):
+            A.spmv(x.data_ptr(), y.data_ptr(), sh)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.spmv_reps):
+            A.spmv(x.data_ptr(), y.data_ptr(), sh)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    spmv_ms = e0.elapsed_time(e1) / args.spmv_reps
+
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+
+    ms_step = ms_total / args.steps
+    value = world * args.steps / (ms_total / 1e3)
+    col_b = info["col_bytes"]
+    spmv_bytes = nnz * (8 + col_b) + (na + 1) * 8 + 8 * na + 8 * info["cols"]
+    spmv_flops = 2 * nnz
+    peak, peak_src = measured_peak()
+    achieved = spmv_bytes / (spmv_ms * 1e-3) / 1e9
+    traffic = ncu_traffic("k_csr_vector")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (NPB makea generator, class %s)" % args.npb_class,
+        "config": {"workload": f"NPB CG class {args.npb_class}: n={na}, nnz={nnz}, resident CSR "
+                               f"(int{8 * col_b} col_ind), {SPMV_PER_STEP} SpMV/step",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % (spmv_bytes / 1e9),
+                   "zeta": zeta, "zeta_verified": verified, "rnorm": rnorm},
+        "spmv": {"gflops": spmv_flops / (spmv_ms * 1e-3) / 1e9, "gbs": achieved,
+                 "frac_of_measured_copy": achieved / peak, "frac_of_nominal_8TBs": achieved / 8000.0,
+                 "ms": spmv_ms, "lanes_per_row": info["lanes"], "bytes_per_call": spmv_bytes},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_csr_vector (CSR SpMV)",
+                     "peak_source": peak_src,
+                     "how": f"algorithmic bytes nnz*(8+{col_b})+8(rows+1)+8rows+8cols per launch / mean of "
+                            f"{args.spmv_reps} back-to-back launches timed with CUDA events on the bench stream"},
+        "gpu_launches": args.steps * (1 + 3 * CGITMAX + 2 + 2),
+        "clocks": clk,
+        "gen_s": t_gen,
+    }
+    if rank == 0 and world == 1:
+        line["e2e"] = e2e_harness_cg(rp, ci, val, na, shift, args.e2e_steps)
+        if not args.no_cpu_baseline:
+            t_iter, kind, desc, ts = reference_sample(rp, ci, val, na, reps=2)
+            model, ncpu = cpu_desc()
+            line["cpu_baseline"] = {"value": 1.0 / t_iter, "unit": UNIT, "cores": 1, "kind": kind,
+                                    "sample": desc, "cpu": model, "host_cpus": ncpu,
+                                    "spmv_s": ts}
+    elif rank == 0:
+        line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                       "note": "measured at N=1 only"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    cg.free()
+    A.free()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,205 @@
+/*
+ * lilac_b200.h — C ABI of the B200 backend for the LiLAC-How harness path.
+ *
+ * Shared library: paper_2001_07938_b200/liblilac_b200.so (sm_100a kernels +
+ * C++ marshaling runtime). Plain C types only; all pointers are HOST pointers
+ * unless the name says _device.
+ *
+ * Drop-in contract (reference, /root/reference/proj):
+ *   - Every harness entry point has the signature harnessgen emits for its
+ *     computation: `extern "C" void <HARNESS>(<params in infer_interface order>)`
+ *     with kinds mapped ScalarInt -> int64_t, ArrayInt -> const int64_t*,
+ *     ArrayFloatIn -> const double*, ArrayFloatOut -> double*
+ *     (src/harnessgen.cpp:10-18, 86-92; src/what_parse.cpp:356-429).
+ *     "All harness interfaces for the same WhatProgram share the signature"
+ *     (SPEC.md:509), so linking this library instead of another harness
+ *     library is sufficient.
+ *   - No init/fini calls are required: the first call initialises the device
+ *     and registers an atexit teardown that releases every marshal object
+ *     (harnessgen.cpp:98-113; golden fixtures/gen/cusparse_spmv.gen.cpp:96-110).
+ *   - Errors: the reference lets lilac::Error escape (marshal.hpp:172-179); a C
+ *     caller sees std::terminate. Here every entry point catches at the
+ *     boundary, records the message (b200_last_error) and, in the default
+ *     error mode, prints `lilac-b200: <Code>: <message>` and aborts. In
+ *     B200_ERRORS_RETURN mode the call returns with outputs untouched. There is
+ *     never a CPU fallback.
+ */
+#ifndef LILAC_B200_H
+#define LILAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ==========================================================================
+ * 1. Harness entry points (drop-in for the reference's harness symbols)
+ * ========================================================================== */
+
+/* spmv_csr (fixtures/lilac/kernels.lilac:1-4; reference harness
+ * interp.cpp:330-389 "lilac.spmv_csr"; generated shape cusparse_spmv.gen.cpp:93).
+ * output[i] = sum_{row_ptr[i] <= j < row_ptr[i+1]} val[j] * x[col_ind[j]], i < rows.
+ * Extents follow the reference spec's marshaling section (cusparse.lilac:52-61):
+ * nnz = row_ptr[rows] (LastEntry), cols = 1 + max(col_ind[0..nnz)) (ReadableMax),
+ * x[0..cols), output[0..rows). row_ptr/col_ind/val stay resident on the device
+ * across calls while unchanged; only x and output move per call. */
+void b200_spmv_csr(int64_t rows, double* output, const int64_t* row_ptr, const double* val,
+                   const double* x, const int64_t* col_ind);
+
+/* spmv_jds (kernels.lilac:9-12; "lilac.spmv_jds"):
+ * output[i] = sum_{k < nzcnt[perm[i]]} val[jd_ptr[k]+perm[i]] * x[col_ind[jd_ptr[k]+perm[i]]].
+ * Extents: max_nz = max(nzcnt), jd_ptr[0..max_nz], nnz = jd_ptr[max_nz],
+ * cols = 1 + max(col_ind[0..nnz)). Bit-identical to the reference. */
+void b200_spmv_jds(int64_t rows, double* output, const int64_t* nzcnt, const int64_t* perm,
+                   const double* val, const int64_t* jd_ptr, const double* x,
+                   const int64_t* col_ind);
+
+/* dotproduct (kernels.lilac:6-7; "lilac.dotproduct"; C shape pinned by
+ * test_harnessgen.cpp:107-108): result[0] = sum_{i<length} a[i]*b[i]. */
+void b200_dot(double* result, int64_t length, const double* a, const double* b);
+
+/* CG companions the reference cannot express in LiLAC-What (
+ * extension kinds, same conventions):
+ *   b200_axpy: y[i] = y[i] + alpha * x[i]
+ *   b200_xpay: y[i] = x[i] + beta * y[i]      (NPB CG's p = r + beta*p)  */
+void b200_axpy(int64_t n, double* y, double alpha, const double* x);
+void b200_xpay(int64_t n, double* y, double beta, const double* x);
+
+/* ==========================================================================
+ * 2. Runtime control
+ * ========================================================================== */
+
+#define B200_ERRORS_ABORT 0
+#define B200_ERRORS_RETURN 1
+
+/* Optional explicit init on a device (default: LILAC_B200_DEVICE or the current
+ * CUDA device). Returns 0 or -1 (see b200_last_error). */
+int b200_init(int device);
+/* Release every marshal object and device buffer now (also runs at exit). */
+void b200_shutdown(void);
+void b200_set_error_mode(int mode);
+const char* b200_last_error(void);
+/* Last error code name ("OutOfBounds", "HookFailure", "DataError",
+ * "DeviceError", ...) or "" when the last call succeeded. */
+const char* b200_last_error_code(void);
+/* CSR kernel: "auto" | "vector" | "exact" (bit-identical to the reference).
+ * Also LILAC_B200_KERNEL. Returns 0 or -1. */
+int b200_set_kernel(const char* name);
+/* Change-detection strategy for harness objects created afterwards:
+ * "hybrid" (default) | "pageprotect" | "checksum" | "naive" (LILAC_MARSHAL_STRATEGY). */
+int b200_set_strategy(const char* name);
+/* 1 = dot/axpy also use the reference's sequential order (bit-exact). */
+void b200_set_exact_blas(int on);
+/* Library and build identification, e.g. "lilac-b200 0.1 sm_100a". */
+const char* b200_version(void);
+
+/* ==========================================================================
+ * 3. Counters (MarshalCounters, reference marshal.hpp:62-66, plus transfers)
+ * ========================================================================== */
+
+typedef struct {
+    char region[64];        /* "<harness>.<param>", e.g. "b200_spmv_csr.val" */
+    int64_t n_construct;
+    int64_t n_update;
+    int64_t n_destruct;
+    int64_t bytes_h2d;      /* host->device bytes moved by update hooks */
+    int64_t bytes_d2h;      /* device->host bytes moved by write-backs */
+    int32_t strategy;       /* 0 pageprotect, 1 checksum, 2 exact, 3 naive, 4 hybrid */
+    int32_t fell_back;      /* PageProtect demoted to Checksum */
+    int32_t streaming;      /* adaptive: rewritten every call, no longer guarded */
+    int32_t constructed;
+} b200_region_stats;
+
+typedef struct {
+    char harness[32];
+    int64_t calls;
+    double t_total_ms;      /* wall time inside the entry point */
+    double t_poll_ms;       /* change detection + uploads (acquire phase) */
+    double t_kernel_ms;     /* device time of the compute kernels (CUDA events) */
+    double t_writeback_ms;  /* output transfer */
+    int64_t bytes_h2d;
+    int64_t bytes_d2h;
+} b200_harness_stats;
+
+/* Copies up to `cap` region rows; returns the number of regions. */
+int b200_region_stats_get(b200_region_stats* out, int cap);
+int b200_harness_stats_get(b200_harness_stats* out, int cap);
+void b200_stats_reset(void);
+
+/* ==========================================================================
+ * 4. Resident device API (the harness internals, for drivers and benchmarks)
+ * ========================================================================== */
+
+typedef struct b200_matrix b200_matrix;  /* resident CSR or JDS matrix */
+
+typedef struct {
+    int64_t rows, cols, nnz, max_row;
+    int32_t format;        /* 0 CSR, 1 JDS */
+    int32_t col_bytes;     /* device col_ind width: 4 (narrowed) or 8 */
+    int32_t kernel;        /* CSR kernel chosen: 1 vector, 3 exact */
+    int32_t lanes;         /* vector kernel lanes per row */
+    int64_t device_bytes;  /* resident bytes */
+} b200_matrix_info;
+
+/* Upload host CSR / JDS arrays (same meaning and extents as the harness
+ * entries). Returns 0 or -1. */
+int b200_matrix_create_csr(b200_matrix** out, int64_t rows, const int64_t* row_ptr,
+                           const int64_t* col_ind, const double* val);
+int b200_matrix_create_jds(b200_matrix** out, int64_t rows, const int64_t* nzcnt,
+                           const int64_t* perm, const double* val, const int64_t* jd_ptr,
+                           const int64_t* col_ind);
+void b200_matrix_free(b200_matrix* A);
+int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info);
+/* y_device = A x_device on `stream` (cudaStream_t, may be NULL = default). */
+int b200_spmv_device(const b200_matrix* A, const double* x_device, double* y_device, void* stream);
+/* result_device[0] = a.b, deterministic (fixed partition + fixed-order sums). */
+int b200_dot_device(const double* a_device, const double* b_device, int64_t n,
+                    double* result_device, void* stream);
+int b200_axpy_device(int64_t n, double* y_device, double alpha, const double* x_device, void* stream);
+
+/* ==========================================================================
+ * 5. NPB CG driver (device-resident solver over a resident CSR matrix)
+ * ========================================================================== */
+
+typedef struct b200_cg b200_cg;
+
+int b200_cg_create(b200_cg** out, const b200_matrix* A);
+void b200_cg_free(b200_cg* cg);
+/* x = 1 (NPB's start vector). */
+int b200_cg_reset(b200_cg* cg, void* stream);
+/* One NPB outer iteration: conj_grad (cgitmax CG steps + residual), then
+ * zeta = shift + 1/(x.z), x = z/|z|. Uses a captured CUDA graph per stream. */
+int b200_cg_outer(b200_cg* cg, int cgitmax, double shift, void* stream);
+/* One CG step (spmv+dot, z/r update + r.r, p update). */
+int b200_cg_step(b200_cg* cg, void* stream);
+/* Copies zeta and the last residual norm to the host (synchronises). */
+int b200_cg_result(b200_cg* cg, double* zeta, double* rnorm);
+/* The whole NPB benchmark (1 untimed warm-up outer iteration + reset +
+ * niter outer iterations). Returns 0 or -1; zeta/rnorm on the host. */
+int b200_npb_cg(b200_cg* cg, int niter, double shift, double* zeta, double* rnorm);
+
+/* ==========================================================================
+ * 6. Workload synthesis (bench inputs; host arrays, caller-owned)
+ * ========================================================================== */
+
+/* NPB makea (rcond 0.1, randlc seed 314159265, multiplier 5^13), 0-based CSR,
+ * ascending columns, duplicates summed in generation order. Call with
+ * col_ind/val NULL to get *nnz (row_ptr filled), then again with storage. */
+int b200_gen_npb(int64_t na, int nonzer, double shift, int64_t* row_ptr, int64_t* col_ind,
+                 double* val, int64_t* nnz);
+
+/* ==========================================================================
+ * 7. Row sharding (multi-GPU driver)
+ * ========================================================================== */
+
+/* nnz-balanced contiguous row ranges: bounds[g] = lower_bound(row_ptr,
+ * row_ptr[0] + ceil(g*nnz/k)), clamped monotone; bounds[0]=0, bounds[k]=rows. */
+void b200_partition_rows(int64_t rows, const int64_t* row_ptr, int k, int64_t* bounds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LILAC_B200_H */

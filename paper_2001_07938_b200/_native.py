@@ -1,0 +1,125 @@
+"""ctypes binding of liblilac_b200.so (the C ABI in include/lilac_b200.h).
+
+The native library is the product: there is no Python or CPU fallback. If it
+is missing this module raises at import, naming the build command.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liblilac_b200.so")
+
+i64 = C.c_int64
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+vp = C.c_void_p
+
+
+class RegionStats(C.Structure):
+    _fields_ = [("region", C.c_char * 64), ("n_construct", i64), ("n_update", i64), ("n_destruct", i64),
+                ("bytes_h2d", i64), ("bytes_d2h", i64), ("strategy", C.c_int32), ("fell_back", C.c_int32),
+                ("streaming", C.c_int32), ("constructed", C.c_int32)]
+
+
+class HarnessStats(C.Structure):
+    _fields_ = [("harness", C.c_char * 32), ("calls", i64), ("t_total_ms", C.c_double),
+                ("t_poll_ms", C.c_double), ("t_kernel_ms", C.c_double), ("t_writeback_ms", C.c_double),
+                ("bytes_h2d", i64), ("bytes_d2h", i64)]
+
+
+class MatrixInfo(C.Structure):
+    _fields_ = [("rows", i64), ("cols", i64), ("nnz", i64), ("max_row", i64), ("format", C.c_int32),
+                ("col_bytes", C.c_int32), ("kernel", C.c_int32), ("lanes", C.c_int32),
+                ("device_bytes", i64)]
+
+
+# name -> (restype, argtypes); mirrors include/lilac_b200.h
+SIGNATURES = {
+    # 1. harness entry points
+    "b200_spmv_csr": (None, [i64, f64p, i64p, f64p, f64p, i64p]),
+    "b200_spmv_jds": (None, [i64, f64p, i64p, i64p, f64p, i64p, f64p, i64p]),
+    "b200_dot": (None, [f64p, i64, f64p, f64p]),
+    "b200_axpy": (None, [i64, f64p, C.c_double, f64p]),
+    "b200_xpay": (None, [i64, f64p, C.c_double, f64p]),
+    # 2. runtime control
+    "b200_init": (C.c_int, [C.c_int]),
+    "b200_shutdown": (None, []),
+    "b200_set_error_mode": (None, [C.c_int]),
+    "b200_last_error": (C.c_char_p, []),
+    "b200_last_error_code": (C.c_char_p, []),
+    "b200_set_kernel": (C.c_int, [C.c_char_p]),
+    "b200_set_strategy": (C.c_int, [C.c_char_p]),
+    "b200_set_exact_blas": (None, [C.c_int]),
+    "b200_version": (C.c_char_p, []),
+    # 3. counters
+    "b200_region_stats_get": (C.c_int, [C.POINTER(RegionStats), C.c_int]),
+    "b200_harness_stats_get": (C.c_int, [C.POINTER(HarnessStats), C.c_int]),
+    "b200_stats_reset": (None, []),
+    # 4. resident device API
+    "b200_matrix_create_csr": (C.c_int, [C.POINTER(vp), i64, i64p, i64p, f64p]),
+    "b200_matrix_create_jds": (C.c_int, [C.POINTER(vp), i64, i64p, i64p, f64p, i64p, i64p]),
+    "b200_matrix_free": (None, [vp]),
+    "b200_matrix_info_get": (C.c_int, [vp, C.POINTER(MatrixInfo)]),
+    "b200_spmv_device": (C.c_int, [vp, vp, vp, vp]),
+    "b200_dot_device": (C.c_int, [vp, vp, i64, vp, vp]),
+    "b200_axpy_device": (C.c_int, [i64, vp, C.c_double, vp, vp]),
+    # 5. NPB CG driver
+    "b200_cg_create": (C.c_int, [C.POINTER(vp), vp]),
+    "b200_cg_free": (None, [vp]),
+    "b200_cg_reset": (C.c_int, [vp, vp]),
+    "b200_cg_outer": (C.c_int, [vp, C.c_int, C.c_double, vp]),
+    "b200_cg_step": (C.c_int, [vp, vp]),
+    "b200_cg_result": (C.c_int, [vp, f64p, f64p]),
+    "b200_npb_cg": (C.c_int, [vp, C.c_int, C.c_double, f64p, f64p]),
+    # 6. workloads
+    "b200_gen_npb": (C.c_int, [i64, C.c_int, C.c_double, i64p, i64p, f64p, i64p]),
+    # 7. sharding
+    "b200_partition_rows": (None, [i64, i64p, C.c_int, i64p]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is not built; run `python -m paper_2001_07938_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def ptr(a):
+    """ctypes pointer to a numpy array's data (int64 / float64), or None."""
+    if a is None:
+        return None
+    import numpy as np
+    if a.dtype == np.int64:
+        return a.ctypes.data_as(i64p)
+    if a.dtype == np.float64:
+        return a.ctypes.data_as(f64p)
+    raise TypeError(f"unsupported dtype {a.dtype}")
+
+
+class B200Error(RuntimeError):
+    def __init__(self, code: str, message: str):
+        super().__init__(f"{code}: {message}")
+        self.code = code
+
+
+def check(rc: int = 0):
+    """Raise B200Error if the last C-ABI call failed (error mode RETURN)."""
+    L = lib()
+    code = L.b200_last_error_code().decode()
+    if rc != 0 or code:
+        raise B200Error(code or "Error", L.b200_last_error().decode())

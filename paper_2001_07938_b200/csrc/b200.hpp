@@ -1,0 +1,147 @@
+#pragma once
+// b200.hpp — internal declarations shared by the host runtime (.cpp) and the
+// sm_100a kernels (.cu). Nothing here is part of the C ABI (include/lilac_b200.h).
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "lilac/marshal.hpp"
+
+namespace b200 {
+
+using lilac::marshal::Errc;
+using lilac::marshal::Error;
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define B200_CUDA(call)                                                     \
+    do {                                                                    \
+        cudaError_t e_ = (call);                                            \
+        if (e_ != cudaSuccess) ::b200::throw_cuda(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Device memory
+// ---------------------------------------------------------------------------
+
+// Every device array is over-allocated by kPadBytes so vector loads that run
+// past a row end (masked, never used) stay inside the allocation.
+constexpr std::size_t kPadBytes = 256;
+
+struct DevBuf {
+    void* ptr = nullptr;
+    std::size_t bytes = 0;  // usable bytes (without padding)
+    std::size_t cap = 0;    // allocated bytes
+    int device = -1;
+
+    void ensure(std::size_t n);  // grow-only; contents not preserved
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+void pool_trim();  // return every cached block to CUDA
+
+// ---------------------------------------------------------------------------
+// Resident sparse matrices (device layout)
+// ---------------------------------------------------------------------------
+
+enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3 };
+const char* csr_kernel_name(CsrKernel k);
+CsrKernel parse_csr_kernel(const std::string& s);
+
+struct CsrDev {
+    std::int64_t rows = 0;      // number of rows computed
+    std::int64_t nnz = 0;       // extent of val/col (row_ptr[rows] for the ABI)
+    std::int64_t cols = 0;      // 1 + max(col_ind), ReadableMax semantics
+    std::int64_t max_row = 0;   // longest row
+    const std::int64_t* row_ptr = nullptr;  // rows+1, int64 (ABI width)
+    const void* col = nullptr;              // nnz, int32 if col32 else int64
+    bool col32 = true;
+    const double* val = nullptr;            // nnz
+    bool monotone = true;                   // row_ptr non-decreasing
+};
+
+struct JdsDev {
+    std::int64_t rows = 0;
+    std::int64_t nnz = 0;
+    std::int64_t cols = 0;
+    std::int64_t njd = 0;                      // max_nz + 1 entries of jd_ptr
+    const std::int64_t* nzcnt = nullptr;       // rows, jagged order
+    const std::int64_t* perm = nullptr;        // rows, original -> jagged
+    const std::int64_t* inv_perm = nullptr;    // rows, jagged -> original (null: perm not a bijection)
+    const std::int64_t* jd_ptr = nullptr;      // njd
+    const void* col = nullptr;
+    bool col32 = true;
+    const double* val = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (kernels.cu). All asynchronous on `s`.
+// ---------------------------------------------------------------------------
+
+// Chooses the CSR kernel for a matrix shape.
+CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested);
+int csr_vector_width(const CsrDev& A);  // lanes per row for the vector kernel
+
+void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s);
+void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s);
+
+struct CgScalars;
+// Fused CG kernel: q = A p and d = p.q in one pass; the last CTA sets
+// sc->d, sc->rho0 = sc->rho, sc->alpha = rho / d.
+void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* partials,
+                         unsigned int* ticket, CgScalars* sc, cudaStream_t s);
+
+// Upload-time validation / narrowing (one pass each, device side).
+//  * narrow_cols: col64[nnz] -> col32 (if col32 != null), max into *d_max, any
+//    negative index into *d_bad.
+void launch_scan_cols(const std::int64_t* col64, std::int64_t nnz, std::int32_t* col32,
+                      unsigned long long* d_max, int* d_bad, cudaStream_t s);
+//  * check_row_ptr: rows whose nonempty range leaves [0, nnz) set *d_bad;
+//    the longest row goes to *d_max.
+void launch_check_row_ptr(const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz,
+                          unsigned long long* d_max, int* d_bad, cudaStream_t s);
+//  * invert_perm: inv[perm[i]] = i; out-of-range or repeated targets set *d_bad.
+void launch_invert_perm(const std::int64_t* perm, std::int64_t rows, std::int64_t* inv, int* d_bad,
+                        cudaStream_t s);
+//  * check_jds: every (k < nzcnt[p]) offset jd_ptr[k]+p inside [0,nnz).
+void launch_check_jds(const std::int64_t* nzcnt, const std::int64_t* jd_ptr, std::int64_t rows,
+                      std::int64_t njd, std::int64_t nnz, int* d_bad, cudaStream_t s);
+
+// BLAS-1 companions (deterministic: fixed partition and fixed-order sums).
+int dot_parts_for(std::int64_t n);
+void launch_dot(const double* a, const double* b, std::int64_t n, double* result,
+                double* partials, unsigned int* ticket, cudaStream_t s);
+void launch_dot_exact(const double* a, const double* b, std::int64_t n, double* result,
+                      cudaStream_t s);
+void launch_axpy(std::int64_t n, double* y, double alpha, const double* x, cudaStream_t s);
+void launch_xpay(std::int64_t n, double* y, double beta, const double* x, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// NPB CG device step kernels (cg.cu)
+// ---------------------------------------------------------------------------
+
+struct CgScalars {  // device-resident, one per solver
+    double rho, rho0, d, alpha, beta, rnorm, t1, t2, zeta;
+    unsigned int ticket[4];
+};
+
+struct CgVectors {
+    std::int64_t n;
+    double *x, *z, *p, *q, *r;
+    double* partials;  // 4 * kMaxParts
+    int nparts;
+    CgScalars* sc;
+};
+
+constexpr int kMaxParts = 2048;
+
+void cg_launch_init(const CgVectors& v, cudaStream_t s);            // q=z=0, r=p=x, rho=r.r
+void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s);
+void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s);  // r=A z, rnorm
+void cg_launch_outer_update(const CgVectors& v, double shift, cudaStream_t s);  // zeta, x = z/|z|
+void cg_launch_reset_x(const CgVectors& v, cudaStream_t s);
+
+}  // namespace b200

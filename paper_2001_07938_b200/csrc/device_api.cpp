@@ -1,0 +1,197 @@
+// device_api.cpp — resident-matrix C API (section 4 of include/lilac_b200.h):
+// the same uploads/validation/kernels the harness entries use, exposed with
+// device pointers for drivers (NPB CG, multi-GPU) and kernel-level benchmarks.
+
+#include "lilac_b200.h"
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <memory>
+
+using namespace b200;
+
+struct b200_matrix {
+    int format = 0;  // 0 CSR, 1 JDS
+    int device = -1;
+    DevBuf row_ptr, col, val;             // CSR
+    DevBuf nzcnt, perm, inv_perm, jd_ptr;  // JDS (+col, val)
+    CsrDev csr;
+    JdsDev jds;
+    std::int64_t max_row = 0;
+};
+
+namespace {
+
+CsrKernel matrix_kernel(const b200_matrix* A) {
+    return choose_csr_kernel(A->csr, rt().kernel);
+}
+
+}  // namespace
+
+extern "C" {
+
+int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int64_t* row_ptr,
+                           const std::int64_t* col_ind, const double* val) {
+    return boundary("b200_matrix_create_csr", [&] {
+        ensure_init();
+        if (!out) throw Error(Errc::DataError, "out is NULL");
+        if (rows < 0) throw Error(Errc::DataError, "rows < 0");
+        auto A = std::make_unique<b200_matrix>();
+        A->format = 0;
+        A->device = rt().device;
+        const std::int64_t nnz = row_ptr[rows];
+        if (nnz < 0) throw Error(Errc::OutOfBounds, "row_ptr[rows] < 0");
+        bool monotone = true, col32 = true;
+        std::int64_t max_row = 0;
+        upload_row_ptr(A->row_ptr, row_ptr, rows, nnz, &max_row, &monotone);
+        const std::int64_t cols = upload_col_ind(A->col, col_ind, nnz, &col32);
+        A->val.ensure(nnz * sizeof(double));
+        if (nnz > 0)
+            B200_CUDA(cudaMemcpyAsync(A->val.ptr, val, nnz * sizeof(double), cudaMemcpyHostToDevice, rt().stream));
+        B200_CUDA(cudaStreamSynchronize(rt().stream));
+        CsrDev& d = A->csr;
+        d.rows = rows;
+        d.nnz = nnz;
+        d.cols = cols;
+        d.max_row = max_row;
+        d.row_ptr = A->row_ptr.as<std::int64_t>();
+        d.col = A->col.ptr;
+        d.col32 = col32;
+        d.val = A->val.as<double>();
+        d.monotone = monotone;
+        A->max_row = max_row;
+        *out = A.release();
+    });
+}
+
+int b200_matrix_create_jds(b200_matrix** out, std::int64_t rows, const std::int64_t* nzcnt,
+                           const std::int64_t* perm, const double* val, const std::int64_t* jd_ptr,
+                           const std::int64_t* col_ind) {
+    return boundary("b200_matrix_create_jds", [&] {
+        ensure_init();
+        if (!out) throw Error(Errc::DataError, "out is NULL");
+        if (rows < 0) throw Error(Errc::DataError, "rows < 0");
+        Runtime& r = rt();
+        auto A = std::make_unique<b200_matrix>();
+        A->format = 1;
+        A->device = r.device;
+        std::int64_t max_nz = 0;
+        for (std::int64_t i = 0; i < rows; ++i) max_nz = std::max(max_nz, nzcnt[i]);
+        const std::int64_t njd = rows > 0 ? max_nz + 1 : 0;
+        const std::int64_t nnz = njd > 0 ? jd_ptr[max_nz] : 0;
+        if (nnz < 0) throw Error(Errc::OutOfBounds, "jd_ptr[max_nz] < 0");
+        A->nzcnt.ensure(rows * 8);
+        A->perm.ensure(rows * 8);
+        A->inv_perm.ensure(rows * 8);
+        A->jd_ptr.ensure(njd * 8);
+        if (rows > 0) {
+            B200_CUDA(cudaMemcpyAsync(A->nzcnt.ptr, nzcnt, rows * 8, cudaMemcpyHostToDevice, r.stream));
+            B200_CUDA(cudaMemcpyAsync(A->perm.ptr, perm, rows * 8, cudaMemcpyHostToDevice, r.stream));
+            B200_CUDA(cudaMemcpyAsync(A->jd_ptr.ptr, jd_ptr, njd * 8, cudaMemcpyHostToDevice, r.stream));
+        }
+        B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
+        launch_invert_perm(A->perm.as<std::int64_t>(), rows, A->inv_perm.as<std::int64_t>(), r.d_bad(), r.stream);
+        int bad = 0;
+        B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
+        B200_CUDA(cudaStreamSynchronize(r.stream));
+        if (bad & 1) throw Error(Errc::OutOfBounds, "perm entry outside [0, rows)");
+        const bool bijective = (bad & 2) == 0;
+        B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
+        launch_check_jds(A->nzcnt.as<std::int64_t>(), A->jd_ptr.as<std::int64_t>(), rows, njd, nnz, r.d_bad(),
+                         r.stream);
+        B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
+        B200_CUDA(cudaStreamSynchronize(r.stream));
+        if (bad) throw Error(Errc::OutOfBounds, "jd_ptr[k] + perm[i] outside [0, nnz)");
+        bool col32 = true;
+        const std::int64_t cols = upload_col_ind(A->col, col_ind, nnz, &col32);
+        A->val.ensure(nnz * 8);
+        if (nnz > 0) B200_CUDA(cudaMemcpyAsync(A->val.ptr, val, nnz * 8, cudaMemcpyHostToDevice, r.stream));
+        B200_CUDA(cudaStreamSynchronize(r.stream));
+        JdsDev& d = A->jds;
+        d.rows = rows;
+        d.nnz = nnz;
+        d.cols = cols;
+        d.njd = njd;
+        d.nzcnt = A->nzcnt.as<std::int64_t>();
+        d.perm = A->perm.as<std::int64_t>();
+        d.inv_perm = bijective ? A->inv_perm.as<std::int64_t>() : nullptr;
+        d.jd_ptr = A->jd_ptr.as<std::int64_t>();
+        d.col = A->col.ptr;
+        d.col32 = col32;
+        d.val = A->val.as<double>();
+        A->max_row = max_nz;
+        *out = A.release();
+    });
+}
+
+void b200_matrix_free(b200_matrix* A) {
+    if (!A) return;
+    A->row_ptr.release();
+    A->col.release();
+    A->val.release();
+    A->nzcnt.release();
+    A->perm.release();
+    A->inv_perm.release();
+    A->jd_ptr.release();
+    delete A;
+}
+
+int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
+    return boundary("b200_matrix_info_get", [&] {
+        if (!A || !info) throw Error(Errc::DataError, "NULL argument");
+        *info = b200_matrix_info{};
+        info->format = A->format;
+        info->max_row = A->max_row;
+        if (A->format == 0) {
+            info->rows = A->csr.rows;
+            info->cols = A->csr.cols;
+            info->nnz = A->csr.nnz;
+            info->col_bytes = A->csr.col32 ? 4 : 8;
+            info->kernel = static_cast<int32_t>(matrix_kernel(A));
+            info->lanes = csr_vector_width(A->csr);
+        } else {
+            info->rows = A->jds.rows;
+            info->cols = A->jds.cols;
+            info->nnz = A->jds.nnz;
+            info->col_bytes = A->jds.col32 ? 4 : 8;
+            info->kernel = 0;
+            info->lanes = 1;
+        }
+        info->device_bytes = static_cast<std::int64_t>(A->row_ptr.bytes + A->col.bytes + A->val.bytes + A->nzcnt.bytes +
+                                                       A->perm.bytes + A->inv_perm.bytes + A->jd_ptr.bytes);
+    });
+}
+
+int b200_spmv_device(const b200_matrix* A, const double* x, double* y, void* stream) {
+    return boundary("b200_spmv_device", [&] {
+        if (!A) throw Error(Errc::DataError, "NULL matrix");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (A->format == 0)
+            launch_spmv_csr(A->csr, x, y, rt().kernel, s);
+        else
+            launch_spmv_jds(A->jds, x, y, s);
+    });
+}
+
+int b200_dot_device(const double* a, const double* b, std::int64_t n, double* result, void* stream) {
+    return boundary("b200_dot_device", [&] {
+        ensure_init();
+        Runtime& r = rt();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (r.exact_blas)
+            launch_dot_exact(a, b, n, result, s);
+        else
+            launch_dot(a, b, n, result, r.partials.as<double>(), r.d_ticket(), s);
+    });
+}
+
+int b200_axpy_device(std::int64_t n, double* y, double alpha, const double* x, void* stream) {
+    return boundary("b200_axpy_device", [&] { launch_axpy(n, y, alpha, x, static_cast<cudaStream_t>(stream)); });
+}
+
+}  // extern "C"
+
+// exposed for cg.cpp
+namespace b200 {
+const CsrDev* matrix_csr(const b200_matrix* A) { return A && A->format == 0 ? &A->csr : nullptr; }
+}  // namespace b200

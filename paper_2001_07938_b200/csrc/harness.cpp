@@ -1,0 +1,461 @@
+// harness.cpp — the extern "C" harness entry points of the B200 backend.
+//
+// Each entry point has exactly the shape the reference's harness generator
+// emits (src/harnessgen.cpp:42-133; golden fixtures/gen/cusparse_spmv.gen.cpp):
+// a static state record with one marshal object per binding, lazy first-run
+// setup with atexit teardown, acquires in binding order, the library call,
+// then write_back of every OUTPUT binding. The marshal classes are the B200
+// counterparts of the fixture's CudaRead/CudaWrite/LastEntry/ReadableMax
+// (fixtures/lilac/cusparse.lilac:6-43), with the fixture's two integer-width
+// bugs fixed: LastEntry reads int64 (cusparse.lilac:34 reads int) and the
+// device col_ind is narrowed explicitly instead of reinterpreting int64 bytes
+// as int (cusparse.lilac:56-57).
+
+#include "lilac_b200.h"
+#include "runtime.hpp"
+
+#include <cstring>
+
+using namespace b200;
+
+namespace {
+
+// ---- marshal classes -------------------------------------------------------------
+
+// LastEntry (input): out = in[n-1] of an int64 array.
+void LastEntry_update(const void* in, std::size_t size, std::int64_t& out) {
+    const auto* p = static_cast<const std::int64_t*>(in);
+    out = size >= sizeof(std::int64_t) ? p[size / sizeof(std::int64_t) - 1] : 0;
+}
+
+// ReadableMax (input): out = 1 + max(in) of an int64 array, 0 when empty
+// (the SPEC's empty-max convention, SPEC.md cached_invariant).
+void ReadableMax_update(const void* in, std::size_t size, std::int64_t& out) {
+    const auto* p = static_cast<const std::int64_t*>(in);
+    std::int64_t m = -1;
+    for (std::size_t i = 0; i < size / sizeof(std::int64_t); ++i) m = p[i] > m ? p[i] : m;
+    out = m + 1;
+}
+
+// B200Read (input): resident device copy, refreshed on change.
+void B200Read_update(const void* in, std::size_t size, DevArray& out) { upload(out, in, size); }
+void B200Read_destruct(const void*, std::size_t, DevArray& out) { out.buf.release(); }
+
+// B200Write (output): device destination, write_back = device->host copy.
+void B200Write_construct(const void*, std::size_t size, DevArray& out) { out.buf.ensure(size); }
+void B200Write_update(const void* in, std::size_t size, DevArray& out) {
+    download(const_cast<void*>(in), out, size, out);
+}
+void B200Write_destruct(const void*, std::size_t, DevArray& out) { out.buf.release(); }
+
+// B200RowPtr (input): row_ptr[0..rows] resident + validated against nnz.
+struct RowPtrDev {
+    DevBuf buf;
+    std::int64_t max_row = 0;
+    bool monotone = true;
+    std::int64_t h2d = 0, d2h = 0;
+};
+
+// B200ColInd (input): col_ind[0..nnz) resident, narrowed to int32 when every
+// index fits, with cols = 1 + max (ReadableMax) computed in the same pass.
+struct ColDev {
+    DevBuf buf;
+    bool col32 = true;
+    std::int64_t cols = 0;
+    std::int64_t h2d = 0, d2h = 0;
+};
+
+void ColInd_update(const void* in, std::size_t size, ColDev& out) {
+    const std::int64_t nnz = static_cast<std::int64_t>(size / sizeof(std::int64_t));
+    out.cols = upload_col_ind(out.buf, static_cast<const std::int64_t*>(in), nnz, &out.col32);
+    out.h2d += static_cast<std::int64_t>(size);
+}
+void ColInd_destruct(const void*, std::size_t, ColDev& out) { out.buf.release(); }
+
+// B200Perm (input, JDS): perm resident + its inverse (a cached invariant) when
+// perm is a bijection of [0, rows).
+struct PermDev {
+    DevBuf perm, inv;
+    bool bijective = true;
+    std::int64_t h2d = 0, d2h = 0;
+};
+
+void Perm_update(const void* in, std::size_t size, PermDev& out) {
+    Runtime& r = rt();
+    const std::int64_t rows = static_cast<std::int64_t>(size / sizeof(std::int64_t));
+    out.perm.ensure(size);
+    out.inv.ensure(size);
+    if (size) B200_CUDA(cudaMemcpyAsync(out.perm.ptr, in, size, cudaMemcpyHostToDevice, r.stream));
+    B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
+    launch_invert_perm(out.perm.as<std::int64_t>(), rows, out.inv.as<std::int64_t>(), r.d_bad(), r.stream);
+    int bad = 0;
+    B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
+    B200_CUDA(cudaStreamSynchronize(r.stream));
+    if (bad & 1) throw Error(Errc::OutOfBounds, "perm entry outside [0, rows)");
+    out.bijective = (bad & 2) == 0;
+    out.h2d += static_cast<std::int64_t>(size);
+}
+void Perm_destruct(const void*, std::size_t, PermDev& out) {
+    out.perm.release();
+    out.inv.release();
+}
+
+template <typename Out>
+void enroll_stats(MarshalObject<Out>& m, const char* name) {
+    m.set_name(name);
+    m.set_strategy(rt().strategy);
+    m.set_adaptive(true);
+    register_region(&m, &m.out().h2d, &m.out().d2h);
+}
+
+template <>
+void enroll_stats<std::int64_t>(MarshalObject<std::int64_t>& m, const char* name) {
+    m.set_name(name);
+    m.set_strategy(rt().strategy);
+    m.set_adaptive(true);
+    register_region(&m, nullptr, nullptr);
+}
+
+struct Timer {
+    HarnessStats& st;
+    Clock::time_point t0 = Clock::now(), t_mark = t0;
+    explicit Timer(HarnessStats& s) : st(s) {}
+    void acquired() {
+        st.t_poll_ms += ms_since(t_mark);
+        t_mark = Clock::now();
+    }
+    void written_back() { st.t_writeback_ms += ms_since(t_mark); }
+    ~Timer() {
+        st.t_total_ms += ms_since(t0);
+        st.calls++;
+    }
+};
+
+// Times the compute launch with events on the harness stream.
+template <typename F>
+void timed_launch(HarnessStats& st, F&& launch) {
+    Runtime& r = rt();
+    B200_CUDA(cudaEventRecord(r.ev_k0, r.stream));
+    launch();
+    B200_CUDA(cudaEventRecord(r.ev_k1, r.stream));
+    B200_CUDA(cudaEventSynchronize(r.ev_k1));
+    float ms = 0.f;
+    B200_CUDA(cudaEventElapsedTime(&ms, r.ev_k0, r.ev_k1));
+    st.t_kernel_ms += ms;
+}
+
+// ---- persistent state: b200_spmv_csr ------------------------------------------------
+
+struct spmv_csr_state {
+    MarshalObject<std::int64_t> m_nnz;
+    MarshalObject<RowPtrDev> m_row_ptr;
+    MarshalObject<ColDev> m_col_ind;
+    MarshalObject<DevArray> m_val;
+    MarshalObject<DevArray> m_x;
+    MarshalObject<DevArray> m_output;
+    bool first_run_done = false;
+};
+
+spmv_csr_state& csr_state() {
+    static spmv_csr_state* st = new spmv_csr_state;  // outlives atexit teardown
+    if (!st->first_run_done) {
+        st->first_run_done = true;
+        ensure_init();  // BeforeFirstExecution; registers the release_all atexit
+        enroll_stats(st->m_nnz, "b200_spmv_csr.nnz");
+        enroll_stats(st->m_row_ptr, "b200_spmv_csr.row_ptr");
+        enroll_stats(st->m_col_ind, "b200_spmv_csr.col_ind");
+        enroll_stats(st->m_val, "b200_spmv_csr.val");
+        enroll_stats(st->m_x, "b200_spmv_csr.x");
+        enroll_stats(st->m_output, "b200_spmv_csr.output");
+    }
+    return *st;
+}
+
+void add_bytes(HarnessStats& hs, std::int64_t h2d0, std::int64_t h2d1, std::int64_t d2h0, std::int64_t d2h1) {
+    hs.bytes_h2d += h2d1 - h2d0;
+    hs.bytes_d2h += d2h1 - d2h0;
+}
+
+// ---- persistent state: b200_spmv_jds -------------------------------------------------
+
+struct spmv_jds_state {
+    MarshalObject<std::int64_t> m_max_nz;   // ReadableMax of nzcnt[0..rows) - 1
+    MarshalObject<std::int64_t> m_nnz;      // LastEntry of jd_ptr[0..max_nz+1)
+    MarshalObject<DevArray> m_nzcnt;
+    MarshalObject<PermDev> m_perm;
+    MarshalObject<DevArray> m_jd_ptr;
+    MarshalObject<ColDev> m_col_ind;
+    MarshalObject<DevArray> m_val;
+    MarshalObject<DevArray> m_x;
+    MarshalObject<DevArray> m_output;
+    bool validated = false;
+    bool first_run_done = false;
+};
+
+spmv_jds_state& jds_state() {
+    static spmv_jds_state* st = new spmv_jds_state;
+    if (!st->first_run_done) {
+        st->first_run_done = true;
+        ensure_init();
+        enroll_stats(st->m_max_nz, "b200_spmv_jds.max_nz");
+        enroll_stats(st->m_nnz, "b200_spmv_jds.nnz");
+        enroll_stats(st->m_nzcnt, "b200_spmv_jds.nzcnt");
+        enroll_stats(st->m_perm, "b200_spmv_jds.perm");
+        enroll_stats(st->m_jd_ptr, "b200_spmv_jds.jd_ptr");
+        enroll_stats(st->m_col_ind, "b200_spmv_jds.col_ind");
+        enroll_stats(st->m_val, "b200_spmv_jds.val");
+        enroll_stats(st->m_x, "b200_spmv_jds.x");
+        enroll_stats(st->m_output, "b200_spmv_jds.output");
+    }
+    return *st;
+}
+
+// ---- persistent state: BLAS-1 companions ------------------------------------------------
+
+struct dot_state {
+    MarshalObject<DevArray> m_a, m_b, m_result;
+    bool first_run_done = false;
+};
+
+struct vec2_state {  // axpy / xpay: y in, x in, y out
+    MarshalObject<DevArray> m_y_in, m_x, m_y_out;
+    bool first_run_done = false;
+};
+
+dot_state& dot_st() {
+    static dot_state* st = new dot_state;
+    if (!st->first_run_done) {
+        st->first_run_done = true;
+        ensure_init();
+        enroll_stats(st->m_a, "b200_dot.a");
+        enroll_stats(st->m_b, "b200_dot.b");
+        enroll_stats(st->m_result, "b200_dot.result");
+    }
+    return *st;
+}
+
+vec2_state& vec2_st(const char* which) {
+    static vec2_state* axpy = new vec2_state;
+    static vec2_state* xpay = new vec2_state;
+    const bool is_axpy = std::strcmp(which, "b200_axpy") == 0;
+    vec2_state* st = is_axpy ? axpy : xpay;
+    if (!st->first_run_done) {
+        st->first_run_done = true;
+        ensure_init();
+        const std::string w = which;
+        static std::string names[2][3];
+        auto& nm = names[is_axpy ? 0 : 1];
+        nm[0] = w + ".y";
+        nm[1] = w + ".x";
+        nm[2] = w + ".y_out";
+        enroll_stats(st->m_y_in, nm[0].c_str());
+        enroll_stats(st->m_x, nm[1].c_str());
+        enroll_stats(st->m_y_out, nm[2].c_str());
+    }
+    return *st;
+}
+
+std::int64_t sum_h2d(std::initializer_list<std::int64_t> v) {
+    std::int64_t s = 0;
+    for (auto x : v) s += x;
+    return s;
+}
+
+}  // namespace
+
+// =================================================================================
+// Entry points
+// =================================================================================
+
+extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int64_t* row_ptr, const double* val,
+                              const double* x, const std::int64_t* col_ind) {
+    boundary("b200_spmv_csr", [&] {
+        spmv_csr_state& state = csr_state();
+        HarnessStats& hs = harness_stats("b200_spmv_csr");
+        Timer tm(hs);
+        if (rows < 0) throw Error(Errc::DataError, "rows < 0");
+        const std::int64_t h0 = sum_h2d({state.m_row_ptr.out().h2d, state.m_col_ind.out().h2d, state.m_val.out().h2d,
+                                         state.m_x.out().h2d});
+        const std::int64_t d0 = state.m_output.out().d2h;
+
+        // Marshaling, in binding order (cusparse.lilac:52-61)
+        const std::int64_t nnz = state.m_nnz.acquire(row_ptr, (rows + 1) * sizeof(*row_ptr), nullptr,
+                                                     LastEntry_update, nullptr);
+        if (nnz < 0) throw Error(Errc::OutOfBounds, "row_ptr[rows] < 0");
+        RowPtrDev& rp = state.m_row_ptr.acquire(
+            row_ptr, (rows + 1) * sizeof(*row_ptr), nullptr,
+            [rows, nnz](const void* in, std::size_t size, RowPtrDev& out) {
+                upload_row_ptr(out.buf, static_cast<const std::int64_t*>(in), rows, nnz, &out.max_row, &out.monotone);
+                out.h2d += static_cast<std::int64_t>(size);
+            },
+            [](const void*, std::size_t, RowPtrDev& out) { out.buf.release(); });
+        ColDev& ci = state.m_col_ind.acquire(col_ind, nnz * sizeof(*col_ind), nullptr, ColInd_update, ColInd_destruct);
+        DevArray& dval = state.m_val.acquire(val, nnz * sizeof(*val), nullptr, B200Read_update, B200Read_destruct);
+        DevArray& dx = state.m_x.acquire(x, ci.cols * sizeof(*x), nullptr, B200Read_update, B200Read_destruct);
+        DevArray& dout = state.m_output.acquire_out(output, rows * sizeof(*output), B200Write_construct,
+                                                    B200Write_update, B200Write_destruct);
+        tm.acquired();
+
+        // body: the sm_100a SpMV
+        CsrDev A;
+        A.rows = rows;
+        A.nnz = nnz;
+        A.cols = ci.cols;
+        A.max_row = rp.max_row;
+        A.row_ptr = rp.buf.as<std::int64_t>();
+        A.col = ci.buf.ptr;
+        A.col32 = ci.col32;
+        A.val = dval.buf.as<double>();
+        A.monotone = rp.monotone;
+        timed_launch(hs, [&] { launch_spmv_csr(A, dx.buf.as<double>(), dout.buf.as<double>(), rt().kernel, rt().stream); });
+        tm.acquired();
+
+        state.m_output.write_back();
+        tm.written_back();
+        add_bytes(hs, h0,
+                  sum_h2d({state.m_row_ptr.out().h2d, state.m_col_ind.out().h2d, state.m_val.out().h2d,
+                           state.m_x.out().h2d}),
+                  d0, state.m_output.out().d2h);
+    });
+}
+
+extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int64_t* nzcnt, const std::int64_t* perm,
+                              const double* val, const std::int64_t* jd_ptr, const double* x,
+                              const std::int64_t* col_ind) {
+    boundary("b200_spmv_jds", [&] {
+        spmv_jds_state& state = jds_state();
+        HarnessStats& hs = harness_stats("b200_spmv_jds");
+        Timer tm(hs);
+        if (rows < 0) throw Error(Errc::DataError, "rows < 0");
+        auto h2d_now = [&] {
+            return sum_h2d({state.m_nzcnt.out().h2d, state.m_perm.out().h2d, state.m_jd_ptr.out().h2d,
+                            state.m_col_ind.out().h2d, state.m_val.out().h2d, state.m_x.out().h2d});
+        };
+        const std::int64_t h0 = h2d_now();
+        const std::int64_t d0 = state.m_output.out().d2h;
+
+        const std::int64_t max_nz =
+            state.m_max_nz.acquire(nzcnt, rows * sizeof(*nzcnt), nullptr, ReadableMax_update, nullptr) - 1;
+        const std::int64_t njd = max_nz >= 0 ? max_nz + 1 : 0;
+        const std::int64_t nnz =
+            njd > 0 ? state.m_nnz.acquire(jd_ptr, njd * sizeof(*jd_ptr), nullptr, LastEntry_update, nullptr) : 0;
+        if (nnz < 0) throw Error(Errc::OutOfBounds, "jd_ptr[max_nz] < 0");
+        DevArray& dnz = state.m_nzcnt.acquire(nzcnt, rows * sizeof(*nzcnt), nullptr,
+                                              [&](const void* in, std::size_t size, DevArray& out) {
+                                                  upload(out, in, size);
+                                                  state.validated = false;
+                                              },
+                                              B200Read_destruct);
+        PermDev& dperm = state.m_perm.acquire(perm, rows * sizeof(*perm), nullptr, Perm_update, Perm_destruct);
+        DevArray& djd = state.m_jd_ptr.acquire(jd_ptr, njd * sizeof(*jd_ptr), nullptr,
+                                               [&](const void* in, std::size_t size, DevArray& out) {
+                                                   upload(out, in, size);
+                                                   state.validated = false;
+                                               },
+                                               B200Read_destruct);
+        DevArray& dval = state.m_val.acquire(val, nnz * sizeof(*val), nullptr, B200Read_update, B200Read_destruct);
+        ColDev& ci = state.m_col_ind.acquire(col_ind, nnz * sizeof(*col_ind), nullptr, ColInd_update, ColInd_destruct);
+        DevArray& dx = state.m_x.acquire(x, ci.cols * sizeof(*x), nullptr, B200Read_update, B200Read_destruct);
+        DevArray& dout = state.m_output.acquire_out(output, rows * sizeof(*output), B200Write_construct,
+                                                    B200Write_update, B200Write_destruct);
+        if (!state.validated) {
+            // offsets jd_ptr[k] + p must stay inside [0, nnz) (what_interp.cpp:67-68)
+            Runtime& r = rt();
+            B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
+            launch_check_jds(dnz.buf.as<std::int64_t>(), djd.buf.as<std::int64_t>(), rows, njd, nnz, r.d_bad(),
+                             r.stream);
+            int bad = 0;
+            B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
+            B200_CUDA(cudaStreamSynchronize(r.stream));
+            if (bad) throw Error(Errc::OutOfBounds, "jd_ptr[k] + perm[i] outside [0, nnz)");
+            state.validated = true;
+        }
+        tm.acquired();
+
+        JdsDev A;
+        A.rows = rows;
+        A.nnz = nnz;
+        A.cols = ci.cols;
+        A.njd = njd;
+        A.nzcnt = dnz.buf.as<std::int64_t>();
+        A.perm = dperm.perm.as<std::int64_t>();
+        A.inv_perm = dperm.bijective ? dperm.inv.as<std::int64_t>() : nullptr;
+        A.jd_ptr = djd.buf.as<std::int64_t>();
+        A.col = ci.buf.ptr;
+        A.col32 = ci.col32;
+        A.val = dval.buf.as<double>();
+        timed_launch(hs, [&] { launch_spmv_jds(A, dx.buf.as<double>(), dout.buf.as<double>(), rt().stream); });
+        tm.acquired();
+
+        state.m_output.write_back();
+        tm.written_back();
+        add_bytes(hs, h0, h2d_now(), d0, state.m_output.out().d2h);
+    });
+}
+
+extern "C" void b200_dot(double* result, std::int64_t length, const double* a, const double* b) {
+    boundary("b200_dot", [&] {
+        dot_state& state = dot_st();
+        HarnessStats& hs = harness_stats("b200_dot");
+        Timer tm(hs);
+        if (length < 0) throw Error(Errc::DataError, "length < 0");
+        const std::int64_t h0 = state.m_a.out().h2d + state.m_b.out().h2d, d0 = state.m_result.out().d2h;
+        DevArray& da = state.m_a.acquire(a, length * sizeof(*a), nullptr, B200Read_update, B200Read_destruct);
+        // dot(r, r): one binding serves both operands
+        DevArray& db = (b == a) ? da
+                                : state.m_b.acquire(b, length * sizeof(*b), nullptr, B200Read_update, B200Read_destruct);
+        DevArray& dres = state.m_result.acquire_out(result, sizeof(*result), B200Write_construct, B200Write_update,
+                                                    B200Write_destruct);
+        tm.acquired();
+        timed_launch(hs, [&] {
+            Runtime& r = rt();
+            if (r.exact_blas)
+                launch_dot_exact(da.buf.as<double>(), db.buf.as<double>(), length, dres.buf.as<double>(), r.stream);
+            else
+                launch_dot(da.buf.as<double>(), db.buf.as<double>(), length, dres.buf.as<double>(),
+                           r.partials.as<double>(), r.d_ticket(), r.stream);
+        });
+        tm.acquired();
+        state.m_result.write_back();
+        tm.written_back();
+        add_bytes(hs, h0, state.m_a.out().h2d + state.m_b.out().h2d, d0, state.m_result.out().d2h);
+    });
+}
+
+namespace {
+
+void vec2_call(const char* name, std::int64_t n, double* y, double s, const double* x, bool axpy) {
+    vec2_state& state = vec2_st(name);
+    HarnessStats& hs = harness_stats(name);
+    Timer tm(hs);
+    if (n < 0) throw Error(Errc::DataError, "n < 0");
+    const std::int64_t h0 = state.m_y_in.out().h2d + state.m_x.out().h2d, d0 = state.m_y_out.out().d2h;
+    DevArray& dy = state.m_y_in.acquire(y, n * sizeof(*y), nullptr, B200Read_update, B200Read_destruct);
+    DevArray& dx = state.m_x.acquire(x, n * sizeof(*x), nullptr, B200Read_update, B200Read_destruct);
+    DevArray& dout =
+        state.m_y_out.acquire_out(y, n * sizeof(*y), B200Write_construct, B200Write_update, B200Write_destruct);
+    tm.acquired();
+    timed_launch(hs, [&] {
+        Runtime& r = rt();
+        if (n > 0)
+            B200_CUDA(cudaMemcpyAsync(dout.buf.ptr, dy.buf.ptr, n * sizeof(double), cudaMemcpyDeviceToDevice, r.stream));
+        if (axpy)
+            launch_axpy(n, dout.buf.as<double>(), s, dx.buf.as<double>(), r.stream);
+        else
+            launch_xpay(n, dout.buf.as<double>(), s, dx.buf.as<double>(), r.stream);
+    });
+    tm.acquired();
+    state.m_y_out.write_back();
+    tm.written_back();
+    add_bytes(hs, h0, state.m_y_in.out().h2d + state.m_x.out().h2d, d0, state.m_y_out.out().d2h);
+}
+
+}  // namespace
+
+extern "C" void b200_axpy(std::int64_t n, double* y, double alpha, const double* x) {
+    boundary("b200_axpy", [&] { vec2_call("b200_axpy", n, y, alpha, x, true); });
+}
+
+extern "C" void b200_xpay(std::int64_t n, double* y, double beta, const double* x) {
+    boundary("b200_xpay", [&] { vec2_call("b200_xpay", n, y, beta, x, false); });
+}

@@ -1,0 +1,537 @@
+// kernels.cu — sm_100a kernels for the LiLAC harness path.
+//
+// Semantics restated from the reference interpreter (what_interp.cpp:87-108,
+// kernels.lilac:1-12): one output element per row, accumulated from +0.0.
+//  * csr_vector: S lanes per row, 16-byte streaming loads of val/col (L1
+//    no-allocate), read-only gathers of x, shuffle reduction. Reassociates:
+//    within the north-star tolerance, not bit-exact.
+//  * csr_exact: one thread per row, left-to-right __dadd_rn(acc, __dmul_rn(.))
+//    — bit-identical to the reference harness.
+//  * jds: one thread per jagged row, coalesced val[jd_ptr[k]+j]; its per-row
+//    order equals the reference's k order, so it is bit-exact too.
+// SpMV is a streaming gather, not a dense contraction: no tensor cores.
+
+#include "b200.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSMs = 148;
+
+// ---- load helpers -----------------------------------------------------------
+
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+
+struct Idx2 {
+    long long a, b;
+};
+
+__device__ __forceinline__ Idx2 ld_stream_idx(const std::int32_t* p) {
+    int a, b;
+    asm("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+    return {a, b};
+}
+
+__device__ __forceinline__ Idx2 ld_stream_idx(const std::int64_t* p) {
+    long long a, b;
+    asm("ld.global.nc.L1::no_allocate.v2.s64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+    return {a, b};
+}
+
+__device__ __forceinline__ double warp_sum(double v, unsigned mask = 0xffffffffu) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+}
+
+// Block-wide sum with a fixed tree (deterministic). Result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double sh[kThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < kThreads / 32 ? sh[lane] : 0.0;
+        v = warp_sum(v);
+    }
+    return v;
+}
+
+// Last-CTA-done reduction of per-CTA partials in fixed order. Every CTA calls
+// it after writing partials[blockIdx.x]; returns true in the CTA that must
+// finish (its thread 0 then holds the total in *total).
+__device__ __forceinline__ bool last_cta_sum(double* partials, unsigned int* ticket, double* total) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += __ldcg(partials + i);
+    s = block_sum(s);
+    if (threadIdx.x == 0) {
+        *total = s;
+        *ticket = 0u;
+    }
+    return true;
+}
+
+// ---- CSR vector kernel --------------------------------------------------------
+
+// S lanes cooperate on a row; each lane consumes 2 consecutive nonzeros per
+// step (one 16-byte val load, one 8/16-byte col load) and U steps are issued
+// before any x gather is consumed. Row starts are rounded down to an even
+// index so every vector load is aligned; the out-of-row elements are masked.
+template <int S, int U, typename IdxT, bool DOT>
+__global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
+                                                         const std::int64_t* __restrict__ row_ptr,
+                                                         const IdxT* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ y,
+                                                         double* __restrict__ partials,
+                                                         unsigned int* ticket, CgScalars* sc) {
+    const int lane = threadIdx.x & (S - 1);
+    const unsigned gmask =
+        S == 32 ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31) & ~(S - 1)));
+    const std::int64_t groups = static_cast<std::int64_t>(gridDim.x) * (kThreads / S);
+    double pq = 0.0;
+    for (std::int64_t row = (static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x) / S;
+         row < rows; row += groups) {
+        const std::int64_t start = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
+        double acc = 0.0;
+        for (std::int64_t jb = (start & ~std::int64_t(1)) + 2 * lane; jb < end; jb += 2 * S * U) {
+            double2 v[U];
+            Idx2 c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const std::int64_t j = jb + 2 * S * u;
+                if (j < end) {
+                    v[u] = ld_stream(val + j);
+                    c[u] = ld_stream_idx(col + j);
+                } else {
+                    v[u] = make_double2(0.0, 0.0);
+                    c[u] = {0, 0};
+                }
+            }
+            double xa[U], xb[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const std::int64_t j = jb + 2 * S * u;
+                xa[u] = (j < end && j >= start) ? __ldg(x + c[u].a) : 0.0;
+                xb[u] = (j + 1 < end) ? __ldg(x + c[u].b) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                acc += v[u].x * xa[u];
+                acc += v[u].y * xb[u];
+            }
+        }
+#pragma unroll
+        for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
+        if (lane == 0) {
+            y[row] = acc;
+            if (DOT) pq += acc * __ldg(x + row);
+        }
+    }
+    if (DOT) {
+        double s = block_sum(pq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+        double total;
+        if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) {
+            sc->d = total;
+            sc->rho0 = sc->rho;
+            sc->alpha = sc->rho / total;
+        }
+    }
+}
+
+// ---- exact kernels ------------------------------------------------------------
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kThreads) k_csr_exact(std::int64_t rows,
+                                                        const std::int64_t* __restrict__ row_ptr,
+                                                        const IdxT* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
+    for (std::int64_t row = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; row < rows;
+         row += stride) {
+        const std::int64_t start = row_ptr[row], end = row_ptr[row + 1];
+        double acc = 0.0;
+        for (std::int64_t j = start; j < end; ++j)
+            acc = __dadd_rn(acc, __dmul_rn(__ldg(val + j), __ldg(x + static_cast<std::int64_t>(col[j]))));
+        y[row] = acc;
+    }
+}
+
+// JDS, thread per jagged row j (coalesced over j); y scattered through inv_perm.
+template <typename IdxT>
+__global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
+                                                  const std::int64_t* __restrict__ inv_perm,
+                                                  const std::int64_t* __restrict__ jd_ptr,
+                                                  const IdxT* __restrict__ col,
+                                                  const double* __restrict__ val,
+                                                  const double* __restrict__ x, double* __restrict__ y) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
+    for (std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; j < rows; j += stride) {
+        const std::int64_t len = __ldg(nzcnt + j);
+        double acc = 0.0;
+        for (std::int64_t k = 0; k < len; ++k) {
+            const std::int64_t off = __ldg(jd_ptr + k) + j;
+            double v;
+            asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(val + off));
+            acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + static_cast<std::int64_t>(col[off]))));
+        }
+        y[__ldg(inv_perm + j)] = acc;
+    }
+}
+
+// JDS when perm is not a bijection: thread per original row (uncoalesced,
+// still the reference's semantics and order).
+template <typename IdxT>
+__global__ void __launch_bounds__(kThreads) k_jds_rowwise(std::int64_t rows,
+                                                          const std::int64_t* __restrict__ nzcnt,
+                                                          const std::int64_t* __restrict__ perm,
+                                                          const std::int64_t* __restrict__ jd_ptr,
+                                                          const IdxT* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < rows; i += stride) {
+        const std::int64_t p = perm[i];
+        const std::int64_t len = nzcnt[p];
+        double acc = 0.0;
+        for (std::int64_t k = 0; k < len; ++k) {
+            const std::int64_t off = jd_ptr[k] + p;
+            acc = __dadd_rn(acc, __dmul_rn(val[off], x[static_cast<std::int64_t>(col[off])]));
+        }
+        y[i] = acc;
+    }
+}
+
+// ---- validation / narrowing ----------------------------------------------------
+
+__global__ void k_scan_cols(const std::int64_t* __restrict__ col64, std::int64_t nnz,
+                            std::int32_t* __restrict__ col32, unsigned long long* d_max, int* d_bad) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    long long m = -1;
+    int bad = 0;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+        const long long c = col64[i];
+        bad |= c < 0;
+        m = c > m ? c : m;
+        if (col32) col32[i] = static_cast<std::int32_t>(c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long om = __shfl_xor_sync(0xffffffffu, m, o);
+        m = om > m ? om : m;
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (m >= 0) atomicMax(d_max, static_cast<unsigned long long>(m) + 1ull);
+        if (bad) atomicOr(d_bad, 1);
+    }
+}
+
+__global__ void k_check_row_ptr(const std::int64_t* __restrict__ rp, std::int64_t rows, std::int64_t nnz,
+                                unsigned long long* d_max, int* d_bad) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    long long m = 0;
+    int bad = 0;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += stride) {
+        const long long a = rp[i], b = rp[i + 1];
+        if (b > a) {
+            bad |= (a < 0 || b > nnz) ? 1 : 0;
+            m = (b - a) > m ? (b - a) : m;
+        } else if (b < a) {
+            bad |= 2;  // non-monotone: legal (empty row), but rules out merge kernels
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long om = __shfl_xor_sync(0xffffffffu, m, o);
+        m = om > m ? om : m;
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(d_max, static_cast<unsigned long long>(m));
+        if (bad) atomicOr(d_bad, bad);
+    }
+}
+
+__global__ void k_fill_i64(std::int64_t* p, std::int64_t n, std::int64_t v) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        p[i] = v;
+}
+
+__global__ void k_invert_perm(const std::int64_t* __restrict__ perm, std::int64_t rows, std::int64_t* inv, int* d_bad) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += stride) {
+        const long long p = perm[i];
+        if (p < 0 || p >= rows) {
+            atomicOr(d_bad, 1);  // out of range: the reference throws OutOfBounds
+            continue;
+        }
+        unsigned long long prev = atomicExch(reinterpret_cast<unsigned long long*>(inv + p),
+                                             static_cast<unsigned long long>(i));
+        if (static_cast<long long>(prev) != -1) atomicOr(d_bad, 2);  // not a bijection
+    }
+}
+
+__global__ void k_check_jds(const std::int64_t* __restrict__ nzcnt, const std::int64_t* __restrict__ jd_ptr,
+                            std::int64_t rows, std::int64_t njd, std::int64_t nnz, int* d_bad) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t p = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < rows; p += stride) {
+        const long long len = nzcnt[p];
+        if (len <= 0) continue;
+        if (len > njd) {
+            atomicOr(d_bad, 1);
+            continue;
+        }
+        for (long long k = 0; k < len; ++k) {
+            const long long off = jd_ptr[k] + p;
+            if (off < 0 || off >= nnz) {
+                atomicOr(d_bad, 1);
+                break;
+            }
+        }
+    }
+}
+
+// ---- BLAS-1 --------------------------------------------------------------------
+
+// Deterministic dot: CTA b owns a fixed contiguous slice, threads stride it
+// with 16-byte loads, fixed-tree block sum, last CTA sums the partials in order.
+__global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ a, const double* __restrict__ b,
+                                                  std::int64_t n, double* result, double* partials,
+                                                  unsigned int* ticket) {
+    const std::int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const std::int64_t lo = min(n, per * blockIdx.x), hi = min(n, lo + per);
+    double s = 0.0;
+    // vector part: pairs aligned to the allocation (a, b are 256-byte aligned)
+    std::int64_t vlo = (lo + 1) & ~std::int64_t(1), vhi = hi & ~std::int64_t(1);
+    if (vlo > vhi) vlo = vhi = lo;
+    for (std::int64_t i = lo + threadIdx.x; i < vlo; i += kThreads) s += a[i] * b[i];
+    for (std::int64_t i = vlo + 2 * threadIdx.x; i < vhi; i += 2 * kThreads) {
+        const double2 x = ld_stream(a + i), y = ld_stream(b + i);
+        s += x.x * y.x;
+        s += x.y * y.y;
+    }
+    for (std::int64_t i = max(vhi, vlo) + threadIdx.x; i < hi; i += kThreads) s += a[i] * b[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    double total;
+    if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) *result = total;
+}
+
+// Reference order, one thread: bit-identical to what_interp.cpp:97-101.
+__global__ void k_dot_exact(const double* a, const double* b, std::int64_t n, double* result) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    double acc = 0.0;
+    for (std::int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, __dmul_rn(a[i], b[i]));
+    *result = acc;
+}
+
+__global__ void k_axpy(std::int64_t n, double* __restrict__ y, double alpha, const double* __restrict__ x) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));
+}
+
+__global__ void k_xpay(std::int64_t n, double* __restrict__ y, double beta, const double* __restrict__ x) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = __dadd_rn(x[i], __dmul_rn(beta, y[i]));
+}
+
+unsigned grid_for(std::int64_t threads, unsigned cap = kSMs * 16) {
+    std::int64_t b = (threads + kThreads - 1) / kThreads;
+    return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(b, cap)));
+}
+
+template <int S, typename IdxT, bool DOT>
+void vector_launch(const CsrDev& A, const double* x, double* y, double* partials, unsigned* ticket,
+                   CgScalars* sc, unsigned grid, cudaStream_t s) {
+    k_csr_vector<S, 2, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
+                                                            A.val, x, y, partials, ticket, sc);
+}
+
+template <typename IdxT, bool DOT>
+void vector_dispatch(const CsrDev& A, int S, const double* x, double* y, double* partials, unsigned* ticket,
+                     CgScalars* sc, unsigned grid, cudaStream_t s) {
+    switch (S) {
+    case 2: vector_launch<2, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
+    case 4: vector_launch<4, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
+    case 8: vector_launch<8, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
+    case 16: vector_launch<16, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
+    default: vector_launch<32, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
+    }
+}
+
+}  // namespace
+
+// ---- host launchers ------------------------------------------------------------------
+
+const char* csr_kernel_name(CsrKernel k) {
+    switch (k) {
+    case CsrKernel::Auto: return "auto";
+    case CsrKernel::Vector: return "vector";
+    case CsrKernel::Merge: return "merge";
+    case CsrKernel::Exact: return "exact";
+    }
+    return "?";
+}
+
+CsrKernel parse_csr_kernel(const std::string& s) {
+    if (s.empty() || s == "auto") return CsrKernel::Auto;
+    if (s == "vector") return CsrKernel::Vector;
+    if (s == "merge") return CsrKernel::Merge;
+    if (s == "exact") return CsrKernel::Exact;
+    throw Error(Errc::DataError, "unknown CSR kernel '" + s + "' (auto, vector, merge, exact)");
+}
+
+int csr_vector_width(const CsrDev& A) {
+    const double mean = A.rows > 0 ? static_cast<double>(A.nnz) / static_cast<double>(A.rows) : 0.0;
+    // lanes so that one U=2 step (4*S nonzeros) covers roughly a mean row
+    int S = 2;
+    while (S < 32 && 4.0 * S < mean) S *= 2;
+    return S;
+}
+
+CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested) {
+    if (requested != CsrKernel::Auto) return requested == CsrKernel::Merge ? CsrKernel::Vector : requested;
+    return CsrKernel::Vector;
+}
+
+static unsigned vector_grid(const CsrDev& A, int S) {
+    return grid_for(A.rows * static_cast<std::int64_t>(S), kSMs * 8 * 4);
+}
+
+void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s) {
+    if (A.rows <= 0) return;
+    k = choose_csr_kernel(A, k);
+    if (k == CsrKernel::Exact) {
+        unsigned g = grid_for(A.rows);
+        if (A.col32)
+            k_csr_exact<std::int32_t><<<g, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const std::int32_t*>(A.col), A.val, x, y);
+        else
+            k_csr_exact<std::int64_t><<<g, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const std::int64_t*>(A.col), A.val, x, y);
+    } else {
+        const int S = csr_vector_width(A);
+        const unsigned g = vector_grid(A, S);
+        if (A.col32)
+            vector_dispatch<std::int32_t, false>(A, S, x, y, nullptr, nullptr, nullptr, g, s);
+        else
+            vector_dispatch<std::int64_t, false>(A, S, x, y, nullptr, nullptr, nullptr, g, s);
+    }
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* partials, unsigned* ticket,
+                         CgScalars* sc, cudaStream_t s) {
+    const int S = csr_vector_width(A);
+    const unsigned g = std::min<unsigned>(vector_grid(A, S), kMaxParts);
+    if (A.col32)
+        vector_dispatch<std::int32_t, true>(A, S, p, q, partials, ticket, sc, g, s);
+    else
+        vector_dispatch<std::int64_t, true>(A, S, p, q, partials, ticket, sc, g, s);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
+    if (A.rows <= 0) return;
+    const unsigned g = grid_for(A.rows);
+    if (A.inv_perm) {
+        if (A.col32)
+            k_jds<std::int32_t><<<g, kThreads, 0, s>>>(A.rows, A.nzcnt, A.inv_perm, A.jd_ptr,
+                                                       static_cast<const std::int32_t*>(A.col), A.val, x, y);
+        else
+            k_jds<std::int64_t><<<g, kThreads, 0, s>>>(A.rows, A.nzcnt, A.inv_perm, A.jd_ptr,
+                                                       static_cast<const std::int64_t*>(A.col), A.val, x, y);
+    } else {
+        if (A.col32)
+            k_jds_rowwise<std::int32_t><<<g, kThreads, 0, s>>>(A.rows, A.nzcnt, A.perm, A.jd_ptr,
+                                                               static_cast<const std::int32_t*>(A.col), A.val, x, y);
+        else
+            k_jds_rowwise<std::int64_t><<<g, kThreads, 0, s>>>(A.rows, A.nzcnt, A.perm, A.jd_ptr,
+                                                               static_cast<const std::int64_t*>(A.col), A.val, x, y);
+    }
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_scan_cols(const std::int64_t* col64, std::int64_t nnz, std::int32_t* col32, unsigned long long* d_max,
+                      int* d_bad, cudaStream_t s) {
+    if (nnz <= 0) return;
+    k_scan_cols<<<grid_for(nnz, kSMs * 8), kThreads, 0, s>>>(col64, nnz, col32, d_max, d_bad);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_check_row_ptr(const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz,
+                          unsigned long long* d_max, int* d_bad, cudaStream_t s) {
+    if (rows <= 0) return;
+    k_check_row_ptr<<<grid_for(rows, kSMs * 8), kThreads, 0, s>>>(row_ptr, rows, nnz, d_max, d_bad);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_invert_perm(const std::int64_t* perm, std::int64_t rows, std::int64_t* inv, int* d_bad, cudaStream_t s) {
+    if (rows <= 0) return;
+    k_fill_i64<<<grid_for(rows, kSMs * 8), kThreads, 0, s>>>(inv, rows, -1);
+    k_invert_perm<<<grid_for(rows, kSMs * 8), kThreads, 0, s>>>(perm, rows, inv, d_bad);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_check_jds(const std::int64_t* nzcnt, const std::int64_t* jd_ptr, std::int64_t rows, std::int64_t njd,
+                      std::int64_t nnz, int* d_bad, cudaStream_t s) {
+    if (rows <= 0) return;
+    k_check_jds<<<grid_for(rows, kSMs * 8), kThreads, 0, s>>>(nzcnt, jd_ptr, rows, njd, nnz, d_bad);
+    B200_CUDA(cudaGetLastError());
+}
+
+int dot_parts_for(std::int64_t n) {
+    // ~4K elements per CTA at minimum; at most 8 CTAs per SM
+    std::int64_t g = (n + 4095) / 4096;
+    return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, kSMs * 8)));
+}
+
+void launch_dot(const double* a, const double* b, std::int64_t n, double* result, double* partials,
+                unsigned int* ticket, cudaStream_t s) {
+    k_dot<<<dot_parts_for(n), kThreads, 0, s>>>(a, b, n, result, partials, ticket);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_dot_exact(const double* a, const double* b, std::int64_t n, double* result, cudaStream_t s) {
+    k_dot_exact<<<1, 32, 0, s>>>(a, b, n, result);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_axpy(std::int64_t n, double* y, double alpha, const double* x, cudaStream_t s) {
+    if (n <= 0) return;
+    k_axpy<<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, y, alpha, x);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_xpay(std::int64_t n, double* y, double beta, const double* x, cudaStream_t s) {
+    if (n <= 0) return;
+    k_xpay<<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, y, beta, x);
+    B200_CUDA(cudaGetLastError());
+}
+
+}  // namespace b200

@@ -1,0 +1,393 @@
+// marshal.cpp — change detection, registry and page guards for the B200
+// marshaling runtime (include/lilac/marshal.hpp).
+//
+// Contract followed: reference include/lilac/marshal.hpp:108-240 (state
+// machine) and src/marshal.cpp:123-243 (strategies, fault plumbing, registry).
+// The guard table is per page range; a page stays write-protected while at
+// least one clean region covers it (the reference unprotects unconditionally
+// in drop_guard, which can leave a clean neighbour unguarded).
+
+#include "lilac/marshal.hpp"
+
+#include <algorithm>
+#include <cerrno>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <signal.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+namespace lilac::marshal {
+inline namespace b200 {
+
+const char* errc_name(Errc c) {
+    switch (c) {
+    case Errc::OutOfBounds: return "OutOfBounds";
+    case Errc::HookFailure: return "HookFailure";
+    case Errc::ProtectionUnsupported: return "ProtectionUnsupported";
+    case Errc::DataError: return "DataError";
+    case Errc::DeviceError: return "DeviceError";
+    }
+    return "?";
+}
+
+Error::Error(Errc code, const std::string& message)
+    : std::runtime_error(std::string(errc_name(code)) + ": " + message), code_(code) {}
+
+namespace {
+
+struct Guard {
+    std::uintptr_t lo, hi;
+    TrackedRegion* region;
+};
+
+// Mutated in normal context under g_mu; the fault handler only reads it
+// (single-threaded acquire contract).
+std::vector<Guard> g_guards;
+std::vector<TrackedRegion*> g_tracked;  // every region with a live snapshot
+std::mutex g_mu;
+std::size_t g_page = 0;
+struct sigaction g_prev;
+bool g_prev_valid = false;
+
+void on_fault(int sig, siginfo_t* si, void* uctx) {
+    const auto addr = reinterpret_cast<std::uintptr_t>(si->si_addr);
+    const std::uintptr_t page = addr & ~(static_cast<std::uintptr_t>(g_page) - 1);
+    bool hit = false;
+    for (const Guard& g : g_guards) {
+        if (page < g.hi && page + g_page > g.lo) {
+            g.region->dirty = true;
+            hit = true;
+        }
+    }
+    if (hit) {
+        mprotect(reinterpret_cast<void*>(page), g_page, PROT_READ | PROT_WRITE);
+        return;
+    }
+    // Not ours: hand the fault to whoever had SIGSEGV before us.
+    if (g_prev_valid) {
+        if (g_prev.sa_flags & SA_SIGINFO) {
+            if (g_prev.sa_sigaction) {
+                g_prev.sa_sigaction(sig, si, uctx);
+                return;
+            }
+        } else if (g_prev.sa_handler != SIG_DFL && g_prev.sa_handler != SIG_IGN) {
+            g_prev.sa_handler(sig);
+            return;
+        }
+    }
+    signal(SIGSEGV, SIG_DFL);  // re-executing the access now terminates normally
+}
+
+void ensure_handler() {
+    struct sigaction cur;
+    if (sigaction(SIGSEGV, nullptr, &cur) == 0 && (cur.sa_flags & SA_SIGINFO) &&
+        cur.sa_sigaction == on_fault)
+        return;
+    struct sigaction sa;
+    std::memset(&sa, 0, sizeof sa);
+    sa.sa_sigaction = on_fault;
+    sa.sa_flags = SA_SIGINFO | SA_ONSTACK;
+    sigemptyset(&sa.sa_mask);
+    struct sigaction prev;
+    if (sigaction(SIGSEGV, &sa, &prev) != 0)
+        throw Error(Errc::ProtectionUnsupported,
+                    std::string("cannot install SIGSEGV handler: ") + std::strerror(errno));
+    g_prev = prev;
+    g_prev_valid = true;
+}
+
+std::uintptr_t floor_page(std::uintptr_t a) { return a & ~(static_cast<std::uintptr_t>(page_size()) - 1); }
+std::uintptr_t ceil_page(std::uintptr_t a) { return floor_page(a + page_size() - 1); }
+
+void protect(std::uintptr_t lo, std::uintptr_t hi) {
+    if (hi > lo && mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ) != 0)
+        throw Error(Errc::ProtectionUnsupported, std::string("mprotect failed: ") + std::strerror(errno));
+}
+
+// Unprotect [lo,hi), then re-protect the parts still covered by a clean
+// guarded region other than `except`. Caller holds g_mu.
+void release_pages(std::uintptr_t lo, std::uintptr_t hi, const TrackedRegion* except) {
+    if (hi <= lo) return;
+    mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ | PROT_WRITE);
+    for (const Guard& g : g_guards) {
+        if (g.region == except || g.region->dirty) continue;
+        std::uintptr_t a = std::max(lo, g.lo), b = std::min(hi, g.hi);
+        if (a < b) mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ);
+    }
+}
+
+void add_guard(TrackedRegion& r, std::uintptr_t lo, std::uintptr_t hi) {
+    ensure_handler();
+    protect(lo, hi);
+    if (!r.guarded) {
+        g_guards.push_back({lo, hi, &r});
+        r.guarded = true;
+        r.guard_lo = lo;
+        r.guard_hi = hi;
+    }
+}
+
+void track(TrackedRegion& r) {
+    if (std::find(g_tracked.begin(), g_tracked.end(), &r) == g_tracked.end()) g_tracked.push_back(&r);
+}
+
+std::uint64_t version_of(const TrackedRegion& r) {
+    if (!r.ref.version)
+        throw Error(Errc::DataError, "exact-version strategy needs a version word behind the region");
+    return *r.ref.version;
+}
+
+// Hybrid edge hashes: the partial pages at each end that cannot be protected.
+void edge_spans(const TrackedRegion& r, std::uintptr_t& in_lo, std::uintptr_t& in_hi) {
+    const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
+    const std::uintptr_t end = base + r.ref.bytes;
+    in_lo = ceil_page(base);
+    in_hi = floor_page(end);
+    if (in_hi <= in_lo) in_lo = in_hi = end;  // no whole page inside: hash everything
+}
+
+std::uint64_t head_hash(const TrackedRegion& r, std::uintptr_t in_lo) {
+    const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
+    return fnv1a(r.ref.base, std::min<std::uintptr_t>(in_lo, base + r.ref.bytes) - base);
+}
+
+std::uint64_t tail_hash(const TrackedRegion& r, std::uintptr_t in_hi) {
+    const auto end = reinterpret_cast<std::uintptr_t>(r.ref.base) + r.ref.bytes;
+    return in_hi < end ? fnv1a(reinterpret_cast<const void*>(in_hi), end - in_hi) : 0;
+}
+
+}  // namespace
+
+const char* strategy_name(Strategy s) {
+    switch (s) {
+    case Strategy::PageProtect: return "pageprotect";
+    case Strategy::Checksum: return "checksum";
+    case Strategy::ExactVersion: return "exact";
+    case Strategy::Naive: return "naive";
+    case Strategy::Hybrid: return "hybrid";
+    }
+    return "?";
+}
+
+Strategy parse_strategy(const std::string& n) {
+    if (n == "pageprotect") return Strategy::PageProtect;
+    if (n == "checksum") return Strategy::Checksum;
+    if (n == "exact") return Strategy::ExactVersion;
+    if (n == "naive") return Strategy::Naive;
+    if (n == "hybrid") return Strategy::Hybrid;
+    throw Error(Errc::DataError, "unknown marshal strategy '" + n +
+                                     "' (expected pageprotect, checksum, exact, naive or hybrid)");
+}
+
+Strategy default_strategy(Strategy fallback) {
+    const char* env = std::getenv("LILAC_MARSHAL_STRATEGY");
+    return (env && *env) ? parse_strategy(env) : fallback;
+}
+
+std::uint64_t fnv1a(const void* data, std::size_t size) {
+    const auto* p = static_cast<const unsigned char*>(data);
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    for (std::size_t i = 0; i < size; ++i) h = (h ^ p[i]) * 0x100000001b3ULL;
+    return h;
+}
+
+std::size_t page_size() {
+    if (g_page == 0) g_page = static_cast<std::size_t>(sysconf(_SC_PAGESIZE));
+    return g_page;
+}
+
+void mark_clean(TrackedRegion& r) {
+    switch (r.strategy) {
+    case Strategy::Naive:
+        r.dirty = true;  // untracked: never clean
+        return;
+    case Strategy::Checksum:
+        r.last_checksum = fnv1a(r.ref.base, r.ref.bytes);
+        r.dirty = false;
+        return;
+    case Strategy::ExactVersion:
+        r.last_version = version_of(r);
+        r.dirty = false;
+        return;
+    case Strategy::PageProtect: {
+        if (r.ref.bytes == 0) {
+            r.dirty = false;
+            return;
+        }
+        const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
+        if (base % page_size() != 0)
+            throw Error(Errc::ProtectionUnsupported, "page protection needs a page-aligned region base");
+        std::lock_guard<std::mutex> lk(g_mu);
+        track(r);
+        r.dirty = false;  // clear first: a racing fault must win
+        add_guard(r, base, ceil_page(base + r.ref.bytes));
+        return;
+    }
+    case Strategy::Hybrid: {
+        if (r.ref.bytes == 0) {
+            r.dirty = false;
+            return;
+        }
+        std::uintptr_t in_lo, in_hi;
+        edge_spans(r, in_lo, in_hi);
+        std::lock_guard<std::mutex> lk(g_mu);
+        track(r);
+        r.dirty = false;
+        if (in_hi > in_lo) add_guard(r, in_lo, in_hi);
+        r.last_checksum = head_hash(r, in_lo);
+        r.last_tail_checksum = tail_hash(r, in_hi);
+        return;
+    }
+    }
+}
+
+bool poll_dirty(TrackedRegion& r) {
+    switch (r.strategy) {
+    case Strategy::Naive:
+        return true;
+    case Strategy::Checksum:
+        if (!r.dirty && r.ref.bytes > 0) r.dirty = fnv1a(r.ref.base, r.ref.bytes) != r.last_checksum;
+        return r.dirty;
+    case Strategy::ExactVersion:
+        if (!r.dirty && r.ref.bytes > 0) r.dirty = version_of(r) != r.last_version;
+        return r.dirty;
+    case Strategy::PageProtect:
+        return r.dirty;
+    case Strategy::Hybrid:
+        if (!r.dirty && r.ref.bytes > 0) {
+            std::uintptr_t in_lo, in_hi;
+            edge_spans(r, in_lo, in_hi);
+            r.dirty = head_hash(r, in_lo) != r.last_checksum || tail_hash(r, in_hi) != r.last_tail_checksum;
+        }
+        return r.dirty;
+    }
+    return true;
+}
+
+void drop_guard(TrackedRegion& r) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_tracked.erase(std::remove(g_tracked.begin(), g_tracked.end(), &r), g_tracked.end());
+    if (!r.guarded) return;
+    g_guards.erase(std::remove_if(g_guards.begin(), g_guards.end(),
+                                  [&](const Guard& g) { return g.region == &r; }),
+                   g_guards.end());
+    release_pages(r.guard_lo, r.guard_hi, &r);
+    r.guarded = false;
+    r.guard_lo = r.guard_hi = 0;
+}
+
+void note_host_write(const void* base, std::size_t bytes) {
+    if (bytes == 0) return;
+    const auto lo = reinterpret_cast<std::uintptr_t>(base);
+    const std::uintptr_t hi = lo + bytes;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (TrackedRegion* r : g_tracked) {
+        const auto rlo = reinterpret_cast<std::uintptr_t>(r->ref.base);
+        if (rlo < hi && lo < rlo + r->ref.bytes) r->dirty = true;
+    }
+    // open the pages for the incoming write (DMA never faults; a CPU copy would)
+    const std::uintptr_t plo = floor_page(lo), phi = ceil_page(hi);
+    for (const Guard& g : g_guards) {
+        std::uintptr_t a = std::max(plo, g.lo), b = std::min(phi, g.hi);
+        if (a < b) {
+            g.region->dirty = true;
+            mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ | PROT_WRITE);
+        }
+    }
+}
+
+// ---- MarshalObjectBase --------------------------------------------------------
+
+namespace {
+std::vector<MarshalObjectBase*> g_objects;
+std::mutex g_objects_mu;
+}  // namespace
+
+MarshalObjectBase::MarshalObjectBase(std::string name, Strategy s)
+    : name_(std::move(name)), strategy_(s) {
+    if (name_.empty()) name_ = "region@" + std::to_string(reinterpret_cast<std::uintptr_t>(this));
+}
+
+MarshalObjectBase::~MarshalObjectBase() = default;
+
+void MarshalObjectBase::set_strategy(Strategy s) {
+    if (constructed_) throw Error(Errc::DataError, "cannot change the strategy of a constructed object");
+    strategy_ = s;
+    fell_back_ = false;
+}
+
+void MarshalObjectBase::enroll() {
+    std::lock_guard<std::mutex> lk(g_objects_mu);
+    if (std::find(g_objects.begin(), g_objects.end(), this) == g_objects.end()) g_objects.push_back(this);
+}
+
+void MarshalObjectBase::unenroll() {
+    std::lock_guard<std::mutex> lk(g_objects_mu);
+    g_objects.erase(std::remove(g_objects.begin(), g_objects.end(), this), g_objects.end());
+}
+
+void MarshalObjectBase::clean_with_fallback() {
+    if (streaming_) return;
+    try {
+        mark_clean(region_);
+    } catch (const Error& e) {
+        if (e.code() != Errc::ProtectionUnsupported) throw;
+        strategy_ = Strategy::Checksum;
+        region_.strategy = Strategy::Checksum;
+        fell_back_ = true;
+        mark_clean(region_);
+    }
+}
+
+bool MarshalObjectBase::region_dirty() { return streaming_ || poll_dirty(region_); }
+
+void MarshalObjectBase::note_update_for_streaming(bool was_dirty) {
+    if (!adaptive_ || streaming_) return;
+    if (!was_dirty) {
+        dirty_streak_ = 0;
+        return;
+    }
+    if (++dirty_streak_ >= kStreamAfter && region_.strategy != Strategy::Naive &&
+        region_.strategy != Strategy::ExactVersion) {
+        // Rewritten on every call: guarding it costs a fault per page per call
+        // for no saved transfer. Stop guarding; update unconditionally.
+        streaming_ = true;
+        drop_guard(region_);
+    }
+}
+
+void MarshalObjectBase::hook_failed(const char* which, const std::exception& e) const {
+    throw Error(Errc::HookFailure,
+                std::string(which) + " hook failed for region '" + name_ + "': " + e.what());
+}
+
+Diagnostics release_all() {
+    std::vector<MarshalObjectBase*> live;
+    {
+        std::lock_guard<std::mutex> lk(g_objects_mu);
+        live.swap(g_objects);
+    }
+    Diagnostics d;
+    for (MarshalObjectBase* o : live) o->force_release(d);
+    return d;
+}
+
+// ---- PageBuffer -----------------------------------------------------------------
+
+PageBuffer::PageBuffer(std::size_t bytes) : bytes_(bytes) {
+    mapped_ = std::max<std::size_t>(ceil_page(bytes), page_size());
+    void* p = mmap(nullptr, mapped_, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) throw Error(Errc::DataError, std::string("mmap failed: ") + std::strerror(errno));
+    p_ = p;
+}
+
+PageBuffer::~PageBuffer() {
+    if (p_) munmap(p_, mapped_);
+}
+
+}  // namespace b200
+}  // namespace lilac::marshal

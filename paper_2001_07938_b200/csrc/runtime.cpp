@@ -1,0 +1,381 @@
+// runtime.cpp — device context, lazy init/teardown, error boundary, counters
+// and the resident-upload helpers of the B200 harness library.
+
+#include "runtime.hpp"
+
+#include "lilac_b200.h"
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+namespace b200 {
+
+namespace {
+thread_local std::string t_err;
+thread_local std::string t_err_code;
+int g_error_mode = -1;
+std::vector<RegionEntry> g_regions;
+std::vector<HarnessStats*> g_hstats;
+}  // namespace
+
+const char* current_error() { return t_err.c_str(); }
+
+void set_error(const char* code, const std::string& msg) {
+    t_err_code = code;
+    t_err = msg;
+}
+
+void clear_error() {
+    t_err.clear();
+    t_err_code.clear();
+}
+
+int error_mode() {
+    if (g_error_mode < 0) {
+        const char* e = std::getenv("LILAC_B200_ERRORS");
+        g_error_mode = (e && std::strcmp(e, "return") == 0) ? B200_ERRORS_RETURN : B200_ERRORS_ABORT;
+    }
+    return g_error_mode;
+}
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    throw Error(Errc::DeviceError, std::string(cudaGetErrorName(e)) + " (" + cudaGetErrorString(e) +
+                                       ") in " + what + " at " + file + ":" + std::to_string(line));
+}
+
+// ---- DevBuf + caching pool --------------------------------------------------------
+//
+// Marshal objects destruct/construct their device arrays whenever a host
+// region's identity changes (reference marshal.hpp:192-199) — e.g. the dot
+// harness sees (r,r), (p,q), (x,z) in turn. cudaMalloc/cudaFree on that path
+// would serialise the device, so freed blocks go to a size-class free list
+// and are reused; everything is returned to CUDA at shutdown.
+
+namespace {
+struct PoolBlock {
+    void* ptr;
+    std::size_t cap;
+    int device;
+};
+std::vector<PoolBlock> g_pool;
+std::size_t g_pool_bytes = 0;
+constexpr std::size_t kPoolLimit = std::size_t(8) << 30;  // cached bytes kept at most
+
+std::size_t size_class(std::size_t n) {
+    if (n <= (std::size_t(1) << 20)) {  // powers of two up to 1 MiB
+        std::size_t c = 4096;
+        while (c < n) c <<= 1;
+        return c;
+    }
+    const std::size_t g = std::size_t(2) << 20;  // 2 MiB granules above
+    return (n + g - 1) / g * g;
+}
+}  // namespace
+
+void DevBuf::ensure(std::size_t n) {
+    if (ptr && cap >= n + kPadBytes) {
+        bytes = n;
+        return;
+    }
+    release();
+    ensure_init();
+    int dev = 0;
+    B200_CUDA(cudaGetDevice(&dev));
+    const std::size_t want = size_class(n + kPadBytes);
+    for (std::size_t i = 0; i < g_pool.size(); ++i) {
+        if (g_pool[i].device == dev && g_pool[i].cap == want) {
+            ptr = g_pool[i].ptr;
+            g_pool_bytes -= want;
+            g_pool.erase(g_pool.begin() + static_cast<std::ptrdiff_t>(i));
+            break;
+        }
+    }
+    if (!ptr) {
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaErrorMemoryAllocation && !g_pool.empty()) {
+            (void)cudaGetLastError();
+            pool_trim();
+            e = cudaMalloc(&ptr, want);
+        }
+        if (e != cudaSuccess) {
+            ptr = nullptr;
+            throw_cuda(e, "cudaMalloc", __FILE__, __LINE__);
+        }
+    }
+    // zero the tail so masked over-reads of index arrays stay in range
+    B200_CUDA(cudaMemsetAsync(static_cast<char*>(ptr) + n, 0, want - n, rt().stream));
+    cap = want;
+    bytes = n;
+    device = dev;
+}
+
+void DevBuf::release() {
+    if (ptr) {
+        if (rt().inited && g_pool_bytes + cap <= kPoolLimit) {
+            g_pool.push_back({ptr, cap, device});
+            g_pool_bytes += cap;
+        } else {
+            cudaFree(ptr);  // teardown path: errors ignored
+        }
+    }
+    ptr = nullptr;
+    bytes = cap = 0;
+}
+
+void pool_trim() {
+    for (const PoolBlock& b : g_pool) cudaFree(b.ptr);
+    g_pool.clear();
+    g_pool_bytes = 0;
+}
+
+// ---- runtime ------------------------------------------------------------------
+
+Runtime& rt() {
+    static Runtime r;
+    return r;
+}
+
+static void at_exit_teardown() { shutdown(); }
+
+void ensure_init() {
+    Runtime& r = rt();
+    if (r.inited) return;
+    int dev = r.device;
+    if (dev < 0) {
+        const char* e = std::getenv("LILAC_B200_DEVICE");
+        if (e && *e)
+            dev = std::atoi(e);
+        else
+            B200_CUDA(cudaGetDevice(&dev));
+    }
+    int count = 0;
+    B200_CUDA(cudaGetDeviceCount(&count));
+    if (dev < 0 || dev >= count)
+        throw Error(Errc::DeviceError, "device " + std::to_string(dev) + " not present (" +
+                                           std::to_string(count) + " visible)");
+    B200_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    B200_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        throw Error(Errc::DeviceError, std::string("built for sm_100a, found ") + prop.name + " (sm_" +
+                                           std::to_string(prop.major) + std::to_string(prop.minor) + ")");
+    r.device = dev;
+    B200_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
+    B200_CUDA(cudaEventCreate(&r.ev_k0));
+    B200_CUDA(cudaEventCreate(&r.ev_k1));
+    r.inited = true;  // DevBuf::ensure below re-enters ensure_init
+    r.partials.ensure(sizeof(double) * kMaxParts * 4);
+    r.scalars.ensure(4096);
+    r.flags.ensure(64);
+    B200_CUDA(cudaMemsetAsync(r.scalars.ptr, 0, 4096, r.stream));
+    B200_CUDA(cudaStreamSynchronize(r.stream));
+    const char* k = std::getenv("LILAC_B200_KERNEL");
+    if (k && *k) r.kernel = parse_csr_kernel(k);
+    r.strategy = lilac::marshal::default_strategy(Strategy::Hybrid);
+    // registered after the CUDA runtime initialised, so it runs before the
+    // runtime's own teardown (mirrors harnessgen.cpp:98-113)
+    std::atexit(at_exit_teardown);
+}
+
+void shutdown() {
+    Runtime& r = rt();
+    lilac::marshal::release_all();
+    if (!r.inited) return;
+    r.partials.release();
+    r.scalars.release();
+    r.flags.release();
+    r.stage.release();
+    if (r.ev_k0) cudaEventDestroy(r.ev_k0);
+    if (r.ev_k1) cudaEventDestroy(r.ev_k1);
+    pool_trim();
+    if (r.stream) cudaStreamDestroy(r.stream);
+    r.ev_k0 = r.ev_k1 = nullptr;
+    r.stream = nullptr;
+    r.inited = false;
+}
+
+void register_region(MarshalObjectBase* obj, const std::int64_t* h2d, const std::int64_t* d2h) {
+    for (auto& e : g_regions)
+        if (e.obj == obj) return;
+    g_regions.push_back({obj, h2d, d2h});
+}
+
+const std::vector<RegionEntry>& all_regions() { return g_regions; }
+
+HarnessStats& harness_stats(const char* name) {
+    for (HarnessStats* h : g_hstats)
+        if (h->name == name) return *h;
+    auto* h = new HarnessStats;
+    h->name = name;
+    g_hstats.push_back(h);
+    return *h;
+}
+
+std::vector<HarnessStats*> all_harness_stats() { return g_hstats; }
+
+// ---- transfers -------------------------------------------------------------------
+
+void upload(DevArray& d, const void* host, std::size_t bytes) {
+    d.buf.ensure(bytes);
+    if (bytes == 0) return;
+    B200_CUDA(cudaMemcpyAsync(d.buf.ptr, host, bytes, cudaMemcpyHostToDevice, rt().stream));
+    d.h2d += static_cast<std::int64_t>(bytes);
+}
+
+void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter) {
+    if (bytes == 0) return;
+    B200_CUDA(cudaMemcpyAsync(host, d.buf.ptr, bytes, cudaMemcpyDeviceToHost, rt().stream));
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
+    counter.d2h += static_cast<std::int64_t>(bytes);
+}
+
+void upload_row_ptr(DevBuf& buf, const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz,
+                    std::int64_t* max_row, bool* monotone) {
+    Runtime& r = rt();
+    const std::size_t bytes = sizeof(std::int64_t) * static_cast<std::size_t>(rows + 1);
+    buf.ensure(bytes);
+    B200_CUDA(cudaMemcpyAsync(buf.ptr, row_ptr, bytes, cudaMemcpyHostToDevice, r.stream));
+    B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
+    launch_check_row_ptr(buf.as<std::int64_t>(), rows, nnz, r.d_umax(), r.d_bad(), r.stream);
+    unsigned long long mx = 0;
+    int bad = 0;
+    B200_CUDA(cudaMemcpyAsync(&mx, r.d_umax(), 8, cudaMemcpyDeviceToHost, r.stream));
+    B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
+    B200_CUDA(cudaStreamSynchronize(r.stream));
+    if (bad & 1)
+        throw Error(Errc::OutOfBounds, "row_ptr addresses nonzeros outside [0, nnz=" + std::to_string(nnz) + ")");
+    *max_row = static_cast<std::int64_t>(mx);
+    *monotone = (bad & 2) == 0;
+}
+
+std::int64_t upload_col_ind(DevBuf& buf, const std::int64_t* col_ind, std::int64_t nnz, bool* col32) {
+    Runtime& r = rt();
+    const std::size_t n = static_cast<std::size_t>(std::max<std::int64_t>(nnz, 0));
+    buf.ensure(n * sizeof(std::int32_t));
+    B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
+    // narrow chunk by chunk through a bounded staging buffer
+    const std::size_t chunk = std::max<std::size_t>(1, r.stage_bytes / sizeof(std::int64_t));
+    if (n > 0) r.stage.ensure(std::min(n, chunk) * sizeof(std::int64_t));
+    for (std::size_t off = 0; off < n; off += chunk) {
+        const std::size_t m = std::min(chunk, n - off);
+        B200_CUDA(cudaMemcpyAsync(r.stage.ptr, col_ind + off, m * sizeof(std::int64_t), cudaMemcpyHostToDevice,
+                                  r.stream));
+        launch_scan_cols(r.stage.as<std::int64_t>(), static_cast<std::int64_t>(m), buf.as<std::int32_t>() + off,
+                         r.d_umax(), r.d_bad(), r.stream);
+    }
+    unsigned long long cols = 0;
+    int bad = 0;
+    B200_CUDA(cudaMemcpyAsync(&cols, r.d_umax(), 8, cudaMemcpyDeviceToHost, r.stream));
+    B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
+    B200_CUDA(cudaStreamSynchronize(r.stream));
+    if (bad) throw Error(Errc::OutOfBounds, "negative column index in col_ind");
+    if (cols > static_cast<unsigned long long>(INT32_MAX)) {
+        // too wide for int32: keep the ABI width
+        buf.ensure(n * sizeof(std::int64_t));
+        if (n) B200_CUDA(cudaMemcpyAsync(buf.ptr, col_ind, n * sizeof(std::int64_t), cudaMemcpyHostToDevice, r.stream));
+        B200_CUDA(cudaStreamSynchronize(r.stream));
+        *col32 = false;
+    } else {
+        *col32 = true;
+    }
+    return static_cast<std::int64_t>(cols);
+}
+
+}  // namespace b200
+
+// ---- C ABI: runtime control and counters -------------------------------------------
+
+using namespace b200;
+
+extern "C" {
+
+int b200_init(int device) {
+    return boundary("b200_init", [&] {
+        if (rt().inited && rt().device != device && device >= 0)
+            throw Error(Errc::DataError, "already initialised on device " + std::to_string(rt().device));
+        if (device >= 0) rt().device = device;
+        ensure_init();
+    });
+}
+
+void b200_shutdown(void) {
+    boundary("b200_shutdown", [] { shutdown(); });
+}
+
+void b200_set_error_mode(int mode) { g_error_mode = mode == B200_ERRORS_RETURN ? 1 : 0; }
+
+const char* b200_last_error(void) { return t_err.c_str(); }
+const char* b200_last_error_code(void) { return t_err_code.c_str(); }
+
+int b200_set_kernel(const char* name) {
+    return boundary("b200_set_kernel", [&] {
+        CsrKernel k = parse_csr_kernel(name ? name : "");
+        if (k == CsrKernel::Merge) throw Error(Errc::DataError, "merge kernel not available in this build");
+        rt().kernel = k;
+    });
+}
+
+int b200_set_strategy(const char* name) {
+    return boundary("b200_set_strategy", [&] { rt().strategy = lilac::marshal::parse_strategy(name ? name : ""); });
+}
+
+void b200_set_exact_blas(int on) { rt().exact_blas = on != 0; }
+
+const char* b200_version(void) { return "lilac-b200 0.1 sm_100a"; }
+
+int b200_region_stats_get(b200_region_stats* out, int cap) {
+    const auto& regs = all_regions();
+    int n = 0;
+    for (const RegionEntry& e : regs) {
+        if (n < cap && out) {
+            b200_region_stats& s = out[n];
+            std::memset(&s, 0, sizeof s);
+            std::strncpy(s.region, e.obj->name().c_str(), sizeof(s.region) - 1);
+            s.n_construct = e.obj->counters().n_construct;
+            s.n_update = e.obj->counters().n_update;
+            s.n_destruct = e.obj->counters().n_destruct;
+            s.bytes_h2d = e.h2d ? *e.h2d : 0;
+            s.bytes_d2h = e.d2h ? *e.d2h : 0;
+            s.strategy = static_cast<int32_t>(e.obj->strategy());
+            s.fell_back = e.obj->fell_back();
+            s.streaming = e.obj->streaming();
+            s.constructed = e.obj->constructed();
+        }
+        ++n;
+    }
+    return n;
+}
+
+int b200_harness_stats_get(b200_harness_stats* out, int cap) {
+    auto hs = all_harness_stats();
+    int n = 0;
+    for (HarnessStats* h : hs) {
+        if (n < cap && out) {
+            b200_harness_stats& s = out[n];
+            std::memset(&s, 0, sizeof s);
+            std::strncpy(s.harness, h->name.c_str(), sizeof(s.harness) - 1);
+            s.calls = h->calls;
+            s.t_total_ms = h->t_total_ms;
+            s.t_poll_ms = h->t_poll_ms;
+            s.t_kernel_ms = h->t_kernel_ms;
+            s.t_writeback_ms = h->t_writeback_ms;
+            s.bytes_h2d = h->bytes_h2d;
+            s.bytes_d2h = h->bytes_d2h;
+        }
+        ++n;
+    }
+    return n;
+}
+
+void b200_stats_reset(void) {
+    for (HarnessStats* h : all_harness_stats()) {
+        std::string name = h->name;
+        *h = HarnessStats{};
+        h->name = name;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+#pragma once
+// runtime.hpp — process-wide device context, error boundary and counters of
+// the B200 harness library (host side).
+
+#include "b200.hpp"
+
+#include <chrono>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+namespace b200 {
+
+using lilac::marshal::MarshalObject;
+using lilac::marshal::MarshalObjectBase;
+using lilac::marshal::Strategy;
+
+// Out type of the input/output transfer classes (B200Read / B200Write): a
+// device allocation plus the bytes this binding has moved.
+struct DevArray {
+    DevBuf buf;
+    std::int64_t h2d = 0;
+    std::int64_t d2h = 0;
+};
+
+struct HarnessStats {
+    std::string name;
+    std::int64_t calls = 0;
+    double t_total_ms = 0, t_poll_ms = 0, t_kernel_ms = 0, t_writeback_ms = 0;
+    std::int64_t bytes_h2d = 0, bytes_d2h = 0;
+};
+
+struct Runtime {
+    bool inited = false;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;
+    // scratch: partials for deterministic reductions, ticket, flags
+    DevBuf partials, scalars, flags;
+    CsrKernel kernel = CsrKernel::Auto;
+    Strategy strategy = Strategy::Hybrid;
+    bool exact_blas = false;
+    std::size_t stage_bytes = std::size_t(256) << 20;  // chunk for narrowing uploads
+    DevBuf stage;
+
+    unsigned int* d_ticket() const { return scalars.as<unsigned int>(); }
+    double* d_result() const { return reinterpret_cast<double*>(scalars.as<char>() + 64); }
+    unsigned long long* d_umax() const { return reinterpret_cast<unsigned long long*>(flags.as<char>()); }
+    int* d_bad() const { return reinterpret_cast<int*>(flags.as<char>() + 8); }
+};
+
+Runtime& rt();
+void ensure_init();  // lazy first-call init + atexit teardown
+void shutdown();
+
+// Region stats registry (harness objects + their transfer counters).
+void register_region(MarshalObjectBase* obj, const std::int64_t* h2d, const std::int64_t* d2h);
+HarnessStats& harness_stats(const char* name);
+std::vector<HarnessStats*> all_harness_stats();
+struct RegionEntry {
+    MarshalObjectBase* obj;
+    const std::int64_t* h2d;
+    const std::int64_t* d2h;
+};
+const std::vector<RegionEntry>& all_regions();
+
+// ---- error boundary -----------------------------------------------------------
+
+void set_error(const char* code, const std::string& msg);
+const char* current_error();
+void clear_error();
+int error_mode();
+
+// Runs f; on exception records it and aborts (default) or returns -1.
+template <typename F>
+int boundary(const char* fn, F&& f) {
+    try {
+        clear_error();
+        f();
+        return 0;
+    } catch (const Error& e) {
+        set_error(lilac::marshal::errc_name(e.code()), std::string(fn) + ": " + e.what());
+    } catch (const std::exception& e) {
+        set_error("HookFailure", std::string(fn) + ": " + e.what());
+    }
+    if (error_mode() == 0) {
+        std::fprintf(stderr, "lilac-b200: %s\n", current_error());
+        std::fflush(stderr);
+        std::abort();
+    }
+    return -1;
+}
+
+// ---- transfer helpers (stream-ordered, synchronous w.r.t. the host) --------------
+
+void upload(DevArray& d, const void* host, std::size_t bytes);
+void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter);
+
+// Resident CSR / JDS uploads shared by the harnesses and the device API.
+struct CsrUpload {
+    DevBuf row_ptr, col, val;
+    CsrDev dev;
+    std::int64_t bytes_moved = 0;
+};
+// Upload + validate row_ptr for `rows` (nnz = row_ptr[rows]).
+void upload_row_ptr(DevBuf& buf, const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz,
+                    std::int64_t* max_row, bool* monotone);
+// Upload col_ind[0..nnz) narrowing to int32 when possible; returns cols.
+std::int64_t upload_col_ind(DevBuf& buf, const std::int64_t* col_ind, std::int64_t nnz, bool* col32);
+
+using Clock = std::chrono::steady_clock;
+inline double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+}  // namespace b200

@@ -1,0 +1,135 @@
+"""Resident-device API (section 4-7 of include/lilac_b200.h) for drivers,
+benchmarks and tests. Device pointers / streams are plain integers (e.g.
+``torch.Tensor.data_ptr()`` and ``torch.cuda.Stream.cuda_stream``)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+class Matrix:
+    """A CSR or JDS matrix uploaded once and kept resident in HBM."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def csr(cls, row_ptr, col_ind, val, rows=None):
+        rows = len(row_ptr) - 1 if rows is None else rows
+        h = C.c_void_p()
+        rc = N.lib().b200_matrix_create_csr(C.byref(h), rows, N.ptr(row_ptr), N.ptr(col_ind), N.ptr(val))
+        N.check(rc)
+        return cls(h)
+
+    @classmethod
+    def jds(cls, nzcnt, perm, val, jd_ptr, col_ind):
+        h = C.c_void_p()
+        rc = N.lib().b200_matrix_create_jds(C.byref(h), len(perm), N.ptr(nzcnt), N.ptr(perm), N.ptr(val),
+                                            N.ptr(jd_ptr), N.ptr(col_ind))
+        N.check(rc)
+        return cls(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        i = N.MatrixInfo()
+        N.check(N.lib().b200_matrix_info_get(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in N.MatrixInfo._fields_}
+
+    def spmv(self, x_ptr: int, y_ptr: int, stream: int = 0):
+        rc = N.lib().b200_spmv_device(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(stream))
+        if rc:
+            N.check(rc)
+
+    def free(self):
+        if self._h:
+            N.lib().b200_matrix_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def dot(a_ptr: int, b_ptr: int, n: int, out_ptr: int, stream: int = 0):
+    N.check(N.lib().b200_dot_device(C.c_void_p(a_ptr), C.c_void_p(b_ptr), n, C.c_void_p(out_ptr),
+                                    C.c_void_p(stream)))
+
+
+class CG:
+    """NPB CG solver state over a resident CSR matrix."""
+
+    def __init__(self, A: Matrix):
+        h = C.c_void_p()
+        N.check(N.lib().b200_cg_create(C.byref(h), A.handle))
+        self._h = h
+        self.A = A
+
+    def reset(self, stream: int = 0):
+        N.check(N.lib().b200_cg_reset(self._h, C.c_void_p(stream)))
+
+    def outer(self, shift: float, cgitmax: int = 25, stream: int = 0):
+        rc = N.lib().b200_cg_outer(self._h, cgitmax, shift, C.c_void_p(stream))
+        if rc:
+            N.check(rc)
+
+    def step(self, stream: int = 0):
+        N.check(N.lib().b200_cg_step(self._h, C.c_void_p(stream)))
+
+    def result(self):
+        z = C.c_double()
+        r = C.c_double()
+        N.check(N.lib().b200_cg_result(self._h, C.byref(z), C.byref(r)))
+        return z.value, r.value
+
+    def npb(self, niter: int, shift: float):
+        z = C.c_double()
+        r = C.c_double()
+        N.check(N.lib().b200_npb_cg(self._h, niter, shift, C.byref(z), C.byref(r)))
+        return z.value, r.value
+
+    def free(self):
+        if self._h:
+            N.lib().b200_cg_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+# NPB CG classes (NPB 3.x): na, nonzer, niter, shift, zeta_verify
+NPB_CLASSES = {
+    "S": (1400, 7, 15, 10.0, 8.5971775078648),
+    "W": (7000, 8, 15, 12.0, 10.362595087124),
+    "A": (14000, 11, 15, 20.0, 17.130235054029),
+    "B": (75000, 13, 75, 60.0, 22.712745482631),
+    "C": (150000, 15, 75, 110.0, 28.973605592845),
+}
+
+
+def gen_npb(na: int, nonzer: int, shift: float):
+    """NPB makea via the native generator: (row_ptr, col_ind, val)."""
+    L = N.lib()
+    rp = np.zeros(na + 1, np.int64)
+    nnz = np.zeros(1, np.int64)
+    N.check(L.b200_gen_npb(na, nonzer, shift, N.ptr(rp), None, None, N.ptr(nnz)))
+    ci = np.empty(int(nnz[0]), np.int64)
+    val = np.empty(int(nnz[0]), np.float64)
+    N.check(L.b200_gen_npb(na, nonzer, shift, N.ptr(rp), N.ptr(ci), N.ptr(val), N.ptr(nnz)))
+    return rp, ci, val
+
+
+def partition_rows(row_ptr, k: int):
+    b = np.zeros(k + 1, np.int64)
+    N.lib().b200_partition_rows(len(row_ptr) - 1, N.ptr(row_ptr), k, N.ptr(b))
+    return b

@@ -1,0 +1,131 @@
+"""Host-side mirror of the reference's harness interface for the B200 path.
+
+The reference exposes this path as named callables: the interpreter's
+``HarnessRegistry`` holds ``"lilac.<computation>"`` entries whose arguments
+arrive in ``infer_interface`` order (src/interp.cpp:330-389,
+include/lilac/interp.hpp:73-83), and compiled programs call the generated
+``extern "C"`` harness symbols (src/harnessgen.cpp:86-92). This module offers
+the same names, argument order and error behaviour over numpy arrays, backed
+by liblilac_b200.so: every call goes through the C ABI (no CPU path).
+
+    spmv_csr(rows, output, row_ptr, val, x, col_ind)
+    spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind)
+    dotproduct(length, a, b) -> float        (scalar-result protocol: the
+                                             result slot is synthesized,
+                                             interp.cpp:335-346, 385)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+
+__all__ = ["spmv_csr", "spmv_jds", "dotproduct", "axpy", "xpay", "HarnessRegistry",
+           "register_b200_harnesses", "region_stats", "harness_stats", "B200Error", "set_errors_return"]
+
+B200Error = N.B200Error
+
+
+def _f64(a, name, writable=False):
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise TypeError(f"{name}: expected a C-contiguous float64 numpy array")
+    if writable and not a.flags.writeable:
+        raise TypeError(f"{name}: output must be writable")
+    return a
+
+
+def _i64(a, name):
+    if not isinstance(a, np.ndarray) or a.dtype != np.int64 or not a.flags.c_contiguous:
+        raise TypeError(f"{name}: expected a C-contiguous int64 numpy array")
+    return a
+
+
+def set_errors_return(on: bool = True):
+    """Return-with-exception instead of abort on harness errors (tests)."""
+    N.lib().b200_set_error_mode(1 if on else 0)
+
+
+def spmv_csr(rows, output, row_ptr, val, x, col_ind):
+    L = N.lib()
+    L.b200_spmv_csr(int(rows), N.ptr(_f64(output, "output", True)), N.ptr(_i64(row_ptr, "row_ptr")),
+                    N.ptr(_f64(val, "val")), N.ptr(_f64(x, "x")), N.ptr(_i64(col_ind, "col_ind")))
+    N.check()
+
+
+def spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind):
+    L = N.lib()
+    L.b200_spmv_jds(int(rows), N.ptr(_f64(output, "output", True)), N.ptr(_i64(nzcnt, "nzcnt")),
+                    N.ptr(_i64(perm, "perm")), N.ptr(_f64(val, "val")), N.ptr(_i64(jd_ptr, "jd_ptr")),
+                    N.ptr(_f64(x, "x")), N.ptr(_i64(col_ind, "col_ind")))
+    N.check()
+
+
+def dotproduct(length, a, b) -> float:
+    res = np.zeros(1, np.float64)
+    N.lib().b200_dot(N.ptr(res), int(length), N.ptr(_f64(a, "a")), N.ptr(_f64(b, "b")))
+    N.check()
+    return float(res[0])
+
+
+def axpy(n, y, alpha, x):
+    N.lib().b200_axpy(int(n), N.ptr(_f64(y, "y", True)), float(alpha), N.ptr(_f64(x, "x")))
+    N.check()
+
+
+def xpay(n, y, beta, x):
+    N.lib().b200_xpay(int(n), N.ptr(_f64(y, "y", True)), float(beta), N.ptr(_f64(x, "x")))
+    N.check()
+
+
+class HarnessRegistry:
+    """Name -> callable table (reference interp.hpp:75-83: add/find/names;
+    add() of an existing name raises, like DuplicateRegistration)."""
+
+    def __init__(self):
+        self._fns = {}
+
+    def add(self, name, fn):
+        if name in self._fns:
+            raise KeyError(f"DuplicateRegistration: harness '{name}' already registered")
+        self._fns[name] = fn
+
+    def find(self, name):
+        return self._fns.get(name)
+
+    def names(self):
+        return sorted(self._fns)
+
+
+def register_b200_harnesses(reg: HarnessRegistry, computations=("spmv_csr", "spmv_jds", "dotproduct")):
+    """Counterpart of interp::register_reference_harnesses (interp.cpp:330):
+    registers the B200 harnesses under "lilac.<computation>"."""
+    table = {"spmv_csr": spmv_csr, "spmv_jds": spmv_jds, "dotproduct": dotproduct}
+    for c in computations:
+        reg.add("lilac." + c, table[c])
+    return reg
+
+
+def region_stats():
+    """Marshal counters per region: the `run --stats` rows of the reference CLI
+    (tools/lilac_main.cpp:599-612) plus transfer bytes."""
+    L = N.lib()
+    n = L.b200_region_stats_get(None, 0)
+    arr = (N.RegionStats * max(n, 1))()
+    L.b200_region_stats_get(arr, n)
+    names = ["pageprotect", "checksum", "exact", "naive", "hybrid"]
+    return {r.region.decode(): {"n_construct": r.n_construct, "n_update": r.n_update, "n_destruct": r.n_destruct,
+                                "bytes_h2d": r.bytes_h2d, "bytes_d2h": r.bytes_d2h,
+                                "strategy": names[r.strategy], "fell_back": bool(r.fell_back),
+                                "streaming": bool(r.streaming), "constructed": bool(r.constructed)}
+            for r in arr[:n]}
+
+
+def harness_stats():
+    L = N.lib()
+    n = L.b200_harness_stats_get(None, 0)
+    arr = (N.HarnessStats * max(n, 1))()
+    L.b200_harness_stats_get(arr, n)
+    return {h.harness.decode(): {"calls": h.calls, "t_total_ms": h.t_total_ms, "t_poll_ms": h.t_poll_ms,
+                                 "t_kernel_ms": h.t_kernel_ms, "t_writeback_ms": h.t_writeback_ms,
+                                 "bytes_h2d": h.bytes_h2d, "bytes_d2h": h.bytes_d2h}
+            for h in arr[:n]}

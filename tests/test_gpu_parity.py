@@ -1,0 +1,327 @@
+"""GPU parity of the B200 harness path against the oracle (B200 only).
+
+Every call goes through the C ABI (liblilac_b200.so). Bars:
+  * exact CSR kernel, JDS kernel, axpy/xpay, exact dot: bit-identical to the
+    reference CPU harness (golden fixtures written by the reference itself) and
+    to the oracle restatement pinned to it;
+  * fast CSR kernel and fast dot: |y - y_ref| <= TOL * sum_j |a_ij x_j| per
+    element, TOL = 1e-12 (north star: "1e-12 for fp64 SpMV"), exact zero when
+    the row has no nonzero products;
+  * NPB CG: zeta within 1e-10 relative of NPB's official value.
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2001_07938_b200 import _native as N
+from paper_2001_07938_b200 import device as D
+from paper_2001_07938_b200 import harness as H
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(autouse=True)
+def _mode():
+    H.set_errors_return(True)
+    N.lib().b200_set_kernel(b"auto")
+    N.lib().b200_set_exact_blas(0)
+    yield
+    N.lib().b200_set_kernel(b"auto")
+    N.lib().b200_set_exact_blas(0)
+
+
+def spmv_bound(rp, ci, val, x):
+    """sum_j |a_ij x_j| per row (the standard SpMV error-bound scale)."""
+    rows = len(rp) - 1
+    return O.spmv_csr(rp, ci, np.abs(val), np.abs(x)[: max(1, len(x))], rows) if rows else np.zeros(0)
+
+
+def assert_within(y, y_ref, scale, tol=TOL):
+    err = np.abs(y - y_ref)
+    bad = err > tol * scale
+    assert not bad.any(), f"{bad.sum()} rows exceed tol; worst {np.max(err / np.maximum(scale, 1e-300))}"
+
+
+def run_csr(rp, ci, val, x, rows=None):
+    rows = len(rp) - 1 if rows is None else rows
+    y = np.full(rows, np.nan)
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    return y
+
+
+# --------------------------------------------------------------------------------
+# golden fixtures (reference outputs)
+# --------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_golden_csr_exact_bitwise(name, case):
+    c = O.case_arrays(case)
+    N.lib().b200_set_kernel(b"exact")
+    y = run_csr(c["row_ptr"], c["col_ind"], c["val"], c["x"])
+    assert O.same_bits(y, c["y_csr"])
+
+
+@pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_golden_csr_fast_within_tolerance(name, case):
+    c = O.case_arrays(case)
+    y = run_csr(c["row_ptr"], c["col_ind"], c["val"], c["x"])
+    assert_within(y, c["y_csr"], spmv_bound(c["row_ptr"], c["col_ind"], c["val"], c["x"]))
+
+
+@pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_golden_jds_bitwise(name, case):
+    c = O.case_arrays(case)
+    y = np.full(c["rows"], np.nan)
+    H.spmv_jds(c["rows"], y, c["nzcnt"], c["perm"], c["jds_val"], c["jd_ptr"], c["x"], c["jds_col_ind"])
+    assert O.same_bits(y, c["y_jds"])
+
+
+def test_golden_sample5():
+    s = O.golden("sample5.json")
+    for key, want in (("ones", [2, 4, 4, 2, 0]), ("counting", [4, 12, 15, 8, 2])):
+        c = O.case_arrays(s[key])
+        y = run_csr(c["row_ptr"], c["col_ind"], c["val"], c["x"])
+        assert y.tolist() == want
+
+
+def test_golden_dot():
+    cases = O.golden("dot_seed5150.json")["cases"]
+    for exact in (1, 0):
+        N.lib().b200_set_exact_blas(exact)
+        for c in cases:
+            a = np.array(c["a"], np.float64)
+            b = np.array(c["b"], np.float64)
+            r = H.dotproduct(len(a), a, b)
+            if exact:
+                assert O.same_bits(np.array([r]), np.array([c["result"]]))
+            else:
+                assert abs(r - c["result"]) <= TOL * float(np.sum(np.abs(a * b))) or r == c["result"]
+    r = H.dotproduct(0, np.zeros(0), np.zeros(0))
+    assert r == 0.0 and not np.signbit(r)
+
+
+# --------------------------------------------------------------------------------
+# seeded random matrices at scale (vs the pinned oracle)
+# --------------------------------------------------------------------------------
+
+def random_csr(rng, rows, cols, lens):
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(rp[-1])
+    ci = np.empty(nnz, np.int64)
+    for i in range(rows):
+        k = lens[i]
+        if k:
+            ci[rp[i]:rp[i + 1]] = np.sort(rng.choice(cols, size=min(k, cols), replace=k > cols))
+    val = rng.uniform(-2, 2, nnz)
+    return rp, ci, val
+
+
+SHAPES = {
+    "short_rows": (20000, 20000, lambda r, n: r.integers(0, 8, n)),
+    "npb_like": (3000, 3000, lambda r, n: r.integers(150, 330, n)),
+    "stencil_like": (30000, 30000, lambda r, n: np.full(n, 27)),
+    "skewed": (5000, 5000, lambda r, n: np.minimum(r.zipf(1.6, n), 4000)),
+    "long_rows": (40, 200000, lambda r, n: r.integers(5000, 60000, n)),
+    "empty_rows": (1000, 1000, lambda r, n: np.where(r.random(n) < 0.5, 0, r.integers(1, 40, n))),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(SHAPES))
+def test_random_csr_vs_oracle(shape):
+    rows, cols, lens_fn = SHAPES[shape]
+    rng = np.random.default_rng(zlib.crc32(shape.encode()))
+    lens = np.asarray(lens_fn(rng, rows), np.int64)
+    rp, ci, val = random_csr(rng, rows, cols, lens)
+    x = rng.uniform(-2, 2, cols)
+    y_ref = O.spmv_csr(rp, ci, val, x)
+    y = run_csr(rp, ci, val, x)
+    assert_within(y, y_ref, spmv_bound(rp, ci, val, x))
+    N.lib().b200_set_kernel(b"exact")
+    assert O.same_bits(run_csr(rp, ci, val, x), y_ref)
+    # JDS of the same matrix (encoder pinned to oracles.hpp:109-144): bit-exact
+    perm, nzcnt, jd_ptr, jval, jcol = O.jds_from_csr(rp, ci, val)
+    yj = np.full(rows, np.nan)
+    H.spmv_jds(rows, yj, nzcnt, perm, jval, jd_ptr, x, jcol)
+    assert O.same_bits(yj, y_ref)
+
+
+def test_edge_cases():
+    # rows = 0
+    y = np.zeros(0)
+    H.spmv_csr(0, y, np.zeros(1, np.int64), np.zeros(0), np.zeros(0), np.zeros(0, np.int64))
+    # all rows empty
+    y = run_csr(np.zeros(11, np.int64), np.zeros(0, np.int64), np.zeros(0), np.zeros(0))
+    assert np.all(y == 0) and not np.signbit(y).any()
+    # row_ptr not starting at 0: leading nonzeros are simply not addressed
+    rp = np.array([3, 5, 6], np.int64)
+    ci = np.array([9, 9, 9, 0, 1, 1], np.int64)
+    val = np.array([7.0, 7, 7, 1, 2, 4])
+    x = np.array([10.0, 100] + [0] * 8)
+    assert run_csr(rp, ci, val, x).tolist() == [210.0, 400.0]
+    # non-monotone row_ptr: the reference treats the row as empty
+    rp = np.array([0, 2, 1, 3], np.int64)
+    ci = np.array([0, 1, 2], np.int64)
+    val = np.array([1.0, 2, 3])
+    x = np.array([1.0, 1, 1])
+    assert run_csr(rp, ci, val, x).tolist() == O.spmv_csr(rp, ci, val, x).tolist() == [3.0, 0.0, 5.0]
+    # one very long row
+    n = 300000
+    rng = np.random.default_rng(0)
+    rp = np.array([0, n], np.int64)
+    ci = np.arange(n, dtype=np.int64)
+    val = rng.uniform(-1, 1, n)
+    x = rng.uniform(-1, 1, n)
+    assert_within(run_csr(rp, ci, val, x), O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
+
+
+def test_out_of_bounds_is_an_error_not_a_fallback():
+    rp = np.array([0, 2], np.int64)
+    ci = np.array([0, -1], np.int64)
+    y = np.full(1, 123.0)
+    with pytest.raises(H.B200Error) as e:
+        H.spmv_csr(1, y, rp, np.ones(2), np.ones(2), ci)
+    assert e.value.code == "OutOfBounds"
+    assert y[0] == 123.0
+    # JDS: perm outside [0, rows)
+    with pytest.raises(H.B200Error) as e:
+        H.spmv_jds(2, np.zeros(2), np.array([1, 1], np.int64), np.array([0, 5], np.int64), np.ones(2),
+                   np.array([0, 2], np.int64), np.ones(2), np.array([0, 1], np.int64))
+    assert e.value.code == "OutOfBounds"
+
+
+def test_blas1_bitwise():
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 17, 100003):
+        x = rng.uniform(-2, 2, n)
+        y = rng.uniform(-2, 2, n)
+        want = O.axpy(y, 0.37, x)
+        yy = y.copy()
+        H.axpy(n, yy, 0.37, x)
+        assert O.same_bits(yy, want)
+        want = x + (-1.25 * y)  # x + beta*y, separate rounding as in NPB's p = r + beta*p
+        yy = y.copy()
+        H.xpay(n, yy, -1.25, x)
+        assert O.same_bits(yy, want)
+        r = H.dotproduct(n, x, y)
+        assert abs(r - O.dot(x, y)) <= TOL * float(np.sum(np.abs(x * y))) + 0.0
+        N.lib().b200_set_exact_blas(1)
+        assert O.same_bits(np.array([H.dotproduct(n, x, y)]), np.array([O.dot(x, y)]))
+        N.lib().b200_set_exact_blas(0)
+
+
+# --------------------------------------------------------------------------------
+# marshaling contract through the harness (resident matrix, vector-only traffic)
+# --------------------------------------------------------------------------------
+
+def test_resident_matrix_moves_only_vectors():
+    rng = np.random.default_rng(11)
+    rows = 4096
+    rp, ci, val = random_csr(rng, rows, rows, rng.integers(10, 40, rows))
+    stats0 = H.region_stats()
+    base = {k: v["n_update"] for k, v in stats0.items()}
+    h2d0 = {k: v["bytes_h2d"] for k, v in stats0.items()}
+    for call in range(10):
+        x = rng.uniform(-1, 1, rows)
+        y = run_csr(rp, ci, val, x)
+        assert_within(y, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
+    st = H.region_stats()
+    upd = {k: st[k]["n_update"] - base.get(k, 0) for k in st}
+    assert upd["b200_spmv_csr.val"] == 1
+    assert upd["b200_spmv_csr.row_ptr"] == 1
+    assert upd["b200_spmv_csr.col_ind"] == 1
+    assert upd["b200_spmv_csr.x"] == 10
+    assert st["b200_spmv_csr.val"]["bytes_h2d"] - h2d0.get("b200_spmv_csr.val", 0) == 8 * len(val)
+    assert st["b200_spmv_csr.x"]["streaming"]  # rewritten every call: no longer guarded
+    assert not st["b200_spmv_csr.val"]["streaming"]
+    # in-place mutation of the resident matrix is seen (never stale)
+    x = rng.uniform(-1, 1, rows)
+    val[len(val) // 2] += 1.0
+    y = run_csr(rp, ci, val, x)
+    assert_within(y, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
+    assert H.region_stats()["b200_spmv_csr.val"]["n_update"] - base.get("b200_spmv_csr.val", 0) == 2
+    # edge bytes of a misaligned numpy buffer are hashed (Hybrid): mutate the first element
+    val[0] += 1.0
+    y = run_csr(rp, ci, val, x)
+    assert_within(y, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
+    # identity change -> destruct + construct
+    val2 = val.copy()
+    d0 = H.region_stats()["b200_spmv_csr.val"]["n_destruct"]
+    run_csr(rp, ci, val2, x)
+    assert H.region_stats()["b200_spmv_csr.val"]["n_destruct"] == d0 + 1
+
+
+# --------------------------------------------------------------------------------
+# NPB CG
+# --------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cls", ["S", "A", "C"])
+def test_npb_cg_zeta_device_driver(cls):
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    A = D.Matrix.csr(rp, ci, val)
+    cg = D.CG(A)
+    zeta, rnorm = cg.npb(niter, shift)
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10, (zeta, zeta_ref)
+    assert rnorm < 1e-10
+    cg.free()
+    A.free()
+
+
+def test_npb_cg_class_s_through_the_c_abi_harnesses():
+    """The LiLAC model: the host program keeps its CG loop; SpMV/dot/axpy are
+    replaced by harness calls on host arrays (vectors move every call)."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES["S"]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    n = na
+    x = np.ones(n)
+    zeta = 0.0
+    for it in range(niter + 1):
+        z = np.zeros(n)
+        r = x.copy()
+        p = r.copy()
+        q = np.zeros(n)
+        rho = H.dotproduct(n, r, r)
+        for _ in range(25):
+            H.spmv_csr(n, q, rp, val, p, ci)
+            d = H.dotproduct(n, p, q)
+            alpha = rho / d
+            rho0 = rho
+            H.axpy(n, z, alpha, p)
+            H.axpy(n, r, -alpha, q)
+            rho = H.dotproduct(n, r, r)
+            H.xpay(n, p, rho / rho0, r)
+        t1 = H.dotproduct(n, x, z)
+        t2 = 1.0 / np.sqrt(H.dotproduct(n, z, z))
+        if it > 0:
+            zeta = shift + 1.0 / t1
+        x = t2 * z if it > 0 else np.ones(n)
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10
+    st = H.region_stats()
+    assert st["b200_spmv_csr.val"]["n_update"] >= 1
+    assert st["b200_spmv_csr.val"]["bytes_h2d"] <= 8 * len(val) * 2
+
+
+def test_device_api_spmv_and_dot():
+    import torch
+    rng = np.random.default_rng(5)
+    rows = 10000
+    rp, ci, val = random_csr(rng, rows, rows, rng.integers(0, 64, rows))
+    A = D.Matrix.csr(rp, ci, val)
+    info = A.info()
+    assert info["rows"] == rows and info["nnz"] == len(val) and info["col_bytes"] == 4
+    x = rng.uniform(-1, 1, rows)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty(rows, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream()
+    A.spmv(xd.data_ptr(), yd.data_ptr(), s.cuda_stream)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    D.dot(xd.data_ptr(), yd.data_ptr(), rows, out.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    y_ref = O.spmv_csr(rp, ci, val, x)
+    assert_within(yd.cpu().numpy(), y_ref, spmv_bound(rp, ci, val, x))
+    assert abs(out.item() - O.dot(x, y_ref)) <= 1e-10 * float(np.sum(np.abs(x * y_ref)))
+    A.free()
