@@ -47,9 +47,31 @@ void pool_trim();  // return every cached block to CUDA
 // Resident sparse matrices (device layout)
 // ---------------------------------------------------------------------------
 
-enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3 };
+enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3, Tiled = 4 };
 const char* csr_kernel_name(CsrKernel k);
 CsrKernel parse_csr_kernel(const std::string& s);
+
+// Tiled CSR (upload-time cached invariant, tcsr_build.cpp): rows cut into
+// tiles (one CTA each), columns into slabs of kSlabW that fit shared memory.
+// Inside a tile the nonzeros are ordered slab-major, then by the owning warp's
+// contiguous row range, then by row, so each (slab, warp) is one contiguous
+// run; each nonzero carries a packed key = slab-local column | tile-local row
+// << 16 (4 bytes, the same HBM cost as an int32 column index).
+constexpr int kTileThreads = 1024;
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kSlabW = 12288;       // columns per slab: 2 x 96 KB double-buffered in smem
+constexpr int kMaxTileRows = 4096;  // tile-local row fits the key and the smem y buffer
+
+struct TcsrDev {
+    std::int64_t ntiles = 0;
+    int nslabs = 0;
+    std::int64_t cols = 0;
+    const std::int64_t* tile_row0 = nullptr;  // ntiles + 1 row bounds
+    const std::int64_t* tile_base = nullptr;  // ntiles + 1 element offsets
+    const std::int32_t* woff = nullptr;       // ntiles x (nslabs*kTileWarps + 1), tile-relative
+    const double* val = nullptr;              // nnz, tiled order
+    const std::uint32_t* key = nullptr;       // nnz, lcol | lrow << 16
+};
 
 struct CsrDev {
     std::int64_t rows = 0;      // number of rows computed
@@ -61,6 +83,7 @@ struct CsrDev {
     bool col32 = true;
     const double* val = nullptr;            // nnz
     bool monotone = true;                   // row_ptr non-decreasing
+    const TcsrDev* tiled = nullptr;         // present when the tiled layout was built
 };
 
 struct JdsDev {
@@ -86,6 +109,9 @@ CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested);
 int csr_vector_width(const CsrDev& A);  // lanes per row for the vector kernel
 
 void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s);
+// Tiled kernel (tcsr.cu); partials/ticket/sc non-null = fused p.q for CG.
+void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
+                       unsigned int* ticket, struct CgScalars* sc, cudaStream_t s);
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s);
 
 struct CgScalars;

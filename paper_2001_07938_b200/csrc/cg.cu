@@ -158,7 +158,7 @@ void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
 }
 
 void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
-    launch_spmv_csr(A, v.z, v.r, CsrKernel::Vector, s);
+    launch_spmv_csr(A, v.z, v.r, CsrKernel::Auto, s);
     k_cg_resid<<<vec_grid(v), kThreads, 0, s>>>(v);
     B200_CUDA(cudaGetLastError());
 }

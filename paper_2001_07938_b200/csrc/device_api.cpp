@@ -4,6 +4,7 @@
 
 #include "lilac_b200.h"
 #include "runtime.hpp"
+#include "tcsr.hpp"
 
 #include <algorithm>
 #include <memory>
@@ -17,6 +18,7 @@ struct b200_matrix {
     DevBuf nzcnt, perm, inv_perm, jd_ptr;  // JDS (+col, val)
     CsrDev csr;
     JdsDev jds;
+    TcsrOwner tiled;
     std::int64_t max_row = 0;
 };
 
@@ -60,6 +62,7 @@ int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int6
         d.val = A->val.as<double>();
         d.monotone = monotone;
         A->max_row = max_row;
+        if (A->tiled.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel)) d.tiled = &A->tiled.dev;
         *out = A.release();
     });
 }
@@ -133,6 +136,7 @@ void b200_matrix_free(b200_matrix* A) {
     A->perm.release();
     A->inv_perm.release();
     A->jd_ptr.release();
+    A->tiled.release();
     delete A;
 }
 
@@ -158,7 +162,8 @@ int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
             info->lanes = 1;
         }
         info->device_bytes = static_cast<std::int64_t>(A->row_ptr.bytes + A->col.bytes + A->val.bytes + A->nzcnt.bytes +
-                                                       A->perm.bytes + A->inv_perm.bytes + A->jd_ptr.bytes);
+                                                       A->perm.bytes + A->inv_perm.bytes + A->jd_ptr.bytes) +
+                             A->tiled.bytes;
     });
 }
 

@@ -13,6 +13,7 @@
 
 #include "lilac_b200.h"
 #include "runtime.hpp"
+#include "tcsr.hpp"
 
 #include <cstring>
 
@@ -153,8 +154,20 @@ struct spmv_csr_state {
     MarshalObject<DevArray> m_val;
     MarshalObject<DevArray> m_x;
     MarshalObject<DevArray> m_output;
+    TcsrOwner tiled;                // derived layout, rebuilt when the matrix changes
+    std::int64_t tiled_stamp = -1;  // sum of matrix update/construct counters it was built at
+    CsrKernel tiled_policy = CsrKernel::Auto;
     bool first_run_done = false;
 };
+
+std::int64_t matrix_stamp(const spmv_csr_state& st) {
+    std::int64_t s = 0;
+    for (const MarshalObjectBase* m :
+         {static_cast<const MarshalObjectBase*>(&st.m_row_ptr), static_cast<const MarshalObjectBase*>(&st.m_col_ind),
+          static_cast<const MarshalObjectBase*>(&st.m_val)})
+        s += m->counters().n_update + m->counters().n_construct;
+    return s;
+}
 
 spmv_csr_state& csr_state() {
     static spmv_csr_state* st = new spmv_csr_state;  // outlives atexit teardown
@@ -307,6 +320,15 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         A.col32 = ci.col32;
         A.val = dval.buf.as<double>();
         A.monotone = rp.monotone;
+        // derived tiled layout: rebuilt only when row_ptr/col_ind/val were re-marshaled
+        const std::int64_t stamp = matrix_stamp(state);
+        if (stamp != state.tiled_stamp || rt().kernel != state.tiled_policy) {
+            state.tiled.refresh(rows, row_ptr, col_ind, val, ci.cols, rp.monotone, rp.max_row, rt().kernel);
+            state.tiled_stamp = stamp;
+            state.tiled_policy = rt().kernel;
+        }
+        if (state.tiled.valid) A.tiled = &state.tiled.dev;
+        tm.acquired();
         timed_launch(hs, [&] { launch_spmv_csr(A, dx.buf.as<double>(), dout.buf.as<double>(), rt().kernel, rt().stream); });
         tm.acquired();
 

@@ -396,6 +396,7 @@ const char* csr_kernel_name(CsrKernel k) {
     case CsrKernel::Vector: return "vector";
     case CsrKernel::Merge: return "merge";
     case CsrKernel::Exact: return "exact";
+    case CsrKernel::Tiled: return "tiled";
     }
     return "?";
 }
@@ -405,7 +406,8 @@ CsrKernel parse_csr_kernel(const std::string& s) {
     if (s == "vector") return CsrKernel::Vector;
     if (s == "merge") return CsrKernel::Merge;
     if (s == "exact") return CsrKernel::Exact;
-    throw Error(Errc::DataError, "unknown CSR kernel '" + s + "' (auto, vector, merge, exact)");
+    if (s == "tiled") return CsrKernel::Tiled;
+    throw Error(Errc::DataError, "unknown CSR kernel '" + s + "' (auto, vector, tiled, exact)");
 }
 
 int csr_vector_width(const CsrDev& A) {
@@ -417,8 +419,11 @@ int csr_vector_width(const CsrDev& A) {
 }
 
 CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested) {
-    if (requested != CsrKernel::Auto) return requested == CsrKernel::Merge ? CsrKernel::Vector : requested;
-    return CsrKernel::Vector;
+    if (requested == CsrKernel::Exact) return CsrKernel::Exact;
+    if (requested == CsrKernel::Vector || requested == CsrKernel::Merge) return CsrKernel::Vector;
+    // Auto / Tiled: the tiled layout exists only when it was judged to pay
+    // (tcsr_wanted) or was forced at upload
+    return A.tiled ? CsrKernel::Tiled : CsrKernel::Vector;
 }
 
 static unsigned vector_grid(const CsrDev& A, int S) {
@@ -428,6 +433,10 @@ static unsigned vector_grid(const CsrDev& A, int S) {
 void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s) {
     if (A.rows <= 0) return;
     k = choose_csr_kernel(A, k);
+    if (k == CsrKernel::Tiled) {
+        launch_spmv_tiled(*A.tiled, A.rows, x, y, nullptr, nullptr, nullptr, s);
+        return;
+    }
     if (k == CsrKernel::Exact) {
         unsigned g = grid_for(A.rows);
         if (A.col32)
@@ -447,6 +456,10 @@ void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, c
 
 void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* partials, unsigned* ticket,
                          CgScalars* sc, cudaStream_t s) {
+    if (A.tiled) {
+        launch_spmv_tiled(*A.tiled, A.rows, p, q, partials, ticket, sc, s);
+        return;
+    }
     const int S = csr_vector_width(A);
     const unsigned g = std::min<unsigned>(vector_grid(A, S), kMaxParts);
     if (A.col32)

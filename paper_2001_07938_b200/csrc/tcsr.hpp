@@ -1,0 +1,41 @@
+#pragma once
+// tcsr.hpp — host side of the tiled CSR layout (builder + device owner).
+
+#include "b200.hpp"
+
+#include <cstdint>
+#include <vector>
+
+namespace b200 {
+
+struct TcsrHost {
+    std::int64_t ntiles = 0;
+    int nslabs = 0;
+    std::int64_t cols = 0;
+    std::vector<std::int64_t> tile_row0, tile_base;
+    std::vector<std::int32_t> woff;
+    std::vector<double> val;
+    std::vector<std::uint32_t> key;
+};
+
+// Does the tiled layout pay for this matrix? (monotone row_ptr, >= 1M nnz,
+// no row dominating a warp's share, and poor x-gather locality.) `forced`
+// skips the size/locality tests.
+bool tcsr_wanted(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, std::int64_t cols,
+                 bool monotone, std::int64_t max_row, bool forced);
+void tcsr_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind,
+                     const double* val, std::int64_t cols, TcsrHost& out);
+
+struct TcsrOwner {
+    DevBuf tile_row0, tile_base, woff, val, key;
+    TcsrDev dev;
+    bool valid = false;
+    std::int64_t bytes = 0;
+    void upload(const TcsrHost& h);
+    void release();
+    // Rebuild (or drop) the layout for new host arrays under the kernel policy.
+    bool refresh(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, const double* val,
+                 std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy);
+};
+
+}  // namespace b200

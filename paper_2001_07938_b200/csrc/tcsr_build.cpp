@@ -1,0 +1,195 @@
+// tcsr_build.cpp — builds the tiled CSR layout (see b200.hpp TcsrDev) from the
+// caller's host CSR arrays at upload time, and decides when it pays.
+//
+// The layout is a cached invariant of (row_ptr, col_ind, val): the harness
+// rebuilds it only when one of them was re-marshaled. It is built on the host
+// (the arrays are there anyway at upload), in parallel over tiles, in O(nnz).
+
+#include "runtime.hpp"
+#include "tcsr.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+namespace b200 {
+
+namespace {
+
+std::int64_t lower_bound_rows(const std::int64_t* rp, std::int64_t lo, std::int64_t hi, std::int64_t v) {
+    // first r in [lo, hi] with rp[r] >= v
+    return std::lower_bound(rp + lo, rp + hi + 1, v) - rp;
+}
+
+template <typename F>
+void parallel_tiles(std::int64_t n, F&& f) {
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 64));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (std::int64_t i = t; i < n; i += nt) f(i);
+        });
+    for (auto& x : th) x.join();
+}
+
+int device_sms() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+}  // namespace
+
+bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, std::int64_t cols,
+                 bool monotone, std::int64_t max_row, bool forced) {
+    if (!monotone || rows <= 0) return false;
+    const std::int64_t nnz = rp[rows] - rp[0];
+    if (nnz <= 0 || cols <= 0) return false;
+    if (forced) return true;
+    if (nnz < (std::int64_t(1) << 20) || rows < 148 * kTileWarps) return false;
+    // one row must not dominate a warp's share (the tiled kernel never splits rows)
+    const std::int64_t per_warp = nnz / (static_cast<std::int64_t>(device_sms()) * kTileWarps);
+    if (max_row > 16 * std::max<std::int64_t>(per_warp, 64)) return false;
+    // gather locality: distinct 32-byte x sectors per nonzero over windows of
+    // 32 consecutive rows (a warp's worth). ~1 = every gather its own sector.
+    double ratio_sum = 0;
+    int windows = 0;
+    std::vector<std::int64_t> sec;
+    for (int w = 0; w < 64; ++w) {
+        const std::int64_t r0 = rows * w / 64, r1 = std::min(rows, r0 + 32);
+        sec.clear();
+        for (std::int64_t j = rp[r0]; j < rp[r1]; ++j) sec.push_back(ci[j] >> 2);
+        if (sec.size() < 64) continue;
+        std::sort(sec.begin(), sec.end());
+        const auto distinct = std::unique(sec.begin(), sec.end()) - sec.begin();
+        ratio_sum += static_cast<double>(distinct) / static_cast<double>(sec.size());
+        ++windows;
+    }
+    return windows > 0 && ratio_sum / windows > 0.3;
+}
+
+void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* val,
+                     std::int64_t cols, TcsrHost& h) {
+    const std::int64_t base0 = rp[0];
+    const std::int64_t nnz = rp[rows] - base0;
+    const int sms = device_sms();
+    h.cols = cols;
+    h.nslabs = static_cast<int>((cols + kSlabW - 1) / kSlabW);
+    // tiles: nnz-balanced, a multiple of the SM count, none taller than kMaxTileRows
+    std::vector<std::int64_t> bounds;
+    const std::int64_t want = std::max<std::int64_t>(sms, (rows + kMaxTileRows - 1) / kMaxTileRows);
+    const std::int64_t nt0 = (want + sms - 1) / sms * sms;
+    bounds.push_back(0);
+    for (std::int64_t g = 1; g < nt0; ++g) {
+        std::int64_t r = lower_bound_rows(rp, 0, rows, base0 + (nnz * g + nt0 - 1) / nt0);
+        r = std::max(std::min(r, rows), bounds.back());
+        bounds.push_back(r);
+    }
+    bounds.push_back(rows);
+    h.tile_row0.clear();
+    for (std::size_t t = 0; t + 1 < bounds.size(); ++t) {
+        const std::int64_t a = bounds[t], b = bounds[t + 1];
+        const std::int64_t pieces = std::max<std::int64_t>(1, (b - a + kMaxTileRows - 1) / kMaxTileRows);
+        for (std::int64_t p = 0; p < pieces; ++p) h.tile_row0.push_back(a + (b - a) * p / pieces);
+    }
+    h.tile_row0.push_back(rows);
+    h.ntiles = static_cast<std::int64_t>(h.tile_row0.size()) - 1;
+    h.tile_base.resize(h.ntiles + 1);
+    for (std::int64_t t = 0; t <= h.ntiles; ++t) h.tile_base[t] = rp[h.tile_row0[t]] - base0;
+    const std::int64_t per_tile = static_cast<std::int64_t>(h.nslabs) * kTileWarps + 1;
+    h.woff.assign(static_cast<std::size_t>(h.ntiles * per_tile), 0);
+    h.val.resize(static_cast<std::size_t>(nnz));
+    h.key.resize(static_cast<std::size_t>(nnz));
+
+    parallel_tiles(h.ntiles, [&](std::int64_t t) {
+        const std::int64_t row0 = h.tile_row0[t], row1 = h.tile_row0[t + 1];
+        const std::int64_t tb = h.tile_base[t];
+        // warp row ranges, nnz-balanced
+        std::int64_t wb[kTileWarps + 1];
+        wb[0] = row0;
+        const std::int64_t tn = rp[row1] - rp[row0];
+        for (int g = 1; g < kTileWarps; ++g) {
+            std::int64_t r = lower_bound_rows(rp, row0, row1, rp[row0] + (tn * g + kTileWarps - 1) / kTileWarps);
+            wb[g] = std::max(std::min(r, row1), wb[g - 1]);
+        }
+        wb[kTileWarps] = row1;
+        std::int32_t* wo = h.woff.data() + t * per_tile;
+        std::vector<std::int64_t> cnt(static_cast<std::size_t>(per_tile), 0);
+        for (int w = 0; w < kTileWarps; ++w)
+            for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
+                for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) cnt[(ci[j] / kSlabW) * kTileWarps + w]++;
+        std::int64_t off = 0;
+        for (std::int64_t i = 0; i + 1 < per_tile; ++i) {
+            wo[i] = static_cast<std::int32_t>(off);
+            off += cnt[i];
+        }
+        wo[per_tile - 1] = static_cast<std::int32_t>(off);
+        std::vector<std::int64_t> cur(wo, wo + per_tile);
+        for (int w = 0; w < kTileWarps; ++w)
+            for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r) {
+                const std::uint32_t lrow = static_cast<std::uint32_t>(r - row0) << 16;
+                for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
+                    const std::int64_t k = ci[j] / kSlabW;
+                    const std::int64_t pos = tb + cur[k * kTileWarps + w]++;
+                    h.val[pos] = val[j];
+                    h.key[pos] = lrow | static_cast<std::uint32_t>(ci[j] - k * kSlabW);
+                }
+            }
+    });
+}
+
+void TcsrOwner::upload(const TcsrHost& h) {
+    cudaStream_t s = rt().stream;
+    tile_row0.ensure(h.tile_row0.size() * 8);
+    tile_base.ensure(h.tile_base.size() * 8);
+    woff.ensure(h.woff.size() * 4);
+    val.ensure(h.val.size() * 8);
+    key.ensure(h.key.size() * 4);
+    B200_CUDA(cudaMemcpyAsync(tile_row0.ptr, h.tile_row0.data(), h.tile_row0.size() * 8, cudaMemcpyHostToDevice, s));
+    B200_CUDA(cudaMemcpyAsync(tile_base.ptr, h.tile_base.data(), h.tile_base.size() * 8, cudaMemcpyHostToDevice, s));
+    if (!h.woff.empty())
+        B200_CUDA(cudaMemcpyAsync(woff.ptr, h.woff.data(), h.woff.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!h.val.empty()) {
+        B200_CUDA(cudaMemcpyAsync(val.ptr, h.val.data(), h.val.size() * 8, cudaMemcpyHostToDevice, s));
+        B200_CUDA(cudaMemcpyAsync(key.ptr, h.key.data(), h.key.size() * 4, cudaMemcpyHostToDevice, s));
+    }
+    B200_CUDA(cudaStreamSynchronize(s));
+    dev.ntiles = h.ntiles;
+    dev.nslabs = h.nslabs;
+    dev.cols = h.cols;
+    dev.tile_row0 = tile_row0.as<std::int64_t>();
+    dev.tile_base = tile_base.as<std::int64_t>();
+    dev.woff = woff.as<std::int32_t>();
+    dev.val = val.as<double>();
+    dev.key = key.as<std::uint32_t>();
+    bytes = static_cast<std::int64_t>(tile_row0.bytes + tile_base.bytes + woff.bytes + val.bytes + key.bytes);
+    valid = true;
+}
+
+void TcsrOwner::release() {
+    tile_row0.release();
+    tile_base.release();
+    woff.release();
+    val.release();
+    key.release();
+    dev = TcsrDev{};
+    valid = false;
+    bytes = 0;
+}
+
+bool TcsrOwner::refresh(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* v,
+                        std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy) {
+    const bool forced = policy == CsrKernel::Tiled;
+    if (policy == CsrKernel::Vector || policy == CsrKernel::Exact ||
+        !tcsr_wanted(rows, rp, ci, cols, monotone, max_row, forced)) {
+        release();
+        return false;
+    }
+    TcsrHost h;
+    tcsr_build_host(rows, rp, ci, v, cols, h);
+    upload(h);
+    return true;
+}
+
+}  // namespace b200

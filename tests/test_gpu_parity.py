@@ -73,6 +73,14 @@ def test_golden_csr_fast_within_tolerance(name, case):
 
 
 @pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_golden_csr_tiled_within_tolerance(name, case):
+    c = O.case_arrays(case)
+    N.lib().b200_set_kernel(b"tiled")
+    y = run_csr(c["row_ptr"], c["col_ind"], c["val"], c["x"])
+    assert_within(y, c["y_csr"], spmv_bound(c["row_ptr"], c["col_ind"], c["val"], c["x"]))
+
+
+@pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
 def test_golden_jds_bitwise(name, case):
     c = O.case_arrays(case)
     y = np.full(c["rows"], np.nan)
@@ -140,6 +148,9 @@ def test_random_csr_vs_oracle(shape):
     y_ref = O.spmv_csr(rp, ci, val, x)
     y = run_csr(rp, ci, val, x)
     assert_within(y, y_ref, spmv_bound(rp, ci, val, x))
+    for kernel in (b"vector", b"tiled"):
+        N.lib().b200_set_kernel(kernel)
+        assert_within(run_csr(rp, ci, val, x), y_ref, spmv_bound(rp, ci, val, x))
     N.lib().b200_set_kernel(b"exact")
     assert O.same_bits(run_csr(rp, ci, val, x), y_ref)
     # JDS of the same matrix (encoder pinned to oracles.hpp:109-144): bit-exact
@@ -224,8 +235,9 @@ def test_resident_matrix_moves_only_vectors():
     stats0 = H.region_stats()
     base = {k: v["n_update"] for k, v in stats0.items()}
     h2d0 = {k: v["bytes_h2d"] for k, v in stats0.items()}
+    x = np.zeros(rows)
     for call in range(10):
-        x = rng.uniform(-1, 1, rows)
+        x[:] = rng.uniform(-1, 1, rows)  # the host rewrites x in place every call
         y = run_csr(rp, ci, val, x)
         assert_within(y, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
     st = H.region_stats()
@@ -238,7 +250,7 @@ def test_resident_matrix_moves_only_vectors():
     assert st["b200_spmv_csr.x"]["streaming"]  # rewritten every call: no longer guarded
     assert not st["b200_spmv_csr.val"]["streaming"]
     # in-place mutation of the resident matrix is seen (never stale)
-    x = rng.uniform(-1, 1, rows)
+    x[:] = rng.uniform(-1, 1, rows)
     val[len(val) // 2] += 1.0
     y = run_csr(rp, ci, val, x)
     assert_within(y, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
@@ -258,11 +270,15 @@ def test_resident_matrix_moves_only_vectors():
 # NPB CG
 # --------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("cls", ["S", "A", "C"])
-def test_npb_cg_zeta_device_driver(cls):
+@pytest.mark.parametrize("cls,kernel", [("S", b"auto"), ("A", b"auto"), ("A", b"tiled"), ("A", b"vector"),
+                                        ("C", b"auto"), ("C", b"vector")])
+def test_npb_cg_zeta_device_driver(cls, kernel):
     na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
     rp, ci, val = D.gen_npb(na, nonzer, shift)
+    N.lib().b200_set_kernel(kernel)
     A = D.Matrix.csr(rp, ci, val)
+    if cls == "C" and kernel == b"auto":
+        assert A.info()["kernel"] == 4  # the tiled layout is chosen for NPB's random columns
     cg = D.CG(A)
     zeta, rnorm = cg.npb(niter, shift)
     assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10, (zeta, zeta_ref)
