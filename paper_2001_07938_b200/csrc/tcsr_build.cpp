@@ -9,6 +9,7 @@
 #include "tcsr.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -78,7 +79,9 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     h.nslabs = static_cast<int>((cols + kSlabW - 1) / kSlabW);
     // tiles: nnz-balanced, a multiple of the SM count, none taller than kMaxTileRows
     std::vector<std::int64_t> bounds;
-    const std::int64_t want = std::max<std::int64_t>(sms, (rows + kMaxTileRows - 1) / kMaxTileRows);
+    const char* tps = std::getenv("LILAC_B200_TILES_PER_SM");
+    const std::int64_t per_sm = (tps && *tps) ? std::max(1, std::atoi(tps)) : 1;
+    const std::int64_t want = std::max<std::int64_t>(sms * per_sm, (rows + kMaxTileRows - 1) / kMaxTileRows);
     const std::int64_t nt0 = (want + sms - 1) / sms * sms;
     bounds.push_back(0);
     for (std::int64_t g = 1; g < nt0; ++g) {

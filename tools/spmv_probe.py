@@ -49,10 +49,11 @@ def main():
     N.check(N.lib().b200_init(0))
     rp, ci, val = D.gen_npb(150000, 15, 110.0)
     n = len(rp) - 1
-    for kern in (b"auto", b"vector", b"tiled"):
+    for kern in (b"vector", b"tiled"):
         N.lib().b200_set_kernel(kern)
         A = D.Matrix.csr(rp, ci, val)
-        report("npb_c/" + kern.decode(), A, rp, a.reps)
+        report("npb_c/" + kern.decode() + "/pf" + os.environ.get("LILAC_B200_TILED_PF", "d"), A, rp, a.reps)
+        report("npb_c/" + kern.decode() + "/again", A, rp, a.reps)
         A.free()
     N.lib().b200_set_kernel(b"auto")
     if a.only == "npb":
