@@ -26,10 +26,7 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned kSent = 0xffffu;  // sentinel tile-local row (> kMaxTileRows)
 constexpr std::size_t kTileSmem = sizeof(double) * (2 * kSlabW + kMaxTileRows);
-#ifndef B200_TILED_PREFETCH
-#define B200_TILED_PREFETCH 1
-#endif
-constexpr int kPrefetch = B200_TILED_PREFETCH;  // chunks in flight beyond the one being reduced
+constexpr int kDefaultEpl = 4;  // nonzeros per lane per chunk (4 or 8)
 
 __device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -104,6 +101,24 @@ __device__ __forceinline__ void issue_slab(const TcsrDev& T, const double* __res
     if (even) bulk_g2s(xs, src, static_cast<unsigned>(even) * 8u, mbar);
 }
 
+// Asynchronous L2 prefetch of [p, p+bytes) by the bulk-copy engine: no
+// registers, no completion tracking. Range widened to 16-byte granules.
+__device__ __forceinline__ void prefetch_l2(const void* p, std::size_t bytes) {
+    const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(p) & ~std::uintptr_t(15);
+    const std::uintptr_t e = (reinterpret_cast<std::uintptr_t>(p) + bytes + 15) & ~std::uintptr_t(15);
+    if (e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<unsigned>(e - a))
+                     : "memory");
+}
+
+// Prefetch a (slab, warp) run's val and key bytes into L2.
+__device__ __forceinline__ void prefetch_run(const double* vb, const std::uint32_t* kb, int lo, int hi) {
+    if (hi > lo) {
+        prefetch_l2(vb + lo, static_cast<std::size_t>(hi - lo) * 8);
+        prefetch_l2(kb + lo, static_cast<std::size_t>(hi - lo) * 4);
+    }
+}
+
 __device__ __forceinline__ double lds_f64(std::uint32_t addr) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
@@ -116,29 +131,47 @@ __device__ __forceinline__ void sts_add_f64(std::uint32_t addr, double v) {
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(o + v));
 }
 
-struct Chunk {
-    double2 v0, v1;
-    uint4 k;
-};
-
-// A lane's four consecutive nonzeros of a (slab, warp) run, tile-relative
-// index j (predicated on j < hi; over-reads stay inside the padded arrays).
-__device__ __forceinline__ Chunk load_chunk(const double* vb, const std::uint32_t* kb, int j, int hi) {
-    Chunk c;
-    if (j < hi) {
-        ld_stream_f64x4(vb + j, c.v0, c.v1);
-        c.k = ld_stream_u32x4(kb + j);
-    } else {
-        c.v0 = c.v1 = make_double2(0.0, 0.0);
-        c.k = make_uint4(0, 0, 0, 0);
-    }
-    return c;
+__device__ __forceinline__ void ld_stream_u32x8(const std::uint32_t* p, unsigned (&k)[8]) {
+    asm("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3]), "=r"(k[4]), "=r"(k[5]), "=r"(k[6]), "=r"(k[7])
+        : "l"(p));
 }
 
-// One 128-nonzero piece, after the lane-local pass: lane holds its head run
-// (k0, p0) and tail run (k1, p1) (k0 == k1: a single run, value p1). Row keys
-// are non-decreasing across lanes. Adds every row's piece-sum into yp[row]
-// (rows are owned by this warp).
+// A lane's EPL consecutive nonzeros of a (slab, warp) run (tile-relative
+// index j, EPL-aligned in absolute terms so every load is 32-byte aligned).
+template <int EPL>
+struct Chunk {
+    double v[EPL];
+    unsigned k[EPL];
+};
+
+template <int EPL>
+__device__ __forceinline__ void load_chunk(Chunk<EPL>& c, const double* vb, const std::uint32_t* kb, int j, int hi) {
+    if (j < hi) {
+        if constexpr (EPL == 4) {
+            double2 a, b;
+            ld_stream_f64x4(vb + j, a, b);
+            c.v[0] = a.x, c.v[1] = a.y, c.v[2] = b.x, c.v[3] = b.y;
+            const uint4 k = ld_stream_u32x4(kb + j);
+            c.k[0] = k.x, c.k[1] = k.y, c.k[2] = k.z, c.k[3] = k.w;
+        } else {
+            double2 a, b, d, e;
+            ld_stream_f64x4(vb + j, a, b);
+            ld_stream_f64x4(vb + j + 4, d, e);
+            c.v[0] = a.x, c.v[1] = a.y, c.v[2] = b.x, c.v[3] = b.y;
+            c.v[4] = d.x, c.v[5] = d.y, c.v[6] = e.x, c.v[7] = e.y;
+            ld_stream_u32x8(kb + j, c.k);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) c.v[e] = 0.0, c.k[e] = 0;
+    }
+}
+
+// One warp piece after the lane-local pass: lane holds its head run (k0, p0)
+// and tail run (k1, p1) (k0 == k1: a single run, value p1). Row keys are
+// non-decreasing across lanes. Adds every row's piece-sum into yp[row]
+// (rows are owned by this warp: no atomics, fixed order).
 __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1, double p1, int lane,
                                              std::uint32_t yp_s) {
     const bool split = k0 != k1;
@@ -158,15 +191,16 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
     if ((lane == 31 || nk0 != k1) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
 }
 
-// Lane-local pass over 4 consecutive nonzeros (keys non-decreasing): rows
+// Lane-local pass over EPL consecutive nonzeros (keys non-decreasing): rows
 // strictly inside the lane are exclusive to it and flushed here; the head and
 // tail runs go to the warp-level reduce_piece.
-__device__ __forceinline__ void lane_runs(const unsigned (&key)[4], const double (&p)[4], int lane,
+template <int EPL>
+__device__ __forceinline__ void lane_runs(const unsigned (&key)[EPL], const double (&p)[EPL], int lane,
                                           std::uint32_t yp_s) {
     double acc = p[0], head = 0.0;
     unsigned rk = key[0];
 #pragma unroll
-    for (int e = 1; e < 4; ++e) {
+    for (int e = 1; e < EPL; ++e) {
         if (key[e] == rk) {
             acc += p[e];
         } else {
@@ -183,54 +217,53 @@ __device__ __forceinline__ void lane_runs(const unsigned (&key)[4], const double
 
 // Processes a (slab, warp) run [lo, hi) (tile-relative) against the slab in
 // shared memory at xb_s. Interior chunks take an unmasked fast path; the first
-// and last chunk of a run mask elements outside [lo, hi).
-template <int PF, int MODE>
+// and last chunk of a run mask elements outside [lo, hi). The run's bytes were
+// prefetched into L2 one slab ahead, so loads here are L2 hits.
+template <int EPL, int MODE, bool RPF>
 __device__ __forceinline__ void process_run(const double* vb, const std::uint32_t* kb, int mis, int lo, int hi,
                                             std::uint32_t xb_s, std::uint32_t yp_s, int lane) {
-    // 32-byte alignment is absolute: `mis` = tile base mod 4
-    const int c0 = ((lo + mis) & ~3) - mis;
-    Chunk q[PF + 1];
+    constexpr int CH = 32 * EPL;
+    const int c0 = ((lo + mis) & ~(EPL - 1)) - mis;  // absolute EPL alignment; mis = base mod EPL
+    Chunk<EPL> cur, nxt;
+    if (RPF) load_chunk<EPL>(cur, vb, kb, c0 + EPL * lane, hi);
+    for (int c = c0; c < hi; c += CH) {
+        if (RPF)
+            load_chunk<EPL>(nxt, vb, kb, c + CH + EPL * lane, hi);  // one chunk ahead in registers
+        else
+            load_chunk<EPL>(cur, vb, kb, c + EPL * lane, hi);
+        unsigned key[EPL];
+        double p[EPL];
+        if (c >= lo && c + CH <= hi) {  // warp-uniform: every element valid
 #pragma unroll
-    for (int i = 0; i < PF; ++i) q[i] = load_chunk(vb, kb, c0 + 128 * i + 4 * lane, hi);
-    for (int c = c0; c < hi; c += 128) {
-        q[PF] = load_chunk(vb, kb, c + 128 * PF + 4 * lane, hi);  // prefetch PF chunks ahead
-        const Chunk cur = q[0];
-#pragma unroll
-        for (int i = 0; i < PF; ++i) q[i] = q[i + 1];
-        const double ev[4] = {cur.v0.x, cur.v0.y, cur.v1.x, cur.v1.y};
-        const unsigned kw[4] = {cur.k.x, cur.k.y, cur.k.z, cur.k.w};
-        unsigned key[4];
-        double p[4];
-        if (c >= lo && c + 128 <= hi) {  // warp-uniform: every element valid
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const double xv = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (kw[e] & 0xffffu));
-                key[e] = kw[e] >> 16;
-                p[e] = ev[e] * xv;
+            for (int e = 0; e < EPL; ++e) {
+                const double xv = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (cur.k[e] & 0xffffu));
+                key[e] = cur.k[e] >> 16;
+                p[e] = cur.v[e] * xv;
             }
         } else {
-            const int j = c + 4 * lane;
+            const int j = c + EPL * lane;
             const int front = lo - j, back = hi - j;  // element e valid iff front <= e < back
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const double xv = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (kw[e] & 0xffffu));
-                key[e] = e < back ? kw[e] >> 16 : kSent;
-                p[e] = (e >= front && e < back) ? ev[e] * xv : 0.0;
+            for (int e = 0; e < EPL; ++e) {
+                const double xv = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (cur.k[e] & 0xffffu));
+                key[e] = e < back ? cur.k[e] >> 16 : kSent;
+                p[e] = (e >= front && e < back) ? cur.v[e] * xv : 0.0;
             }
             // leading elements before lo (first chunk, lane 0) take the next key
 #pragma unroll
-            for (int e = 2; e >= 0; --e)
+            for (int e = EPL - 2; e >= 0; --e)
                 if (e < front) key[e] = key[e + 1];
         }
         if (MODE >= 2) {
             if (p[0] == 12345.678) sts_add_f64(yp_s, p[1]);  // probe: no reduction
         } else {
-            lane_runs(key, p, lane, yp_s);
+            lane_runs<EPL>(key, p, lane, yp_s);
         }
+        if (RPF) cur = nxt;
     }
 }
 
-template <bool DOT, int PF, int MODE = 0>
+template <bool DOT, int EPL, int MODE = 0>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_spmv_tiled(TcsrDev T, const double* __restrict__ x, double* __restrict__ y, double* partials,
                  unsigned int* ticket, CgScalars* sc) {
@@ -260,6 +293,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         const std::uint32_t* kb = T.key + base;
         const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
         for (int r = tid; r < nrows; r += kTileThreads) yp[r] = 0.0;
+        if (lane == 0 && T.nslabs > 0) prefetch_run(vb, kb, wo[warp], wo[warp + 1]);
         if (tid == 0 && T.nslabs > 0 && MODE < 5) {
             issue_slab(T, x, xs, 0, &mbar[0]);
             if (T.nslabs > 1) issue_slab(T, x, xs + kSlabW, 1, &mbar[1]);
@@ -277,8 +311,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                 mbar_wait(&mbar[1], phase1);
                 phase1 ^= 1;
             }
-            process_run<PF, MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
-                vb, kb, static_cast<int>(base & 3), wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1],
+            if (lane == 0 && k + 1 < T.nslabs)  // next slab's run streams into L2 meanwhile
+                prefetch_run(vb, kb, wo[(k + 1) * kTileWarps + warp], wo[(k + 1) * kTileWarps + warp + 1]);
+            process_run<EPL, MODE == 5 ? 3 : (MODE == 6 ? 0 : (MODE == 7 ? 0 : MODE)), MODE != 7>(
+                vb, kb, static_cast<int>(base & (EPL - 1)), wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1],
                 xs_s + 8u * static_cast<unsigned>(buf * kSlabW), yp_s, lane);
             __syncwarp();
             if (lane == 0) {
@@ -337,62 +373,55 @@ int g_sms = 0;
 
 }  // namespace
 
-template <int MODE, int PF>
-void launch_probe(const TcsrDev& T, const double* x, double* y, unsigned grid, cudaStream_t s) {
+template <int EPL, int MODE>
+void launch_variant(const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
+                    CgScalars* sc, unsigned grid, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, PF, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, EPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kTileSmem)));
-        configured = true;
-    }
-    k_spmv_tiled<false, PF, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr);
-}
-
-template <int PF>
-void launch_pf(const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket, CgScalars* sc,
-               unsigned grid, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kTileSmem)));
-        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<true, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<true, EPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kTileSmem)));
         configured = true;
     }
     if (partials)
-        k_spmv_tiled<true, PF><<<std::min<unsigned>(grid, kMaxParts), kTileThreads, kTileSmem, s>>>(T, x, y, partials,
-                                                                                                   ticket, sc);
+        k_spmv_tiled<true, EPL, MODE><<<std::min<unsigned>(grid, kMaxParts), kTileThreads, kTileSmem, s>>>(
+            T, x, y, partials, ticket, sc);
     else
-        k_spmv_tiled<false, PF><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr);
+        k_spmv_tiled<false, EPL, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr);
+}
+
+template <int EPL>
+void launch_epl(int mode, const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
+                CgScalars* sc, unsigned grid, cudaStream_t s) {
+    switch (partials ? 0 : mode) {  // probes (wrong results, timing only) never for the fused CG path
+    case 1: launch_variant<EPL, 1>(T, x, y, partials, ticket, sc, grid, s); break;
+    case 2: launch_variant<EPL, 2>(T, x, y, partials, ticket, sc, grid, s); break;
+    case 5: launch_variant<EPL, 5>(T, x, y, partials, ticket, sc, grid, s); break;
+    case 6: launch_variant<EPL, 6>(T, x, y, partials, ticket, sc, grid, s); break;
+    case 7: launch_variant<EPL, 7>(T, x, y, partials, ticket, sc, grid, s); break;
+    default: launch_variant<EPL, 0>(T, x, y, partials, ticket, sc, grid, s); break;
+    }
 }
 
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
                        unsigned int* ticket, CgScalars* sc, cudaStream_t s) {
-    static int pf = -1;
-    if (pf < 0) {
+    static int epl = -1, mode = 0;
+    if (epl < 0) {
         int dev = 0;
         B200_CUDA(cudaGetDevice(&dev));
         B200_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
-        const char* e = std::getenv("LILAC_B200_TILED_PF");
-        pf = (e && *e) ? std::atoi(e) : kPrefetch;
+        const char* e = std::getenv("LILAC_B200_TILED_EPL");
+        epl = (e && *e) ? std::atoi(e) : kDefaultEpl;
+        const char* m = std::getenv("LILAC_B200_TILED_PROBE");  // timing probes only: wrong results
+        mode = (m && *m) ? std::atoi(m) : 0;
     }
     if (rows <= 0 || T.ntiles <= 0) return;
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(T.ntiles, g_sms));
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = std::getenv("LILAC_B200_TILED_PROBE");  // timing probes only: wrong results
-        mode = (e && *e) ? std::atoi(e) : 0;
-    }
-    if (mode == 1 && !partials) launch_probe<1, 1>(T, x, y, grid, s);
-    else if (mode == 2 && !partials) launch_probe<2, 1>(T, x, y, grid, s);
-    else if (mode == 3 && !partials) launch_probe<3, 1>(T, x, y, grid, s);
-    else if (mode == 4 && !partials) launch_probe<3, 2>(T, x, y, grid, s);
-    else if (mode == 5 && !partials) launch_probe<5, 1>(T, x, y, grid, s);
-    else if (mode == 6 && !partials) launch_probe<6, 1>(T, x, y, grid, s);
-    else if (pf >= 2)
-        launch_pf<2>(T, x, y, partials, ticket, sc, grid, s);
+    if (epl == 8)
+        launch_epl<8>(mode, T, x, y, partials, ticket, sc, grid, s);
     else
-        launch_pf<1>(T, x, y, partials, ticket, sc, grid, s);
+        launch_epl<4>(mode, T, x, y, partials, ticket, sc, grid, s);
     B200_CUDA(cudaGetLastError());
 }
 

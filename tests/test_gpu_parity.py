@@ -295,6 +295,7 @@ def test_npb_cg_class_s_through_the_c_abi_harnesses():
     n = na
     x = np.ones(n)
     zeta = 0.0
+    h2d0 = H.region_stats().get("b200_spmv_csr.val", {}).get("bytes_h2d", 0)
     for it in range(niter + 1):
         z = np.zeros(n)
         r = x.copy()
@@ -317,8 +318,8 @@ def test_npb_cg_class_s_through_the_c_abi_harnesses():
         x = t2 * z if it > 0 else np.ones(n)
     assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10
     st = H.region_stats()
-    assert st["b200_spmv_csr.val"]["n_update"] >= 1
-    assert st["b200_spmv_csr.val"]["bytes_h2d"] <= 8 * len(val) * 2
+    # the matrix moved once; every later call moved only vectors
+    assert st["b200_spmv_csr.val"]["bytes_h2d"] - h2d0 == 8 * len(val)
 
 
 def test_device_api_spmv_and_dot():
