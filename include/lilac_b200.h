@@ -198,6 +198,33 @@ int b200_gen_npb(int64_t na, int nonzer, double shift, int64_t* row_ptr, int64_t
  * row_ptr[0] + ceil(g*nnz/k)), clamped monotone; bounds[0]=0, bounds[k]=rows. */
 void b200_partition_rows(int64_t rows, const int64_t* row_ptr, int k, int64_t* bounds);
 
+/* Row-sharded NPB CG: each shard owns rows [bounds[g],
+ * bounds[g+1]), keeps them resident, and all-gathers p every CG step (NCCL
+ * over NVLink; grouped broadcasts for the variable slice sizes); the two dot
+ * products are gathered in rank order and summed identically on every shard. */
+typedef struct b200_dist_cg b200_dist_cg;
+
+/* NCCL unique id (128 bytes) for b200_dist_cg_create_nccl; create on rank 0
+ * and share it (e.g. torch.distributed broadcast). */
+int b200_dist_nccl_id(void* id128);
+/* One shard per process: this process is `rank` of `world` and owns rows
+ * [bounds[rank], bounds[rank+1]); row_ptr has (rows+1) entries for those rows
+ * with offsets into col_ind/val (global column indices). */
+int b200_dist_cg_create_nccl(b200_dist_cg** out, int rank, int world, const void* nccl_id, int64_t n,
+                             const int64_t* bounds, const int64_t* row_ptr, const int64_t* col_ind,
+                             const double* val);
+/* k shards on this process's GPU exchanging by device copies: the same
+ * sharded algorithm, for single-GPU verification. Full CSR on input. */
+int b200_dist_cg_create_local(b200_dist_cg** out, int k, int64_t n, const int64_t* row_ptr,
+                              const int64_t* col_ind, const double* val);
+void b200_dist_cg_free(b200_dist_cg* d);
+int b200_dist_cg_reset(b200_dist_cg* d, void* stream);
+int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream);
+int b200_dist_cg_result(b200_dist_cg* d, double* zeta, double* rnorm);
+int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double* rnorm);
+int b200_dist_cg_info(const b200_dist_cg* d, int shard, int64_t* row0, int64_t* rows, int64_t* nnz,
+                      int32_t* tiled);
+
 #ifdef __cplusplus
 }
 #endif

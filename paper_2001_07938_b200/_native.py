@@ -77,6 +77,15 @@ SIGNATURES = {
     "b200_gen_npb": (C.c_int, [i64, C.c_int, C.c_double, i64p, i64p, f64p, i64p]),
     # 7. sharding
     "b200_partition_rows": (None, [i64, i64p, C.c_int, i64p]),
+    "b200_dist_nccl_id": (C.c_int, [vp]),
+    "b200_dist_cg_create_nccl": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, vp, i64, i64p, i64p, i64p, f64p]),
+    "b200_dist_cg_create_local": (C.c_int, [C.POINTER(vp), C.c_int, i64, i64p, i64p, f64p]),
+    "b200_dist_cg_free": (None, [vp]),
+    "b200_dist_cg_reset": (C.c_int, [vp, vp]),
+    "b200_dist_cg_outer": (C.c_int, [vp, C.c_int, C.c_double, vp]),
+    "b200_dist_cg_result": (C.c_int, [vp, f64p, f64p]),
+    "b200_dist_npb": (C.c_int, [vp, C.c_int, C.c_double, f64p, f64p]),
+    "b200_dist_cg_info": (C.c_int, [vp, C.c_int, i64p, i64p, i64p, C.POINTER(C.c_int32)]),
 }
 
 _lib = None

@@ -111,14 +111,15 @@ int csr_vector_width(const CsrDev& A);  // lanes per row for the vector kernel
 void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s);
 // Tiled kernel (tcsr.cu); partials/ticket/sc non-null = fused p.q for CG.
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
-                       unsigned int* ticket, struct CgScalars* sc, cudaStream_t s);
+                       unsigned int* ticket, struct CgScalars* sc, cudaStream_t s, std::int64_t dot_off = 0);
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s);
 
 struct CgScalars;
 // Fused CG kernel: q = A p and d = p.q in one pass; the last CTA sets
 // sc->d, sc->rho0 = sc->rho, sc->alpha = rho / d.
+// `dot_off`: global index of local row 0 (the dot reads p[dot_off + row]).
 void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* partials,
-                         unsigned int* ticket, CgScalars* sc, cudaStream_t s);
+                         unsigned int* ticket, CgScalars* sc, cudaStream_t s, std::int64_t dot_off = 0);
 
 // Upload-time validation / narrowing (one pass each, device side).
 //  * narrow_cols: col64[nnz] -> col32 (if col32 != null), max into *d_max, any
@@ -149,14 +150,19 @@ void launch_xpay(std::int64_t n, double* y, double beta, const double* x, cudaSt
 // NPB CG device step kernels (cg.cu)
 // ---------------------------------------------------------------------------
 
-struct CgScalars {  // device-resident, one per solver
+struct CgScalars {  // device-resident, one per solver (shard)
     double rho, rho0, d, alpha, beta, rnorm, t1, t2, zeta;
     unsigned int ticket[4];
+    int nranks;     // > 1: sharded mode — reductions stop at this shard's partial (part[]); exchange + fin_* follow
+    int pad;
+    double part[4];
 };
 
 struct CgVectors {
-    std::int64_t n;
-    double *x, *z, *p, *q, *r;
+    std::int64_t n;          // rows owned (all rows on one GPU)
+    double *x, *z, *p, *q, *r;  // owned slices; p/z point into p_full/z_full at row0
+    double *p_full, *z_full;    // full-length replicas the SpMV reads
+    std::int64_t row0;
     double* partials;  // 4 * kMaxParts
     int nparts;
     CgScalars* sc;
@@ -169,5 +175,18 @@ void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s);
 void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s);  // r=A z, rnorm
 void cg_launch_outer_update(const CgVectors& v, double shift, cudaStream_t s);  // zeta, x = z/|z|
 void cg_launch_reset_x(const CgVectors& v, cudaStream_t s);
+
+// Single steps (the sharded driver interleaves exchanges between them).
+void cg_launch_spmv_dot(const CsrDev& A, const CgVectors& v, cudaStream_t s);
+void cg_launch_update_zr(const CgVectors& v, cudaStream_t s);
+void cg_launch_update_p(const CgVectors& v, cudaStream_t s);
+void cg_launch_norms(const CgVectors& v, double shift, cudaStream_t s);
+void cg_launch_scale_x(const CgVectors& v, cudaStream_t s);
+void cg_launch_resid_partial(const CgVectors& v, cudaStream_t s);
+
+// Sharded CG (nranks > 1): finalize scalars from the rank-ordered gathered
+// partials of all shards (`gathered` holds nranks * stride doubles).
+enum class CgFin : int { Rho = 0, Alpha = 1, Beta = 2, Rnorm = 3, Norms = 4 };
+void cg_launch_fin(CgFin what, CgScalars* sc, const double* gathered, int nranks, double shift, cudaStream_t s);
 
 }  // namespace b200

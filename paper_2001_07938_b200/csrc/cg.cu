@@ -79,7 +79,12 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(CgVectors v) {
         rr += xi * xi;
     }
     double part[1] = {rr}, tot[1];
-    if (finish<1>(part, v.partials, &v.sc->ticket[1], tot) && threadIdx.x == 0) v.sc->rho = tot[0];
+    if (finish<1>(part, v.partials, &v.sc->ticket[1], tot) && threadIdx.x == 0) {
+        if (v.sc->nranks > 1)
+            v.sc->part[0] = tot[0];
+        else
+            v.sc->rho = tot[0];
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_cg_update_zr(CgVectors v) {
@@ -94,8 +99,12 @@ __global__ void __launch_bounds__(kThreads) k_cg_update_zr(CgVectors v) {
     }
     double part[1] = {rr}, tot[1];
     if (finish<1>(part, v.partials, &v.sc->ticket[1], tot) && threadIdx.x == 0) {
-        v.sc->rho = tot[0];
-        v.sc->beta = tot[0] / v.sc->rho0;
+        if (v.sc->nranks > 1) {
+            v.sc->part[0] = tot[0];
+        } else {
+            v.sc->rho = tot[0];
+            v.sc->beta = tot[0] / v.sc->rho0;
+        }
     }
 }
 
@@ -111,7 +120,12 @@ __global__ void __launch_bounds__(kThreads) k_cg_resid(CgVectors v) {
         s += d * d;
     }
     double part[1] = {s}, tot[1];
-    if (finish<1>(part, v.partials, &v.sc->ticket[2], tot) && threadIdx.x == 0) v.sc->rnorm = sqrt(tot[0]);
+    if (finish<1>(part, v.partials, &v.sc->ticket[2], tot) && threadIdx.x == 0) {
+        if (v.sc->nranks > 1)
+            v.sc->part[0] = tot[0];
+        else
+            v.sc->rnorm = sqrt(tot[0]);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_cg_norms(CgVectors v, double shift) {
@@ -123,9 +137,43 @@ __global__ void __launch_bounds__(kThreads) k_cg_norms(CgVectors v, double shift
     }
     double part[2] = {a, b}, tot[2];
     if (finish<2>(part, v.partials, &v.sc->ticket[3], tot) && threadIdx.x == 0) {
-        v.sc->t1 = tot[0];
-        v.sc->t2 = 1.0 / sqrt(tot[1]);
-        v.sc->zeta = shift + 1.0 / tot[0];
+        if (v.sc->nranks > 1) {
+            v.sc->part[0] = tot[0];
+            v.sc->part[1] = tot[1];
+        } else {
+            v.sc->t1 = tot[0];
+            v.sc->t2 = 1.0 / sqrt(tot[1]);
+            v.sc->zeta = shift + 1.0 / tot[0];
+        }
+    }
+}
+
+// Sharded finalisation: sum the shards' partials in rank order (deterministic).
+__global__ void k_cg_fin(int what, CgScalars* sc, const double* __restrict__ g, int nranks, double shift) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int stride = what == static_cast<int>(CgFin::Norms) ? 2 : 1;
+    double a = 0.0, b = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+        a += g[r * stride];
+        if (stride == 2) b += g[r * stride + 1];
+    }
+    switch (static_cast<CgFin>(what)) {
+    case CgFin::Rho: sc->rho = a; break;
+    case CgFin::Alpha:
+        sc->d = a;
+        sc->rho0 = sc->rho;
+        sc->alpha = sc->rho / a;
+        break;
+    case CgFin::Beta:
+        sc->rho = a;
+        sc->beta = a / sc->rho0;
+        break;
+    case CgFin::Rnorm: sc->rnorm = sqrt(a); break;
+    case CgFin::Norms:
+        sc->t1 = a;
+        sc->t2 = 1.0 / sqrt(b);
+        sc->zeta = shift + 1.0 / a;
+        break;
     }
 }
 
@@ -150,15 +198,48 @@ void cg_launch_init(const CgVectors& v, cudaStream_t s) {
     B200_CUDA(cudaGetLastError());
 }
 
-void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
-    launch_spmv_csr_dot(A, v.p, v.q, v.partials, &v.sc->ticket[0], v.sc, s);
+void cg_launch_fin(CgFin what, CgScalars* sc, const double* gathered, int nranks, double shift, cudaStream_t s) {
+    k_cg_fin<<<1, 32, 0, s>>>(static_cast<int>(what), sc, gathered, nranks, shift);
+    B200_CUDA(cudaGetLastError());
+}
+
+void cg_launch_spmv_dot(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
+    launch_spmv_csr_dot(A, v.p_full, v.q, v.partials, &v.sc->ticket[0], v.sc, s, v.row0);
+}
+
+void cg_launch_update_zr(const CgVectors& v, cudaStream_t s) {
     k_cg_update_zr<<<vec_grid(v), kThreads, 0, s>>>(v);
+    B200_CUDA(cudaGetLastError());
+}
+
+void cg_launch_update_p(const CgVectors& v, cudaStream_t s) {
     k_cg_update_p<<<vec_grid(v), kThreads, 0, s>>>(v);
     B200_CUDA(cudaGetLastError());
 }
 
+void cg_launch_norms(const CgVectors& v, double shift, cudaStream_t s) {
+    k_cg_norms<<<vec_grid(v), kThreads, 0, s>>>(v, shift);
+    B200_CUDA(cudaGetLastError());
+}
+
+void cg_launch_scale_x(const CgVectors& v, cudaStream_t s) {
+    k_cg_scale_x<<<vec_grid(v), kThreads, 0, s>>>(v);
+    B200_CUDA(cudaGetLastError());
+}
+
+void cg_launch_resid_partial(const CgVectors& v, cudaStream_t s) {
+    k_cg_resid<<<vec_grid(v), kThreads, 0, s>>>(v);
+    B200_CUDA(cudaGetLastError());
+}
+
+void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
+    cg_launch_spmv_dot(A, v, s);
+    cg_launch_update_zr(v, s);
+    cg_launch_update_p(v, s);
+}
+
 void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
-    launch_spmv_csr(A, v.z, v.r, CsrKernel::Auto, s);
+    launch_spmv_csr(A, v.z_full, v.r, CsrKernel::Auto, s);
     k_cg_resid<<<vec_grid(v), kThreads, 0, s>>>(v);
     B200_CUDA(cudaGetLastError());
 }

@@ -83,6 +83,9 @@ int b200_cg_create(b200_cg** out, const b200_matrix* Am) {
         cg->v.p = cg->p.as<double>();
         cg->v.q = cg->q.as<double>();
         cg->v.r = cg->r.as<double>();
+        cg->v.p_full = cg->v.p;
+        cg->v.z_full = cg->v.z;
+        cg->v.row0 = 0;
         cg->v.partials = cg->partials.as<double>();
         cg->v.sc = cg->scalars.as<CgScalars>();
         cg_launch_reset_x(cg->v, rt().stream);

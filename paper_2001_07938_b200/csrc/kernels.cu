@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
                                                          const double* __restrict__ x,
                                                          double* __restrict__ y,
                                                          double* __restrict__ partials,
-                                                         unsigned int* ticket, CgScalars* sc) {
+                                                         unsigned int* ticket, CgScalars* sc,
+                                                         std::int64_t dot_off) {
     const int lane = threadIdx.x & (S - 1);
     const unsigned gmask =
         S == 32 ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31) & ~(S - 1)));
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
         for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
         if (lane == 0) {
             y[row] = acc;
-            if (DOT) pq += acc * __ldg(x + row);
+            if (DOT) pq += acc * __ldg(x + dot_off + row);
         }
     }
     if (DOT) {
@@ -152,9 +153,13 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
         if (threadIdx.x == 0) partials[blockIdx.x] = s;
         double total;
         if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) {
-            sc->d = total;
-            sc->rho0 = sc->rho;
-            sc->alpha = sc->rho / total;
+            if (sc->nranks > 1) {
+                sc->part[0] = total;  // the shard's partial; alpha after the exchange
+            } else {
+                sc->d = total;
+                sc->rho0 = sc->rho;
+                sc->alpha = sc->rho / total;
+            }
         }
     }
 }
@@ -369,20 +374,20 @@ unsigned grid_for(std::int64_t threads, unsigned cap = kSMs * 16) {
 
 template <int S, typename IdxT, bool DOT>
 void vector_launch(const CsrDev& A, const double* x, double* y, double* partials, unsigned* ticket,
-                   CgScalars* sc, unsigned grid, cudaStream_t s) {
+                   CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
     k_csr_vector<S, 2, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
-                                                            A.val, x, y, partials, ticket, sc);
+                                                            A.val, x, y, partials, ticket, sc, dot_off);
 }
 
 template <typename IdxT, bool DOT>
 void vector_dispatch(const CsrDev& A, int S, const double* x, double* y, double* partials, unsigned* ticket,
-                     CgScalars* sc, unsigned grid, cudaStream_t s) {
+                     CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off = 0) {
     switch (S) {
-    case 2: vector_launch<2, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
-    case 4: vector_launch<4, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
-    case 8: vector_launch<8, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
-    case 16: vector_launch<16, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
-    default: vector_launch<32, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s); break;
+    case 2: vector_launch<2, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 4: vector_launch<4, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 8: vector_launch<8, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 16: vector_launch<16, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    default: vector_launch<32, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
     }
 }
 
@@ -455,17 +460,17 @@ void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, c
 }
 
 void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* partials, unsigned* ticket,
-                         CgScalars* sc, cudaStream_t s) {
+                         CgScalars* sc, cudaStream_t s, std::int64_t dot_off) {
     if (A.tiled) {
-        launch_spmv_tiled(*A.tiled, A.rows, p, q, partials, ticket, sc, s);
+        launch_spmv_tiled(*A.tiled, A.rows, p, q, partials, ticket, sc, s, dot_off);
         return;
     }
     const int S = csr_vector_width(A);
     const unsigned g = std::min<unsigned>(vector_grid(A, S), kMaxParts);
     if (A.col32)
-        vector_dispatch<std::int32_t, true>(A, S, p, q, partials, ticket, sc, g, s);
+        vector_dispatch<std::int32_t, true>(A, S, p, q, partials, ticket, sc, g, s, dot_off);
     else
-        vector_dispatch<std::int64_t, true>(A, S, p, q, partials, ticket, sc, g, s);
+        vector_dispatch<std::int64_t, true>(A, S, p, q, partials, ticket, sc, g, s, dot_off);
     B200_CUDA(cudaGetLastError());
 }
 

@@ -266,7 +266,7 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint32_
 template <bool DOT, int EPL, int MODE = 0>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_spmv_tiled(TcsrDev T, const double* __restrict__ x, double* __restrict__ y, double* partials,
-                 unsigned int* ticket, CgScalars* sc) {
+                 unsigned int* ticket, CgScalars* sc, std::int64_t dot_off) {
     extern __shared__ __align__(128) double smem[];
     double* xs = smem;               // [2][kSlabW]
     double* yp = smem + 2 * kSlabW;  // [kMaxTileRows]
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         for (int r = tid; r < nrows; r += kTileThreads) {
             const double v = yp[r];
             y[row0 + r] = v;
-            if (DOT) pq += v * __ldg(x + row0 + r);
+            if (DOT) pq += v * __ldg(x + dot_off + row0 + r);
         }
         __syncthreads();  // yp reused by the next tile
     }
@@ -359,9 +359,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             if (warp == 0) {
                 a = warp_sum(red[lane]);
                 if (lane == 0) {
-                    sc->d = a;
-                    sc->rho0 = sc->rho;
-                    sc->alpha = sc->rho / a;
+                    if (sc->nranks > 1) {
+                        sc->part[0] = a;  // the shard's partial; alpha after the exchange
+                    } else {
+                        sc->d = a;
+                        sc->rho0 = sc->rho;
+                        sc->alpha = sc->rho / a;
+                    }
                     *ticket = 0u;
                 }
             }
@@ -375,7 +379,7 @@ int g_sms = 0;
 
 template <int EPL, int MODE>
 void launch_variant(const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
-                    CgScalars* sc, unsigned grid, cudaStream_t s) {
+                    CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
     static bool configured = false;
     if (!configured) {
         B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, EPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -386,26 +390,26 @@ void launch_variant(const TcsrDev& T, const double* x, double* y, double* partia
     }
     if (partials)
         k_spmv_tiled<true, EPL, MODE><<<std::min<unsigned>(grid, kMaxParts), kTileThreads, kTileSmem, s>>>(
-            T, x, y, partials, ticket, sc);
+            T, x, y, partials, ticket, sc, dot_off);
     else
-        k_spmv_tiled<false, EPL, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr);
+        k_spmv_tiled<false, EPL, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr, 0);
 }
 
 template <int EPL>
 void launch_epl(int mode, const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
-                CgScalars* sc, unsigned grid, cudaStream_t s) {
+                CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
     switch (partials ? 0 : mode) {  // probes (wrong results, timing only) never for the fused CG path
-    case 1: launch_variant<EPL, 1>(T, x, y, partials, ticket, sc, grid, s); break;
-    case 2: launch_variant<EPL, 2>(T, x, y, partials, ticket, sc, grid, s); break;
-    case 5: launch_variant<EPL, 5>(T, x, y, partials, ticket, sc, grid, s); break;
-    case 6: launch_variant<EPL, 6>(T, x, y, partials, ticket, sc, grid, s); break;
-    case 7: launch_variant<EPL, 7>(T, x, y, partials, ticket, sc, grid, s); break;
-    default: launch_variant<EPL, 0>(T, x, y, partials, ticket, sc, grid, s); break;
+    case 1: launch_variant<EPL, 1>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 2: launch_variant<EPL, 2>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 5: launch_variant<EPL, 5>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 6: launch_variant<EPL, 6>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 7: launch_variant<EPL, 7>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    default: launch_variant<EPL, 0>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     }
 }
 
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
-                       unsigned int* ticket, CgScalars* sc, cudaStream_t s) {
+                       unsigned int* ticket, CgScalars* sc, cudaStream_t s, std::int64_t dot_off) {
     static int epl = -1, mode = 0;
     if (epl < 0) {
         int dev = 0;
@@ -419,9 +423,9 @@ void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, dou
     if (rows <= 0 || T.ntiles <= 0) return;
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(T.ntiles, g_sms));
     if (epl == 8)
-        launch_epl<8>(mode, T, x, y, partials, ticket, sc, grid, s);
+        launch_epl<8>(mode, T, x, y, partials, ticket, sc, grid, s, dot_off);
     else
-        launch_epl<4>(mode, T, x, y, partials, ticket, sc, grid, s);
+        launch_epl<4>(mode, T, x, y, partials, ticket, sc, grid, s, dot_off);
     B200_CUDA(cudaGetLastError());
 }
 

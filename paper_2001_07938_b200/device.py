@@ -133,3 +133,73 @@ def partition_rows(row_ptr, k: int):
     b = np.zeros(k + 1, np.int64)
     N.lib().b200_partition_rows(len(row_ptr) - 1, N.ptr(row_ptr), k, N.ptr(b))
     return b
+
+
+class DistCG:
+    """Row-sharded NPB CG (include/lilac_b200.h section 7).
+
+    ``DistCG.local(k, row_ptr, col_ind, val)``: k shards on this GPU (device-copy
+    exchange) — the sharded algorithm on one B200.
+    ``DistCG.nccl(rank, world, nccl_id, n, bounds, row_ptr, col_ind, val)``: one
+    shard per process; ``row_ptr`` covers this rank's rows only."""
+
+    def __init__(self, handle, world):
+        self._h = handle
+        self.world = world
+
+    @classmethod
+    def local(cls, k, row_ptr, col_ind, val):
+        h = C.c_void_p()
+        N.check(N.lib().b200_dist_cg_create_local(C.byref(h), k, len(row_ptr) - 1, N.ptr(row_ptr),
+                                                  N.ptr(col_ind), N.ptr(val)))
+        return cls(h, k)
+
+    @classmethod
+    def nccl(cls, rank, world, nccl_id: bytes, n, bounds, row_ptr, col_ind, val):
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        N.check(N.lib().b200_dist_cg_create_nccl(C.byref(h), rank, world, idbuf, n, N.ptr(bounds),
+                                                 N.ptr(row_ptr), N.ptr(col_ind), N.ptr(val)))
+        return cls(h, world)
+
+    @staticmethod
+    def nccl_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        N.check(N.lib().b200_dist_nccl_id(buf))
+        return buf.raw
+
+    def reset(self, stream: int = 0):
+        N.check(N.lib().b200_dist_cg_reset(self._h, C.c_void_p(stream)))
+
+    def outer(self, shift: float, cgitmax: int = 25, stream: int = 0):
+        rc = N.lib().b200_dist_cg_outer(self._h, cgitmax, shift, C.c_void_p(stream))
+        if rc:
+            N.check(rc)
+
+    def result(self):
+        z, r = C.c_double(), C.c_double()
+        N.check(N.lib().b200_dist_cg_result(self._h, C.byref(z), C.byref(r)))
+        return z.value, r.value
+
+    def npb(self, niter: int, shift: float):
+        z, r = C.c_double(), C.c_double()
+        N.check(N.lib().b200_dist_npb(self._h, niter, shift, C.byref(z), C.byref(r)))
+        return z.value, r.value
+
+    def info(self, shard: int = 0):
+        r0, rows, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        tiled = C.c_int32()
+        N.check(N.lib().b200_dist_cg_info(self._h, shard, C.byref(r0), C.byref(rows), C.byref(nnz),
+                                          C.byref(tiled)))
+        return {"row0": r0.value, "rows": rows.value, "nnz": nnz.value, "tiled": bool(tiled.value)}
+
+    def free(self):
+        if self._h:
+            N.lib().b200_dist_cg_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

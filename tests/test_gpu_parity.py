@@ -342,3 +342,43 @@ def test_device_api_spmv_and_dot():
     assert_within(yd.cpu().numpy(), y_ref, spmv_bound(rp, ci, val, x))
     assert abs(out.item() - O.dot(x, y_ref)) <= 1e-10 * float(np.sum(np.abs(x * y_ref)))
     A.free()
+
+
+# --------------------------------------------------------------------------------
+# row-sharded driver (the multi-GPU algorithm, exercised on one GPU)
+# --------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cls,k", [("S", 1), ("S", 2), ("S", 3), ("A", 2), ("A", 4), ("A", 8), ("C", 8)])
+def test_sharded_cg_local_shards(cls, k):
+    """k shards on one GPU exchanging by device copies: the same code path as
+    the NCCL driver minus the transport. zeta must verify and agree with the
+    1-GPU solver to ~1e-12 (only the dot-product association differs)."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    d = D.DistCG.local(k, rp, ci, val)
+    bounds = D.partition_rows(rp, k)
+    for g in range(k):
+        info = d.info(g)
+        assert info["row0"] == bounds[g] and info["rows"] == bounds[g + 1] - bounds[g]
+        assert info["nnz"] == rp[bounds[g + 1]] - rp[bounds[g]]
+    zeta, rnorm = d.npb(niter, shift)
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10, (zeta, zeta_ref)
+    A = D.Matrix.csr(rp, ci, val)
+    cg = D.CG(A)
+    z1, _ = cg.npb(niter, shift)
+    assert abs(zeta - z1) <= 1e-12 * abs(z1)
+    d.free()
+    cg.free()
+    A.free()
+
+
+def test_sharded_cg_nccl_single_rank():
+    """NCCL transport with world = 1 (the only topology one GPU allows)."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES["S"]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    nid = D.DistCG.nccl_id()
+    bounds = np.array([0, na], np.int64)
+    d = D.DistCG.nccl(0, 1, nid, na, bounds, rp, ci, val)
+    zeta, _ = d.npb(niter, shift)
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10
+    d.free()
