@@ -352,6 +352,13 @@ def run_ours(args):
         shard_rows = (r0, r1)
     info = A.info()
 
+    # correctness gate: the full NPB benchmark must verify before we time anything
+    if args.no_verify:
+        zeta, rnorm, verified = None, None, None
+    else:
+        zeta, rnorm = cg.npb(niter, shift)
+        verified = abs(zeta - zeta_ref) / zeta_ref <= 1e-10
+
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     cg.reset(sh)

@@ -106,6 +106,7 @@ typedef struct {
     int64_t n_destruct;
     int64_t bytes_h2d;      /* host->device bytes moved by update hooks */
     int64_t bytes_d2h;      /* device->host bytes moved by write-backs */
+    int64_t bytes_d2d;      /* bytes served from a device mirror instead of the host */
     int32_t strategy;       /* 0 pageprotect, 1 checksum, 2 exact, 3 naive, 4 hybrid */
     int32_t fell_back;      /* PageProtect demoted to Checksum */
     int32_t streaming;      /* adaptive: rewritten every call, no longer guarded */
@@ -121,12 +122,20 @@ typedef struct {
     double t_writeback_ms;  /* output transfer */
     int64_t bytes_h2d;
     int64_t bytes_d2h;
+    int64_t bytes_d2d;      /* inputs served from device mirrors (no host transfer) */
 } b200_harness_stats;
 
 /* Copies up to `cap` region rows; returns the number of regions. */
 int b200_region_stats_get(b200_region_stats* out, int cap);
 int b200_harness_stats_get(b200_harness_stats* out, int cap);
 void b200_stats_reset(void);
+/* Change-detection cost counters since process start: SIGSEGV traps taken,
+ * mprotect calls, bytes hashed; and device bytes currently held as mirrors. */
+int b200_marshal_counters(int64_t* faults, int64_t* mprotects, int64_t* hash_bytes, int64_t* mirror_bytes);
+/* Host-side phase accumulators (ns, counts): mirror fetch, mirror poll, D2D,
+ * H2D, D2H+sync, mirror publish, publish guard, acquire, launch. Returns the
+ * number of phases. */
+int b200_host_profile(int64_t* ns, int64_t* counts, int cap);
 
 /* ==========================================================================
  * 4. Resident device API (the harness internals, for drivers and benchmarks)

@@ -19,14 +19,14 @@ vp = C.c_void_p
 
 class RegionStats(C.Structure):
     _fields_ = [("region", C.c_char * 64), ("n_construct", i64), ("n_update", i64), ("n_destruct", i64),
-                ("bytes_h2d", i64), ("bytes_d2h", i64), ("strategy", C.c_int32), ("fell_back", C.c_int32),
+                ("bytes_h2d", i64), ("bytes_d2h", i64), ("bytes_d2d", i64), ("strategy", C.c_int32), ("fell_back", C.c_int32),
                 ("streaming", C.c_int32), ("constructed", C.c_int32)]
 
 
 class HarnessStats(C.Structure):
     _fields_ = [("harness", C.c_char * 32), ("calls", i64), ("t_total_ms", C.c_double),
                 ("t_poll_ms", C.c_double), ("t_kernel_ms", C.c_double), ("t_writeback_ms", C.c_double),
-                ("bytes_h2d", i64), ("bytes_d2h", i64)]
+                ("bytes_h2d", i64), ("bytes_d2h", i64), ("bytes_d2d", i64)]
 
 
 class MatrixInfo(C.Structure):
@@ -57,6 +57,8 @@ SIGNATURES = {
     "b200_region_stats_get": (C.c_int, [C.POINTER(RegionStats), C.c_int]),
     "b200_harness_stats_get": (C.c_int, [C.POINTER(HarnessStats), C.c_int]),
     "b200_stats_reset": (None, []),
+    "b200_marshal_counters": (C.c_int, [i64p, i64p, i64p, i64p]),
+    "b200_host_profile": (C.c_int, [i64p, i64p, C.c_int]),
     # 4. resident device API
     "b200_matrix_create_csr": (C.c_int, [C.POINTER(vp), i64, i64p, i64p, f64p]),
     "b200_matrix_create_jds": (C.c_int, [C.POINTER(vp), i64, i64p, i64p, f64p, i64p, i64p]),

@@ -16,6 +16,7 @@
 #include "tcsr.hpp"
 
 #include <cstring>
+#include <vector>
 
 using namespace b200;
 
@@ -54,7 +55,7 @@ struct RowPtrDev {
     DevBuf buf;
     std::int64_t max_row = 0;
     bool monotone = true;
-    std::int64_t h2d = 0, d2h = 0;
+    std::int64_t h2d = 0, d2h = 0, d2d = 0;
 };
 
 // B200ColInd (input): col_ind[0..nnz) resident, narrowed to int32 when every
@@ -63,7 +64,7 @@ struct ColDev {
     DevBuf buf;
     bool col32 = true;
     std::int64_t cols = 0;
-    std::int64_t h2d = 0, d2h = 0;
+    std::int64_t h2d = 0, d2h = 0, d2d = 0;
 };
 
 void ColInd_update(const void* in, std::size_t size, ColDev& out) {
@@ -78,7 +79,7 @@ void ColInd_destruct(const void*, std::size_t, ColDev& out) { out.buf.release();
 struct PermDev {
     DevBuf perm, inv;
     bool bijective = true;
-    std::int64_t h2d = 0, d2h = 0;
+    std::int64_t h2d = 0, d2h = 0, d2d = 0;
 };
 
 void Perm_update(const void* in, std::size_t size, PermDev& out) {
@@ -106,7 +107,7 @@ void enroll_stats(MarshalObject<Out>& m, const char* name) {
     m.set_name(name);
     m.set_strategy(rt().strategy);
     m.set_adaptive(true);
-    register_region(&m, &m.out().h2d, &m.out().d2h);
+    register_region(&m, &m.out().h2d, &m.out().d2h, &m.out().d2d);
 }
 
 template <>
@@ -114,7 +115,7 @@ void enroll_stats<std::int64_t>(MarshalObject<std::int64_t>& m, const char* name
     m.set_name(name);
     m.set_strategy(rt().strategy);
     m.set_adaptive(true);
-    register_region(&m, nullptr, nullptr);
+    register_region(&m, nullptr, nullptr, nullptr);
 }
 
 struct Timer {
@@ -132,17 +133,26 @@ struct Timer {
     }
 };
 
-// Times the compute launch with events on the harness stream.
+// Brackets the compute launch with events on the harness stream. No sync
+// here: the write-back's stream sync completes the events, and
+// collect_kernel_time reads them afterwards (one host sync per call).
 template <typename F>
 void timed_launch(HarnessStats& st, F&& launch) {
+    PhaseTimer pt(kPhLaunch);
     Runtime& r = rt();
     B200_CUDA(cudaEventRecord(r.ev_k0, r.stream));
     launch();
     B200_CUDA(cudaEventRecord(r.ev_k1, r.stream));
-    B200_CUDA(cudaEventSynchronize(r.ev_k1));
+    (void)st;
+}
+
+void collect_kernel_time(HarnessStats& st) {
+    Runtime& r = rt();
     float ms = 0.f;
-    B200_CUDA(cudaEventElapsedTime(&ms, r.ev_k0, r.ev_k1));
-    st.t_kernel_ms += ms;
+    if (cudaEventElapsedTime(&ms, r.ev_k0, r.ev_k1) == cudaSuccess)
+        st.t_kernel_ms += ms;
+    else
+        (void)cudaGetLastError();  // not complete (empty write-back): clear the non-sticky status
 }
 
 // ---- persistent state: b200_spmv_csr ------------------------------------------------
@@ -189,6 +199,21 @@ void add_bytes(HarnessStats& hs, std::int64_t h2d0, std::int64_t h2d1, std::int6
     hs.bytes_d2h += d2h1 - d2h0;
 }
 
+// bytes served from device mirrors during one call (all DevArray inputs)
+struct D2dMeter {
+    HarnessStats& hs;
+    std::vector<const std::int64_t*> ctrs;
+    std::int64_t start = 0;
+    D2dMeter(HarnessStats& h, std::initializer_list<const std::int64_t*> c) : hs(h), ctrs(c) {
+        for (auto* p : ctrs) start += *p;
+    }
+    ~D2dMeter() {
+        std::int64_t now = 0;
+        for (auto* p : ctrs) now += *p;
+        hs.bytes_d2d += now - start;
+    }
+};
+
 // ---- persistent state: b200_spmv_jds -------------------------------------------------
 
 struct spmv_jds_state {
@@ -225,13 +250,64 @@ spmv_jds_state& jds_state() {
 
 // ---- persistent state: BLAS-1 companions ------------------------------------------------
 
+// A binding served by K marshal objects chosen by region identity (LRU). The
+// reference keeps one object per binding, so a harness called on alternating
+// arrays (CG: dot(r,r), dot(p,q), dot(x,z)) destructs and reconstructs on
+// every call (marshal.hpp:192-199) — re-guarding pages, re-allocating, and
+// dropping the streaming state each time. Each cached object still follows
+// the reference state machine for its own region.
+template <typename Out, int K>
+struct BindingCache {
+    MarshalObject<Out> objs[K];
+    std::uint64_t used[K] = {};
+    std::uint64_t clock = 0;
+
+    void enroll(const std::string& name) {
+        static std::vector<std::string> keep;  // names outlive the objects' registration
+        for (int i = 0; i < K; ++i) {
+            keep.push_back(name + "[" + std::to_string(i) + "]");
+            enroll_stats(objs[i], keep.back().c_str());
+        }
+    }
+    MarshalObject<Out>& pick(const void* base, std::size_t bytes) {
+        int victim = -1;
+        for (int i = 0; i < K; ++i) {
+            const auto& r = objs[i].region().ref;
+            if (objs[i].constructed() && r.base == base && r.bytes == bytes) {
+                used[i] = ++clock;
+                return objs[i];
+            }
+        }
+        for (int i = 0; i < K; ++i)
+            if (!objs[i].constructed()) {
+                victim = i;
+                break;
+            }
+        if (victim < 0) {
+            victim = 0;
+            for (int i = 1; i < K; ++i)
+                if (used[i] < used[victim]) victim = i;
+        }
+        used[victim] = ++clock;
+        return objs[victim];
+    }
+    std::int64_t sum(std::int64_t Out::*field) {
+        std::int64_t t = 0;
+        for (auto& o : objs) t += o.out().*field;
+        return t;
+    }
+};
+
+constexpr int kBindingCache = 4;
+
 struct dot_state {
-    MarshalObject<DevArray> m_a, m_b, m_result;
+    BindingCache<DevArray, kBindingCache> m_a, m_b;
+    MarshalObject<DevArray> m_result;
     bool first_run_done = false;
 };
 
 struct vec2_state {  // axpy / xpay: y in, x in, y out
-    MarshalObject<DevArray> m_y_in, m_x, m_y_out;
+    BindingCache<DevArray, kBindingCache> m_y_in, m_x, m_y_out;
     bool first_run_done = false;
 };
 
@@ -240,8 +316,8 @@ dot_state& dot_st() {
     if (!st->first_run_done) {
         st->first_run_done = true;
         ensure_init();
-        enroll_stats(st->m_a, "b200_dot.a");
-        enroll_stats(st->m_b, "b200_dot.b");
+        st->m_a.enroll("b200_dot.a");
+        st->m_b.enroll("b200_dot.b");
         enroll_stats(st->m_result, "b200_dot.result");
     }
     return *st;
@@ -256,14 +332,9 @@ vec2_state& vec2_st(const char* which) {
         st->first_run_done = true;
         ensure_init();
         const std::string w = which;
-        static std::string names[2][3];
-        auto& nm = names[is_axpy ? 0 : 1];
-        nm[0] = w + ".y";
-        nm[1] = w + ".x";
-        nm[2] = w + ".y_out";
-        enroll_stats(st->m_y_in, nm[0].c_str());
-        enroll_stats(st->m_x, nm[1].c_str());
-        enroll_stats(st->m_y_out, nm[2].c_str());
+        st->m_y_in.enroll(w + ".y");
+        st->m_x.enroll(w + ".x");
+        st->m_y_out.enroll(w + ".y_out");
     }
     return *st;
 }
@@ -289,6 +360,7 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         if (rows < 0) throw Error(Errc::DataError, "rows < 0");
         const std::int64_t h0 = sum_h2d({state.m_row_ptr.out().h2d, state.m_col_ind.out().h2d, state.m_val.out().h2d,
                                          state.m_x.out().h2d});
+        D2dMeter dm(hs, {&state.m_x.out().d2d, &state.m_val.out().d2d});
         const std::int64_t d0 = state.m_output.out().d2h;
 
         // Marshaling, in binding order (cusparse.lilac:52-61)
@@ -333,6 +405,7 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         tm.acquired();
 
         state.m_output.write_back();
+        collect_kernel_time(hs);
         tm.written_back();
         add_bytes(hs, h0,
                   sum_h2d({state.m_row_ptr.out().h2d, state.m_col_ind.out().h2d, state.m_val.out().h2d,
@@ -355,6 +428,7 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         };
         const std::int64_t h0 = h2d_now();
         const std::int64_t d0 = state.m_output.out().d2h;
+        D2dMeter dm(hs, {&state.m_x.out().d2d, &state.m_val.out().d2d});
 
         const std::int64_t max_nz =
             state.m_max_nz.acquire(nzcnt, rows * sizeof(*nzcnt), nullptr, ReadableMax_update, nullptr) - 1;
@@ -410,6 +484,7 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         tm.acquired();
 
         state.m_output.write_back();
+        collect_kernel_time(hs);
         tm.written_back();
         add_bytes(hs, h0, h2d_now(), d0, state.m_output.out().d2h);
     });
@@ -421,11 +496,15 @@ extern "C" void b200_dot(double* result, std::int64_t length, const double* a, c
         HarnessStats& hs = harness_stats("b200_dot");
         Timer tm(hs);
         if (length < 0) throw Error(Errc::DataError, "length < 0");
-        const std::int64_t h0 = state.m_a.out().h2d + state.m_b.out().h2d, d0 = state.m_result.out().d2h;
-        DevArray& da = state.m_a.acquire(a, length * sizeof(*a), nullptr, B200Read_update, B200Read_destruct);
+        const std::size_t bytes = length * sizeof(double);
+        auto& oa = state.m_a.pick(a, bytes);
+        auto& ob = state.m_b.pick(b, bytes);
+        const std::int64_t h0 = state.m_a.sum(&DevArray::h2d) + state.m_b.sum(&DevArray::h2d),
+                           d0 = state.m_result.out().d2h,
+                           dd0 = state.m_a.sum(&DevArray::d2d) + state.m_b.sum(&DevArray::d2d);
+        DevArray& da = oa.acquire(a, bytes, nullptr, B200Read_update, B200Read_destruct);
         // dot(r, r): one binding serves both operands
-        DevArray& db = (b == a) ? da
-                                : state.m_b.acquire(b, length * sizeof(*b), nullptr, B200Read_update, B200Read_destruct);
+        DevArray& db = (b == a) ? da : ob.acquire(b, bytes, nullptr, B200Read_update, B200Read_destruct);
         DevArray& dres = state.m_result.acquire_out(result, sizeof(*result), B200Write_construct, B200Write_update,
                                                     B200Write_destruct);
         tm.acquired();
@@ -439,8 +518,11 @@ extern "C" void b200_dot(double* result, std::int64_t length, const double* a, c
         });
         tm.acquired();
         state.m_result.write_back();
+        collect_kernel_time(hs);
         tm.written_back();
-        add_bytes(hs, h0, state.m_a.out().h2d + state.m_b.out().h2d, d0, state.m_result.out().d2h);
+        add_bytes(hs, h0, state.m_a.sum(&DevArray::h2d) + state.m_b.sum(&DevArray::h2d), d0,
+                  state.m_result.out().d2h);
+        hs.bytes_d2d += state.m_a.sum(&DevArray::d2d) + state.m_b.sum(&DevArray::d2d) - dd0;
     });
 }
 
@@ -451,25 +533,33 @@ void vec2_call(const char* name, std::int64_t n, double* y, double s, const doub
     HarnessStats& hs = harness_stats(name);
     Timer tm(hs);
     if (n < 0) throw Error(Errc::DataError, "n < 0");
-    const std::int64_t h0 = state.m_y_in.out().h2d + state.m_x.out().h2d, d0 = state.m_y_out.out().d2h;
-    DevArray& dy = state.m_y_in.acquire(y, n * sizeof(*y), nullptr, B200Read_update, B200Read_destruct);
-    DevArray& dx = state.m_x.acquire(x, n * sizeof(*x), nullptr, B200Read_update, B200Read_destruct);
-    DevArray& dout =
-        state.m_y_out.acquire_out(y, n * sizeof(*y), B200Write_construct, B200Write_update, B200Write_destruct);
+    const std::size_t bytes = n * sizeof(double);
+    auto& oy = state.m_y_in.pick(y, bytes);
+    auto& ox = state.m_x.pick(x, bytes);
+    auto& oo = state.m_y_out.pick(y, bytes);
+    const std::int64_t h0 = state.m_y_in.sum(&DevArray::h2d) + state.m_x.sum(&DevArray::h2d),
+                       d0 = state.m_y_out.sum(&DevArray::d2h),
+                       dd0 = state.m_y_in.sum(&DevArray::d2d) + state.m_x.sum(&DevArray::d2d);
+    DevArray& dy = oy.acquire(y, bytes, nullptr, B200Read_update, B200Read_destruct);
+    DevArray& dx = ox.acquire(x, bytes, nullptr, B200Read_update, B200Read_destruct);
+    DevArray& dout = oo.acquire_out(y, bytes, B200Write_construct, B200Write_update, B200Write_destruct);
     tm.acquired();
     timed_launch(hs, [&] {
         Runtime& r = rt();
         if (n > 0)
-            B200_CUDA(cudaMemcpyAsync(dout.buf.ptr, dy.buf.ptr, n * sizeof(double), cudaMemcpyDeviceToDevice, r.stream));
+            B200_CUDA(cudaMemcpyAsync(dout.buf.ptr, dy.buf.ptr, bytes, cudaMemcpyDeviceToDevice, r.stream));
         if (axpy)
             launch_axpy(n, dout.buf.as<double>(), s, dx.buf.as<double>(), r.stream);
         else
             launch_xpay(n, dout.buf.as<double>(), s, dx.buf.as<double>(), r.stream);
     });
     tm.acquired();
-    state.m_y_out.write_back();
+    oo.write_back();
+    collect_kernel_time(hs);
     tm.written_back();
-    add_bytes(hs, h0, state.m_y_in.out().h2d + state.m_x.out().h2d, d0, state.m_y_out.out().d2h);
+    add_bytes(hs, h0, state.m_y_in.sum(&DevArray::h2d) + state.m_x.sum(&DevArray::h2d), d0,
+              state.m_y_out.sum(&DevArray::d2h));
+    hs.bytes_d2d += state.m_y_in.sum(&DevArray::d2d) + state.m_x.sum(&DevArray::d2d) - dd0;
 }
 
 }  // namespace

@@ -50,6 +50,7 @@ std::vector<Guard> g_guards;
 std::vector<TrackedRegion*> g_tracked;  // every region with a live snapshot
 std::mutex g_mu;
 std::size_t g_page = 0;
+volatile long g_stat_faults = 0, g_stat_mprotect = 0, g_stat_hash_bytes = 0;
 struct sigaction g_prev;
 bool g_prev_valid = false;
 
@@ -64,7 +65,21 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
         }
     }
     if (hit) {
-        mprotect(reinterpret_cast<void*>(page), g_page, PROT_READ | PROT_WRITE);
+        g_stat_faults = g_stat_faults + 1;
+        // A region is dirty after its first trapped write: open its whole
+        // guard range now (one fault per region per clean cycle instead of one
+        // per page), then re-close pages still covered by a clean region.
+        for (const Guard& g : g_guards)
+            if (page < g.hi && page + g_page > g.lo)
+                mprotect(reinterpret_cast<void*>(g.lo), g.hi - g.lo, PROT_READ | PROT_WRITE);
+        for (const Guard& g : g_guards) {
+            if (g.region->dirty) continue;
+            for (const Guard& h : g_guards) {
+                if (!h.region->dirty || !(page < h.hi && page + g_page > h.lo)) continue;
+                const std::uintptr_t a = g.lo > h.lo ? g.lo : h.lo, b = g.hi < h.hi ? g.hi : h.hi;
+                if (a < b) mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ);
+            }
+        }
         return;
     }
     // Not ours: hand the fault to whoever had SIGSEGV before us.
@@ -104,6 +119,7 @@ std::uintptr_t floor_page(std::uintptr_t a) { return a & ~(static_cast<std::uint
 std::uintptr_t ceil_page(std::uintptr_t a) { return floor_page(a + page_size() - 1); }
 
 void protect(std::uintptr_t lo, std::uintptr_t hi) {
+    g_stat_mprotect = g_stat_mprotect + 1;
     if (hi > lo && mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ) != 0)
         throw Error(Errc::ProtectionUnsupported, std::string("mprotect failed: ") + std::strerror(errno));
 }
@@ -112,6 +128,7 @@ void protect(std::uintptr_t lo, std::uintptr_t hi) {
 // guarded region other than `except`. Caller holds g_mu.
 void release_pages(std::uintptr_t lo, std::uintptr_t hi, const TrackedRegion* except) {
     if (hi <= lo) return;
+    g_stat_mprotect = g_stat_mprotect + 1;
     mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ | PROT_WRITE);
     for (const Guard& g : g_guards) {
         if (g.region == except || g.region->dirty) continue;
@@ -152,6 +169,7 @@ void edge_spans(const TrackedRegion& r, std::uintptr_t& in_lo, std::uintptr_t& i
 
 std::uint64_t head_hash(const TrackedRegion& r, std::uintptr_t in_lo) {
     const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
+    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(std::min<std::uintptr_t>(in_lo, base + r.ref.bytes) - base);
     return fnv1a(r.ref.base, std::min<std::uintptr_t>(in_lo, base + r.ref.bytes) - base);
 }
 
@@ -278,6 +296,12 @@ void drop_guard(TrackedRegion& r) {
     release_pages(r.guard_lo, r.guard_hi, &r);
     r.guarded = false;
     r.guard_lo = r.guard_hi = 0;
+}
+
+void debug_counters(long* faults, long* mprotects, long* hash_bytes) {
+    *faults = g_stat_faults;
+    *mprotects = g_stat_mprotect;
+    *hash_bytes = g_stat_hash_bytes;
 }
 
 void note_host_write(const void* base, std::size_t bytes) {

@@ -7,11 +7,23 @@
 
 #include <algorithm>
 #include <climits>
+#include <map>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 namespace b200 {
+
+namespace {
+std::int64_t g_phase_ns[kPhCount] = {};
+std::int64_t g_phase_n[kPhCount] = {};
+}  // namespace
+
+void host_phase_add(int ph, std::int64_t ns) {
+    g_phase_ns[ph] += ns;
+    g_phase_n[ph] += 1;
+}
 
 namespace {
 thread_local std::string t_err;
@@ -183,6 +195,7 @@ void ensure_init() {
 void shutdown() {
     Runtime& r = rt();
     lilac::marshal::release_all();
+    mirrors_clear();
     if (!r.inited) return;
     r.partials.release();
     r.scalars.release();
@@ -197,10 +210,11 @@ void shutdown() {
     r.inited = false;
 }
 
-void register_region(MarshalObjectBase* obj, const std::int64_t* h2d, const std::int64_t* d2h) {
+void register_region(MarshalObjectBase* obj, const std::int64_t* h2d, const std::int64_t* d2h,
+                     const std::int64_t* d2d) {
     for (auto& e : g_regions)
         if (e.obj == obj) return;
-    g_regions.push_back({obj, h2d, d2h});
+    g_regions.push_back({obj, h2d, d2h, d2d});
 }
 
 const std::vector<RegionEntry>& all_regions() { return g_regions; }
@@ -221,16 +235,120 @@ std::vector<HarnessStats*> all_harness_stats() { return g_hstats; }
 void upload(DevArray& d, const void* host, std::size_t bytes) {
     d.buf.ensure(bytes);
     if (bytes == 0) return;
+    {
+        PhaseTimer pt(kPhMirrorFetch);
+        if (mirror_fetch(d.buf.ptr, host, bytes, rt().stream)) {
+            d.d2d += static_cast<std::int64_t>(bytes);
+            return;
+        }
+    }
+    PhaseTimer pt(kPhH2D);
     B200_CUDA(cudaMemcpyAsync(d.buf.ptr, host, bytes, cudaMemcpyHostToDevice, rt().stream));
     d.h2d += static_cast<std::int64_t>(bytes);
 }
 
 void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter) {
     if (bytes == 0) return;
-    B200_CUDA(cudaMemcpyAsync(host, d.buf.ptr, bytes, cudaMemcpyDeviceToHost, rt().stream));
-    B200_CUDA(cudaStreamSynchronize(rt().stream));
+    {
+        PhaseTimer pt(kPhD2H);
+        B200_CUDA(cudaMemcpyAsync(host, d.buf.ptr, bytes, cudaMemcpyDeviceToHost, rt().stream));
+        B200_CUDA(cudaStreamSynchronize(rt().stream));
+    }
+    PhaseTimer pt(kPhPublish);
+    // publish only after the bytes landed (pinned D2H is asynchronous: the
+    // mirror's edge hashes must see the written data)
+    mirror_publish(host, bytes, d.buf.ptr, rt().stream);
     counter.d2h += static_cast<std::int64_t>(bytes);
 }
+
+// ---- device mirrors ------------------------------------------------------------------
+
+namespace {
+
+struct Mirror {
+    lilac::marshal::TrackedRegion reg;
+    DevBuf buf;
+};
+
+std::map<std::uintptr_t, std::unique_ptr<Mirror>> g_mirrors;  // keyed by host base
+std::size_t g_mirror_total = 0;
+constexpr std::size_t kMirrorMin = std::size_t(8) << 10;  // smaller arrays: not worth a guard
+constexpr std::size_t kMirrorLimit = std::size_t(4) << 30;  // device bytes kept as mirrors
+
+bool mirrors_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("LILAC_B200_MIRRORS");
+        on = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+    }
+    return on == 1;
+}
+
+void drop_mirror(std::map<std::uintptr_t, std::unique_ptr<Mirror>>::iterator it) {
+    lilac::marshal::drop_guard(it->second->reg);
+    g_mirror_total -= it->second->buf.cap;
+    it->second->buf.release();
+    g_mirrors.erase(it);
+}
+
+}  // namespace
+
+bool mirror_fetch(void* dev_dst, const void* host, std::size_t bytes, cudaStream_t s) {
+    if (g_mirrors.empty()) return false;
+    const auto h = reinterpret_cast<std::uintptr_t>(host);
+    auto it = g_mirrors.upper_bound(h);
+    if (it == g_mirrors.begin()) return false;
+    --it;
+    Mirror& m = *it->second;
+    if (h + bytes > it->first + m.reg.ref.bytes) return false;  // not contained
+    {
+        PhaseTimer pt(kPhMirrorPoll);
+        if (lilac::marshal::poll_dirty(m.reg)) {  // the host wrote it since the write-back
+            drop_mirror(it);
+            return false;
+        }
+    }
+    PhaseTimer pt(kPhD2D);
+    B200_CUDA(cudaMemcpyAsync(dev_dst, m.buf.as<char>() + (h - it->first), bytes, cudaMemcpyDeviceToDevice, s));
+    return true;
+}
+
+void mirror_publish(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s) {
+    if (!mirrors_enabled() || bytes < kMirrorMin) return;
+    const auto h = reinterpret_cast<std::uintptr_t>(host);
+    // drop every mirror overlapping the written range (stale now)
+    for (auto it = g_mirrors.begin(); it != g_mirrors.end();) {
+        const std::uintptr_t lo = it->first, hi = lo + it->second->reg.ref.bytes;
+        if (lo < h + bytes && h < hi) {
+            auto nx = std::next(it);
+            drop_mirror(it);
+            it = nx;
+        } else {
+            ++it;
+        }
+    }
+    if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
+    auto m = std::make_unique<Mirror>();
+    m->buf.ensure(bytes);
+    B200_CUDA(cudaMemcpyAsync(m->buf.ptr, dev_src, bytes, cudaMemcpyDeviceToDevice, s));
+    m->reg.ref = {host, bytes, nullptr};
+    m->reg.strategy = lilac::marshal::Strategy::Hybrid;
+    try {
+        PhaseTimer pt(kPhPublishGuard);
+        lilac::marshal::mark_clean(m->reg);  // guard: a host write invalidates the mirror
+    } catch (const Error&) {
+        m->buf.release();  // pages that cannot be protected get no mirror
+        return;
+    }
+    g_mirror_total += m->buf.cap;
+    g_mirrors.emplace(h, std::move(m));
+}
+
+void mirrors_clear() {
+    while (!g_mirrors.empty()) drop_mirror(g_mirrors.begin());
+}
+
+std::int64_t mirror_bytes() { return static_cast<std::int64_t>(g_mirror_total); }
 
 void upload_row_ptr(DevBuf& buf, const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz,
                     std::int64_t* max_row, bool* monotone) {
@@ -339,6 +457,7 @@ int b200_region_stats_get(b200_region_stats* out, int cap) {
             s.n_destruct = e.obj->counters().n_destruct;
             s.bytes_h2d = e.h2d ? *e.h2d : 0;
             s.bytes_d2h = e.d2h ? *e.d2h : 0;
+            s.bytes_d2d = e.d2d ? *e.d2d : 0;
             s.strategy = static_cast<int32_t>(e.obj->strategy());
             s.fell_back = e.obj->fell_back();
             s.streaming = e.obj->streaming();
@@ -364,10 +483,29 @@ int b200_harness_stats_get(b200_harness_stats* out, int cap) {
             s.t_writeback_ms = h->t_writeback_ms;
             s.bytes_h2d = h->bytes_h2d;
             s.bytes_d2h = h->bytes_d2h;
+            s.bytes_d2d = h->bytes_d2d;
         }
         ++n;
     }
     return n;
+}
+
+int b200_host_profile(int64_t* ns, int64_t* counts, int cap) {
+    for (int i = 0; i < kPhCount && i < cap; ++i) {
+        ns[i] = g_phase_ns[i];
+        counts[i] = g_phase_n[i];
+    }
+    return kPhCount;
+}
+
+int b200_marshal_counters(int64_t* faults, int64_t* mprotects, int64_t* hash_bytes, int64_t* mirror_bytes) {
+    long f = 0, m = 0, h = 0;
+    lilac::marshal::debug_counters(&f, &m, &h);
+    if (faults) *faults = f;
+    if (mprotects) *mprotects = m;
+    if (hash_bytes) *hash_bytes = h;
+    if (mirror_bytes) *mirror_bytes = b200::mirror_bytes();
+    return 0;
 }
 
 void b200_stats_reset(void) {

@@ -22,13 +22,14 @@ struct DevArray {
     DevBuf buf;
     std::int64_t h2d = 0;
     std::int64_t d2h = 0;
+    std::int64_t d2d = 0;  // bytes served from a device mirror instead of the host
 };
 
 struct HarnessStats {
     std::string name;
     std::int64_t calls = 0;
     double t_total_ms = 0, t_poll_ms = 0, t_kernel_ms = 0, t_writeback_ms = 0;
-    std::int64_t bytes_h2d = 0, bytes_d2h = 0;
+    std::int64_t bytes_h2d = 0, bytes_d2h = 0, bytes_d2d = 0;
 };
 
 struct Runtime {
@@ -55,13 +56,15 @@ void ensure_init();  // lazy first-call init + atexit teardown
 void shutdown();
 
 // Region stats registry (harness objects + their transfer counters).
-void register_region(MarshalObjectBase* obj, const std::int64_t* h2d, const std::int64_t* d2h);
+void register_region(MarshalObjectBase* obj, const std::int64_t* h2d, const std::int64_t* d2h,
+                     const std::int64_t* d2d);
 HarnessStats& harness_stats(const char* name);
 std::vector<HarnessStats*> all_harness_stats();
 struct RegionEntry {
     MarshalObjectBase* obj;
     const std::int64_t* h2d;
     const std::int64_t* d2h;
+    const std::int64_t* d2d;
 };
 const std::vector<RegionEntry>& all_regions();
 
@@ -94,8 +97,19 @@ int boundary(const char* fn, F&& f) {
 
 // ---- transfer helpers (stream-ordered, synchronous w.r.t. the host) --------------
 
+// upload: H2D, or D2D from a valid device mirror of the same host bytes.
 void upload(DevArray& d, const void* host, std::size_t bytes);
+// download: D2H write-back; then publishes a device mirror of the host region.
 void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter);
+
+// Device mirrors (the coherence layer of SURVEY §8(f)1): after a write-back the
+// device holds the exact bytes of the host region; the region is guarded like
+// a Hybrid marshal region, and while no host write touched it any later upload
+// of (a sub-range of) it is served device-to-device. LILAC_B200_MIRRORS=0 off.
+bool mirror_fetch(void* dev_dst, const void* host, std::size_t bytes, cudaStream_t s);
+void mirror_publish(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s);
+void mirrors_clear();
+std::int64_t mirror_bytes();
 
 // Resident CSR / JDS uploads shared by the harnesses and the device API.
 struct CsrUpload {
@@ -110,6 +124,17 @@ void upload_row_ptr(DevBuf& buf, const std::int64_t* row_ptr, std::int64_t rows,
 std::int64_t upload_col_ind(DevBuf& buf, const std::int64_t* col_ind, std::int64_t nnz, bool* col32);
 
 using Clock = std::chrono::steady_clock;
+
+// Host-side phase accumulators (ns), read by b200_host_profile().
+enum HostPhase { kPhMirrorFetch, kPhMirrorPoll, kPhD2D, kPhH2D, kPhD2H, kPhPublish, kPhPublishGuard,
+                 kPhAcquire, kPhLaunch, kPhCount };
+void host_phase_add(int ph, std::int64_t ns);
+struct PhaseTimer {
+    int ph;
+    Clock::time_point t0 = Clock::now();
+    explicit PhaseTimer(int p) : ph(p) {}
+    ~PhaseTimer() { host_phase_add(ph, std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count()); }
+};
 inline double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }

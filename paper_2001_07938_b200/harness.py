@@ -114,7 +114,7 @@ def region_stats():
     L.b200_region_stats_get(arr, n)
     names = ["pageprotect", "checksum", "exact", "naive", "hybrid"]
     return {r.region.decode(): {"n_construct": r.n_construct, "n_update": r.n_update, "n_destruct": r.n_destruct,
-                                "bytes_h2d": r.bytes_h2d, "bytes_d2h": r.bytes_d2h,
+                                "bytes_h2d": r.bytes_h2d, "bytes_d2h": r.bytes_d2h, "bytes_d2d": r.bytes_d2d,
                                 "strategy": names[r.strategy], "fell_back": bool(r.fell_back),
                                 "streaming": bool(r.streaming), "constructed": bool(r.constructed)}
             for r in arr[:n]}
@@ -127,5 +127,5 @@ def harness_stats():
     L.b200_harness_stats_get(arr, n)
     return {h.harness.decode(): {"calls": h.calls, "t_total_ms": h.t_total_ms, "t_poll_ms": h.t_poll_ms,
                                  "t_kernel_ms": h.t_kernel_ms, "t_writeback_ms": h.t_writeback_ms,
-                                 "bytes_h2d": h.bytes_h2d, "bytes_d2h": h.bytes_d2h}
+                                 "bytes_h2d": h.bytes_h2d, "bytes_d2h": h.bytes_d2h, "bytes_d2d": h.bytes_d2d}
             for h in arr[:n]}

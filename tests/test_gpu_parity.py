@@ -382,3 +382,26 @@ def test_sharded_cg_nccl_single_rank():
     zeta, _ = d.npb(niter, shift)
     assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10
     d.free()
+
+
+def test_device_mirrors_serve_written_back_vectors_and_never_go_stale():
+    """A harness output written back to the host is mirrored on the device;
+    the next harness that reads those bytes gets them device-to-device, and
+    any host write (interior page or hashed edge) invalidates the mirror."""
+    rng = np.random.default_rng(31)
+    n = 20000
+    rp, ci, val = random_csr(rng, n, n, rng.integers(5, 30, n))
+    x = rng.uniform(-1, 1, n)
+    y = np.zeros(n)
+    H.spmv_csr(n, y, rp, val, x, ci)
+    st0 = H.harness_stats()["b200_dot"] if "b200_dot" in H.harness_stats() else {"bytes_d2d": 0, "bytes_h2d": 0}
+    r1 = H.dotproduct(n, y, y)
+    st1 = H.harness_stats()["b200_dot"]
+    assert st1["bytes_d2d"] - st0["bytes_d2d"] == 8 * n  # served from the device mirror
+    assert st1["bytes_h2d"] - st0["bytes_h2d"] == 0
+    assert abs(r1 - O.dot(y, y)) <= 1e-12 * O.dot(y, y)
+    for idx in (n // 2, 0, n - 1):  # interior page, head edge, tail edge
+        H.spmv_csr(n, y, rp, val, x, ci)  # republish
+        y[idx] += 3.0
+        r = H.dotproduct(n, y, y)
+        assert abs(r - O.dot(y, y)) <= 1e-12 * O.dot(y, y), idx
