@@ -61,6 +61,8 @@ constexpr int kTileThreads = 1024;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kSlabW = 12288;       // columns per slab: 2 x 96 KB double-buffered in smem
 constexpr int kMaxTileRows = 4096;  // tile-local row fits the key and the smem y buffer
+constexpr int kRunAlign = 4;        // (slab, warp) runs start and end on 4-nonzero (32 B) boundaries
+constexpr std::uint32_t kPadKey = 0xffffu << 16;  // padding entry: sentinel row, column 0, value 0
 
 struct TcsrDev {
     std::int64_t ntiles = 0;

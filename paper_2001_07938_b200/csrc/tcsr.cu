@@ -26,7 +26,6 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned kSent = 0xffffu;  // sentinel tile-local row (> kMaxTileRows)
 constexpr std::size_t kTileSmem = sizeof(double) * (2 * kSlabW + kMaxTileRows);
-constexpr int kDefaultEpl = 4;  // nonzeros per lane per chunk (4 or 8)
 
 __device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -131,46 +130,28 @@ __device__ __forceinline__ void sts_add_f64(std::uint32_t addr, double v) {
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(o + v));
 }
 
-__device__ __forceinline__ void ld_stream_u32x8(const std::uint32_t* p, unsigned (&k)[8]) {
-    asm("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3]), "=r"(k[4]), "=r"(k[5]), "=r"(k[6]), "=r"(k[7])
-        : "l"(p));
-}
 
-// A lane's EPL consecutive nonzeros of a (slab, warp) run (tile-relative
-// index j, EPL-aligned in absolute terms so every load is 32-byte aligned).
-template <int EPL>
+// A lane's four consecutive nonzeros of a (slab, warp) run: one 256-bit val
+// load and one 128-bit key load, both 32/16-byte aligned (runs start on
+// kRunAlign boundaries). Lanes past the run end get zeros (and sentinel keys).
 struct Chunk {
-    double v[EPL];
-    unsigned k[EPL];
+    double2 v0, v1;
+    uint4 k;
 };
 
-template <int EPL>
-__device__ __forceinline__ void load_chunk(Chunk<EPL>& c, const double* vb, const std::uint32_t* kb, int j, int hi) {
+__device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std::uint32_t* kb, int j, int hi) {
     if (j < hi) {
-        if constexpr (EPL == 4) {
-            double2 a, b;
-            ld_stream_f64x4(vb + j, a, b);
-            c.v[0] = a.x, c.v[1] = a.y, c.v[2] = b.x, c.v[3] = b.y;
-            const uint4 k = ld_stream_u32x4(kb + j);
-            c.k[0] = k.x, c.k[1] = k.y, c.k[2] = k.z, c.k[3] = k.w;
-        } else {
-            double2 a, b, d, e;
-            ld_stream_f64x4(vb + j, a, b);
-            ld_stream_f64x4(vb + j + 4, d, e);
-            c.v[0] = a.x, c.v[1] = a.y, c.v[2] = b.x, c.v[3] = b.y;
-            c.v[4] = d.x, c.v[5] = d.y, c.v[6] = e.x, c.v[7] = e.y;
-            ld_stream_u32x8(kb + j, c.k);
-        }
+        ld_stream_f64x4(vb + j, c.v0, c.v1);
+        c.k = ld_stream_u32x4(kb + j);
     } else {
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) c.v[e] = 0.0, c.k[e] = 0;
+        c.v0 = c.v1 = make_double2(0.0, 0.0);
+        c.k = make_uint4(kPadKey, kPadKey, kPadKey, kPadKey);
     }
 }
 
-// One warp piece after the lane-local pass: lane holds its head run (k0, p0)
-// and tail run (k1, p1) (k0 == k1: a single run, value p1). Row keys are
-// non-decreasing across lanes. Adds every row's piece-sum into yp[row]
+// One 128-nonzero piece after the lane-local pass: lane holds its head run
+// (k0, p0) and tail run (k1, p1) (k0 == k1: a single run, value p1). Row keys
+// are non-decreasing across lanes. Adds every row's piece-sum into yp[row]
 // (rows are owned by this warp: no atomics, fixed order).
 __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1, double p1, int lane,
                                              std::uint32_t yp_s) {
@@ -191,79 +172,53 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
     if ((lane == 31 || nk0 != k1) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
 }
 
-// Lane-local pass over EPL consecutive nonzeros (keys non-decreasing): rows
-// strictly inside the lane are exclusive to it and flushed here; the head and
-// tail runs go to the warp-level reduce_piece.
-template <int EPL>
-__device__ __forceinline__ void lane_runs(const unsigned (&key)[EPL], const double (&p)[EPL], int lane,
-                                          std::uint32_t yp_s) {
-    double acc = p[0], head = 0.0;
-    unsigned rk = key[0];
-#pragma unroll
-    for (int e = 1; e < EPL; ++e) {
-        if (key[e] == rk) {
-            acc += p[e];
-        } else {
-            if (rk == key[0])
-                head = acc;
-            else if (rk != kSent)
-                sts_add_f64(yp_s + 8u * rk, acc);
-            rk = key[e];
-            acc = p[e];
-        }
-    }
-    reduce_piece(key[0], head, rk, acc, lane, yp_s);
-}
-
-// Processes a (slab, warp) run [lo, hi) (tile-relative) against the slab in
-// shared memory at xb_s. Interior chunks take an unmasked fast path; the first
-// and last chunk of a run mask elements outside [lo, hi). The run's bytes were
-// prefetched into L2 one slab ahead, so loads here are L2 hits.
-template <int EPL, int MODE, bool RPF>
-__device__ __forceinline__ void process_run(const double* vb, const std::uint32_t* kb, int mis, int lo, int hi,
+// Processes a (slab, warp) run [lo, hi) (tile-relative, both multiples of
+// kRunAlign) against the slab in shared memory at xb_s. The run's bytes were
+// prefetched into L2 one slab ahead, so these loads are L2 hits; the next
+// chunk is loaded into registers while this one is reduced.
+template <int MODE>
+__device__ __forceinline__ void process_run(const double* vb, const std::uint32_t* kb, int lo, int hi,
                                             std::uint32_t xb_s, std::uint32_t yp_s, int lane) {
-    constexpr int CH = 32 * EPL;
-    const int c0 = ((lo + mis) & ~(EPL - 1)) - mis;  // absolute EPL alignment; mis = base mod EPL
-    Chunk<EPL> cur, nxt;
-    if (RPF) load_chunk<EPL>(cur, vb, kb, c0 + EPL * lane, hi);
-    for (int c = c0; c < hi; c += CH) {
-        if (RPF)
-            load_chunk<EPL>(nxt, vb, kb, c + CH + EPL * lane, hi);  // one chunk ahead in registers
-        else
-            load_chunk<EPL>(cur, vb, kb, c + EPL * lane, hi);
-        unsigned key[EPL];
-        double p[EPL];
-        if (c >= lo && c + CH <= hi) {  // warp-uniform: every element valid
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                const double xv = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (cur.k[e] & 0xffffu));
-                key[e] = cur.k[e] >> 16;
-                p[e] = cur.v[e] * xv;
-            }
+    Chunk cur, nxt;
+    load_chunk(cur, vb, kb, lo + 4 * lane, hi);
+    for (int c = lo; c < hi; c += 128) {
+        load_chunk(nxt, vb, kb, c + 128 + 4 * lane, hi);
+        const unsigned k0 = cur.k.x >> 16, k1 = cur.k.y >> 16, k2 = cur.k.z >> 16, k3 = cur.k.w >> 16;
+        double p0, p1, p2, p3;
+        if (MODE == 1 || MODE == 3) {  // probe: no gather
+            p0 = cur.v0.x, p1 = cur.v0.y, p2 = cur.v1.x, p3 = cur.v1.y;
         } else {
-            const int j = c + EPL * lane;
-            const int front = lo - j, back = hi - j;  // element e valid iff front <= e < back
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                const double xv = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (cur.k[e] & 0xffffu));
-                key[e] = e < back ? cur.k[e] >> 16 : kSent;
-                p[e] = (e >= front && e < back) ? cur.v[e] * xv : 0.0;
-            }
-            // leading elements before lo (first chunk, lane 0) take the next key
-#pragma unroll
-            for (int e = EPL - 2; e >= 0; --e)
-                if (e < front) key[e] = key[e + 1];
+            p0 = cur.v0.x * lds_f64(xb_s + 8u * (cur.k.x & 0xffffu));
+            p1 = cur.v0.y * lds_f64(xb_s + 8u * (cur.k.y & 0xffffu));
+            p2 = cur.v1.x * lds_f64(xb_s + 8u * (cur.k.z & 0xffffu));
+            p3 = cur.v1.y * lds_f64(xb_s + 8u * (cur.k.w & 0xffffu));
         }
         if (MODE >= 2) {
-            if (p[0] == 12345.678) sts_add_f64(yp_s, p[1]);  // probe: no reduction
+            if (p0 == 12345.678) sts_add_f64(yp_s, p1 + p2 + p3);  // probe: no reduction
         } else {
-            lane_runs<EPL>(key, p, lane, yp_s);
+            // lane-local pass, branch-free for the common case (keys sorted):
+            // tail run = elements equal to k3, head run = elements equal to k0
+            double tail = p3;
+            tail += k2 == k3 ? p2 : 0.0;
+            tail += k1 == k3 ? p1 : 0.0;
+            tail += k0 == k3 ? p0 : 0.0;
+            double head = p0;
+            head += k1 == k0 ? p1 : 0.0;
+            head += k2 == k0 ? p2 : 0.0;
+            // rows strictly inside the lane (a row with <= 2 nonzeros in this
+            // slab) are exclusive to it: flushed here, rarely taken
+            const bool in1 = k1 != k0 && k1 != k3, in2 = k2 != k0 && k2 != k3;
+            if (in1 | in2) {
+                if (in1) sts_add_f64(yp_s + 8u * k1, k2 == k1 ? p1 + p2 : p1);
+                if (in2 && k2 != k1) sts_add_f64(yp_s + 8u * k2, p2);
+            }
+            reduce_piece(k0, head, k3, tail, lane, yp_s);
         }
-        if (RPF) cur = nxt;
+        cur = nxt;
     }
 }
 
-template <bool DOT, int EPL, int MODE = 0>
+template <bool DOT, int MODE = 0>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_spmv_tiled(TcsrDev T, const double* __restrict__ x, double* __restrict__ y, double* partials,
                  unsigned int* ticket, CgScalars* sc, std::int64_t dot_off) {
@@ -313,8 +268,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             }
             if (lane == 0 && k + 1 < T.nslabs)  // next slab's run streams into L2 meanwhile
                 prefetch_run(vb, kb, wo[(k + 1) * kTileWarps + warp], wo[(k + 1) * kTileWarps + warp + 1]);
-            process_run<EPL, MODE == 5 ? 3 : (MODE == 6 ? 0 : (MODE == 7 ? 0 : MODE)), MODE != 7>(
-                vb, kb, static_cast<int>(base & (EPL - 1)), wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1],
+            process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
+                vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1],
                 xs_s + 8u * static_cast<unsigned>(buf * kSlabW), yp_s, lane);
             __syncwarp();
             if (lane == 0) {
@@ -377,55 +332,43 @@ int g_sms = 0;
 
 }  // namespace
 
-template <int EPL, int MODE>
+template <int MODE>
 void launch_variant(const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
                     CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
     static bool configured = false;
     if (!configured) {
-        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, EPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kTileSmem)));
-        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<true, EPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kTileSmem)));
         configured = true;
     }
     if (partials)
-        k_spmv_tiled<true, EPL, MODE><<<std::min<unsigned>(grid, kMaxParts), kTileThreads, kTileSmem, s>>>(
+        k_spmv_tiled<true, MODE><<<std::min<unsigned>(grid, kMaxParts), kTileThreads, kTileSmem, s>>>(
             T, x, y, partials, ticket, sc, dot_off);
     else
-        k_spmv_tiled<false, EPL, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr, 0);
-}
-
-template <int EPL>
-void launch_epl(int mode, const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
-                CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
-    switch (partials ? 0 : mode) {  // probes (wrong results, timing only) never for the fused CG path
-    case 1: launch_variant<EPL, 1>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 2: launch_variant<EPL, 2>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 5: launch_variant<EPL, 5>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 6: launch_variant<EPL, 6>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 7: launch_variant<EPL, 7>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    default: launch_variant<EPL, 0>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    }
+        k_spmv_tiled<false, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr, 0);
 }
 
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
                        unsigned int* ticket, CgScalars* sc, cudaStream_t s, std::int64_t dot_off) {
-    static int epl = -1, mode = 0;
-    if (epl < 0) {
+    static int mode = -1;
+    if (mode < 0) {
         int dev = 0;
         B200_CUDA(cudaGetDevice(&dev));
         B200_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
-        const char* e = std::getenv("LILAC_B200_TILED_EPL");
-        epl = (e && *e) ? std::atoi(e) : kDefaultEpl;
         const char* m = std::getenv("LILAC_B200_TILED_PROBE");  // timing probes only: wrong results
         mode = (m && *m) ? std::atoi(m) : 0;
     }
     if (rows <= 0 || T.ntiles <= 0) return;
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(T.ntiles, g_sms));
-    if (epl == 8)
-        launch_epl<8>(mode, T, x, y, partials, ticket, sc, grid, s, dot_off);
-    else
-        launch_epl<4>(mode, T, x, y, partials, ticket, sc, grid, s, dot_off);
+    switch (partials ? 0 : mode) {  // probes never on the fused CG path
+    case 1: launch_variant<1>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 2: launch_variant<2>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 5: launch_variant<5>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 6: launch_variant<6>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    default: launch_variant<0>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    }
     B200_CUDA(cudaGetLastError());
 }
 

@@ -98,18 +98,16 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     }
     h.tile_row0.push_back(rows);
     h.ntiles = static_cast<std::int64_t>(h.tile_row0.size()) - 1;
-    h.tile_base.resize(h.ntiles + 1);
-    for (std::int64_t t = 0; t <= h.ntiles; ++t) h.tile_base[t] = rp[h.tile_row0[t]] - base0;
     const std::int64_t per_tile = static_cast<std::int64_t>(h.nslabs) * kTileWarps + 1;
     h.woff.assign(static_cast<std::size_t>(h.ntiles * per_tile), 0);
-    h.val.resize(static_cast<std::size_t>(nnz));
-    h.key.resize(static_cast<std::size_t>(nnz));
 
+    // pass 1: warp row ranges (nnz-balanced) and per-(slab, warp) counts
+    std::vector<std::int64_t> wbounds(static_cast<std::size_t>(h.ntiles * (kTileWarps + 1)));
+    std::vector<std::int64_t> counts(static_cast<std::size_t>(h.ntiles * (per_tile - 1)), 0);
+    std::vector<std::int64_t> padded(static_cast<std::size_t>(h.ntiles), 0);
     parallel_tiles(h.ntiles, [&](std::int64_t t) {
         const std::int64_t row0 = h.tile_row0[t], row1 = h.tile_row0[t + 1];
-        const std::int64_t tb = h.tile_base[t];
-        // warp row ranges, nnz-balanced
-        std::int64_t wb[kTileWarps + 1];
+        std::int64_t* wb = wbounds.data() + t * (kTileWarps + 1);
         wb[0] = row0;
         const std::int64_t tn = rp[row1] - rp[row0];
         for (int g = 1; g < kTileWarps; ++g) {
@@ -117,15 +115,35 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
             wb[g] = std::max(std::min(r, row1), wb[g - 1]);
         }
         wb[kTileWarps] = row1;
-        std::int32_t* wo = h.woff.data() + t * per_tile;
-        std::vector<std::int64_t> cnt(static_cast<std::size_t>(per_tile), 0);
+        std::int64_t* cnt = counts.data() + t * (per_tile - 1);
         for (int w = 0; w < kTileWarps; ++w)
             for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
                 for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) cnt[(ci[j] / kSlabW) * kTileWarps + w]++;
+        std::int64_t tot = 0;
+        for (std::int64_t i = 0; i + 1 < per_tile; ++i) tot += (cnt[i] + kRunAlign - 1) / kRunAlign * kRunAlign;
+        padded[t] = tot;
+    });
+    // tile bases: every run starts on a kRunAlign-element boundary and is padded
+    // to a multiple of it (pad entries: val 0, sentinel row), so the kernel
+    // never masks individual elements
+    h.tile_base.resize(h.ntiles + 1);
+    h.tile_base[0] = 0;
+    for (std::int64_t t = 0; t < h.ntiles; ++t) h.tile_base[t + 1] = h.tile_base[t] + padded[t];
+    const std::int64_t total = h.tile_base[h.ntiles];
+    h.val.assign(static_cast<std::size_t>(total), 0.0);
+    h.key.assign(static_cast<std::size_t>(total), kPadKey);
+
+    // pass 2: offsets and scatter (slab-major, warp range, row order kept)
+    parallel_tiles(h.ntiles, [&](std::int64_t t) {
+        const std::int64_t row0 = h.tile_row0[t];
+        const std::int64_t tb = h.tile_base[t];
+        const std::int64_t* wb = wbounds.data() + t * (kTileWarps + 1);
+        const std::int64_t* cnt = counts.data() + t * (per_tile - 1);
+        std::int32_t* wo = h.woff.data() + t * per_tile;
         std::int64_t off = 0;
         for (std::int64_t i = 0; i + 1 < per_tile; ++i) {
             wo[i] = static_cast<std::int32_t>(off);
-            off += cnt[i];
+            off += (cnt[i] + kRunAlign - 1) / kRunAlign * kRunAlign;
         }
         wo[per_tile - 1] = static_cast<std::int32_t>(off);
         std::vector<std::int64_t> cur(wo, wo + per_tile);
