@@ -75,6 +75,16 @@ struct TcsrDev {
     const std::uint32_t* key = nullptr;       // nnz, lcol | lrow << 16
 };
 
+// Merge-path plan (merge.cu): per-CTA start coordinates on the merge of row
+// ends and nonzeros, plus one carry slot per CTA. Cached invariant of row_ptr.
+struct MergeDev {
+    std::int64_t nctas = 0;
+    const std::int64_t* coord_row = nullptr;  // nctas + 1
+    const std::int64_t* coord_nz = nullptr;   // nctas + 1 (relative to row_ptr[0])
+    std::int64_t* carry_row = nullptr;        // nctas
+    double* carry_val = nullptr;              // nctas
+};
+
 struct CsrDev {
     std::int64_t rows = 0;      // number of rows computed
     std::int64_t nnz = 0;       // extent of val/col (row_ptr[rows] for the ABI)
@@ -86,6 +96,7 @@ struct CsrDev {
     const double* val = nullptr;            // nnz
     bool monotone = true;                   // row_ptr non-decreasing
     const TcsrDev* tiled = nullptr;         // present when the tiled layout was built
+    const MergeDev* merge = nullptr;        // present when the merge plan was built
 };
 
 struct JdsDev {
@@ -111,6 +122,16 @@ CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested);
 int csr_vector_width(const CsrDev& A);  // lanes per row for the vector kernel
 
 void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s);
+struct CgScalars;
+// Merge-path kernel (merge.cu) for skewed rows.
+std::int64_t merge_ctas(std::int64_t rows, std::int64_t nnz);
+void launch_merge_plan(const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz, std::int64_t* coord_row,
+                       std::int64_t* coord_nz, cudaStream_t s);
+void launch_spmv_merge(const CsrDev& A, const double* x, double* y, cudaStream_t s);
+// p.q of a finished SpMV into the CG scalars (alpha, or the shard partial).
+void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, double* partials, unsigned int* ticket,
+                           CgScalars* sc, cudaStream_t s);
+
 // Tiled kernel (tcsr.cu); partials/ticket/sc non-null = fused p.q for CG.
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
                        unsigned int* ticket, struct CgScalars* sc, cudaStream_t s, std::int64_t dot_off = 0);

@@ -148,6 +148,24 @@ __global__ void __launch_bounds__(kThreads) k_cg_norms(CgVectors v, double shift
     }
 }
 
+// p.q after a merge-path SpMV (same scalar protocol as the fused kernels).
+__global__ void __launch_bounds__(kThreads) k_cg_dot_scalars(const double* __restrict__ p,
+                                                              const double* __restrict__ q, std::int64_t n,
+                                                              double* partials, unsigned int* ticket, CgScalars* sc) {
+    double a = 0.0;
+    GRID_STRIDE(i, n) a += p[i] * q[i];
+    double part[1] = {a}, tot[1];
+    if (finish<1>(part, partials, ticket, tot) && threadIdx.x == 0) {
+        if (sc->nranks > 1) {
+            sc->part[0] = tot[0];
+        } else {
+            sc->d = tot[0];
+            sc->rho0 = sc->rho;
+            sc->alpha = sc->rho / tot[0];
+        }
+    }
+}
+
 // Sharded finalisation: sum the shards' partials in rank order (deterministic).
 __global__ void k_cg_fin(int what, CgScalars* sc, const double* __restrict__ g, int nranks, double shift) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -195,6 +213,14 @@ unsigned vec_grid(const CgVectors& v) {
 
 void cg_launch_init(const CgVectors& v, cudaStream_t s) {
     k_cg_init<<<vec_grid(v), kThreads, 0, s>>>(v);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, double* partials, unsigned int* ticket,
+                           CgScalars* sc, cudaStream_t s) {
+    std::int64_t g = (n + kThreads * 4 - 1) / (kThreads * 4);
+    g = std::max<std::int64_t>(1, std::min<std::int64_t>(g, std::min(kMaxParts, 148 * 8)));
+    k_cg_dot_scalars<<<static_cast<unsigned>(g), kThreads, 0, s>>>(p, q, n, partials, ticket, sc);
     B200_CUDA(cudaGetLastError());
 }
 

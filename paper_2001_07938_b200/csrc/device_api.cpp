@@ -19,6 +19,7 @@ struct b200_matrix {
     CsrDev csr;
     JdsDev jds;
     TcsrOwner tiled;
+    MergeOwner merge;
     std::int64_t max_row = 0;
 };
 
@@ -63,6 +64,7 @@ int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int6
         d.monotone = monotone;
         A->max_row = max_row;
         if (A->tiled.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel)) d.tiled = &A->tiled.dev;
+        if (!d.tiled && A->merge.refresh(d, row_ptr, rt().kernel)) d.merge = &A->merge.dev;
         *out = A.release();
     });
 }
@@ -137,6 +139,7 @@ void b200_matrix_free(b200_matrix* A) {
     A->inv_perm.release();
     A->jd_ptr.release();
     A->tiled.release();
+    A->merge.release();
     delete A;
 }
 

@@ -34,6 +34,7 @@ struct Shard {
     DevBuf row_ptr, col, val;
     CsrDev A;
     TcsrOwner tiled;
+    MergeOwner merge;
     DevBuf x, q, r, p_full, z_full, partials, scalars, gathered;
     CgVectors v{};
 
@@ -41,6 +42,7 @@ struct Shard {
         for (DevBuf* b : {&row_ptr, &col, &val, &x, &q, &r, &p_full, &z_full, &partials, &scalars, &gathered})
             b->release();
         tiled.release();
+        merge.release();
     }
 };
 
@@ -89,6 +91,8 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
     if (s.tiled.refresh(rows, lrp.data(), ci + base, val + base, n, monotone, max_row, rt().kernel)) {
         s.tiled.dev.cols = n;
         A.tiled = &s.tiled.dev;
+    } else if (s.merge.refresh(A, lrp.data(), rt().kernel)) {
+        A.merge = &s.merge.dev;
     }
     const std::size_t own = sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(rows, 1));
     for (DevBuf* b : {&s.x, &s.q, &s.r}) b->ensure(own);

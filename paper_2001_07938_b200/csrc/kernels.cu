@@ -425,10 +425,14 @@ int csr_vector_width(const CsrDev& A) {
 
 CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested) {
     if (requested == CsrKernel::Exact) return CsrKernel::Exact;
-    if (requested == CsrKernel::Vector || requested == CsrKernel::Merge) return CsrKernel::Vector;
-    // Auto / Tiled: the tiled layout exists only when it was judged to pay
-    // (tcsr_wanted) or was forced at upload
-    return A.tiled ? CsrKernel::Tiled : CsrKernel::Vector;
+    if (requested == CsrKernel::Vector) return CsrKernel::Vector;
+    if (requested == CsrKernel::Merge) return A.merge ? CsrKernel::Merge : CsrKernel::Vector;
+    if (requested == CsrKernel::Tiled) return A.tiled ? CsrKernel::Tiled : CsrKernel::Vector;
+    // Auto: the derived layouts exist only when they were judged to pay at
+    // upload (tcsr_wanted / merge_wanted)
+    if (A.tiled) return CsrKernel::Tiled;
+    if (A.merge) return CsrKernel::Merge;
+    return CsrKernel::Vector;
 }
 
 static unsigned vector_grid(const CsrDev& A, int S) {
@@ -440,6 +444,10 @@ void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, c
     k = choose_csr_kernel(A, k);
     if (k == CsrKernel::Tiled) {
         launch_spmv_tiled(*A.tiled, A.rows, x, y, nullptr, nullptr, nullptr, s);
+        return;
+    }
+    if (k == CsrKernel::Merge) {
+        launch_spmv_merge(A, x, y, s);
         return;
     }
     if (k == CsrKernel::Exact) {
@@ -463,6 +471,11 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
                          CgScalars* sc, cudaStream_t s, std::int64_t dot_off) {
     if (A.tiled) {
         launch_spmv_tiled(*A.tiled, A.rows, p, q, partials, ticket, sc, s, dot_off);
+        return;
+    }
+    if (A.merge) {  // rows finish only after the carry fix-up: dot in its own pass
+        launch_spmv_merge(A, p, q, s);
+        launch_cg_dot_scalars(p + dot_off, q, A.rows, partials, ticket, sc, s);
         return;
     }
     const int S = csr_vector_width(A);

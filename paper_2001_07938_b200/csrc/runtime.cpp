@@ -431,7 +431,6 @@ const char* b200_last_error_code(void) { return t_err_code.c_str(); }
 int b200_set_kernel(const char* name) {
     return boundary("b200_set_kernel", [&] {
         CsrKernel k = parse_csr_kernel(name ? name : "");
-        if (k == CsrKernel::Merge) throw Error(Errc::DataError, "merge kernel not available in this build");
         rt().kernel = k;  // layouts are (re)decided at the next upload
     });
 }

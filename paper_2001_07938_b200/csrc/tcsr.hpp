@@ -38,4 +38,17 @@ struct TcsrOwner {
                  std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy);
 };
 
+// Merge-path plan owner (merge.cu). Built for monotone row_ptr when rows are
+// skewed (max row >= 4096 and > 32x the mean) or when forced.
+bool merge_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, bool monotone, bool forced);
+
+struct MergeOwner {
+    DevBuf coord_row, coord_nz, carry_row, carry_val;
+    MergeDev dev;
+    bool valid = false;
+    // row_ptr_host: the caller's array (rows + 1 entries); A: the resident matrix
+    bool refresh(const CsrDev& A, const std::int64_t* row_ptr_host, CsrKernel policy);
+    void release();
+};
+
 }  // namespace b200

@@ -52,6 +52,12 @@ bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* 
     // one row must not dominate a warp's share (the tiled kernel never splits rows)
     const std::int64_t per_warp = nnz / (static_cast<std::int64_t>(device_sms()) * kTileWarps);
     if (max_row > 16 * std::max<std::int64_t>(per_warp, 64)) return false;
+    // every tile re-reads all of x slab by slab: each (slab, warp) run must be
+    // long enough to amortise a slab (Kronecker scale 22 has ~41 nonzeros per
+    // run over 342 slabs and loses 40x; NPB class C has ~590 over 13)
+    const std::int64_t nslabs = (cols + kSlabW - 1) / kSlabW;
+    const std::int64_t tiles = std::max<std::int64_t>(device_sms(), (rows + kMaxTileRows - 1) / kMaxTileRows);
+    if (nnz / (tiles * nslabs * kTileWarps) < 256) return false;
     // gather locality: distinct 32-byte x sectors per nonzero over windows of
     // 32 consecutive rows (a warp's worth). ~1 = every gather its own sector.
     double ratio_sum = 0;
@@ -211,6 +217,46 @@ bool TcsrOwner::refresh(std::int64_t rows, const std::int64_t* rp, const std::in
     tcsr_build_host(rows, rp, ci, v, cols, h);
     upload(h);
     return true;
+}
+
+bool merge_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, bool monotone, bool forced) {
+    if (!monotone || rows <= 0) return false;
+    if (forced) return true;
+    const double mean = static_cast<double>(nnz) / static_cast<double>(rows);
+    return max_row >= 4096 && static_cast<double>(max_row) > 32.0 * mean;
+}
+
+bool MergeOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel policy) {
+    const std::int64_t nnz = A.rows > 0 ? rp[A.rows] - rp[0] : 0;
+    const bool forced = policy == CsrKernel::Merge;
+    if (policy == CsrKernel::Vector || policy == CsrKernel::Exact || policy == CsrKernel::Tiled ||
+        !merge_wanted(A.rows, nnz, A.max_row, A.monotone, forced)) {
+        release();
+        return false;
+    }
+    const std::int64_t n = merge_ctas(A.rows, nnz);
+    coord_row.ensure(sizeof(std::int64_t) * (n + 1));
+    coord_nz.ensure(sizeof(std::int64_t) * (n + 1));
+    carry_row.ensure(sizeof(std::int64_t) * std::max<std::int64_t>(n, 1));
+    carry_val.ensure(sizeof(double) * std::max<std::int64_t>(n, 1));
+    launch_merge_plan(A.row_ptr, A.rows, nnz, coord_row.as<std::int64_t>(), coord_nz.as<std::int64_t>(), rt().stream);
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
+    dev.nctas = n;
+    dev.coord_row = coord_row.as<std::int64_t>();
+    dev.coord_nz = coord_nz.as<std::int64_t>();
+    dev.carry_row = carry_row.as<std::int64_t>();
+    dev.carry_val = carry_val.as<double>();
+    valid = true;
+    return true;
+}
+
+void MergeOwner::release() {
+    coord_row.release();
+    coord_nz.release();
+    carry_row.release();
+    carry_val.release();
+    dev = MergeDev{};
+    valid = false;
 }
 
 }  // namespace b200

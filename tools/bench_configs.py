@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 from paper_2001_07938_b200 import _native as N  # noqa: E402
 from paper_2001_07938_b200 import device as D  # noqa: E402
 
-KERN = {1: "vector", 3: "exact", 4: "tiled", 0: "jds"}
+KERN = {1: "vector", 2: "merge", 3: "exact", 4: "tiled", 0: "jds"}
 
 
 def peak():
@@ -202,7 +202,11 @@ def main():
         lines.append(report(f"27-point stencil N={a.stencil_n} CSR", A, len(rp) - 1, max(5, a.reps // 5), stream,
                             extra={"gen_s": gen_s}))
         A.free()
-    path = os.path.join(ROOT, "profiles", f"r{a.round:02d}_configs.md")
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "configs.jsonl"), "a") as f:
+        for ln in lines:
+            f.write(json.dumps(ln) + "\n")
+    path = os.path.join(ROOT, "gpurun_out", f"r{a.round:02d}_configs.md")
     with open(path, "w") as f:
         f.write(f"# Round {a.round}: SpMV on every BASELINE config shape (1 B200, tools/bench_configs.py)\n\n")
         f.write(f"Peak for the fraction: measured copy {peak():.1f} GB/s (MEASURED_PEAKS.json). Algorithmic bytes "
