@@ -196,7 +196,22 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
     for (std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; j < rows; j += stride) {
         const std::int64_t len = __ldg(nzcnt + j);
         double acc = 0.0;
-        for (std::int64_t k = 0; k < len; ++k) {
+        std::int64_t k = 0;
+        // 4 diagonals' loads in flight, accumulated in the reference k order
+        for (; k + 4 <= len; k += 4) {
+            std::int64_t off[4];
+            double v[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) off[u] = __ldg(jd_ptr + k + u) + j;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off[u]));
+                xv[u] = __ldg(x + static_cast<std::int64_t>(__ldg(col + off[u])));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+        }
+        for (; k < len; ++k) {
             const std::int64_t off = __ldg(jd_ptr + k) + j;
             double v;
             asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(val + off));
