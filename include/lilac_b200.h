@@ -170,6 +170,22 @@ int b200_dot_device(const double* a_device, const double* b_device, int64_t n,
                     double* result_device, void* stream);
 int b200_axpy_device(int64_t n, double* y_device, double alpha, const double* x_device, void* stream);
 
+/* Device buffers for harness TUs generated from a LiLAC-How spec
+ * (paper_2001_07938_b200/specs/b200.lilac, emitted by the reference's own
+ * harnessgen::gen_all): the marshal classes' code blocks call these. */
+typedef struct {
+    void* ptr;
+    size_t bytes;
+} B200Buf;
+int b200_dbuf_alloc(B200Buf* b, size_t bytes);
+int b200_dbuf_upload(B200Buf* b, const void* host, size_t bytes);  /* (re)allocates, H2D */
+int b200_dbuf_download(void* host, const B200Buf* b, size_t bytes);
+void b200_dbuf_free(B200Buf* b);
+/* y = A x on device arrays at the ABI widths (int64 row_ptr/col_ind, f64),
+ * rows/nnz/cols as the spec's marshaling derives them; synchronises. */
+int b200_spmv_csr_dev(int64_t rows, int64_t nnz, int64_t cols, const void* row_ptr, const void* col_ind,
+                      const void* val, const void* x, void* y);
+
 /* ==========================================================================
  * 5. NPB CG driver (device-resident solver over a resident CSR matrix)
  * ========================================================================== */

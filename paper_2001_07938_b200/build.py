@@ -82,7 +82,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
               "-Xlinker", "-Bsymbolic", "-lpthread", "-ldl", "-lrt"], verbose)
         os.replace(tmp, LIB)
     build_cpp_tests(force, verbose)
+    build_generated_harness(force, verbose)
     return LIB
+
+
+GEN_LIB = os.path.join(PKG, "liblilac_b200_gen.so")
+
+
+def build_generated_harness(force: bool = False, verbose: bool = False):
+    """tests/golden/b200gen_spmv_csr.gen.cpp — emitted by the reference's own
+    harness generator from specs/b200.lilac (tools/gen_b200_harness.py) — is
+    compiled unchanged against include/lilac/marshal.hpp and linked to the
+    B200 library: the drop-in behind the reference's plugin API."""
+    src = os.path.join(ROOT, "tests", "golden", "b200gen_spmv_csr.gen.cpp")
+    if not os.path.exists(src):
+        return
+    deps = [src, LIB, os.path.join(INCLUDE, "lilac", "marshal.hpp"), os.path.join(INCLUDE, "lilac_b200.h")]
+    if force or _stale(GEN_LIB, deps):
+        _run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-Wno-unused-parameter", f"-I{INCLUDE}",
+              "-o", GEN_LIB, src, f"-L{PKG}", "-llilac_b200",
+              "-Wl,-rpath,$ORIGIN", "-lpthread"], verbose)
 
 
 def build_cpp_tests(force: bool = False, verbose: bool = False):

@@ -197,6 +197,59 @@ int b200_axpy_device(std::int64_t n, double* y, double alpha, const double* x, v
     return boundary("b200_axpy_device", [&] { launch_axpy(n, y, alpha, x, static_cast<cudaStream_t>(stream)); });
 }
 
+int b200_dbuf_alloc(B200Buf* b, std::size_t bytes) {
+    return boundary("b200_dbuf_alloc", [&] {
+        ensure_init();
+        b->ptr = nullptr;
+        b->bytes = bytes;
+        B200_CUDA(cudaMalloc(&b->ptr, bytes + kPadBytes));
+    });
+}
+
+int b200_dbuf_upload(B200Buf* b, const void* host, std::size_t bytes) {
+    return boundary("b200_dbuf_upload", [&] {
+        ensure_init();
+        if (!b->ptr || b->bytes < bytes) {
+            if (b->ptr) cudaFree(b->ptr);
+            b->ptr = nullptr;
+            B200_CUDA(cudaMalloc(&b->ptr, bytes + kPadBytes));
+            b->bytes = bytes;
+        }
+        if (bytes) B200_CUDA(cudaMemcpy(b->ptr, host, bytes, cudaMemcpyHostToDevice));
+    });
+}
+
+int b200_dbuf_download(void* host, const B200Buf* b, std::size_t bytes) {
+    return boundary("b200_dbuf_download", [&] {
+        if (bytes) B200_CUDA(cudaMemcpy(host, b->ptr, bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+void b200_dbuf_free(B200Buf* b) {
+    if (b && b->ptr) cudaFree(b->ptr);
+    if (b) {
+        b->ptr = nullptr;
+        b->bytes = 0;
+    }
+}
+
+int b200_spmv_csr_dev(std::int64_t rows, std::int64_t nnz, std::int64_t cols, const void* row_ptr,
+                      const void* col_ind, const void* val, const void* x, void* y) {
+    return boundary("b200_spmv_csr_dev", [&] {
+        ensure_init();
+        CsrDev A;
+        A.rows = rows;
+        A.nnz = nnz;
+        A.cols = cols;
+        A.row_ptr = static_cast<const std::int64_t*>(row_ptr);
+        A.col = col_ind;
+        A.col32 = false;  // ABI width, as the spec marshals it
+        A.val = static_cast<const double*>(val);
+        launch_spmv_csr(A, static_cast<const double*>(x), static_cast<double*>(y), CsrKernel::Vector, rt().stream);
+        B200_CUDA(cudaStreamSynchronize(rt().stream));
+    });
+}
+
 }  // extern "C"
 
 // exposed for cg.cpp
