@@ -31,20 +31,35 @@ __device__ __forceinline__ double2 ld_stream(const double* p) {
     return r;
 }
 
+// matrix streams: read once, L2 evict_first (keeps x and the rest resident)
+__device__ __forceinline__ double2 ld_stream_ef(const double* p, std::uint64_t pol) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+        : "=d"(r.x), "=d"(r.y)
+        : "l"(p), "l"(pol));
+    return r;
+}
+
 struct Idx2 {
     long long a, b;
 };
 
-__device__ __forceinline__ Idx2 ld_stream_idx(const std::int32_t* p) {
+__device__ __forceinline__ Idx2 ld_stream_idx(const std::int32_t* p, std::uint64_t pol) {
     int a, b;
-    asm("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(a), "=r"(b) : "l"(p), "l"(pol));
     return {a, b};
 }
 
-__device__ __forceinline__ Idx2 ld_stream_idx(const std::int64_t* p) {
+__device__ __forceinline__ Idx2 ld_stream_idx(const std::int64_t* p, std::uint64_t pol) {
     long long a, b;
-    asm("ld.global.nc.L1::no_allocate.v2.s64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s64 {%0, %1}, [%2], %3;" : "=l"(a), "=l"(b) : "l"(p), "l"(pol));
     return {a, b};
+}
+
+__device__ __forceinline__ std::uint64_t make_evict_first() {
+    std::uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 __device__ __forceinline__ double warp_sum(double v, unsigned mask = 0xffffffffu) {
@@ -109,6 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
     const unsigned gmask =
         S == 32 ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31) & ~(S - 1)));
     const std::int64_t groups = static_cast<std::int64_t>(gridDim.x) * (kThreads / S);
+    const std::uint64_t pol = make_evict_first();
     double pq = 0.0;
     for (std::int64_t row = (static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x) / S;
          row < rows; row += groups) {
@@ -121,8 +137,8 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
             for (int u = 0; u < U; ++u) {
                 const std::int64_t j = jb + 2 * S * u;
                 if (j < end) {
-                    v[u] = ld_stream(val + j);
-                    c[u] = ld_stream_idx(col + j);
+                    v[u] = ld_stream_ef(val + j, pol);
+                    c[u] = ld_stream_idx(col + j, pol);
                 } else {
                     v[u] = make_double2(0.0, 0.0);
                     c[u] = {0, 0};

@@ -52,26 +52,32 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* b, unsigned parity) {
         : "memory");
 }
 
+// x slabs are re-read by every tile: keep them in L2 (evict_last)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(b))
-                 : "memory");
+    std::uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(b)), "l"(pol)
+        : "memory");
 }
 
 // 256-bit load (sm_100): one instruction moves a lane's 32 contiguous bytes,
-// so a warp instruction covers 1 KB with every sector fully used.
-__device__ __forceinline__ void ld_stream_f64x4(const double* p, double2& a, double2& b) {
-    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+// so a warp instruction covers 1 KB with every sector fully used. The matrix
+// is read once: L2 evict_first once consumed, so it does not push out x or the
+// runs prefetched for the next slab.
+__device__ __forceinline__ void ld_stream_f64x4(const double* p, double2& a, double2& b, std::uint64_t pol) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
         : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
-        : "l"(p));
+        : "l"(p), "l"(pol));
 }
 
-__device__ __forceinline__ uint4 ld_stream_u32x4(const std::uint32_t* p) {
+__device__ __forceinline__ uint4 ld_stream_u32x4(const std::uint32_t* p, std::uint64_t pol) {
     uint4 r;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-        : "l"(p));
+        : "l"(p), "l"(pol));
     return r;
 }
 
@@ -139,10 +145,11 @@ struct Chunk {
     uint4 k;
 };
 
-__device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std::uint32_t* kb, int j, int hi) {
+__device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std::uint32_t* kb, int j, int hi,
+                                           std::uint64_t pol) {
     if (j < hi) {
-        ld_stream_f64x4(vb + j, c.v0, c.v1);
-        c.k = ld_stream_u32x4(kb + j);
+        ld_stream_f64x4(vb + j, c.v0, c.v1, pol);
+        c.k = ld_stream_u32x4(kb + j, pol);
     } else {
         c.v0 = c.v1 = make_double2(0.0, 0.0);
         c.k = make_uint4(kPadKey, kPadKey, kPadKey, kPadKey);
@@ -179,10 +186,12 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
 template <int MODE>
 __device__ __forceinline__ void process_run(const double* vb, const std::uint32_t* kb, int lo, int hi,
                                             std::uint32_t xb_s, std::uint32_t yp_s, int lane) {
+    std::uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     Chunk cur, nxt;
-    load_chunk(cur, vb, kb, lo + 4 * lane, hi);
+    load_chunk(cur, vb, kb, lo + 4 * lane, hi, pol);
     for (int c = lo; c < hi; c += 128) {
-        load_chunk(nxt, vb, kb, c + 128 + 4 * lane, hi);
+        load_chunk(nxt, vb, kb, c + 128 + 4 * lane, hi, pol);
         const unsigned k0 = cur.k.x >> 16, k1 = cur.k.y >> 16, k2 = cur.k.z >> 16, k3 = cur.k.w >> 16;
         double p0, p1, p2, p3;
         if (MODE == 1 || MODE == 3) {  // probe: no gather
