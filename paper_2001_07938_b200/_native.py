@@ -29,6 +29,10 @@ class HarnessStats(C.Structure):
                 ("bytes_h2d", i64), ("bytes_d2h", i64), ("bytes_d2d", i64)]
 
 
+class B200Buf(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("bytes", C.c_size_t)]
+
+
 class MatrixInfo(C.Structure):
     _fields_ = [("rows", i64), ("cols", i64), ("nnz", i64), ("max_row", i64), ("format", C.c_int32),
                 ("col_bytes", C.c_int32), ("kernel", C.c_int32), ("lanes", C.c_int32),
@@ -67,6 +71,11 @@ SIGNATURES = {
     "b200_spmv_device": (C.c_int, [vp, vp, vp, vp]),
     "b200_dot_device": (C.c_int, [vp, vp, i64, vp, vp]),
     "b200_axpy_device": (C.c_int, [i64, vp, C.c_double, vp, vp]),
+    "b200_dbuf_alloc": (C.c_int, [C.POINTER(B200Buf), C.c_size_t]),
+    "b200_dbuf_upload": (C.c_int, [C.POINTER(B200Buf), vp, C.c_size_t]),
+    "b200_dbuf_download": (C.c_int, [vp, C.POINTER(B200Buf), C.c_size_t]),
+    "b200_dbuf_free": (None, [C.POINTER(B200Buf)]),
+    "b200_spmv_csr_dev": (C.c_int, [i64, i64, i64, vp, vp, vp, vp, vp]),
     # 5. NPB CG driver
     "b200_cg_create": (C.c_int, [C.POINTER(vp), vp]),
     "b200_cg_free": (None, [vp]),
