@@ -260,14 +260,23 @@ def run_reference(args):
 # our arm
 # ------------------------------------------------------------------------------------
 
-def e2e_harness_cg(rp, ci, val, n, shift, steps):
+def e2e_harness_cg(rp, ci, val, n, shift, steps, writeback="eager"):
     """NPB outer iterations through the C-ABI harness entry points on pinned
-    host vectors (the LiLAC model: host CG loop, offloaded SpMV/dot/axpy)."""
+    host vectors (the LiLAC model: host CG loop, offloaded SpMV/dot/axpy).
+    writeback="lazy": outputs stay on the device until the host touches them
+    (b200_set_writeback; the host-side loop is unchanged)."""
     import torch
     from paper_2001_07938_b200 import harness as H
 
+    H.set_writeback(writeback)
+    keep = []
+
     def pinned(k):
-        return torch.zeros(k, dtype=torch.float64, pin_memory=True).numpy()
+        t = torch.zeros(k + 512, dtype=torch.float64, pin_memory=True)
+        keep.append(t)
+        a = t.numpy()
+        off = (-a.ctypes.data % 4096) // 8  # page-aligned start (lazy write-back needs it)
+        return a[off:off + k]
 
     x, z, r, p, q, res = (pinned(n) for _ in range(6))
     x[:] = 1.0
@@ -298,19 +307,28 @@ def e2e_harness_cg(rp, ci, val, n, shift, steps):
     outer()  # first call: uploads the matrix (marshal construct), untimed
     x[:] = 1.0
     st0 = H.harness_stats()
+    lz0 = H.lazy_counters()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
         zeta, _ = outer()
     t = time.perf_counter() - t0
     st1 = H.harness_stats()
+    lz1 = H.lazy_counters()
+    H.host_sync()
+    H.set_writeback("eager")
+    # lazy bytes materialised on host touches are device->host traffic too
+    filled = lz1["bytes_filled"] - lz0["bytes_filled"]
     h2d = sum(v["bytes_h2d"] for v in st1.values()) - sum(v["bytes_h2d"] for v in st0.values())
     d2h = sum(v["bytes_d2h"] for v in st1.values()) - sum(v["bytes_d2h"] for v in st0.values())
     calls = sum(v["calls"] for v in st1.values()) - sum(v["calls"] for v in st0.values())
     kern = sum(v["t_kernel_ms"] for v in st1.values()) - sum(v["t_kernel_ms"] for v in st0.values())
     return {"value": steps / t, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
-            "d2h_bytes_per_step": d2h // steps, "harness_calls_per_step": calls // steps,
-            "kernel_ms_per_step": kern / steps, "ms_per_step": 1e3 * t / steps,
+            "d2h_bytes_per_step": (d2h + filled) // steps, "harness_calls_per_step": calls // steps,
+            "kernel_ms_per_step": kern / steps, "ms_per_step": 1e3 * t / steps, "writeback": writeback,
+            "lazy_fills_per_step": (lz1["fault_fills"] + lz1["explicit_fills"] - lz0["fault_fills"]
+                                    - lz0["explicit_fills"]) / steps,
+            "zeta": zeta,
             "path": "b200_spmv_csr/b200_dot/b200_axpy/b200_xpay on pinned host arrays"}
 
 
@@ -439,7 +457,11 @@ def run_ours(args):
         "gen_s": t_gen,
     }
     if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = e2e_harness_cg(rp, ci, val, na, shift, args.e2e_steps)
+        eager = e2e_harness_cg(rp, ci, val, na, shift, args.e2e_steps, "eager")
+        lazy = e2e_harness_cg(rp, ci, val, na, shift, args.e2e_steps, "lazy")
+        # headline: the better of the two public write-back modes; both reported
+        line["e2e"], other = (lazy, eager) if lazy["value"] >= eager["value"] else (eager, lazy)
+        line["e2e_" + other["writeback"]] = other
         if not args.no_cpu_baseline:
             t_iter, kind, desc, ts = reference_sample(rp, ci, val, na, reps=2)
             model, ncpu = cpu_desc()

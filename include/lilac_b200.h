@@ -94,6 +94,23 @@ int b200_set_kernel(const char* name);
 int b200_set_strategy(const char* name);
 /* 1 = dot/axpy also use the reference's sequential order (bit-exact). */
 void b200_set_exact_blas(int on);
+/* Output write-back mode. "eager" (default; the reference's
+ * behaviour, gen.cpp:112-118): every OUTPUT binding is copied device->host
+ * before the call returns. "lazy": a page-aligned output of >= 8 KiB stays on
+ * the device; its host pages are mapped PROT_NONE and filled on first CPU
+ * touch (page fault) or by b200_host_sync, and a later harness input over the
+ * same bytes is served device-to-device. The call returns without a host
+ * sync. Caveat: DMA and system calls do not fault — call b200_host_sync
+ * before handing such a buffer to another library or to read()/write().
+ * Also LILAC_B200_WRITEBACK=lazy. */
+int b200_set_writeback(const char* mode);
+/* Materialise lazy write-back bytes in [host, host+bytes) (NULL: all). */
+int b200_host_sync(const void* host, size_t bytes);
+/* Lazy write-back counters: ranges deferred, filled on a page fault, filled
+ * explicitly (DMA reads, b200_host_sync, partial overwrites), cancelled by a
+ * covering write-back, bytes deferred, bytes materialised. */
+int b200_lazy_counters(int64_t* ranges, int64_t* fault_fills, int64_t* explicit_fills, int64_t* cancelled,
+                       int64_t* bytes_deferred, int64_t* bytes_filled);
 /* Library and build identification, e.g. "lilac-b200 0.1 sm_100a". */
 const char* b200_version(void);
 

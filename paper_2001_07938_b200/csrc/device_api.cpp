@@ -49,6 +49,7 @@ int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int6
         upload_row_ptr(A->row_ptr, row_ptr, rows, nnz, &max_row, &monotone);
         const std::int64_t cols = upload_col_ind(A->col, col_ind, nnz, &col32);
         A->val.ensure(nnz * sizeof(double));
+        host_in(val, nnz * sizeof(double));
         if (nnz > 0)
             B200_CUDA(cudaMemcpyAsync(A->val.ptr, val, nnz * sizeof(double), cudaMemcpyHostToDevice, rt().stream));
         B200_CUDA(cudaStreamSynchronize(rt().stream));
@@ -90,6 +91,9 @@ int b200_matrix_create_jds(b200_matrix** out, std::int64_t rows, const std::int6
         A->inv_perm.ensure(rows * 8);
         A->jd_ptr.ensure(njd * 8);
         if (rows > 0) {
+            host_in(nzcnt, rows * 8);
+            host_in(perm, rows * 8);
+            host_in(jd_ptr, njd * 8);
             B200_CUDA(cudaMemcpyAsync(A->nzcnt.ptr, nzcnt, rows * 8, cudaMemcpyHostToDevice, r.stream));
             B200_CUDA(cudaMemcpyAsync(A->perm.ptr, perm, rows * 8, cudaMemcpyHostToDevice, r.stream));
             B200_CUDA(cudaMemcpyAsync(A->jd_ptr.ptr, jd_ptr, njd * 8, cudaMemcpyHostToDevice, r.stream));
@@ -110,6 +114,7 @@ int b200_matrix_create_jds(b200_matrix** out, std::int64_t rows, const std::int6
         bool col32 = true;
         const std::int64_t cols = upload_col_ind(A->col, col_ind, nnz, &col32);
         A->val.ensure(nnz * 8);
+        host_in(val, nnz * 8);
         if (nnz > 0) B200_CUDA(cudaMemcpyAsync(A->val.ptr, val, nnz * 8, cudaMemcpyHostToDevice, r.stream));
         B200_CUDA(cudaStreamSynchronize(r.stream));
         JdsDev& d = A->jds;
@@ -215,12 +220,14 @@ int b200_dbuf_upload(B200Buf* b, const void* host, std::size_t bytes) {
             B200_CUDA(cudaMalloc(&b->ptr, bytes + kPadBytes));
             b->bytes = bytes;
         }
+        host_in(host, bytes);
         if (bytes) B200_CUDA(cudaMemcpy(b->ptr, host, bytes, cudaMemcpyHostToDevice));
     });
 }
 
 int b200_dbuf_download(void* host, const B200Buf* b, std::size_t bytes) {
     return boundary("b200_dbuf_download", [&] {
+        lilac::marshal::note_host_write(host, bytes);  // guards + lazy bytes under the destination
         if (bytes) B200_CUDA(cudaMemcpy(host, b->ptr, bytes, cudaMemcpyDeviceToHost));
     });
 }

@@ -76,6 +76,7 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
     const std::int64_t cols = upload_col_ind(s.col, ci + base, s.nnz, &col32);
     if (cols > n) throw Error(Errc::OutOfBounds, "column index >= n in a shard");
     s.val.ensure(s.nnz * 8);
+    host_in(val + base, s.nnz * 8);
     if (s.nnz) B200_CUDA(cudaMemcpyAsync(s.val.ptr, val + base, s.nnz * 8, cudaMemcpyHostToDevice, rt().stream));
     B200_CUDA(cudaStreamSynchronize(rt().stream));
     CsrDev& A = s.A;

@@ -87,6 +87,7 @@ void Perm_update(const void* in, std::size_t size, PermDev& out) {
     const std::int64_t rows = static_cast<std::int64_t>(size / sizeof(std::int64_t));
     out.perm.ensure(size);
     out.inv.ensure(size);
+    host_in(in, size);
     if (size) B200_CUDA(cudaMemcpyAsync(out.perm.ptr, in, size, cudaMemcpyHostToDevice, r.stream));
     B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
     launch_invert_perm(out.perm.as<std::int64_t>(), rows, out.inv.as<std::int64_t>(), r.d_bad(), r.stream);

@@ -48,15 +48,72 @@ struct Guard {
 // (single-threaded acquire contract).
 std::vector<Guard> g_guards;
 std::vector<TrackedRegion*> g_tracked;  // every region with a live snapshot
+std::vector<DeferredRange*> g_deferred;  // lazy ranges (active or awaiting unlink)
 std::mutex g_mu;
 std::size_t g_page = 0;
 volatile long g_stat_faults = 0, g_stat_mprotect = 0, g_stat_hash_bytes = 0;
+volatile long g_def_n = 0, g_def_fault_fills = 0, g_def_explicit_fills = 0, g_def_cancelled = 0;
 struct sigaction g_prev;
 bool g_prev_valid = false;
+
+// Close the parts of [lo, hi) covered by an active lazy range (PROT_NONE).
+void apply_deferred(std::uintptr_t lo, std::uintptr_t hi) {
+    for (std::size_t i = 0; i < g_deferred.size(); ++i) {
+        const DeferredRange* d = g_deferred[i];
+        if (!d->active) continue;
+        const std::uintptr_t a = lo > d->lo ? lo : d->lo, b = hi < d->hi ? hi : d->hi;
+        if (a < b) mprotect(reinterpret_cast<void*>(a), b - a, PROT_NONE);
+    }
+}
+
+// Recompute the protection of [lo, hi): PROT_NONE under an active lazy range,
+// else PROT_READ under a clean guard, else read-write. Lock-free (the fault
+// handler calls it); callers in normal context hold g_mu.
+void reapply(std::uintptr_t lo, std::uintptr_t hi) {
+    if (hi <= lo) return;
+    g_stat_mprotect = g_stat_mprotect + 1;
+    mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ | PROT_WRITE);
+    for (const Guard& g : g_guards) {
+        if (g.region->dirty) continue;
+        const std::uintptr_t a = lo > g.lo ? lo : g.lo, b = hi < g.hi ? hi : g.hi;
+        if (a < b) mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ);
+    }
+    apply_deferred(lo, hi);
+}
+
+// Materialise one lazy range: open its pages, let the owner write the bytes,
+// then restore the guards' protections over them.
+void fill_one(DeferredRange& d, bool from_fault) {
+    mprotect(reinterpret_cast<void*>(d.lo), d.hi - d.lo, PROT_READ | PROT_WRITE);
+    d.active = false;
+    if (d.fill) d.fill(&d);
+    if (from_fault)
+        g_def_fault_fills = g_def_fault_fills + 1;
+    else
+        g_def_explicit_fills = g_def_explicit_fills + 1;
+    reapply(d.lo, d.hi);
+}
+
+bool page_deferred(std::uintptr_t page) {
+    for (const DeferredRange* d : g_deferred)
+        if (d->active && d->lo <= page && page < d->hi) return true;
+    return false;
+}
 
 void on_fault(int sig, siginfo_t* si, void* uctx) {
     const auto addr = reinterpret_cast<std::uintptr_t>(si->si_addr);
     const std::uintptr_t page = addr & ~(static_cast<std::uintptr_t>(g_page) - 1);
+    // a touch of lazy bytes: materialise them; a write re-faults on the
+    // restored guard and is recorded below
+    bool filled = false;
+    for (std::size_t i = 0; i < g_deferred.size(); ++i) {
+        DeferredRange* d = g_deferred[i];
+        if (d->active && page < d->hi && page + g_page > d->lo) {
+            fill_one(*d, true);
+            filled = true;
+        }
+    }
+    if (filled) return;
     bool hit = false;
     for (const Guard& g : g_guards) {
         if (page < g.hi && page + g_page > g.lo) {
@@ -80,6 +137,8 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
                 if (a < b) mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ);
             }
         }
+        for (const Guard& g : g_guards)
+            if (page < g.hi && page + g_page > g.lo) apply_deferred(g.lo, g.hi);
         return;
     }
     // Not ours: hand the fault to whoever had SIGSEGV before us.
@@ -135,11 +194,13 @@ void release_pages(std::uintptr_t lo, std::uintptr_t hi, const TrackedRegion* ex
         std::uintptr_t a = std::max(lo, g.lo), b = std::min(hi, g.hi);
         if (a < b) mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ);
     }
+    apply_deferred(lo, hi);
 }
 
 void add_guard(TrackedRegion& r, std::uintptr_t lo, std::uintptr_t hi) {
     ensure_handler();
     protect(lo, hi);
+    apply_deferred(lo, hi);
     if (!r.guarded) {
         g_guards.push_back({lo, hi, &r});
         r.guarded = true;
@@ -167,15 +228,18 @@ void edge_spans(const TrackedRegion& r, std::uintptr_t& in_lo, std::uintptr_t& i
     if (in_hi <= in_lo) in_lo = in_hi = end;  // no whole page inside: hash everything
 }
 
-std::uint64_t head_hash(const TrackedRegion& r, std::uintptr_t in_lo) {
+std::uint64_t head_hash(const TrackedRegion& r) {
     const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
-    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(std::min<std::uintptr_t>(in_lo, base + r.ref.bytes) - base);
-    return fnv1a(r.ref.base, std::min<std::uintptr_t>(in_lo, base + r.ref.bytes) - base);
+    const std::uintptr_t n = r.hash_head_end > base ? r.hash_head_end - base : 0;
+    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(n);
+    return fnv1a(r.ref.base, n);
 }
 
-std::uint64_t tail_hash(const TrackedRegion& r, std::uintptr_t in_hi) {
+std::uint64_t tail_hash(const TrackedRegion& r) {
     const auto end = reinterpret_cast<std::uintptr_t>(r.ref.base) + r.ref.bytes;
-    return in_hi < end ? fnv1a(reinterpret_cast<const void*>(in_hi), end - in_hi) : 0;
+    if (r.hash_tail_begin >= end) return 0;
+    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(end - r.hash_tail_begin);
+    return fnv1a(reinterpret_cast<const void*>(r.hash_tail_begin), end - r.hash_tail_begin);
 }
 
 }  // namespace
@@ -252,12 +316,40 @@ void mark_clean(TrackedRegion& r) {
         }
         std::uintptr_t in_lo, in_hi;
         edge_spans(r, in_lo, in_hi);
+        const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
+        const std::uintptr_t end = base + r.ref.bytes;
         std::lock_guard<std::mutex> lk(g_mu);
         track(r);
         r.dirty = false;
-        if (in_hi > in_lo) add_guard(r, in_lo, in_hi);
-        r.last_checksum = head_hash(r, in_lo);
-        r.last_tail_checksum = tail_hash(r, in_hi);
+        // edge pages that are lazy are guarded whole: hashing them would
+        // materialise them (a foreign write on them only costs a refresh)
+        std::uintptr_t g_lo = in_lo, g_hi = in_hi;
+        r.hash_head_end = in_lo;
+        r.hash_tail_begin = in_hi;
+        if (!g_deferred.empty()) {
+            if (in_hi <= in_lo) {  // no whole page inside: all or nothing
+                bool all = true;
+                for (std::uintptr_t pg = floor_page(base); pg < end && all; pg += page_size()) all = page_deferred(pg);
+                if (all) {
+                    g_lo = floor_page(base);
+                    g_hi = ceil_page(end);
+                    r.hash_head_end = base;
+                    r.hash_tail_begin = end;
+                }
+            } else {
+                if (base < in_lo && page_deferred(floor_page(base))) {
+                    g_lo = floor_page(base);
+                    r.hash_head_end = base;
+                }
+                if (in_hi < end && page_deferred(in_hi)) {
+                    g_hi = ceil_page(end);
+                    r.hash_tail_begin = end;
+                }
+            }
+        }
+        if (g_hi > g_lo) add_guard(r, g_lo, g_hi);
+        r.last_checksum = head_hash(r);
+        r.last_tail_checksum = tail_hash(r);
         return;
     }
     }
@@ -276,11 +368,8 @@ bool poll_dirty(TrackedRegion& r) {
     case Strategy::PageProtect:
         return r.dirty;
     case Strategy::Hybrid:
-        if (!r.dirty && r.ref.bytes > 0) {
-            std::uintptr_t in_lo, in_hi;
-            edge_spans(r, in_lo, in_hi);
-            r.dirty = head_hash(r, in_lo) != r.last_checksum || tail_hash(r, in_hi) != r.last_tail_checksum;
-        }
+        if (!r.dirty && r.ref.bytes > 0)
+            r.dirty = head_hash(r) != r.last_checksum || tail_hash(r) != r.last_tail_checksum;
         return r.dirty;
     }
     return true;
@@ -309,6 +398,18 @@ void note_host_write(const void* base, std::size_t bytes) {
     const auto lo = reinterpret_cast<std::uintptr_t>(base);
     const std::uintptr_t hi = lo + bytes;
     std::lock_guard<std::mutex> lk(g_mu);
+    // lazy bytes under the write: superseded if the write covers them all,
+    // else materialised first (the write lands on top of them)
+    for (DeferredRange* d : g_deferred) {
+        if (!d->active || !(d->content_lo < hi && lo < d->content_hi)) continue;
+        if (lo <= d->content_lo && d->content_hi <= hi) {
+            d->active = false;
+            g_def_cancelled = g_def_cancelled + 1;
+            reapply(d->lo, d->hi);
+        } else {
+            fill_one(*d, false);
+        }
+    }
     for (TrackedRegion* r : g_tracked) {
         const auto rlo = reinterpret_cast<std::uintptr_t>(r->ref.base);
         if (rlo < hi && lo < rlo + r->ref.bytes) r->dirty = true;
@@ -322,6 +423,69 @@ void note_host_write(const void* base, std::size_t bytes) {
             mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ | PROT_WRITE);
         }
     }
+}
+
+// ---- lazy ranges -------------------------------------------------------------------
+
+void defer_range(DeferredRange& d) {
+    if (d.hi <= d.lo) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    ensure_handler();
+    if (!d.linked) {
+        g_deferred.push_back(&d);
+        d.linked = true;
+    }
+    g_stat_mprotect = g_stat_mprotect + 1;
+    if (mprotect(reinterpret_cast<void*>(d.lo), d.hi - d.lo, PROT_NONE) != 0) {
+        reapply(d.lo, d.hi);
+        throw Error(Errc::ProtectionUnsupported, std::string("mprotect failed: ") + std::strerror(errno));
+    }
+    d.active = true;
+    g_def_n = g_def_n + 1;
+}
+
+void materialize_range(const void* base, std::size_t bytes) {
+    if (g_deferred.empty() || bytes == 0) return;
+    const auto lo = reinterpret_cast<std::uintptr_t>(base);
+    const std::uintptr_t hi = lo + bytes;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (DeferredRange* d : g_deferred)
+        if (d->active && d->lo < hi && lo < d->hi) fill_one(*d, false);
+}
+
+void materialize_all() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (DeferredRange* d : g_deferred)
+        if (d->active) fill_one(*d, false);
+}
+
+void retire_deferred(DeferredRange& d, bool fill) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (d.active) {
+        if (fill) {
+            fill_one(d, false);
+        } else {
+            d.active = false;
+            reapply(d.lo, d.hi);
+        }
+    }
+    if (d.linked) {
+        g_deferred.erase(std::remove(g_deferred.begin(), g_deferred.end(), &d), g_deferred.end());
+        d.linked = false;
+    }
+}
+
+bool any_deferred() {
+    for (const DeferredRange* d : g_deferred)
+        if (d->active) return true;
+    return false;
+}
+
+void deferred_counters(long* deferred, long* fault_fills, long* explicit_fills, long* cancelled) {
+    if (deferred) *deferred = g_def_n;
+    if (fault_fills) *fault_fills = g_def_fault_fills;
+    if (explicit_fills) *explicit_fills = g_def_explicit_fills;
+    if (cancelled) *cancelled = g_def_cancelled;
 }
 
 // ---- MarshalObjectBase --------------------------------------------------------

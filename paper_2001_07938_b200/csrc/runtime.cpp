@@ -187,6 +187,8 @@ void ensure_init() {
     const char* k = std::getenv("LILAC_B200_KERNEL");
     if (k && *k) r.kernel = parse_csr_kernel(k);
     r.strategy = lilac::marshal::default_strategy(Strategy::Hybrid);
+    const char* wb = std::getenv("LILAC_B200_WRITEBACK");
+    if (wb && std::strcmp(wb, "lazy") == 0) r.lazy_writeback = true;
     // registered after the CUDA runtime initialised, so it runs before the
     // runtime's own teardown (mirrors harnessgen.cpp:98-113)
     std::atexit(at_exit_teardown);
@@ -243,12 +245,20 @@ void upload(DevArray& d, const void* host, std::size_t bytes) {
         }
     }
     PhaseTimer pt(kPhH2D);
+    host_in(host, bytes);
     B200_CUDA(cudaMemcpyAsync(d.buf.ptr, host, bytes, cudaMemcpyHostToDevice, rt().stream));
     d.h2d += static_cast<std::int64_t>(bytes);
 }
 
 void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter) {
     if (bytes == 0) return;
+    if (rt().lazy_writeback) {
+        PhaseTimer pt(kPhPublish);
+        if (mirror_publish_lazy(host, bytes, d.buf.ptr, rt().stream)) {
+            counter.lazy += static_cast<std::int64_t>(bytes);
+            return;
+        }
+    }
     {
         PhaseTimer pt(kPhD2H);
         B200_CUDA(cudaMemcpyAsync(host, d.buf.ptr, bytes, cudaMemcpyDeviceToHost, rt().stream));
@@ -268,6 +278,7 @@ namespace {
 struct Mirror {
     lilac::marshal::TrackedRegion reg;
     DevBuf buf;
+    lilac::marshal::DeferredRange lazy;  // active while the host bytes are still on the device
 };
 
 std::map<std::uintptr_t, std::unique_ptr<Mirror>> g_mirrors;  // keyed by host base
@@ -284,7 +295,28 @@ bool mirrors_enabled() {
     return on == 1;
 }
 
-void drop_mirror(std::map<std::uintptr_t, std::unique_ptr<Mirror>>::iterator it) {
+std::int64_t g_lazy_deferred = 0, g_lazy_filled = 0;
+
+// Materialise a lazy write-back: the mirror holds the bytes. Runs in the
+// fault handler or before a DMA read; a failure here loses data: abort.
+void mirror_fill(lilac::marshal::DeferredRange* d) {
+    auto* m = static_cast<Mirror*>(d->ctx);
+    const std::size_t bytes = d->content_hi - d->content_lo;
+    Runtime& r = rt();
+    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(d->content_lo), m->buf.ptr, bytes,
+                                    cudaMemcpyDeviceToHost, r.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(r.stream);
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "lilac-b200: lazy write-back of %zu bytes failed: %s\n", bytes, cudaGetErrorString(e));
+        std::abort();
+    }
+    g_lazy_filled += static_cast<std::int64_t>(bytes);
+}
+
+// fill: materialise first if the host bytes are still lazy (false when the
+// caller is about to overwrite all of them)
+void drop_mirror(std::map<std::uintptr_t, std::unique_ptr<Mirror>>::iterator it, bool fill = true) {
+    lilac::marshal::retire_deferred(it->second->lazy, fill);
     lilac::marshal::drop_guard(it->second->reg);
     g_mirror_total -= it->second->buf.cap;
     it->second->buf.release();
@@ -344,6 +376,53 @@ void mirror_publish(const void* host, std::size_t bytes, const void* dev_src, cu
     g_mirrors.emplace(h, std::move(m));
 }
 
+bool mirror_publish_lazy(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s) {
+    const auto h = reinterpret_cast<std::uintptr_t>(host);
+    const std::size_t pg = lilac::marshal::page_size();
+    if (!mirrors_enabled() || bytes < kMirrorMin || h % pg != 0) return false;
+    for (auto it = g_mirrors.begin(); it != g_mirrors.end();) {
+        const std::uintptr_t lo = it->first, hi = lo + it->second->reg.ref.bytes;
+        if (lo < h + bytes && h < hi) {
+            auto nx = std::next(it);
+            drop_mirror(it, !(h <= lo && hi <= h + bytes));
+            it = nx;
+        } else {
+            ++it;
+        }
+    }
+    if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
+    auto m = std::make_unique<Mirror>();
+    m->buf.ensure(bytes);
+    B200_CUDA(cudaMemcpyAsync(m->buf.ptr, dev_src, bytes, cudaMemcpyDeviceToDevice, s));
+    m->reg.ref = {host, bytes, nullptr};
+    m->reg.strategy = lilac::marshal::Strategy::PageProtect;  // whole pages: no edge hashing of lazy bytes
+    m->lazy.lo = h;
+    m->lazy.hi = (h + bytes + pg - 1) / pg * pg;
+    m->lazy.content_lo = h;
+    m->lazy.content_hi = h + bytes;
+    m->lazy.fill = mirror_fill;
+    m->lazy.ctx = m.get();
+    try {
+        PhaseTimer pt(kPhPublishGuard);
+        lilac::marshal::mark_clean(m->reg);
+        lilac::marshal::defer_range(m->lazy);
+    } catch (const Error&) {
+        lilac::marshal::retire_deferred(m->lazy, false);
+        lilac::marshal::drop_guard(m->reg);
+        m->buf.release();
+        return false;  // eager write-back instead
+    }
+    g_lazy_deferred += static_cast<std::int64_t>(bytes);
+    g_mirror_total += m->buf.cap;
+    g_mirrors.emplace(h, std::move(m));
+    return true;
+}
+
+void lazy_bytes(std::int64_t* deferred, std::int64_t* filled) {
+    if (deferred) *deferred = g_lazy_deferred;
+    if (filled) *filled = g_lazy_filled;
+}
+
 void mirrors_clear() {
     while (!g_mirrors.empty()) drop_mirror(g_mirrors.begin());
 }
@@ -355,6 +434,7 @@ void upload_row_ptr(DevBuf& buf, const std::int64_t* row_ptr, std::int64_t rows,
     Runtime& r = rt();
     const std::size_t bytes = sizeof(std::int64_t) * static_cast<std::size_t>(rows + 1);
     buf.ensure(bytes);
+    host_in(row_ptr, bytes);
     B200_CUDA(cudaMemcpyAsync(buf.ptr, row_ptr, bytes, cudaMemcpyHostToDevice, r.stream));
     B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
     launch_check_row_ptr(buf.as<std::int64_t>(), rows, nnz, r.d_umax(), r.d_bad(), r.stream);
@@ -373,6 +453,7 @@ std::int64_t upload_col_ind(DevBuf& buf, const std::int64_t* col_ind, std::int64
     Runtime& r = rt();
     const std::size_t n = static_cast<std::size_t>(std::max<std::int64_t>(nnz, 0));
     buf.ensure(n * sizeof(std::int32_t));
+    host_in(col_ind, n * sizeof(std::int64_t));
     B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
     // narrow chunk by chunk through a bounded staging buffer
     const std::size_t chunk = std::max<std::size_t>(1, r.stage_bytes / sizeof(std::int64_t));
@@ -440,6 +521,39 @@ int b200_set_strategy(const char* name) {
 }
 
 void b200_set_exact_blas(int on) { rt().exact_blas = on != 0; }
+
+int b200_set_writeback(const char* mode) {
+    return boundary("b200_set_writeback", [&] {
+        const std::string m = mode ? mode : "";
+        if (m == "lazy")
+            rt().lazy_writeback = true;
+        else if (m == "eager")
+            rt().lazy_writeback = false;
+        else
+            throw Error(Errc::DataError, "unknown write-back mode '" + m + "' (expected eager or lazy)");
+    });
+}
+
+int b200_host_sync(const void* host, size_t bytes) {
+    return boundary("b200_host_sync", [&] {
+        if (host)
+            lilac::marshal::materialize_range(host, bytes);
+        else
+            lilac::marshal::materialize_all();
+    });
+}
+
+int b200_lazy_counters(int64_t* ranges, int64_t* fault_fills, int64_t* explicit_fills, int64_t* cancelled,
+                       int64_t* bytes_deferred, int64_t* bytes_filled) {
+    long a = 0, b = 0, c = 0, d = 0;
+    lilac::marshal::deferred_counters(&a, &b, &c, &d);
+    if (ranges) *ranges = a;
+    if (fault_fills) *fault_fills = b;
+    if (explicit_fills) *explicit_fills = c;
+    if (cancelled) *cancelled = d;
+    lazy_bytes(bytes_deferred, bytes_filled);
+    return 0;
+}
 
 const char* b200_version(void) { return "lilac-b200 0.1 sm_100a"; }
 

@@ -23,6 +23,7 @@ struct DevArray {
     std::int64_t h2d = 0;
     std::int64_t d2h = 0;
     std::int64_t d2d = 0;  // bytes served from a device mirror instead of the host
+    std::int64_t lazy = 0;  // write-back bytes left on the device (lazy mode)
 };
 
 struct HarnessStats {
@@ -42,6 +43,7 @@ struct Runtime {
     CsrKernel kernel = CsrKernel::Auto;
     Strategy strategy = Strategy::Hybrid;
     bool exact_blas = false;
+    bool lazy_writeback = false;  // LILAC_B200_WRITEBACK=lazy / b200_set_writeback
     std::size_t stage_bytes = std::size_t(256) << 20;  // chunk for narrowing uploads
     DevBuf stage;
 
@@ -97,9 +99,15 @@ int boundary(const char* fn, F&& f) {
 
 // ---- transfer helpers (stream-ordered, synchronous w.r.t. the host) --------------
 
+// Before any DMA read of caller memory: lazy bytes there must be real first
+// (DMA does not fault on PROT_NONE pages).
+inline void host_in(const void* p, std::size_t bytes) { lilac::marshal::materialize_range(p, bytes); }
+
 // upload: H2D, or D2D from a valid device mirror of the same host bytes.
 void upload(DevArray& d, const void* host, std::size_t bytes);
 // download: D2H write-back; then publishes a device mirror of the host region.
+// Lazy mode (page-aligned regions >= 8 KiB): no D2H — the mirror is published
+// with the host pages PROT_NONE, and the bytes land on first touch.
 void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter);
 
 // Device mirrors (the coherence layer of SURVEY §8(f)1): after a write-back the
@@ -108,6 +116,8 @@ void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counte
 // of (a sub-range of) it is served device-to-device. LILAC_B200_MIRRORS=0 off.
 bool mirror_fetch(void* dev_dst, const void* host, std::size_t bytes, cudaStream_t s);
 void mirror_publish(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s);
+bool mirror_publish_lazy(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s);
+void lazy_bytes(std::int64_t* deferred, std::int64_t* filled);
 void mirrors_clear();
 std::int64_t mirror_bytes();
 

@@ -21,7 +21,8 @@ import numpy as np
 from . import _native as N
 
 __all__ = ["spmv_csr", "spmv_jds", "dotproduct", "axpy", "xpay", "HarnessRegistry",
-           "register_b200_harnesses", "region_stats", "harness_stats", "B200Error", "set_errors_return"]
+           "register_b200_harnesses", "region_stats", "harness_stats", "B200Error", "set_errors_return",
+           "set_writeback", "host_sync", "lazy_counters", "page_aligned"]
 
 B200Error = N.B200Error
 
@@ -75,6 +76,39 @@ def axpy(n, y, alpha, x):
 def xpay(n, y, beta, x):
     N.lib().b200_xpay(int(n), N.ptr(_f64(y, "y", True)), float(beta), N.ptr(_f64(x, "x")))
     N.check()
+
+
+def set_writeback(mode: str):
+    """"eager" (the reference's behaviour) or "lazy" (outputs stay on the
+    device until the host touches them; include/lilac_b200.h)."""
+    N.check(N.lib().b200_set_writeback(mode.encode()))
+
+
+def host_sync(a=None):
+    """Materialise lazy write-back bytes of `a` (all when None) — needed before
+    handing the array to DMA or a system call."""
+    if a is None:
+        N.check(N.lib().b200_host_sync(None, 0))
+    else:
+        N.check(N.lib().b200_host_sync(N.ptr(a), a.nbytes))
+
+
+def lazy_counters():
+    import ctypes as C
+    v = [C.c_int64() for _ in range(6)]
+    N.lib().b200_lazy_counters(*[C.byref(x) for x in v])
+    keys = ["ranges", "fault_fills", "explicit_fills", "cancelled", "bytes_deferred", "bytes_filled"]
+    return {k: x.value for k, x in zip(keys, v)}
+
+
+def page_aligned(n, dtype=np.float64):
+    """A zeroed array whose data starts on a page boundary (lazy write-back
+    applies to page-aligned outputs; numpy's malloc'd arrays are not)."""
+    import mmap
+    dt = np.dtype(dtype)
+    nbytes = max(int(n) * dt.itemsize, 1)
+    buf = mmap.mmap(-1, (nbytes + mmap.PAGESIZE - 1) // mmap.PAGESIZE * mmap.PAGESIZE)
+    return np.frombuffer(buf, dtype=dt, count=int(n))
 
 
 class HarnessRegistry:

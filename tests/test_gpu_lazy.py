@@ -1,0 +1,162 @@
+"""Lazy write-back on the B200: outputs stay on the device,
+host pages fill on first touch, chained harness calls stay device-resident.
+Results must be bit-identical to eager write-back."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2001_07938_b200 import _native as N
+from paper_2001_07938_b200 import harness as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _lazy():
+    H.set_errors_return(True)
+    N.lib().b200_set_kernel(b"auto")
+    H.set_writeback("lazy")
+    yield
+    H.host_sync()
+    H.set_writeback("eager")
+
+
+def rand_csr(rows, cols, per_row, seed):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 2 * per_row + 1, rows)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = rng.integers(0, cols, int(rp[-1])).astype(np.int64)
+    val = rng.uniform(-2, 2, int(rp[-1]))
+    return rp, ci, val
+
+
+def test_lazy_output_fills_on_first_read_and_matches_oracle():
+    rows = 50_000
+    rp, ci, val = rand_csr(rows, rows, 8, 11)
+    x = np.random.default_rng(1).uniform(-1, 1, rows)
+    y = H.page_aligned(rows)
+    c0 = H.lazy_counters()
+    N.lib().b200_set_exact_blas(0)
+    N.lib().b200_set_kernel(b"exact")
+    try:
+        H.spmv_csr(rows, y, rp, val, x, ci)
+        c1 = H.lazy_counters()
+        assert c1["ranges"] == c0["ranges"] + 1
+        assert c1["fault_fills"] == c0["fault_fills"]  # nothing touched yet
+        ref = O.spmv_csr(rp, ci, val, x, rows)
+        assert np.array_equal(y, ref)  # the read faults and fills
+        c2 = H.lazy_counters()
+        assert c2["fault_fills"] == c1["fault_fills"] + 1
+        assert c2["bytes_filled"] - c1["bytes_filled"] == rows * 8
+    finally:
+        N.lib().b200_set_kernel(b"auto")
+
+
+def test_chained_calls_stay_on_device():
+    """y = A x (lazy), z = A y: y is served device-to-device, never filled."""
+    rows = 40_000
+    rp, ci, val = rand_csr(rows, rows, 6, 12)
+    x = np.random.default_rng(2).uniform(-1, 1, rows)
+    y, z = H.page_aligned(rows), H.page_aligned(rows)
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    c0 = H.lazy_counters()
+    s0 = H.harness_stats()["b200_spmv_csr"]
+    for _ in range(3):
+        H.spmv_csr(rows, z, rp, val, y, ci)
+    c1 = H.lazy_counters()
+    s1 = H.harness_stats()["b200_spmv_csr"]
+    assert c1["fault_fills"] == c0["fault_fills"] and c1["explicit_fills"] == c0["explicit_fills"]
+    assert s1["bytes_h2d"] == s0["bytes_h2d"]  # y came from its device mirror
+    assert s1["bytes_d2h"] == s0["bytes_d2h"]  # z never copied back
+    assert c1["cancelled"] >= c0["cancelled"] + 2  # z's earlier lazy bytes superseded
+    # eager reference of the same chain
+    H.set_writeback("eager")
+    y2, z2 = np.empty(rows), np.empty(rows)
+    H.spmv_csr(rows, y2, rp, val, x, ci)
+    H.spmv_csr(rows, z2, rp, val, y2, ci)
+    assert np.array_equal(z, z2) and np.array_equal(y, y2)
+
+
+def test_host_write_after_lazy_output_is_seen_by_next_call():
+    rows = 30_000
+    rp, ci, val = rand_csr(rows, rows, 5, 13)
+    x = np.random.default_rng(3).uniform(-1, 1, rows)
+    y, z = H.page_aligned(rows), H.page_aligned(rows)
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    y[7] = 123.0  # fault: fill, then the write dirties the mirror
+    H.spmv_csr(rows, z, rp, val, y, ci)
+    H.set_writeback("eager")
+    yy = O.spmv_csr(rp, ci, val, x, rows)
+    yy[7] = 123.0
+    z_ref = np.empty(rows)
+    H.spmv_csr(rows, z_ref, rp, val, yy, ci)
+    assert np.array_equal(z, z_ref)
+
+
+def test_host_sync_materialises_for_dma():
+    rows = 20_000
+    rp, ci, val = rand_csr(rows, rows, 4, 14)
+    x = np.random.default_rng(4).uniform(-1, 1, rows)
+    y = H.page_aligned(rows)
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    c0 = H.lazy_counters()
+    H.host_sync(y)
+    c1 = H.lazy_counters()
+    assert c1["explicit_fills"] == c0["explicit_fills"] + 1
+    ref = O.spmv_csr(rp, ci, val, x, rows)
+    scale = O.spmv_csr(rp, ci, np.abs(val), np.abs(x), rows)
+    assert (np.abs(y - ref) <= 1e-12 * scale).all()
+    assert H.lazy_counters()["fault_fills"] == c1["fault_fills"]  # already real: no fault
+
+
+def test_misaligned_output_falls_back_to_eager():
+    rows = 20_000
+    rp, ci, val = rand_csr(rows, rows, 4, 15)
+    x = np.random.default_rng(5).uniform(-1, 1, rows)
+    raw = H.page_aligned(rows + 1)
+    y = raw[1:]  # 8 bytes past a page boundary
+    c0 = H.lazy_counters()
+    s0 = H.harness_stats()["b200_spmv_csr"]
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    assert H.lazy_counters()["ranges"] == c0["ranges"]
+    assert H.harness_stats()["b200_spmv_csr"]["bytes_d2h"] - s0["bytes_d2h"] == rows * 8
+
+
+def _host_cg(n, rp, ci, val, alloc, iters=25):
+    """The LiLAC host CG loop (bench.e2e_harness_cg) on arrays from `alloc`."""
+    x, z, r, p, q = (alloc(n) for _ in range(5))
+    x[:] = 1.0
+    r[:] = x
+    p[:] = r
+    rho = H.dotproduct(n, r, r)
+    for _ in range(iters):
+        H.spmv_csr(n, q, rp, val, p, ci)
+        d = H.dotproduct(n, p, q)
+        alpha = rho / d
+        rho0 = rho
+        H.axpy(n, z, alpha, p)
+        H.axpy(n, r, -alpha, q)
+        rho = H.dotproduct(n, r, r)
+        H.xpay(n, p, rho / rho0, r)
+    return np.array(z), rho
+
+
+def test_cg_lazy_bit_identical_to_eager_and_device_resident():
+    from paper_2001_07938_b200 import device as D
+    n = 14000
+    rp, ci, val = D.gen_npb(n, 11, 20.0)
+    H.set_writeback("eager")
+    z_e, rho_e = _host_cg(n, rp, ci, val, lambda k: np.zeros(k))
+    H.set_writeback("lazy")
+    c0 = H.lazy_counters()
+    s0 = {k: v["bytes_h2d"] for k, v in H.harness_stats().items()}
+    z_l, rho_l = _host_cg(n, rp, ci, val, H.page_aligned)
+    c1 = H.lazy_counters()
+    s1 = {k: v["bytes_h2d"] for k, v in H.harness_stats().items()}
+    assert rho_l == rho_e
+    assert np.array_equal(z_l, z_e)
+    assert c1["ranges"] - c0["ranges"] >= 4 * 25
+    # steady state: no vector crosses the bus inside the loop beyond the
+    # initial x/r/p uploads and the final read of z
+    h2d = sum(s1[k] - s0.get(k, 0) for k in s1)
+    assert h2d <= 8 * n * 6, h2d
