@@ -83,7 +83,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.replace(tmp, LIB)
     build_cpp_tests(force, verbose)
     build_generated_harness(force, verbose)
+    build_python_ext(force, verbose)
     return LIB
+
+
+def build_python_ext(force: bool = False, verbose: bool = False):
+    """paper_2001_07938_b200/_harness*.so: the CPython binding of the harness
+    entry points (csrc/pyext/harness_module.c), linked to liblilac_b200.so."""
+    import sysconfig
+    src = os.path.join(CSRC, "pyext", "harness_module.c")
+    out = os.path.join(PKG, "_harness" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if force or _stale(out, [src, LIB, os.path.join(INCLUDE, "lilac_b200.h")]):
+        _run(["gcc", "-O2", "-fPIC", "-shared", "-Wall", f"-I{sysconfig.get_paths()['include']}", f"-I{INCLUDE}",
+              "-o", out, src, f"-L{PKG}", "-llilac_b200", "-Wl,-rpath,$ORIGIN"], verbose)
+    return out
 
 
 GEN_LIB = os.path.join(PKG, "liblilac_b200_gen.so")

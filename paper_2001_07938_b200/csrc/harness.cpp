@@ -41,7 +41,7 @@ void ReadableMax_update(const void* in, std::size_t size, std::int64_t& out) {
 
 // B200Read (input): resident device copy, refreshed on change.
 void B200Read_update(const void* in, std::size_t size, DevArray& out) { upload(out, in, size); }
-void B200Read_destruct(const void*, std::size_t, DevArray& out) { out.buf.release(); }
+void B200Read_destruct(const void*, std::size_t, DevArray& out) { out.release(); }
 
 // B200Write (output): device destination, write_back = device->host copy.
 void B200Write_construct(const void*, std::size_t size, DevArray& out) { out.buf.ensure(size); }
@@ -392,7 +392,7 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         A.row_ptr = rp.buf.as<std::int64_t>();
         A.col = ci.buf.ptr;
         A.col32 = ci.col32;
-        A.val = dval.buf.as<double>();
+        A.val = dval.data<double>();
         A.monotone = rp.monotone;
         // derived tiled layout: rebuilt only when row_ptr/col_ind/val were re-marshaled
         const std::int64_t stamp = matrix_stamp(state);
@@ -408,7 +408,7 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         if (state.tiled.valid) A.tiled = &state.tiled.dev;
         if (state.merge.valid) A.merge = &state.merge.dev;
         tm.acquired();
-        timed_launch(hs, [&] { launch_spmv_csr(A, dx.buf.as<double>(), dout.buf.as<double>(), rt().kernel, rt().stream); });
+        timed_launch(hs, [&] { launch_spmv_csr(A, dx.data<double>(), dout.buf.as<double>(), rt().kernel, rt().stream); });
         tm.acquired();
 
         state.m_output.write_back();
@@ -465,7 +465,7 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
             // offsets jd_ptr[k] + p must stay inside [0, nnz) (what_interp.cpp:67-68)
             Runtime& r = rt();
             B200_CUDA(cudaMemsetAsync(r.flags.ptr, 0, 16, r.stream));
-            launch_check_jds(dnz.buf.as<std::int64_t>(), djd.buf.as<std::int64_t>(), rows, njd, nnz, r.d_bad(),
+            launch_check_jds(dnz.data<std::int64_t>(), djd.data<std::int64_t>(), rows, njd, nnz, r.d_bad(),
                              r.stream);
             int bad = 0;
             B200_CUDA(cudaMemcpyAsync(&bad, r.d_bad(), 4, cudaMemcpyDeviceToHost, r.stream));
@@ -480,14 +480,14 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         A.nnz = nnz;
         A.cols = ci.cols;
         A.njd = njd;
-        A.nzcnt = dnz.buf.as<std::int64_t>();
+        A.nzcnt = dnz.data<std::int64_t>();
         A.perm = dperm.perm.as<std::int64_t>();
         A.inv_perm = dperm.bijective ? dperm.inv.as<std::int64_t>() : nullptr;
-        A.jd_ptr = djd.buf.as<std::int64_t>();
+        A.jd_ptr = djd.data<std::int64_t>();
         A.col = ci.buf.ptr;
         A.col32 = ci.col32;
-        A.val = dval.buf.as<double>();
-        timed_launch(hs, [&] { launch_spmv_jds(A, dx.buf.as<double>(), dout.buf.as<double>(), rt().stream); });
+        A.val = dval.data<double>();
+        timed_launch(hs, [&] { launch_spmv_jds(A, dx.data<double>(), dout.buf.as<double>(), rt().stream); });
         tm.acquired();
 
         state.m_output.write_back();
@@ -518,9 +518,9 @@ extern "C" void b200_dot(double* result, std::int64_t length, const double* a, c
         timed_launch(hs, [&] {
             Runtime& r = rt();
             if (r.exact_blas)
-                launch_dot_exact(da.buf.as<double>(), db.buf.as<double>(), length, dres.buf.as<double>(), r.stream);
+                launch_dot_exact(da.data<double>(), db.data<double>(), length, dres.buf.as<double>(), r.stream);
             else
-                launch_dot(da.buf.as<double>(), db.buf.as<double>(), length, dres.buf.as<double>(),
+                launch_dot(da.data<double>(), db.data<double>(), length, dres.buf.as<double>(),
                            r.partials.as<double>(), r.d_ticket(), r.stream);
         });
         tm.acquired();
@@ -554,11 +554,11 @@ void vec2_call(const char* name, std::int64_t n, double* y, double s, const doub
     timed_launch(hs, [&] {
         Runtime& r = rt();
         if (n > 0)
-            B200_CUDA(cudaMemcpyAsync(dout.buf.ptr, dy.buf.ptr, bytes, cudaMemcpyDeviceToDevice, r.stream));
+            B200_CUDA(cudaMemcpyAsync(dout.buf.ptr, dy.data<char>(), bytes, cudaMemcpyDeviceToDevice, r.stream));
         if (axpy)
-            launch_axpy(n, dout.buf.as<double>(), s, dx.buf.as<double>(), r.stream);
+            launch_axpy(n, dout.buf.as<double>(), s, dx.data<double>(), r.stream);
         else
-            launch_xpay(n, dout.buf.as<double>(), s, dx.buf.as<double>(), r.stream);
+            launch_xpay(n, dout.buf.as<double>(), s, dx.data<double>(), r.stream);
     });
     tm.acquired();
     oo.write_back();

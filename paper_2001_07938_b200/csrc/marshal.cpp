@@ -228,18 +228,38 @@ void edge_spans(const TrackedRegion& r, std::uintptr_t& in_lo, std::uintptr_t& i
     if (in_hi <= in_lo) in_lo = in_hi = end;  // no whole page inside: hash everything
 }
 
-std::uint64_t head_hash(const TrackedRegion& r) {
+// Hybrid edge snapshot: head bytes then tail bytes.
+std::size_t head_len(const TrackedRegion& r) {
     const auto base = reinterpret_cast<std::uintptr_t>(r.ref.base);
-    const std::uintptr_t n = r.hash_head_end > base ? r.hash_head_end - base : 0;
-    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(n);
-    return fnv1a(r.ref.base, n);
+    return r.hash_head_end > base ? r.hash_head_end - base : 0;
 }
 
-std::uint64_t tail_hash(const TrackedRegion& r) {
+std::size_t tail_len(const TrackedRegion& r) {
     const auto end = reinterpret_cast<std::uintptr_t>(r.ref.base) + r.ref.bytes;
-    if (r.hash_tail_begin >= end) return 0;
-    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(end - r.hash_tail_begin);
-    return fnv1a(reinterpret_cast<const void*>(r.hash_tail_begin), end - r.hash_tail_begin);
+    return r.hash_tail_begin < end ? end - r.hash_tail_begin : 0;
+}
+
+void snapshot_edges(TrackedRegion& r) {
+    const std::size_t h = head_len(r), t = tail_len(r);
+    r.edges.resize(h + t);
+    if (h) std::memcpy(r.edges.data(), r.ref.base, h);
+    if (t) std::memcpy(r.edges.data() + h, reinterpret_cast<const void*>(r.hash_tail_begin), t);
+    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(h + t);
+}
+
+bool edges_changed(const TrackedRegion& r) {
+    const std::size_t h = head_len(r), t = tail_len(r);
+    g_stat_hash_bytes = g_stat_hash_bytes + static_cast<long>(h + t);
+    if (r.edges.size() != h + t) return true;
+    if (h && std::memcmp(r.edges.data(), r.ref.base, h) != 0) return true;
+    return t && std::memcmp(r.edges.data() + h, reinterpret_cast<const void*>(r.hash_tail_begin), t) != 0;
+}
+
+// Is [lo, hi) inside one active lazy range?
+bool covered_by_deferred(std::uintptr_t lo, std::uintptr_t hi) {
+    for (const DeferredRange* d : g_deferred)
+        if (d->active && d->lo <= lo && hi <= d->hi) return true;
+    return false;
 }
 
 }  // namespace
@@ -348,8 +368,7 @@ void mark_clean(TrackedRegion& r) {
             }
         }
         if (g_hi > g_lo) add_guard(r, g_lo, g_hi);
-        r.last_checksum = head_hash(r);
-        r.last_tail_checksum = tail_hash(r);
+        snapshot_edges(r);
         return;
     }
     }
@@ -368,8 +387,7 @@ bool poll_dirty(TrackedRegion& r) {
     case Strategy::PageProtect:
         return r.dirty;
     case Strategy::Hybrid:
-        if (!r.dirty && r.ref.bytes > 0)
-            r.dirty = head_hash(r) != r.last_checksum || tail_hash(r) != r.last_tail_checksum;
+        if (!r.dirty && r.ref.bytes > 0) r.dirty = edges_changed(r);
         return r.dirty;
     }
     return true;
@@ -398,10 +416,34 @@ void note_host_write(const void* base, std::size_t bytes) {
     const auto lo = reinterpret_cast<std::uintptr_t>(base);
     const std::uintptr_t hi = lo + bytes;
     std::lock_guard<std::mutex> lk(g_mu);
-    // lazy bytes under the write: superseded if the write covers them all,
-    // else materialised first (the write lands on top of them)
+    for (TrackedRegion* r : g_tracked) {
+        const auto rlo = reinterpret_cast<std::uintptr_t>(r->ref.base);
+        if (rlo < hi && lo < rlo + r->ref.bytes) r->dirty = true;
+    }
+    // open the pages for the incoming write (DMA never faults; a CPU copy
+    // would); lazy pages stay closed
+    const std::uintptr_t plo = floor_page(lo), phi = ceil_page(hi);
+    bool guarded = false;
+    for (const Guard& g : g_guards) {
+        if (g.lo < phi && plo < g.hi) {
+            g.region->dirty = true;
+            guarded = true;
+        }
+    }
+    if (guarded && !covered_by_deferred(plo, phi)) {
+        g_stat_mprotect = g_stat_mprotect + 1;
+        mprotect(reinterpret_cast<void*>(plo), phi - plo, PROT_READ | PROT_WRITE);
+        apply_deferred(plo, phi);
+    }
+}
+
+void supersede_range(const void* base, std::size_t bytes) {
+    if (g_deferred.empty() || bytes == 0) return;
+    const auto lo = reinterpret_cast<std::uintptr_t>(base);
+    const std::uintptr_t hi = lo + bytes;
+    std::lock_guard<std::mutex> lk(g_mu);
     for (DeferredRange* d : g_deferred) {
-        if (!d->active || !(d->content_lo < hi && lo < d->content_hi)) continue;
+        if (!d->active || !(d->lo < hi && lo < d->hi)) continue;
         if (lo <= d->content_lo && d->content_hi <= hi) {
             d->active = false;
             g_def_cancelled = g_def_cancelled + 1;
@@ -410,19 +452,19 @@ void note_host_write(const void* base, std::size_t bytes) {
             fill_one(*d, false);
         }
     }
-    for (TrackedRegion* r : g_tracked) {
-        const auto rlo = reinterpret_cast<std::uintptr_t>(r->ref.base);
-        if (rlo < hi && lo < rlo + r->ref.bytes) r->dirty = true;
+}
+
+bool reclean_covered(TrackedRegion& r) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!r.guarded || !covered_by_deferred(r.guard_lo, r.guard_hi)) return false;
+    if (r.strategy == Strategy::Hybrid) {
+        if (head_len(r) || tail_len(r)) return false;  // has hashed edges: full mark_clean
+    } else if (r.strategy != Strategy::PageProtect) {
+        return false;
     }
-    // open the pages for the incoming write (DMA never faults; a CPU copy would)
-    const std::uintptr_t plo = floor_page(lo), phi = ceil_page(hi);
-    for (const Guard& g : g_guards) {
-        std::uintptr_t a = std::max(plo, g.lo), b = std::min(phi, g.hi);
-        if (a < b) {
-            g.region->dirty = true;
-            mprotect(reinterpret_cast<void*>(a), b - a, PROT_READ | PROT_WRITE);
-        }
-    }
+    track(r);
+    r.dirty = false;
+    return true;
 }
 
 // ---- lazy ranges -------------------------------------------------------------------

@@ -235,39 +235,42 @@ std::vector<HarnessStats*> all_harness_stats() { return g_hstats; }
 // ---- transfers -------------------------------------------------------------------
 
 void upload(DevArray& d, const void* host, std::size_t bytes) {
-    d.buf.ensure(bytes);
-    if (bytes == 0) return;
-    {
+    if (bytes > 0) {
         PhaseTimer pt(kPhMirrorFetch);
-        if (mirror_fetch(d.buf.ptr, host, bytes, rt().stream)) {
+        if (mirror_fetch(d, host, bytes)) {
             d.d2d += static_cast<std::int64_t>(bytes);
             return;
         }
     }
+    d.lent.reset();
+    d.view = nullptr;
+    d.buf.ensure(bytes);
+    if (bytes == 0) return;
     PhaseTimer pt(kPhH2D);
     host_in(host, bytes);
     B200_CUDA(cudaMemcpyAsync(d.buf.ptr, host, bytes, cudaMemcpyHostToDevice, rt().stream));
     d.h2d += static_cast<std::int64_t>(bytes);
 }
 
-void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter) {
+void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter) {
     if (bytes == 0) return;
     if (rt().lazy_writeback) {
         PhaseTimer pt(kPhPublish);
-        if (mirror_publish_lazy(host, bytes, d.buf.ptr, rt().stream)) {
+        if (mirror_publish_lazy(host, bytes, d.buf)) {
             counter.lazy += static_cast<std::int64_t>(bytes);
             return;
         }
     }
     {
         PhaseTimer pt(kPhD2H);
+        lilac::marshal::supersede_range(host, bytes);  // lazy bytes under the destination
         B200_CUDA(cudaMemcpyAsync(host, d.buf.ptr, bytes, cudaMemcpyDeviceToHost, rt().stream));
         B200_CUDA(cudaStreamSynchronize(rt().stream));
     }
     PhaseTimer pt(kPhPublish);
     // publish only after the bytes landed (pinned D2H is asynchronous: the
-    // mirror's edge hashes must see the written data)
-    mirror_publish(host, bytes, d.buf.ptr, rt().stream);
+    // mirror's edge snapshot must see the written data)
+    mirror_publish(host, bytes, d.buf);
     counter.d2h += static_cast<std::int64_t>(bytes);
 }
 
@@ -277,7 +280,7 @@ namespace {
 
 struct Mirror {
     lilac::marshal::TrackedRegion reg;
-    DevBuf buf;
+    std::shared_ptr<const DevBuf> buf;  // immutable once published; borrowed by inputs
     lilac::marshal::DeferredRange lazy;  // active while the host bytes are still on the device
 };
 
@@ -295,6 +298,18 @@ bool mirrors_enabled() {
     return on == 1;
 }
 
+// Take src's device allocation (no copy) as an immutable shared buffer; src
+// gets a fresh allocation of the same size from the pool.
+std::shared_ptr<const DevBuf> steal(DevBuf& src, std::size_t bytes) {
+    auto* b = new DevBuf(src);
+    src = DevBuf{};
+    src.ensure(bytes);
+    return std::shared_ptr<const DevBuf>(b, [](const DevBuf* p) {
+        const_cast<DevBuf*>(p)->release();
+        delete p;
+    });
+}
+
 std::int64_t g_lazy_deferred = 0, g_lazy_filled = 0;
 
 // Materialise a lazy write-back: the mirror holds the bytes. Runs in the
@@ -303,7 +318,7 @@ void mirror_fill(lilac::marshal::DeferredRange* d) {
     auto* m = static_cast<Mirror*>(d->ctx);
     const std::size_t bytes = d->content_hi - d->content_lo;
     Runtime& r = rt();
-    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(d->content_lo), m->buf.ptr, bytes,
+    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(d->content_lo), m->buf->ptr, bytes,
                                     cudaMemcpyDeviceToHost, r.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r.stream);
     if (e != cudaSuccess) {
@@ -318,14 +333,28 @@ void mirror_fill(lilac::marshal::DeferredRange* d) {
 void drop_mirror(std::map<std::uintptr_t, std::unique_ptr<Mirror>>::iterator it, bool fill = true) {
     lilac::marshal::retire_deferred(it->second->lazy, fill);
     lilac::marshal::drop_guard(it->second->reg);
-    g_mirror_total -= it->second->buf.cap;
-    it->second->buf.release();
+    g_mirror_total -= it->second->buf->cap;
     g_mirrors.erase(it);
+}
+
+// drop every mirror overlapping [h, h+bytes); lazy ones are filled unless the
+// range covers them (their bytes are superseded)
+void drop_overlapping(std::uintptr_t h, std::size_t bytes) {
+    for (auto it = g_mirrors.begin(); it != g_mirrors.end();) {
+        const std::uintptr_t lo = it->first, hi = lo + it->second->reg.ref.bytes;
+        if (lo < h + bytes && h < hi) {
+            auto nx = std::next(it);
+            drop_mirror(it, !(h <= lo && hi <= h + bytes));
+            it = nx;
+        } else {
+            ++it;
+        }
+    }
 }
 
 }  // namespace
 
-bool mirror_fetch(void* dev_dst, const void* host, std::size_t bytes, cudaStream_t s) {
+bool mirror_fetch(DevArray& d, const void* host, std::size_t bytes) {
     if (g_mirrors.empty()) return false;
     const auto h = reinterpret_cast<std::uintptr_t>(host);
     auto it = g_mirrors.upper_bound(h);
@@ -340,68 +369,60 @@ bool mirror_fetch(void* dev_dst, const void* host, std::size_t bytes, cudaStream
             return false;
         }
     }
-    PhaseTimer pt(kPhD2D);
-    B200_CUDA(cudaMemcpyAsync(dev_dst, m.buf.as<char>() + (h - it->first), bytes, cudaMemcpyDeviceToDevice, s));
+    // zero-copy: borrow the mirror's buffer (the device buffer d owned, if
+    // any, is kept for a later host upload)
+    d.lent = m.buf;
+    d.view = m.buf->as<const char>() + (h - it->first);
     return true;
 }
 
-void mirror_publish(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s) {
+void mirror_publish(const void* host, std::size_t bytes, DevBuf& src) {
     if (!mirrors_enabled() || bytes < kMirrorMin) return;
     const auto h = reinterpret_cast<std::uintptr_t>(host);
-    // drop every mirror overlapping the written range (stale now)
-    for (auto it = g_mirrors.begin(); it != g_mirrors.end();) {
-        const std::uintptr_t lo = it->first, hi = lo + it->second->reg.ref.bytes;
-        if (lo < h + bytes && h < hi) {
-            auto nx = std::next(it);
-            drop_mirror(it);
-            it = nx;
-        } else {
-            ++it;
-        }
-    }
+    drop_overlapping(h, bytes);  // stale now
     if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
     auto m = std::make_unique<Mirror>();
-    m->buf.ensure(bytes);
-    B200_CUDA(cudaMemcpyAsync(m->buf.ptr, dev_src, bytes, cudaMemcpyDeviceToDevice, s));
     m->reg.ref = {host, bytes, nullptr};
     m->reg.strategy = lilac::marshal::Strategy::Hybrid;
     try {
         PhaseTimer pt(kPhPublishGuard);
         lilac::marshal::mark_clean(m->reg);  // guard: a host write invalidates the mirror
     } catch (const Error&) {
-        m->buf.release();  // pages that cannot be protected get no mirror
-        return;
+        return;  // pages that cannot be protected get no mirror
     }
-    g_mirror_total += m->buf.cap;
+    m->buf = steal(src, bytes);
+    g_mirror_total += m->buf->cap;
     g_mirrors.emplace(h, std::move(m));
 }
 
-bool mirror_publish_lazy(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s) {
+bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src) {
     const auto h = reinterpret_cast<std::uintptr_t>(host);
     const std::size_t pg = lilac::marshal::page_size();
     if (!mirrors_enabled() || bytes < kMirrorMin || h % pg != 0) return false;
-    for (auto it = g_mirrors.begin(); it != g_mirrors.end();) {
-        const std::uintptr_t lo = it->first, hi = lo + it->second->reg.ref.bytes;
-        if (lo < h + bytes && h < hi) {
-            auto nx = std::next(it);
-            drop_mirror(it, !(h <= lo && hi <= h + bytes));
-            it = nx;
-        } else {
-            ++it;
-        }
+    auto same = g_mirrors.find(h);
+    if (same != g_mirrors.end() && same->second->reg.ref.bytes == bytes && same->second->lazy.active &&
+        lilac::marshal::reclean_covered(same->second->reg)) {
+        // steady state (rewritten before the host looked): swap in the new
+        // device bytes; pages stay PROT_NONE, no system call
+        Mirror& m = *same->second;
+        g_mirror_total -= m.buf->cap;
+        m.buf = steal(src, bytes);
+        g_mirror_total += m.buf->cap;
+        g_lazy_deferred += static_cast<std::int64_t>(bytes);
+        return true;
     }
+    drop_overlapping(h, bytes);
     if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
     auto m = std::make_unique<Mirror>();
-    m->buf.ensure(bytes);
-    B200_CUDA(cudaMemcpyAsync(m->buf.ptr, dev_src, bytes, cudaMemcpyDeviceToDevice, s));
     m->reg.ref = {host, bytes, nullptr};
-    m->reg.strategy = lilac::marshal::Strategy::PageProtect;  // whole pages: no edge hashing of lazy bytes
+    m->reg.strategy = lilac::marshal::Strategy::PageProtect;  // whole pages: no edge reads of lazy bytes
     m->lazy.lo = h;
     m->lazy.hi = (h + bytes + pg - 1) / pg * pg;
     m->lazy.content_lo = h;
     m->lazy.content_hi = h + bytes;
     m->lazy.fill = mirror_fill;
     m->lazy.ctx = m.get();
+    m->buf = steal(src, bytes);  // before defer_range: a fill needs the bytes
     try {
         PhaseTimer pt(kPhPublishGuard);
         lilac::marshal::mark_clean(m->reg);
@@ -409,11 +430,14 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, const void* dev_sr
     } catch (const Error&) {
         lilac::marshal::retire_deferred(m->lazy, false);
         lilac::marshal::drop_guard(m->reg);
-        m->buf.release();
-        return false;  // eager write-back instead
+        // give the bytes back to the caller for an eager write-back
+        src.release();
+        src = *m->buf;
+        const_cast<DevBuf&>(*m->buf) = DevBuf{};
+        return false;
     }
     g_lazy_deferred += static_cast<std::int64_t>(bytes);
-    g_mirror_total += m->buf.cap;
+    g_mirror_total += m->buf->cap;
     g_mirrors.emplace(h, std::move(m));
     return true;
 }

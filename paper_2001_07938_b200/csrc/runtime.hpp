@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdio>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -20,10 +21,23 @@ using lilac::marshal::Strategy;
 // device allocation plus the bytes this binding has moved.
 struct DevArray {
     DevBuf buf;
+    // An input served from a device mirror borrows the mirror's (immutable)
+    // buffer instead of copying it; the reference keeps it alive.
+    std::shared_ptr<const DevBuf> lent;
+    const char* view = nullptr;
     std::int64_t h2d = 0;
     std::int64_t d2h = 0;
     std::int64_t d2d = 0;  // bytes served from a device mirror instead of the host
     std::int64_t lazy = 0;  // write-back bytes left on the device (lazy mode)
+
+    // the device bytes of an input binding
+    template <typename T>
+    const T* data() const { return lent ? reinterpret_cast<const T*>(view) : buf.as<const T>(); }
+    void release() {
+        lent.reset();
+        view = nullptr;
+        buf.release();
+    }
 };
 
 struct HarnessStats {
@@ -105,18 +119,19 @@ inline void host_in(const void* p, std::size_t bytes) { lilac::marshal::material
 
 // upload: H2D, or D2D from a valid device mirror of the same host bytes.
 void upload(DevArray& d, const void* host, std::size_t bytes);
-// download: D2H write-back; then publishes a device mirror of the host region.
+// download: D2H write-back; then publishes a device mirror of the host region
+// (the mirror takes d's buffer; d gets a fresh one from the pool).
 // Lazy mode (page-aligned regions >= 8 KiB): no D2H — the mirror is published
 // with the host pages PROT_NONE, and the bytes land on first touch.
-void download(void* host, const DevArray& d, std::size_t bytes, DevArray& counter);
+void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter);
 
 // Device mirrors (the coherence layer of SURVEY §8(f)1): after a write-back the
 // device holds the exact bytes of the host region; the region is guarded like
 // a Hybrid marshal region, and while no host write touched it any later upload
 // of (a sub-range of) it is served device-to-device. LILAC_B200_MIRRORS=0 off.
-bool mirror_fetch(void* dev_dst, const void* host, std::size_t bytes, cudaStream_t s);
-void mirror_publish(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s);
-bool mirror_publish_lazy(const void* host, std::size_t bytes, const void* dev_src, cudaStream_t s);
+bool mirror_fetch(DevArray& d, const void* host, std::size_t bytes);
+void mirror_publish(const void* host, std::size_t bytes, DevBuf& src);
+bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src);
 void lazy_bytes(std::int64_t* deferred, std::int64_t* filled);
 void mirrors_clear();
 std::int64_t mirror_bytes();

@@ -46,7 +46,28 @@ def set_errors_return(on: bool = True):
     N.lib().b200_set_error_mode(1 if on else 0)
 
 
+def _ext():
+    """The CPython binding (csrc/pyext/harness_module.c) — same C-ABI calls
+    without ctypes' per-argument marshalling cost; None if not built."""
+    global _EXT
+    if _EXT is False:
+        try:
+            N.lib()  # loads liblilac_b200.so (and fails loudly if it is missing)
+            from . import _harness as E
+            E.set_error_class(B200Error)
+            _EXT = E
+        except ImportError:
+            _EXT = None
+    return _EXT
+
+
+_EXT = False
+
+
 def spmv_csr(rows, output, row_ptr, val, x, col_ind):
+    E = _ext()
+    if E is not None:
+        return E.spmv_csr(int(rows), output, row_ptr, val, x, col_ind)
     L = N.lib()
     L.b200_spmv_csr(int(rows), N.ptr(_f64(output, "output", True)), N.ptr(_i64(row_ptr, "row_ptr")),
                     N.ptr(_f64(val, "val")), N.ptr(_f64(x, "x")), N.ptr(_i64(col_ind, "col_ind")))
@@ -54,6 +75,9 @@ def spmv_csr(rows, output, row_ptr, val, x, col_ind):
 
 
 def spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind):
+    E = _ext()
+    if E is not None:
+        return E.spmv_jds(int(rows), output, nzcnt, perm, val, jd_ptr, x, col_ind)
     L = N.lib()
     L.b200_spmv_jds(int(rows), N.ptr(_f64(output, "output", True)), N.ptr(_i64(nzcnt, "nzcnt")),
                     N.ptr(_i64(perm, "perm")), N.ptr(_f64(val, "val")), N.ptr(_i64(jd_ptr, "jd_ptr")),
@@ -62,6 +86,9 @@ def spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind):
 
 
 def dotproduct(length, a, b) -> float:
+    E = _ext()
+    if E is not None:
+        return E.dotproduct(int(length), a, b)
     res = np.zeros(1, np.float64)
     N.lib().b200_dot(N.ptr(res), int(length), N.ptr(_f64(a, "a")), N.ptr(_f64(b, "b")))
     N.check()
@@ -69,11 +96,17 @@ def dotproduct(length, a, b) -> float:
 
 
 def axpy(n, y, alpha, x):
+    E = _ext()
+    if E is not None:
+        return E.axpy(int(n), y, float(alpha), x)
     N.lib().b200_axpy(int(n), N.ptr(_f64(y, "y", True)), float(alpha), N.ptr(_f64(x, "x")))
     N.check()
 
 
 def xpay(n, y, beta, x):
+    E = _ext()
+    if E is not None:
+        return E.xpay(int(n), y, float(beta), x)
     N.lib().b200_xpay(int(n), N.ptr(_f64(y, "y", True)), float(beta), N.ptr(_f64(x, "x")))
     N.check()
 

@@ -106,3 +106,28 @@ def test_no_cpu_fallback_without_gpu():
         assert np.all(y == 0)  # outputs untouched
     finally:
         H.set_errors_return(False)
+
+
+def test_python_binding_checks_arguments_before_calling():
+    """The CPython binding (csrc/pyext/harness_module.c) is built and rejects
+    wrong dtypes / layouts / read-only outputs without calling the library."""
+    import numpy as np
+    from paper_2001_07938_b200 import harness as H
+    E = H._ext()
+    assert E is not None, "paper_2001_07938_b200/_harness*.so not built"
+    rp = np.array([0, 1], np.int64)
+    ci = np.array([0], np.int64)
+    val = np.ones(1)
+    x = np.ones(1)
+    with pytest.raises(TypeError, match="output"):
+        H.spmv_csr(1, np.zeros(1, np.float32), rp, val, x, ci)
+    with pytest.raises(TypeError, match="row_ptr"):
+        H.spmv_csr(1, np.zeros(1), rp.astype(np.int32), val, x, ci)
+    with pytest.raises(TypeError, match="x"):
+        H.spmv_csr(1, np.zeros(1), rp, val, np.ones(4)[::2], ci)
+    ro = np.zeros(1)
+    ro.flags.writeable = False
+    with pytest.raises(TypeError, match="output"):
+        H.spmv_csr(1, ro, rp, val, x, ci)
+    with pytest.raises(TypeError, match="y"):
+        H.axpy(1, ro, 1.0, x)

@@ -11,6 +11,7 @@ from paper_2001_07938_b200 import harness as H  # noqa: E402
 
 N.check(N.lib().b200_init(0))
 cls = sys.argv[1] if len(sys.argv) > 1 else "C"
+mode = sys.argv[2] if len(sys.argv) > 2 else "eager"
 na, nonzer, niter, shift, _ = bench.NPB[cls]
 rp, ci, val = D.gen_npb(na, nonzer, shift)
 N.lib().b200_stats_reset()
@@ -26,7 +27,19 @@ def mc():
 
 m0 = mc()
 t0 = time.perf_counter()
-r = bench.e2e_harness_cg(rp, ci, val, na, shift, 3)
+bench.e2e_harness_cg(rp, ci, val, na, shift, 1, mode)  # warm (matrix upload)
+N.lib().b200_stats_reset()
+m0 = mc()
+r = bench.e2e_harness_cg(rp, ci, val, na, shift, 3, mode)
+print("lazy counters", H.lazy_counters())
+# Python-side cost of one wrapper call with the C work removed: time the
+# argument marshalling (ctypes pointers + error check) alone
+x = np.zeros(na)
+t = time.perf_counter()
+for _ in range(2000):
+    N.ptr(x), N.ptr(x), N.ptr(rp), N.ptr(val), N.ptr(ci)
+    N.check()
+print("python arg marshalling per spmv-shaped call: %.1f us" % ((time.perf_counter() - t) / 2000 * 1e6))
 print("e2e", {k: v for k, v in r.items() if k != "path"})
 print("faults, mprotects, hash_bytes, mirror_bytes delta:", (mc() - m0).tolist())
 ns = np.zeros(16, np.int64)
