@@ -104,8 +104,19 @@ void b200_set_exact_blas(int on);
  * before handing such a buffer to another library or to read()/write().
  * Also LILAC_B200_WRITEBACK=lazy. */
 int b200_set_writeback(const char* mode);
+/* Per-call profiling (host phase timers, kernel time via CUDA events in the
+ * harness stats). Off by default: it costs clock reads and two event records
+ * per call. Also LILAC_B200_PROFILE=1. */
+void b200_set_profiling(int on);
 /* Materialise lazy write-back bytes in [host, host+bytes) (NULL: all). */
 int b200_host_sync(const void* host, size_t bytes);
+/* The caller is about to free (or hand to an allocator) [host, host+bytes):
+ * drop every binding, device mirror, page guard and lazy range over it,
+ * without filling (NULL: everything). Guards and lazy pages must not outlive
+ * the memory they describe: a recycled buffer would otherwise be served stale
+ * device bytes or receive an old lazy fill. Call b200_host_sync first to
+ * keep the lazy bytes. */
+int b200_host_forget(const void* host, size_t bytes);
 /* Lazy write-back counters: ranges deferred, filled on a page fault, filled
  * explicitly (DMA reads, b200_host_sync, partial overwrites), cancelled by a
  * covering write-back, bytes deferred, bytes materialised. */

@@ -36,7 +36,9 @@ struct DevBuf {
     std::size_t cap = 0;    // allocated bytes
     int device = -1;
 
-    void ensure(std::size_t n);  // grow-only; contents not preserved
+    // grow-only; contents not preserved. zero_tail: clear the padding past n
+    // (index arrays: masked over-reads must stay in range)
+    void ensure(std::size_t n, bool zero_tail = true);
     void release();
     template <typename T>
     T* as() const { return static_cast<T*>(ptr); }
@@ -162,12 +164,24 @@ void launch_check_jds(const std::int64_t* nzcnt, const std::int64_t* jd_ptr, std
 
 // BLAS-1 companions (deterministic: fixed partition and fixed-order sums).
 int dot_parts_for(std::int64_t n);
-void launch_dot(const double* a, const double* b, std::int64_t n, double* result,
-                double* partials, unsigned int* ticket, cudaStream_t s);
-void launch_dot_exact(const double* a, const double* b, std::int64_t n, double* result,
-                      cudaStream_t s);
+// Host-mapped scalar slot: a reducing kernel also writes its result there and
+// then `seq` to `flag` (device pointers of pinned mapped memory), so the host
+// can spin on the flag instead of a D2H copy + stream sync. value==nullptr: off.
+struct HostSlot {
+    double* value = nullptr;
+    unsigned* flag = nullptr;
+    unsigned seq = 0;
+};
+void launch_dot(const double* a, const double* b, std::int64_t n, double* result, double* partials,
+                unsigned int* ticket, cudaStream_t s, HostSlot slot = {});
+void launch_dot_exact(const double* a, const double* b, std::int64_t n, double* result, cudaStream_t s,
+                      HostSlot slot = {});
 void launch_axpy(std::int64_t n, double* y, double alpha, const double* x, cudaStream_t s);
 void launch_xpay(std::int64_t n, double* y, double beta, const double* x, cudaStream_t s);
+// out-of-place forms (out may alias y): the harness writes its output binding
+// straight from the input binding's device bytes
+void launch_axpy_to(std::int64_t n, double* out, const double* y, double alpha, const double* x, cudaStream_t s);
+void launch_xpay_to(std::int64_t n, double* out, const double* y, double beta, const double* x, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // NPB CG device step kernels (cg.cu)

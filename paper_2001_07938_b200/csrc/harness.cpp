@@ -141,6 +141,10 @@ template <typename F>
 void timed_launch(HarnessStats& st, F&& launch) {
     PhaseTimer pt(kPhLaunch);
     Runtime& r = rt();
+    if (!g_profile) {
+        launch();
+        return;
+    }
     B200_CUDA(cudaEventRecord(r.ev_k0, r.stream));
     launch();
     B200_CUDA(cudaEventRecord(r.ev_k1, r.stream));
@@ -148,6 +152,7 @@ void timed_launch(HarnessStats& st, F&& launch) {
 }
 
 void collect_kernel_time(HarnessStats& st) {
+    if (!g_profile) return;
     Runtime& r = rt();
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, r.ev_k0, r.ev_k1) == cudaSuccess)
@@ -512,16 +517,26 @@ extern "C" void b200_dot(double* result, std::int64_t length, const double* a, c
         DevArray& da = oa.acquire(a, bytes, nullptr, B200Read_update, B200Read_destruct);
         // dot(r, r): one binding serves both operands
         DevArray& db = (b == a) ? da : ob.acquire(b, bytes, nullptr, B200Read_update, B200Read_destruct);
-        DevArray& dres = state.m_result.acquire_out(result, sizeof(*result), B200Write_construct, B200Write_update,
-                                                    B200Write_destruct);
+        // the kernel also posts the result to the pinned mapped slot; the
+        // write-back (B200Write's update) waits on it instead of D2H + sync
+        const HostSlot slot = rt().next_slot();
+        DevArray& dres = state.m_result.acquire_out(
+            result, sizeof(*result), B200Write_construct,
+            [seq = slot.seq](const void* in, std::size_t size, DevArray& out) {
+                const double v = wait_host_slot(seq);
+                std::memcpy(const_cast<void*>(in), &v, size < sizeof v ? size : sizeof v);
+                out.d2h += static_cast<std::int64_t>(sizeof v);
+            },
+            B200Write_destruct);
         tm.acquired();
         timed_launch(hs, [&] {
             Runtime& r = rt();
             if (r.exact_blas)
-                launch_dot_exact(da.data<double>(), db.data<double>(), length, dres.buf.as<double>(), r.stream);
+                launch_dot_exact(da.data<double>(), db.data<double>(), length, dres.buf.as<double>(), r.stream,
+                                 slot);
             else
                 launch_dot(da.data<double>(), db.data<double>(), length, dres.buf.as<double>(),
-                           r.partials.as<double>(), r.d_ticket(), r.stream);
+                           r.partials.as<double>(), r.d_ticket(), r.stream, slot);
         });
         tm.acquired();
         state.m_result.write_back();
@@ -541,26 +556,34 @@ void vec2_call(const char* name, std::int64_t n, double* y, double s, const doub
     Timer tm(hs);
     if (n < 0) throw Error(Errc::DataError, "n < 0");
     const std::size_t bytes = n * sizeof(double);
+    PhaseTimer pt_pick(kPhPick);
     auto& oy = state.m_y_in.pick(y, bytes);
     auto& ox = state.m_x.pick(x, bytes);
     auto& oo = state.m_y_out.pick(y, bytes);
     const std::int64_t h0 = state.m_y_in.sum(&DevArray::h2d) + state.m_x.sum(&DevArray::h2d),
                        d0 = state.m_y_out.sum(&DevArray::d2h),
                        dd0 = state.m_y_in.sum(&DevArray::d2d) + state.m_x.sum(&DevArray::d2d);
+    pt_pick.stop();
+    PhaseTimer pt_acq(kPhAcquire);
     DevArray& dy = oy.acquire(y, bytes, nullptr, B200Read_update, B200Read_destruct);
     DevArray& dx = ox.acquire(x, bytes, nullptr, B200Read_update, B200Read_destruct);
+    pt_acq.stop();
+    PhaseTimer pt_out(kPhAcquireOut);
     DevArray& dout = oo.acquire_out(y, bytes, B200Write_construct, B200Write_update, B200Write_destruct);
+    pt_out.stop();
     tm.acquired();
     timed_launch(hs, [&] {
         Runtime& r = rt();
-        if (n > 0)
-            B200_CUDA(cudaMemcpyAsync(dout.buf.ptr, dy.data<char>(), bytes, cudaMemcpyDeviceToDevice, r.stream));
         if (axpy)
-            launch_axpy(n, dout.buf.as<double>(), s, dx.data<double>(), r.stream);
+            launch_axpy_to(n, dout.buf.as<double>(), dy.data<double>(), s, dx.data<double>(), r.stream);
         else
-            launch_xpay(n, dout.buf.as<double>(), s, dx.data<double>(), r.stream);
+            launch_xpay_to(n, dout.buf.as<double>(), dy.data<double>(), s, dx.data<double>(), r.stream);
     });
     tm.acquired();
+    {
+        PhaseTimer pt(kPhNote);
+        lilac::marshal::note_host_write(y, bytes);  // (write_back repeats it; timed here)
+    }
     oo.write_back();
     collect_kernel_time(hs);
     tm.written_back();

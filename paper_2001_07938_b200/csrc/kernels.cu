@@ -356,9 +356,18 @@ __global__ void k_check_jds(const std::int64_t* __restrict__ nzcnt, const std::i
 
 // Deterministic dot: CTA b owns a fixed contiguous slice, threads stride it
 // with 16-byte loads, fixed-tree block sum, last CTA sums the partials in order.
+// Publishes a scalar result to host-mapped memory: value, system fence, then
+// the call's sequence number (the host spins on it instead of a D2H + sync).
+__device__ __forceinline__ void post_host(double v, HostSlot slot) {
+    if (!slot.value) return;
+    *reinterpret_cast<volatile double*>(slot.value) = v;
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned*>(slot.flag) = slot.seq;
+}
+
 __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ a, const double* __restrict__ b,
                                                   std::int64_t n, double* result, double* partials,
-                                                  unsigned int* ticket) {
+                                                  unsigned int* ticket, HostSlot slot) {
     const std::int64_t per = (n + gridDim.x - 1) / gridDim.x;
     const std::int64_t lo = min(n, per * blockIdx.x), hi = min(n, lo + per);
     double s = 0.0;
@@ -375,27 +384,28 @@ __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ a, 
     s = block_sum(s);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
     double total;
-    if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) *result = total;
+    if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) {
+        *result = total;
+        post_host(total, slot);
+    }
 }
 
 // Reference order, one thread: bit-identical to what_interp.cpp:97-101.
-__global__ void k_dot_exact(const double* a, const double* b, std::int64_t n, double* result) {
+__global__ void k_dot_exact(const double* a, const double* b, std::int64_t n, double* result, HostSlot slot) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     double acc = 0.0;
     for (std::int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, __dmul_rn(a[i], b[i]));
     *result = acc;
+    post_host(acc, slot);
 }
 
-__global__ void k_axpy(std::int64_t n, double* __restrict__ y, double alpha, const double* __restrict__ x) {
+// out = y + alpha*x (axpy) or out = x + beta*y (xpay); out may alias y (each
+// element is read before it is written by the same thread).
+template <bool XPAY>
+__global__ void k_vec2(std::int64_t n, double* out, const double* y, double s, const double* __restrict__ x) {
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));
-}
-
-__global__ void k_xpay(std::int64_t n, double* __restrict__ y, double beta, const double* __restrict__ x) {
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        y[i] = __dadd_rn(x[i], __dmul_rn(beta, y[i]));
+        out[i] = XPAY ? __dadd_rn(x[i], __dmul_rn(s, y[i])) : __dadd_rn(y[i], __dmul_rn(s, x[i]));
 }
 
 unsigned grid_for(std::int64_t threads, unsigned cap = kSMs * 16) {
@@ -574,25 +584,34 @@ int dot_parts_for(std::int64_t n) {
 }
 
 void launch_dot(const double* a, const double* b, std::int64_t n, double* result, double* partials,
-                unsigned int* ticket, cudaStream_t s) {
-    k_dot<<<dot_parts_for(n), kThreads, 0, s>>>(a, b, n, result, partials, ticket);
+                unsigned int* ticket, cudaStream_t s, HostSlot slot) {
+    k_dot<<<dot_parts_for(n), kThreads, 0, s>>>(a, b, n, result, partials, ticket, slot);
     B200_CUDA(cudaGetLastError());
 }
 
-void launch_dot_exact(const double* a, const double* b, std::int64_t n, double* result, cudaStream_t s) {
-    k_dot_exact<<<1, 32, 0, s>>>(a, b, n, result);
+void launch_dot_exact(const double* a, const double* b, std::int64_t n, double* result, cudaStream_t s,
+                      HostSlot slot) {
+    k_dot_exact<<<1, 32, 0, s>>>(a, b, n, result, slot);
     B200_CUDA(cudaGetLastError());
 }
 
 void launch_axpy(std::int64_t n, double* y, double alpha, const double* x, cudaStream_t s) {
-    if (n <= 0) return;
-    k_axpy<<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, y, alpha, x);
-    B200_CUDA(cudaGetLastError());
+    launch_axpy_to(n, y, y, alpha, x, s);
 }
 
 void launch_xpay(std::int64_t n, double* y, double beta, const double* x, cudaStream_t s) {
+    launch_xpay_to(n, y, y, beta, x, s);
+}
+
+void launch_axpy_to(std::int64_t n, double* out, const double* y, double alpha, const double* x, cudaStream_t s) {
     if (n <= 0) return;
-    k_xpay<<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, y, beta, x);
+    k_vec2<false><<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, out, y, alpha, x);
+    B200_CUDA(cudaGetLastError());
+}
+
+void launch_xpay_to(std::int64_t n, double* out, const double* y, double beta, const double* x, cudaStream_t s) {
+    if (n <= 0) return;
+    k_vec2<true><<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, out, y, beta, x);
     B200_CUDA(cudaGetLastError());
 }
 

@@ -13,11 +13,13 @@
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 #include <mutex>
 #include <vector>
 
 #include <signal.h>
 #include <sys/mman.h>
+#include <fcntl.h>
 #include <unistd.h>
 
 namespace lilac::marshal {
@@ -83,10 +85,41 @@ void reapply(std::uintptr_t lo, std::uintptr_t hi) {
 
 // Materialise one lazy range: open its pages, let the owner write the bytes,
 // then restore the guards' protections over them.
+const bool g_trace = std::getenv("LILAC_MARSHAL_TRACE") != nullptr;
+
+void trace(const char* what, std::uintptr_t a, std::uintptr_t b) {
+    if (!g_trace) return;
+    char buf[128];
+    const int n = std::snprintf(buf, sizeof buf, "[marshal] %s %#lx..%#lx\n", what, (unsigned long)a, (unsigned long)b);
+    if (n > 0) (void)!write(2, buf, static_cast<std::size_t>(n));
+}
+
+// Can the process read the byte at a? (A write(2) of it into a pipe fails
+// with EFAULT instead of faulting.) Normal context only.
+bool page_readable(std::uintptr_t a) {
+    static int fds[2] = {-1, -1};
+    if (fds[0] < 0 && pipe2(fds, O_NONBLOCK | O_CLOEXEC) != 0) return false;
+    if (write(fds[1], reinterpret_cast<const void*>(a), 1) != 1) return false;
+    char c;
+    (void)!read(fds[0], &c, 1);
+    return true;
+}
+
 void fill_one(DeferredRange& d, bool from_fault) {
-    mprotect(reinterpret_cast<void*>(d.lo), d.hi - d.lo, PROT_READ | PROT_WRITE);
+    trace(from_fault ? "fill(fault)" : "fill", d.lo, d.hi);
     d.active = false;
+    // A range is ours only while its pages are still PROT_NONE: memory freed
+    // and mapped again (readable) must not receive the old bytes.
+    if (!from_fault && (page_readable(d.lo) || page_readable(d.hi - 1))) {
+        trace("stale (remapped)", d.lo, d.hi);
+        return;
+    }
+    if (mprotect(reinterpret_cast<void*>(d.lo), d.hi - d.lo, PROT_READ | PROT_WRITE) != 0) {
+        trace("stale (unmapped)", d.lo, d.hi);
+        return;  // the memory is gone: nothing to fill
+    }
     if (d.fill) d.fill(&d);
+    trace("filled", d.lo, d.hi);
     if (from_fault)
         g_def_fault_fills = g_def_fault_fills + 1;
     else
@@ -102,7 +135,12 @@ bool page_deferred(std::uintptr_t page) {
 
 void on_fault(int sig, siginfo_t* si, void* uctx) {
     const auto addr = reinterpret_cast<std::uintptr_t>(si->si_addr);
+    trace("fault", addr, static_cast<std::uintptr_t>(si->si_code));
     const std::uintptr_t page = addr & ~(static_cast<std::uintptr_t>(g_page) - 1);
+    // only protection faults on mapped pages can be ours (an access to
+    // unmapped memory inside a stale range must crash, not loop)
+    if (si->si_code != SEGV_ACCERR) goto not_ours;
+    {
     // a touch of lazy bytes: materialise them; a write re-faults on the
     // restored guard and is recorded below
     bool filled = false;
@@ -126,9 +164,11 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
         // A region is dirty after its first trapped write: open its whole
         // guard range now (one fault per region per clean cycle instead of one
         // per page), then re-close pages still covered by a clean region.
+        bool opened = false;
         for (const Guard& g : g_guards)
             if (page < g.hi && page + g_page > g.lo)
-                mprotect(reinterpret_cast<void*>(g.lo), g.hi - g.lo, PROT_READ | PROT_WRITE);
+                opened |= mprotect(reinterpret_cast<void*>(g.lo), g.hi - g.lo, PROT_READ | PROT_WRITE) == 0;
+        if (!opened) goto not_ours;  // cannot lift it: re-executing would loop
         for (const Guard& g : g_guards) {
             if (g.region->dirty) continue;
             for (const Guard& h : g_guards) {
@@ -141,6 +181,8 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
             if (page < g.hi && page + g_page > g.lo) apply_deferred(g.lo, g.hi);
         return;
     }
+    }
+not_ours:
     // Not ours: hand the fault to whoever had SIGSEGV before us.
     if (g_prev_valid) {
         if (g_prev.sa_flags & SA_SIGINFO) {
@@ -603,6 +645,36 @@ Diagnostics release_all() {
     }
     Diagnostics d;
     for (MarshalObjectBase* o : live) o->force_release(d);
+    return d;
+}
+
+Diagnostics forget_range(const void* base, std::size_t bytes) {
+    Diagnostics d;
+    if (bytes == 0) return d;
+    const auto lo = reinterpret_cast<std::uintptr_t>(base);
+    const std::uintptr_t hi = lo + bytes;
+    std::vector<MarshalObjectBase*> hit;
+    {
+        std::lock_guard<std::mutex> lk(g_objects_mu);
+        for (MarshalObjectBase* o : g_objects) {
+            const auto rlo = reinterpret_cast<std::uintptr_t>(o->region_.ref.base);
+            if (o->constructed_ && rlo < hi && lo < rlo + o->region_.ref.bytes) hit.push_back(o);
+        }
+        g_objects.erase(std::remove_if(g_objects.begin(), g_objects.end(),
+                                       [&](MarshalObjectBase* o) {
+                                           return std::find(hit.begin(), hit.end(), o) != hit.end();
+                                       }),
+                        g_objects.end());
+    }
+    for (MarshalObjectBase* o : hit) o->force_release(d);
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (DeferredRange* r : g_deferred) {
+        if (r->active && r->content_lo < hi && lo < r->content_hi) {
+            r->active = false;
+            g_def_cancelled = g_def_cancelled + 1;
+            reapply(r->lo, r->hi);
+        }
+    }
     return d;
 }
 

@@ -12,8 +12,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <atomic>
+#include <sched.h>
 
 namespace b200 {
+
+bool g_profile = [] {
+    const char* e = std::getenv("LILAC_B200_PROFILE");
+    return e && std::strcmp(e, "1") == 0;
+}();
 
 namespace {
 std::int64_t g_phase_ns[kPhCount] = {};
@@ -87,7 +94,7 @@ std::size_t size_class(std::size_t n) {
 }
 }  // namespace
 
-void DevBuf::ensure(std::size_t n) {
+void DevBuf::ensure(std::size_t n, bool zero_tail) {
     if (ptr && cap >= n + kPadBytes) {
         bytes = n;
         return;
@@ -106,6 +113,7 @@ void DevBuf::ensure(std::size_t n) {
         }
     }
     if (!ptr) {
+        host_phase_add(kPhMalloc, 0);
         cudaError_t e = cudaMalloc(&ptr, want);
         if (e == cudaErrorMemoryAllocation && !g_pool.empty()) {
             (void)cudaGetLastError();
@@ -118,7 +126,7 @@ void DevBuf::ensure(std::size_t n) {
         }
     }
     // zero the tail so masked over-reads of index arrays stay in range
-    B200_CUDA(cudaMemsetAsync(static_cast<char*>(ptr) + n, 0, want - n, rt().stream));
+    if (zero_tail) B200_CUDA(cudaMemsetAsync(static_cast<char*>(ptr) + n, 0, want - n, rt().stream));
     cap = want;
     bytes = n;
     device = dev;
@@ -178,6 +186,17 @@ void ensure_init() {
     B200_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
     B200_CUDA(cudaEventCreate(&r.ev_k0));
     B200_CUDA(cudaEventCreate(&r.ev_k1));
+    {
+        void* h = nullptr;
+        B200_CUDA(cudaHostAlloc(&h, 128, cudaHostAllocMapped));
+        std::memset(h, 0, 128);
+        r.h_slot_val = static_cast<double*>(h);
+        r.h_slot_flag = reinterpret_cast<unsigned*>(static_cast<char*>(h) + 64);
+        void* d = nullptr;
+        B200_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+        r.dslot.value = static_cast<double*>(d);
+        r.dslot.flag = reinterpret_cast<unsigned*>(static_cast<char*>(d) + 64);
+    }
     r.inited = true;  // DevBuf::ensure below re-enters ensure_init
     r.partials.ensure(sizeof(double) * kMaxParts * 4);
     r.scalars.ensure(4096);
@@ -194,6 +213,26 @@ void ensure_init() {
     std::atexit(at_exit_teardown);
 }
 
+double wait_host_slot(unsigned seq) {
+    Runtime& r = rt();
+    volatile unsigned* flag = r.h_slot_flag;
+    for (unsigned long spin = 1;; ++spin) {
+        if (*flag == seq) break;
+        if ((spin & 1023) == 0) {
+            const cudaError_t e = cudaStreamQuery(r.stream);
+            if (e == cudaSuccess) {
+                if (*flag == seq) break;
+                throw Error(Errc::DeviceError, "result slot not posted by a completed kernel");
+            }
+            if (e != cudaErrorNotReady) throw_cuda(e, "cudaStreamQuery", __FILE__, __LINE__);
+            if (spin > (1ul << 20)) sched_yield();  // a long queue: stop burning the core
+        }
+        __builtin_ia32_pause();
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return *reinterpret_cast<volatile double*>(r.h_slot_val);
+}
+
 void shutdown() {
     Runtime& r = rt();
     lilac::marshal::release_all();
@@ -203,6 +242,10 @@ void shutdown() {
     r.scalars.release();
     r.flags.release();
     r.stage.release();
+    if (r.h_slot_val) cudaFreeHost(r.h_slot_val);
+    r.h_slot_val = nullptr;
+    r.h_slot_flag = nullptr;
+    r.dslot = HostSlot{};
     if (r.ev_k0) cudaEventDestroy(r.ev_k0);
     if (r.ev_k1) cudaEventDestroy(r.ev_k1);
     pool_trim();
@@ -301,9 +344,10 @@ bool mirrors_enabled() {
 // Take src's device allocation (no copy) as an immutable shared buffer; src
 // gets a fresh allocation of the same size from the pool.
 std::shared_ptr<const DevBuf> steal(DevBuf& src, std::size_t bytes) {
+    PhaseTimer pt(kPhSteal);
     auto* b = new DevBuf(src);
     src = DevBuf{};
-    src.ensure(bytes);
+    src.ensure(bytes, false);  // an f64 output: its padding is never indexed
     return std::shared_ptr<const DevBuf>(b, [](const DevBuf* p) {
         const_cast<DevBuf*>(p)->release();
         delete p;
@@ -447,6 +491,20 @@ void lazy_bytes(std::int64_t* deferred, std::int64_t* filled) {
     if (filled) *filled = g_lazy_filled;
 }
 
+void mirrors_forget(const void* host, std::size_t bytes) {
+    const auto h = reinterpret_cast<std::uintptr_t>(host);
+    for (auto it = g_mirrors.begin(); it != g_mirrors.end();) {
+        const std::uintptr_t lo = it->first, hi = lo + it->second->reg.ref.bytes;
+        auto nx = std::next(it);
+        if (lo < h + bytes && h < hi) drop_mirror(it, false);
+        it = nx;
+    }
+}
+
+void mirrors_drop_all() {
+    while (!g_mirrors.empty()) drop_mirror(g_mirrors.begin(), false);
+}
+
 void mirrors_clear() {
     while (!g_mirrors.empty()) drop_mirror(g_mirrors.begin());
 }
@@ -546,6 +604,8 @@ int b200_set_strategy(const char* name) {
 
 void b200_set_exact_blas(int on) { rt().exact_blas = on != 0; }
 
+void b200_set_profiling(int on) { g_profile = on != 0; }
+
 int b200_set_writeback(const char* mode) {
     return boundary("b200_set_writeback", [&] {
         const std::string m = mode ? mode : "";
@@ -564,6 +624,18 @@ int b200_host_sync(const void* host, size_t bytes) {
             lilac::marshal::materialize_range(host, bytes);
         else
             lilac::marshal::materialize_all();
+    });
+}
+
+int b200_host_forget(const void* host, size_t bytes) {
+    return boundary("b200_host_forget", [&] {
+        if (!host) {
+            lilac::marshal::release_all();
+            mirrors_drop_all();
+            return;
+        }
+        mirrors_forget(host, bytes);
+        lilac::marshal::forget_range(host, bytes);
     });
 }
 

@@ -60,6 +60,17 @@ struct Runtime {
     bool lazy_writeback = false;  // LILAC_B200_WRITEBACK=lazy / b200_set_writeback
     std::size_t stage_bytes = std::size_t(256) << 20;  // chunk for narrowing uploads
     DevBuf stage;
+    // pinned, device-mapped scalar result slot (dot results; HostSlot)
+    double* h_slot_val = nullptr;
+    unsigned* h_slot_flag = nullptr;
+    HostSlot dslot;  // device pointers of the same
+    unsigned slot_seq = 0;
+
+    HostSlot next_slot() {
+        HostSlot s = dslot;
+        s.seq = ++slot_seq;
+        return s;
+    }
 
     unsigned int* d_ticket() const { return scalars.as<unsigned int>(); }
     double* d_result() const { return reinterpret_cast<double*>(scalars.as<char>() + 64); }
@@ -69,6 +80,9 @@ struct Runtime {
 
 Runtime& rt();
 void ensure_init();  // lazy first-call init + atexit teardown
+// Spin until the kernel that was given HostSlot seq `seq` posted its value
+// (checking the stream for errors now and then); returns the value.
+double wait_host_slot(unsigned seq);
 void shutdown();
 
 // Region stats registry (harness objects + their transfer counters).
@@ -133,7 +147,9 @@ bool mirror_fetch(DevArray& d, const void* host, std::size_t bytes);
 void mirror_publish(const void* host, std::size_t bytes, DevBuf& src);
 bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src);
 void lazy_bytes(std::int64_t* deferred, std::int64_t* filled);
-void mirrors_clear();
+void mirrors_clear();                                    // lazy bytes filled first
+void mirrors_forget(const void* host, std::size_t bytes);  // the caller frees it: no fill
+void mirrors_drop_all();
 std::int64_t mirror_bytes();
 
 // Resident CSR / JDS uploads shared by the harnesses and the device API.
@@ -152,13 +168,23 @@ using Clock = std::chrono::steady_clock;
 
 // Host-side phase accumulators (ns), read by b200_host_profile().
 enum HostPhase { kPhMirrorFetch, kPhMirrorPoll, kPhD2D, kPhH2D, kPhD2H, kPhPublish, kPhPublishGuard,
-                 kPhAcquire, kPhLaunch, kPhCount };
+                 kPhAcquire, kPhLaunch, kPhPick, kPhAcquireOut, kPhSteal, kPhNote, kPhMalloc, kPhCount };
+// Phase timers and per-call kernel events cost clock reads and CUDA API calls
+// on every harness call: off unless LILAC_B200_PROFILE=1 / b200_set_profiling.
+extern bool g_profile;
 void host_phase_add(int ph, std::int64_t ns);
 struct PhaseTimer {
     int ph;
-    Clock::time_point t0 = Clock::now();
-    explicit PhaseTimer(int p) : ph(p) {}
-    ~PhaseTimer() { host_phase_add(ph, std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count()); }
+    Clock::time_point t0;
+    explicit PhaseTimer(int p) : ph(g_profile ? p : -1) {
+        if (ph >= 0) t0 = Clock::now();
+    }
+    void stop() {
+        if (ph < 0) return;
+        host_phase_add(ph, std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+        ph = -1;
+    }
+    ~PhaseTimer() { stop(); }
 };
 inline double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();

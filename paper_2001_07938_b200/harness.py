@@ -16,13 +16,15 @@ by liblilac_b200.so: every call goes through the C ABI (no CPU path).
 """
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 
 from . import _native as N
 
 __all__ = ["spmv_csr", "spmv_jds", "dotproduct", "axpy", "xpay", "HarnessRegistry",
            "register_b200_harnesses", "region_stats", "harness_stats", "B200Error", "set_errors_return",
-           "set_writeback", "host_sync", "lazy_counters", "page_aligned"]
+           "set_writeback", "host_sync", "host_forget", "lazy_counters", "page_aligned"]
 
 B200Error = N.B200Error
 
@@ -126,6 +128,15 @@ def host_sync(a=None):
         N.check(N.lib().b200_host_sync(N.ptr(a), a.nbytes))
 
 
+def host_forget(a=None):
+    """Drop every binding / mirror / guard / lazy range over `a` (all when
+    None) before its memory is freed or recycled (include/lilac_b200.h)."""
+    if a is None:
+        N.check(N.lib().b200_host_forget(None, 0))
+    else:
+        N.check(N.lib().b200_host_forget(N.ptr(a), a.nbytes))
+
+
 def lazy_counters():
     import ctypes as C
     v = [C.c_int64() for _ in range(6)]
@@ -140,8 +151,21 @@ def page_aligned(n, dtype=np.float64):
     import mmap
     dt = np.dtype(dtype)
     nbytes = max(int(n) * dt.itemsize, 1)
-    buf = mmap.mmap(-1, (nbytes + mmap.PAGESIZE - 1) // mmap.PAGESIZE * mmap.PAGESIZE)
-    return np.frombuffer(buf, dtype=dt, count=int(n))
+    size = (nbytes + mmap.PAGESIZE - 1) // mmap.PAGESIZE * mmap.PAGESIZE
+    buf = mmap.mmap(-1, size)
+    a = np.frombuffer(buf, dtype=dt, count=int(n))
+    # unmapped when the last view dies: forget it first (no stale guard or
+    # lazy fill may outlive the mapping)
+    addr = a.ctypes.data
+    weakref.finalize(buf, _forget_addr, addr, size)
+    return a
+
+
+def _forget_addr(addr, size):
+    try:
+        N.lib().b200_host_forget(addr, size)
+    except Exception:  # interpreter teardown
+        pass
 
 
 class HarnessRegistry:

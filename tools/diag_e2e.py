@@ -10,6 +10,12 @@ from paper_2001_07938_b200 import device as D  # noqa: E402
 from paper_2001_07938_b200 import harness as H  # noqa: E402
 
 N.check(N.lib().b200_init(0))
+PROFILE = os.environ.get("DIAG_PROFILE", "1") == "1"
+N.lib().b200_set_profiling(1 if PROFILE else 0)
+t = time.perf_counter()
+for _ in range(100000):
+    time.perf_counter_ns()
+print("clock read: %.3f us" % ((time.perf_counter() - t) / 100000 * 1e6))
 cls = sys.argv[1] if len(sys.argv) > 1 else "C"
 mode = sys.argv[2] if len(sys.argv) > 2 else "eager"
 na, nonzer, niter, shift, _ = bench.NPB[cls]
@@ -39,13 +45,23 @@ t = time.perf_counter()
 for _ in range(2000):
     N.ptr(x), N.ptr(x), N.ptr(rp), N.ptr(val), N.ptr(ci)
     N.check()
-print("python arg marshalling per spmv-shaped call: %.1f us" % ((time.perf_counter() - t) / 2000 * 1e6))
+print("ctypes arg marshalling per spmv-shaped call: %.1f us" % ((time.perf_counter() - t) / 2000 * 1e6))
+E = H._ext()
+bad = np.zeros(na, np.float32)
+t = time.perf_counter()
+for _ in range(2000):
+    try:
+        E.axpy(na, bad, 1.0, x)  # rejected at argument checking: binding cost alone
+    except TypeError:
+        pass
+print("binding call + type error per call: %.2f us" % ((time.perf_counter() - t) / 2000 * 1e6))
 print("e2e", {k: v for k, v in r.items() if k != "path"})
 print("faults, mprotects, hash_bytes, mirror_bytes delta:", (mc() - m0).tolist())
 ns = np.zeros(16, np.int64)
 cnt = np.zeros(16, np.int64)
 k = N.lib().b200_host_profile(N.ptr(ns), N.ptr(cnt), 16)
-names = ["mirror_fetch", "mirror_poll", "d2d", "h2d", "d2h+sync", "publish", "publish_guard", "acquire", "launch"]
+names = ["mirror_fetch", "mirror_poll", "d2d", "h2d", "d2h+sync", "publish", "publish_guard", "acquire(vec2 in)",
+         "launch", "pick(vec2)", "acquire_out(vec2)", "steal", "note_write(vec2)", "cudaMalloc"]
 for i in range(k):
     print(f"  {names[i]:14s} n={cnt[i]:7d} total={ns[i]/1e6:9.2f} ms mean={ns[i]/max(cnt[i],1)/1e3:8.1f} us")
 for name, s in H.harness_stats().items():
