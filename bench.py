@@ -430,7 +430,7 @@ def run_ours(args):
     spmv_flops = 2 * snnz
     peak, peak_src = measured_peak()
     achieved = spmv_bytes / (spmv_ms * 1e-3) / 1e9
-    kname = {1: "k_csr_vector", 2: "k_spmv_merge", 3: "k_csr_exact", 4: "k_spmv_tiled"}.get(info["kernel"], "k_csr_vector")
+    kname = {1: "k_csr_vector", 2: "k_spmv_merge", 3: "k_csr_exact", 4: "k_spmv_tiled", 5: "k_csr_chunks"}.get(info["kernel"], "k_csr_vector")
     traffic = ncu_traffic(kname)
 
     line = {

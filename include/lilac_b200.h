@@ -85,8 +85,9 @@ const char* b200_last_error(void);
  * "DeviceError", ...) or "" when the last call succeeded. */
 const char* b200_last_error_code(void);
 /* CSR kernel policy, applied at the next matrix upload: "auto" (tiled for
- * poor x locality, merge for skewed rows, else vector) | "vector" | "tiled" |
- * "merge" | "exact" (bit-identical to the reference). Also LILAC_B200_KERNEL.
+ * poor x locality, split for skewed rows, else vector) | "vector" | "tiled" |
+ * "split" | "merge" | "exact" (bit-identical to the reference). Also
+ * LILAC_B200_KERNEL.
  * Returns 0 or -1. */
 int b200_set_kernel(const char* name);
 /* Change-detection strategy for harness objects created afterwards:
@@ -177,7 +178,7 @@ typedef struct {
     int64_t rows, cols, nnz, max_row;
     int32_t format;        /* 0 CSR, 1 JDS */
     int32_t col_bytes;     /* device col_ind width: 4 (narrowed) or 8 */
-    int32_t kernel;        /* CSR kernel chosen: 1 vector, 2 merge, 3 exact, 4 tiled */
+    int32_t kernel;        /* CSR kernel chosen: 1 vector, 2 merge, 3 exact, 4 tiled, 5 split */
     int32_t lanes;         /* vector kernel lanes per row */
     int64_t device_bytes;  /* resident bytes */
 } b200_matrix_info;

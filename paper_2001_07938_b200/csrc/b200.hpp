@@ -49,7 +49,7 @@ void pool_trim();  // return every cached block to CUDA
 // Resident sparse matrices (device layout)
 // ---------------------------------------------------------------------------
 
-enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3, Tiled = 4 };
+enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3, Tiled = 4, Split = 5 };
 const char* csr_kernel_name(CsrKernel k);
 CsrKernel parse_csr_kernel(const std::string& s);
 
@@ -87,6 +87,20 @@ struct MergeDev {
     double* carry_val = nullptr;              // nctas
 };
 
+// Split plan (split.cu) for skewed rows: rows longer than short_max leave the
+// vector kernel and are cut into chunks of <= kSplitChunk nonzeros, one warp
+// each; chunk partials are summed per row in chunk order (deterministic).
+constexpr std::int64_t kSplitChunk = 2048;
+struct SplitDev {
+    std::int64_t short_max = 0;            // longest row the vector kernel keeps
+    std::int64_t nlong = 0, nchunks = 0;
+    const std::int64_t* long_rows = nullptr;  // nlong
+    const std::int64_t* long_first = nullptr; // nlong + 1: first chunk of each long row
+    const std::int64_t* chunk_lo = nullptr;   // nchunks: absolute nonzero range
+    const std::int64_t* chunk_hi = nullptr;
+    double* partial = nullptr;                // nchunks
+};
+
 struct CsrDev {
     std::int64_t rows = 0;      // number of rows computed
     std::int64_t nnz = 0;       // extent of val/col (row_ptr[rows] for the ABI)
@@ -99,6 +113,7 @@ struct CsrDev {
     bool monotone = true;                   // row_ptr non-decreasing
     const TcsrDev* tiled = nullptr;         // present when the tiled layout was built
     const MergeDev* merge = nullptr;        // present when the merge plan was built
+    const SplitDev* split = nullptr;        // present when the split plan was built
 };
 
 struct JdsDev {
@@ -130,6 +145,11 @@ std::int64_t merge_ctas(std::int64_t rows, std::int64_t nnz);
 void launch_merge_plan(const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz, std::int64_t* coord_row,
                        std::int64_t* coord_nz, cudaStream_t s);
 void launch_spmv_merge(const CsrDev& A, const double* x, double* y, cudaStream_t s);
+// vector kernel over the rows of length <= max_len (longer rows untouched)
+void launch_csr_vector_short(const CsrDev& A, const double* x, double* y, std::int64_t max_len, cudaStream_t s);
+// Split kernels (split.cu): vector kernel on short rows + warp-per-chunk on long
+// rows + per-row chunk sums.
+void launch_spmv_split(const CsrDev& A, const double* x, double* y, cudaStream_t s);
 // p.q of a finished SpMV into the CG scalars (alpha, or the shard partial).
 void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, double* partials, unsigned int* ticket,
                            CgScalars* sc, cudaStream_t s);

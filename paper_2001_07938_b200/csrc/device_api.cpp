@@ -20,6 +20,7 @@ struct b200_matrix {
     JdsDev jds;
     TcsrOwner tiled;
     MergeOwner merge;
+    SplitOwner split;
     std::int64_t max_row = 0;
 };
 
@@ -65,6 +66,7 @@ int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int6
         d.monotone = monotone;
         A->max_row = max_row;
         if (A->tiled.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel)) d.tiled = &A->tiled.dev;
+        if (!d.tiled && A->split.refresh(d, row_ptr, rt().kernel)) d.split = &A->split.dev;
         if (!d.tiled && A->merge.refresh(d, row_ptr, rt().kernel)) d.merge = &A->merge.dev;
         *out = A.release();
     });
@@ -145,6 +147,7 @@ void b200_matrix_free(b200_matrix* A) {
     A->jd_ptr.release();
     A->tiled.release();
     A->merge.release();
+    A->split.release();
     delete A;
 }
 

@@ -35,6 +35,7 @@ struct Shard {
     CsrDev A;
     TcsrOwner tiled;
     MergeOwner merge;
+    SplitOwner split;
     DevBuf x, q, r, p_full, z_full, partials, scalars, gathered;
     CgVectors v{};
 
@@ -43,6 +44,7 @@ struct Shard {
             b->release();
         tiled.release();
         merge.release();
+        split.release();
     }
 };
 
@@ -92,8 +94,9 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
     if (s.tiled.refresh(rows, lrp.data(), ci + base, val + base, n, monotone, max_row, rt().kernel)) {
         s.tiled.dev.cols = n;
         A.tiled = &s.tiled.dev;
-    } else if (s.merge.refresh(A, lrp.data(), rt().kernel)) {
-        A.merge = &s.merge.dev;
+    } else {
+        if (s.split.refresh(A, lrp.data(), rt().kernel)) A.split = &s.split.dev;
+        if (s.merge.refresh(A, lrp.data(), rt().kernel)) A.merge = &s.merge.dev;
     }
     const std::size_t own = sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(rows, 1));
     for (DevBuf* b : {&s.x, &s.q, &s.r}) b->ensure(own);

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
                                                          double* __restrict__ y,
                                                          double* __restrict__ partials,
                                                          unsigned int* ticket, CgScalars* sc,
-                                                         std::int64_t dot_off) {
+                                                         std::int64_t dot_off, std::int64_t max_len) {
     const int lane = threadIdx.x & (S - 1);
     const unsigned gmask =
         S == 32 ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31) & ~(S - 1)));
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
     for (std::int64_t row = (static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x) / S;
          row < rows; row += groups) {
         const std::int64_t start = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
+        if (end - start > max_len) continue;  // a long row of the split plan: chunked elsewhere
         double acc = 0.0;
         for (std::int64_t jb = (start & ~std::int64_t(1)) + 2 * lane; jb < end; jb += 2 * S * U) {
             double2 v[U];
@@ -415,20 +416,21 @@ unsigned grid_for(std::int64_t threads, unsigned cap = kSMs * 16) {
 
 template <int S, typename IdxT, bool DOT>
 void vector_launch(const CsrDev& A, const double* x, double* y, double* partials, unsigned* ticket,
-                   CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
+                   CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off, std::int64_t max_len) {
     k_csr_vector<S, 2, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
-                                                            A.val, x, y, partials, ticket, sc, dot_off);
+                                                            A.val, x, y, partials, ticket, sc, dot_off, max_len);
 }
 
 template <typename IdxT, bool DOT>
 void vector_dispatch(const CsrDev& A, int S, const double* x, double* y, double* partials, unsigned* ticket,
-                     CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off = 0) {
+                     CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off = 0,
+                     std::int64_t max_len = INT64_MAX) {
     switch (S) {
-    case 2: vector_launch<2, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 4: vector_launch<4, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 8: vector_launch<8, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    case 16: vector_launch<16, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
-    default: vector_launch<32, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 2: vector_launch<2, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off, max_len); break;
+    case 4: vector_launch<4, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off, max_len); break;
+    case 8: vector_launch<8, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off, max_len); break;
+    case 16: vector_launch<16, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off, max_len); break;
+    default: vector_launch<32, IdxT, DOT>(A, x, y, partials, ticket, sc, grid, s, dot_off, max_len); break;
     }
 }
 
@@ -443,6 +445,7 @@ const char* csr_kernel_name(CsrKernel k) {
     case CsrKernel::Merge: return "merge";
     case CsrKernel::Exact: return "exact";
     case CsrKernel::Tiled: return "tiled";
+    case CsrKernel::Split: return "split";
     }
     return "?";
 }
@@ -451,6 +454,7 @@ CsrKernel parse_csr_kernel(const std::string& s) {
     if (s.empty() || s == "auto") return CsrKernel::Auto;
     if (s == "vector") return CsrKernel::Vector;
     if (s == "merge") return CsrKernel::Merge;
+    if (s == "split") return CsrKernel::Split;
     if (s == "exact") return CsrKernel::Exact;
     if (s == "tiled") return CsrKernel::Tiled;
     throw Error(Errc::DataError, "unknown CSR kernel '" + s + "' (auto, vector, tiled, exact)");
@@ -468,16 +472,27 @@ CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested) {
     if (requested == CsrKernel::Exact) return CsrKernel::Exact;
     if (requested == CsrKernel::Vector) return CsrKernel::Vector;
     if (requested == CsrKernel::Merge) return A.merge ? CsrKernel::Merge : CsrKernel::Vector;
+    if (requested == CsrKernel::Split) return A.split ? CsrKernel::Split : CsrKernel::Vector;
     if (requested == CsrKernel::Tiled) return A.tiled ? CsrKernel::Tiled : CsrKernel::Vector;
     // Auto: the derived layouts exist only when they were judged to pay at
     // upload (tcsr_wanted / merge_wanted)
     if (A.tiled) return CsrKernel::Tiled;
+    if (A.split) return CsrKernel::Split;
     if (A.merge) return CsrKernel::Merge;
     return CsrKernel::Vector;
 }
 
 static unsigned vector_grid(const CsrDev& A, int S) {
     return grid_for(A.rows * static_cast<std::int64_t>(S), kSMs * 8 * 4);
+}
+
+void launch_csr_vector_short(const CsrDev& A, const double* x, double* y, std::int64_t max_len, cudaStream_t s) {
+    const int S = csr_vector_width(A);
+    const unsigned g = vector_grid(A, S);
+    if (A.col32)
+        vector_dispatch<std::int32_t, false>(A, S, x, y, nullptr, nullptr, nullptr, g, s, 0, max_len);
+    else
+        vector_dispatch<std::int64_t, false>(A, S, x, y, nullptr, nullptr, nullptr, g, s, 0, max_len);
 }
 
 void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s) {
@@ -489,6 +504,10 @@ void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, c
     }
     if (k == CsrKernel::Merge) {
         launch_spmv_merge(A, x, y, s);
+        return;
+    }
+    if (k == CsrKernel::Split) {
+        launch_spmv_split(A, x, y, s);
         return;
     }
     if (k == CsrKernel::Exact) {
@@ -514,8 +533,11 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
         launch_spmv_tiled(*A.tiled, A.rows, p, q, partials, ticket, sc, s, dot_off);
         return;
     }
-    if (A.merge) {  // rows finish only after the carry fix-up: dot in its own pass
-        launch_spmv_merge(A, p, q, s);
+    if (A.split || A.merge) {  // rows finish only after the fix-up: dot in its own pass
+        if (A.split)
+            launch_spmv_split(A, p, q, s);
+        else
+            launch_spmv_merge(A, p, q, s);
         launch_cg_dot_scalars(p + dot_off, q, A.rows, partials, ticket, sc, s);
         return;
     }

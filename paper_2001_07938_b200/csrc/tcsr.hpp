@@ -51,4 +51,14 @@ struct MergeOwner {
     void release();
 };
 
+// Split plan owner (split.cu). Built from the caller's row_ptr for monotone
+// matrices with skewed rows (the merge_wanted test) or when forced.
+struct SplitOwner {
+    DevBuf long_rows, long_first, chunk_lo, chunk_hi, partial;
+    SplitDev dev;
+    bool valid = false;
+    bool refresh(const CsrDev& A, const std::int64_t* row_ptr_host, CsrKernel policy);
+    void release();
+};
+
 }  // namespace b200

@@ -228,9 +228,10 @@ bool merge_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, boo
 
 bool MergeOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel policy) {
     const std::int64_t nnz = A.rows > 0 ? rp[A.rows] - rp[0] : 0;
+    // built on request only: for Auto the split plan serves skewed matrices
+    // (faster on the Kronecker operator)
     const bool forced = policy == CsrKernel::Merge;
-    if (policy == CsrKernel::Vector || policy == CsrKernel::Exact || policy == CsrKernel::Tiled ||
-        !merge_wanted(A.rows, nnz, A.max_row, A.monotone, forced)) {
+    if (!forced || !merge_wanted(A.rows, nnz, A.max_row, A.monotone, forced)) {
         release();
         return false;
     }
@@ -248,6 +249,61 @@ bool MergeOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel poli
     dev.carry_val = carry_val.as<double>();
     valid = true;
     return true;
+}
+
+bool SplitOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel policy) {
+    const std::int64_t nnz = A.rows > 0 ? rp[A.rows] - rp[0] : 0;
+    const bool forced = policy == CsrKernel::Split;
+    if ((policy != CsrKernel::Auto && !forced) || !merge_wanted(A.rows, nnz, A.max_row, A.monotone, forced)) {
+        release();
+        return false;
+    }
+    // rows longer than 8 vector-kernel steps of the chosen width go to chunks
+    const std::int64_t short_max = std::max<std::int64_t>(64, 32 * csr_vector_width(A));
+    std::vector<std::int64_t> lrows, lfirst, clo, chi;
+    for (std::int64_t r = 0; r < A.rows; ++r) {
+        const std::int64_t a = rp[r], b = rp[r + 1];
+        if (b - a <= short_max) continue;
+        lrows.push_back(r);
+        lfirst.push_back(static_cast<std::int64_t>(clo.size()));
+        for (std::int64_t c = a; c < b; c += kSplitChunk) {
+            clo.push_back(c);
+            chi.push_back(std::min(b, c + kSplitChunk));
+        }
+    }
+    lfirst.push_back(static_cast<std::int64_t>(clo.size()));
+    auto put = [](DevBuf& d, const std::vector<std::int64_t>& h) {
+        d.ensure(sizeof(std::int64_t) * std::max<std::size_t>(h.size(), 1));
+        if (!h.empty())
+            B200_CUDA(cudaMemcpyAsync(d.ptr, h.data(), h.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice,
+                                      rt().stream));
+    };
+    put(long_rows, lrows);
+    put(long_first, lfirst);
+    put(chunk_lo, clo);
+    put(chunk_hi, chi);
+    partial.ensure(sizeof(double) * std::max<std::size_t>(clo.size(), 1));
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
+    dev.short_max = short_max;
+    dev.nlong = static_cast<std::int64_t>(lrows.size());
+    dev.nchunks = static_cast<std::int64_t>(clo.size());
+    dev.long_rows = long_rows.as<std::int64_t>();
+    dev.long_first = long_first.as<std::int64_t>();
+    dev.chunk_lo = chunk_lo.as<std::int64_t>();
+    dev.chunk_hi = chunk_hi.as<std::int64_t>();
+    dev.partial = partial.as<double>();
+    valid = true;
+    return true;
+}
+
+void SplitOwner::release() {
+    long_rows.release();
+    long_first.release();
+    chunk_lo.release();
+    chunk_hi.release();
+    partial.release();
+    dev = SplitDev{};
+    valid = false;
 }
 
 void MergeOwner::release() {

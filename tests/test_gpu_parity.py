@@ -89,6 +89,14 @@ def test_golden_csr_merge_within_tolerance(name, case):
 
 
 @pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_golden_csr_split_within_tolerance(name, case):
+    c = O.case_arrays(case)
+    N.lib().b200_set_kernel(b"split")
+    y = run_csr(c["row_ptr"], c["col_ind"], c["val"], c["x"])
+    assert_within(y, c["y_csr"], spmv_bound(c["row_ptr"], c["col_ind"], c["val"], c["x"]))
+
+
+@pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
 def test_golden_jds_bitwise(name, case):
     c = O.case_arrays(case)
     y = np.full(c["rows"], np.nan)
@@ -156,7 +164,7 @@ def test_random_csr_vs_oracle(shape):
     y_ref = O.spmv_csr(rp, ci, val, x)
     y = run_csr(rp, ci, val, x)
     assert_within(y, y_ref, spmv_bound(rp, ci, val, x))
-    for kernel in (b"vector", b"tiled", b"merge"):
+    for kernel in (b"vector", b"tiled", b"merge", b"split"):
         N.lib().b200_set_kernel(kernel)
         assert_within(run_csr(rp, ci, val, x), y_ref, spmv_bound(rp, ci, val, x))
     N.lib().b200_set_kernel(b"exact")
@@ -279,7 +287,7 @@ def test_resident_matrix_moves_only_vectors():
 # --------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("cls,kernel", [("S", b"auto"), ("A", b"auto"), ("A", b"tiled"), ("A", b"vector"),
-                                        ("A", b"merge"), ("C", b"auto"), ("C", b"vector")])
+                                        ("A", b"merge"), ("A", b"split"), ("C", b"auto"), ("C", b"vector")])
 def test_npb_cg_zeta_device_driver(cls, kernel):
     na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
     rp, ci, val = D.gen_npb(na, nonzer, shift)
@@ -415,10 +423,11 @@ def test_device_mirrors_serve_written_back_vectors_and_never_go_stale():
         assert abs(r - O.dot(y, y)) <= 1e-12 * O.dot(y, y), idx
 
 
-def test_power_law_rows_choose_merge_and_match():
+def test_power_law_rows_choose_split_and_match():
     """Kronecker-like skew (one row of 200k nonzeros among short rows): the
-    auto policy builds the merge-path plan; result within tolerance and
-    deterministic (bit-identical across calls)."""
+    auto policy builds the split plan (long rows in warp chunks); the forced
+    merge-path kernel agrees; results within tolerance and deterministic
+    (bit-identical across calls)."""
     rng = np.random.default_rng(99)
     n = 300000
     lens = np.minimum(rng.zipf(2.0, n), 200000).astype(np.int64)
@@ -428,9 +437,13 @@ def test_power_law_rows_choose_merge_and_match():
     val = rng.uniform(-1, 1, int(rp[-1]))
     x = rng.uniform(-1, 1, n)
     A = D.Matrix.csr(rp, ci, val)
-    assert A.info()["kernel"] == 2  # merge
+    assert A.info()["kernel"] == 5  # split
     A.free()
-    y1 = run_csr(rp, ci, val, x)
-    y2 = run_csr(rp, ci, val, x)
-    assert O.same_bits(y1, y2)
-    assert_within(y1, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
+    y_ref = O.spmv_csr(rp, ci, val, x)
+    bound = spmv_bound(rp, ci, val, x)
+    for kernel in (b"auto", b"merge"):
+        N.lib().b200_set_kernel(kernel)
+        y1 = run_csr(rp, ci, val, x)
+        y2 = run_csr(rp, ci, val, x)
+        assert O.same_bits(y1, y2)
+        assert_within(y1, y_ref, bound)

@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 from paper_2001_07938_b200 import _native as N  # noqa: E402
 from paper_2001_07938_b200 import device as D  # noqa: E402
 
-KERN = {1: "vector", 2: "merge", 3: "exact", 4: "tiled", 0: "jds"}
+KERN = {1: "vector", 2: "merge", 3: "exact", 4: "tiled", 5: "split", 0: "jds"}
 
 
 def peak():
