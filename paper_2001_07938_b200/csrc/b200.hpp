@@ -94,11 +94,15 @@ constexpr std::int64_t kSplitChunk = 2048;
 struct SplitDev {
     std::int64_t short_max = 0;            // longest row the vector kernel keeps
     std::int64_t nlong = 0, nchunks = 0;
+    std::int64_t nnz_short = 0;            // nonzeros in the short rows
     const std::int64_t* long_rows = nullptr;  // nlong
     const std::int64_t* long_first = nullptr; // nlong + 1: first chunk of each long row
     const std::int64_t* chunk_lo = nullptr;   // nchunks: absolute nonzero range
     const std::int64_t* chunk_hi = nullptr;
+    const std::int64_t* chunk_row = nullptr;  // nchunks: index into long_rows
     double* partial = nullptr;                // nchunks
+    unsigned* done = nullptr;                 // nlong: chunks finished this call (reset by the last)
+    unsigned long long* work = nullptr;       // work-unit counter (zeroed before each launch)
 };
 
 struct CsrDev {
@@ -145,10 +149,7 @@ std::int64_t merge_ctas(std::int64_t rows, std::int64_t nnz);
 void launch_merge_plan(const std::int64_t* row_ptr, std::int64_t rows, std::int64_t nnz, std::int64_t* coord_row,
                        std::int64_t* coord_nz, cudaStream_t s);
 void launch_spmv_merge(const CsrDev& A, const double* x, double* y, cudaStream_t s);
-// vector kernel over the rows of length <= max_len (longer rows untouched)
-void launch_csr_vector_short(const CsrDev& A, const double* x, double* y, std::int64_t max_len, cudaStream_t s);
-// Split kernels (split.cu): vector kernel on short rows + warp-per-chunk on long
-// rows + per-row chunk sums.
+// Split kernel (kernels.cu): vector rows + warp-per-chunk long rows in one launch.
 void launch_spmv_split(const CsrDev& A, const double* x, double* y, cudaStream_t s);
 // p.q of a finished SpMV into the CG scalars (alpha, or the shard partial).
 void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, double* partials, unsigned int* ticket,

@@ -62,6 +62,37 @@ __device__ __forceinline__ std::uint64_t make_evict_first() {
     return pol;
 }
 
+__device__ __forceinline__ std::uint64_t make_evict_last() {
+    std::uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ long long ld_stream_col(const std::int32_t* p, std::uint64_t pol) {
+    int v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ long long ld_stream_col(const std::int64_t* p, std::uint64_t pol) {
+    long long v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ double ld_stream_val(const double* p, std::uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// x gathers: keep x in L2 (evict_last)
+__device__ __forceinline__ double ld_gather(const double* p, std::uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ double warp_sum(double v, unsigned mask = 0xffffffffu) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
@@ -110,6 +141,53 @@ __device__ __forceinline__ bool last_cta_sum(double* partials, unsigned int* tic
 // step (one 16-byte val load, one 8/16-byte col load) and U steps are issued
 // before any x gather is consumed. Row starts are rounded down to an even
 // index so every vector load is aligned; the out-of-row elements are masked.
+// One row's partial sum on one lane of an S-lane group: each lane consumes 2
+// consecutive nonzeros per step (one 16-byte val load, one 8/16-byte col load)
+// and U steps are issued before any x gather is consumed. The row start is
+// rounded down to an even index so every vector load is aligned; the
+// out-of-row elements are masked. The caller reduces over the group.
+template <int S, int U, typename IdxT>
+__device__ __forceinline__ double vector_row(std::int64_t start, std::int64_t end, int lane,
+                                             const IdxT* __restrict__ col, const double* __restrict__ val,
+                                             const double* __restrict__ x, std::uint64_t pol) {
+    double acc = 0.0;
+    for (std::int64_t jb = (start & ~std::int64_t(1)) + 2 * lane; jb < end; jb += 2 * S * U) {
+        double2 v[U];
+        Idx2 c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const std::int64_t j = jb + 2 * S * u;
+            if (j < end) {
+                v[u] = ld_stream_ef(val + j, pol);
+                c[u] = ld_stream_idx(col + j, pol);
+            } else {
+                v[u] = make_double2(0.0, 0.0);
+                c[u] = {0, 0};
+            }
+        }
+        double xa[U], xb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const std::int64_t j = jb + 2 * S * u;
+            xa[u] = (j < end && j >= start) ? __ldg(x + c[u].a) : 0.0;
+            xb[u] = (j + 1 < end) ? __ldg(x + c[u].b) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            acc += v[u].x * xa[u];
+            acc += v[u].y * xb[u];
+        }
+    }
+    return acc;
+}
+
+template <int S>
+__device__ __forceinline__ unsigned group_mask() {
+    return S == 32 ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31) & ~(S - 1)));
+}
+
+// S lanes cooperate on a row (vector_row). Rows longer than max_len are left
+// to the split plan's chunk path.
 template <int S, int U, typename IdxT, bool DOT>
 __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
                                                          const std::int64_t* __restrict__ row_ptr,
@@ -121,8 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
                                                          unsigned int* ticket, CgScalars* sc,
                                                          std::int64_t dot_off, std::int64_t max_len) {
     const int lane = threadIdx.x & (S - 1);
-    const unsigned gmask =
-        S == 32 ? 0xffffffffu : (((1u << S) - 1u) << ((threadIdx.x & 31) & ~(S - 1)));
+    const unsigned gmask = group_mask<S>();
     const std::int64_t groups = static_cast<std::int64_t>(gridDim.x) * (kThreads / S);
     const std::uint64_t pol = make_evict_first();
     double pq = 0.0;
@@ -130,34 +207,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
          row < rows; row += groups) {
         const std::int64_t start = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
         if (end - start > max_len) continue;  // a long row of the split plan: chunked elsewhere
-        double acc = 0.0;
-        for (std::int64_t jb = (start & ~std::int64_t(1)) + 2 * lane; jb < end; jb += 2 * S * U) {
-            double2 v[U];
-            Idx2 c[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const std::int64_t j = jb + 2 * S * u;
-                if (j < end) {
-                    v[u] = ld_stream_ef(val + j, pol);
-                    c[u] = ld_stream_idx(col + j, pol);
-                } else {
-                    v[u] = make_double2(0.0, 0.0);
-                    c[u] = {0, 0};
-                }
-            }
-            double xa[U], xb[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const std::int64_t j = jb + 2 * S * u;
-                xa[u] = (j < end && j >= start) ? __ldg(x + c[u].a) : 0.0;
-                xb[u] = (j + 1 < end) ? __ldg(x + c[u].b) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                acc += v[u].x * xa[u];
-                acc += v[u].y * xb[u];
-            }
-        }
+        double acc = vector_row<S, U>(start, end, lane, col, val, x, pol);
 #pragma unroll
         for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
         if (lane == 0) {
@@ -178,6 +228,84 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
                 sc->alpha = sc->rho / total;
             }
         }
+    }
+}
+
+// ---- split kernel (skewed rows) -------------------------------------------------
+//
+// One launch; warps pull work units from a global counter: first the chunks of
+// the long rows (<= kSplitChunk nonzeros each, 8 loads in flight per lane),
+// then blocks of short rows walked as the vector kernel does. The warp that
+// completes a long row's last chunk sums the row's partials in chunk order
+// (deterministic) and stores y. Why not merge-path alone: on the Kronecker
+// scale-22 operator it is bound by shared-memory latency (binary searches, the
+// sequential merge walk) at 0.92 ms.
+constexpr int kChunkU = 8;
+constexpr int kShortPasses = 8;  // short-row unit: 8 passes of the warp's 32/S row groups
+
+template <int S, typename IdxT>
+__global__ void __launch_bounds__(kThreads) k_csr_split(std::int64_t rows, const std::int64_t* __restrict__ row_ptr,
+                                                        const IdxT* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ x, double* __restrict__ y,
+                                                        SplitDev P, unsigned long long* work) {
+    constexpr std::int64_t kRowsPerUnit = kShortPasses * (32 / S);
+    const int lane = threadIdx.x & 31;
+    const std::uint64_t pol = make_evict_first(), pgather = make_evict_last();
+    const std::int64_t short_units = (rows + kRowsPerUnit - 1) / kRowsPerUnit;
+    for (;;) {
+        std::int64_t u = 0;
+        if (lane == 0) u = static_cast<std::int64_t>(atomicAdd(work, 1ull));
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= P.nchunks + short_units) return;
+        if (u >= P.nchunks) {  // a block of short rows
+            const std::int64_t r0 = (u - P.nchunks) * kRowsPerUnit;
+            const int glane = lane & (S - 1);
+            const unsigned gmask = group_mask<S>();
+            for (std::int64_t row = r0 + lane / S; row < r0 + kRowsPerUnit && row < rows; row += 32 / S) {
+                const std::int64_t start = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
+                if (end - start > P.short_max) continue;
+                double acc = vector_row<S, 2>(start, end, glane, col, val, x, pol);
+#pragma unroll
+                for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
+                if (glane == 0) y[row] = acc;
+            }
+            continue;
+        }
+        const std::int64_t lo = __ldg(P.chunk_lo + u), hi = __ldg(P.chunk_hi + u);
+        double acc = 0.0;
+        for (std::int64_t jb = lo + lane; jb < hi; jb += 32 * kChunkU) {
+            long long cc[kChunkU];
+            double vv[kChunkU];
+#pragma unroll
+            for (int k = 0; k < kChunkU; ++k) {
+                const std::int64_t j = jb + 32 * k;
+                cc[k] = j < hi ? ld_stream_col(col + j, pol) : 0;
+                vv[k] = j < hi ? ld_stream_val(val + j, pol) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < kChunkU; ++k)
+                if (jb + 32 * k < hi) acc += vv[k] * ld_gather(x + cc[k], pgather);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const std::int64_t i = __ldg(P.chunk_row + u);
+            const std::int64_t f0 = __ldg(P.long_first + i), f1 = __ldg(P.long_first + i + 1);
+            if (f1 - f0 == 1) {
+                y[__ldg(P.long_rows + i)] = acc;
+            } else {
+                P.partial[u] = acc;
+                __threadfence();
+                if (atomicAdd(P.done + i, 1u) == static_cast<unsigned>(f1 - f0 - 1)) {
+                    __threadfence();
+                    double sum = 0.0;
+                    for (std::int64_t k = f0; k < f1; ++k) sum += __ldcg(P.partial + k);
+                    y[__ldg(P.long_rows + i)] = sum;
+                    P.done[i] = 0u;  // ready for the next call
+                }
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -486,13 +614,40 @@ static unsigned vector_grid(const CsrDev& A, int S) {
     return grid_for(A.rows * static_cast<std::int64_t>(S), kSMs * 8 * 4);
 }
 
-void launch_csr_vector_short(const CsrDev& A, const double* x, double* y, std::int64_t max_len, cudaStream_t s) {
+template <int S, typename IdxT>
+void split_launch(const CsrDev& A, const double* x, double* y, cudaStream_t s) {
+    const SplitDev& P = *A.split;
+    static unsigned per_sm = 0;
+    if (!per_sm) {
+        int b = 0;
+        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_csr_split<S, IdxT>, kThreads, 0));
+        per_sm = static_cast<unsigned>(std::max(b, 1));
+    }
+    // one resident wave of warps pulling work units; the counter restarts per call
+    B200_CUDA(cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), s));
+    k_csr_split<S, IdxT><<<kSMs * per_sm, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
+                                                            A.val, x, y, P, P.work);
+}
+
+template <typename IdxT>
+void split_dispatch(const CsrDev& A, int S, const double* x, double* y, cudaStream_t s) {
+    switch (S) {
+    case 2: split_launch<2, IdxT>(A, x, y, s); break;
+    case 4: split_launch<4, IdxT>(A, x, y, s); break;
+    case 8: split_launch<8, IdxT>(A, x, y, s); break;
+    case 16: split_launch<16, IdxT>(A, x, y, s); break;
+    default: split_launch<32, IdxT>(A, x, y, s); break;
+    }
+}
+
+void launch_spmv_split(const CsrDev& A, const double* x, double* y, cudaStream_t s) {
+    if (A.rows <= 0) return;
     const int S = csr_vector_width(A);
-    const unsigned g = vector_grid(A, S);
     if (A.col32)
-        vector_dispatch<std::int32_t, false>(A, S, x, y, nullptr, nullptr, nullptr, g, s, 0, max_len);
+        split_dispatch<std::int32_t>(A, S, x, y, s);
     else
-        vector_dispatch<std::int64_t, false>(A, S, x, y, nullptr, nullptr, nullptr, g, s, 0, max_len);
+        split_dispatch<std::int64_t>(A, S, x, y, s);
+    B200_CUDA(cudaGetLastError());
 }
 
 void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, cudaStream_t s) {

@@ -58,6 +58,20 @@ volatile long g_def_n = 0, g_def_fault_fills = 0, g_def_explicit_fills = 0, g_de
 struct sigaction g_prev;
 bool g_prev_valid = false;
 
+// mprotect(RW) over [lo, hi). A stale range over memory the caller freed may
+// contain unmapped holes (a trimmed heap); mprotect then fails as a whole at
+// the first hole and leaves the pages after it protected with no guard left to
+// claim their faults — so fall back to page by page. Returns whether any page
+// is mapped. Async-signal-safe.
+bool open_pages(std::uintptr_t lo, std::uintptr_t hi) {
+    if (hi <= lo) return true;
+    if (mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ | PROT_WRITE) == 0) return true;
+    bool any = false;
+    for (std::uintptr_t p = lo; p < hi; p += g_page)
+        any |= mprotect(reinterpret_cast<void*>(p), g_page, PROT_READ | PROT_WRITE) == 0;
+    return any;
+}
+
 // Close the parts of [lo, hi) covered by an active lazy range (PROT_NONE).
 void apply_deferred(std::uintptr_t lo, std::uintptr_t hi) {
     for (std::size_t i = 0; i < g_deferred.size(); ++i) {
@@ -74,7 +88,7 @@ void apply_deferred(std::uintptr_t lo, std::uintptr_t hi) {
 void reapply(std::uintptr_t lo, std::uintptr_t hi) {
     if (hi <= lo) return;
     g_stat_mprotect = g_stat_mprotect + 1;
-    mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ | PROT_WRITE);
+    open_pages(lo, hi);
     for (const Guard& g : g_guards) {
         if (g.region->dirty) continue;
         const std::uintptr_t a = lo > g.lo ? lo : g.lo, b = hi < g.hi ? hi : g.hi;
@@ -164,11 +178,10 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
         // A region is dirty after its first trapped write: open its whole
         // guard range now (one fault per region per clean cycle instead of one
         // per page), then re-close pages still covered by a clean region.
-        bool opened = false;
         for (const Guard& g : g_guards)
-            if (page < g.hi && page + g_page > g.lo)
-                opened |= mprotect(reinterpret_cast<void*>(g.lo), g.hi - g.lo, PROT_READ | PROT_WRITE) == 0;
-        if (!opened) goto not_ours;  // cannot lift it: re-executing would loop
+            if (page < g.hi && page + g_page > g.lo) open_pages(g.lo, g.hi);
+        // the faulting page itself must end writable, or re-executing loops
+        if (mprotect(reinterpret_cast<void*>(page), g_page, PROT_READ | PROT_WRITE) != 0) goto not_ours;
         for (const Guard& g : g_guards) {
             if (g.region->dirty) continue;
             for (const Guard& h : g_guards) {
@@ -183,6 +196,7 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
     }
     }
 not_ours:
+    trace("not ours", addr, static_cast<std::uintptr_t>(g_guards.size()));
     // Not ours: hand the fault to whoever had SIGSEGV before us.
     if (g_prev_valid) {
         if (g_prev.sa_flags & SA_SIGINFO) {
@@ -221,8 +235,11 @@ std::uintptr_t ceil_page(std::uintptr_t a) { return floor_page(a + page_size() -
 
 void protect(std::uintptr_t lo, std::uintptr_t hi) {
     g_stat_mprotect = g_stat_mprotect + 1;
-    if (hi > lo && mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ) != 0)
-        throw Error(Errc::ProtectionUnsupported, std::string("mprotect failed: ") + std::strerror(errno));
+    if (hi > lo && mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ) != 0) {
+        const int err = errno;
+        open_pages(lo, hi);  // undo a partial protection: no guard will own it
+        throw Error(Errc::ProtectionUnsupported, std::string("mprotect failed: ") + std::strerror(err));
+    }
 }
 
 // Unprotect [lo,hi), then re-protect the parts still covered by a clean
@@ -230,7 +247,7 @@ void protect(std::uintptr_t lo, std::uintptr_t hi) {
 void release_pages(std::uintptr_t lo, std::uintptr_t hi, const TrackedRegion* except) {
     if (hi <= lo) return;
     g_stat_mprotect = g_stat_mprotect + 1;
-    mprotect(reinterpret_cast<void*>(lo), hi - lo, PROT_READ | PROT_WRITE);
+    open_pages(lo, hi);
     for (const Guard& g : g_guards) {
         if (g.region == except || g.region->dirty) continue;
         std::uintptr_t a = std::max(lo, g.lo), b = std::min(hi, g.hi);
@@ -474,7 +491,7 @@ void note_host_write(const void* base, std::size_t bytes) {
     }
     if (guarded && !covered_by_deferred(plo, phi)) {
         g_stat_mprotect = g_stat_mprotect + 1;
-        mprotect(reinterpret_cast<void*>(plo), phi - plo, PROT_READ | PROT_WRITE);
+        open_pages(plo, phi);
         apply_deferred(plo, phi);
     }
 }

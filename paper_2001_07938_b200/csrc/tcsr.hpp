@@ -54,7 +54,7 @@ struct MergeOwner {
 // Split plan owner (split.cu). Built from the caller's row_ptr for monotone
 // matrices with skewed rows (the merge_wanted test) or when forced.
 struct SplitOwner {
-    DevBuf long_rows, long_first, chunk_lo, chunk_hi, partial;
+    DevBuf long_rows, long_first, chunk_lo, chunk_hi, chunk_row, partial, done, work;
     SplitDev dev;
     bool valid = false;
     bool refresh(const CsrDev& A, const std::int64_t* row_ptr_host, CsrKernel policy);

@@ -260,16 +260,21 @@ bool SplitOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel poli
     }
     // rows longer than 8 vector-kernel steps of the chosen width go to chunks
     const std::int64_t short_max = std::max<std::int64_t>(64, 32 * csr_vector_width(A));
-    std::vector<std::int64_t> lrows, lfirst, clo, chi;
+    std::vector<std::int64_t> lrows, lfirst, clo, chi, crow;
+    std::int64_t nnz_short = 0;
     for (std::int64_t r = 0; r < A.rows; ++r) {
         const std::int64_t a = rp[r], b = rp[r + 1];
-        if (b - a <= short_max) continue;
-        lrows.push_back(r);
+        if (b - a <= short_max) {
+            nnz_short += std::max<std::int64_t>(b - a, 0);
+            continue;
+        }
         lfirst.push_back(static_cast<std::int64_t>(clo.size()));
         for (std::int64_t c = a; c < b; c += kSplitChunk) {
             clo.push_back(c);
             chi.push_back(std::min(b, c + kSplitChunk));
+            crow.push_back(static_cast<std::int64_t>(lrows.size()));
         }
+        lrows.push_back(r);
     }
     lfirst.push_back(static_cast<std::int64_t>(clo.size()));
     auto put = [](DevBuf& d, const std::vector<std::int64_t>& h) {
@@ -282,7 +287,11 @@ bool SplitOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel poli
     put(long_first, lfirst);
     put(chunk_lo, clo);
     put(chunk_hi, chi);
+    put(chunk_row, crow);
     partial.ensure(sizeof(double) * std::max<std::size_t>(clo.size(), 1));
+    done.ensure(sizeof(unsigned) * std::max<std::size_t>(lrows.size(), 1));
+    work.ensure(sizeof(unsigned long long));
+    B200_CUDA(cudaMemsetAsync(done.ptr, 0, sizeof(unsigned) * std::max<std::size_t>(lrows.size(), 1), rt().stream));
     B200_CUDA(cudaStreamSynchronize(rt().stream));
     dev.short_max = short_max;
     dev.nlong = static_cast<std::int64_t>(lrows.size());
@@ -291,7 +300,11 @@ bool SplitOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel poli
     dev.long_first = long_first.as<std::int64_t>();
     dev.chunk_lo = chunk_lo.as<std::int64_t>();
     dev.chunk_hi = chunk_hi.as<std::int64_t>();
+    dev.chunk_row = chunk_row.as<std::int64_t>();
     dev.partial = partial.as<double>();
+    dev.done = done.as<unsigned>();
+    dev.work = work.as<unsigned long long>();
+    dev.nnz_short = nnz_short;
     valid = true;
     return true;
 }
@@ -301,7 +314,10 @@ void SplitOwner::release() {
     long_first.release();
     chunk_lo.release();
     chunk_hi.release();
+    chunk_row.release();
     partial.release();
+    done.release();
+    work.release();
     dev = SplitDev{};
     valid = false;
 }
