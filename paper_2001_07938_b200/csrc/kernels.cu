@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kSMs = 148;
+constexpr int kJdsU = 16;  // JDS diagonals in flight per thread
 
 // ---- load helpers -----------------------------------------------------------
 
@@ -342,19 +343,22 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
         const std::int64_t len = __ldg(nzcnt + j);
         double acc = 0.0;
         std::int64_t k = 0;
-        // 4 diagonals' loads in flight, accumulated in the reference k order
-        for (; k + 4 <= len; k += 4) {
-            std::int64_t off[4];
-            double v[4], xv[4];
+        // kJdsU diagonals in flight: all val/col loads of the group, then all x
+        // gathers, then the sums in the reference k order (two memory round
+        // trips per group; the longest jagged rows set the kernel time)
+        for (; k + kJdsU <= len; k += kJdsU) {
+            double v[kJdsU], xv[kJdsU];
+            long long c[kJdsU];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) off[u] = __ldg(jd_ptr + k + u) + j;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off[u]));
-                xv[u] = __ldg(x + static_cast<std::int64_t>(__ldg(col + off[u])));
+            for (int u = 0; u < kJdsU; ++u) {
+                const std::int64_t off = __ldg(jd_ptr + k + u) + j;
+                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
+                c[u] = static_cast<long long>(__ldg(col + off));
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+            for (int u = 0; u < kJdsU; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
         }
         for (; k < len; ++k) {
             const std::int64_t off = __ldg(jd_ptr + k) + j;
