@@ -177,53 +177,82 @@ def ncu_traffic(kernel_substr: str):
 # reference CPU harness (oracle/_ref) — the baseline arm
 # ------------------------------------------------------------------------------------
 
-def reference_sample(rp, ci, val, n, reps=1, row_frac=8):
-    """Times the reference's own HarnessFn ("lilac.spmv_csr", interp.cpp:330-389)
-    on the first rows/row_frac rows (a bounded sample of the SpMV) and
-    "lilac.dotproduct" on full-length vectors. Returns (seconds per NPB
-    iteration extrapolated, kind, sample description)."""
+def host_threads():
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def reference_sample(rp, ci, val, n, reps=1, row_frac=1, threads=None):
+    """Times the reference's own HarnessFns ("lilac.spmv_csr" /
+    "lilac.dotproduct", interp.cpp:330-389) on `threads` host threads: the
+    rows [0, n/row_frac) are cut into nnz-balanced slices, each slice a separate
+    HarnessFn call on its own interpreter Memory, run concurrently (the
+    interpreter has no shared mutable state; ctypes releases the GIL); the
+    dot products likewise by element slices. Returns (seconds per NPB
+    iteration, kind, sample description, seconds per full SpMV, threads)."""
+    import threading
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as O
+    T = threads or host_threads()
     rows_s = max(1, n // row_frac)
-    nnz_s = int(rp[rows_s])
+    nnz_s = int(rp[rows_s] - rp[0])
     x = np.ones(n)
+    bounds = [0]
+    for t in range(1, T):
+        bounds.append(max(bounds[-1], int(np.searchsorted(rp[: rows_s + 1], rp[0] + nnz_s * t // T))))
+    bounds.append(rows_s)
+    ebounds = [n * t // T for t in range(T + 1)]
     if O.ref_available():
         R = O.ref()
         kind = "reference"
-        h = R.ref_prepare_csr(rows_s, O.ptr(rp), O.ptr(val), O.ptr(x), O.ptr(ci), nnz_s, n)
-        hd = R.ref_prepare_dot(n, O.ptr(x), O.ptr(x))
-        call = lambda hh: R.ref_call(hh)  # noqa: E731
-        free = R.ref_free
+        keep = []
+        hs, hd = [], []
+        for t in range(T):
+            r0, r1 = bounds[t], bounds[t + 1]
+            a, b = int(rp[r0]), int(rp[r1])
+            rpt = np.ascontiguousarray(rp[r0:r1 + 1] - rp[r0])
+            cit, vt = np.ascontiguousarray(ci[a:b]), np.ascontiguousarray(val[a:b])
+            keep += [rpt, cit, vt]
+            hs.append(R.ref_prepare_csr(r1 - r0, O.ptr(rpt), O.ptr(vt), O.ptr(x), O.ptr(cit), b - a, n))
+            e0, e1 = ebounds[t], ebounds[t + 1]
+            xs = np.ascontiguousarray(x[e0:e1])
+            keep.append(xs)
+            hd.append(R.ref_prepare_dot(e1 - e0, O.ptr(xs), O.ptr(xs)))
+
+        def run(handles):
+            th = [threading.Thread(target=lambda h=h: R.ref_call(h)) for h in handles]
+            t0 = time.perf_counter()
+            for t_ in th:
+                t_.start()
+            for t_ in th:
+                t_.join()
+            return time.perf_counter() - t0
     else:
         kind = "port"
-        h = hd = None
-        free = None
-    t_spmv = []
-    t_dot = []
+        hs = hd = None
+
+        def run(handles):
+            t0 = time.perf_counter()
+            O.spmv_csr_mt(rp[: rows_s + 1], ci[:nnz_s], val[:nnz_s], x, T) if handles == "spmv" else O.dot(x, x)
+            return time.perf_counter() - t0
+    t_spmv, t_dot = [], []
     for _ in range(reps):
-        t0 = time.perf_counter()
-        if h is not None:
-            assert call(h) == 0
-        else:
-            O.spmv_csr(rp[: rows_s + 1], ci[:nnz_s], val[:nnz_s], x)
-        t_spmv.append(time.perf_counter() - t0)
-        t0 = time.perf_counter()
-        if hd is not None:
-            assert call(hd) == 0
-        else:
-            O.dot(x, x)
-        t_dot.append(time.perf_counter() - t0)
-    if free:
-        free(h)
-        free(hd)
-    ts = min(t_spmv) * (int(rp[n]) / max(nnz_s, 1))
+        t_spmv.append(run(hs if hs is not None else "spmv"))
+        t_dot.append(run(hd if hd is not None else "dot"))
+    if hs is not None:
+        for h in hs + hd:
+            R.ref_free(h)
+    ts = min(t_spmv) * (int(rp[n] - rp[0]) / max(nnz_s, 1))
     td = min(t_dot)
     dots_per_iter = 2 * CGITMAX + 3
     t_iter = SPMV_PER_STEP * ts + dots_per_iter * td
-    desc = (f"{'lilac.spmv_csr HarnessFn (oracle/_ref)' if kind == 'reference' else 'oracle port'} on rows "
-            f"[0,{rows_s}) ({nnz_s} nnz) scaled to nnz={int(rp[n])}, x{SPMV_PER_STEP} SpMV + "
-            f"{dots_per_iter} full-length dotproduct calls per NPB iteration; host CG vector updates not counted")
-    return t_iter, kind, desc, ts
+    desc = (f"{'lilac.spmv_csr/lilac.dotproduct HarnessFns (oracle/_ref)' if kind == 'reference' else 'oracle port'}"
+            f" on {T} host threads (nnz-balanced row slices, one interpreter Memory each), rows [0,{rows_s}) "
+            f"({nnz_s} nnz) of nnz={int(rp[n] - rp[0])}; x{SPMV_PER_STEP} SpMV + {dots_per_iter} full-length dots "
+            f"per NPB iteration; host CG vector updates not counted")
+    return t_iter, kind, desc, ts, T
 
 
 def run_reference(args):
@@ -236,7 +265,7 @@ def run_reference(args):
     rp, ci, val = O.npb_makea(na, nonzer, shift)
     steps = []
     for i in range(args.warmup + args.steps):
-        t_iter, kind, desc, _ = reference_sample(rp, ci, val, na, reps=1)
+        t_iter, kind, desc, _, threads = reference_sample(rp, ci, val, na, reps=1)
         if i >= args.warmup:
             steps.append(t_iter)
     ms = statistics.mean(steps) * 1e3
@@ -248,7 +277,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (NPB makea)",
         "config": {"workload": f"NPB CG class {args.npb_class} (n={na}, nnz={int(rp[-1])}) SpMV harness path",
                    "sample": desc},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": desc,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc,
                          "cpu": model, "host_cpus": ncpu},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -463,9 +492,9 @@ def run_ours(args):
         line["e2e"], other = (lazy, eager) if lazy["value"] >= eager["value"] else (eager, lazy)
         line["e2e_" + other["writeback"]] = other
         if not args.no_cpu_baseline:
-            t_iter, kind, desc, ts = reference_sample(rp, ci, val, na, reps=2)
+            t_iter, kind, desc, ts, threads = reference_sample(rp, ci, val, na, reps=2)
             model, ncpu = cpu_desc()
-            line["cpu_baseline"] = {"value": 1.0 / t_iter, "unit": UNIT, "cores": 1, "kind": kind,
+            line["cpu_baseline"] = {"value": 1.0 / t_iter, "unit": UNIT, "cores": threads, "kind": kind,
                                     "sample": desc, "cpu": model, "host_cpus": ncpu,
                                     "spmv_s": ts}
     elif rank == 0:
