@@ -198,6 +198,17 @@ int b200_spmv_device(const b200_matrix* A, const double* x_device, double* y_dev
 int b200_dot_device(const double* a_device, const double* b_device, int64_t n,
                     double* result_device, void* stream);
 int b200_axpy_device(int64_t n, double* y_device, double alpha, const double* x_device, void* stream);
+/* The 27-point stencil operator on an nx^3 grid (SURVEY §8(d) input 5),
+ * generated directly in HBM: rows in lexicographic (i, j, k) order, each
+ * row's neighbours in increasing column order, `diag` on the diagonal and
+ * `offdiag` elsewhere (26.1 / -1 gives the SPD operator of the config). nx^3
+ * must fit int32 columns (nx <= 1290). */
+int b200_matrix_create_stencil27(b200_matrix** out, int64_t nx, double diag, double offdiag);
+/* `iters` PageRank steps on device vectors (SURVEY §8(d) input 4):
+ * work = A x; x = damping*work + (1-damping)/n. A is the column-stochastic
+ * transposed adjacency; x holds the start vector (e.g. 1/n). */
+int b200_pagerank_device(const b200_matrix* A, double damping, int iters, double* x_device, double* work_device,
+                         void* stream);
 
 /* Device buffers for harness TUs generated from a LiLAC-How spec
  * (paper_2001_07938_b200/specs/b200.lilac, emitted by the reference's own
@@ -232,6 +243,10 @@ int b200_cg_outer(b200_cg* cg, int cgitmax, double shift, void* stream);
 int b200_cg_step(b200_cg* cg, void* stream);
 /* Copies zeta and the last residual norm to the host (synchronises). */
 int b200_cg_result(b200_cg* cg, double* zeta, double* rnorm);
+/* Plain CG on A z = b from z = 0: `iters` steps (the conj_grad recurrence),
+ * then rnorm = |b - A z|. b_device / z_device: device arrays of n doubles
+ * (z_device may be NULL). Synchronises. */
+int b200_cg_solve(b200_cg* cg, const double* b_device, int iters, double* z_device, double* rnorm);
 /* The whole NPB benchmark (1 untimed warm-up outer iteration + reset +
  * niter outer iterations). Returns 0 or -1; zeta/rnorm on the host. */
 int b200_npb_cg(b200_cg* cg, int niter, double shift, double* zeta, double* rnorm);

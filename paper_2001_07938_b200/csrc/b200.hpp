@@ -234,6 +234,13 @@ void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s);  /
 void cg_launch_outer_update(const CgVectors& v, double shift, cudaStream_t s);  // zeta, x = z/|z|
 void cg_launch_reset_x(const CgVectors& v, cudaStream_t s);
 
+// Workload pieces (workloads_dev.cu): the 27-point stencil matrix generated in
+// HBM (int32 columns) and the PageRank update x = d*ax + (1-d)/n.
+std::int64_t stencil27_nnz(std::int64_t nx);
+void gen_stencil27_device(std::int64_t nx, double diag, double off, DevBuf& row_ptr, DevBuf& col, DevBuf& val,
+                          cudaStream_t s);
+void launch_pagerank_update(std::int64_t n, double* x, const double* ax, double d, cudaStream_t s);
+
 // Single steps (the sharded driver interleaves exchanges between them).
 void cg_launch_spmv_dot(const CsrDev& A, const CgVectors& v, cudaStream_t s);
 void cg_launch_update_zr(const CgVectors& v, cudaStream_t s);

@@ -127,6 +127,23 @@ int b200_cg_result(b200_cg* cg, double* zeta, double* rnorm) {
     });
 }
 
+int b200_cg_solve(b200_cg* cg, const double* b, int iters, double* z_out, double* rnorm) {
+    return boundary("b200_cg_solve", [&] {
+        if (iters < 0) throw Error(Errc::DataError, "iters < 0");
+        cudaStream_t s = rt().stream;
+        const std::size_t bytes = sizeof(double) * static_cast<std::size_t>(cg->v.n);
+        if (bytes) B200_CUDA(cudaMemcpyAsync(cg->v.x, b, bytes, cudaMemcpyDeviceToDevice, s));
+        cg_launch_init(cg->v, s);  // z = 0, r = p = b
+        for (int it = 0; it < iters; ++it) cg_launch_iteration(cg->A, cg->v, s);
+        cg_launch_residual(cg->A, cg->v, s);  // |b - A z|
+        if (z_out && bytes) B200_CUDA(cudaMemcpyAsync(z_out, cg->v.z, bytes, cudaMemcpyDeviceToDevice, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        CgScalars sc;
+        B200_CUDA(cudaMemcpy(&sc, cg->v.sc, sizeof sc, cudaMemcpyDeviceToHost));
+        if (rnorm) *rnorm = sc.rnorm;
+    });
+}
+
 int b200_npb_cg(b200_cg* cg, int niter, double shift, double* zeta, double* rnorm) {
     return boundary("b200_npb_cg", [&] {
         cudaStream_t s = rt().stream;

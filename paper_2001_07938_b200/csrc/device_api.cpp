@@ -7,6 +7,7 @@
 #include "tcsr.hpp"
 
 #include <algorithm>
+#include <climits>
 #include <memory>
 
 using namespace b200;
@@ -175,6 +176,45 @@ int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
         info->device_bytes = static_cast<std::int64_t>(A->row_ptr.bytes + A->col.bytes + A->val.bytes + A->nzcnt.bytes +
                                                        A->perm.bytes + A->inv_perm.bytes + A->jd_ptr.bytes) +
                              A->tiled.bytes;
+    });
+}
+
+int b200_matrix_create_stencil27(b200_matrix** out, std::int64_t nx, double diag, double offdiag) {
+    return boundary("b200_matrix_create_stencil27", [&] {
+        ensure_init();
+        if (!out) throw Error(Errc::DataError, "out is NULL");
+        if (nx < 1) throw Error(Errc::DataError, "nx < 1");
+        const std::int64_t n = nx * nx * nx;
+        if (n - 1 > INT32_MAX) throw Error(Errc::DataError, "nx^3 exceeds int32 column indices");
+        auto A = std::make_unique<b200_matrix>();
+        A->format = 0;
+        A->device = rt().device;
+        gen_stencil27_device(nx, diag, offdiag, A->row_ptr, A->col, A->val, rt().stream);
+        CsrDev& d = A->csr;
+        d.rows = n;
+        d.nnz = stencil27_nnz(nx);
+        d.cols = n;
+        d.max_row = std::min<std::int64_t>(27, n);
+        d.row_ptr = A->row_ptr.as<std::int64_t>();
+        d.col = A->col.ptr;
+        d.col32 = true;
+        d.val = A->val.as<double>();
+        d.monotone = true;
+        A->max_row = d.max_row;
+        *out = A.release();
+    });
+}
+
+int b200_pagerank_device(const b200_matrix* A, double damping, int iters, double* x, double* work, void* stream) {
+    return boundary("b200_pagerank_device", [&] {
+        if (!A || A->format != 0) throw Error(Errc::DataError, "PageRank needs a CSR matrix");
+        if (A->csr.rows != A->csr.cols && A->csr.cols > A->csr.rows)
+            throw Error(Errc::DataError, "PageRank needs a square operator");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        for (int it = 0; it < iters; ++it) {
+            launch_spmv_csr(A->csr, x, work, rt().kernel, s);
+            launch_pagerank_update(A->csr.rows, x, work, damping, s);
+        }
     });
 }
 

@@ -32,9 +32,21 @@ class Matrix:
         N.check(rc)
         return cls(h)
 
+    @classmethod
+    def stencil27(cls, nx: int, diag: float = 26.1, offdiag: float = -1.0):
+        """The 27-point stencil operator on an nx^3 grid, generated in HBM."""
+        h = C.c_void_p()
+        N.check(N.lib().b200_matrix_create_stencil27(C.byref(h), int(nx), float(diag), float(offdiag)))
+        return cls(h)
+
     @property
     def handle(self):
         return self._h
+
+    def pagerank(self, damping: float, iters: int, x_ptr: int, work_ptr: int, stream: int = 0):
+        """`iters` steps of x = damping*(A x) + (1-damping)/n on device vectors."""
+        N.check(N.lib().b200_pagerank_device(self._h, float(damping), int(iters), C.c_void_p(x_ptr),
+                                             C.c_void_p(work_ptr), C.c_void_p(stream)))
 
     def info(self) -> dict:
         i = N.MatrixInfo()
@@ -88,6 +100,13 @@ class CG:
         r = C.c_double()
         N.check(N.lib().b200_cg_result(self._h, C.byref(z), C.byref(r)))
         return z.value, r.value
+
+    def solve(self, b_ptr: int, iters: int, z_ptr: int = 0) -> float:
+        """Plain CG on A z = b from z = 0 for `iters` steps; returns |b - A z|."""
+        r = C.c_double()
+        N.check(N.lib().b200_cg_solve(self._h, C.c_void_p(b_ptr), int(iters), C.c_void_p(z_ptr or None),
+                                      C.byref(r)))
+        return r.value
 
     def npb(self, niter: int, shift: float):
         z = C.c_double()
@@ -180,6 +199,13 @@ class DistCG:
         z, r = C.c_double(), C.c_double()
         N.check(N.lib().b200_dist_cg_result(self._h, C.byref(z), C.byref(r)))
         return z.value, r.value
+
+    def solve(self, b_ptr: int, iters: int, z_ptr: int = 0) -> float:
+        """Plain CG on A z = b from z = 0 for `iters` steps; returns |b - A z|."""
+        r = C.c_double()
+        N.check(N.lib().b200_cg_solve(self._h, C.c_void_p(b_ptr), int(iters), C.c_void_p(z_ptr or None),
+                                      C.byref(r)))
+        return r.value
 
     def npb(self, niter: int, shift: float):
         z, r = C.c_double(), C.c_double()

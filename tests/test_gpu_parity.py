@@ -447,3 +447,80 @@ def test_power_law_rows_choose_split_and_match():
         y2 = run_csr(rp, ci, val, x)
         assert O.same_bits(y1, y2)
         assert_within(y1, y_ref, bound)
+
+
+# --------------------------------------------------------------------------------
+# workload pieces of the BASELINE configs (SURVEY §8(d) inputs 4 and 5)
+# --------------------------------------------------------------------------------
+
+def _stencil27_host(nx):
+    """Host restatement of the 27-point operator (tools/bench_configs.py)."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from bench_configs import gen_stencil27
+    return gen_stencil27(nx)
+
+
+@pytest.mark.parametrize("nx", [1, 2, 3, 17])
+def test_device_stencil_matches_host_generator(nx):
+    import torch
+    rp, ci, val = _stencil27_host(nx)
+    A = D.Matrix.stencil27(nx)
+    info = A.info()
+    assert info["rows"] == nx ** 3 and info["nnz"] == len(val) and info["max_row"] == min(27, nx ** 3)
+    rng = np.random.default_rng(nx)
+    xh = rng.uniform(-1, 1, nx ** 3)
+    x = torch.from_numpy(xh).cuda()
+    y = torch.empty_like(x)
+    N.lib().b200_set_kernel(b"exact")  # kernel policy is applied at upload: exact here
+    A.spmv(x.data_ptr(), y.data_ptr())
+    torch.cuda.synchronize()
+    y_ref = O.spmv_csr(rp, ci, val, xh)
+    assert_within(y.cpu().numpy(), y_ref, spmv_bound(rp, ci, val, xh))
+    A.free()
+
+
+def test_pagerank_device_matches_host_iteration():
+    import torch
+    rng = np.random.default_rng(3)
+    n = 5000
+    src = rng.integers(0, n, 60000)
+    dst = rng.integers(0, n, 60000)
+    outdeg = np.bincount(src, minlength=n).astype(np.float64)
+    order = np.lexsort((src, dst))
+    src, dst = src[order], dst[order]
+    rp = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
+    ci = src.astype(np.int64)
+    val = 1.0 / outdeg[src]
+    A = D.Matrix.csr(rp, ci, val)
+    x = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    w = torch.empty_like(x)
+    A.pagerank(0.85, 20, x.data_ptr(), w.data_ptr())
+    torch.cuda.synchronize()
+    xr = np.full(n, 1.0 / n)
+    for _ in range(20):
+        xr = 0.85 * O.spmv_csr(rp, ci, val, xr) + 0.15 / n
+    assert np.allclose(x.cpu().numpy(), xr, rtol=1e-12, atol=1e-15)
+    A.free()
+
+
+def test_cg_solve_on_the_stencil_converges():
+    import torch
+    nx = 24
+    rp, ci, val = _stencil27_host(nx)
+    A = D.Matrix.stencil27(nx)
+    cg = D.CG(A)
+    ones = torch.ones(nx ** 3, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(ones)
+    A.spmv(ones.data_ptr(), b.data_ptr())
+    z = torch.empty_like(ones)
+    r50 = cg.solve(b.data_ptr(), 50, z.data_ptr())
+    bh = b.cpu().numpy()
+    zh = z.cpu().numpy()
+    # the reported residual is |b - A z| of the returned z, and CG converged to 1
+    assert abs(r50 - np.linalg.norm(bh - O.spmv_csr(rp, ci, val, zh))) <= 1e-9 * np.linalg.norm(bh)
+    assert r50 < 1e-8 * np.linalg.norm(bh)
+    assert np.abs(zh - 1.0).max() < 1e-8
+    cg.free()
+    A.free()
