@@ -473,7 +473,7 @@ def test_device_stencil_matches_host_generator(nx):
     xh = rng.uniform(-1, 1, nx ** 3)
     x = torch.from_numpy(xh).cuda()
     y = torch.empty_like(x)
-    N.lib().b200_set_kernel(b"exact")  # kernel policy is applied at upload: exact here
+    N.lib().b200_set_kernel(b"exact")  # read at launch by the device API
     A.spmv(x.data_ptr(), y.data_ptr())
     torch.cuda.synchronize()
     y_ref = O.spmv_csr(rp, ci, val, xh)

@@ -156,7 +156,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="parboil,kron,stencil,npb")
     ap.add_argument("--reps", type=int, default=50)
-    ap.add_argument("--stencil-n", type=int, default=256)
+    ap.add_argument("--stencil-n", type=int, default=420)
     ap.add_argument("--kron-scale", type=int, default=22)
     ap.add_argument("--round", type=int, default=1)
     a = ap.parse_args()
@@ -191,16 +191,59 @@ def main():
         rp, ci, val = gen_kronecker(a.kron_scale)
         gen_s = time.time() - t0
         A = D.Matrix.csr(rp, ci, val)
-        lines.append(report(f"PageRank Kronecker scale {a.kron_scale} (A^T, skewed rows)", A, len(rp) - 1, a.reps,
-                            stream, extra={"gen_s": gen_s}))
+        n = len(rp) - 1
+        line = report(f"PageRank Kronecker scale {a.kron_scale} (A^T, skewed rows)", A, n, a.reps, stream,
+                      extra={"gen_s": gen_s})
+        lines.append(line)
+        # the workload: 20 PageRank steps (SpMV + x = 0.85 Ax + 0.15/n)
+        x = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+        w = torch.empty_like(x)
+        A.pagerank(0.85, 2, x.data_ptr(), w.data_ptr(), stream.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x.fill_(1.0 / n)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        A.pagerank(0.85, 20, x.data_ptr(), w.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        pr = {"config": f"PageRank Kronecker scale {a.kron_scale}: 20 iterations", "kernel": line["kernel"],
+              "rows": n, "nnz": line["nnz"], "max_row": line["max_row"], "us": e0.elapsed_time(e1) * 1e3,
+              "gflops": 20 * 2 * line["nnz"] / (e0.elapsed_time(e1) * 1e-3) / 1e9,
+              "gbs": 20 * line["bytes_per_call"] / (e0.elapsed_time(e1) * 1e-3) / 1e9,
+              "frac_of_measured_copy": 20 * line["bytes_per_call"] / (e0.elapsed_time(e1) * 1e-3) / 1e9 / peak(),
+              "bytes_per_call": 20 * line["bytes_per_call"], "sum_x": float(x.sum().item())}
+        print(json.dumps(pr), flush=True)
+        lines.append(pr)
         A.free()
     if "stencil" in only:
+        nx = a.stencil_n
         t0 = time.time()
-        rp, ci, val = gen_stencil27(a.stencil_n)
+        A = D.Matrix.stencil27(nx)  # generated in HBM
+        torch.cuda.synchronize()
         gen_s = time.time() - t0
-        A = D.Matrix.csr(rp, ci, val)
-        lines.append(report(f"27-point stencil N={a.stencil_n} CSR", A, len(rp) - 1, max(5, a.reps // 5), stream,
-                            extra={"gen_s": gen_s}))
+        n = nx ** 3
+        line = report(f"27-point stencil N={nx} CSR (device-generated)", A, n, max(5, a.reps // 10), stream,
+                      extra={"gen_s": gen_s})
+        lines.append(line)
+        # the workload: 50 CG iterations on A z = A 1 from z = 0
+        cg = D.CG(A)
+        ones = torch.ones(n, dtype=torch.float64, device="cuda")
+        b = torch.empty_like(ones)
+        A.spmv(ones.data_ptr(), b.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        cg.solve(b.data_ptr(), 2)
+        t0 = time.perf_counter()
+        rn = cg.solve(b.data_ptr(), 50)
+        dt = time.perf_counter() - t0
+        it_bytes = line["bytes_per_call"] + 96 * n
+        cgl = {"config": f"27-point stencil N={nx}: CG 50 iterations (b = A*1)", "kernel": line["kernel"],
+               "rows": n, "nnz": line["nnz"], "max_row": line["max_row"], "us": dt * 1e6,
+               "gflops": 50 * (2 * line["nnz"] + 10 * n) / dt / 1e9, "gbs": 50 * it_bytes / dt / 1e9,
+               "frac_of_measured_copy": 50 * it_bytes / dt / 1e9 / peak(), "bytes_per_call": 50 * it_bytes,
+               "rnorm_rel": rn / float(torch.linalg.norm(b).item())}
+        print(json.dumps(cgl), flush=True)
+        lines.append(cgl)
+        cg.free()
         A.free()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "configs.jsonl"), "a") as f:
