@@ -16,6 +16,9 @@
 // identical sharded algorithm for tests on a single B200.
 
 #include "exchange.hpp"
+
+#include <cstdlib>
+#include <cstring>
 #include "lilac_b200.h"
 #include "runtime.hpp"
 #include "tcsr.hpp"
@@ -58,6 +61,12 @@ struct b200_dist_cg {
     std::int64_t n = 0;
     cudaStream_t stream = nullptr;
     int steps_exchanges = 0;
+    // one outer iteration captured as a CUDA graph (kernels, exchange copies
+    // and NCCL collectives alike), keyed by (stream, cgitmax, shift)
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t graph_stream = nullptr;
+    int graph_cgitmax = -1;
+    double graph_shift = 0.0;
 };
 
 namespace {
@@ -179,6 +188,44 @@ void dist_outer(b200_dist_cg* d, int cgitmax, double shift, cudaStream_t st) {
     for (auto& s : d->shards) cg_launch_scale_x(s->v, st);
 }
 
+// Replays one outer iteration from a graph: at 8 shards a CG step is ~40 us
+// of device work against ~10 launches + 3 collectives issued from the host,
+// so launch overhead would otherwise bound the scaling. LILAC_B200_DIST_GRAPH=0
+// issues the launches directly.
+void dist_outer_graph(b200_dist_cg* d, int cgitmax, double shift, cudaStream_t st) {
+    static const bool on = [] {
+        const char* e = std::getenv("LILAC_B200_DIST_GRAPH");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (!on) {
+        dist_outer(d, cgitmax, shift, st);
+        return;
+    }
+    if (!d->graph || d->graph_stream != st || d->graph_cgitmax != cgitmax || d->graph_shift != shift) {
+        if (d->graph) {
+            cudaGraphExecDestroy(d->graph);
+            d->graph = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        B200_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            dist_outer(d, cgitmax, shift, st);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        B200_CUDA(cudaStreamEndCapture(st, &g));
+        const cudaError_t e = cudaGraphInstantiate(&d->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) throw_cuda(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+        d->graph_stream = st;
+        d->graph_cgitmax = cgitmax;
+        d->graph_shift = shift;
+    }
+    B200_CUDA(cudaGraphLaunch(d->graph, st));
+}
+
 b200_dist_cg* finish_create(std::unique_ptr<b200_dist_cg>& d) {
     d->stream = rt().stream;
     return d.release();
@@ -236,6 +283,7 @@ int b200_dist_cg_create_nccl(b200_dist_cg** out, int rank, int world, const void
 
 void b200_dist_cg_free(b200_dist_cg* d) {
     if (!d) return;
+    if (d->graph) cudaGraphExecDestroy(d->graph);
     for (auto& s : d->shards) s->release();
     delete d;
 }
@@ -249,7 +297,7 @@ int b200_dist_cg_reset(b200_dist_cg* d, void* stream) {
 
 int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream) {
     return boundary("b200_dist_cg_outer", [&] {
-        dist_outer(d, cgitmax, shift, stream ? static_cast<cudaStream_t>(stream) : d->stream);
+        dist_outer_graph(d, cgitmax, shift, stream ? static_cast<cudaStream_t>(stream) : d->stream);
     });
 }
 
@@ -267,9 +315,9 @@ int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double
     return boundary("b200_dist_npb", [&] {
         cudaStream_t st = d->stream;
         for (auto& s : d->shards) cg_launch_reset_x(s->v, st);
-        dist_outer(d, 25, shift, st);  // NPB's untimed warm-up iteration
+        dist_outer_graph(d, 25, shift, st);  // NPB's untimed warm-up iteration
         for (auto& s : d->shards) cg_launch_reset_x(s->v, st);
-        for (int it = 0; it < niter; ++it) dist_outer(d, 25, shift, st);
+        for (int it = 0; it < niter; ++it) dist_outer_graph(d, 25, shift, st);
         B200_CUDA(cudaStreamSynchronize(st));
         CgScalars sc;
         B200_CUDA(cudaMemcpy(&sc, d->shards[0]->v.sc, sizeof sc, cudaMemcpyDeviceToHost));
