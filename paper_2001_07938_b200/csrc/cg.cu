@@ -204,9 +204,12 @@ __global__ void k_cg_fill(double* x, std::int64_t n, double val) {
     GRID_STRIDE(i, n) x[i] = val;
 }
 
+// Two elements per thread: the CG vectors are L2-resident between steps, so
+// these kernels are latency-bound — all of a thread's loads should be in
+// flight at once rather than walked in a grid-stride loop.
 unsigned vec_grid(const CgVectors& v) {
-    std::int64_t g = (v.n + kThreads * 4 - 1) / (kThreads * 4);
-    return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, std::min(kMaxParts, 148 * 8))));
+    std::int64_t g = (v.n + kThreads * 2 - 1) / (kThreads * 2);
+    return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, std::min(kMaxParts, 148 * 16))));
 }
 
 }  // namespace
