@@ -168,8 +168,13 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
     const bool head = lane == 0 || pk != k1;
     const unsigned hm = __ballot_sync(kFull, head);
     const int seg = 31 - __clz(hm & (kFull >> (31 - lane)));
+    // only as many doubling steps as the longest row segment of the piece
+    // needs (NPB: rows span ~5 lanes, so usually 3 of the 5; each f64 step
+    // is two SHFLs + a DADD)
+    const int maxspan = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(lane - seg + 1)));
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
+        if (d >= maxspan) break;
         const double t = __shfl_up_sync(kFull, s, d);
         if (lane - d >= seg) s += t;
     }
