@@ -179,9 +179,12 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
         if (lane - d >= seg) s += t;
     }
     const double ps = __shfl_up_sync(kFull, s, 1);
-    const unsigned nk0 = __shfl_down_sync(kFull, k0, 1);
-    if (split && k0 != kSent) sts_add_f64(yp_s + 8u * k0, (lane > 0 && pk == k0) ? p0 + ps : p0);
-    if ((lane == 31 || nk0 != k1) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
+    // does the next lane's head continue my tail row? (its pk == its k0; a
+    // ballot bit instead of a shuffle of k0)
+    const bool cont = lane > 0 && pk == k0;
+    const unsigned cm = __ballot_sync(kFull, cont);
+    if (split && k0 != kSent) sts_add_f64(yp_s + 8u * k0, cont ? p0 + ps : p0);
+    if ((lane == 31 || !((cm >> (lane + 1)) & 1u)) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
 }
 
 // Processes a (slab, warp) run [lo, hi) (tile-relative, both multiples of
