@@ -178,13 +178,14 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
         const double t = __shfl_up_sync(kFull, s, d);
         if (lane - d >= seg) s += t;
     }
-    const double ps = __shfl_up_sync(kFull, s, 1);
-    // does the next lane's head continue my tail row? (its pk == its k0; a
-    // ballot bit instead of a shuffle of k0)
-    const bool cont = lane > 0 && pk == k0;
-    const unsigned cm = __ballot_sync(kFull, cont);
-    if (split && k0 != kSent) sts_add_f64(yp_s + 8u * k0, cont ? p0 + ps : p0);
-    if ((lane == 31 || !((cm >> (lane + 1)) & 1u)) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
+    // Two store passes, each touching distinct rows: (1) every segment's sum
+    // at its last lane (the next lane starts a segment); (2) the head run of
+    // every split lane. A row continuing from lane i-1's tail into lane i's
+    // head gets both; the passes are ordered, so no shuffle of the scan value
+    // into the split lane is needed.
+    if ((lane == 31 || ((hm >> (lane + 1)) & 1u)) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
+    __syncwarp();
+    if (split && k0 != kSent) sts_add_f64(yp_s + 8u * k0, p0);
 }
 
 // Processes a (slab, warp) run [lo, hi) (tile-relative, both multiples of
