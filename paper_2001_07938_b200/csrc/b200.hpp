@@ -65,6 +65,11 @@ constexpr int kSlabW = 12288;       // columns per slab: 2 x 96 KB double-buffer
 constexpr int kMaxTileRows = 4096;  // tile-local row fits the key and the smem y buffer
 constexpr int kRunAlign = 4;        // (slab, warp) runs start and end on 4-nonzero (32 B) boundaries
 constexpr std::uint32_t kPadKey = 0xffffu << 16;  // padding entry: sentinel row, column 0, value 0
+// key = lrow << 16 | kKeyCont? | lcol: kKeyCont marks an element whose row
+// continues the row of the element before it in its (slab, warp) run
+constexpr std::uint32_t kKeyCont = 1u << 14;
+constexpr std::uint32_t kKeyColMask = kKeyCont - 1u;
+static_assert(kSlabW <= static_cast<int>(kKeyColMask) + 1, "slab columns must fit below the continuation bit");
 
 struct TcsrDev {
     std::int64_t ntiles = 0;

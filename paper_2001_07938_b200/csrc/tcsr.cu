@@ -160,12 +160,13 @@ __device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std
 // (k0, p0) and tail run (k1, p1) (k0 == k1: a single run, value p1). Row keys
 // are non-decreasing across lanes. Adds every row's piece-sum into yp[row]
 // (rows are owned by this warp: no atomics, fixed order).
-__device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1, double p1, int lane,
+// `cont`: the lane's first element continues the row of the element before it
+// (a layout bit, kKeyCont), so a non-split lane starts a segment iff !cont.
+__device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1, double p1, bool cont, int lane,
                                              std::uint32_t yp_s) {
     const bool split = k0 != k1;
     double s = p1;
-    const unsigned pk = __shfl_up_sync(kFull, k1, 1);
-    const bool head = lane == 0 || pk != k1;
+    const bool head = lane == 0 || split || !cont;
     const unsigned hm = __ballot_sync(kFull, head);
     const int seg = 31 - __clz(hm & (kFull >> (31 - lane)));
     // only as many doubling steps as the longest row segment of the piece
@@ -206,10 +207,10 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint32_
         if (MODE == 1 || MODE == 3) {  // probe: no gather
             p0 = cur.v0.x, p1 = cur.v0.y, p2 = cur.v1.x, p3 = cur.v1.y;
         } else {
-            p0 = cur.v0.x * lds_f64(xb_s + 8u * (cur.k.x & 0xffffu));
-            p1 = cur.v0.y * lds_f64(xb_s + 8u * (cur.k.y & 0xffffu));
-            p2 = cur.v1.x * lds_f64(xb_s + 8u * (cur.k.z & 0xffffu));
-            p3 = cur.v1.y * lds_f64(xb_s + 8u * (cur.k.w & 0xffffu));
+            p0 = cur.v0.x * lds_f64(xb_s + 8u * (cur.k.x & kKeyColMask));
+            p1 = cur.v0.y * lds_f64(xb_s + 8u * (cur.k.y & kKeyColMask));
+            p2 = cur.v1.x * lds_f64(xb_s + 8u * (cur.k.z & kKeyColMask));
+            p3 = cur.v1.y * lds_f64(xb_s + 8u * (cur.k.w & kKeyColMask));
         }
         if (MODE >= 2) {
             if (p0 == 12345.678) sts_add_f64(yp_s, p1 + p2 + p3);  // probe: no reduction
@@ -230,7 +231,7 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint32_
                 if (in1) sts_add_f64(yp_s + 8u * k1, k2 == k1 ? p1 + p2 : p1);
                 if (in2 && k2 != k1) sts_add_f64(yp_s + 8u * k2, p2);
             }
-            reduce_piece(k0, head, k3, tail, lane, yp_s);
+            reduce_piece(k0, head, k3, tail, (cur.k.x & kKeyCont) != 0u, lane, yp_s);
         }
         cur = nxt;
     }

@@ -153,14 +153,17 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
         }
         wo[per_tile - 1] = static_cast<std::int32_t>(off);
         std::vector<std::int64_t> cur(wo, wo + per_tile);
+        std::vector<std::int64_t> last(static_cast<std::size_t>(per_tile), -1);  // last row written per run
         for (int w = 0; w < kTileWarps; ++w)
             for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r) {
                 const std::uint32_t lrow = static_cast<std::uint32_t>(r - row0) << 16;
                 for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
                     const std::int64_t k = ci[j] / kSlabW;
-                    const std::int64_t pos = tb + cur[k * kTileWarps + w]++;
+                    const std::int64_t run = k * kTileWarps + w;
+                    const std::int64_t pos = tb + cur[run]++;
                     h.val[pos] = val[j];
-                    h.key[pos] = lrow | static_cast<std::uint32_t>(ci[j] - k * kSlabW);
+                    h.key[pos] = lrow | (last[run] == r ? kKeyCont : 0u) | static_cast<std::uint32_t>(ci[j] - k * kSlabW);
+                    last[run] = r;
                 }
             }
     });
