@@ -585,10 +585,6 @@ void vec2_call(const char* name, std::int64_t n, double* y, double s, const doub
             launch_xpay_to(n, dout.buf.as<double>(), dy.data<double>(), s, dx.data<double>(), r.stream);
     });
     tm.acquired();
-    {
-        PhaseTimer pt(kPhNote);
-        lilac::marshal::note_host_write(y, bytes);  // (write_back repeats it; timed here)
-    }
     oo.write_back();
     collect_kernel_time(hs);
     tm.written_back();

@@ -168,7 +168,7 @@ using Clock = std::chrono::steady_clock;
 
 // Host-side phase accumulators (ns), read by b200_host_profile().
 enum HostPhase { kPhMirrorFetch, kPhMirrorPoll, kPhD2D, kPhH2D, kPhD2H, kPhPublish, kPhPublishGuard,
-                 kPhAcquire, kPhLaunch, kPhPick, kPhAcquireOut, kPhSteal, kPhNote, kPhMalloc, kPhCount };
+                 kPhAcquire, kPhLaunch, kPhPick, kPhAcquireOut, kPhSteal, kPhMalloc, kPhCount };
 // Phase timers and per-call kernel events cost clock reads and CUDA API calls
 // on every harness call: off unless LILAC_B200_PROFILE=1 / b200_set_profiling.
 extern bool g_profile;

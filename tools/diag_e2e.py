@@ -61,7 +61,7 @@ ns = np.zeros(16, np.int64)
 cnt = np.zeros(16, np.int64)
 k = N.lib().b200_host_profile(N.ptr(ns), N.ptr(cnt), 16)
 names = ["mirror_fetch", "mirror_poll", "d2d", "h2d", "d2h+sync", "publish", "publish_guard", "acquire(vec2 in)",
-         "launch", "pick(vec2)", "acquire_out(vec2)", "steal", "note_write(vec2)", "cudaMalloc"]
+         "launch", "pick(vec2)", "acquire_out(vec2)", "steal", "cudaMalloc"]
 for i in range(k):
     print(f"  {names[i]:14s} n={cnt[i]:7d} total={ns[i]/1e6:9.2f} ms mean={ns[i]/max(cnt[i],1)/1e3:8.1f} us")
 for name, s in H.harness_stats().items():
