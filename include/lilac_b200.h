@@ -163,9 +163,11 @@ void b200_stats_reset(void);
 /* Change-detection cost counters since process start: SIGSEGV traps taken,
  * mprotect calls, bytes hashed; and device bytes currently held as mirrors. */
 int b200_marshal_counters(int64_t* faults, int64_t* mprotects, int64_t* hash_bytes, int64_t* mirror_bytes);
-/* Host-side phase accumulators (ns, counts): mirror fetch, mirror poll, D2D,
- * H2D, D2H+sync, mirror publish, publish guard, acquire, launch. Returns the
- * number of phases. */
+/* Host-side phase accumulators (ns, counts), collected while profiling is on
+ * (b200_set_profiling): mirror fetch, mirror poll, D2D, H2D, D2H+sync, mirror
+ * publish, publish guard, acquire (axpy/xpay inputs), launch, binding pick,
+ * acquire_out, buffer hand-over, cudaMalloc (count only). Returns the number
+ * of phases. */
 int b200_host_profile(int64_t* ns, int64_t* counts, int cap);
 
 /* ==========================================================================
