@@ -52,6 +52,7 @@ interp::HarnessRegistry& reg() {
         ps.push_back(what::parse_what(programs::kSpmvCsr));
         ps.push_back(what::parse_what(programs::kSpmvJds));
         ps.push_back(what::parse_what(programs::kDotProduct));
+        ps.push_back(what::parse_what(programs::kGemm));
         interp::register_reference_harnesses(h, ps);
         return h;
     }();
@@ -91,6 +92,17 @@ std::vector<double> ref_jds(const oracle::Jds& m, const std::vector<double>& xv)
                                        interp::Pointer{ci, 0}};
     (*reg().find("lilac.spmv_jds"))(mem, args);
     return mem.floats(out);
+}
+
+std::vector<double> ref_gemm(std::int64_t n, std::int64_t m, std::int64_t p, const std::vector<double>& av,
+                             const std::vector<double>& bv) {
+    interp::Memory mem;
+    int c = mem.alloc_floats("c", std::vector<double>(static_cast<size_t>(n * m), 0.0));
+    int a = mem.alloc_floats("a", av);
+    int b = mem.alloc_floats("b", bv);
+    std::vector<interp::Value> args = {n, m, interp::Pointer{c, 0}, p, interp::Pointer{a, 0}, interp::Pointer{b, 0}};
+    (*reg().find("lilac.gemm"))(mem, args);
+    return mem.floats(c);
 }
 
 double ref_dot(const std::vector<double>& av, const std::vector<double>& bv) {
@@ -186,7 +198,8 @@ int main(int argc, char** argv) {
     }
 
     // test_interp.cpp:215-300 — seed 424242, 50 trials, rectangular, density 0.4;
-    // the gemm draws are replayed (and discarded) to keep the stream aligned.
+    // each case also carries the gemm harness call of the same trial
+    // (n = rows, m = cols, a = random_dense(n, p), b = random_dense(p, m)).
     {
         std::mt19937_64 rng(424242);
         std::ostringstream os;
@@ -196,10 +209,15 @@ int main(int argc, char** argv) {
             std::int64_t cols = 1 + static_cast<std::int64_t>(rng() % 8);
             std::vector<double> dense = oracle::random_dense(rng, rows, cols, 0.4);
             std::vector<double> x = oracle::random_vector(rng, cols);
-            os << (t ? "," : "") << case_json(rows, cols, dense, x);
+            std::string cj = case_json(rows, cols, dense, x);
             std::int64_t p = 1 + static_cast<std::int64_t>(rng() % 6);
-            (void)oracle::random_dense(rng, rows, p, 0.8);
-            (void)oracle::random_dense(rng, p, cols, 0.8);
+            std::vector<double> ga = oracle::random_dense(rng, rows, p, 0.8);
+            std::vector<double> gb = oracle::random_dense(rng, p, cols, 0.8);
+            std::ostringstream g;
+            g << ",\"gemm\":{\"n\":" << rows << ",\"m\":" << cols << ",\"p\":" << p << ",\"a\":" << arr(ga)
+              << ",\"b\":" << arr(gb) << ",\"c\":" << arr(ref_gemm(rows, cols, p, ga, gb)) << "}}";
+            cj.back() == '}' ? cj.pop_back() : void();
+            os << (t ? "," : "") << cj << g.str();
         }
         os << "]}";
         write(dir + "/interp_harness_seed424242.json", os.str());
@@ -231,7 +249,8 @@ int main(int argc, char** argv) {
            << "],[\"foobar\"," << marshal::fnv1a("foobar", 6) << "]],"
            << "\"signatures\":{\"spmv_csr\":" << sig_of(programs::kSpmvCsr)
            << ",\"spmv_jds\":" << sig_of(programs::kSpmvJds)
-           << ",\"dotproduct\":" << sig_of(programs::kDotProduct) << "}}";
+           << ",\"dotproduct\":" << sig_of(programs::kDotProduct)
+           << ",\"gemm\":" << sig_of(programs::kGemm) << "}}";
         write(dir + "/abi.json", os.str());
     }
     std::printf("golden fixtures written to %s\n", dir.c_str());

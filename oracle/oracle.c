@@ -450,3 +450,14 @@ double orc_npb_cg(int64_t n, const int64_t* row_ptr, const int64_t* col_ind, con
     if (rnorm_out) *rnorm_out = rnorm;
     return zeta;
 }
+
+/* gemm (kernels.lilac:14-19) in what_interp.cpp's order: forall i, forall j,
+ * acc = +0.0, k ascending, separate mul and add (-ffp-contract=off). */
+void orc_gemm(int64_t n, int64_t m, double* c, int64_t p, const double* a, const double* b) {
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < m; ++j) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < p; ++k) acc += a[i * p + k] * b[k * m + j];
+            c[i * m + j] = acc;
+        }
+}

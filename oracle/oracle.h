@@ -6,7 +6,7 @@
  * CPU baseline. The product path (paper_2001_07938_b200/) never links it.
  *
  * Parity status: PINNED. Every function below that restates reference
- * semantics is checked bit-for-bit against tests/golden/*.json, which were
+ * semantics is checked bit-for-bit against the tests/golden JSON fixtures, which were
  * produced by the reference itself (oracle/_ref, built from
  * /root/reference/proj/src by oracle/Makefile; see tests/golden/README.md).
  * The exceptions are marked "unpinned" (axpy: not a reference computation;
@@ -37,6 +37,8 @@ int orc_spmv_jds(int64_t rows, double* output, const int64_t* nzcnt, const int64
 
 /* dotproduct, kernels.lilac:6-7; result[0] = sum_{i<length} a[i]*b[i] from +0.0. */
 void orc_dot(double* result, int64_t length, const double* a, const double* b);
+/* gemm, kernels.lilac:14-19: c[i*m+j] = sum_{k<p} a[i*p+k]*b[k*m+j] from +0.0, k ascending. */
+void orc_gemm(int64_t n, int64_t m, double* c, int64_t p, const double* a, const double* b);
 
 /* Unpinned CG companion (not expressible in LiLAC-What): y[i] = y[i] + alpha*x[i]. */
 void orc_axpy(int64_t n, double* y, double alpha, const double* x);

@@ -45,6 +45,7 @@ SIGNATURES = {
     "b200_spmv_csr": (None, [i64, f64p, i64p, f64p, f64p, i64p]),
     "b200_spmv_jds": (None, [i64, f64p, i64p, i64p, f64p, i64p, f64p, i64p]),
     "b200_dot": (None, [f64p, i64, f64p, f64p]),
+    "b200_gemm": (None, [i64, i64, f64p, i64, f64p, f64p]),
     "b200_axpy": (None, [i64, f64p, C.c_double, f64p]),
     "b200_xpay": (None, [i64, f64p, C.c_double, f64p]),
     # 2. runtime control

@@ -181,6 +181,24 @@ interp::Value call_dot(interp::Memory& mem, const std::vector<interp::Value>& a)
     return result;
 }
 
+// gemm(n, m, c, p, a, b) (kernels.lilac:14-19)
+interp::Value call_gemm(interp::Memory& mem, const std::vector<interp::Value>& a) {
+    check_arity(a, 6);
+    const std::int64_t n = as_int(a[0], "n"), m = as_int(a[1], "m");
+    FloatSlice c = floats(mem, as_ptr(a[2], "c"), "c");
+    const std::int64_t p = as_int(a[3], "p");
+    FloatSlice A = floats(mem, as_ptr(a[4], "a"), "a");
+    FloatSlice B = floats(mem, as_ptr(a[5], "b"), "b");
+    if (n < 0 || m < 0 || p < 0) throw Error(Errc::DataError, "negative gemm extent");
+    if (n * m > c.n) oob("c", n * m, c.n);
+    if (n * p > A.n) oob("a", n * p, A.n);
+    if (p * m > B.n) oob("b", p * m, B.n);
+    b200_gemm(n, m, c.p, p, A.p, B.p);
+    rethrow_b200();
+    bump_versions(mem, c, n * m);
+    return {};
+}
+
 }  // namespace
 
 std::vector<std::string> register_b200_harnesses(interp::HarnessRegistry& reg,
@@ -197,6 +215,10 @@ std::vector<std::string> register_b200_harnesses(interp::HarnessRegistry& reg,
                               {K::ScalarInt, K::ArrayFloatOut, K::ArrayInt, K::ArrayInt, K::ArrayFloatIn,
                                K::ArrayInt, K::ArrayFloatIn, K::ArrayInt}))
             fn = call_jds;
+        else if (signature_is(sig, {"n", "m", "c", "p", "a", "b"},
+                              {K::ScalarInt, K::ScalarInt, K::ArrayFloatOut, K::ScalarInt, K::ArrayFloatIn,
+                               K::ArrayFloatIn}))
+            fn = call_gemm;
         else if (sig.scalar_result &&
                  signature_is(sig, {"result", "length", "a", "b"},
                               {K::ArrayFloatOut, K::ScalarInt, K::ArrayFloatIn, K::ArrayFloatIn}))

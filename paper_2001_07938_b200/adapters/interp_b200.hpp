@@ -23,7 +23,7 @@
 namespace lilac_b200 {
 
 // Registers "lilac.<name>" for every program in `whats` whose computation the
-// B200 library implements (spmv_csr, spmv_jds, dotproduct — recognised by
+// B200 library implements (spmv_csr, spmv_jds, dotproduct, gemm — recognised by
 // name and checked against infer_interface's signature). Others are skipped
 // and returned, so a caller can fall back to the reference harness for them.
 // Switches the library to B200_ERRORS_RETURN: failures surface as

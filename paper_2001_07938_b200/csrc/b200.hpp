@@ -206,6 +206,9 @@ void launch_axpy(std::int64_t n, double* y, double alpha, const double* x, cudaS
 void launch_xpay(std::int64_t n, double* y, double beta, const double* x, cudaStream_t s);
 // out-of-place forms (out may alias y): the harness writes its output binding
 // straight from the input binding's device bytes
+// gemm (gemm.cu): c = a b, row-major; exact = the reference's k order
+void launch_gemm(std::int64_t n, std::int64_t m, std::int64_t p, const double* a, const double* b, double* c,
+                 bool exact, cudaStream_t s);
 void launch_axpy_to(std::int64_t n, double* out, const double* y, double alpha, const double* x, cudaStream_t s);
 void launch_xpay_to(std::int64_t n, double* out, const double* y, double beta, const double* x, cudaStream_t s);
 

@@ -314,6 +314,23 @@ struct dot_state {
     bool first_run_done = false;
 };
 
+struct gemm_state {
+    MarshalObject<DevArray> m_c, m_a, m_b;
+    bool first_run_done = false;
+};
+
+gemm_state& gemm_st() {
+    static gemm_state* st = new gemm_state;
+    if (!st->first_run_done) {
+        st->first_run_done = true;
+        ensure_init();
+        enroll_stats(st->m_c, "b200_gemm.c");
+        enroll_stats(st->m_a, "b200_gemm.a");
+        enroll_stats(st->m_b, "b200_gemm.b");
+    }
+    return *st;
+}
+
 struct vec2_state {  // axpy / xpay: y in, x in, y out
     BindingCache<DevArray, kBindingCache> m_y_in, m_x, m_y_out;
     bool first_run_done = false;
@@ -594,6 +611,33 @@ void vec2_call(const char* name, std::int64_t n, double* y, double s, const doub
 }
 
 }  // namespace
+
+extern "C" void b200_gemm(std::int64_t n, std::int64_t m, double* c, std::int64_t p, const double* a,
+                          const double* b) {
+    boundary("b200_gemm", [&] {
+        gemm_state& state = gemm_st();
+        HarnessStats& hs = harness_stats("b200_gemm");
+        Timer tm(hs);
+        if (n < 0 || m < 0 || p < 0) throw Error(Errc::DataError, "negative gemm extent");
+        const std::int64_t h0 = state.m_a.out().h2d + state.m_b.out().h2d, d0 = state.m_c.out().d2h;
+        D2dMeter dm(hs, {&state.m_a.out().d2d, &state.m_b.out().d2d});
+        // binding order of infer_interface: c (output), a, b (kernels.lilac:14-19)
+        DevArray& dc = state.m_c.acquire_out(c, n * m * sizeof(double), B200Write_construct, B200Write_update,
+                                             B200Write_destruct);
+        DevArray& da = state.m_a.acquire(a, n * p * sizeof(double), nullptr, B200Read_update, B200Read_destruct);
+        DevArray& db = state.m_b.acquire(b, p * m * sizeof(double), nullptr, B200Read_update, B200Read_destruct);
+        tm.acquired();
+        timed_launch(hs, [&] {
+            launch_gemm(n, m, p, da.data<double>(), db.data<double>(), dc.buf.as<double>(), rt().exact_blas,
+                        rt().stream);
+        });
+        tm.acquired();
+        state.m_c.write_back();
+        collect_kernel_time(hs);
+        tm.written_back();
+        add_bytes(hs, h0, state.m_a.out().h2d + state.m_b.out().h2d, d0, state.m_c.out().d2h);
+    });
+}
 
 extern "C" void b200_axpy(std::int64_t n, double* y, double alpha, const double* x) {
     boundary("b200_axpy", [&] { vec2_call("b200_axpy", n, y, alpha, x, true); });

@@ -142,6 +142,27 @@ static PyObject* vec2(PyObject* args, int axpy) {
     return check_error();
 }
 
+static PyObject* py_gemm(PyObject* self, PyObject* args) {
+    long long n, m, p;
+    PyObject *o_c, *o_a, *o_b;
+    if (!PyArg_ParseTuple(args, "LLOLOO", &n, &m, &o_c, &p, &o_a, &o_b)) return NULL;
+    Py_buffer v[3];
+    if (get(o_c, &v[0], F64_OUT, "c")) return NULL;
+    if (get(o_a, &v[1], F64_IN, "a")) return release_all(v, 1), NULL;
+    if (get(o_b, &v[2], F64_IN, "b")) return release_all(v, 2), NULL;
+    if (n < 0 || m < 0 || p < 0 || v[0].len < n * m * 8 || v[1].len < n * p * 8 || v[2].len < p * m * 8) {
+        release_all(v, 3);
+        PyErr_SetString(PyExc_ValueError, "gemm: arrays shorter than n*m (c), n*p (a), p*m (b)");
+        return NULL;
+    }
+    Py_BEGIN_ALLOW_THREADS
+    b200_gemm((int64_t)n, (int64_t)m, (double*)v[0].buf, (int64_t)p, (const double*)v[1].buf,
+              (const double*)v[2].buf);
+    Py_END_ALLOW_THREADS
+    release_all(v, 3);
+    return check_error();
+}
+
 static PyObject* py_axpy(PyObject* self, PyObject* args) { return vec2(args, 1); }
 static PyObject* py_xpay(PyObject* self, PyObject* args) { return vec2(args, 0); }
 
@@ -156,6 +177,7 @@ static PyMethodDef methods[] = {
     {"spmv_csr", py_spmv_csr, METH_VARARGS, "spmv_csr(rows, output, row_ptr, val, x, col_ind)"},
     {"spmv_jds", py_spmv_jds, METH_VARARGS, "spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind)"},
     {"dotproduct", py_dotproduct, METH_VARARGS, "dotproduct(length, a, b) -> float"},
+    {"gemm", py_gemm, METH_VARARGS, "gemm(n, m, c, p, a, b): c = a b (row-major)"},
     {"axpy", py_axpy, METH_VARARGS, "axpy(n, y, alpha, x): y += alpha*x"},
     {"xpay", py_xpay, METH_VARARGS, "xpay(n, y, beta, x): y = x + beta*y"},
     {"set_error_class", py_set_error_class, METH_O, "exception class raised as cls(code, message)"},

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native as N
 
-__all__ = ["spmv_csr", "spmv_jds", "dotproduct", "axpy", "xpay", "HarnessRegistry",
+__all__ = ["spmv_csr", "spmv_jds", "dotproduct", "gemm", "axpy", "xpay", "HarnessRegistry",
            "register_b200_harnesses", "region_stats", "harness_stats", "B200Error", "set_errors_return",
            "set_writeback", "host_sync", "host_forget", "lazy_counters", "page_aligned"]
 
@@ -95,6 +95,18 @@ def dotproduct(length, a, b) -> float:
     N.lib().b200_dot(N.ptr(res), int(length), N.ptr(_f64(a, "a")), N.ptr(_f64(b, "b")))
     N.check()
     return float(res[0])
+
+
+def gemm(n, m, c, p, a, b):
+    """c[i*m + j] = sum_k a[i*p + k] * b[k*m + j] (kernels.lilac:14-19)."""
+    E = _ext()
+    if E is not None:
+        return E.gemm(int(n), int(m), c, int(p), a, b)
+    for arr, need, name in ((c, n * m, "c"), (a, n * p, "a"), (b, p * m, "b")):
+        if _f64(arr, name, name == "c").size < need:
+            raise ValueError("gemm: arrays shorter than n*m (c), n*p (a), p*m (b)")
+    N.lib().b200_gemm(int(n), int(m), N.ptr(c), int(p), N.ptr(a), N.ptr(b))
+    N.check()
 
 
 def axpy(n, y, alpha, x):
@@ -187,10 +199,10 @@ class HarnessRegistry:
         return sorted(self._fns)
 
 
-def register_b200_harnesses(reg: HarnessRegistry, computations=("spmv_csr", "spmv_jds", "dotproduct")):
+def register_b200_harnesses(reg: HarnessRegistry, computations=("spmv_csr", "spmv_jds", "dotproduct", "gemm")):
     """Counterpart of interp::register_reference_harnesses (interp.cpp:330):
     registers the B200 harnesses under "lilac.<computation>"."""
-    table = {"spmv_csr": spmv_csr, "spmv_jds": spmv_jds, "dotproduct": dotproduct}
+    table = {"spmv_csr": spmv_csr, "spmv_jds": spmv_jds, "dotproduct": dotproduct, "gemm": gemm}
     for c in computations:
         reg.add("lilac." + c, table[c])
     return reg

@@ -52,6 +52,7 @@ def oracle() -> C.CDLL:
     L.orc_spmv_jds.argtypes = [I64, f64p, i64p, i64p, f64p, i64p, f64p, i64p, I64, I64, I64]
     L.orc_spmv_jds.restype = C.c_int
     L.orc_dot.argtypes = [f64p, I64, f64p, f64p]
+    L.orc_gemm.argtypes = [I64, I64, f64p, I64, f64p, f64p]
     L.orc_axpy.argtypes = [I64, f64p, C.c_double, f64p]
     L.orc_spmv_csr_mt.argtypes = [I64, f64p, i64p, f64p, f64p, i64p, C.c_int]
     L.orc_count_nonzeros.argtypes = [I64, I64, f64p]
@@ -137,6 +138,14 @@ def dot(a, b):
     r = np.zeros(1, dtype=np.float64)
     oracle().orc_dot(ptr(r), len(a), ptr(a), ptr(b))
     return r[0]
+
+
+def gemm(n, m, p, a, b):
+    """c (n x m) = a (n x p) b (p x m), row-major, the reference's k order."""
+    c = np.zeros(n * m, dtype=np.float64)
+    oracle().orc_gemm(n, m, ptr(c), p, ptr(np.ascontiguousarray(a, np.float64).ravel()),
+                      ptr(np.ascontiguousarray(b, np.float64).ravel()))
+    return c
 
 
 def axpy(y, alpha, x):

@@ -44,7 +44,7 @@ def test_harness_signatures_match_reference_infer_interface():
     infer_interface order (tests/golden/abi.json, written by the reference)."""
     sigs = O.golden("abi.json")["signatures"]
     kinds = {"scalar-int": N.i64, "array-int": N.i64p, "array-float-in": N.f64p, "array-float-out": N.f64p}
-    table = {"spmv_csr": "b200_spmv_csr", "spmv_jds": "b200_spmv_jds", "dotproduct": "b200_dot"}
+    table = {"spmv_csr": "b200_spmv_csr", "spmv_jds": "b200_spmv_jds", "dotproduct": "b200_dot", "gemm": "b200_gemm"}
     for comp, fn in table.items():
         want = [kinds[k] for _, k in sigs[comp]]
         got = N.SIGNATURES[fn][1]
@@ -79,7 +79,7 @@ def test_gen_npb_bit_exact_vs_oracle_makea(cls):
 
 def test_harness_registry_mirror():
     reg = H.register_b200_harnesses(H.HarnessRegistry())
-    assert reg.names() == ["lilac.dotproduct", "lilac.spmv_csr", "lilac.spmv_jds"]
+    assert reg.names() == ["lilac.dotproduct", "lilac.gemm", "lilac.spmv_csr", "lilac.spmv_jds"]
     with pytest.raises(KeyError):
         reg.add("lilac.spmv_csr", lambda: None)
 

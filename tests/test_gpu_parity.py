@@ -524,3 +524,39 @@ def test_cg_solve_on_the_stencil_converges():
     assert np.abs(zh - 1.0).max() < 1e-8
     cg.free()
     A.free()
+
+
+# --------------------------------------------------------------------------------
+# gemm (kernels.lilac:14-19)
+# --------------------------------------------------------------------------------
+
+def test_gemm_exact_bitwise_vs_reference_golden():
+    """b200_gemm with exact BLAS vs the reference's lilac.gemm outputs."""
+    N.lib().b200_set_exact_blas(1)
+    for c in O.golden("interp_harness_seed424242.json")["cases"]:
+        g = c["gemm"]
+        n, m, p = g["n"], g["m"], g["p"]
+        out = np.full(n * m, np.nan)
+        H.gemm(n, m, out, p, np.array(g["a"]), np.array(g["b"]))
+        assert O.same_bits(out, np.array(g["c"], np.float64))
+
+
+@pytest.mark.parametrize("n,m,p", [(1, 1, 1), (7, 5, 3), (300, 200, 250), (512, 384, 1024), (33, 1, 0)])
+def test_gemm_fast_and_exact_vs_oracle(n, m, p):
+    rng = np.random.default_rng(n * 1000 + m + p)
+    a = rng.uniform(-2, 2, n * p)
+    b = rng.uniform(-2, 2, p * m)
+    ref = O.gemm(n, m, p, a, b)
+    scale = O.gemm(n, m, p, np.abs(a), np.abs(b))
+    out = np.full(n * m, np.nan)
+    H.gemm(n, m, out, p, a, b)  # cuBLAS DGEMM
+    assert (np.abs(out - ref) <= TOL * scale + (scale == 0) * 0).all()
+    N.lib().b200_set_exact_blas(1)
+    out2 = np.full(n * m, np.nan)
+    H.gemm(n, m, out2, p, a, b)
+    assert O.same_bits(out2, ref)
+
+
+def test_gemm_argument_checks():
+    with pytest.raises(ValueError):
+        H.gemm(4, 4, np.zeros(15), 4, np.zeros(16), np.zeros(16))

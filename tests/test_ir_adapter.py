@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SHIM = os.path.join(ROOT, "oracle", "_ref", "liblilac_ir_b200.so")
 IRDIR = os.path.join(ROOT, "tests", "golden", "ir")
 
-# the reference's kernels.lilac computations (fixtures/lilac/kernels.lilac:1-12)
+# the reference's kernels.lilac computations (fixtures/lilac/kernels.lilac:1-19)
 SPEC = b"""
 COMPUTATION spmv_csr
 forall (0 <= i < rows) {
@@ -32,6 +32,13 @@ result = dot (0 <= i < length) a[i] * b[i];
 COMPUTATION spmv_jds
 forall (0 <= i < rows) {
     output[i] = dot (0 <= k < nzcnt[perm[i]]) val[jd_ptr[k] + perm[i]] * x[col_ind[jd_ptr[k] + perm[i]]];
+}
+
+COMPUTATION gemm
+forall (0 <= i < n) {
+    forall (0 <= j < m) {
+        c[i * m + j] = dot (0 <= k < p) a[i * p + k] * b[k * m + j];
+    }
 }
 """
 
@@ -184,6 +191,28 @@ def test_reference_harness_reproduces_the_original_module():
         s.close()
 
 
+def gemm_session(n, m, p, seed):
+    rng = np.random.default_rng(seed)
+    s = Session("gemm_loops.lir", "gemm")
+    s.scalar(n)
+    s.scalar(m)
+    out = s.floats("out", np.zeros(max(n * m, 1)))
+    s.scalar(p)
+    s.floats("L", rng.uniform(-2, 2, max(n * p, 1)))
+    s.floats("R", rng.uniform(-2, 2, max(p * m, 1)))
+    return s, out
+
+
+def test_gemm_loops_rewritten_and_reproduced_by_the_reference_harness():
+    s, out = gemm_session(9, 7, 5, 1)
+    assert s.applied == 1
+    assert "call @lilac.gemm(%rows, %cols, %out, %inner, %L, %R)" in s.text(1)
+    s.run(0, NONE, "matmul")
+    y0 = s.read(out, 63)
+    s.run(1, REFERENCE, "matmul")
+    assert s.read(out, 63).tobytes() == y0.tobytes()
+
+
 def test_rewritten_module_needs_a_registered_harness():
     rp, ci, val, _ = sample5()
     s, _, _ = csr_session(rp, ci, val, np.ones(5))
@@ -280,3 +309,23 @@ def test_b200_registry_raises_out_of_bounds_like_the_reference():
         with pytest.raises(RuntimeError, match="OutOfBounds"):
             s.run(1, backend, "csr_rows")
         s.close()
+
+
+@pytest.mark.gpu
+def test_b200_registry_gemm_through_the_pipeline(exact_kernels):
+    s, out = gemm_session(40, 33, 27, 2)
+    s.run(0, NONE, "matmul")
+    y0 = s.read(out, 40 * 33)
+    s.run(1, B200, "matmul")
+    assert s.read(out, 40 * 33).tobytes() == y0.tobytes()
+
+
+@pytest.mark.gpu
+def test_b200_registry_gemm_fast_path_within_tolerance():
+    n, m, p = 64, 48, 80
+    s, out = gemm_session(n, m, p, 3)
+    s.run(0, NONE, "matmul")
+    y0 = s.read(out, n * m)
+    s.run(1, B200, "matmul")
+    y1 = s.read(out, n * m)
+    assert np.allclose(y1, y0, rtol=0, atol=1e-12 * 4 * p)

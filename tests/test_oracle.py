@@ -126,3 +126,13 @@ def test_oracle_matches_reference_harness_at_scale():
     assert b"OutOfBounds" in R.ref_last_error()
     R.ref_free(h)
     del C
+
+
+def test_oracle_gemm_matches_reference_harness_golden():
+    """orc_gemm vs the reference's lilac.gemm HarnessFn outputs
+    (test_interp.cpp:276-297 trials, seed 424242): bit-exact."""
+    cases = O.golden("interp_harness_seed424242.json")["cases"]
+    for c in cases:
+        g = c["gemm"]
+        out = O.gemm(g["n"], g["m"], g["p"], np.array(g["a"]), np.array(g["b"]))
+        assert O.same_bits(out, np.array(g["c"], np.float64))
