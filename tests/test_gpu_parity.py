@@ -537,7 +537,7 @@ def test_gemm_exact_bitwise_vs_reference_golden():
         g = c["gemm"]
         n, m, p = g["n"], g["m"], g["p"]
         out = np.full(n * m, np.nan)
-        H.gemm(n, m, out, p, np.array(g["a"]), np.array(g["b"]))
+        H.gemm(n, m, out, p, np.array(g["a"], np.float64), np.array(g["b"], np.float64))
         assert O.same_bits(out, np.array(g["c"], np.float64))
 
 

@@ -134,5 +134,5 @@ def test_oracle_gemm_matches_reference_harness_golden():
     cases = O.golden("interp_harness_seed424242.json")["cases"]
     for c in cases:
         g = c["gemm"]
-        out = O.gemm(g["n"], g["m"], g["p"], np.array(g["a"]), np.array(g["b"]))
+        out = O.gemm(g["n"], g["m"], g["p"], np.array(g["a"], np.float64), np.array(g["b"], np.float64))
         assert O.same_bits(out, np.array(g["c"], np.float64))
