@@ -42,6 +42,61 @@ int device_sms() {
 
 }  // namespace
 
+namespace {
+
+// Bank-pair of an f64 x entry in the smem slab (32 banks x 4 bytes).
+inline unsigned bank_pair(std::uint32_t key) { return (key & kKeyColMask) & 15u; }
+
+// The kernel gathers x for a 128-nonzero piece as 4 warp instructions (slot s
+// of every lane's 4 consecutive nonzeros); an 8-byte shared load is served
+// per half-warp, and its wavefronts grow with the number of lanes hitting the
+// same bank pair. Nonzeros of the same row are interchangeable inside a lane
+// (the lane-local sums do not care), so each lane's same-row groups are
+// permuted — greedily, lane by lane — to spread every slot's columns over the
+// 16 bank pairs. Row keys and continuation bits stay with their positions.
+void balance_gather_banks(double* val, std::uint32_t* key, std::int64_t lo, std::int64_t hi) {
+    static const int perms[24][4] = {
+        {0, 1, 2, 3}, {0, 1, 3, 2}, {0, 2, 1, 3}, {0, 2, 3, 1}, {0, 3, 1, 2}, {0, 3, 2, 1},
+        {1, 0, 2, 3}, {1, 0, 3, 2}, {1, 2, 0, 3}, {1, 2, 3, 0}, {1, 3, 0, 2}, {1, 3, 2, 0},
+        {2, 0, 1, 3}, {2, 0, 3, 1}, {2, 1, 0, 3}, {2, 1, 3, 0}, {2, 3, 0, 1}, {2, 3, 1, 0},
+        {3, 0, 1, 2}, {3, 0, 2, 1}, {3, 1, 0, 2}, {3, 1, 2, 0}, {3, 2, 0, 1}, {3, 2, 1, 0}};
+    for (std::int64_t c = lo; c < hi; c += 128) {
+        int cnt[4][2][16] = {};
+        for (int lane = 0; lane < 32; ++lane) {
+            const std::int64_t p = c + 4 * lane;
+            if (p + 4 > hi) break;
+            const int half = lane >> 4;
+            std::uint32_t k[4];
+            double v[4];
+            for (int e = 0; e < 4; ++e) {
+                k[e] = key[p + e];
+                v[e] = val[p + e];
+            }
+            int best = 0, best_score = 1 << 30;
+            for (int q = 0; q < 24; ++q) {
+                bool ok = true;  // only same-row exchanges
+                for (int e = 0; e < 4 && ok; ++e) ok = (k[perms[q][e]] >> 16) == (k[e] >> 16);
+                if (!ok) continue;
+                int score = 0;
+                for (int e = 0; e < 4; ++e) score += cnt[e][half][bank_pair(k[perms[q][e]])];
+                if (score < best_score) {
+                    best_score = score;
+                    best = q;
+                }
+            }
+            for (int e = 0; e < 4; ++e) {
+                const std::uint32_t src = k[perms[best][e]];
+                // the row bits and continuation bit belong to the position
+                key[p + e] = (k[e] & ~kKeyColMask) | (src & kKeyColMask);
+                val[p + e] = v[perms[best][e]];
+                ++cnt[e][half][bank_pair(src)];
+            }
+        }
+    }
+}
+
+}  // namespace
+
 bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, std::int64_t cols,
                  bool monotone, std::int64_t max_row, bool forced) {
     if (!monotone || rows <= 0) return false;
@@ -139,7 +194,12 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     h.val.assign(static_cast<std::size_t>(total), 0.0);
     h.key.assign(static_cast<std::size_t>(total), kPadKey);
 
-    // pass 2: offsets and scatter (slab-major, warp range, row order kept)
+    // pass 2: offsets and scatter (slab-major, warp range, row order kept),
+    // then the bank balancing of every run (LILAC_B200_TILED_BANKS=0: off)
+    const bool balance = [] {
+        const char* e = std::getenv("LILAC_B200_TILED_BANKS");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
     parallel_tiles(h.ntiles, [&](std::int64_t t) {
         const std::int64_t row0 = h.tile_row0[t];
         const std::int64_t tb = h.tile_base[t];
@@ -166,6 +226,9 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
                     last[run] = r;
                 }
             }
+        if (balance)
+            for (std::int64_t i = 0; i + 1 < per_tile; ++i)
+                balance_gather_banks(h.val.data() + tb, h.key.data() + tb, wo[i], wo[i + 1]);
     });
 }
 
