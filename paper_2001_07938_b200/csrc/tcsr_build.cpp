@@ -44,53 +44,42 @@ int device_sms() {
 
 namespace {
 
-// Bank-pair of an f64 x entry in the smem slab (32 banks x 4 bytes).
-inline unsigned bank_pair(std::uint32_t key) { return (key & kKeyColMask) & 15u; }
-
 // The kernel gathers x for a 128-nonzero piece as 4 warp instructions (slot s
 // of every lane's 4 consecutive nonzeros); an 8-byte shared load is served
 // per half-warp, and its wavefronts grow with the number of lanes hitting the
-// same bank pair. Nonzeros of the same row are interchangeable inside a lane
-// (the lane-local sums do not care), so each lane's same-row groups are
-// permuted — greedily, lane by lane — to spread every slot's columns over the
-// 16 bank pairs. Row keys and continuation bits stay with their positions.
+// same bank pair. The nonzeros of one row inside a piece are interchangeable
+// (the kernel's sums only need them grouped by row), so each row segment's
+// nonzeros are dealt to its positions greedily, each position taking the
+// remaining nonzero whose bank pair is least used by its (slot, half-warp).
+// Row keys and continuation bits stay with their positions.
 void balance_gather_banks(double* val, std::uint32_t* key, std::int64_t lo, std::int64_t hi) {
-    static const int perms[24][4] = {
-        {0, 1, 2, 3}, {0, 1, 3, 2}, {0, 2, 1, 3}, {0, 2, 3, 1}, {0, 3, 1, 2}, {0, 3, 2, 1},
-        {1, 0, 2, 3}, {1, 0, 3, 2}, {1, 2, 0, 3}, {1, 2, 3, 0}, {1, 3, 0, 2}, {1, 3, 2, 0},
-        {2, 0, 1, 3}, {2, 0, 3, 1}, {2, 1, 0, 3}, {2, 1, 3, 0}, {2, 3, 0, 1}, {2, 3, 1, 0},
-        {3, 0, 1, 2}, {3, 0, 2, 1}, {3, 1, 0, 2}, {3, 1, 2, 0}, {3, 2, 0, 1}, {3, 2, 1, 0}};
+    std::vector<std::pair<std::uint32_t, double>> pool;
     for (std::int64_t c = lo; c < hi; c += 128) {
+        const std::int64_t e = std::min<std::int64_t>(hi, c + 128);
         int cnt[4][2][16] = {};
-        for (int lane = 0; lane < 32; ++lane) {
-            const std::int64_t p = c + 4 * lane;
-            if (p + 4 > hi) break;
-            const int half = lane >> 4;
-            std::uint32_t k[4];
-            double v[4];
-            for (int e = 0; e < 4; ++e) {
-                k[e] = key[p + e];
-                v[e] = val[p + e];
-            }
-            int best = 0, best_score = 1 << 30;
-            for (int q = 0; q < 24; ++q) {
-                bool ok = true;  // only same-row exchanges
-                for (int e = 0; e < 4 && ok; ++e) ok = (k[perms[q][e]] >> 16) == (k[e] >> 16);
-                if (!ok) continue;
-                int score = 0;
-                for (int e = 0; e < 4; ++e) score += cnt[e][half][bank_pair(k[perms[q][e]])];
-                if (score < best_score) {
-                    best_score = score;
-                    best = q;
+        for (std::int64_t a = c; a < e;) {
+            std::int64_t b = a + 1;
+            while (b < e && (key[b] >> 16) == (key[a] >> 16)) ++b;
+            pool.clear();
+            for (std::int64_t q = a; q < b; ++q) pool.emplace_back(key[q] & kKeyColMask, val[q]);
+            for (std::int64_t q = a; q < b; ++q) {
+                const int off = static_cast<int>(q - c), slot = off & 3, half = (off >> 2) >> 4;
+                std::size_t best = 0;
+                int best_n = 1 << 30;
+                for (std::size_t u = 0; u < pool.size(); ++u) {
+                    const int n = cnt[slot][half][pool[u].first & 15u];
+                    if (n < best_n) {
+                        best_n = n;
+                        best = u;
+                    }
                 }
+                key[q] = (key[q] & ~kKeyColMask) | pool[best].first;
+                val[q] = pool[best].second;
+                ++cnt[slot][half][pool[best].first & 15u];
+                pool[best] = pool.back();
+                pool.pop_back();
             }
-            for (int e = 0; e < 4; ++e) {
-                const std::uint32_t src = k[perms[best][e]];
-                // the row bits and continuation bit belong to the position
-                key[p + e] = (k[e] & ~kKeyColMask) | (src & kKeyColMask);
-                val[p + e] = v[perms[best][e]];
-                ++cnt[e][half][bank_pair(src)];
-            }
+            a = b;
         }
     }
 }
