@@ -361,6 +361,35 @@ def e2e_harness_cg(rp, ci, val, n, shift, steps, writeback="eager"):
             "path": "b200_spmv_csr/b200_dot/b200_axpy/b200_xpay on pinned host arrays"}
 
 
+def e2e_dist(cg, shard_rows, shift, steps, stream, world):
+    """N > 1: each rank feeds its x slice from pinned host memory, runs one NPB
+    outer iteration through the sharded public API (b200_dist_cg_load_x /
+    _outer / _result) and reads zeta and rnorm back; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    rows = shard_rows[1] - shard_rows[0]
+    x = torch.ones(max(rows, 1), dtype=torch.float64, pin_memory=True)
+    sh = stream.cuda_stream
+
+    def step():
+        cg.load_x(x.data_ptr(), sh)
+        cg.outer(shift, CGITMAX, sh)
+        return cg.result()  # synchronises, copies the scalars back
+
+    for _ in range(3):
+        step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    secs = float(t.item())
+    return {"value": steps / secs, "unit": UNIT, "h2d_bytes_per_step": 8 * rows * world,
+            "d2h_bytes_per_step": 128 * world, "ms_per_step": 1e3 * secs / steps,
+            "path": "b200_dist_cg_load_x/_outer/_result per rank (x slice from pinned host, scalars back)"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -497,9 +526,8 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": 1.0 / t_iter, "unit": UNIT, "cores": threads, "kind": kind,
                                     "sample": desc, "cpu": model, "host_cpus": ncpu,
                                     "spmv_s": ts}
-    elif rank == 0:
-        line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                       "note": "measured at N=1 only"}
+    elif world > 1:
+        line["e2e"] = e2e_dist(cg, shard_rows, shift, args.e2e_steps * 10, stream, world)
     if rank == 0:
         print(json.dumps(line), flush=True)
     cg.free()

@@ -299,6 +299,9 @@ void b200_dist_cg_free(b200_dist_cg* d);
 int b200_dist_cg_reset(b200_dist_cg* d, void* stream);
 int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream);
 int b200_dist_cg_result(b200_dist_cg* d, double* zeta, double* rnorm);
+/* x of the shards held by this process (in shard order, i.e. its owned rows)
+ * from host memory (pinned for an asynchronous copy) on `stream`. */
+int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream);
 int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double* rnorm);
 int b200_dist_cg_info(const b200_dist_cg* d, int shard, int64_t* row0, int64_t* rows, int64_t* nnz,
                       int32_t* tiled);

@@ -295,6 +295,19 @@ int b200_dist_cg_reset(b200_dist_cg* d, void* stream) {
     });
 }
 
+int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream) {
+    return boundary("b200_dist_cg_load_x", [&] {
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        std::int64_t off = 0;
+        for (auto& s : d->shards) {
+            const std::size_t bytes = sizeof(double) * static_cast<std::size_t>(s->rows);
+            host_in(x_host + off, bytes);
+            if (bytes) B200_CUDA(cudaMemcpyAsync(s->v.x, x_host + off, bytes, cudaMemcpyHostToDevice, st));
+            off += s->rows;
+        }
+    });
+}
+
 int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream) {
     return boundary("b200_dist_cg_outer", [&] {
         dist_outer_graph(d, cgitmax, shift, stream ? static_cast<cudaStream_t>(stream) : d->stream);

@@ -200,6 +200,10 @@ class DistCG:
         N.check(N.lib().b200_dist_cg_result(self._h, C.byref(z), C.byref(r)))
         return z.value, r.value
 
+    def load_x(self, x_host_ptr: int, stream: int = 0):
+        """x of this process's shards from host memory (its owned rows)."""
+        N.check(N.lib().b200_dist_cg_load_x(self._h, C.c_void_p(x_host_ptr), C.c_void_p(stream)))
+
     def solve(self, b_ptr: int, iters: int, z_ptr: int = 0) -> float:
         """Plain CG on A z = b from z = 0 for `iters` steps; returns |b - A z|."""
         r = C.c_double()

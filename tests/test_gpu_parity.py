@@ -400,6 +400,24 @@ def test_sharded_cg_nccl_single_rank():
     d.free()
 
 
+def test_sharded_cg_load_x_from_host_matches_reset():
+    """b200_dist_cg_load_x (the e2e feed at N > 1): x = 1 from host memory
+    gives the outer iteration reset() gives, bit for bit."""
+    import torch
+    na, nonzer, niter, shift, _ = D.NPB_CLASSES["A"]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    d = D.DistCG.local(3, rp, ci, val)
+    d.reset()
+    d.outer(shift)
+    z_reset, r_reset = d.result()
+    x = torch.ones(na, dtype=torch.float64, pin_memory=True)
+    d.load_x(x.data_ptr())
+    d.outer(shift)
+    z_load, r_load = d.result()
+    assert z_load == z_reset and r_load == r_reset
+    d.free()
+
+
 def test_device_mirrors_serve_written_back_vectors_and_never_go_stale():
     """A harness output written back to the host is mirrored on the device;
     the next harness that reads those bytes gets them device-to-device, and
