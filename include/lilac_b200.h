@@ -302,6 +302,19 @@ int b200_dist_cg_result(b200_dist_cg* d, double* zeta, double* rnorm);
 /* x of the shards held by this process (in shard order, i.e. its owned rows)
  * from host memory (pinned for an asynchronous copy) on `stream`. */
 int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream);
+/* Peer-memory exchange (no collective library): each shard stores its scalar
+ * partials and its p / z slice straight into every peer's buffers and raises
+ * an epoch flag per sender; receivers wait on the flags (p2p.cu).
+ *  - local shards (b200_dist_cg_create_local): b200_dist_cg_use_p2p_local;
+ *  - one shard per process (b200_dist_cg_create_nccl): b200_dist_cg_p2p_export
+ *    writes this rank's three CUDA IPC handles (192 bytes), the caller
+ *    all-gathers them (rank-major) and passes all to b200_dist_cg_p2p_attach.
+ * A wait without progress for 5 s fails the next result call (DeviceError). */
+int b200_dist_cg_use_p2p_local(b200_dist_cg* d);
+int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out192);
+int b200_dist_cg_p2p_attach(b200_dist_cg* d, const void* handles);
+/* 0 local device copies, 1 NCCL, 2 peer memory. */
+int b200_dist_cg_transport(const b200_dist_cg* d);
 int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double* rnorm);
 int b200_dist_cg_info(const b200_dist_cg* d, int shard, int64_t* row0, int64_t* rows, int64_t* nnz,
                       int32_t* tiled);

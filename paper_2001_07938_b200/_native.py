@@ -105,6 +105,10 @@ SIGNATURES = {
     "b200_dist_cg_outer": (C.c_int, [vp, C.c_int, C.c_double, vp]),
     "b200_dist_cg_result": (C.c_int, [vp, f64p, f64p]),
     "b200_dist_cg_load_x": (C.c_int, [vp, vp, vp]),
+    "b200_dist_cg_use_p2p_local": (C.c_int, [vp]),
+    "b200_dist_cg_p2p_export": (C.c_int, [vp, vp]),
+    "b200_dist_cg_p2p_attach": (C.c_int, [vp, vp]),
+    "b200_dist_cg_transport": (C.c_int, [vp]),
     "b200_dist_npb": (C.c_int, [vp, C.c_int, C.c_double, f64p, f64p]),
     "b200_dist_cg_info": (C.c_int, [vp, C.c_int, i64p, i64p, i64p, C.POINTER(C.c_int32)]),
 }

@@ -58,9 +58,12 @@ struct b200_dist_cg {
     std::vector<std::unique_ptr<Shard>> shards;
     std::vector<std::int64_t> bounds;  // world + 1
     int world = 1;
+    int rank = 0;
+    int transport = 0;  // 0 local device copies, 1 NCCL, 2 peer memory
     std::int64_t n = 0;
     cudaStream_t stream = nullptr;
     int steps_exchanges = 0;
+    std::unique_ptr<PeerExchange> pending;  // exported, not attached yet
     // one outer iteration captured as a CUDA graph (kernels, exchange copies
     // and NCCL collectives alike), keyed by (stream, cgitmax, shift)
     cudaGraphExec_t graph = nullptr;
@@ -256,6 +259,7 @@ int b200_dist_cg_create_local(b200_dist_cg** out, int k, std::int64_t n, const s
             d->shards.push_back(std::move(s));
         }
         d->ex = std::make_unique<LocalExchange>(k);
+        d->transport = 0;
         *out = finish_create(d);
     });
 }
@@ -277,6 +281,8 @@ int b200_dist_cg_create_nccl(b200_dist_cg** out, int rank, int world, const void
         load_shard(*s, n, r0, r1 - r0, row_ptr, col_ind, val, world);
         d->shards.push_back(std::move(s));
         d->ex = std::make_unique<NcclExchange>(rank, world, nccl_id, d->bounds);
+        d->rank = rank;
+        d->transport = 1;
         *out = finish_create(d);
     });
 }
@@ -294,6 +300,68 @@ int b200_dist_cg_reset(b200_dist_cg* d, void* stream) {
         for (auto& s : d->shards) cg_launch_reset_x(s->v, st);
     });
 }
+
+}  // extern "C"
+
+namespace {
+
+PeerExchange::ShardBufs bufs_of(const Shard& s) {
+    PeerExchange::ShardBufs b;
+    b.p_full = s.v.p_full;
+    b.z_full = s.v.z_full;
+    b.row0 = s.row0;
+    b.rows = s.rows;
+    return b;
+}
+
+void drop_graph(b200_dist_cg* d) {
+    if (d->graph) cudaGraphExecDestroy(d->graph);
+    d->graph = nullptr;
+}
+
+void check_peer_errors(b200_dist_cg* d) {
+    if (d->transport != 2) return;
+    if (static_cast<PeerExchange*>(d->ex.get())->timed_out())
+        throw Error(Errc::DeviceError, "peer-memory exchange: a wait for a peer timed out");
+}
+
+}  // namespace
+
+extern "C" {
+
+int b200_dist_cg_use_p2p_local(b200_dist_cg* d) {
+    return boundary("b200_dist_cg_use_p2p_local", [&] {
+        if (d->transport != 0) throw Error(Errc::DataError, "peer memory between local shards only");
+        std::vector<PeerExchange::ShardBufs> b;
+        for (auto& s : d->shards) b.push_back(bufs_of(*s));
+        B200_CUDA(cudaStreamSynchronize(d->stream));
+        d->ex = std::make_unique<PeerExchange>(b);
+        d->transport = 2;
+        drop_graph(d);
+    });
+}
+
+int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out192) {
+    return boundary("b200_dist_cg_p2p_export", [&] {
+        if (d->transport != 1 || d->shards.size() != 1)
+            throw Error(Errc::DataError, "IPC export: one shard per process (the NCCL driver)");
+        d->pending = std::make_unique<PeerExchange>(d->rank, d->world, bufs_of(*d->shards[0]));
+        d->pending->export_handles(out192);
+    });
+}
+
+int b200_dist_cg_p2p_attach(b200_dist_cg* d, const void* handles) {
+    return boundary("b200_dist_cg_p2p_attach", [&] {
+        if (!d->pending) throw Error(Errc::DataError, "call b200_dist_cg_p2p_export first");
+        d->pending->attach(handles);
+        B200_CUDA(cudaDeviceSynchronize());
+        d->ex = std::move(d->pending);
+        d->transport = 2;
+        drop_graph(d);
+    });
+}
+
+int b200_dist_cg_transport(const b200_dist_cg* d) { return d ? d->transport : -1; }
 
 int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream) {
     return boundary("b200_dist_cg_load_x", [&] {
@@ -318,6 +386,7 @@ int b200_dist_cg_result(b200_dist_cg* d, double* zeta, double* rnorm) {
     return boundary("b200_dist_cg_result", [&] {
         CgScalars sc;
         B200_CUDA(cudaDeviceSynchronize());
+        check_peer_errors(d);
         B200_CUDA(cudaMemcpy(&sc, d->shards[0]->v.sc, sizeof sc, cudaMemcpyDeviceToHost));
         if (zeta) *zeta = sc.zeta;
         if (rnorm) *rnorm = sc.rnorm;
@@ -332,6 +401,7 @@ int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double
         for (auto& s : d->shards) cg_launch_reset_x(s->v, st);
         for (int it = 0; it < niter; ++it) dist_outer_graph(d, 25, shift, st);
         B200_CUDA(cudaStreamSynchronize(st));
+        check_peer_errors(d);
         CgScalars sc;
         B200_CUDA(cudaMemcpy(&sc, d->shards[0]->v.sc, sizeof sc, cudaMemcpyDeviceToHost));
         if (zeta) *zeta = sc.zeta;

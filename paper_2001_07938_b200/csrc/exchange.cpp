@@ -2,10 +2,13 @@
 // CG driver. See exchange.hpp.
 
 #include "exchange.hpp"
+#include "runtime.hpp"
 
 #include <nccl.h>
 
 #include <dlfcn.h>
+
+#include <cstring>
 
 #include <mutex>
 #include <string>
@@ -129,6 +132,139 @@ void NcclExchange::exchange_vector(std::vector<ShardView>& shards, std::vector<d
                    "ncclBroadcast");
     }
     check_nccl(nccl().GroupEnd(), "ncclGroupEnd");
+}
+
+// ---- PeerExchange --------------------------------------------------------------------
+
+namespace {
+
+PeerPtrs peer_of(double* p_full, double* z_full, char* mbox) {
+    PeerPtrs pp;
+    pp.p_full = p_full;
+    pp.z_full = z_full;
+    pp.gathered = reinterpret_cast<double*>(mbox + kMboxGathered);
+    pp.flags = reinterpret_cast<unsigned long long*>(mbox + kMboxFlags);
+    return pp;
+}
+
+}  // namespace
+
+Mailbox PeerExchange::mailbox(const Local& l) const {
+    char* b = l.mbox.as<char>();
+    Mailbox mb;
+    mb.gathered = reinterpret_cast<double*>(b + kMboxGathered);
+    mb.flags = reinterpret_cast<unsigned long long*>(b + kMboxFlags);
+    mb.epoch = reinterpret_cast<unsigned long long*>(b + kMboxEpoch);
+    mb.ticket = reinterpret_cast<unsigned int*>(b + kMboxTicket);
+    mb.err = reinterpret_cast<int*>(b + kMboxErr);
+    return mb;
+}
+
+void PeerExchange::upload_table(Local& l, const std::vector<PeerPtrs>& peers) {
+    l.table.ensure(sizeof(PeerPtrs) * peers.size());
+    B200_CUDA(cudaMemcpyAsync(l.table.ptr, peers.data(), sizeof(PeerPtrs) * peers.size(), cudaMemcpyHostToDevice,
+                              rt().stream));
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
+}
+
+PeerExchange::PeerExchange(const std::vector<ShardBufs>& local) : world_(static_cast<int>(local.size())) {
+    if (world_ < 1 || world_ > kP2pMaxWorld) throw Error(Errc::DataError, "peer exchange: 1..64 shards");
+    shards_.resize(local.size());
+    std::vector<PeerPtrs> peers;
+    for (int i = 0; i < world_; ++i) {
+        Local& l = shards_[i];
+        l.rank = i;
+        l.bufs = local[i];
+        l.mbox.ensure(kMboxBytes);
+        B200_CUDA(cudaMemsetAsync(l.mbox.ptr, 0, kMboxBytes, rt().stream));
+        peers.push_back(peer_of(l.bufs.p_full, l.bufs.z_full, l.mbox.as<char>()));
+    }
+    for (Local& l : shards_) upload_table(l, peers);
+}
+
+PeerExchange::PeerExchange(int rank, int world, const ShardBufs& mine) : world_(world) {
+    if (world < 1 || world > kP2pMaxWorld || rank < 0 || rank >= world)
+        throw Error(Errc::DataError, "peer exchange: bad rank/world");
+    shards_.resize(1);
+    Local& l = shards_[0];
+    l.rank = rank;
+    l.bufs = mine;
+    l.mbox.ensure(kMboxBytes);
+    B200_CUDA(cudaMemsetAsync(l.mbox.ptr, 0, kMboxBytes, rt().stream));
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
+}
+
+PeerExchange::~PeerExchange() {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    for (Local& l : shards_) {
+        l.mbox.release();
+        l.table.release();
+    }
+}
+
+void PeerExchange::export_handles(void* out192) const {
+    if (shards_.size() != 1) throw Error(Errc::DataError, "IPC export needs one shard per process");
+    const Local& l = shards_[0];
+    auto* o = static_cast<char*>(out192);
+    cudaIpcMemHandle_t h;
+    for (int k = 0; k < 3; ++k) {
+        void* base = k == 0 ? static_cast<void*>(l.bufs.p_full)
+                            : (k == 1 ? static_cast<void*>(l.bufs.z_full) : l.mbox.ptr);
+        B200_CUDA(cudaIpcGetMemHandle(&h, base));
+        static_assert(sizeof h == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(o + 64 * k, &h, sizeof h);
+    }
+}
+
+void PeerExchange::attach(const void* handles) {
+    if (shards_.size() != 1) throw Error(Errc::DataError, "IPC attach needs one shard per process");
+    Local& l = shards_[0];
+    const auto* in = static_cast<const char*>(handles);
+    std::vector<PeerPtrs> peers;
+    for (int r = 0; r < world_; ++r) {
+        if (r == l.rank) {
+            peers.push_back(peer_of(l.bufs.p_full, l.bufs.z_full, l.mbox.as<char>()));
+            continue;
+        }
+        void* m[3];
+        for (int k = 0; k < 3; ++k) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, in + 192 * r + 64 * k, sizeof h);
+            B200_CUDA(cudaIpcOpenMemHandle(&m[k], h, cudaIpcMemLazyEnablePeerAccess));
+            opened_.push_back(m[k]);
+        }
+        peers.push_back(peer_of(static_cast<double*>(m[0]), static_cast<double*>(m[1]), static_cast<char*>(m[2])));
+    }
+    upload_table(l, peers);
+}
+
+void PeerExchange::exchange_scalars(std::vector<ShardView>& views, int npart) {
+    if (npart > kP2pMaxPart) throw Error(Errc::DataError, "peer exchange: too many scalars");
+    for (std::size_t i = 0; i < shards_.size(); ++i)
+        p2p_push_scalars(views[i].partial, npart, shards_[i].table.as<PeerPtrs>(), world_, shards_[i].rank,
+                         mailbox(shards_[i]), views[i].stream);
+    for (std::size_t i = 0; i < shards_.size(); ++i)
+        p2p_wait(world_, mailbox(shards_[i]), npart, views[i].gathered, views[i].stream);
+}
+
+void PeerExchange::exchange_vector(std::vector<ShardView>& views, std::vector<double*> fulls) {
+    for (std::size_t i = 0; i < shards_.size(); ++i) {
+        const Local& l = shards_[i];
+        const bool z = fulls[i] == l.bufs.z_full;
+        p2p_push_vector(fulls[i] + l.bufs.row0, l.bufs.rows, l.bufs.row0, l.table.as<PeerPtrs>(), world_, l.rank, z,
+                        mailbox(l), views[i].stream);
+    }
+    for (std::size_t i = 0; i < shards_.size(); ++i)
+        p2p_wait(world_, mailbox(shards_[i]), 0, nullptr, views[i].stream);
+}
+
+bool PeerExchange::timed_out() const {
+    for (const Local& l : shards_) {
+        int e = 0;
+        B200_CUDA(cudaMemcpy(&e, mailbox(l).err, sizeof e, cudaMemcpyDeviceToHost));
+        if (e) return true;
+    }
+    return false;
 }
 
 }  // namespace b200

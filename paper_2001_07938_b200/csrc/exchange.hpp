@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "p2p.hpp"
+
 namespace b200 {
 
 struct ShardView {
@@ -59,6 +61,46 @@ private:
     int rank_, world_;
     void* comm_ = nullptr;
     std::vector<std::int64_t> bounds_;
+};
+
+// Peer-memory exchange (p2p.cu): each shard pushes into its peers' replicas
+// and mailboxes and waits on per-sender epoch flags. Either k shards of this
+// process (peers addressed directly) or one shard per process (peers mapped
+// with CUDA IPC: export() this shard's three handles, attach() everyone's).
+class PeerExchange : public Exchange {
+public:
+    struct ShardBufs {
+        double* p_full;
+        double* z_full;
+        std::int64_t row0, rows;
+    };
+    // k local shards, ranks 0..k-1
+    explicit PeerExchange(const std::vector<ShardBufs>& local);
+    // one shard of `world` (this process), peers attached later
+    PeerExchange(int rank, int world, const ShardBufs& mine);
+    ~PeerExchange() override;
+    int nshards() const override { return static_cast<int>(shards_.size()); }
+    void exchange_scalars(std::vector<ShardView>& shards, int npart) override;
+    void exchange_vector(std::vector<ShardView>& shards, std::vector<double*> fulls) override;
+    // IPC: three 64-byte handles (p_full, z_full, mailbox) of this shard
+    void export_handles(void* out192) const;
+    // handles of all `world` ranks (rank-major, 192 bytes each); maps the others
+    void attach(const void* handles);
+    // a wait timed out somewhere (checked after a run)
+    bool timed_out() const;
+
+private:
+    struct Local {
+        int rank = 0;
+        ShardBufs bufs{};
+        DevBuf mbox;
+        DevBuf table;  // world PeerPtrs
+    };
+    void upload_table(Local& l, const std::vector<PeerPtrs>& peers);
+    Mailbox mailbox(const Local& l) const;
+    std::vector<Local> shards_;
+    int world_ = 1;
+    std::vector<void*> opened_;  // IPC mappings to close
 };
 
 void nccl_unique_id(void* out128);

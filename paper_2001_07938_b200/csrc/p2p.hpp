@@ -1,0 +1,47 @@
+#pragma once
+// p2p.hpp — peer-memory exchange of the sharded CG driver (p2p.cu).
+
+#include "b200.hpp"
+
+#include <cstdint>
+
+namespace b200 {
+
+constexpr int kP2pMaxWorld = 64;
+constexpr int kP2pMaxPart = 2;
+
+// Where a shard receives: its p / z replicas and its mailbox (scalar slots +
+// one flag per sender). A PeerPtrs table (device memory) lists every shard's,
+// as this shard sees them (IPC mappings for other processes).
+struct PeerPtrs {
+    double* p_full;
+    double* z_full;
+    double* gathered;             // [2][kP2pMaxWorld][kP2pMaxPart]
+    unsigned long long* flags;    // [kP2pMaxWorld]
+};
+
+// This shard's own mailbox words (device memory).
+struct Mailbox {
+    double* gathered;
+    unsigned long long* flags;
+    unsigned long long* epoch;    // exchanges done by this shard
+    unsigned int* ticket;         // last-CTA detection of the vector push
+    int* err;                     // set when a wait timed out
+};
+
+// Mailbox block layout (one allocation, exported by CUDA IPC).
+constexpr std::size_t kMboxGathered = 0;
+constexpr std::size_t kMboxFlags = sizeof(double) * 2 * kP2pMaxWorld * kP2pMaxPart;
+constexpr std::size_t kMboxEpoch = kMboxFlags + sizeof(unsigned long long) * kP2pMaxWorld;
+constexpr std::size_t kMboxTicket = kMboxEpoch + sizeof(unsigned long long);
+constexpr std::size_t kMboxErr = kMboxTicket + sizeof(unsigned int);
+constexpr std::size_t kMboxBytes = 4096;
+static_assert(kMboxErr + sizeof(int) <= kMboxBytes, "mailbox layout");
+
+void p2p_push_scalars(const double* partial, int npart, const PeerPtrs* peers, int world, int rank, Mailbox mb,
+                      cudaStream_t s);
+void p2p_push_vector(const double* src, std::int64_t rows, std::int64_t row0, const PeerPtrs* peers, int world,
+                     int rank, bool z, Mailbox mb, cudaStream_t s);
+void p2p_wait(int world, Mailbox mb, int npart, double* out, cudaStream_t s);
+
+}  // namespace b200

@@ -200,6 +200,24 @@ class DistCG:
         N.check(N.lib().b200_dist_cg_result(self._h, C.byref(z), C.byref(r)))
         return z.value, r.value
 
+    def use_p2p_local(self):
+        """Exchange between the local shards through peer memory (p2p.cu)."""
+        N.check(N.lib().b200_dist_cg_use_p2p_local(self._h))
+
+    def p2p_export(self) -> bytes:
+        """This rank's three CUDA IPC handles (192 bytes) for p2p_attach."""
+        buf = C.create_string_buffer(192)
+        N.check(N.lib().b200_dist_cg_p2p_export(self._h, buf))
+        return buf.raw
+
+    def p2p_attach(self, handles: bytes):
+        """All ranks' handles, rank-major (world x 192 bytes)."""
+        N.check(N.lib().b200_dist_cg_p2p_attach(self._h, C.create_string_buffer(bytes(handles), len(handles))))
+
+    @property
+    def transport(self) -> str:
+        return {0: "local", 1: "nccl", 2: "p2p"}.get(N.lib().b200_dist_cg_transport(self._h), "?")
+
     def load_x(self, x_host_ptr: int, stream: int = 0):
         """x of this process's shards from host memory (its owned rows)."""
         N.check(N.lib().b200_dist_cg_load_x(self._h, C.c_void_p(x_host_ptr), C.c_void_p(stream)))

@@ -400,6 +400,40 @@ def test_sharded_cg_nccl_single_rank():
     d.free()
 
 
+@pytest.mark.parametrize("cls,k", [("S", 2), ("A", 3), ("A", 8), ("C", 4)])
+def test_sharded_cg_peer_memory_exchange_local(cls, k):
+    """Peer-memory exchange between local shards (the kernels the IPC path
+    runs between processes): zeta bit-identical to the device-copy exchange
+    (same partials, same rank-order sums)."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    d0 = D.DistCG.local(k, rp, ci, val)
+    z0, r0 = d0.npb(niter, shift)
+    d0.free()
+    d = D.DistCG.local(k, rp, ci, val)
+    d.use_p2p_local()
+    assert d.transport == "p2p"
+    z1, r1 = d.npb(niter, shift)
+    assert abs(z1 - zeta_ref) / zeta_ref <= 1e-10
+    assert z1 == z0 and r1 == r0
+    d.free()
+
+
+def test_sharded_cg_peer_memory_ipc_single_rank():
+    """The IPC export/attach path with world = 1 (no peer to map; exercises
+    cudaIpcGetMemHandle and the switch of transport)."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES["S"]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    d = D.DistCG.nccl(0, 1, D.DistCG.nccl_id(), na, np.array([0, na], np.int64), rp, ci, val)
+    h = d.p2p_export()
+    assert len(h) == 192
+    d.p2p_attach(h)
+    assert d.transport == "p2p"
+    zeta, _ = d.npb(niter, shift)
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10
+    d.free()
+
+
 def test_sharded_cg_load_x_from_host_matches_reset():
     """b200_dist_cg_load_x (the e2e feed at N > 1): x = 1 from host memory
     gives the outer iteration reset() gives, bit for bit."""

@@ -17,6 +17,8 @@ na, nonzer, niter, shift, zref = D.NPB_CLASSES[cls]
 N.check(N.lib().b200_init(0))
 rp, ci, val = D.gen_npb(na, nonzer, shift)
 d = D.DistCG.local(k, rp, ci, val)
+if os.environ.get("DIST_P2P", "0") == "1":
+    d.use_p2p_local()
 s = torch.cuda.Stream()
 d.reset(s.cuda_stream)
 for _ in range(3):
@@ -30,5 +32,5 @@ for _ in range(10):
 e1.record(s)
 host = (time.perf_counter() - t0) / 10
 torch.cuda.synchronize()
-print(f"k={k} class {cls} graph={os.environ.get('LILAC_B200_DIST_GRAPH', '1')}: "
+print(f"k={k} class {cls} transport={d.transport} graph={os.environ.get('LILAC_B200_DIST_GRAPH', '1')}: "
       f"{e0.elapsed_time(e1) / 10:.3f} ms/outer (host issue {host * 1e3:.3f} ms)")
