@@ -177,8 +177,15 @@ void dist_outer(b200_dist_cg* d, int cgitmax, double shift, cudaStream_t st) {
         gather_scalars(d, st, 1, CgFin::Alpha, 0.0);
         for (auto& s : d->shards) cg_launch_update_zr(s->v, st);
         gather_scalars(d, st, 1, CgFin::Beta, 0.0);
-        for (auto& s : d->shards) cg_launch_update_p(s->v, st);
-        gather_vector(d, st, false);
+        {
+            auto vs = views(d, st);
+            std::vector<const CgVectors*> cv;
+            for (auto& s : d->shards) cv.push_back(&s->v);
+            if (!d->ex->update_p_exchange(vs, cv)) {  // not fused: update, then exchange
+                for (auto& s : d->shards) cg_launch_update_p(s->v, st);
+                gather_vector(d, st, false);
+            }
+        }
     }
     gather_vector(d, st, true);  // residual r = A z needs all of z
     for (auto& s : d->shards) {

@@ -258,6 +258,15 @@ void PeerExchange::exchange_vector(std::vector<ShardView>& views, std::vector<do
         p2p_wait(world_, mailbox(shards_[i]), 0, nullptr, views[i].stream);
 }
 
+bool PeerExchange::update_p_exchange(std::vector<ShardView>& views, const std::vector<const CgVectors*>& v) {
+    for (std::size_t i = 0; i < shards_.size(); ++i)
+        p2p_update_p_push(*v[i], shards_[i].table.as<PeerPtrs>(), world_, shards_[i].rank, mailbox(shards_[i]),
+                          views[i].stream);
+    for (std::size_t i = 0; i < shards_.size(); ++i)
+        p2p_wait(world_, mailbox(shards_[i]), 0, nullptr, views[i].stream);
+    return true;
+}
+
 bool PeerExchange::timed_out() const {
     for (const Local& l : shards_) {
         int e = 0;

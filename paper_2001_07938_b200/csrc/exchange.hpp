@@ -33,6 +33,13 @@ public:
     virtual void exchange_scalars(std::vector<ShardView>& shards, int npart) = 0;
     // every shard's full[row0_r .. row0_r+rows_r) = shard r's slice.
     virtual void exchange_vector(std::vector<ShardView>& shards, std::vector<double*> fulls) = 0;
+    // The CG p update fused with its exchange, if this transport can; false =
+    // the caller runs the update and exchange_vector.
+    virtual bool update_p_exchange(std::vector<ShardView>& shards, const std::vector<const CgVectors*>& v) {
+        (void)shards;
+        (void)v;
+        return false;
+    }
 };
 
 class LocalExchange : public Exchange {
@@ -82,6 +89,7 @@ public:
     int nshards() const override { return static_cast<int>(shards_.size()); }
     void exchange_scalars(std::vector<ShardView>& shards, int npart) override;
     void exchange_vector(std::vector<ShardView>& shards, std::vector<double*> fulls) override;
+    bool update_p_exchange(std::vector<ShardView>& shards, const std::vector<const CgVectors*>& v) override;
     // IPC: three 64-byte handles (p_full, z_full, mailbox) of this shard
     void export_handles(void* out192) const;
     // handles of all `world` ranks (rank-major, 192 bytes each); maps the others

@@ -80,6 +80,28 @@ __global__ void k_push_vector(const double* __restrict__ src, std::int64_t rows,
     raise_flags(peers, world, rank, mb);
 }
 
+// p = r + beta*p over this shard's rows, each new value stored locally and
+// into every peer's replica in the same pass (the CG p update fused with its
+// exchange); the last CTA raises the flags
+__global__ void k_update_p_push(CgVectors v, const PeerPtrs* __restrict__ peers, int world, int rank, Mailbox mb) {
+    const double beta = v.sc->beta;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < v.n; i += stride) {
+        const double pv = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
+        v.p[i] = pv;
+        for (int r = 0; r < world; ++r)
+            if (r != rank) peers[r].p_full[v.row0 + i] = pv;
+    }
+    __threadfence_system();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(mb.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    *mb.ticket = 0u;
+    raise_flags(peers, world, rank, mb);
+}
+
 // waits for every sender's flag to reach this shard's epoch; for a scalar
 // exchange copies the epoch's slot into `out` (rank-major, npart each)
 __global__ void k_wait(int world, Mailbox mb, int npart, double* __restrict__ out) {
@@ -115,6 +137,13 @@ void p2p_push_vector(const double* src, std::int64_t rows, std::int64_t row0, co
     const unsigned grid =
         static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((rows + 255) / 256, 148)));
     k_push_vector<<<grid, 256, 0, s>>>(src, rows, row0, peers, world, rank, z ? 1 : 0, mb);
+    B200_CUDA(cudaGetLastError());
+}
+
+void p2p_update_p_push(const CgVectors& v, const PeerPtrs* peers, int world, int rank, Mailbox mb, cudaStream_t s) {
+    const unsigned grid =
+        static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((v.n + 511) / 512, 148 * 4)));
+    k_update_p_push<<<grid, 256, 0, s>>>(v, peers, world, rank, mb);
     B200_CUDA(cudaGetLastError());
 }
 

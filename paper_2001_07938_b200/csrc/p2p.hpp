@@ -43,5 +43,7 @@ void p2p_push_scalars(const double* partial, int npart, const PeerPtrs* peers, i
 void p2p_push_vector(const double* src, std::int64_t rows, std::int64_t row0, const PeerPtrs* peers, int world,
                      int rank, bool z, Mailbox mb, cudaStream_t s);
 void p2p_wait(int world, Mailbox mb, int npart, double* out, cudaStream_t s);
+// the CG p update (p = r + beta*p, own rows) fused with the push of the slice
+void p2p_update_p_push(const CgVectors& v, const PeerPtrs* peers, int world, int rank, Mailbox mb, cudaStream_t s);
 
 }  // namespace b200
