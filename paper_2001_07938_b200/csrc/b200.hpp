@@ -222,6 +222,9 @@ struct CgScalars {  // device-resident, one per solver (shard)
     int nranks;     // > 1: sharded mode — reductions stop at this shard's partial (part[]); exchange + fin_* follow
     int pad;
     double part[4];
+    // peer-memory exchange (p2p.hpp P2pDesc, device memory) or null: when set,
+    // the kernel that produces the partials also pushes them to the peers
+    const void* p2p;
 };
 
 struct CgVectors {

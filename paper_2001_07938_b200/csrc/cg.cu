@@ -10,6 +10,8 @@
 // the scalar NPB loop bit for bit; only the dot products reassociate.
 
 #include "b200.hpp"
+#include "cg_fin.cuh"
+#include "p2p.hpp"
 
 #include <algorithm>
 
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(CgVectors v) {
     double part[1] = {rr}, tot[1];
     if (finish<1>(part, v.partials, &v.sc->ticket[1], tot) && threadIdx.x == 0) {
         if (v.sc->nranks > 1)
-            v.sc->part[0] = tot[0];
+            p2p_publish(v.sc, tot, 1);
         else
             v.sc->rho = tot[0];
     }
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_update_zr(CgVectors v) {
     double part[1] = {rr}, tot[1];
     if (finish<1>(part, v.partials, &v.sc->ticket[1], tot) && threadIdx.x == 0) {
         if (v.sc->nranks > 1) {
-            v.sc->part[0] = tot[0];
+            p2p_publish(v.sc, tot, 1);
         } else {
             v.sc->rho = tot[0];
             v.sc->beta = tot[0] / v.sc->rho0;
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_resid(CgVectors v) {
     double part[1] = {s}, tot[1];
     if (finish<1>(part, v.partials, &v.sc->ticket[2], tot) && threadIdx.x == 0) {
         if (v.sc->nranks > 1)
-            v.sc->part[0] = tot[0];
+            p2p_publish(v.sc, tot, 1);
         else
             v.sc->rnorm = sqrt(tot[0]);
     }
@@ -138,8 +140,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_norms(CgVectors v, double shift
     double part[2] = {a, b}, tot[2];
     if (finish<2>(part, v.partials, &v.sc->ticket[3], tot) && threadIdx.x == 0) {
         if (v.sc->nranks > 1) {
-            v.sc->part[0] = tot[0];
-            v.sc->part[1] = tot[1];
+            p2p_publish(v.sc, tot, 2);
         } else {
             v.sc->t1 = tot[0];
             v.sc->t2 = 1.0 / sqrt(tot[1]);
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_dot_scalars(const double* __res
     double part[1] = {a}, tot[1];
     if (finish<1>(part, partials, ticket, tot) && threadIdx.x == 0) {
         if (sc->nranks > 1) {
-            sc->part[0] = tot[0];
+            p2p_publish(sc, tot, 1);
         } else {
             sc->d = tot[0];
             sc->rho0 = sc->rho;
@@ -169,30 +170,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_dot_scalars(const double* __res
 // Sharded finalisation: sum the shards' partials in rank order (deterministic).
 __global__ void k_cg_fin(int what, CgScalars* sc, const double* __restrict__ g, int nranks, double shift) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int stride = what == static_cast<int>(CgFin::Norms) ? 2 : 1;
-    double a = 0.0, b = 0.0;
-    for (int r = 0; r < nranks; ++r) {
-        a += g[r * stride];
-        if (stride == 2) b += g[r * stride + 1];
-    }
-    switch (static_cast<CgFin>(what)) {
-    case CgFin::Rho: sc->rho = a; break;
-    case CgFin::Alpha:
-        sc->d = a;
-        sc->rho0 = sc->rho;
-        sc->alpha = sc->rho / a;
-        break;
-    case CgFin::Beta:
-        sc->rho = a;
-        sc->beta = a / sc->rho0;
-        break;
-    case CgFin::Rnorm: sc->rnorm = sqrt(a); break;
-    case CgFin::Norms:
-        sc->t1 = a;
-        sc->t2 = 1.0 / sqrt(b);
-        sc->zeta = shift + 1.0 / a;
-        break;
-    }
+    cg_fin_apply(what, sc, g, nranks, shift);
 }
 
 __global__ void __launch_bounds__(kThreads) k_cg_scale_x(CgVectors v) {

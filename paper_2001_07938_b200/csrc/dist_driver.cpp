@@ -157,6 +157,9 @@ std::vector<ShardView> views(b200_dist_cg* d, cudaStream_t st) {
 
 void gather_scalars(b200_dist_cg* d, cudaStream_t st, int npart, CgFin fin, double shift) {
     auto vs = views(d, st);
+    std::vector<CgScalars*> scs;
+    for (auto& s : d->shards) scs.push_back(s->v.sc);
+    if (d->ex->scalars_fin(vs, npart, fin, scs, shift)) return;  // pushed by the producers; wait + fin
     d->ex->exchange_scalars(vs, npart);
     for (auto& s : d->shards) cg_launch_fin(fin, s->v.sc, s->gathered.as<double>(), d->world, shift, st);
 }
@@ -342,7 +345,11 @@ int b200_dist_cg_use_p2p_local(b200_dist_cg* d) {
         std::vector<PeerExchange::ShardBufs> b;
         for (auto& s : d->shards) b.push_back(bufs_of(*s));
         B200_CUDA(cudaStreamSynchronize(d->stream));
-        d->ex = std::make_unique<PeerExchange>(b);
+        auto px = std::make_unique<PeerExchange>(b);
+        std::vector<CgScalars*> scs;
+        for (auto& s : d->shards) scs.push_back(s->v.sc);
+        px->bind_producers(scs);
+        d->ex = std::move(px);
         d->transport = 2;
         drop_graph(d);
     });
@@ -361,6 +368,7 @@ int b200_dist_cg_p2p_attach(b200_dist_cg* d, const void* handles) {
     return boundary("b200_dist_cg_p2p_attach", [&] {
         if (!d->pending) throw Error(Errc::DataError, "call b200_dist_cg_p2p_export first");
         d->pending->attach(handles);
+        d->pending->bind_producers({d->shards[0]->v.sc});
         B200_CUDA(cudaDeviceSynchronize());
         d->ex = std::move(d->pending);
         d->transport = 2;

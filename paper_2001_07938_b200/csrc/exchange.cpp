@@ -8,6 +8,7 @@
 
 #include <dlfcn.h>
 
+#include <cstddef>
 #include <cstring>
 
 #include <mutex>
@@ -199,6 +200,7 @@ PeerExchange::~PeerExchange() {
     for (Local& l : shards_) {
         l.mbox.release();
         l.table.release();
+        l.desc.release();
     }
 }
 
@@ -265,6 +267,30 @@ bool PeerExchange::update_p_exchange(std::vector<ShardView>& views, const std::v
     for (std::size_t i = 0; i < shards_.size(); ++i)
         p2p_wait(world_, mailbox(shards_[i]), 0, nullptr, views[i].stream);
     return true;
+}
+
+bool PeerExchange::scalars_fin(std::vector<ShardView>& views, int npart, CgFin fin, const std::vector<CgScalars*>& sc,
+                               double shift) {
+    for (std::size_t i = 0; i < shards_.size(); ++i)
+        p2p_wait_fin(world_, mailbox(shards_[i]), npart, static_cast<int>(fin), sc[i], shift, views[i].stream);
+    return true;
+}
+
+void PeerExchange::bind_producers(const std::vector<CgScalars*>& sc) {
+    for (std::size_t i = 0; i < shards_.size(); ++i) {
+        Local& l = shards_[i];
+        P2pDesc d;
+        d.peers = l.table.as<PeerPtrs>();
+        d.mb = mailbox(l);
+        d.world = world_;
+        d.rank = l.rank;
+        l.desc.ensure(sizeof d);
+        B200_CUDA(cudaMemcpyAsync(l.desc.ptr, &d, sizeof d, cudaMemcpyHostToDevice, rt().stream));
+        const void* dp = l.desc.ptr;
+        B200_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(sc[i]) + offsetof(CgScalars, p2p), &dp, sizeof dp,
+                                  cudaMemcpyHostToDevice, rt().stream));
+    }
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
 }
 
 bool PeerExchange::timed_out() const {

@@ -40,6 +40,18 @@ public:
         (void)v;
         return false;
     }
+    // Receive side of a scalar exchange whose partials the producing kernels
+    // already pushed, fused with the finalisation, if this transport can;
+    // false = the caller runs exchange_scalars + fin.
+    virtual bool scalars_fin(std::vector<ShardView>& shards, int npart, CgFin fin, const std::vector<CgScalars*>& sc,
+                             double shift) {
+        (void)shards;
+        (void)npart;
+        (void)fin;
+        (void)sc;
+        (void)shift;
+        return false;
+    }
 };
 
 class LocalExchange : public Exchange {
@@ -90,6 +102,11 @@ public:
     void exchange_scalars(std::vector<ShardView>& shards, int npart) override;
     void exchange_vector(std::vector<ShardView>& shards, std::vector<double*> fulls) override;
     bool update_p_exchange(std::vector<ShardView>& shards, const std::vector<const CgVectors*>& v) override;
+    bool scalars_fin(std::vector<ShardView>& shards, int npart, CgFin fin, const std::vector<CgScalars*>& sc,
+                     double shift) override;
+    // point each shard's CgScalars::p2p at its descriptor: its producing
+    // kernels then push their partials themselves
+    void bind_producers(const std::vector<CgScalars*>& sc);
     // IPC: three 64-byte handles (p_full, z_full, mailbox) of this shard
     void export_handles(void* out192) const;
     // handles of all `world` ranks (rank-major, 192 bytes each); maps the others
@@ -103,6 +120,7 @@ private:
         ShardBufs bufs{};
         DevBuf mbox;
         DevBuf table;  // world PeerPtrs
+        DevBuf desc;   // P2pDesc
     };
     void upload_table(Local& l, const std::vector<PeerPtrs>& peers);
     Mailbox mailbox(const Local& l) const;

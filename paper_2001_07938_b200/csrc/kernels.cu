@@ -12,6 +12,7 @@
 // SpMV is a streaming gather, not a dense contraction: no tensor cores.
 
 #include "b200.hpp"
+#include "p2p.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
         double total;
         if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) {
             if (sc->nranks > 1) {
-                sc->part[0] = total;  // the shard's partial; alpha after the exchange
+                p2p_publish(sc, &total, 1);  // the shard's partial; alpha after the exchange
             } else {
                 sc->d = total;
                 sc->rho0 = sc->rho;

@@ -21,6 +21,7 @@
 
 #include "b200.hpp"
 #include "p2p.hpp"
+#include "cg_fin.cuh"
 
 namespace b200 {
 
@@ -124,7 +125,35 @@ __global__ void k_wait(int world, Mailbox mb, int npart, double* __restrict__ ou
                 mb.gathered + (slot * kP2pMaxWorld + r) * kP2pMaxPart + k);
 }
 
+__global__ void k_wait_fin(int world, Mailbox mb, int npart, int fin, CgScalars* sc, double shift) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long e = *mb.epoch;
+    if (!*reinterpret_cast<volatile int*>(mb.err)) {
+        const unsigned long long t0 = globaltimer_ns();
+        for (int r = 0; r < world; ++r) {
+            while (ld_acquire_sys(mb.flags + r) < e) {
+                if (globaltimer_ns() - t0 > 5000000000ull) {
+                    *mb.err = 1;
+                    break;
+                }
+            }
+        }
+    }
+    double g[kP2pMaxWorld * kP2pMaxPart];
+    const unsigned long long slot = e & 1ull;
+    for (int r = 0; r < world; ++r)
+        for (int k = 0; k < npart; ++k)
+            g[r * npart + k] = *reinterpret_cast<volatile double*>(
+                mb.gathered + (slot * kP2pMaxWorld + r) * kP2pMaxPart + k);
+    cg_fin_apply(fin, sc, g, world, shift);
+}
+
 }  // namespace
+
+void p2p_wait_fin(int world, Mailbox mb, int npart, int fin, CgScalars* sc, double shift, cudaStream_t s) {
+    k_wait_fin<<<1, 32, 0, s>>>(world, mb, npart, fin, sc, shift);
+    B200_CUDA(cudaGetLastError());
+}
 
 void p2p_push_scalars(const double* partial, int npart, const PeerPtrs* peers, int world, int rank, Mailbox mb,
                       cudaStream_t s) {

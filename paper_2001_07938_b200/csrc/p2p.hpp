@@ -38,6 +38,40 @@ constexpr std::size_t kMboxErr = kMboxTicket + sizeof(unsigned int);
 constexpr std::size_t kMboxBytes = 4096;
 static_assert(kMboxErr + sizeof(int) <= kMboxBytes, "mailbox layout");
 
+// What a producing kernel needs to push its partials itself (device memory;
+// CgScalars::p2p points here while the peer-memory exchange is attached).
+struct P2pDesc {
+    const PeerPtrs* peers;
+    Mailbox mb;
+    int world;
+    int rank;
+};
+
+#ifdef __CUDACC__
+// Called by the one thread that finalises a shard's partials: stores them in
+// sc->part and, with a peer-memory exchange attached, into every peer's
+// mailbox slot for the next epoch, then raises this shard's flags.
+__device__ __forceinline__ void p2p_publish(CgScalars* sc, const double* vals, int npart) {
+    for (int k = 0; k < npart; ++k) sc->part[k] = vals[k];
+    const P2pDesc* d = static_cast<const P2pDesc*>(sc->p2p);
+    if (!d) return;
+    const unsigned long long e = *d->mb.epoch + 1;
+    const unsigned long long slot = e & 1ull;
+    for (int r = 0; r < d->world; ++r)
+        for (int k = 0; k < npart; ++k)
+            d->peers[r].gathered[(slot * kP2pMaxWorld + d->rank) * kP2pMaxPart + k] = vals[k];
+    *d->mb.epoch = e;
+    __threadfence_system();
+    for (int r = 0; r < d->world; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(d->peers[r].flags + d->rank), "l"(e) : "memory");
+}
+#endif
+
+// waits for the epoch's partials of every shard, then applies the CG
+// finalisation `fin` (cg.cu CgFin) to sc — the exchange's receive side and
+// fin_* in one kernel
+void p2p_wait_fin(int world, Mailbox mb, int npart, int fin, CgScalars* sc, double shift, cudaStream_t s);
+
 void p2p_push_scalars(const double* partial, int npart, const PeerPtrs* peers, int world, int rank, Mailbox mb,
                       cudaStream_t s);
 void p2p_push_vector(const double* src, std::int64_t rows, std::int64_t row0, const PeerPtrs* peers, int world,

@@ -15,6 +15,7 @@
 // by one warp: no atomics, deterministic order). y is written once per tile.
 
 #include "b200.hpp"
+#include "p2p.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                 a = warp_sum(red[lane]);
                 if (lane == 0) {
                     if (sc->nranks > 1) {
-                        sc->part[0] = a;  // the shard's partial; alpha after the exchange
+                        p2p_publish(sc, &a, 1);  // the shard's partial; alpha after the exchange
                     } else {
                         sc->d = a;
                         sc->rho0 = sc->rho;
