@@ -307,11 +307,14 @@ int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream);
  * an epoch flag per sender; receivers wait on the flags (p2p.cu).
  *  - local shards (b200_dist_cg_create_local): b200_dist_cg_use_p2p_local;
  *  - one shard per process (b200_dist_cg_create_nccl): b200_dist_cg_p2p_export
- *    writes this rank's three CUDA IPC handles (192 bytes), the caller
- *    all-gathers them (rank-major) and passes all to b200_dist_cg_p2p_attach.
+ *    writes this rank's record (208 bytes: three CUDA IPC handles and its
+ *    column footprint), the caller all-gathers them (rank-major) and passes
+ *    all to b200_dist_cg_p2p_attach.
+ * A shard pushes to each peer only the part of its slice inside the peer's
+ * column footprint (all of it for NPB; a halo for banded / stencil rows).
  * A wait without progress for 5 s fails the next result call (DeviceError). */
 int b200_dist_cg_use_p2p_local(b200_dist_cg* d);
-int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out192);
+int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out208);
 int b200_dist_cg_p2p_attach(b200_dist_cg* d, const void* handles);
 /* 0 local device copies, 1 NCCL, 2 peer memory. */
 int b200_dist_cg_transport(const b200_dist_cg* d);

@@ -34,6 +34,7 @@ namespace {
 
 struct Shard {
     std::int64_t row0 = 0, rows = 0, nnz = 0;
+    std::int64_t cmin = 0, cmax = 0;  // column footprint [cmin, cmax): the p / z entries its SpMV reads
     DevBuf row_ptr, col, val;
     CsrDev A;
     TcsrOwner tiled;
@@ -89,6 +90,10 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
     upload_row_ptr(s.row_ptr, lrp.data(), rows, s.nnz, &max_row, &monotone);
     const std::int64_t cols = upload_col_ind(s.col, ci + base, s.nnz, &col32);
     if (cols > n) throw Error(Errc::OutOfBounds, "column index >= n in a shard");
+    std::int64_t cmin = cols;
+    for (std::int64_t j = 0; j < s.nnz; ++j) cmin = std::min(cmin, ci[base + j]);
+    s.cmin = s.nnz ? cmin : 0;
+    s.cmax = cols;
     s.val.ensure(s.nnz * 8);
     host_in(val + base, s.nnz * 8);
     if (s.nnz) B200_CUDA(cudaMemcpyAsync(s.val.ptr, val + base, s.nnz * 8, cudaMemcpyHostToDevice, rt().stream));
@@ -321,6 +326,8 @@ PeerExchange::ShardBufs bufs_of(const Shard& s) {
     b.z_full = s.v.z_full;
     b.row0 = s.row0;
     b.rows = s.rows;
+    b.fmin = s.cmin;
+    b.fmax = s.cmax;
     return b;
 }
 
@@ -355,12 +362,12 @@ int b200_dist_cg_use_p2p_local(b200_dist_cg* d) {
     });
 }
 
-int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out192) {
+int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out) {
     return boundary("b200_dist_cg_p2p_export", [&] {
         if (d->transport != 1 || d->shards.size() != 1)
             throw Error(Errc::DataError, "IPC export: one shard per process (the NCCL driver)");
         d->pending = std::make_unique<PeerExchange>(d->rank, d->world, bufs_of(*d->shards[0]));
-        d->pending->export_handles(out192);
+        d->pending->export_handles(out);
     });
 }
 

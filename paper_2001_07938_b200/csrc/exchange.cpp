@@ -168,6 +168,22 @@ void PeerExchange::upload_table(Local& l, const std::vector<PeerPtrs>& peers) {
     B200_CUDA(cudaStreamSynchronize(rt().stream));
 }
 
+void PeerExchange::upload_send(Local& l, const std::vector<std::int64_t>& fmin, const std::vector<std::int64_t>& fmax) {
+    std::vector<std::int64_t> send(2 * static_cast<std::size_t>(world_), 0);
+    const std::int64_t a = l.bufs.row0, b = l.bufs.row0 + l.bufs.rows;
+    for (int r = 0; r < world_; ++r) {
+        const std::int64_t lo = std::max(a, fmin[r]), hi = std::min(b, fmax[r]);
+        if (hi > lo) {
+            send[2 * r] = lo - a;
+            send[2 * r + 1] = hi - a;
+        }
+    }
+    l.send.ensure(sizeof(std::int64_t) * send.size());
+    B200_CUDA(cudaMemcpyAsync(l.send.ptr, send.data(), sizeof(std::int64_t) * send.size(), cudaMemcpyHostToDevice,
+                              rt().stream));
+    B200_CUDA(cudaStreamSynchronize(rt().stream));
+}
+
 PeerExchange::PeerExchange(const std::vector<ShardBufs>& local) : world_(static_cast<int>(local.size())) {
     if (world_ < 1 || world_ > kP2pMaxWorld) throw Error(Errc::DataError, "peer exchange: 1..64 shards");
     shards_.resize(local.size());
@@ -180,7 +196,15 @@ PeerExchange::PeerExchange(const std::vector<ShardBufs>& local) : world_(static_
         B200_CUDA(cudaMemsetAsync(l.mbox.ptr, 0, kMboxBytes, rt().stream));
         peers.push_back(peer_of(l.bufs.p_full, l.bufs.z_full, l.mbox.as<char>()));
     }
-    for (Local& l : shards_) upload_table(l, peers);
+    std::vector<std::int64_t> fmin, fmax;
+    for (const ShardBufs& b : local) {
+        fmin.push_back(b.fmin);
+        fmax.push_back(b.fmax);
+    }
+    for (Local& l : shards_) {
+        upload_table(l, peers);
+        upload_send(l, fmin, fmax);
+    }
 }
 
 PeerExchange::PeerExchange(int rank, int world, const ShardBufs& mine) : world_(world) {
@@ -201,13 +225,16 @@ PeerExchange::~PeerExchange() {
         l.mbox.release();
         l.table.release();
         l.desc.release();
+        l.send.release();
     }
 }
 
-void PeerExchange::export_handles(void* out192) const {
+void PeerExchange::export_handles(void* out) const {
     if (shards_.size() != 1) throw Error(Errc::DataError, "IPC export needs one shard per process");
     const Local& l = shards_[0];
-    auto* o = static_cast<char*>(out192);
+    auto* o = static_cast<char*>(out);
+    std::memcpy(o + 192, &l.bufs.fmin, sizeof(std::int64_t));
+    std::memcpy(o + 200, &l.bufs.fmax, sizeof(std::int64_t));
     cudaIpcMemHandle_t h;
     for (int k = 0; k < 3; ++k) {
         void* base = k == 0 ? static_cast<void*>(l.bufs.p_full)
@@ -223,6 +250,11 @@ void PeerExchange::attach(const void* handles) {
     Local& l = shards_[0];
     const auto* in = static_cast<const char*>(handles);
     std::vector<PeerPtrs> peers;
+    std::vector<std::int64_t> fmin(world_), fmax(world_);
+    for (int r = 0; r < world_; ++r) {
+        std::memcpy(&fmin[r], in + kP2pRecord * r + 192, sizeof(std::int64_t));
+        std::memcpy(&fmax[r], in + kP2pRecord * r + 200, sizeof(std::int64_t));
+    }
     for (int r = 0; r < world_; ++r) {
         if (r == l.rank) {
             peers.push_back(peer_of(l.bufs.p_full, l.bufs.z_full, l.mbox.as<char>()));
@@ -231,13 +263,14 @@ void PeerExchange::attach(const void* handles) {
         void* m[3];
         for (int k = 0; k < 3; ++k) {
             cudaIpcMemHandle_t h;
-            std::memcpy(&h, in + 192 * r + 64 * k, sizeof h);
+            std::memcpy(&h, in + kP2pRecord * r + 64 * k, sizeof h);
             B200_CUDA(cudaIpcOpenMemHandle(&m[k], h, cudaIpcMemLazyEnablePeerAccess));
             opened_.push_back(m[k]);
         }
         peers.push_back(peer_of(static_cast<double*>(m[0]), static_cast<double*>(m[1]), static_cast<char*>(m[2])));
     }
     upload_table(l, peers);
+    upload_send(l, fmin, fmax);
 }
 
 void PeerExchange::exchange_scalars(std::vector<ShardView>& views, int npart) {
@@ -254,7 +287,7 @@ void PeerExchange::exchange_vector(std::vector<ShardView>& views, std::vector<do
         const Local& l = shards_[i];
         const bool z = fulls[i] == l.bufs.z_full;
         p2p_push_vector(fulls[i] + l.bufs.row0, l.bufs.rows, l.bufs.row0, l.table.as<PeerPtrs>(), world_, l.rank, z,
-                        mailbox(l), views[i].stream);
+                        mailbox(l), l.send.as<std::int64_t>(), views[i].stream);
     }
     for (std::size_t i = 0; i < shards_.size(); ++i)
         p2p_wait(world_, mailbox(shards_[i]), 0, nullptr, views[i].stream);
@@ -263,7 +296,7 @@ void PeerExchange::exchange_vector(std::vector<ShardView>& views, std::vector<do
 bool PeerExchange::update_p_exchange(std::vector<ShardView>& views, const std::vector<const CgVectors*>& v) {
     for (std::size_t i = 0; i < shards_.size(); ++i)
         p2p_update_p_push(*v[i], shards_[i].table.as<PeerPtrs>(), world_, shards_[i].rank, mailbox(shards_[i]),
-                          views[i].stream);
+                          shards_[i].send.as<std::int64_t>(), views[i].stream);
     for (std::size_t i = 0; i < shards_.size(); ++i)
         p2p_wait(world_, mailbox(shards_[i]), 0, nullptr, views[i].stream);
     return true;

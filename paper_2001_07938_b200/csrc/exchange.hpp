@@ -92,6 +92,7 @@ public:
         double* p_full;
         double* z_full;
         std::int64_t row0, rows;
+        std::int64_t fmin, fmax;  // column footprint: the replica entries this shard's SpMV reads
     };
     // k local shards, ranks 0..k-1
     explicit PeerExchange(const std::vector<ShardBufs>& local);
@@ -107,9 +108,10 @@ public:
     // point each shard's CgScalars::p2p at its descriptor: its producing
     // kernels then push their partials themselves
     void bind_producers(const std::vector<CgScalars*>& sc);
-    // IPC: three 64-byte handles (p_full, z_full, mailbox) of this shard
-    void export_handles(void* out192) const;
-    // handles of all `world` ranks (rank-major, 192 bytes each); maps the others
+    // IPC: this shard's record — three 64-byte handles (p_full, z_full,
+    // mailbox) and its column footprint (2 x int64): kP2pRecord bytes
+    void export_handles(void* out) const;
+    // records of all `world` ranks (rank-major); maps the others
     void attach(const void* handles);
     // a wait timed out somewhere (checked after a run)
     bool timed_out() const;
@@ -121,7 +123,9 @@ private:
         DevBuf mbox;
         DevBuf table;  // world PeerPtrs
         DevBuf desc;   // P2pDesc
+        DevBuf send;   // world x {lo, hi}: the part of my slice each peer reads
     };
+    void upload_send(Local& l, const std::vector<std::int64_t>& fmin, const std::vector<std::int64_t>& fmax);
     void upload_table(Local& l, const std::vector<PeerPtrs>& peers);
     Mailbox mailbox(const Local& l) const;
     std::vector<Local> shards_;

@@ -63,14 +63,17 @@ __global__ void k_push_scalars(const double* __restrict__ partial, int npart, co
 // one CTA copies the slice to every peer (grid-stride), the last CTA raises
 // the flags
 __global__ void k_push_vector(const double* __restrict__ src, std::int64_t rows, std::int64_t row0,
-                              const PeerPtrs* __restrict__ peers, int world, int rank, int which, Mailbox mb) {
+                              const PeerPtrs* __restrict__ peers, int world, int rank, int which, Mailbox mb,
+                              const std::int64_t* __restrict__ send) {
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (int r = 0; r < world; ++r) {
         if (r == rank) continue;  // src is this shard's own slice of the same buffer
         double* dst = (which ? peers[r].z_full : peers[r].p_full) + row0;
-        for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += stride)
+        const std::int64_t lo = send[2 * r], hi = send[2 * r + 1];
+        for (std::int64_t i = lo + static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < hi; i += stride)
             dst[i] = src[i];
     }
+    (void)rows;
     __threadfence_system();
     __syncthreads();
     __shared__ bool last;
@@ -84,14 +87,15 @@ __global__ void k_push_vector(const double* __restrict__ src, std::int64_t rows,
 // p = r + beta*p over this shard's rows, each new value stored locally and
 // into every peer's replica in the same pass (the CG p update fused with its
 // exchange); the last CTA raises the flags
-__global__ void k_update_p_push(CgVectors v, const PeerPtrs* __restrict__ peers, int world, int rank, Mailbox mb) {
+__global__ void k_update_p_push(CgVectors v, const PeerPtrs* __restrict__ peers, int world, int rank, Mailbox mb,
+                                const std::int64_t* __restrict__ send) {
     const double beta = v.sc->beta;
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < v.n; i += stride) {
         const double pv = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
         v.p[i] = pv;
         for (int r = 0; r < world; ++r)
-            if (r != rank) peers[r].p_full[v.row0 + i] = pv;
+            if (r != rank && i >= send[2 * r] && i < send[2 * r + 1]) peers[r].p_full[v.row0 + i] = pv;
     }
     __threadfence_system();
     __syncthreads();
@@ -162,17 +166,18 @@ void p2p_push_scalars(const double* partial, int npart, const PeerPtrs* peers, i
 }
 
 void p2p_push_vector(const double* src, std::int64_t rows, std::int64_t row0, const PeerPtrs* peers, int world,
-                     int rank, bool z, Mailbox mb, cudaStream_t s) {
+                     int rank, bool z, Mailbox mb, const std::int64_t* send, cudaStream_t s) {
     const unsigned grid =
         static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((rows + 255) / 256, 148)));
-    k_push_vector<<<grid, 256, 0, s>>>(src, rows, row0, peers, world, rank, z ? 1 : 0, mb);
+    k_push_vector<<<grid, 256, 0, s>>>(src, rows, row0, peers, world, rank, z ? 1 : 0, mb, send);
     B200_CUDA(cudaGetLastError());
 }
 
-void p2p_update_p_push(const CgVectors& v, const PeerPtrs* peers, int world, int rank, Mailbox mb, cudaStream_t s) {
+void p2p_update_p_push(const CgVectors& v, const PeerPtrs* peers, int world, int rank, Mailbox mb,
+                       const std::int64_t* send, cudaStream_t s) {
     const unsigned grid =
         static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((v.n + 511) / 512, 148 * 4)));
-    k_update_p_push<<<grid, 256, 0, s>>>(v, peers, world, rank, mb);
+    k_update_p_push<<<grid, 256, 0, s>>>(v, peers, world, rank, mb, send);
     B200_CUDA(cudaGetLastError());
 }
 

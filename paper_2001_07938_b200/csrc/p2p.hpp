@@ -8,6 +8,7 @@
 namespace b200 {
 
 constexpr int kP2pMaxWorld = 64;
+constexpr std::size_t kP2pRecord = 3 * 64 + 2 * sizeof(std::int64_t);  // IPC handles + footprint
 constexpr int kP2pMaxPart = 2;
 
 // Where a shard receives: its p / z replicas and its mailbox (scalar slots +
@@ -74,10 +75,13 @@ void p2p_wait_fin(int world, Mailbox mb, int npart, int fin, CgScalars* sc, doub
 
 void p2p_push_scalars(const double* partial, int npart, const PeerPtrs* peers, int world, int rank, Mailbox mb,
                       cudaStream_t s);
+// send: world x {lo, hi} offsets into this shard's slice — the rows of it in
+// each peer's column footprint (banded / stencil operators: a halo)
 void p2p_push_vector(const double* src, std::int64_t rows, std::int64_t row0, const PeerPtrs* peers, int world,
-                     int rank, bool z, Mailbox mb, cudaStream_t s);
+                     int rank, bool z, Mailbox mb, const std::int64_t* send, cudaStream_t s);
 void p2p_wait(int world, Mailbox mb, int npart, double* out, cudaStream_t s);
 // the CG p update (p = r + beta*p, own rows) fused with the push of the slice
-void p2p_update_p_push(const CgVectors& v, const PeerPtrs* peers, int world, int rank, Mailbox mb, cudaStream_t s);
+void p2p_update_p_push(const CgVectors& v, const PeerPtrs* peers, int world, int rank, Mailbox mb,
+                       const std::int64_t* send, cudaStream_t s);
 
 }  // namespace b200

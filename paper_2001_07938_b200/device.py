@@ -205,13 +205,14 @@ class DistCG:
         N.check(N.lib().b200_dist_cg_use_p2p_local(self._h))
 
     def p2p_export(self) -> bytes:
-        """This rank's three CUDA IPC handles (192 bytes) for p2p_attach."""
-        buf = C.create_string_buffer(192)
+        """This rank's record for p2p_attach (208 bytes: three CUDA IPC
+        handles and its column footprint)."""
+        buf = C.create_string_buffer(208)
         N.check(N.lib().b200_dist_cg_p2p_export(self._h, buf))
         return buf.raw
 
     def p2p_attach(self, handles: bytes):
-        """All ranks' handles, rank-major (world x 192 bytes)."""
+        """All ranks' records, rank-major (world x 208 bytes)."""
         N.check(N.lib().b200_dist_cg_p2p_attach(self._h, C.create_string_buffer(bytes(handles), len(handles))))
 
     @property

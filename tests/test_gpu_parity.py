@@ -419,6 +419,22 @@ def test_sharded_cg_peer_memory_exchange_local(cls, k):
     d.free()
 
 
+def test_sharded_cg_peer_memory_halo_on_a_stencil():
+    """Banded rows: each shard pushes only the halo its peers read; the
+    sharded CG recurrence still matches the device-copy exchange bit for bit."""
+    rp, ci, val = _stencil27_host(16)
+    n = len(rp) - 1
+    d0 = D.DistCG.local(4, rp, ci, val)
+    z0, r0 = d0.npb(3, 0.0)
+    d0.free()
+    d = D.DistCG.local(4, rp, ci, val)
+    d.use_p2p_local()
+    z1, r1 = d.npb(3, 0.0)
+    assert z1 == z0 and r1 == r0 and np.isfinite(z1)
+    d.free()
+    assert n == 4096
+
+
 def test_sharded_cg_peer_memory_ipc_single_rank():
     """The IPC export/attach path with world = 1 (no peer to map; exercises
     cudaIpcGetMemHandle and the switch of transport)."""
@@ -426,7 +442,7 @@ def test_sharded_cg_peer_memory_ipc_single_rank():
     rp, ci, val = D.gen_npb(na, nonzer, shift)
     d = D.DistCG.nccl(0, 1, D.DistCG.nccl_id(), na, np.array([0, na], np.int64), rp, ci, val)
     h = d.p2p_export()
-    assert len(h) == 192
+    assert len(h) == 208
     d.p2p_attach(h)
     assert d.transport == "p2p"
     zeta, _ = d.npb(niter, shift)
