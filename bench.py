@@ -414,14 +414,11 @@ def run_ours(args):
         shard_rows = (0, na)
     else:
         # one shard per rank: nnz-balanced row ranges, NCCL id shared via torch.distributed
+        from paper_2001_07938_b200 import dist as PD
         bounds = D.partition_rows(rp, world)
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(D.DistCG.nccl_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
+        nid = PD.broadcast_bytes(D.DistCG.nccl_id() if rank == 0 else None, 128, "cuda")
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-        cg = D.DistCG.nccl(rank, world, bytes(idt.cpu().numpy().tobytes()), na, bounds, rp[r0:r1 + 1].copy(),
-                           ci, val)
+        cg = D.DistCG.nccl(rank, world, nid, na, bounds, rp[r0:r1 + 1].copy(), ci, val)
         # this rank's row block as a plain resident matrix, for the kernel roofline line
         A = D.Matrix.csr(np.ascontiguousarray(rp[r0:r1 + 1] - rp[r0]), np.ascontiguousarray(ci[rp[r0]:rp[r1]]),
                          np.ascontiguousarray(val[rp[r0]:rp[r1]]))
@@ -432,29 +429,20 @@ def run_ours(args):
     if world > 1:
         transport = "nccl"
         if os.environ.get("LILAC_B200_DIST_P2P", "1") != "0":
-            # peer-memory exchange (p2p.cu): IPC handles all-gathered over
-            # torch.distributed; kept only if the sharded NPB run verifies
-            try:
-                mine = torch.frombuffer(bytearray(cg.p2p_export()), dtype=torch.uint8).cuda()
-                allh = [torch.empty_like(mine) for _ in range(world)]
-                dist.all_gather(allh, mine)
-                cg.p2p_attach(b"".join(bytes(h.cpu().numpy().tobytes()) for h in allh))
+            # peer-memory exchange (p2p.cu): kept only if the sharded NPB run
+            # verifies on every rank
+            from paper_2001_07938_b200 import dist as PD
+
+            def verify():
                 zp, _ = cg.npb(niter, shift)
-                ok = torch.tensor([1.0 if abs(zp - zeta_ref) / zeta_ref <= 1e-10 else 0.0], device="cuda")
-            except Exception as e:  # noqa: BLE001 - any failure falls back to NCCL
-                print(f"rank {rank}: peer-memory exchange unavailable ({e}); using NCCL", file=sys.stderr)
-                ok = torch.tensor([0.0], device="cuda")
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            if ok.item() == 1.0:
+                return abs(zp - zeta_ref) / zeta_ref <= 1e-10
+
+            if PD.attach_peer_memory(cg, verify, "cuda"):
                 transport = "p2p"
             else:
                 cg.free()
-                idt2 = torch.zeros(128, dtype=torch.uint8, device="cuda")
-                if rank == 0:
-                    idt2.copy_(torch.frombuffer(bytearray(D.DistCG.nccl_id()), dtype=torch.uint8))
-                dist.broadcast(idt2, 0)
-                cg = D.DistCG.nccl(rank, world, bytes(idt2.cpu().numpy().tobytes()), na, bounds,
-                                   rp[r0:r1 + 1].copy(), ci, val)
+                nid = PD.broadcast_bytes(D.DistCG.nccl_id() if rank == 0 else None, 128, "cuda")
+                cg = D.DistCG.nccl(rank, world, nid, na, bounds, rp[r0:r1 + 1].copy(), ci, val)
 
     # correctness gate: the full NPB benchmark must verify before we time anything
     if args.no_verify:

@@ -120,3 +120,60 @@ def test_sharded_cg_gloo(world):
     rp, ci, val = O.npb_makea(1400, 7, 10.0)
     z1, _ = O.npb_cg(rp, ci, val, 15, 10.0)
     assert abs(zeta - z1) <= 1e-12 * abs(z1)
+
+
+# ---- the cross-process handshake of the peer-memory exchange (dist.py) ----------
+
+class _FakeCG:
+    """Stands in for DistCG: a rank-specific 208-byte record; remembers what
+    p2p_attach received."""
+
+    def __init__(self, rank, fail_attach=False):
+        self.record = bytes([rank + 1]) * 200 + rank.to_bytes(8, "little")
+        self.got = None
+        self.fail_attach = fail_attach
+
+    def p2p_export(self):
+        return self.record
+
+    def p2p_attach(self, blob):
+        if self.fail_attach:
+            raise RuntimeError("no peer access")
+        self.got = blob
+
+
+def _handshake_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2001_07938_b200 import dist as PD
+    out = {}
+    out["bcast"] = PD.broadcast_bytes(b"nccl-id-" + bytes(120) if rank == 0 else None, 128, "cpu")
+    cg = _FakeCG(rank)
+    out["kept"] = PD.attach_peer_memory(cg, lambda: True, "cpu")
+    out["blob"] = cg.got
+    # one rank's verification fails: nobody keeps it
+    out["kept_when_one_fails"] = PD.attach_peer_memory(_FakeCG(rank), lambda: rank == 0, "cpu")
+    # one rank cannot map its peers: nobody keeps it, no exception escapes
+    out["kept_when_attach_fails"] = PD.attach_peer_memory(_FakeCG(rank, fail_attach=rank == 1), lambda: True, "cpu")
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+def test_peer_memory_handshake_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_handshake_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    expect_blob = _FakeCG(0).record + _FakeCG(1).record  # rank-major
+    for r in range(2):
+        assert res[r]["bcast"] == b"nccl-id-" + bytes(120)
+        assert res[r]["kept"] is True
+        assert res[r]["blob"] == expect_blob
+        assert res[r]["kept_when_one_fails"] is False
+        assert res[r]["kept_when_attach_fails"] is False
