@@ -84,7 +84,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     build_cpp_tests(force, verbose)
     build_generated_harness(force, verbose)
     build_python_ext(force, verbose)
+    build_examples(force, verbose)
     return LIB
+
+
+EX_LIB = os.path.join(PKG, "libnpb_host_cg.so")
+
+
+def build_examples(force: bool = False, verbose: bool = False):
+    """examples/npb_host_cg.c — a C host program on the harness ABI (the e2e
+    leg of bench.py), linked to liblilac_b200.so."""
+    src = os.path.join(PKG, "examples", "npb_host_cg.c")
+    if force or _stale(EX_LIB, [src, LIB, os.path.join(INCLUDE, "lilac_b200.h")]):
+        _run(["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-Wall", f"-I{INCLUDE}", "-o", EX_LIB, src, f"-L{PKG}",
+              "-llilac_b200", "-Wl,-rpath,$ORIGIN", "-lm"], verbose)
 
 
 def build_python_ext(force: bool = False, verbose: bool = False):
