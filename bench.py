@@ -565,7 +565,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (NPB makea generator, class %s)" % args.npb_class,
         "config": {"workload": f"NPB CG class {args.npb_class}: n={na}, nnz={nnz}, resident CSR "
-                               f"(int{8 * col_b} col_ind), {SPMV_PER_STEP} SpMV/step",
+                               + ("(tiled layout, 16-bit slab-local column keys)" if info["kernel"] == 4
+                                  else f"(int{8 * col_b} col_ind)") + f", {SPMV_PER_STEP} SpMV/step",
                    "parallelism": f"row-sharded x{world} ({transport} exchange of p and the dot partials per CG "
                                   "step, CUDA graph per NPB iteration)" if world > 1
                    else "single GPU, CUDA graph per NPB iteration",

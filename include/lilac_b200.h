@@ -184,7 +184,7 @@ typedef struct b200_matrix b200_matrix;  /* resident CSR or JDS matrix */
 typedef struct {
     int64_t rows, cols, nnz, max_row;
     int32_t format;        /* 0 CSR, 1 JDS */
-    int32_t col_bytes;     /* device col_ind width: 4 (narrowed) or 8 */
+    int32_t col_bytes;     /* column index width the kernel streams: 8, 4 (narrowed) or 2 (tiled keys) */
     int32_t kernel;        /* CSR kernel chosen: 1 vector, 2 merge, 3 exact, 4 tiled, 5 split */
     int32_t lanes;         /* vector kernel lanes per row */
     int64_t device_bytes;  /* resident bytes */

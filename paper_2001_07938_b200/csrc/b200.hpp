@@ -56,20 +56,28 @@ CsrKernel parse_csr_kernel(const std::string& s);
 // Tiled CSR (upload-time cached invariant, tcsr_build.cpp): rows cut into
 // tiles (one CTA each), columns into slabs of kSlabW that fit shared memory.
 // Inside a tile the nonzeros are ordered slab-major, then by the owning warp's
-// contiguous row range, then by row, so each (slab, warp) is one contiguous
-// run; each nonzero carries a packed key = slab-local column | tile-local row
-// << 16 (4 bytes, the same HBM cost as an int32 column index).
+// contiguous row range, then by row, so each (slab, warp) is one run. A run's
+// nonzeros (in that order) are cut into 4-nonzero chunks and the chunks into
+// 32 contiguous lane ranges (lane l gets chunks [l*m + min(l, r), ...), m or
+// m + 1 of them); chunk i of lane l is stored at run offset (32 i + l) * 4, so
+// every warp-wide chunk load is one contiguous 1 KB burst while each lane
+// walks its own range in order, summing rows in registers. Each nonzero has a
+// 2-byte key = slab-local column | kKeyStart when it opens a row (never set on
+// a lane's first nonzero); each lane has a 2-byte descriptor = tile-local row
+// of its first nonzero | kLaneCont when that row began in an earlier lane.
+// HBM cost: 10 bytes per stored nonzero + 64 bytes per run.
 constexpr int kTileThreads = 1024;
 constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kSlabW = 12288;       // columns per slab: 2 x 96 KB double-buffered in smem
-constexpr int kMaxTileRows = 4096;  // tile-local row fits the key and the smem y buffer
-constexpr int kRunAlign = 4;        // (slab, warp) runs start and end on 4-nonzero (32 B) boundaries
-constexpr std::uint32_t kPadKey = 0xffffu << 16;  // padding entry: sentinel row, column 0, value 0
-// key = lrow << 16 | kKeyCont? | lcol: kKeyCont marks an element whose row
-// continues the row of the element before it in its (slab, warp) run
-constexpr std::uint32_t kKeyCont = 1u << 14;
-constexpr std::uint32_t kKeyColMask = kKeyCont - 1u;
-static_assert(kSlabW <= static_cast<int>(kKeyColMask) + 1, "slab columns must fit below the continuation bit");
+constexpr int kSlabW = 12288;            // columns per slab: 2 x 96 KB double-buffered in smem
+constexpr int kSlabStride = kSlabW + 2;  // + a zero cell (column kSlabW) read by padding entries
+constexpr int kMaxTileRows = 4096;       // tile-local rows fit a descriptor and the smem y buffer
+constexpr int kChunk = 4;                // nonzeros per lane per load (one 256-bit val load)
+constexpr std::uint16_t kKeyStart = 1u << 15;
+constexpr std::uint16_t kKeyColMask = (1u << 14) - 1u;
+constexpr std::uint16_t kLaneCont = 1u << 15;
+// padding entry: value 0 times the zero cell (never an Inf or NaN of x)
+constexpr std::uint16_t kPadKey = static_cast<std::uint16_t>(kSlabW);
+static_assert(kSlabW <= static_cast<int>(kKeyColMask), "slab columns and the zero cell must fit the key");
 
 struct TcsrDev {
     std::int64_t ntiles = 0;
@@ -77,9 +85,10 @@ struct TcsrDev {
     std::int64_t cols = 0;
     const std::int64_t* tile_row0 = nullptr;  // ntiles + 1 row bounds
     const std::int64_t* tile_base = nullptr;  // ntiles + 1 element offsets
-    const std::int32_t* woff = nullptr;       // ntiles x (nslabs*kTileWarps + 1), tile-relative
-    const double* val = nullptr;              // nnz, tiled order
-    const std::uint32_t* key = nullptr;       // nnz, lcol | lrow << 16
+    const std::int32_t* woff = nullptr;       // ntiles x (nslabs*kTileWarps + 1): run element offsets, tile-relative
+    const std::uint16_t* lrow = nullptr;      // ntiles x nslabs*kTileWarps x 32 lane descriptors
+    const double* val = nullptr;              // stored nonzeros (+ pads), tiled order
+    const std::uint16_t* key = nullptr;       // same: slab-local column | kKeyStart?
 };
 
 // Merge-path plan (merge.cu): per-CTA start coordinates on the merge of row

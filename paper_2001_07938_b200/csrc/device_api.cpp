@@ -162,8 +162,9 @@ int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
             info->rows = A->csr.rows;
             info->cols = A->csr.cols;
             info->nnz = A->csr.nnz;
-            info->col_bytes = A->csr.col32 ? 4 : 8;
             info->kernel = static_cast<int32_t>(matrix_kernel(A));
+            // column index width the chosen kernel streams (tiled: 16-bit slab-local keys)
+            info->col_bytes = info->kernel == static_cast<int32_t>(CsrKernel::Tiled) ? 2 : (A->csr.col32 ? 4 : 8);
             info->lanes = csr_vector_width(A->csr);
         } else {
             info->rows = A->jds.rows;

@@ -6,13 +6,16 @@
 // x is staged in shared memory one column slab at a time (cp.async.bulk into a
 // double buffer, completion on an mbarrier), so a gather costs a few bank
 // cycles instead of 32 L1 wavefronts, while val/key stream from HBM with
-// fully coalesced 16-byte loads.
+// fully coalesced 256-bit loads.
 //
 // One CTA (32 warps) per tile; warp w owns a contiguous row range of the tile.
-// For each slab the warp streams its contiguous (slab, warp) run two nonzeros
-// per lane, gathers x from smem, and reduces by row with a shuffle-based
-// segmented scan; row partials accumulate in a shared y buffer (rows are owned
-// by one warp: no atomics, deterministic order). y is written once per tile.
+// For each slab the warp streams its (slab, warp) run: each lane walks its own
+// contiguous range of the run (layout in b200.hpp) chunk by chunk, gathers x
+// from smem and sums rows in registers, flushing a row that began and ended
+// inside the lane straight into a shared y buffer; the rows crossing lane
+// boundaries are combined once per run by a shuffle-based segmented scan.
+// Rows are owned by one warp: no atomics, deterministic order. y is written
+// once per tile.
 
 #include "b200.hpp"
 #include "p2p.hpp"
@@ -25,8 +28,11 @@ namespace b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr unsigned kSent = 0xffffu;  // sentinel tile-local row (> kMaxTileRows)
-constexpr std::size_t kTileSmem = sizeof(double) * (2 * kSlabW + kMaxTileRows);
+#ifndef LILAC_PF_AHEAD
+#define LILAC_PF_AHEAD 1
+#endif
+constexpr int kPfAhead = LILAC_PF_AHEAD;
+constexpr std::size_t kTileSmem = sizeof(double) * (2 * kSlabStride + kMaxTileRows);
 
 __device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -74,10 +80,10 @@ __device__ __forceinline__ void ld_stream_f64x4(const double* p, double2& a, dou
         : "l"(p), "l"(pol));
 }
 
-__device__ __forceinline__ uint4 ld_stream_u32x4(const std::uint32_t* p, std::uint64_t pol) {
-    uint4 r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+__device__ __forceinline__ uint2 ld_stream_u16x4(const std::uint16_t* p, std::uint64_t pol) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+        : "=r"(r.x), "=r"(r.y)
         : "l"(p), "l"(pol));
     return r;
 }
@@ -118,10 +124,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p, std::size_t bytes) {
 }
 
 // Prefetch a (slab, warp) run's val and key bytes into L2.
-__device__ __forceinline__ void prefetch_run(const double* vb, const std::uint32_t* kb, int lo, int hi) {
+__device__ __forceinline__ void prefetch_run(const double* vb, const std::uint16_t* kb, int lo, int hi) {
     if (hi > lo) {
         prefetch_l2(vb + lo, static_cast<std::size_t>(hi - lo) * 8);
-        prefetch_l2(kb + lo, static_cast<std::size_t>(hi - lo) * 4);
+        prefetch_l2(kb + lo, static_cast<std::size_t>(hi - lo) * 2);
     }
 }
 
@@ -138,41 +144,65 @@ __device__ __forceinline__ void sts_add_f64(std::uint32_t addr, double v) {
 }
 
 
-// A lane's four consecutive nonzeros of a (slab, warp) run: one 256-bit val
-// load and one 128-bit key load, both 32/16-byte aligned (runs start on
-// kRunAlign boundaries). Lanes past the run end get zeros (and sentinel keys).
+// One chunk of a lane's range: 4 nonzeros, one 256-bit val load and one
+// 64-bit key load (4 x 16-bit keys), both aligned (chunks are 32 B).
 struct Chunk {
     double2 v0, v1;
-    uint4 k;
+    uint2 k;
 };
 
-__device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std::uint32_t* kb, int j, int hi,
+__device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std::uint16_t* kb, unsigned e,
                                            std::uint64_t pol) {
-    if (j < hi) {
-        ld_stream_f64x4(vb + j, c.v0, c.v1, pol);
-        c.k = ld_stream_u32x4(kb + j, pol);
-    } else {
-        c.v0 = c.v1 = make_double2(0.0, 0.0);
-        c.k = make_uint4(kPadKey, kPadKey, kPadKey, kPadKey);
-    }
+    ld_stream_f64x4(vb + e, c.v0, c.v1, pol);
+    c.k = ld_stream_u16x4(kb + e, pol);
 }
 
-// One 128-nonzero piece after the lane-local pass: lane holds its head run
-// (k0, p0) and tail run (k1, p1) (k0 == k1: a single run, value p1). Row keys
-// are non-decreasing across lanes. Adds every row's piece-sum into yp[row]
-// (rows are owned by this warp: no atomics, fixed order).
-// `cont`: the lane's first element continues the row of the element before it
-// (a layout bit, kKeyCont), so a non-split lane starts a segment iff !cont.
-__device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1, double p1, bool cont, int lane,
-                                             std::uint32_t yp_s) {
-    const bool split = k0 != k1;
+// A lane's walk state over its range: the row being summed, its partial
+// sum, and the head run (the lane's first row, which may have begun in an
+// earlier lane) once a later row starts.
+struct Walk {
+    unsigned row;
+    double acc, head;
+    bool in_head;
+};
+
+template <int MODE>
+__device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::uint32_t xb_s, std::uint32_t yp_s) {
+    const double p = (MODE == 1 || MODE == 3) ? v : v * lds_f64(xb_s + 8u * (key & kKeyColMask));
+    if (MODE >= 2) {
+        w.acc += p;
+        return;
+    }
+    if (key & kKeyStart) {  // a new row: the previous one is complete
+        if (!w.in_head) sts_add_f64(yp_s + 8u * w.row, w.acc);  // began and ended in this lane: exclusive
+        else w.head = w.acc;
+        w.in_head = false;
+        ++w.row;
+        w.acc = 0.0;
+    }
+    w.acc += p;
+}
+
+template <int MODE>
+__device__ __forceinline__ void walk_chunk(Walk& w, const Chunk& c, std::uint32_t xb_s, std::uint32_t yp_s) {
+    walk_one<MODE>(w, c.v0.x, c.k.x & 0xffffu, xb_s, yp_s);
+    walk_one<MODE>(w, c.v0.y, c.k.x >> 16, xb_s, yp_s);
+    walk_one<MODE>(w, c.v1.x, c.k.y & 0xffffu, xb_s, yp_s);
+    walk_one<MODE>(w, c.v1.y, c.k.y >> 16, xb_s, yp_s);
+}
+
+// Combines the lanes' boundary rows once per run: lane l holds its head run
+// (k0, p0, only when split) and its tail run (k1, p1); rows are
+// non-decreasing across lanes. Adds each row's sum into yp[row] (rows are
+// owned by this warp: no atomics, fixed order). `cont`: the lane's first row
+// began in an earlier lane; inactive lanes (no chunks) are segment heads that
+// store nothing.
+__device__ __forceinline__ void reduce_lanes(unsigned k0, double p0, unsigned k1, double p1, bool split, bool cont,
+                                             bool active, int lane, std::uint32_t yp_s) {
     double s = p1;
-    const bool head = lane == 0 || split || !cont;
+    const bool head = lane == 0 || split || !cont || !active;
     const unsigned hm = __ballot_sync(kFull, head);
     const int seg = 31 - __clz(hm & (kFull >> (31 - lane)));
-    // only as many doubling steps as the longest row segment of the piece
-    // needs (NPB: rows span ~5 lanes, so usually 3 of the 5; each f64 step
-    // is two SHFLs + a DADD)
     const int maxspan = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(lane - seg + 1)));
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -180,62 +210,41 @@ __device__ __forceinline__ void reduce_piece(unsigned k0, double p0, unsigned k1
         const double t = __shfl_up_sync(kFull, s, d);
         if (lane - d >= seg) s += t;
     }
-    // Two store passes, each touching distinct rows: (1) every segment's sum
-    // at its last lane (the next lane starts a segment); (2) the head run of
-    // every split lane. A row continuing from lane i-1's tail into lane i's
-    // head gets both; the passes are ordered, so no shuffle of the scan value
-    // into the split lane is needed.
-    if ((lane == 31 || ((hm >> (lane + 1)) & 1u)) && k1 != kSent) sts_add_f64(yp_s + 8u * k1, s);
+    // two ordered store passes over distinct rows: (1) every segment's sum at
+    // its last lane; (2) the head run of every split lane (a row running from
+    // lane i-1's tail into lane i's head gets both)
+    if (active && (lane == 31 || ((hm >> (lane + 1)) & 1u))) sts_add_f64(yp_s + 8u * k1, s);
     __syncwarp();
-    if (split && k0 != kSent) sts_add_f64(yp_s + 8u * k0, p0);
+    if (active && split) sts_add_f64(yp_s + 8u * k0, p0);
 }
 
-// Processes a (slab, warp) run [lo, hi) (tile-relative, both multiples of
-// kRunAlign) against the slab in shared memory at xb_s. The run's bytes were
-// prefetched into L2 one slab ahead, so these loads are L2 hits; the next
-// chunk is loaded into registers while this one is reduced.
+// Processes a (slab, warp) run [lo, hi) (tile-relative, multiples of kChunk)
+// with lane descriptor `ld` against the slab in shared memory at xb_s. The
+// run's bytes were prefetched into L2 one slab ahead; the next chunk is
+// loaded while the current one is walked.
 template <int MODE>
-__device__ __forceinline__ void process_run(const double* vb, const std::uint32_t* kb, int lo, int hi,
+__device__ __forceinline__ void process_run(const double* vb, const std::uint16_t* kb, int lo, int hi, unsigned ld,
                                             std::uint32_t xb_s, std::uint32_t yp_s, int lane) {
     std::uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    Chunk cur, nxt;
-    load_chunk(cur, vb, kb, lo + 4 * lane, hi, pol);
-    for (int c = lo; c < hi; c += 128) {
-        load_chunk(nxt, vb, kb, c + 128 + 4 * lane, hi, pol);
-        const unsigned k0 = cur.k.x >> 16, k1 = cur.k.y >> 16, k2 = cur.k.z >> 16, k3 = cur.k.w >> 16;
-        double p0, p1, p2, p3;
-        if (MODE == 1 || MODE == 3) {  // probe: no gather
-            p0 = cur.v0.x, p1 = cur.v0.y, p2 = cur.v1.x, p3 = cur.v1.y;
-        } else {
-            p0 = cur.v0.x * lds_f64(xb_s + 8u * (cur.k.x & kKeyColMask));
-            p1 = cur.v0.y * lds_f64(xb_s + 8u * (cur.k.y & kKeyColMask));
-            p2 = cur.v1.x * lds_f64(xb_s + 8u * (cur.k.z & kKeyColMask));
-            p3 = cur.v1.y * lds_f64(xb_s + 8u * (cur.k.w & kKeyColMask));
-        }
-        if (MODE >= 2) {
-            if (p0 == 12345.678) sts_add_f64(yp_s, p1 + p2 + p3);  // probe: no reduction
-        } else {
-            // lane-local pass, branch-free for the common case (keys sorted):
-            // tail run = elements equal to k3, head run = elements equal to k0
-            double tail = p3;
-            tail += k2 == k3 ? p2 : 0.0;
-            tail += k1 == k3 ? p1 : 0.0;
-            tail += k0 == k3 ? p0 : 0.0;
-            double head = p0;
-            head += k1 == k0 ? p1 : 0.0;
-            head += k2 == k0 ? p2 : 0.0;
-            // rows strictly inside the lane (a row with <= 2 nonzeros in this
-            // slab) are exclusive to it: flushed here, rarely taken
-            const bool in1 = k1 != k0 && k1 != k3, in2 = k2 != k0 && k2 != k3;
-            if (in1 | in2) {
-                if (in1) sts_add_f64(yp_s + 8u * k1, k2 == k1 ? p1 + p2 : p1);
-                if (in2 && k2 != k1) sts_add_f64(yp_s + 8u * k2, p2);
-            }
-            reduce_piece(k0, head, k3, tail, (cur.k.x & kKeyCont) != 0u, lane, yp_s);
-        }
-        cur = nxt;
+    const int C = (hi - lo) / kChunk, m = C >> 5, r = C & 31;
+    const int cnt = m + (lane < r ? 1 : 0), iters = m + (r > 0 ? 1 : 0);
+    const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);  // chunk i at e0 + 128 i
+    Walk w{ld & 0x7fffu, 0.0, 0.0, true};
+    Chunk ca, cb;
+    if (cnt > 0) load_chunk(ca, vb, kb, e0, pol);
+    for (int i = 0; i < iters; i += 2) {
+        if (cnt > i + 1) load_chunk(cb, vb, kb, e0 + 128u * (i + 1), pol);
+        if (cnt > i) walk_chunk<MODE>(w, ca, xb_s, yp_s);
+        if (i + 1 >= iters) break;
+        if (cnt > i + 2) load_chunk(ca, vb, kb, e0 + 128u * (i + 2), pol);
+        if (cnt > i + 1) walk_chunk<MODE>(w, cb, xb_s, yp_s);
     }
+    if (MODE >= 2) {  // probe: no row sums
+        if (w.acc == 12345.678) sts_add_f64(yp_s, w.acc);
+        return;
+    }
+    reduce_lanes(ld & 0x7fffu, w.head, w.row, w.acc, !w.in_head, (ld & kLaneCont) != 0u, cnt > 0, lane, yp_s);
 }
 
 template <bool DOT, int MODE = 0>
@@ -243,8 +252,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     k_spmv_tiled(TcsrDev T, const double* __restrict__ x, double* __restrict__ y, double* partials,
                  unsigned int* ticket, CgScalars* sc, std::int64_t dot_off) {
     extern __shared__ __align__(128) double smem[];
-    double* xs = smem;               // [2][kSlabW]
-    double* yp = smem + 2 * kSlabW;  // [kMaxTileRows]
+    double* xs = smem;                    // [2][kSlabStride]: slab + zero cell
+    double* yp = smem + 2 * kSlabStride;  // [kMaxTileRows]
     __shared__ __align__(8) std::uint64_t mbar[2];
     __shared__ unsigned released[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -252,6 +261,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 
     if (tid == 0) {
         released[0] = released[1] = 0;
+        xs[kSlabW] = xs[kSlabStride + kSlabW] = 0.0;  // padding entries read these
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -265,13 +275,18 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         const int nrows = static_cast<int>(T.tile_row0[t + 1] - row0);
         const std::int64_t base = T.tile_base[t];
         const double* vb = T.val + base;
-        const std::uint32_t* kb = T.key + base;
+        const std::uint16_t* kb = T.key + base;
         const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
+        const std::uint16_t* lr = T.lrow + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps) * 32 + lane;
         for (int r = tid; r < nrows; r += kTileThreads) yp[r] = 0.0;
-        if (lane == 0 && T.nslabs > 0) prefetch_run(vb, kb, wo[warp], wo[warp + 1]);
+        if (lane == 0)  // runs stream into L2 kPfAhead slabs ahead of their use
+            for (int k = 0; k < kPfAhead && k < T.nslabs; ++k)
+                prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
+        // lane descriptors are loaded one run ahead (registers)
+        unsigned dnext = T.nslabs > 0 ? __ldg(lr + warp * 32) : 0u;
         if (tid == 0 && T.nslabs > 0 && MODE < 5) {
             issue_slab(T, x, xs, 0, &mbar[0]);
-            if (T.nslabs > 1) issue_slab(T, x, xs + kSlabW, 1, &mbar[1]);
+            if (T.nslabs > 1) issue_slab(T, x, xs + kSlabStride, 1, &mbar[1]);
         }
         __syncthreads();
         // Free-running slabs: a warp moves on as soon as the next slab has
@@ -286,17 +301,22 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                 mbar_wait(&mbar[1], phase1);
                 phase1 ^= 1;
             }
-            if (lane == 0 && k + 1 < T.nslabs)  // next slab's run streams into L2 meanwhile
-                prefetch_run(vb, kb, wo[(k + 1) * kTileWarps + warp], wo[(k + 1) * kTileWarps + warp + 1]);
+            const unsigned dcur = dnext;
+            if (k + 1 < T.nslabs) {
+                if (lane == 0 && k + kPfAhead < T.nslabs)
+                    prefetch_run(vb, kb, wo[(k + kPfAhead) * kTileWarps + warp],
+                                 wo[(k + kPfAhead) * kTileWarps + warp + 1]);
+                dnext = __ldg(lr + ((k + 1) * kTileWarps + warp) * 32);
+            }
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
-                vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1],
-                xs_s + 8u * static_cast<unsigned>(buf * kSlabW), yp_s, lane);
+                vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1], dcur,
+                xs_s + 8u * static_cast<unsigned>(buf * kSlabStride), yp_s, lane);
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
                 if (atomicAdd(&released[buf], 1u) == kTileWarps - 1) {
                     released[buf] = 0;
-                    if (k + 2 < T.nslabs && MODE < 5) issue_slab(T, x, xs + buf * kSlabW, k + 2, &mbar[buf]);
+                    if (k + 2 < T.nslabs && MODE < 5) issue_slab(T, x, xs + buf * kSlabStride, k + 2, &mbar[buf]);
                 }
             }
         }

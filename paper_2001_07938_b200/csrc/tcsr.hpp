@@ -14,8 +14,9 @@ struct TcsrHost {
     std::int64_t cols = 0;
     std::vector<std::int64_t> tile_row0, tile_base;
     std::vector<std::int32_t> woff;
+    std::vector<std::uint16_t> lrow;
     std::vector<double> val;
-    std::vector<std::uint32_t> key;
+    std::vector<std::uint16_t> key;
 };
 
 // Does the tiled layout pay for this matrix? (monotone row_ptr, >= 1M nnz,
@@ -27,7 +28,7 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::
                      const double* val, std::int64_t cols, TcsrHost& out);
 
 struct TcsrOwner {
-    DevBuf tile_row0, tile_base, woff, val, key;
+    DevBuf tile_row0, tile_base, woff, lrow, val, key;
     TcsrDev dev;
     bool valid = false;
     std::int64_t bytes = 0;

@@ -44,44 +44,147 @@ int device_sms() {
 
 namespace {
 
-// The kernel gathers x for a 128-nonzero piece as 4 warp instructions (slot s
-// of every lane's 4 consecutive nonzeros); an 8-byte shared load is served
-// per half-warp, and its wavefronts grow with the number of lanes hitting the
-// same bank pair. The nonzeros of one row inside a piece are interchangeable
-// (the kernel's sums only need them grouped by row), so each row segment's
-// nonzeros are dealt to its positions greedily, each position taking the
-// remaining nonzero whose bank pair is least used by its (slot, half-warp).
-// Row keys and continuation bits stay with their positions.
-void balance_gather_banks(double* val, std::uint32_t* key, std::int64_t lo, std::int64_t hi) {
-    std::vector<std::pair<std::uint32_t, double>> pool;
-    for (std::int64_t c = lo; c < hi; c += 128) {
-        const std::int64_t e = std::min<std::int64_t>(hi, c + 128);
-        int cnt[4][2][16] = {};
-        for (std::int64_t a = c; a < e;) {
-            std::int64_t b = a + 1;
-            while (b < e && (key[b] >> 16) == (key[a] >> 16)) ++b;
-            pool.clear();
-            for (std::int64_t q = a; q < b; ++q) pool.emplace_back(key[q] & kKeyColMask, val[q]);
-            for (std::int64_t q = a; q < b; ++q) {
-                const int off = static_cast<int>(q - c), slot = off & 3, half = (off >> 2) >> 4;
-                std::size_t best = 0;
-                int best_n = 1 << 30;
-                for (std::size_t u = 0; u < pool.size(); ++u) {
-                    const int n = cnt[slot][half][pool[u].first & 15u];
-                    if (n < best_n) {
-                        best_n = n;
-                        best = u;
+// One (slab, warp) run of a tile: its row segments in row order, each a
+// range of `js` (tile-local nonzero indices in CSR order).
+struct Seg {
+    std::int32_t row;    // tile-local
+    std::int32_t start;  // into TileRuns::js
+    std::int32_t count;
+};
+
+struct TileRuns {
+    std::vector<std::int32_t> js;       // grouped by run, then row (CSR order inside a row)
+    std::vector<Seg> segs;              // grouped by run, row order
+    std::vector<std::int32_t> run_seg;  // runs + 1 offsets into segs
+    std::vector<std::int32_t> run_js;   // runs + 1 offsets into js
+};
+
+// Collects a tile's runs (counting sort by run over the tile's nonzeros). A
+// row left empty between two rows of a run gets a one-entry segment whose
+// nonzero index is -1 (a zero entry), so a run's rows are consecutive.
+void tile_runs(const std::int64_t* rp, const std::int64_t* ci, std::int64_t row0, const std::int64_t* wb,
+               int nslabs, TileRuns& tr) {
+    const std::int64_t runs = static_cast<std::int64_t>(nslabs) * kTileWarps;
+    std::vector<std::int32_t> nnz_run(static_cast<std::size_t>(runs + 1), 0), seg_run(static_cast<std::size_t>(runs + 1), 0);
+    std::vector<std::int64_t> last(static_cast<std::size_t>(runs), -1);
+    for (int w = 0; w < kTileWarps; ++w)
+        for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
+            for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
+                const std::int64_t run = (ci[j] / kSlabW) * kTileWarps + w;
+                ++nnz_run[run + 1];
+                if (last[run] != r) {
+                    if (last[run] >= 0) {  // empty rows in between
+                        nnz_run[run + 1] += static_cast<std::int32_t>(r - last[run] - 1);
+                        seg_run[run + 1] += static_cast<std::int32_t>(r - last[run] - 1);
                     }
+                    last[run] = r;
+                    ++seg_run[run + 1];
                 }
-                key[q] = (key[q] & ~kKeyColMask) | pool[best].first;
-                val[q] = pool[best].second;
-                ++cnt[slot][half][pool[best].first & 15u];
-                pool[best] = pool.back();
-                pool.pop_back();
             }
-            a = b;
+    for (std::int64_t i = 0; i < runs; ++i) {
+        nnz_run[i + 1] += nnz_run[i];
+        seg_run[i + 1] += seg_run[i];
+    }
+    tr.js.assign(static_cast<std::size_t>(nnz_run[runs]), 0);
+    tr.segs.assign(static_cast<std::size_t>(seg_run[runs]), Seg{});
+    tr.run_seg = seg_run;
+    tr.run_js = nnz_run;
+    std::vector<std::int32_t> jc(nnz_run.begin(), nnz_run.end() - 1), sc(seg_run.begin(), seg_run.end() - 1);
+    std::fill(last.begin(), last.end(), -1);
+    const std::int64_t jb = rp[row0];
+    for (int w = 0; w < kTileWarps; ++w)
+        for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
+            for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
+                const std::int64_t run = (ci[j] / kSlabW) * kTileWarps + w;
+                if (last[run] != r) {
+                    if (last[run] >= 0)
+                        for (std::int64_t e = last[run] + 1; e < r; ++e) {
+                            tr.segs[sc[run]++] = Seg{static_cast<std::int32_t>(e - row0), jc[run], 1};
+                            tr.js[jc[run]++] = -1;
+                        }
+                    last[run] = r;
+                    tr.segs[sc[run]++] = Seg{static_cast<std::int32_t>(r - row0), jc[run], 0};
+                }
+                ++tr.segs[sc[run] - 1].count;
+                tr.js[jc[run]++] = static_cast<std::int32_t>(j - jb);
+            }
+}
+
+std::int64_t run_elems(const TileRuns& tr, std::int64_t run) {
+    const std::int64_t e = tr.run_js[run + 1] - tr.run_js[run];
+    return (e + kChunk - 1) / kChunk * kChunk;
+}
+
+// Writes one run (layout in b200.hpp): lane ranges of whole chunks, chunk i
+// of lane l at (32 i + l) * 4. The nonzeros of one row inside one lane are
+// interchangeable (the lane only sums them), so each (chunk, slot) x gather —
+// one shared-memory instruction of the warp, served per half-warp — is dealt
+// greedily: every lane takes the remaining nonzero of its current row
+// segment whose bank pair is least used so far by that instruction's
+// half-warp (LILAC_B200_TILED_BANKS=0: CSR order). Row-start bits stay with
+// their positions.
+void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, const double* val, std::int64_t jb,
+               std::int64_t slab, bool balance, double* hv, std::uint16_t* hk, std::uint16_t* hl) {
+    const std::int64_t js0 = tr.run_js[run], E = tr.run_js[run + 1] - js0;
+    const std::int64_t C = (E + kChunk - 1) / kChunk, m = C / 32, r = C % 32;
+    // the run's nonzeros in order, with their rows
+    std::vector<std::int32_t> rowof(static_cast<std::size_t>(E));
+    for (std::int32_t i = tr.run_seg[run]; i < tr.run_seg[run + 1]; ++i)
+        for (std::int32_t q = 0; q < tr.segs[i].count; ++q) rowof[tr.segs[i].start - js0 + q] = tr.segs[i].row;
+    auto elem = [&](std::int64_t e) {
+        if (tr.js[js0 + e] < 0) return std::make_pair(kPadKey, 0.0);  // empty row
+        const std::int64_t j = jb + tr.js[js0 + e];
+        return std::make_pair(static_cast<std::uint16_t>(ci[j] - slab * kSlabW), val[j]);
+    };
+    std::int64_t cs[32], cn[32];
+    for (int l = 0; l < 32; ++l) {
+        cs[l] = l * m + std::min<std::int64_t>(l, r);
+        cn[l] = m + (l < r ? 1 : 0);
+        hl[l] = 0;
+        if (cn[l] > 0) {
+            const std::int64_t e0 = cs[l] * kChunk;
+            hl[l] = static_cast<std::uint16_t>(rowof[e0] | (e0 > 0 && rowof[e0 - 1] == rowof[e0] ? kLaneCont : 0));
         }
     }
+    // per lane: the pool of its current row segment (refilled at each start)
+    std::vector<std::pair<std::uint16_t, double>> pool[32];
+    for (std::int64_t i = 0; i < m + (r > 0 ? 1 : 0); ++i)
+        for (int sl = 0; sl < kChunk; ++sl) {
+            int cnt[2][16] = {};
+            for (int l = 0; l < 32; ++l) {
+                if (i >= cn[l]) continue;
+                const std::int64_t e = (cs[l] + i) * kChunk + sl, at = (i * 32 + l) * kChunk + sl;
+                if (e >= E) {
+                    hk[at] = kPadKey;
+                    hv[at] = 0.0;
+                    continue;
+                }
+                const bool first = i == 0 && sl == 0;
+                const bool start = !first && rowof[e] != rowof[e - 1];
+                if (first || start) {  // refill: this segment's nonzeros inside the lane, in CSR order
+                    const std::int64_t lane_end = std::min<std::int64_t>(E, (cs[l] + cn[l]) * kChunk);
+                    pool[l].clear();
+                    for (std::int64_t q = e; q < lane_end && rowof[q] == rowof[e]; ++q) pool[l].push_back(elem(q));
+                    std::reverse(pool[l].begin(), pool[l].end());  // back = CSR-earliest
+                }
+                auto& pl = pool[l];
+                std::size_t best = pl.size() - 1;
+                if (balance) {
+                    int best_n = cnt[l >> 4][pl[best].first & 15u];
+                    for (std::size_t u = pl.size() - 1; u-- > 0 && best_n > 0;) {
+                        const int n = cnt[l >> 4][pl[u].first & 15u];
+                        if (n < best_n) {
+                            best_n = n;
+                            best = u;
+                        }
+                    }
+                    ++cnt[l >> 4][pl[best].first & 15u];
+                }
+                hk[at] = static_cast<std::uint16_t>(pl[best].first | (start ? kKeyStart : 0));
+                hv[at] = pl[best].second;
+                pl.erase(pl.begin() + static_cast<std::ptrdiff_t>(best));
+            }
+        }
 }
 
 }  // namespace
@@ -150,11 +253,11 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     h.ntiles = static_cast<std::int64_t>(h.tile_row0.size()) - 1;
     const std::int64_t per_tile = static_cast<std::int64_t>(h.nslabs) * kTileWarps + 1;
     h.woff.assign(static_cast<std::size_t>(h.ntiles * per_tile), 0);
+    h.lrow.assign(static_cast<std::size_t>(h.ntiles * (per_tile - 1) * 32), 0);
 
-    // pass 1: warp row ranges (nnz-balanced) and per-(slab, warp) counts
+    // pass 1: warp row ranges (nnz-balanced) and per-run stored sizes
     std::vector<std::int64_t> wbounds(static_cast<std::size_t>(h.ntiles * (kTileWarps + 1)));
-    std::vector<std::int64_t> counts(static_cast<std::size_t>(h.ntiles * (per_tile - 1)), 0);
-    std::vector<std::int64_t> padded(static_cast<std::size_t>(h.ntiles), 0);
+    std::vector<std::int64_t> relems(static_cast<std::size_t>(h.ntiles * (per_tile - 1)), 0);
     parallel_tiles(h.ntiles, [&](std::int64_t t) {
         const std::int64_t row0 = h.tile_row0[t], row1 = h.tile_row0[t + 1];
         std::int64_t* wb = wbounds.data() + t * (kTileWarps + 1);
@@ -165,26 +268,28 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
             wb[g] = std::max(std::min(r, row1), wb[g - 1]);
         }
         wb[kTileWarps] = row1;
-        std::int64_t* cnt = counts.data() + t * (per_tile - 1);
-        for (int w = 0; w < kTileWarps; ++w)
-            for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
-                for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) cnt[(ci[j] / kSlabW) * kTileWarps + w]++;
-        std::int64_t tot = 0;
-        for (std::int64_t i = 0; i + 1 < per_tile; ++i) tot += (cnt[i] + kRunAlign - 1) / kRunAlign * kRunAlign;
-        padded[t] = tot;
+        TileRuns tr;
+        tile_runs(rp, ci, row0, wb, h.nslabs, tr);
+        for (std::int64_t i = 0; i + 1 < per_tile; ++i) relems[t * (per_tile - 1) + i] = run_elems(tr, i);
     });
-    // tile bases: every run starts on a kRunAlign-element boundary and is padded
-    // to a multiple of it (pad entries: val 0, sentinel row), so the kernel
-    // never masks individual elements
+    // element offsets, tile-relative per run
     h.tile_base.resize(h.ntiles + 1);
     h.tile_base[0] = 0;
-    for (std::int64_t t = 0; t < h.ntiles; ++t) h.tile_base[t + 1] = h.tile_base[t] + padded[t];
+    for (std::int64_t t = 0; t < h.ntiles; ++t) {
+        std::int32_t* wo = h.woff.data() + t * per_tile;
+        std::int64_t off = 0;
+        for (std::int64_t i = 0; i + 1 < per_tile; ++i) {
+            wo[i] = static_cast<std::int32_t>(off);
+            off += relems[t * (per_tile - 1) + i];
+        }
+        wo[per_tile - 1] = static_cast<std::int32_t>(off);
+        h.tile_base[t + 1] = h.tile_base[t] + off;
+    }
     const std::int64_t total = h.tile_base[h.ntiles];
     h.val.assign(static_cast<std::size_t>(total), 0.0);
     h.key.assign(static_cast<std::size_t>(total), kPadKey);
 
-    // pass 2: offsets and scatter (slab-major, warp range, row order kept),
-    // then the bank balancing of every run (LILAC_B200_TILED_BANKS=0: off)
+    // pass 2: the runs
     const bool balance = [] {
         const char* e = std::getenv("LILAC_B200_TILED_BANKS");
         return !(e && std::strcmp(e, "0") == 0);
@@ -193,31 +298,12 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
         const std::int64_t row0 = h.tile_row0[t];
         const std::int64_t tb = h.tile_base[t];
         const std::int64_t* wb = wbounds.data() + t * (kTileWarps + 1);
-        const std::int64_t* cnt = counts.data() + t * (per_tile - 1);
-        std::int32_t* wo = h.woff.data() + t * per_tile;
-        std::int64_t off = 0;
-        for (std::int64_t i = 0; i + 1 < per_tile; ++i) {
-            wo[i] = static_cast<std::int32_t>(off);
-            off += (cnt[i] + kRunAlign - 1) / kRunAlign * kRunAlign;
-        }
-        wo[per_tile - 1] = static_cast<std::int32_t>(off);
-        std::vector<std::int64_t> cur(wo, wo + per_tile);
-        std::vector<std::int64_t> last(static_cast<std::size_t>(per_tile), -1);  // last row written per run
-        for (int w = 0; w < kTileWarps; ++w)
-            for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r) {
-                const std::uint32_t lrow = static_cast<std::uint32_t>(r - row0) << 16;
-                for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
-                    const std::int64_t k = ci[j] / kSlabW;
-                    const std::int64_t run = k * kTileWarps + w;
-                    const std::int64_t pos = tb + cur[run]++;
-                    h.val[pos] = val[j];
-                    h.key[pos] = lrow | (last[run] == r ? kKeyCont : 0u) | static_cast<std::uint32_t>(ci[j] - k * kSlabW);
-                    last[run] = r;
-                }
-            }
-        if (balance)
-            for (std::int64_t i = 0; i + 1 < per_tile; ++i)
-                balance_gather_banks(h.val.data() + tb, h.key.data() + tb, wo[i], wo[i + 1]);
+        const std::int32_t* wo = h.woff.data() + t * per_tile;
+        TileRuns tr;
+        tile_runs(rp, ci, row0, wb, h.nslabs, tr);
+        for (std::int64_t i = 0; i + 1 < per_tile; ++i)
+            write_run(tr, i, ci, val, rp[row0], i / kTileWarps, balance, h.val.data() + tb + wo[i],
+                      h.key.data() + tb + wo[i], h.lrow.data() + (t * (per_tile - 1) + i) * 32);
     });
 }
 
@@ -226,15 +312,18 @@ void TcsrOwner::upload(const TcsrHost& h) {
     tile_row0.ensure(h.tile_row0.size() * 8);
     tile_base.ensure(h.tile_base.size() * 8);
     woff.ensure(h.woff.size() * 4);
+    lrow.ensure(std::max<std::size_t>(h.lrow.size(), 1) * 2);
     val.ensure(h.val.size() * 8);
-    key.ensure(h.key.size() * 4);
+    key.ensure(h.key.size() * 2);
     B200_CUDA(cudaMemcpyAsync(tile_row0.ptr, h.tile_row0.data(), h.tile_row0.size() * 8, cudaMemcpyHostToDevice, s));
     B200_CUDA(cudaMemcpyAsync(tile_base.ptr, h.tile_base.data(), h.tile_base.size() * 8, cudaMemcpyHostToDevice, s));
-    if (!h.woff.empty())
+    if (!h.woff.empty()) {
         B200_CUDA(cudaMemcpyAsync(woff.ptr, h.woff.data(), h.woff.size() * 4, cudaMemcpyHostToDevice, s));
+        B200_CUDA(cudaMemcpyAsync(lrow.ptr, h.lrow.data(), h.lrow.size() * 2, cudaMemcpyHostToDevice, s));
+    }
     if (!h.val.empty()) {
         B200_CUDA(cudaMemcpyAsync(val.ptr, h.val.data(), h.val.size() * 8, cudaMemcpyHostToDevice, s));
-        B200_CUDA(cudaMemcpyAsync(key.ptr, h.key.data(), h.key.size() * 4, cudaMemcpyHostToDevice, s));
+        B200_CUDA(cudaMemcpyAsync(key.ptr, h.key.data(), h.key.size() * 2, cudaMemcpyHostToDevice, s));
     }
     B200_CUDA(cudaStreamSynchronize(s));
     dev.ntiles = h.ntiles;
@@ -243,9 +332,11 @@ void TcsrOwner::upload(const TcsrHost& h) {
     dev.tile_row0 = tile_row0.as<std::int64_t>();
     dev.tile_base = tile_base.as<std::int64_t>();
     dev.woff = woff.as<std::int32_t>();
+    dev.lrow = lrow.as<std::uint16_t>();
     dev.val = val.as<double>();
-    dev.key = key.as<std::uint32_t>();
-    bytes = static_cast<std::int64_t>(tile_row0.bytes + tile_base.bytes + woff.bytes + val.bytes + key.bytes);
+    dev.key = key.as<std::uint16_t>();
+    bytes = static_cast<std::int64_t>(tile_row0.bytes + tile_base.bytes + woff.bytes + lrow.bytes + val.bytes +
+                                      key.bytes);
     valid = true;
 }
 
@@ -253,6 +344,7 @@ void TcsrOwner::release() {
     tile_row0.release();
     tile_base.release();
     woff.release();
+    lrow.release();
     val.release();
     key.release();
     dev = TcsrDev{};
