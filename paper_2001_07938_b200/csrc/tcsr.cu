@@ -173,14 +173,14 @@ __device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::u
         w.acc += p;
         return;
     }
-    if (key & kKeyStart) {  // a new row: the previous one is complete
-        if (!w.in_head) sts_add_f64(yp_s + 8u * w.row, w.acc);  // began and ended in this lane: exclusive
-        else w.head = w.acc;
-        w.in_head = false;
-        ++w.row;
-        w.acc = 0.0;
-    }
-    w.acc += p;
+    // a new row: the previous one is complete (branch-free; the flush of a
+    // row that began and ended in this lane is predicated, exclusive)
+    const bool st = (key & kKeyStart) != 0u;
+    if (st && !w.in_head) sts_add_f64(yp_s + 8u * w.row, w.acc);
+    w.head = st && w.in_head ? w.acc : w.head;
+    w.in_head = w.in_head && !st;
+    w.row += st ? 1u : 0u;
+    w.acc = (st ? 0.0 : w.acc) + p;
 }
 
 template <int MODE>
