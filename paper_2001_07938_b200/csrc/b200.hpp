@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <utility>
 
 #include "lilac/marshal.hpp"
 
@@ -21,6 +22,35 @@ using lilac::marshal::Error;
         cudaError_t e_ = (call);                                            \
         if (e_ != cudaSuccess) ::b200::throw_cuda(e_, #call, __FILE__, __LINE__); \
     } while (0)
+
+// Programmatic dependent launch for the CG step kernels (k_spmv_tiled's p.q
+// variant, k_cg_update_zr, k_cg_update_p): each is launched with programmatic
+// stream serialization, lets its successor launch early
+// (griddepcontrol.launch_dependents) and waits for its predecessor's
+// completion and memory (griddepcontrol.wait) before touching anything the
+// predecessor wrote, so the launch and prologue overlap the predecessor's
+// tail. LILAC_B200_PDL=0 turns it off.
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    B200_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
 
 // ---------------------------------------------------------------------------
 // Device memory
@@ -229,7 +259,7 @@ struct CgScalars {  // device-resident, one per solver (shard)
     double rho, rho0, d, alpha, beta, rnorm, t1, t2, zeta;
     unsigned int ticket[4];
     int nranks;     // > 1: sharded mode — reductions stop at this shard's partial (part[]); exchange + fin_* follow
-    int pad;
+    unsigned int bar;  // grid barrier counter of the fused CG kernel (zeroed before each launch)
     double part[4];
     // peer-memory exchange (p2p.hpp P2pDesc, device memory) or null: when set,
     // the kernel that produces the partials also pushes them to the peers
@@ -250,6 +280,11 @@ constexpr int kMaxParts = 2048;
 
 void cg_launch_init(const CgVectors& v, cudaStream_t s);            // q=z=0, r=p=x, rho=r.r
 void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s);
+// `steps` CG iterations: one persistent fused kernel (tcsr.cu k_cg_tiled) for
+// a tiled matrix on one GPU, else cg_launch_iteration per step.
+void cg_launch_iterations(const CsrDev& A, const CgVectors& v, int steps, cudaStream_t s);
+// Fused single-GPU CG steps over the tiled layout; false if not available.
+bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream_t s);
 void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s);  // r=A z, rnorm
 void cg_launch_outer_update(const CgVectors& v, double shift, cudaStream_t s);  // zeta, x = z/|z|
 void cg_launch_reset_x(const CgVectors& v, cudaStream_t s);

@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(CgVectors v) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_cg_update_zr(CgVectors v) {
+    pdl_trigger();
+    pdl_wait();
     const double alpha = v.sc->alpha;
     double rr = 0.0;
     GRID_STRIDE(i, v.n) {
@@ -111,6 +113,8 @@ __global__ void __launch_bounds__(kThreads) k_cg_update_zr(CgVectors v) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_cg_update_p(CgVectors v) {
+    pdl_trigger();
+    pdl_wait();
     const double beta = v.sc->beta;
     GRID_STRIDE(i, v.n) v.p[i] = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
 }
@@ -215,13 +219,11 @@ void cg_launch_spmv_dot(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
 }
 
 void cg_launch_update_zr(const CgVectors& v, cudaStream_t s) {
-    k_cg_update_zr<<<vec_grid(v), kThreads, 0, s>>>(v);
-    B200_CUDA(cudaGetLastError());
+    launch_pdl(k_cg_update_zr, dim3(vec_grid(v)), dim3(kThreads), 0, s, v);
 }
 
 void cg_launch_update_p(const CgVectors& v, cudaStream_t s) {
-    k_cg_update_p<<<vec_grid(v), kThreads, 0, s>>>(v);
-    B200_CUDA(cudaGetLastError());
+    launch_pdl(k_cg_update_p, dim3(vec_grid(v)), dim3(kThreads), 0, s, v);
 }
 
 void cg_launch_norms(const CgVectors& v, double shift, cudaStream_t s) {
@@ -243,6 +245,11 @@ void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s) {
     cg_launch_spmv_dot(A, v, s);
     cg_launch_update_zr(v, s);
     cg_launch_update_p(v, s);
+}
+
+void cg_launch_iterations(const CsrDev& A, const CgVectors& v, int steps, cudaStream_t s) {
+    if (A.tiled && launch_cg_tiled(*A.tiled, v, steps, s)) return;
+    for (int it = 0; it < steps; ++it) cg_launch_iteration(A, v, s);
 }
 
 void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s) {

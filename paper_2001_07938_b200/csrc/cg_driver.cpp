@@ -32,7 +32,7 @@ cudaStream_t pick(void* stream) {
 
 void record_outer(b200_cg* cg, int cgitmax, double shift, cudaStream_t s) {
     cg_launch_init(cg->v, s);
-    for (int it = 0; it < cgitmax; ++it) cg_launch_iteration(cg->A, cg->v, s);
+    cg_launch_iterations(cg->A, cg->v, cgitmax, s);
     cg_launch_residual(cg->A, cg->v, s);
     cg_launch_outer_update(cg->v, shift, s);
 }
@@ -134,7 +134,7 @@ int b200_cg_solve(b200_cg* cg, const double* b, int iters, double* z_out, double
         const std::size_t bytes = sizeof(double) * static_cast<std::size_t>(cg->v.n);
         if (bytes) B200_CUDA(cudaMemcpyAsync(cg->v.x, b, bytes, cudaMemcpyDeviceToDevice, s));
         cg_launch_init(cg->v, s);  // z = 0, r = p = b
-        for (int it = 0; it < iters; ++it) cg_launch_iteration(cg->A, cg->v, s);
+        cg_launch_iterations(cg->A, cg->v, iters, s);
         cg_launch_residual(cg->A, cg->v, s);  // |b - A z|
         if (z_out && bytes) B200_CUDA(cudaMemcpyAsync(z_out, cg->v.z, bytes, cudaMemcpyDeviceToDevice, s));
         B200_CUDA(cudaStreamSynchronize(s));

@@ -726,3 +726,15 @@ void b200_stats_reset(void) {
 }
 
 }  // extern "C"
+
+namespace b200 {
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LILAC_B200_PDL");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
+}  // namespace b200

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 namespace b200 {
 
@@ -108,7 +109,7 @@ __device__ __forceinline__ void issue_slab(const TcsrDev& T, const double* __res
     const int len = slab_len(T, k);
     const int even = len & ~1;
     const double* src = x + static_cast<std::int64_t>(k) * kSlabW;
-    if (len & 1) xs[even] = src[even];
+    if (len & 1) xs[even] = __ldcg(src + even);  // L2: x may have been written earlier in this kernel
     mbar_arrive_tx(mbar, static_cast<unsigned>(even) * 8u);
     if (even) bulk_g2s(xs, src, static_cast<unsigned>(even) * 8u, mbar);
 }
@@ -247,29 +248,44 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
     reduce_lanes(ld & 0x7fffu, w.head, w.row, w.acc, !w.in_head, (ld & kLaneCont) != 0u, cnt > 0, lane, yp_s);
 }
 
-template <bool DOT, int MODE = 0>
-__global__ void __launch_bounds__(kTileThreads, 1)
-    k_spmv_tiled(TcsrDev T, const double* __restrict__ x, double* __restrict__ y, double* partials,
-                 unsigned int* ticket, CgScalars* sc, std::int64_t dot_off) {
-    extern __shared__ __align__(128) double smem[];
-    double* xs = smem;                    // [2][kSlabStride]: slab + zero cell
-    double* yp = smem + 2 * kSlabStride;  // [kMaxTileRows]
-    __shared__ __align__(8) std::uint64_t mbar[2];
-    __shared__ unsigned released[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const std::uint32_t xs_s = smem_addr(xs), yp_s = smem_addr(yp);
+// Shared-memory state of a tiled SpMV CTA (slab double buffer, row sums,
+// mbarriers), carried across tiles and, in the fused CG kernel, across steps.
+struct TileCta {
+    double* xs;  // [2][kSlabStride]: slab + zero cell
+    double* yp;  // [kMaxTileRows]
+    std::uint64_t* mbar;
+    unsigned* released;
+    std::uint32_t xs_s, yp_s;
+    unsigned phase0, phase1;
+};
 
-    if (tid == 0) {
+__device__ __forceinline__ void tile_cta_init(TileCta& c, double* smem, std::uint64_t* mbar, unsigned* released) {
+    c.xs = smem;
+    c.yp = smem + 2 * kSlabStride;
+    c.mbar = mbar;
+    c.released = released;
+    c.xs_s = smem_addr(c.xs);
+    c.yp_s = smem_addr(c.yp);
+    c.phase0 = c.phase1 = 0;
+    if (threadIdx.x == 0) {
         released[0] = released[1] = 0;
-        xs[kSlabW] = xs[kSlabStride + kSlabW] = 0.0;  // padding entries read these
+        c.xs[kSlabW] = c.xs[kSlabStride + kSlabW] = 0.0;  // padding entries read these
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-    unsigned phase0 = 0, phase1 = 0;
-    double pq = 0.0;
+}
 
+// y = A x over this CTA's tiles; with DOT, returns this thread's share of
+// x.y over the tiles' rows (x read at dot_off + row). COHERENT: x may have been
+// written earlier in the same kernel (fused CG): read it through L2 only.
+template <bool DOT, int MODE, bool COHERENT>
+__device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, double* y, std::int64_t dot_off,
+                                             TileCta& c) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* xs = c.xs;
+    double* yp = c.yp;
+    double pq = 0.0;
     for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
         const std::int64_t row0 = T.tile_row0[t];
         const int nrows = static_cast<int>(T.tile_row0[t + 1] - row0);
@@ -285,8 +301,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         // lane descriptors are loaded one run ahead (registers)
         unsigned dnext = T.nslabs > 0 ? __ldg(lr + warp * 32) : 0u;
         if (tid == 0 && T.nslabs > 0 && MODE < 5) {
-            issue_slab(T, x, xs, 0, &mbar[0]);
-            if (T.nslabs > 1) issue_slab(T, x, xs + kSlabStride, 1, &mbar[1]);
+            if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
+            issue_slab(T, x, xs, 0, &c.mbar[0]);
+            if (T.nslabs > 1) issue_slab(T, x, xs + kSlabStride, 1, &c.mbar[1]);
         }
         __syncthreads();
         // Free-running slabs: a warp moves on as soon as the next slab has
@@ -295,11 +312,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             const int buf = k & 1;
             if (MODE >= 5) {
             } else if (buf == 0) {
-                mbar_wait(&mbar[0], phase0);
-                phase0 ^= 1;
+                mbar_wait(&c.mbar[0], c.phase0);
+                c.phase0 ^= 1;
             } else {
-                mbar_wait(&mbar[1], phase1);
-                phase1 ^= 1;
+                mbar_wait(&c.mbar[1], c.phase1);
+                c.phase1 ^= 1;
             }
             const unsigned dcur = dnext;
             if (k + 1 < T.nslabs) {
@@ -310,13 +327,16 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             }
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
                 vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1], dcur,
-                xs_s + 8u * static_cast<unsigned>(buf * kSlabStride), yp_s, lane);
+                c.xs_s + 8u * static_cast<unsigned>(buf * kSlabStride), c.yp_s, lane);
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
-                if (atomicAdd(&released[buf], 1u) == kTileWarps - 1) {
-                    released[buf] = 0;
-                    if (k + 2 < T.nslabs && MODE < 5) issue_slab(T, x, xs + buf * kSlabStride, k + 2, &mbar[buf]);
+                if (atomicAdd(&c.released[buf], 1u) == kTileWarps - 1) {
+                    c.released[buf] = 0;
+                    if (k + 2 < T.nslabs && MODE < 5) {
+                        if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");
+                        issue_slab(T, x, xs + buf * kSlabStride, k + 2, &c.mbar[buf]);
+                    }
                 }
             }
         }
@@ -324,10 +344,33 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         for (int r = tid; r < nrows; r += kTileThreads) {
             const double v = yp[r];
             y[row0 + r] = v;
-            if (DOT) pq += v * __ldg(x + dot_off + row0 + r);
+            if (DOT) pq += v * (COHERENT ? __ldcg(x + dot_off + row0 + r) : __ldg(x + dot_off + row0 + r));
         }
         __syncthreads();  // yp reused by the next tile
     }
+    return pq;
+}
+
+template <bool DOT, int MODE = 0>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_spmv_tiled(TcsrDev T, const double* __restrict__ x, double* __restrict__ y, double* partials,
+                 unsigned int* ticket, CgScalars* sc, std::int64_t dot_off) {
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) std::uint64_t mbar[2];
+    __shared__ unsigned released[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    TileCta c;
+    tile_cta_init(c, smem, mbar, released);
+    if (DOT) {  // CG step: launched programmatically after update_p
+        pdl_trigger();
+        if (lane == 0 && blockIdx.x < T.ntiles && T.nslabs > 0) {  // the matrix does not depend on it
+            const std::int32_t* wo = T.woff + blockIdx.x * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
+            prefetch_run(T.val + T.tile_base[blockIdx.x], T.key + T.tile_base[blockIdx.x], wo[warp], wo[warp + 1]);
+        }
+        pdl_wait();
+    }
+    __syncthreads();
+    const double pq = spmv_tiles<DOT, MODE, false>(T, x, y, dot_off, c);
 
     if (DOT) {
         __shared__ double red[kTileWarps];
@@ -368,6 +411,109 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
 }
 
+// Grid-wide barrier of a co-resident (cooperative) grid: monotonic counter,
+// `target` advances by gridDim.x per barrier.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// Sum of every thread's v, returned to all threads (fixed tree).
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = warp_sum(red[lane]);
+        if (lane == 0) red[kTileWarps] = v;
+    }
+    __syncthreads();
+    return red[kTileWarps];
+}
+
+// Sum of p[0..n) (the CTAs' partials) in a fixed order: the same bits in
+// every CTA.
+__device__ __forceinline__ double cta_sum_parts(const double* p, int n, double* red) {
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += kTileThreads) a += __ldcg(p + i);
+    return cta_sum(a, red);
+}
+
+// `steps` NPB CG iterations (conj_grad's inner loop) on one GPU in one
+// persistent cooperative kernel: per step q = A p with the p.q partials
+// (spmv_tiles), grid barrier, alpha, z/r update of the CTA's own tile rows
+// with the r.r partials, grid barrier, beta, p update of its own rows, grid
+// barrier. Replaces 3 launches per step; dots are deterministic (fixed
+// per-CTA partition, every CTA sums the partials in CTA order), updates use
+// explicitly rounded mul/add like k_cg_update_zr/k_cg_update_p.
+__global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVectors v, int steps) {
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) std::uint64_t mbar[2];
+    __shared__ unsigned released[2];
+    __shared__ double red[kTileWarps + 1];
+    const int tid = threadIdx.x;
+    TileCta c;
+    tile_cta_init(c, smem, mbar, released);
+    __syncthreads();
+    unsigned target = 0;
+    unsigned* bar = &v.sc->bar;
+    double rho = __ldcg(&v.sc->rho);
+    double* pq_part = v.partials;
+    double* rr_part = v.partials + 2 * kMaxParts;
+    for (int it = 0; it < steps; ++it) {
+        const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c), red);
+        if (tid == 0) pq_part[blockIdx.x] = pq;
+        grid_sync(bar, target);
+        const double d = cta_sum_parts(pq_part, gridDim.x, red);
+        const double alpha = rho / d;
+        double rr = 0.0;
+        for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+            const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
+            for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads) {
+                const double zi = __dadd_rn(v.z[i], __dmul_rn(alpha, v.p[i]));
+                const double ri = __dsub_rn(v.r[i], __dmul_rn(alpha, v.q[i]));
+                v.z[i] = zi;
+                v.r[i] = ri;
+                rr += ri * ri;
+            }
+        }
+        rr = cta_sum(rr, red);
+        if (tid == 0) {
+            rr_part[blockIdx.x] = rr;
+            if (blockIdx.x == 0) {
+                v.sc->d = d;
+                v.sc->rho0 = rho;
+                v.sc->alpha = alpha;
+            }
+        }
+        grid_sync(bar, target);
+        const double rho_new = cta_sum_parts(rr_part, gridDim.x, red);
+        const double beta = rho_new / rho;
+        for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+            const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
+            for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads)
+                v.p[i] = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
+        }
+        if (tid == 0 && blockIdx.x == 0) {
+            v.sc->rho = rho_new;
+            v.sc->beta = beta;
+        }
+        rho = rho_new;
+        grid_sync(bar, target);
+    }
+}
+
 int g_sms = 0;
 
 }  // namespace
@@ -384,8 +530,8 @@ void launch_variant(const TcsrDev& T, const double* x, double* y, double* partia
         configured = true;
     }
     if (partials)
-        k_spmv_tiled<true, MODE><<<std::min<unsigned>(grid, kMaxParts), kTileThreads, kTileSmem, s>>>(
-            T, x, y, partials, ticket, sc, dot_off);
+        launch_pdl(k_spmv_tiled<true, MODE>, dim3(std::min<unsigned>(grid, kMaxParts)), dim3(kTileThreads),
+                   kTileSmem, s, T, x, y, partials, ticket, sc, dot_off);
     else
         k_spmv_tiled<false, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr, 0);
 }
@@ -410,6 +556,39 @@ void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, dou
     default: launch_variant<0>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     }
     B200_CUDA(cudaGetLastError());
+}
+
+bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream_t s) {
+    static int enabled = -1;
+    static int max_grid = 0;
+    if (enabled < 0) {
+        const char* e = std::getenv("LILAC_B200_CG_FUSED");
+        enabled = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+        int dev = 0, coop = 0, per_sm = 0, sms = 0;
+        B200_CUDA(cudaGetDevice(&dev));
+        B200_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        B200_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        B200_CUDA(cudaFuncSetAttribute(k_cg_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kTileSmem)));
+        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tiled, kTileThreads, kTileSmem));
+        max_grid = coop ? per_sm * sms : 0;
+        if (max_grid <= 0) enabled = 0;
+    }
+    if (!enabled || steps <= 0 || T.ntiles <= 0 || v.row0 != 0 || v.p != v.p_full) return false;
+    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>({T.ntiles, max_grid, kMaxParts}));
+    B200_CUDA(cudaMemsetAsync(&v.sc->bar, 0, sizeof(unsigned), s));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = kTileSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    B200_CUDA(cudaLaunchKernelEx(&cfg, k_cg_tiled, T, v, steps));
+    return true;
 }
 
 }  // namespace b200
