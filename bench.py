@@ -552,6 +552,7 @@ def run_ours(args):
     # strong scaling: the job advances one NPB iteration per step whatever N is
     value = args.steps / (ms_total / 1e3)
     col_b = info["col_bytes"]
+    fused_cg = info["kernel"] == 4 and os.environ.get("LILAC_B200_CG_FUSED", "1") != "0"
     snnz, srows = info["nnz"], info["rows"]
     spmv_bytes = snnz * (8 + col_b) + (srows + 1) * 8 + 8 * srows + 8 * info["cols"]
     spmv_flops = 2 * snnz
@@ -581,7 +582,12 @@ def run_ours(args):
                      "peak_source": peak_src,
                      "how": f"algorithmic bytes nnz*(8+{col_b})+8(rows+1)+8rows+8cols per launch / mean of "
                             f"{args.spmv_reps} back-to-back launches timed with CUDA events on the bench stream"},
-        "gpu_launches": args.steps * ((1 + 3 * CGITMAX + 2 + 2) if world == 1 else (1 + 5 * CGITMAX + 6 + 2)),
+        # per NPB iteration: init, the CG steps (one persistent cooperative kernel on one GPU with the
+        # tiled layout, else 3 per step; sharded: 5 per step), residual SpMV + norm, zeta + x update
+        "gpu_launches": args.steps * (((1 + 1 + 2 + 2) if fused_cg else (1 + 3 * CGITMAX + 2 + 2)) if world == 1
+                                      else (1 + 5 * CGITMAX + 6 + 2)),
+        "cg_steps": "one persistent kernel per NPB iteration (grid barriers)" if fused_cg and world == 1
+                    else "3 kernels per CG step (programmatic dependent launch)",
         "clocks": clk,
         "gen_s": t_gen,
     }

@@ -11,4 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/prof_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmv_tiled -s 8 -c 1 \
     -o gpurun_out/prof_top $CMD > gpurun_out/prof_full.log 2>&1
-echo "profile done"
+
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cg_tiled -c 1 \
+    -o gpurun_out/prof_cg $CMD > gpurun_out/prof_cg.log 2>&1
+echo "fused cg profile done"
