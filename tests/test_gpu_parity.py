@@ -176,6 +176,77 @@ def test_random_csr_vs_oracle(shape):
     assert O.same_bits(yj, y_ref)
 
 
+def _short_rows_csr(rng, rows, cols, max_len):
+    """Vectorised random CSR: row lengths in [0, max_len], distinct sorted columns."""
+    lens = rng.integers(0, max_len + 1, rows).astype(np.int64)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(rp[-1])
+    row = np.repeat(np.arange(rows, dtype=np.int64), lens)
+    ci = rng.integers(0, cols, nnz).astype(np.int64)
+    order = np.lexsort((ci, row))
+    ci = ci[order]
+    dup = np.zeros(nnz, bool)
+    dup[1:] = (row[1:] == row[:-1]) & (ci[1:] == ci[:-1])
+    ci[dup] = (ci[dup] + 1) % cols  # rare; keep rows sorted enough for the reference semantics
+    return rp, ci, rng.uniform(-2, 2, nnz)
+
+
+def test_tiled_layout_edge_cases():
+    """Tiled layout (tcsr_build.cpp) corners: more tiles than SMs (several per
+    CTA), rows of 0-3 nonzeros (empty rows inside runs -> zero entries, several
+    row starts per 4-nonzero chunk, lanes without chunks in short runs), an odd
+    column count (odd last slab), and an Inf in x: rows that do not reference
+    it must stay finite (padding entries read the zero cell, never x)."""
+    rng = np.random.default_rng(20240817)
+    rows, cols = 148 * 4096 + 5000, 2 * 12288 + 1
+    rp, ci, val = _short_rows_csr(rng, rows, cols, 3)
+    x = rng.uniform(-2, 2, cols)
+    x[cols - 1] = np.inf
+    y_ref = O.spmv_csr(rp, ci, val, x)
+    N.lib().b200_set_kernel(b"tiled")
+    A = D.Matrix.csr(rp, ci, val)
+    assert A.info()["kernel"] == 4 and A.info()["col_bytes"] == 2
+    A.free()
+    y = run_csr(rp, ci, val, x)
+    fin = np.isfinite(y_ref)
+    assert (~fin).sum() > 0 and fin.sum() > rows // 2
+    assert np.array_equal(np.isfinite(y), fin)
+    assert np.array_equal(y[~fin], y_ref[~fin])  # same signed infinities
+    assert_within(y[fin], y_ref[fin], spmv_bound(rp, ci, val, np.where(np.isfinite(x), x, 0.0))[fin])
+
+
+def test_fused_cg_matches_per_step_kernels():
+    """CG on one GPU with the tiled layout runs its steps in one persistent
+    cooperative kernel (k_cg_tiled) — here with more tiles than SMs; the vector
+    layout runs three kernels per step. Same iterates up to rounding."""
+    import torch
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from bench_configs import gen_stencil27
+    nx = 85  # 614,125 rows > 148 x 4096
+    rp, ci, val = gen_stencil27(nx)
+    n = nx ** 3
+    b = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, n)).cuda()
+    out = {}
+    for kern in (b"tiled", b"vector"):
+        N.lib().b200_set_kernel(kern)
+        A = D.Matrix.csr(rp, ci, val)
+        assert (A.info()["kernel"] == 4) == (kern == b"tiled")
+        cg = D.CG(A)
+        z = torch.empty_like(b)
+        res = cg.solve(b.data_ptr(), 30, z.data_ptr())
+        torch.cuda.synchronize()
+        out[kern] = (res, z.cpu().numpy())
+        cg.free()
+        A.free()
+    (r_t, z_t), (r_v, z_v) = out[b"tiled"], out[b"vector"]
+    bn = float(torch.linalg.norm(b))
+    assert r_v < 0.01 * bn  # CG made progress (kappa ~ 500: not converged in 30 steps)
+    assert abs(r_t - r_v) <= 1e-8 * r_v
+    assert np.abs(z_t - z_v).max() <= 1e-9 * np.abs(z_v).max()
+
+
 def test_edge_cases():
     # rows = 0
     y = np.zeros(0)
