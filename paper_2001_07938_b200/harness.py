@@ -66,7 +66,52 @@ def _ext():
 _EXT = False
 
 
+# ---- host memory lifetime ----------------------------------------------------------
+# The marshaling runtime write-protects pages of the arrays it caches (change
+# detection) and, in lazy mode, leaves output pages inaccessible until read.
+# A C caller owns its arrays for as long as it uses the harness; a numpy array
+# can die and its memory be reused by the allocator while the pages are still
+# protected — a later write by the kernel into that memory (a read() into a
+# buffer) then fails with EFAULT instead of faulting into the handler. So the
+# first time an array's memory reaches the harness, a finalizer on its owner
+# forgets the range (guards dropped, pages restored, cached device copy
+# released) when the owner dies.
+_TRACKED: dict = {}
+
+
+def _owner(a):
+    o = a
+    while isinstance(o, np.ndarray) and o.base is not None:
+        o = o.base
+    return o
+
+
+def _track(*arrays):
+    for a in arrays:
+        if not isinstance(a, np.ndarray) or a.nbytes == 0:
+            continue
+        o = _owner(a)
+        k = id(o)
+        if k in _TRACKED:
+            continue
+        try:
+            if isinstance(o, np.ndarray):
+                addr, size = o.ctypes.data, o.nbytes
+            else:  # a buffer object (mmap, bytearray, ...): its whole range
+                whole = np.frombuffer(o, np.uint8)
+                addr, size = whole.ctypes.data, whole.nbytes
+            _TRACKED[k] = weakref.finalize(o, _untrack, k, addr, size)
+        except (TypeError, ValueError):
+            pass  # not weak-referenceable: nothing to hook
+
+
+def _untrack(k, addr, size):
+    _TRACKED.pop(k, None)
+    _forget_addr(addr, size)
+
+
 def spmv_csr(rows, output, row_ptr, val, x, col_ind):
+    _track(output, row_ptr, val, x, col_ind)
     E = _ext()
     if E is not None:
         return E.spmv_csr(int(rows), output, row_ptr, val, x, col_ind)
@@ -77,6 +122,7 @@ def spmv_csr(rows, output, row_ptr, val, x, col_ind):
 
 
 def spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind):
+    _track(output, nzcnt, perm, val, jd_ptr, x, col_ind)
     E = _ext()
     if E is not None:
         return E.spmv_jds(int(rows), output, nzcnt, perm, val, jd_ptr, x, col_ind)
@@ -88,6 +134,7 @@ def spmv_jds(rows, output, nzcnt, perm, val, jd_ptr, x, col_ind):
 
 
 def dotproduct(length, a, b) -> float:
+    _track(a, b)
     E = _ext()
     if E is not None:
         return E.dotproduct(int(length), a, b)
@@ -99,6 +146,7 @@ def dotproduct(length, a, b) -> float:
 
 def gemm(n, m, c, p, a, b):
     """c[i*m + j] = sum_k a[i*p + k] * b[k*m + j] (kernels.lilac:14-19)."""
+    _track(c, a, b)
     E = _ext()
     if E is not None:
         return E.gemm(int(n), int(m), c, int(p), a, b)
@@ -110,6 +158,7 @@ def gemm(n, m, c, p, a, b):
 
 
 def axpy(n, y, alpha, x):
+    _track(y, x)
     E = _ext()
     if E is not None:
         return E.axpy(int(n), y, float(alpha), x)
@@ -118,6 +167,7 @@ def axpy(n, y, alpha, x):
 
 
 def xpay(n, y, beta, x):
+    _track(y, x)
     E = _ext()
     if E is not None:
         return E.xpay(int(n), y, float(beta), x)

@@ -131,3 +131,22 @@ def test_python_binding_checks_arguments_before_calling():
         H.spmv_csr(1, ro, rp, val, x, ci)
     with pytest.raises(TypeError, match="y"):
         H.axpy(1, ro, 1.0, x)
+
+
+def test_harness_tracks_array_lifetimes():
+    """Every array handed to a harness binding gets a finalizer on its owner
+    that forgets the range (guards, lazy pages, device copy) when it dies, so
+    protected pages never outlive the memory (harness.py _track)."""
+    import gc
+
+    import numpy as np
+
+    from paper_2001_07938_b200 import harness as H
+    base = np.arange(4096, dtype=np.float64)
+    view = base[8:1000]
+    H._track(view, view[3:5], np.zeros(0))
+    assert id(base) in H._TRACKED and len([k for k in H._TRACKED if k == id(base)]) == 1
+    k = id(base)
+    del base, view
+    gc.collect()
+    assert k not in H._TRACKED
