@@ -219,11 +219,15 @@ __device__ __forceinline__ void reduce_lanes(unsigned k0, double p0, unsigned k1
     if (active && split) sts_add_f64(yp_s + 8u * k0, p0);
 }
 
-// Lane `lane`'s first chunk of the run [lo, hi) (none when the run has fewer
-// chunks than lanes and this lane gets none).
-__device__ __forceinline__ void load_first_chunk(Chunk& c, const double* vb, const std::uint16_t* kb, int lo, int hi,
-                                                 int lane, std::uint64_t pol) {
-    if (lane < (hi - lo) / kChunk) load_chunk(c, vb, kb, static_cast<unsigned>(lo + kChunk * lane), pol);
+// Lane `lane`'s chunks 0 and 1 of the run [lo, hi) (those it has: lane l
+// gets m or m + 1 chunks, m = C / 32).
+__device__ __forceinline__ void load_head_chunks(Chunk& c0, Chunk& c1, const double* vb, const std::uint16_t* kb,
+                                                 int lo, int hi, int lane, std::uint64_t pol) {
+    const int C = (hi - lo) / kChunk;
+    const int cnt = (C >> 5) + (lane < (C & 31) ? 1 : 0);
+    const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);
+    if (cnt > 0) load_chunk(c0, vb, kb, e0, pol);
+    if (cnt > 1) load_chunk(c1, vb, kb, e0 + 128u, pol);
 }
 
 // Processes a (slab, warp) run [lo, hi) (tile-relative, multiples of kChunk)
@@ -232,7 +236,7 @@ __device__ __forceinline__ void load_first_chunk(Chunk& c, const double* vb, con
 // loaded while the current one is walked.
 template <int MODE>
 __device__ __forceinline__ void process_run(const double* vb, const std::uint16_t* kb, int lo, int hi, unsigned ld,
-                                            Chunk& first, int next_lo, int next_hi, std::uint32_t xb_s,
+                                            Chunk& ca, Chunk& cb, int next_lo, int next_hi, std::uint32_t xb_s,
                                             std::uint32_t yp_s, int lane) {
     std::uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -240,18 +244,18 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
     const int cnt = m + (lane < r ? 1 : 0), iters = m + (r > 0 ? 1 : 0);
     const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);  // chunk i at e0 + 128 i
     Walk w{ld & 0x7fffu, 0.0, 0.0, true};
-    Chunk& ca = first;  // chunk 0 was loaded during the previous run
-    Chunk cb;
+    // chunks 0 and 1 were loaded during the previous run; each buffer is
+    // refilled with the chunk two ahead as soon as it has been walked
     for (int i = 0; i < iters; i += 2) {
-        if (cnt > i + 1) load_chunk(cb, vb, kb, e0 + 128u * (i + 1), pol);
         if (cnt > i) walk_chunk<MODE>(w, ca, xb_s, yp_s);
-        if (i + 1 >= iters) break;
         if (cnt > i + 2) load_chunk(ca, vb, kb, e0 + 128u * (i + 2), pol);
+        if (i + 1 >= iters) break;
         if (cnt > i + 1) walk_chunk<MODE>(w, cb, xb_s, yp_s);
+        if (cnt > i + 3) load_chunk(cb, vb, kb, e0 + 128u * (i + 3), pol);
     }
-    // the next run's first chunk streams in during this run's lane reduction
-    // and the next slab wait (the matrix does not depend on x)
-    load_first_chunk(first, vb, kb, next_lo, next_hi, lane, pol);
+    // the next run's first two chunks stream in during this run's lane
+    // reduction and the next slab wait (the matrix does not depend on x)
+    load_head_chunks(ca, cb, vb, kb, next_lo, next_hi, lane, pol);
     if (MODE >= 2) {  // probe: no row sums
         if (w.acc == 12345.678) sts_add_f64(yp_s, w.acc);
         return;
@@ -311,11 +315,11 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                 prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
         // lane descriptors and each run's first chunk are loaded one run ahead (registers)
         unsigned dnext = T.nslabs > 0 ? __ldg(lr + warp * 32) : 0u;
-        Chunk first;
+        Chunk ca, cb;
         if (T.nslabs > 0) {
             std::uint64_t pol;
             asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            load_first_chunk(first, vb, kb, wo[warp], wo[warp + 1], lane, pol);
+            load_head_chunks(ca, cb, vb, kb, wo[warp], wo[warp + 1], lane, pol);
         }
         if (tid == 0 && T.nslabs > 0 && MODE < 5) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
@@ -344,7 +348,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             }
             const bool more = k + 1 < T.nslabs;
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
-                vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1], dcur, first,
+                vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1], dcur, ca, cb,
                 more ? wo[(k + 1) * kTileWarps + warp] : 0, more ? wo[(k + 1) * kTileWarps + warp + 1] : 0,
                 c.xs_s + 8u * static_cast<unsigned>(buf * kSlabStride), c.yp_s, lane);
             __syncwarp();
