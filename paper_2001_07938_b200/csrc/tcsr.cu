@@ -440,8 +440,9 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
+        // release: the CTA's writes (ordered before by __syncthreads) become
+        // visible with the arrival; acquire on the poll below
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         unsigned v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
