@@ -39,6 +39,11 @@ __device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
 
+__device__ __forceinline__ std::uint32_t opaque_u32(std::uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+
 __device__ __forceinline__ void mbar_init(std::uint64_t* b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
 }
@@ -279,8 +284,10 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, double* smem, std::uin
     c.yp = smem + 2 * kSlabStride;
     c.mbar = mbar;
     c.released = released;
-    c.xs_s = smem_addr(c.xs);
-    c.yp_s = smem_addr(c.yp);
+    // opaque copies: kept in registers instead of being rebuilt from the
+    // CTA id (S2R) at every use
+    c.xs_s = opaque_u32(smem_addr(c.xs));
+    c.yp_s = opaque_u32(smem_addr(c.yp));
     c.phase0 = c.phase1 = 0;
     if (threadIdx.x == 0) {
         released[0] = released[1] = 0;
