@@ -200,6 +200,7 @@ def main():
         w = torch.empty_like(x)
         A.pagerank(0.85, 2, x.data_ptr(), w.data_ptr(), stream.cuda_stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()  # the warm-up runs on `stream`; reset x only after it
         x.fill_(1.0 / n)
         torch.cuda.synchronize()
         e0.record(stream)
