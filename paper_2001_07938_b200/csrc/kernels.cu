@@ -242,11 +242,14 @@ __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
 // (deterministic) and stores y. Why not merge-path alone: on the Kronecker
 // scale-22 operator it is bound by shared-memory latency (binary searches, the
 // sequential merge walk) at 0.92 ms.
+#ifndef LILAC_SPLIT_MINB
+#define LILAC_SPLIT_MINB 6
+#endif
 constexpr int kChunkU = 8;
 constexpr int kShortPasses = 8;  // short-row unit: 8 passes of the warp's 32/S row groups
 
 template <int S, typename IdxT>
-__global__ void __launch_bounds__(kThreads) k_csr_split(std::int64_t rows, const std::int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kThreads, LILAC_SPLIT_MINB) k_csr_split(std::int64_t rows, const std::int64_t* __restrict__ row_ptr,
                                                         const IdxT* __restrict__ col,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ x, double* __restrict__ y,
