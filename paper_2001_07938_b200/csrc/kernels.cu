@@ -364,11 +364,25 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
 #pragma unroll
             for (int u = 0; u < kJdsU; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
         }
-        for (; k < len; ++k) {
-            const std::int64_t off = __ldg(jd_ptr + k) + j;
-            double v;
-            asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(val + off));
-            acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + static_cast<std::int64_t>(col[off]))));
+        if (k < len) {  // the last < kJdsU diagonals: one masked group, all loads in flight
+            const std::int64_t rem = len - k;
+            double v[kJdsU], xv[kJdsU];
+            long long c[kJdsU];
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) {
+                v[u] = 0.0;
+                c[u] = 0;
+                if (u < rem) {
+                    const std::int64_t off = __ldg(jd_ptr + k + u) + j;
+                    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
+                    c[u] = static_cast<long long>(__ldg(col + off));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) xv[u] = u < rem ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u)
+                if (u < rem) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
         }
         y[__ldg(inv_perm + j)] = acc;
     }
