@@ -15,6 +15,8 @@
 #include "p2p.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 
 namespace b200 {
@@ -190,6 +192,103 @@ __device__ __forceinline__ unsigned group_mask() {
 
 // S lanes cooperate on a row (vector_row). Rows longer than max_len are left
 // to the split plan's chunk path.
+// Rows that fit one U=2 pass of the group (max row + 1 <= 4S: banded and
+// stencil matrices), software-pipelined across the group's rows: the next
+// row's row_ptr and val/col loads are issued before this row's x gathers are
+// consumed, so two rows' streams are in flight per lane.
+struct Pass {
+    double2 v[2];
+    Idx2 c[2];
+};
+
+template <int S, typename IdxT>
+__device__ __forceinline__ void load_pass(Pass& p, std::int64_t start, std::int64_t end, int lane,
+                                          const IdxT* __restrict__ col, const double* __restrict__ val,
+                                          std::uint64_t pol) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const std::int64_t j = (start & ~std::int64_t(1)) + 2 * lane + 2 * S * u;
+        if (j < end) {
+            p.v[u] = ld_stream_ef(val + j, pol);
+            p.c[u] = ld_stream_idx(col + j, pol);
+        } else {
+            p.v[u] = make_double2(0.0, 0.0);
+            p.c[u] = {0, 0};
+        }
+    }
+}
+
+template <int S, typename IdxT, bool DOT>
+__global__ void __launch_bounds__(kThreads) k_csr_vector_1p(std::int64_t rows,
+                                                            const std::int64_t* __restrict__ row_ptr,
+                                                            const IdxT* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ y,
+                                                            double* __restrict__ partials,
+                                                            unsigned int* ticket, CgScalars* sc,
+                                                            std::int64_t dot_off) {
+    const int lane = threadIdx.x & (S - 1);
+    const unsigned gmask = group_mask<S>();
+    const std::int64_t groups = static_cast<std::int64_t>(gridDim.x) * (kThreads / S);
+    const std::uint64_t pol = make_evict_first();
+    double pq = 0.0;
+    std::int64_t row = (static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x) / S;
+    std::int64_t start = 0, end = 0;
+    Pass cur;
+    if (row < rows) {
+        start = __ldg(row_ptr + row);
+        end = __ldg(row_ptr + row + 1);
+        load_pass<S>(cur, start, end, lane, col, val, pol);
+    }
+    for (; row < rows; row += groups) {
+        const std::int64_t nrow = row + groups;
+        std::int64_t nstart = 0, nend = 0;
+        if (nrow < rows) {
+            nstart = __ldg(row_ptr + nrow);
+            nend = __ldg(row_ptr + nrow + 1);
+        }
+        double xa[2], xb[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const std::int64_t j = (start & ~std::int64_t(1)) + 2 * lane + 2 * S * u;
+            xa[u] = (j < end && j >= start) ? __ldg(x + cur.c[u].a) : 0.0;
+            xb[u] = (j + 1 < end) ? __ldg(x + cur.c[u].b) : 0.0;
+        }
+        Pass nxt;
+        if (nrow < rows) load_pass<S>(nxt, nstart, nend, lane, col, val, pol);
+        double acc = 0.0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            acc += cur.v[u].x * xa[u];
+            acc += cur.v[u].y * xb[u];
+        }
+#pragma unroll
+        for (int o = S / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
+        if (lane == 0) {
+            y[row] = acc;
+            if (DOT) pq += acc * __ldg(x + dot_off + row);
+        }
+        cur = nxt;
+        start = nstart;
+        end = nend;
+    }
+    if (DOT) {
+        double s = block_sum(pq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+        double total;
+        if (last_cta_sum(partials, ticket, &total) && threadIdx.x == 0) {
+            if (sc->nranks > 1) {
+                p2p_publish(sc, &total, 1);
+            } else {
+                sc->d = total;
+                sc->rho0 = sc->rho;
+                sc->alpha = sc->rho / total;
+            }
+        }
+    }
+}
+
 template <int S, int U, typename IdxT, bool DOT>
 __global__ void __launch_bounds__(kThreads) k_csr_vector(std::int64_t rows,
                                                          const std::int64_t* __restrict__ row_ptr,
@@ -567,6 +666,22 @@ unsigned grid_for(std::int64_t threads, unsigned cap = kSMs * 16) {
 template <int S, typename IdxT, bool DOT>
 void vector_launch(const CsrDev& A, const double* x, double* y, double* partials, unsigned* ticket,
                    CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off, std::int64_t max_len) {
+    static const int onepass = [] {  // LILAC_B200_VEC_1P: 0 off, 1 whenever rows fit, else by size
+        const char* e = std::getenv("LILAC_B200_VEC_1P");
+        return (e && *e) ? std::atoi(e) : 2;
+    }();
+    // measured on the 27-point stencil: the plain kernel (2048 threads per SM)
+    // wins while the matrix is small (N=256, 3.6e8 nonzeros: 0.73 vs 0.67 of
+    // copy) and degrades as the footprint grows (TLB reach: N=420, 2.0e9
+    // nonzeros: 0.625); the pipelined one (1024 threads, two rows in flight)
+    // holds 0.68 at every size; the crossover is near 8 GB of matrix
+    const std::int64_t mbytes = A.nnz * (A.col32 ? 12 : 16);
+    if (onepass && A.max_row + 1 <= 4 * S && max_len >= A.max_row &&
+        (onepass == 1 || mbytes > (std::int64_t(8) << 30))) {
+        k_csr_vector_1p<S, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
+                                                                A.val, x, y, partials, ticket, sc, dot_off);
+        return;
+    }
     k_csr_vector<S, 2, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
                                                             A.val, x, y, partials, ticket, sc, dot_off, max_len);
 }

@@ -247,6 +247,19 @@ def test_fused_cg_matches_per_step_kernels():
     assert np.abs(z_t - z_v).max() <= 1e-9 * np.abs(z_v).max()
 
 
+def test_vector_one_pass_kernel_forced():
+    """The pipelined one-pass vector kernel is chosen only for matrices over
+    8 GB; tools/vec1p_check.py forces it (LILAC_B200_VEC_1P=1, read once per
+    process, hence the subprocess) on small banded/stencil matrices."""
+    import subprocess
+    import sys
+    import os
+    env = dict(os.environ, LILAC_B200_VEC_1P="1")
+    r = subprocess.run([sys.executable, os.path.join(O.ROOT, "tools", "vec1p_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "vec1p ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_edge_cases():
     # rows = 0
     y = np.zeros(0)
