@@ -108,11 +108,21 @@ constexpr std::uint16_t kLaneCont = 1u << 15;
 // padding entry: value 0 times the zero cell (never an Inf or NaN of x)
 constexpr std::uint16_t kPadKey = static_cast<std::uint16_t>(kSlabW);
 static_assert(kSlabW <= static_cast<int>(kKeyColMask), "slab columns and the zero cell must fit the key");
+// The builder widens the slab to what shared memory leaves after the tile's
+// y buffer: 2 (slab_w + 2) + rows_max doubles within kTileSmemBudget (NPB
+// class C: tiles of <= 1030 rows -> 13,946-column slabs, 11 instead of 13).
+constexpr int kTileSmemBudget = 227 * 1024 - 1024;  // dynamic smem, 1 KB left for static
+constexpr int kSlabWMax = kKeyColMask - 1;           // the zero cell (column slab_w) must fit the key
+inline std::size_t tcsr_smem_bytes(int slab_w, int rows_max) {
+    return sizeof(double) * (2 * static_cast<std::size_t>(slab_w + 2) + static_cast<std::size_t>(rows_max));
+}
 
 struct TcsrDev {
     std::int64_t ntiles = 0;
     int nslabs = 0;
     std::int64_t cols = 0;
+    int slab_w = kSlabW;                      // columns per slab (even)
+    int rows_max = kMaxTileRows;              // tallest tile (y buffer rows)
     const std::int64_t* tile_row0 = nullptr;  // ntiles + 1 row bounds
     const std::int64_t* tile_base = nullptr;  // ntiles + 1 element offsets
     const std::int32_t* woff = nullptr;       // ntiles x (nslabs*kTileWarps + 1): run element offsets, tile-relative

@@ -33,7 +33,8 @@ constexpr unsigned kFull = 0xffffffffu;
 #define LILAC_PF_AHEAD 1
 #endif
 constexpr int kPfAhead = LILAC_PF_AHEAD;
-constexpr std::size_t kTileSmem = sizeof(double) * (2 * kSlabStride + kMaxTileRows);
+// dynamic shared memory of a tiled launch: the matrix's slabs + y buffer
+inline std::size_t tile_smem(const TcsrDev& T) { return tcsr_smem_bytes(T.slab_w, T.rows_max); }
 
 __device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -101,8 +102,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ int slab_len(const TcsrDev& T, int k) {
-    const long long rem = static_cast<long long>(T.cols - static_cast<std::int64_t>(k) * kSlabW);
-    return static_cast<int>(rem < kSlabW ? rem : kSlabW);
+    const long long rem = static_cast<long long>(T.cols - static_cast<std::int64_t>(k) * T.slab_w);
+    return static_cast<int>(rem < T.slab_w ? rem : T.slab_w);
 }
 
 // Start the copy of slab k of x into `xs` through the bulk-copy engine
@@ -113,7 +114,7 @@ __device__ __forceinline__ void issue_slab(const TcsrDev& T, const double* __res
                                            std::uint64_t* mbar) {
     const int len = slab_len(T, k);
     const int even = len & ~1;
-    const double* src = x + static_cast<std::int64_t>(k) * kSlabW;
+    const double* src = x + static_cast<std::int64_t>(k) * T.slab_w;
     if (len & 1) xs[even] = __ldcg(src + even);  // L2: x may have been written earlier in this kernel
     mbar_arrive_tx(mbar, static_cast<unsigned>(even) * 8u);
     if (even) bulk_g2s(xs, src, static_cast<unsigned>(even) * 8u, mbar);
@@ -271,17 +272,20 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
 // Shared-memory state of a tiled SpMV CTA (slab double buffer, row sums,
 // mbarriers), carried across tiles and, in the fused CG kernel, across steps.
 struct TileCta {
-    double* xs;  // [2][kSlabStride]: slab + zero cell
-    double* yp;  // [kMaxTileRows]
+    double* xs;  // [2][stride]: slab + zero cell (stride = slab_w + 2)
+    double* yp;  // [rows_max]
+    int stride;
     std::uint64_t* mbar;
     unsigned* released;
     std::uint32_t xs_s, yp_s;
     unsigned phase0, phase1;
 };
 
-__device__ __forceinline__ void tile_cta_init(TileCta& c, double* smem, std::uint64_t* mbar, unsigned* released) {
+__device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, double* smem, std::uint64_t* mbar,
+                                              unsigned* released) {
+    c.stride = T.slab_w + 2;
     c.xs = smem;
-    c.yp = smem + 2 * kSlabStride;
+    c.yp = smem + 2 * c.stride;
     c.mbar = mbar;
     c.released = released;
     // opaque copies: kept in registers instead of being rebuilt from the
@@ -291,7 +295,7 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, double* smem, std::uin
     c.phase0 = c.phase1 = 0;
     if (threadIdx.x == 0) {
         released[0] = released[1] = 0;
-        c.xs[kSlabW] = c.xs[kSlabStride + kSlabW] = 0.0;  // padding entries read these
+        c.xs[T.slab_w] = c.xs[c.stride + T.slab_w] = 0.0;  // padding entries read these
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -331,7 +335,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         if (tid == 0 && T.nslabs > 0 && MODE < 5) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
             issue_slab(T, x, xs, 0, &c.mbar[0]);
-            if (T.nslabs > 1) issue_slab(T, x, xs + kSlabStride, 1, &c.mbar[1]);
+            if (T.nslabs > 1) issue_slab(T, x, xs + c.stride, 1, &c.mbar[1]);
         }
         __syncthreads();
         // Free-running slabs: a warp moves on as soon as the next slab has
@@ -357,7 +361,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
                 vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1], dcur, ca, cb,
                 more ? wo[(k + 1) * kTileWarps + warp] : 0, more ? wo[(k + 1) * kTileWarps + warp + 1] : 0,
-                c.xs_s + 8u * static_cast<unsigned>(buf * kSlabStride), c.yp_s, lane);
+                c.xs_s + 8u * static_cast<unsigned>(buf * c.stride), c.yp_s, lane);
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
@@ -365,7 +369,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                     c.released[buf] = 0;
                     if (k + 2 < T.nslabs && MODE < 5) {
                         if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");
-                        issue_slab(T, x, xs + buf * kSlabStride, k + 2, &c.mbar[buf]);
+                        issue_slab(T, x, xs + buf * c.stride, k + 2, &c.mbar[buf]);
                     }
                 }
             }
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     __shared__ unsigned released[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     TileCta c;
-    tile_cta_init(c, smem, mbar, released);
+    tile_cta_init(c, T, smem, mbar, released);
     if (DOT) {  // CG step: launched programmatically after update_p
         pdl_trigger();
         if (lane == 0 && blockIdx.x < T.ntiles && T.nslabs > 0) {  // the matrix does not depend on it
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     __shared__ double red[kTileWarps + 1];
     const int tid = threadIdx.x;
     TileCta c;
-    tile_cta_init(c, smem, mbar, released);
+    tile_cta_init(c, T, smem, mbar, released);
     __syncthreads();
     unsigned target = 0;
     unsigned* bar = &v.sc->bar;
@@ -555,16 +559,16 @@ void launch_variant(const TcsrDev& T, const double* x, double* y, double* partia
     static bool configured = false;
     if (!configured) {
         B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kTileSmem)));
+                                       kTileSmemBudget));
         B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kTileSmem)));
+                                       kTileSmemBudget));
         configured = true;
     }
     if (partials)
         launch_pdl(k_spmv_tiled<true, MODE>, dim3(std::min<unsigned>(grid, kMaxParts)), dim3(kTileThreads),
-                   kTileSmem, s, T, x, y, partials, ticket, sc, dot_off);
+                   tile_smem(T), s, T, x, y, partials, ticket, sc, dot_off);
     else
-        k_spmv_tiled<false, MODE><<<grid, kTileThreads, kTileSmem, s>>>(T, x, y, nullptr, nullptr, nullptr, 0);
+        k_spmv_tiled<false, MODE><<<grid, kTileThreads, tile_smem(T), s>>>(T, x, y, nullptr, nullptr, nullptr, 0);
 }
 
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
@@ -599,9 +603,8 @@ bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream
         B200_CUDA(cudaGetDevice(&dev));
         B200_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
         B200_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        B200_CUDA(cudaFuncSetAttribute(k_cg_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kTileSmem)));
-        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tiled, kTileThreads, kTileSmem));
+        B200_CUDA(cudaFuncSetAttribute(k_cg_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBudget));
+        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tiled, kTileThreads, kTileSmemBudget));
         max_grid = coop ? per_sm * sms : 0;
         if (max_grid <= 0) enabled = 0;
     }
@@ -611,7 +614,7 @@ bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kTileThreads);
-    cfg.dynamicSmemBytes = kTileSmem;
+    cfg.dynamicSmemBytes = tile_smem(T);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;

@@ -11,6 +11,7 @@ namespace b200 {
 struct TcsrHost {
     std::int64_t ntiles = 0;
     int nslabs = 0;
+    int slab_w = kSlabW, rows_max = kMaxTileRows;
     std::int64_t cols = 0;
     std::vector<std::int64_t> tile_row0, tile_base;
     std::vector<std::int32_t> woff;

@@ -63,14 +63,14 @@ struct TileRuns {
 // row left empty between two rows of a run gets a one-entry segment whose
 // nonzero index is -1 (a zero entry), so a run's rows are consecutive.
 void tile_runs(const std::int64_t* rp, const std::int64_t* ci, std::int64_t row0, const std::int64_t* wb,
-               int nslabs, TileRuns& tr) {
+               int nslabs, int slab_w, TileRuns& tr) {
     const std::int64_t runs = static_cast<std::int64_t>(nslabs) * kTileWarps;
     std::vector<std::int32_t> nnz_run(static_cast<std::size_t>(runs + 1), 0), seg_run(static_cast<std::size_t>(runs + 1), 0);
     std::vector<std::int64_t> last(static_cast<std::size_t>(runs), -1);
     for (int w = 0; w < kTileWarps; ++w)
         for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
             for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
-                const std::int64_t run = (ci[j] / kSlabW) * kTileWarps + w;
+                const std::int64_t run = (ci[j] / slab_w) * kTileWarps + w;
                 ++nnz_run[run + 1];
                 if (last[run] != r) {
                     if (last[run] >= 0) {  // empty rows in between
@@ -95,7 +95,7 @@ void tile_runs(const std::int64_t* rp, const std::int64_t* ci, std::int64_t row0
     for (int w = 0; w < kTileWarps; ++w)
         for (std::int64_t r = wb[w]; r < wb[w + 1]; ++r)
             for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
-                const std::int64_t run = (ci[j] / kSlabW) * kTileWarps + w;
+                const std::int64_t run = (ci[j] / slab_w) * kTileWarps + w;
                 if (last[run] != r) {
                     if (last[run] >= 0)
                         for (std::int64_t e = last[run] + 1; e < r; ++e) {
@@ -124,7 +124,8 @@ std::int64_t run_elems(const TileRuns& tr, std::int64_t run) {
 // half-warp (LILAC_B200_TILED_BANKS=0: CSR order). Row-start bits stay with
 // their positions.
 void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, const double* val, std::int64_t jb,
-               std::int64_t slab, bool balance, double* hv, std::uint16_t* hk, std::uint16_t* hl) {
+               std::int64_t slab, int slab_w, bool balance, double* hv, std::uint16_t* hk, std::uint16_t* hl) {
+    const std::uint16_t pad = static_cast<std::uint16_t>(slab_w);  // the zero cell
     const std::int64_t js0 = tr.run_js[run], E = tr.run_js[run + 1] - js0;
     const std::int64_t C = (E + kChunk - 1) / kChunk, m = C / 32, r = C % 32;
     // the run's nonzeros in order, with their rows
@@ -132,9 +133,9 @@ void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, con
     for (std::int32_t i = tr.run_seg[run]; i < tr.run_seg[run + 1]; ++i)
         for (std::int32_t q = 0; q < tr.segs[i].count; ++q) rowof[tr.segs[i].start - js0 + q] = tr.segs[i].row;
     auto elem = [&](std::int64_t e) {
-        if (tr.js[js0 + e] < 0) return std::make_pair(kPadKey, 0.0);  // empty row
+        if (tr.js[js0 + e] < 0) return std::make_pair(pad, 0.0);  // empty row
         const std::int64_t j = jb + tr.js[js0 + e];
-        return std::make_pair(static_cast<std::uint16_t>(ci[j] - slab * kSlabW), val[j]);
+        return std::make_pair(static_cast<std::uint16_t>(ci[j] - slab * slab_w), val[j]);
     };
     std::int64_t cs[32], cn[32];
     for (int l = 0; l < 32; ++l) {
@@ -155,7 +156,7 @@ void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, con
                 if (i >= cn[l]) continue;
                 const std::int64_t e = (cs[l] + i) * kChunk + sl, at = (i * 32 + l) * kChunk + sl;
                 if (e >= E) {
-                    hk[at] = kPadKey;
+                    hk[at] = pad;
                     hv[at] = 0.0;
                     continue;
                 }
@@ -229,7 +230,6 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     const std::int64_t nnz = rp[rows] - base0;
     const int sms = device_sms();
     h.cols = cols;
-    h.nslabs = static_cast<int>((cols + kSlabW - 1) / kSlabW);
     // tiles: nnz-balanced, a multiple of the SM count, none taller than kMaxTileRows
     std::vector<std::int64_t> bounds;
     const char* tps = std::getenv("LILAC_B200_TILES_PER_SM");
@@ -251,6 +251,14 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     }
     h.tile_row0.push_back(rows);
     h.ntiles = static_cast<std::int64_t>(h.tile_row0.size()) - 1;
+    // slab width: what shared memory leaves after the tallest tile's y buffer
+    h.rows_max = 1;
+    for (std::int64_t t = 0; t < h.ntiles; ++t)
+        h.rows_max = static_cast<int>(std::max<std::int64_t>(h.rows_max, h.tile_row0[t + 1] - h.tile_row0[t]));
+    h.slab_w = std::min(kSlabWMax, ((kTileSmemBudget / 8 - h.rows_max) / 2 - 2)) & ~7;
+    if (const char* e = std::getenv("LILAC_B200_SLAB_W"))  // experiments: a narrower slab
+        if (std::atoi(e) >= 1024) h.slab_w = std::min(h.slab_w, std::atoi(e) & ~7);
+    h.nslabs = static_cast<int>((cols + h.slab_w - 1) / h.slab_w);
     const std::int64_t per_tile = static_cast<std::int64_t>(h.nslabs) * kTileWarps + 1;
     h.woff.assign(static_cast<std::size_t>(h.ntiles * per_tile), 0);
     h.lrow.assign(static_cast<std::size_t>(h.ntiles * (per_tile - 1) * 32), 0);
@@ -269,7 +277,7 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
         }
         wb[kTileWarps] = row1;
         TileRuns tr;
-        tile_runs(rp, ci, row0, wb, h.nslabs, tr);
+        tile_runs(rp, ci, row0, wb, h.nslabs, h.slab_w, tr);
         for (std::int64_t i = 0; i + 1 < per_tile; ++i) relems[t * (per_tile - 1) + i] = run_elems(tr, i);
     });
     // element offsets, tile-relative per run
@@ -287,7 +295,7 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     }
     const std::int64_t total = h.tile_base[h.ntiles];
     h.val.assign(static_cast<std::size_t>(total), 0.0);
-    h.key.assign(static_cast<std::size_t>(total), kPadKey);
+    h.key.assign(static_cast<std::size_t>(total), static_cast<std::uint16_t>(h.slab_w));
 
     // pass 2: the runs
     const bool balance = [] {
@@ -300,9 +308,9 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
         const std::int64_t* wb = wbounds.data() + t * (kTileWarps + 1);
         const std::int32_t* wo = h.woff.data() + t * per_tile;
         TileRuns tr;
-        tile_runs(rp, ci, row0, wb, h.nslabs, tr);
+        tile_runs(rp, ci, row0, wb, h.nslabs, h.slab_w, tr);
         for (std::int64_t i = 0; i + 1 < per_tile; ++i)
-            write_run(tr, i, ci, val, rp[row0], i / kTileWarps, balance, h.val.data() + tb + wo[i],
+            write_run(tr, i, ci, val, rp[row0], i / kTileWarps, h.slab_w, balance, h.val.data() + tb + wo[i],
                       h.key.data() + tb + wo[i], h.lrow.data() + (t * (per_tile - 1) + i) * 32);
     });
 }
@@ -328,6 +336,8 @@ void TcsrOwner::upload(const TcsrHost& h) {
     B200_CUDA(cudaStreamSynchronize(s));
     dev.ntiles = h.ntiles;
     dev.nslabs = h.nslabs;
+    dev.slab_w = h.slab_w;
+    dev.rows_max = h.rows_max;
     dev.cols = h.cols;
     dev.tile_row0 = tile_row0.as<std::int64_t>();
     dev.tile_base = tile_base.as<std::int64_t>();
