@@ -189,9 +189,11 @@ __global__ void k_cg_fill(double* x, std::int64_t n, double val) {
 // Two elements per thread: the CG vectors are L2-resident between steps, so
 // these kernels are latency-bound — all of a thread's loads should be in
 // flight at once rather than walked in a grid-stride loop.
+// Large vectors (the stencil's 74M rows): one full wave of 8 CTAs per SM
+// walking grid-stride (2048 CTAs were 1.7 waves, the second 73% full).
 unsigned vec_grid(const CgVectors& v) {
     std::int64_t g = (v.n + kThreads * 2 - 1) / (kThreads * 2);
-    return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, std::min(kMaxParts, 148 * 16))));
+    return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, 148 * 8)));
 }
 
 }  // namespace
