@@ -305,9 +305,13 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, doub
 // y = A x over this CTA's tiles; with DOT, returns this thread's share of
 // x.y over the tiles' rows (x read at dot_off + row). COHERENT: x may have been
 // written earlier in the same kernel (fused CG): read it through L2 only.
+// gate (fused CG): a grid barrier this CTA already arrived at; thread 0 waits
+// for it only before the first slab copy of x, so the tile prologue (y
+// buffer, L2 prefetch, descriptors, head chunks: nothing that depends on x)
+// overlaps the barrier.
 template <bool DOT, int MODE, bool COHERENT>
 __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, double* y, std::int64_t dot_off,
-                                             TileCta& c) {
+                                             TileCta& c, const unsigned* gate = nullptr, unsigned gate_target = 0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* xs = c.xs;
     double* yp = c.yp;
@@ -331,6 +335,13 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             std::uint64_t pol;
             asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             load_head_chunks(ca, cb, vb, kb, wo[warp], wo[warp + 1], lane, pol);
+        }
+        if (tid == 0 && gate) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
+            } while (v < gate_target);
+            gate = nullptr;
         }
         if (tid == 0 && T.nslabs > 0 && MODE < 5) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
@@ -462,6 +473,13 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
     __syncthreads();
 }
 
+// Arrival only (the wait is the gate of the next spmv_tiles).
+__device__ __forceinline__ void grid_arrive(unsigned* bar, unsigned& target) {
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+
 // Sum of every thread's v, returned to all threads (fixed tree).
 __device__ __forceinline__ double cta_sum(double v, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -507,7 +525,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     double* pq_part = v.partials;
     double* rr_part = v.partials + 2 * kMaxParts;
     for (int it = 0; it < steps; ++it) {
-        const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c), red);
+        const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c, it > 0 ? bar : nullptr, target),
+                                  red);
         if (tid == 0) pq_part[blockIdx.x] = pq;
         grid_sync(bar, target);
         const double d = cta_sum_parts(pq_part, gridDim.x, red);
@@ -545,7 +564,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
             v.sc->beta = beta;
         }
         rho = rho_new;
-        grid_sync(bar, target);
+        grid_arrive(bar, target);  // p complete before any CTA's slabs read it: waited on in spmv_tiles
     }
 }
 
