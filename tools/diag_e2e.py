@@ -33,7 +33,7 @@ def mc():
 
 m0 = mc()
 t0 = time.perf_counter()
-bench.e2e_harness_cg(rp, ci, val, na, shift, 1, mode)  # warm (matrix upload)
+bench.e2e_harness_cg(rp, ci, val, na, shift, int(os.environ.get("DIAG_WARM", "1")), mode)  # warm (matrix upload)
 N.lib().b200_stats_reset()
 m0 = mc()
 r = bench.e2e_harness_cg(rp, ci, val, na, shift, 3, mode)
