@@ -574,6 +574,7 @@ def run_ours(args):
                    "shard_rows_rank0": list(shard_rows),
                    "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % (spmv_bytes / 1e9),
                    "zeta": zeta, "zeta_verified": verified, "rnorm": rnorm},
+        "cg_iters_per_s": value * CGITMAX,  # CG iterations/s beside NPB outer iterations/s
         "spmv": {"gflops": spmv_flops / (spmv_ms * 1e-3) / 1e9, "gbs": achieved,
                  "frac_of_measured_copy": achieved / peak, "frac_of_nominal_8TBs": achieved / 8000.0,
                  "ms": spmv_ms, "lanes_per_row": info["lanes"], "bytes_per_call": spmv_bytes},
