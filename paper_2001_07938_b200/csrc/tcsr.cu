@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         if (lane == 0) red[warp] = s;
         __syncthreads();
         if (warp == 0) {
-            s = warp_sum(red[lane]);
+            s = warp_sum(lane < kTileWarps ? red[lane] : 0.0);
             if (lane == 0) partials[blockIdx.x] = s;
         }
         __threadfence();
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             if (lane == 0) red[warp] = a;
             __syncthreads();
             if (warp == 0) {
-                a = warp_sum(red[lane]);
+                a = warp_sum(lane < kTileWarps ? red[lane] : 0.0);
                 if (lane == 0) {
                     if (sc->nranks > 1) {
                         p2p_publish(sc, &a, 1);  // the shard's partial; alpha after the exchange
@@ -488,7 +488,7 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
     if (lane == 0) red[warp] = v;
     __syncthreads();
     if (warp == 0) {
-        v = warp_sum(red[lane]);
+        v = warp_sum(lane < kTileWarps ? red[lane] : 0.0);
         if (lane == 0) red[kTileWarps] = v;
     }
     __syncthreads();
