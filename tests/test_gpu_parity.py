@@ -215,6 +215,25 @@ def test_tiled_layout_edge_cases():
     assert_within(y[fin], y_ref[fin], spmv_bound(rp, ci, val, np.where(np.isfinite(x), x, 0.0))[fin])
 
 
+def test_fused_cg_is_deterministic_run_to_run():
+    """The fused CG kernel's dots use a fixed per-CTA partition summed in CTA
+    order, and the tiled SpMV's row sums a fixed layout order: two runs give
+    the same bits."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES["A"]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    N.lib().b200_set_kernel(b"tiled")
+    A = D.Matrix.csr(rp, ci, val)
+    assert A.info()["kernel"] == 4
+    got = []
+    for _ in range(2):
+        cg = D.CG(A)
+        got.append(cg.npb(niter, shift))
+        cg.free()
+    A.free()
+    assert got[0] == got[1], got
+    assert abs(got[0][0] - zeta_ref) / zeta_ref <= 1e-10
+
+
 def test_fused_cg_matches_per_step_kernels():
     """CG on one GPU with the tiled layout runs its steps in one persistent
     cooperative kernel (k_cg_tiled) — here with more tiles than SMs; the vector
