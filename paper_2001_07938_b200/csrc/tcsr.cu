@@ -173,6 +173,10 @@ struct Walk {
     bool in_head;
 };
 
+// MODE: 0 = the kernel. Timing probes (LILAC_B200_TILED_PROBE, wrong results,
+// never on the CG path; tools/tiled_probes.sh): 1 no x gathers, 2 no row
+// sums, 3 neither (loads only), 5 = 3 without slab copies/waits, 6 = 0
+// without slab copies/waits.
 template <int MODE>
 __device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::uint32_t xb_s, std::uint32_t yp_s) {
     const double p = (MODE == 1 || MODE == 3) ? v : v * lds_f64(xb_s + 8u * (key & kKeyColMask));
