@@ -254,6 +254,7 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
     const int cnt = m + (lane < r ? 1 : 0), iters = m + (r > 0 ? 1 : 0);
     const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);  // chunk i at e0 + 128 i
     Walk w{ld & 0x7fffu, 0.0, 0.0, true};
+    xb_s = opaque_u32(xb_s);  // one base register: a gather address is one LEA
     // chunks 0 and 1 were loaded during the previous run; each buffer is
     // refilled with the chunk two ahead as soon as it has been walked
     for (int i = 0; i < iters; i += 2) {
