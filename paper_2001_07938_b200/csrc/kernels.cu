@@ -218,8 +218,10 @@ __device__ __forceinline__ void load_pass(Pass& p, std::int64_t start, std::int6
     }
 }
 
+// Launch bounds for 5 CTAs per SM (48 registers, a 16-byte spill): 5.80 ->
+// 5.37 ms on the N=420 stencil; at 6 (40 registers) the spills cost 7.1 ms.
 template <int S, typename IdxT, bool DOT>
-__global__ void __launch_bounds__(kThreads) k_csr_vector_1p(std::int64_t rows,
+__global__ void __launch_bounds__(kThreads, 5) k_csr_vector_1p(std::int64_t rows,
                                                             const std::int64_t* __restrict__ row_ptr,
                                                             const IdxT* __restrict__ col,
                                                             const double* __restrict__ val,
