@@ -81,6 +81,19 @@ def cpu_desc():
     return model, os.cpu_count()
 
 
+def cpu_sockets():
+    """Distinct physical packages in /proc/cpuinfo (report sockets)."""
+    ids = set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("physical id"):
+                    ids.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return len(ids) or None
+
+
 # ------------------------------------------------------------------------------------
 # clocks during the timed region (B200_PROFILING.md clocks line)
 # ------------------------------------------------------------------------------------
@@ -605,7 +618,7 @@ def run_ours(args):
             t_iter, kind, desc, ts, threads = reference_sample(rp, ci, val, na, reps=2)
             model, ncpu = cpu_desc()
             line["cpu_baseline"] = {"value": 1.0 / t_iter, "unit": UNIT, "cores": threads, "kind": kind,
-                                    "sample": desc, "cpu": model, "host_cpus": ncpu,
+                                    "sample": desc, "cpu": model, "host_cpus": ncpu, "sockets": cpu_sockets(),
                                     "spmv_s": ts}
     elif world > 1:
         line["e2e"] = e2e_dist(cg, shard_rows, shift, args.e2e_steps * 10, stream, world)
