@@ -291,7 +291,7 @@ def run_reference(args):
         "config": {"workload": f"NPB CG class {args.npb_class} (n={na}, nnz={int(rp[-1])}) SpMV harness path",
                    "sample": desc},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc,
-                         "cpu": model, "host_cpus": ncpu},
+                         "cpu": model, "host_cpus": ncpu, "sockets": cpu_sockets()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
