@@ -74,6 +74,9 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(ptr); }
 };
 void pool_trim();  // return every cached block to CUDA
+// Wait for all work on the current device (errors ignored: teardown paths)
+// before buffers that caller streams may still use go back to the pool.
+void device_quiesce();
 
 // ---------------------------------------------------------------------------
 // Resident sparse matrices (device layout)

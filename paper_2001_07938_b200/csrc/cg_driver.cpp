@@ -96,6 +96,7 @@ int b200_cg_create(b200_cg** out, const b200_matrix* Am) {
 
 void b200_cg_free(b200_cg* cg) {
     if (!cg) return;
+    device_quiesce();  // caller-stream work may still use the buffers (see b200_matrix_free)
     if (cg->graph) cudaGraphExecDestroy(cg->graph);
     for (DevBuf* b : {&cg->x, &cg->z, &cg->p, &cg->q, &cg->r, &cg->partials, &cg->scalars}) b->release();
     delete cg;

@@ -139,6 +139,11 @@ int b200_matrix_create_jds(b200_matrix** out, std::int64_t rows, const std::int6
 
 void b200_matrix_free(b200_matrix* A) {
     if (!A) return;
+    // Kernels launched on caller streams (the NULL stream included, which does
+    // not order against the library's non-blocking stream) may still read these
+    // buffers; the caching pool hands blocks out again on rt().stream, so wait
+    // for the device before recycling them.
+    device_quiesce();
     A->row_ptr.release();
     A->col.release();
     A->val.release();
@@ -271,7 +276,12 @@ int b200_dbuf_upload(B200Buf* b, const void* host, std::size_t bytes) {
 
 int b200_dbuf_download(void* host, const B200Buf* b, std::size_t bytes) {
     return boundary("b200_dbuf_download", [&] {
-        lilac::marshal::note_host_write(host, bytes);  // guards + lazy bytes under the destination
+        // A DMA write into caller memory: any lazy write-back range under the
+        // destination is superseded (its device bytes must never be filled over
+        // the new ones), device mirrors of it are stale, and guards are dirtied.
+        lilac::marshal::supersede_range(host, bytes);
+        mirrors_forget(host, bytes);
+        lilac::marshal::note_host_write(host, bytes);
         if (bytes) B200_CUDA(cudaMemcpy(host, b->ptr, bytes, cudaMemcpyDeviceToHost));
     });
 }

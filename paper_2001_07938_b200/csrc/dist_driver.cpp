@@ -304,6 +304,7 @@ int b200_dist_cg_create_nccl(b200_dist_cg** out, int rank, int world, const void
 
 void b200_dist_cg_free(b200_dist_cg* d) {
     if (!d) return;
+    device_quiesce();  // caller-stream work may still use the buffers (see b200_matrix_free)
     if (d->graph) cudaGraphExecDestroy(d->graph);
     for (auto& s : d->shards) s->release();
     delete d;

@@ -623,9 +623,13 @@ __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ a, 
     const std::int64_t per = (n + gridDim.x - 1) / gridDim.x;
     const std::int64_t lo = min(n, per * blockIdx.x), hi = min(n, lo + per);
     double s = 0.0;
-    // vector part: pairs aligned to the allocation (a, b are 256-byte aligned)
-    std::int64_t vlo = (lo + 1) & ~std::int64_t(1), vhi = hi & ~std::int64_t(1);
-    if (vlo > vhi) vlo = vhi = lo;
+    // vector part: 16-byte pairs. a and b may be any 8-byte-aligned views
+    // (a sub-range of a mirror, a torch slice): pair boundaries follow a's
+    // address parity, and when b's parity differs the slice is walked scalar.
+    const unsigned pa = static_cast<unsigned>(reinterpret_cast<std::uintptr_t>(a) >> 3) & 1u;
+    const unsigned pb = static_cast<unsigned>(reinterpret_cast<std::uintptr_t>(b) >> 3) & 1u;
+    std::int64_t vlo = lo + ((lo + pa) & 1), vhi = hi - ((hi + pa) & 1);
+    if (pa != pb || vlo > vhi) vlo = vhi = lo;
     for (std::int64_t i = lo + threadIdx.x; i < vlo; i += kThreads) s += a[i] * b[i];
     for (std::int64_t i = vlo + 2 * threadIdx.x; i < vhi; i += 2 * kThreads) {
         const double2 x = ld_stream(a + i), y = ld_stream(b + i);

@@ -10,6 +10,7 @@
 #include "lilac/marshal.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include <sys/mman.h>
 #include <fcntl.h>
 #include <unistd.h>
+#include <sys/syscall.h>
 
 namespace lilac::marshal {
 inline namespace b200 {
@@ -147,7 +149,35 @@ bool page_deferred(std::uintptr_t page) {
     return false;
 }
 
+// Faults from several threads (a host loop plus worker threads reading
+// caller arrays) are handled one at a time: the guard walk and a lazy fill are
+// not re-entrant. The owner's tid makes a nested fault on the same thread (a
+// fill that itself touches a protected page) proceed instead of deadlocking.
+// A thread that waited may find its page already filled; it then takes the
+// guard path, which can only over-report a write (dirty), never miss one.
+std::atomic<long> g_fault_owner{0};
+
+struct FaultLock {
+    bool held = false;
+    FaultLock() {
+        const long me = static_cast<long>(syscall(SYS_gettid));
+        if (g_fault_owner.load(std::memory_order_acquire) == me) return;  // nested
+        long expect = 0;
+        while (!g_fault_owner.compare_exchange_weak(expect, me, std::memory_order_acq_rel)) {
+            expect = 0;
+            __builtin_ia32_pause();
+        }
+        held = true;
+    }
+    void release() {
+        if (held) g_fault_owner.store(0, std::memory_order_release);
+        held = false;
+    }
+    ~FaultLock() { release(); }
+};
+
 void on_fault(int sig, siginfo_t* si, void* uctx) {
+    FaultLock lock;
     const auto addr = reinterpret_cast<std::uintptr_t>(si->si_addr);
     trace("fault", addr, static_cast<std::uintptr_t>(si->si_code));
     const std::uintptr_t page = addr & ~(static_cast<std::uintptr_t>(g_page) - 1);
@@ -197,6 +227,7 @@ void on_fault(int sig, siginfo_t* si, void* uctx) {
     }
 not_ours:
     trace("not ours", addr, static_cast<std::uintptr_t>(g_guards.size()));
+    lock.release();  // the previous handler may not return here
     // Not ours: hand the fault to whoever had SIGSEGV before us.
     if (g_prev_valid) {
         if (g_prev.sa_flags & SA_SIGINFO) {

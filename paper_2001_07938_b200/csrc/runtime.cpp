@@ -145,6 +145,10 @@ void DevBuf::release() {
     bytes = cap = 0;
 }
 
+void device_quiesce() {
+    if (rt().inited) (void)cudaDeviceSynchronize();
+}
+
 void pool_trim() {
     for (const PoolBlock& b : g_pool) cudaFree(b.ptr);
     g_pool.clear();

@@ -606,6 +606,20 @@ void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, dou
         mode = (m && *m) ? std::atoi(m) : 0;
     }
     if (rows <= 0 || T.ntiles <= 0) return;
+    // The x slabs move by cp.async.bulk, which needs a 16-byte-aligned source.
+    // A caller's x may be any 8-byte-aligned view (a torch slice, a sub-range
+    // of a device mirror): stage it once into an aligned scratch vector on the
+    // same stream (8*cols extra bytes, only in that case).
+    if (reinterpret_cast<std::uintptr_t>(x) & 15u) {
+        static DevBuf xalign;  // one per process; calls are stream-ordered per caller
+        const std::size_t xb = static_cast<std::size_t>(T.cols) * sizeof(double);
+        if (xalign.bytes < xb) {
+            B200_CUDA(cudaStreamSynchronize(s));
+            xalign.ensure(xb, false);
+        }
+        B200_CUDA(cudaMemcpyAsync(xalign.ptr, x, xb, cudaMemcpyDeviceToDevice, s));
+        x = xalign.as<const double>();
+    }
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(T.ntiles, g_sms));
     switch (partials ? 0 : mode) {  // probes never on the fused CG path
     case 1: launch_variant<1>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;

@@ -365,6 +365,15 @@ void TcsrOwner::release() {
 bool TcsrOwner::refresh(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* v,
                         std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy) {
     const bool forced = policy == CsrKernel::Tiled;
+    // The builder reads the caller's arrays on host threads: lazy write-back
+    // bytes there are filled first, from normal context (never by the fault
+    // handler on a worker thread).
+    if (rows > 0) {
+        host_in(rp, sizeof(std::int64_t) * static_cast<std::size_t>(rows + 1));
+        const std::int64_t end = std::max<std::int64_t>(rp[rows], 0);
+        host_in(ci, sizeof(std::int64_t) * static_cast<std::size_t>(end));
+        host_in(v, sizeof(double) * static_cast<std::size_t>(end));
+    }
     if (policy == CsrKernel::Vector || policy == CsrKernel::Exact ||
         !tcsr_wanted(rows, rp, ci, cols, monotone, max_row, forced)) {
         release();
@@ -384,6 +393,7 @@ bool merge_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, boo
 }
 
 bool MergeOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel policy) {
+    if (A.rows > 0) host_in(rp, sizeof(std::int64_t) * static_cast<std::size_t>(A.rows + 1));
     const std::int64_t nnz = A.rows > 0 ? rp[A.rows] - rp[0] : 0;
     // built on request only: for Auto the split plan serves skewed matrices
     // (faster on the Kronecker operator)
@@ -409,6 +419,7 @@ bool MergeOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel poli
 }
 
 bool SplitOwner::refresh(const CsrDev& A, const std::int64_t* rp, CsrKernel policy) {
+    if (A.rows > 0) host_in(rp, sizeof(std::int64_t) * static_cast<std::size_t>(A.rows + 1));
     const std::int64_t nnz = A.rows > 0 ? rp[A.rows] - rp[0] : 0;
     const bool forced = policy == CsrKernel::Split;
     if ((policy != CsrKernel::Auto && !forced) || !merge_wanted(A.rows, nnz, A.max_row, A.monotone, forced)) {
