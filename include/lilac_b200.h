@@ -248,6 +248,14 @@ int b200_cg_reset(b200_cg* cg, void* stream);
 int b200_cg_outer(b200_cg* cg, int cgitmax, double shift, void* stream);
 /* One CG step (spmv+dot, z/r update + r.r, p update). */
 int b200_cg_step(b200_cg* cg, void* stream);
+/* Plain CG in steps (the stencil config): b200_cg_start sets x = b (device
+ * array of n doubles; NULL keeps the current x), z = 0, r = p = b, rho = r.r;
+ * each b200_cg_step advances one iteration; b200_cg_finish computes
+ * rnorm = |b - A z|. b200_cg_scalars copies rho and rnorm to the host on
+ * `stream` (synchronises that stream). */
+int b200_cg_start(b200_cg* cg, const double* b_device, void* stream);
+int b200_cg_finish(b200_cg* cg, void* stream);
+int b200_cg_scalars(b200_cg* cg, void* stream, double* rho, double* rnorm);
 /* Copies zeta and the last residual norm to the host (synchronises). */
 int b200_cg_result(b200_cg* cg, double* zeta, double* rnorm);
 /* Plain CG on A z = b from z = 0: `iters` steps (the conj_grad recurrence),
@@ -268,6 +276,15 @@ int b200_npb_cg(b200_cg* cg, int niter, double shift, double* zeta, double* rnor
 int b200_gen_npb(int64_t na, int nonzer, double shift, int64_t* row_ptr, int64_t* col_ind,
                  double* val, int64_t* nnz);
 
+/* Graph500 Kronecker graph (2^scale vertices, edgefactor * 2^scale edges,
+ * quadrant probabilities a/b/c, counter-based hashed uniforms from `seed`,
+ * vertex labels permuted) as the PageRank operator: CSR of the transposed,
+ * column-stochastic adjacency (row = dst, ascending src, duplicate edges kept,
+ * val = 1/outdeg(src)). row_ptr: 2^scale + 1; col_ind / val: edgefactor *
+ * 2^scale entries. Host threads. */
+int b200_gen_kronecker(int scale, int edgefactor, uint64_t seed, double a, double b, double c, int64_t* row_ptr,
+                       int64_t* col_ind, double* val);
+
 /* ==========================================================================
  * 7. Row sharding (multi-GPU driver)
  * ========================================================================== */
@@ -275,6 +292,17 @@ int b200_gen_npb(int64_t na, int nonzer, double shift, int64_t* row_ptr, int64_t
 /* nnz-balanced contiguous row ranges: bounds[g] = lower_bound(row_ptr,
  * row_ptr[0] + ceil(g*nnz/k)), clamped monotone; bounds[0]=0, bounds[k]=rows. */
 void b200_partition_rows(int64_t rows, const int64_t* row_ptr, int k, int64_t* bounds);
+
+/* Column footprint of a row block: [min col, max col + 1) of its nonzeros
+ * (0, 0 when empty): the replica entries the block's SpMV reads. */
+void b200_shard_footprint(int64_t rows, const int64_t* row_ptr, const int64_t* col_ind, int64_t* fmin,
+                          int64_t* fmax);
+/* The exchange plan: out[(s*world + r)*2 + {0,1}] = the slice-relative range
+ * [lo, hi) of shard s (rows [bounds[s], bounds[s+1])) that rank r reads
+ * (its footprint [fmin[r], fmax[r]) intersected with the shard). The peer
+ * exchange pushes exactly these ranges. Host only. */
+void b200_dist_send_ranges(int world, const int64_t* bounds, const int64_t* fmin, const int64_t* fmax,
+                           int64_t* out);
 
 /* Row-sharded NPB CG: each shard owns rows [bounds[g],
  * bounds[g+1]), keeps them resident, and all-gathers p every CG step (NCCL
@@ -295,6 +323,24 @@ int b200_dist_cg_create_nccl(b200_dist_cg** out, int rank, int world, const void
  * sharded algorithm, for single-GPU verification. Full CSR on input. */
 int b200_dist_cg_create_local(b200_dist_cg** out, int k, int64_t n, const int64_t* row_ptr,
                               const int64_t* col_ind, const double* val);
+/* The 27-point stencil (SURVEY §8(d) input 5) row-sharded: every shard's rows
+ * are generated in its own HBM (nnz-balanced bounds, b200_dist_cg_bounds),
+ * column footprint = its rows' neighbours, so the p exchange moves a halo of
+ * about nx^2 rows per neighbour instead of the whole vector. One shard per
+ * process (NCCL / peer memory) or k local shards on one GPU. */
+int b200_dist_cg_create_stencil27_nccl(b200_dist_cg** out, int rank, int world, const void* nccl_id, int64_t nx,
+                                       double diag, double offdiag);
+int b200_dist_cg_create_stencil27_local(b200_dist_cg** out, int k, int64_t nx, double diag, double offdiag);
+/* bounds[0..world] of the sharded driver's row partition. */
+int b200_dist_cg_bounds(const b200_dist_cg* d, int64_t* bounds);
+/* Plain sharded CG in steps: start_rowsum sets x = b = A 1 (the config's
+ * right-hand side), z = 0, r = p = b; step = one CG iteration (SpMV + dots +
+ * updates + the p exchange); finish = |b - A z| (gathers z); scalars copies
+ * rho and rnorm to the host on `stream`. */
+int b200_dist_cg_start_rowsum(b200_dist_cg* d, void* stream);
+int b200_dist_cg_step(b200_dist_cg* d, void* stream);
+int b200_dist_cg_finish(b200_dist_cg* d, void* stream);
+int b200_dist_cg_scalars(b200_dist_cg* d, void* stream, double* rho, double* rnorm);
 void b200_dist_cg_free(b200_dist_cg* d);
 int b200_dist_cg_reset(b200_dist_cg* d, void* stream);
 int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream);

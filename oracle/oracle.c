@@ -112,6 +112,50 @@ void orc_spmv_csr_mt(int64_t rows, double* output, const int64_t* row_ptr, const
     for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
 }
 
+/* Multi-threaded JDS SpMV: original rows split statically across threads,
+ * each row in the reference's k order (bit-identical to orc_spmv_jds; no
+ * bounds checks: the caller validated the arrays with orc_spmv_jds). */
+typedef struct {
+    int64_t lo, hi;
+    double* output;
+    const int64_t *nzcnt, *perm, *jd_ptr, *col_ind;
+    const double *val, *x;
+} jds_slice;
+
+static void* jds_slice_run(void* arg) {
+    const jds_slice* s = (const jds_slice*)arg;
+    for (int64_t i = s->lo; i < s->hi; ++i) {
+        const int64_t p = s->perm[i], len = s->nzcnt[p];
+        double acc = 0.0;
+        for (int64_t k = 0; k < len; ++k) {
+            const int64_t off = s->jd_ptr[k] + p;
+            acc += s->val[off] * s->x[s->col_ind[off]];
+        }
+        s->output[i] = acc;
+    }
+    return NULL;
+}
+
+void orc_spmv_jds_mt(int64_t rows, double* output, const int64_t* nzcnt, const int64_t* perm,
+                     const double* val, const int64_t* jd_ptr, const double* x, const int64_t* col_ind,
+                     int nthreads) {
+    if (nthreads <= 0) nthreads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (nthreads > 256) nthreads = 256;
+    if (nthreads <= 1 || rows < 4096) {
+        jds_slice s = {0, rows, output, nzcnt, perm, jd_ptr, col_ind, val, x};
+        jds_slice_run(&s);
+        return;
+    }
+    pthread_t th[256];
+    jds_slice sl[256];
+    for (int t = 0; t < nthreads; ++t) {
+        sl[t] = (jds_slice){rows * t / nthreads, rows * (t + 1) / nthreads, output, nzcnt, perm, jd_ptr, col_ind,
+                            val, x};
+        pthread_create(&th[t], NULL, jds_slice_run, &sl[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Encoders                                                                  */
 /* ------------------------------------------------------------------------ */
@@ -421,6 +465,59 @@ static double npb_conj_grad(int64_t n, const int64_t* rowstr, const int64_t* col
         sum = sum + d * d;
     }
     return sqrt(sum);
+}
+
+/* One NPB outer iteration from the caller's x (NPB 3.x cg main loop body):
+ * conj_grad with the SpMV on `nthreads` threads (bit-identical for any count),
+ * then zeta = shift + 1/(x.z), x = z/|z|. Returns zeta; *rnorm_out = |x - A z|.
+ * Scratch: z, p, q, r of n doubles. */
+static double npb_conj_grad_t(int64_t n, const int64_t* rowstr, const int64_t* colidx, const double* a,
+                              const double* x, double* z, double* p, double* q, double* r, int nthreads) {
+    const int cgitmax = 25;
+    double rho = 0.0, d, alpha, beta, rho0, sum;
+    for (int64_t j = 0; j < n; ++j) {
+        q[j] = 0.0;
+        z[j] = 0.0;
+        r[j] = x[j];
+        p[j] = r[j];
+    }
+    for (int64_t j = 0; j < n; ++j) rho = rho + r[j] * r[j];
+    for (int cgit = 1; cgit <= cgitmax; ++cgit) {
+        orc_spmv_csr_mt(n, q, rowstr, a, p, colidx, nthreads);
+        d = 0.0;
+        for (int64_t j = 0; j < n; ++j) d = d + p[j] * q[j];
+        alpha = rho / d;
+        rho0 = rho;
+        rho = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            z[j] = z[j] + alpha * p[j];
+            r[j] = r[j] - alpha * q[j];
+        }
+        for (int64_t j = 0; j < n; ++j) rho = rho + r[j] * r[j];
+        beta = rho / rho0;
+        for (int64_t j = 0; j < n; ++j) p[j] = r[j] + beta * p[j];
+    }
+    orc_spmv_csr_mt(n, r, rowstr, a, z, colidx, nthreads);
+    sum = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        d = x[j] - r[j];
+        sum = sum + d * d;
+    }
+    return sqrt(sum);
+}
+
+double orc_npb_outer(int64_t n, const int64_t* row_ptr, const int64_t* col_ind, const double* val, double* x,
+                     double* z, double* p, double* q, double* r, double shift, int nthreads, double* rnorm_out) {
+    const double rnorm = npb_conj_grad_t(n, row_ptr, col_ind, val, x, z, p, q, r, nthreads);
+    double t1 = 0.0, t2 = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        t1 = t1 + x[j] * z[j];
+        t2 = t2 + z[j] * z[j];
+    }
+    t2 = 1.0 / sqrt(t2);
+    for (int64_t j = 0; j < n; ++j) x[j] = t2 * z[j];
+    if (rnorm_out) *rnorm_out = rnorm;
+    return shift + 1.0 / t1;
 }
 
 double orc_npb_cg(int64_t n, const int64_t* row_ptr, const int64_t* col_ind, const double* val,

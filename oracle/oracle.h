@@ -48,6 +48,12 @@ void orc_axpy(int64_t n, double* y, double alpha, const double* x);
 void orc_spmv_csr_mt(int64_t rows, double* output, const int64_t* row_ptr, const double* val,
                      const double* x, const int64_t* col_ind, int nthreads);
 
+/* Multi-threaded JDS SpMV (original rows split across threads, per-row k order
+ * unchanged: bit-identical to orc_spmv_jds). No bounds checks. */
+void orc_spmv_jds_mt(int64_t rows, double* output, const int64_t* nzcnt, const int64_t* perm,
+                     const double* val, const int64_t* jd_ptr, const double* x, const int64_t* col_ind,
+                     int nthreads);
+
 /* ---- format encoders (tests/support/oracles.hpp:68-156) ---- */
 
 /* csr_from_dense (oracles.hpp:68-84). Caller sizes val/col_ind for the
@@ -90,6 +96,13 @@ int orc_npb_makea(int64_t na, int nonzer, double shift, int64_t* row_ptr, int64_
  * *rnorm_out receives the last residual norm. */
 double orc_npb_cg(int64_t na, const int64_t* row_ptr, const int64_t* col_ind, const double* val,
                   int niter, double shift, double* rnorm_out);
+
+/* One NPB outer iteration from the caller's x (updated in place to z/|z|):
+ * conj_grad with its SpMV on `nthreads` threads (0 = all online CPUs), then
+ * zeta = shift + 1/(x.z). Scratch z, p, q, r: n doubles each. The timed
+ * native CPU baseline of bench.py. */
+double orc_npb_outer(int64_t n, const int64_t* row_ptr, const int64_t* col_ind, const double* val, double* x,
+                     double* z, double* p, double* q, double* r, double shift, int nthreads, double* rnorm_out);
 
 #ifdef __cplusplus
 }

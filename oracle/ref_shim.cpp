@@ -149,6 +149,22 @@ void ref_output(void* h, double* out) {
 
 void ref_free(void* h) { delete static_cast<RefCall*>(h); }
 
+// Overwrite the float buffer behind argument `arg` of a prepared call (e.g.
+// x of spmv_csr = arg 4, a/b of dotproduct = args 1/2) through the reference
+// Memory's own store path (interp.hpp:47-50), so a host CG loop can drive the
+// stock HarnessFn with changing vectors. Returns 0, or -1 on a bad argument.
+int ref_set_floats(void* h, int arg, const double* src, int64_t n) {
+    auto* c = static_cast<RefCall*>(h);
+    if (arg < 0 || arg >= static_cast<int>(c->args.size())) return -1;
+    const auto* p = std::get_if<interp::Pointer>(&c->args[static_cast<size_t>(arg)]);
+    if (!p) return -1;
+    if (n > c->mem.size(p->buffer) - p->offset) return -1;
+    for (int64_t i = 0; i < n; ++i) c->mem.store_float(interp::Pointer{p->buffer, p->offset + i}, src[i]);
+    return 0;
+}
+
+double ref_scalar(void* h) { return static_cast<RefCall*>(h)->scalar; }
+
 // infer_interface (what_parse.cpp:356-429) of a LiLAC-What program:
 // "name:kind,name:kind,...;scalar_result" into buf.
 int ref_infer_interface(const char* what_text, char* buf, int64_t cap) {

@@ -92,15 +92,30 @@ SIGNATURES = {
     "b200_cg_outer": (C.c_int, [vp, C.c_int, C.c_double, vp]),
     "b200_cg_step": (C.c_int, [vp, vp]),
     "b200_cg_result": (C.c_int, [vp, f64p, f64p]),
+    "b200_cg_start": (C.c_int, [vp, vp, vp]),
+    "b200_cg_finish": (C.c_int, [vp, vp]),
+    "b200_cg_scalars": (C.c_int, [vp, vp, f64p, f64p]),
     "b200_npb_cg": (C.c_int, [vp, C.c_int, C.c_double, f64p, f64p]),
     # 6. workloads
     "b200_gen_npb": (C.c_int, [i64, C.c_int, C.c_double, i64p, i64p, f64p, i64p]),
+    "b200_gen_kronecker": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, i64p, i64p,
+                                     f64p]),
     # 7. sharding
     "b200_partition_rows": (None, [i64, i64p, C.c_int, i64p]),
+    "b200_shard_footprint": (None, [i64, i64p, i64p, i64p, i64p]),
+    "b200_dist_send_ranges": (None, [C.c_int, i64p, i64p, i64p, i64p]),
     "b200_dist_nccl_id": (C.c_int, [vp]),
     "b200_dist_cg_create_nccl": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, vp, i64, i64p, i64p, i64p, f64p]),
     "b200_dist_cg_create_local": (C.c_int, [C.POINTER(vp), C.c_int, i64, i64p, i64p, f64p]),
     "b200_dist_cg_free": (None, [vp]),
+    "b200_dist_cg_create_stencil27_nccl": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, vp, i64, C.c_double,
+                                                     C.c_double]),
+    "b200_dist_cg_create_stencil27_local": (C.c_int, [C.POINTER(vp), C.c_int, i64, C.c_double, C.c_double]),
+    "b200_dist_cg_bounds": (C.c_int, [vp, i64p]),
+    "b200_dist_cg_start_rowsum": (C.c_int, [vp, vp]),
+    "b200_dist_cg_step": (C.c_int, [vp, vp]),
+    "b200_dist_cg_finish": (C.c_int, [vp, vp]),
+    "b200_dist_cg_scalars": (C.c_int, [vp, vp, f64p, f64p]),
     "b200_dist_cg_reset": (C.c_int, [vp, vp]),
     "b200_dist_cg_outer": (C.c_int, [vp, C.c_int, C.c_double, vp]),
     "b200_dist_cg_result": (C.c_int, [vp, f64p, f64p]),

@@ -305,6 +305,11 @@ void cg_launch_reset_x(const CgVectors& v, cudaStream_t s);
 // Workload pieces (workloads_dev.cu): the 27-point stencil matrix generated in
 // HBM (int32 columns) and the PageRank update x = d*ax + (1-d)/n.
 std::int64_t stencil27_nnz(std::int64_t nx);
+// nonzeros of rows [0, r) of the stencil (exact, O(nx))
+std::int64_t stencil27_prefix_nnz(std::int64_t nx, std::int64_t r);
+// rows [r0, r1) generated in HBM: rebased int64 row_ptr, int32 col, f64 val
+void gen_stencil27_rows_device(std::int64_t nx, std::int64_t r0, std::int64_t r1, double diag, double off,
+                               DevBuf& row_ptr, DevBuf& col, DevBuf& val, cudaStream_t s);
 void gen_stencil27_device(std::int64_t nx, double diag, double off, DevBuf& row_ptr, DevBuf& col, DevBuf& val,
                           cudaStream_t s);
 void launch_pagerank_update(std::int64_t n, double* x, const double* ax, double d, cudaStream_t s);

@@ -118,6 +118,30 @@ int b200_cg_step(b200_cg* cg, void* stream) {
     return boundary("b200_cg_step", [&] { cg_launch_iteration(cg->A, cg->v, pick(stream)); });
 }
 
+int b200_cg_start(b200_cg* cg, const double* b_device, void* stream) {
+    return boundary("b200_cg_start", [&] {
+        cudaStream_t s = pick(stream);
+        const std::size_t bytes = sizeof(double) * static_cast<std::size_t>(cg->v.n);
+        if (b_device && bytes) B200_CUDA(cudaMemcpyAsync(cg->v.x, b_device, bytes, cudaMemcpyDeviceToDevice, s));
+        cg_launch_init(cg->v, s);  // z = 0, r = p = b, rho = r.r
+    });
+}
+
+int b200_cg_finish(b200_cg* cg, void* stream) {
+    return boundary("b200_cg_finish", [&] { cg_launch_residual(cg->A, cg->v, pick(stream)); });
+}
+
+int b200_cg_scalars(b200_cg* cg, void* stream, double* rho, double* rnorm) {
+    return boundary("b200_cg_scalars", [&] {
+        cudaStream_t s = pick(stream);
+        CgScalars sc;
+        B200_CUDA(cudaMemcpyAsync(&sc, cg->v.sc, sizeof sc, cudaMemcpyDeviceToHost, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        if (rho) *rho = sc.rho;
+        if (rnorm) *rnorm = sc.rnorm;
+    });
+}
+
 int b200_cg_result(b200_cg* cg, double* zeta, double* rnorm) {
     return boundary("b200_cg_result", [&] {
         CgScalars sc;

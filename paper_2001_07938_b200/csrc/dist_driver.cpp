@@ -75,6 +75,8 @@ struct b200_dist_cg {
 
 namespace {
 
+void init_shard_vectors(Shard& s, std::int64_t n, int nranks);
+
 // Upload one row block [row0, row0+rows) given its host arrays (row_ptr with
 // rows+1 entries, absolute offsets into col_ind/val as passed).
 void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, const std::int64_t* rp,
@@ -115,6 +117,13 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
         if (s.split.refresh(A, lrp.data(), rt().kernel)) A.split = &s.split.dev;
         if (s.merge.refresh(A, lrp.data(), rt().kernel)) A.merge = &s.merge.dev;
     }
+    init_shard_vectors(s, n, nranks);
+}
+
+// Per-shard CG state: owned x/q/r, full-length p/z replicas, partials and
+// scalars (sharded mode), CgVectors views.
+void init_shard_vectors(Shard& s, std::int64_t n, int nranks) {
+    const std::int64_t rows = s.rows, row0 = s.row0;
     const std::size_t own = sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(rows, 1));
     for (DevBuf* b : {&s.x, &s.q, &s.r}) b->ensure(own);
     s.p_full.ensure(sizeof(double) * n);
@@ -144,6 +153,53 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
     v.sc = s.scalars.as<CgScalars>();
     cg_launch_reset_x(v, rt().stream);
     B200_CUDA(cudaStreamSynchronize(rt().stream));
+}
+
+// Rows [row0, row0+rows) of the 27-point stencil generated in this GPU's HBM
+// (no host arrays: N = 420 is 2e9 nonzeros). Column footprint: the rows'
+// neighbours, [row0 - nx^2 - nx - 1, row0 + rows + nx^2 + nx + 1) clamped.
+void load_shard_stencil(Shard& s, std::int64_t nx, std::int64_t row0, std::int64_t rows, double diag, double off,
+                        int nranks) {
+    const std::int64_t n = nx * nx * nx;
+    s.row0 = row0;
+    s.rows = rows;
+    gen_stencil27_rows_device(nx, row0, row0 + rows, diag, off, s.row_ptr, s.col, s.val, rt().stream);
+    s.nnz = stencil27_prefix_nnz(nx, row0 + rows) - stencil27_prefix_nnz(nx, row0);
+    const std::int64_t halo = nx * nx + nx + 1;
+    s.cmin = rows ? std::max<std::int64_t>(0, row0 - halo) : 0;
+    s.cmax = rows ? std::min<std::int64_t>(n, row0 + rows + halo) : 0;
+    CsrDev& A = s.A;
+    A.rows = rows;
+    A.nnz = s.nnz;
+    A.cols = n;
+    A.max_row = rows ? 27 : 0;
+    A.row_ptr = s.row_ptr.as<std::int64_t>();
+    A.col = s.col.ptr;
+    A.col32 = true;
+    A.val = s.val.as<double>();
+    A.monotone = true;
+    init_shard_vectors(s, n, nranks);
+}
+
+// nnz-balanced row bounds of the stencil over k shards (the rule of
+// b200_partition_rows on the analytic row pointers).
+std::vector<std::int64_t> stencil_bounds(std::int64_t nx, int k) {
+    const std::int64_t n = nx * nx * nx, nnz = stencil27_prefix_nnz(nx, n);
+    std::vector<std::int64_t> b(static_cast<std::size_t>(k) + 1, 0);
+    for (int g = 1; g < k; ++g) {
+        const std::int64_t target = (nnz * g + k - 1) / k;
+        std::int64_t lo = b[g - 1], hi = n;  // first row r with prefix(r) >= target
+        while (lo < hi) {
+            const std::int64_t mid = lo + (hi - lo) / 2;
+            if (stencil27_prefix_nnz(nx, mid) < target)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        b[g] = lo;
+    }
+    b[k] = n;
+    return b;
 }
 
 std::vector<ShardView> views(b200_dist_cg* d, cudaStream_t st) {
@@ -176,31 +232,54 @@ void gather_vector(b200_dist_cg* d, cudaStream_t st, bool z) {
     d->ex->exchange_vector(vs, fulls);
 }
 
-void dist_outer(b200_dist_cg* d, int cgitmax, double shift, cudaStream_t st) {
-    for (auto& s : d->shards) cg_launch_init(s->v, st);  // q=z=0, r=p=x (owned slices), r.r partial
+
+// Plain CG in steps over the shards (the stencil config): start from
+// x = b = A 1, then one CG iteration per dist_step, dist_finish = |b - A z|.
+void dist_init(b200_dist_cg* d, cudaStream_t st) {
+    for (auto& s : d->shards) cg_launch_init(s->v, st);
     gather_scalars(d, st, 1, CgFin::Rho, 0.0);
     gather_vector(d, st, false);
-    for (int it = 0; it < cgitmax; ++it) {
-        for (auto& s : d->shards) cg_launch_spmv_dot(s->A, s->v, st);
-        gather_scalars(d, st, 1, CgFin::Alpha, 0.0);
-        for (auto& s : d->shards) cg_launch_update_zr(s->v, st);
-        gather_scalars(d, st, 1, CgFin::Beta, 0.0);
-        {
-            auto vs = views(d, st);
-            std::vector<const CgVectors*> cv;
-            for (auto& s : d->shards) cv.push_back(&s->v);
-            if (!d->ex->update_p_exchange(vs, cv)) {  // not fused: update, then exchange
-                for (auto& s : d->shards) cg_launch_update_p(s->v, st);
-                gather_vector(d, st, false);
-            }
-        }
+}
+
+void dist_start_rowsum(b200_dist_cg* d, cudaStream_t st) {
+    for (auto& s : d->shards) {
+        cg_launch_reset_x(s->v, st);  // x = 1 (owned rows)
+        if (s->rows)
+            B200_CUDA(cudaMemcpyAsync(s->v.p, s->v.x, sizeof(double) * static_cast<std::size_t>(s->rows),
+                                      cudaMemcpyDeviceToDevice, st));
     }
-    gather_vector(d, st, true);  // residual r = A z needs all of z
+    gather_vector(d, st, false);  // p replica = 1 over every footprint
+    for (auto& s : d->shards) launch_spmv_csr(s->A, s->v.p_full, s->v.x, CsrKernel::Auto, st);  // b = A 1
+    dist_init(d, st);
+}
+
+void dist_step(b200_dist_cg* d, cudaStream_t st) {
+    for (auto& s : d->shards) cg_launch_spmv_dot(s->A, s->v, st);
+    gather_scalars(d, st, 1, CgFin::Alpha, 0.0);
+    for (auto& s : d->shards) cg_launch_update_zr(s->v, st);
+    gather_scalars(d, st, 1, CgFin::Beta, 0.0);
+    auto vs = views(d, st);
+    std::vector<const CgVectors*> cv;
+    for (auto& s : d->shards) cv.push_back(&s->v);
+    if (!d->ex->update_p_exchange(vs, cv)) {
+        for (auto& s : d->shards) cg_launch_update_p(s->v, st);
+        gather_vector(d, st, false);
+    }
+}
+
+void dist_finish(b200_dist_cg* d, cudaStream_t st) {
+    gather_vector(d, st, true);
     for (auto& s : d->shards) {
         launch_spmv_csr(s->A, s->v.z_full, s->v.r, CsrKernel::Auto, st);
         cg_launch_resid_partial(s->v, st);
     }
     gather_scalars(d, st, 1, CgFin::Rnorm, 0.0);
+}
+
+void dist_outer(b200_dist_cg* d, int cgitmax, double shift, cudaStream_t st) {
+    dist_init(d, st);  // q=z=0, r=p=x (owned slices), rho; p exchanged
+    for (int it = 0; it < cgitmax; ++it) dist_step(d, st);
+    dist_finish(d, st);  // residual r = A z needs all of z
     for (auto& s : d->shards) cg_launch_norms(s->v, shift, st);
     gather_scalars(d, st, 2, CgFin::Norms, shift);
     for (auto& s : d->shards) cg_launch_scale_x(s->v, st);
@@ -295,11 +374,57 @@ int b200_dist_cg_create_nccl(b200_dist_cg** out, int rank, int world, const void
         // row_ptr holds this rank's rows: r1 - r0 + 1 entries (absolute offsets into col_ind/val)
         load_shard(*s, n, r0, r1 - r0, row_ptr, col_ind, val, world);
         d->shards.push_back(std::move(s));
-        d->ex = std::make_unique<NcclExchange>(rank, world, nccl_id, d->bounds);
+        d->ex = std::make_unique<NcclExchange>(rank, world, nccl_id, d->bounds, d->shards[0]->cmin,
+                                               d->shards[0]->cmax);
         d->rank = rank;
         d->transport = 1;
         *out = finish_create(d);
     });
+}
+
+int b200_dist_cg_create_stencil27_nccl(b200_dist_cg** out, int rank, int world, const void* nccl_id, std::int64_t nx,
+                                       double diag, double offdiag) {
+    return boundary("b200_dist_cg_create_stencil27_nccl", [&] {
+        ensure_init();
+        if (world < 1 || rank < 0 || rank >= world) throw Error(Errc::DataError, "bad rank/world");
+        if (nx < 1 || nx > 1290) throw Error(Errc::DataError, "nx must be 1..1290 (int32 columns)");
+        auto d = std::make_unique<b200_dist_cg>();
+        d->world = world;
+        d->n = nx * nx * nx;
+        d->bounds = stencil_bounds(nx, world);
+        auto s = std::make_unique<Shard>();
+        load_shard_stencil(*s, nx, d->bounds[rank], d->bounds[rank + 1] - d->bounds[rank], diag, offdiag, world);
+        d->shards.push_back(std::move(s));
+        d->ex = std::make_unique<NcclExchange>(rank, world, nccl_id, d->bounds, d->shards[0]->cmin,
+                                               d->shards[0]->cmax);
+        d->rank = rank;
+        d->transport = 1;
+        *out = finish_create(d);
+    });
+}
+
+int b200_dist_cg_create_stencil27_local(b200_dist_cg** out, int k, std::int64_t nx, double diag, double offdiag) {
+    return boundary("b200_dist_cg_create_stencil27_local", [&] {
+        ensure_init();
+        if (k < 1 || k > 64) throw Error(Errc::DataError, "shard count must be 1..64");
+        if (nx < 1 || nx > 1290) throw Error(Errc::DataError, "nx must be 1..1290 (int32 columns)");
+        auto d = std::make_unique<b200_dist_cg>();
+        d->world = k;
+        d->n = nx * nx * nx;
+        d->bounds = stencil_bounds(nx, k);
+        for (int g = 0; g < k; ++g) {
+            auto s = std::make_unique<Shard>();
+            load_shard_stencil(*s, nx, d->bounds[g], d->bounds[g + 1] - d->bounds[g], diag, offdiag, k);
+            d->shards.push_back(std::move(s));
+        }
+        d->ex = std::make_unique<LocalExchange>(k);
+        d->transport = 0;
+        *out = finish_create(d);
+    });
+}
+
+int b200_dist_cg_bounds(const b200_dist_cg* d, std::int64_t* bounds) {
+    return boundary("b200_dist_cg_bounds", [&] { std::copy(d->bounds.begin(), d->bounds.end(), bounds); });
 }
 
 void b200_dist_cg_free(b200_dist_cg* d) {
@@ -402,6 +527,34 @@ int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream) {
 int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream) {
     return boundary("b200_dist_cg_outer", [&] {
         dist_outer_graph(d, cgitmax, shift, stream ? static_cast<cudaStream_t>(stream) : d->stream);
+    });
+}
+
+int b200_dist_cg_start_rowsum(b200_dist_cg* d, void* stream) {
+    return boundary("b200_dist_cg_start_rowsum", [&] {
+        dist_start_rowsum(d, stream ? static_cast<cudaStream_t>(stream) : d->stream);
+    });
+}
+
+int b200_dist_cg_step(b200_dist_cg* d, void* stream) {
+    return boundary("b200_dist_cg_step", [&] { dist_step(d, stream ? static_cast<cudaStream_t>(stream) : d->stream); });
+}
+
+int b200_dist_cg_finish(b200_dist_cg* d, void* stream) {
+    return boundary("b200_dist_cg_finish", [&] {
+        dist_finish(d, stream ? static_cast<cudaStream_t>(stream) : d->stream);
+    });
+}
+
+int b200_dist_cg_scalars(b200_dist_cg* d, void* stream, double* rho, double* rnorm) {
+    return boundary("b200_dist_cg_scalars", [&] {
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
+        CgScalars sc;
+        B200_CUDA(cudaMemcpyAsync(&sc, d->shards[0]->v.sc, sizeof sc, cudaMemcpyDeviceToHost, st));
+        B200_CUDA(cudaStreamSynchronize(st));
+        check_peer_errors(d);
+        if (rho) *rho = sc.rho;
+        if (rnorm) *rnorm = sc.rnorm;
     });
 }
 

@@ -25,6 +25,8 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -47,6 +49,8 @@ NcclApi& nccl() {
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
         api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
         api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
         api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
         api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
@@ -100,13 +104,41 @@ void LocalExchange::exchange_vector(std::vector<ShardView>& shards, std::vector<
 
 // ---- NcclExchange --------------------------------------------------------------------
 
-NcclExchange::NcclExchange(int rank, int world, const void* unique_id, const std::vector<std::int64_t>& bounds)
+NcclExchange::NcclExchange(int rank, int world, const void* unique_id, const std::vector<std::int64_t>& bounds,
+                           std::int64_t fmin, std::int64_t fmax)
     : rank_(rank), world_(world), bounds_(bounds) {
     ncclUniqueId id;
     std::memcpy(&id, unique_id, sizeof id);
     ncclComm_t c = nullptr;
     check_nccl(nccl().CommInitRank(&c, world, id, rank), "ncclCommInitRank");
     comm_ = c;
+    // every rank's footprint, then this rank's send/recv ranges
+    DevBuf fp;
+    fp.ensure(sizeof(std::int64_t) * 2 * static_cast<std::size_t>(world + 1));
+    const std::int64_t mine[2] = {fmin, fmax};
+    cudaStream_t st = rt().stream;
+    B200_CUDA(cudaMemcpyAsync(fp.as<std::int64_t>() + 2 * world, mine, sizeof mine, cudaMemcpyHostToDevice, st));
+    check_nccl(nccl().AllGather(fp.as<std::int64_t>() + 2 * world, fp.as<std::int64_t>(), 2, ncclInt64, c, st),
+               "ncclAllGather(footprints)");
+    std::vector<std::int64_t> all(2 * static_cast<std::size_t>(world));
+    B200_CUDA(cudaMemcpyAsync(all.data(), fp.ptr, sizeof(std::int64_t) * all.size(), cudaMemcpyDeviceToHost, st));
+    B200_CUDA(cudaStreamSynchronize(st));
+    fp.release();
+    std::vector<std::int64_t> lo(world), hi(world);
+    for (int r = 0; r < world; ++r) {
+        lo[r] = all[2 * r];
+        hi[r] = all[2 * r + 1];
+    }
+    send_ = send_ranges(bounds_[rank], bounds_[rank + 1] - bounds_[rank], lo, hi);
+    recv_.assign(2 * static_cast<std::size_t>(world), 0);
+    for (int src = 0; src < world; ++src) {
+        const std::vector<std::int64_t> sr = send_ranges(bounds_[src], bounds_[src + 1] - bounds_[src], lo, hi);
+        recv_[2 * src] = sr[2 * rank];
+        recv_[2 * src + 1] = sr[2 * rank + 1];
+        for (int r = 0; r < world; ++r)  // full: every slice goes whole to every rank
+            if (r != src && sr[2 * r + 1] - sr[2 * r] != bounds_[src + 1] - bounds_[src]) full_ = false;
+    }
+    if (!nccl().Send || !nccl().Recv) full_ = true;
 }
 
 NcclExchange::~NcclExchange() {
@@ -121,16 +153,36 @@ void NcclExchange::exchange_scalars(std::vector<ShardView>& shards, int npart) {
 }
 
 void NcclExchange::exchange_vector(std::vector<ShardView>& shards, std::vector<double*> fulls) {
-    // variable-size all-gather: one broadcast per owner, fused in a group
     ShardView& s = shards[0];
     double* full = fulls[0];
     check_nccl(nccl().GroupStart(), "ncclGroupStart");
-    for (int r = 0; r < world_; ++r) {
-        const std::int64_t lo = bounds_[r], n = bounds_[r + 1] - bounds_[r];
-        if (n == 0) continue;
-        check_nccl(nccl().Broadcast(full + lo, full + lo, static_cast<size_t>(n), ncclDouble, r,
-                                    static_cast<ncclComm_t>(comm_), s.stream),
-                   "ncclBroadcast");
+    if (full_) {
+        // every rank reads every slice (NPB's random columns): a variable-size
+        // all-gather as one broadcast per owner, fused in a group
+        for (int r = 0; r < world_; ++r) {
+            const std::int64_t lo = bounds_[r], n = bounds_[r + 1] - bounds_[r];
+            if (n == 0) continue;
+            check_nccl(nccl().Broadcast(full + lo, full + lo, static_cast<size_t>(n), ncclDouble, r,
+                                        static_cast<ncclComm_t>(comm_), s.stream),
+                       "ncclBroadcast");
+        }
+    } else {
+        // footprint-limited (banded / stencil rows): each rank gets only the
+        // part of each slice its SpMV reads — the halo, not the whole vector
+        const std::int64_t mine = bounds_[rank_];
+        for (int r = 0; r < world_; ++r) {
+            if (r == rank_) continue;
+            const std::int64_t slo = send_[2 * r], shi = send_[2 * r + 1];
+            if (shi > slo)
+                check_nccl(nccl().Send(full + mine + slo, static_cast<size_t>(shi - slo), ncclDouble, r,
+                                       static_cast<ncclComm_t>(comm_), s.stream),
+                           "ncclSend");
+            const std::int64_t rlo = recv_[2 * r], rhi = recv_[2 * r + 1];
+            if (rhi > rlo)
+                check_nccl(nccl().Recv(full + bounds_[r] + rlo, static_cast<size_t>(rhi - rlo), ncclDouble, r,
+                                       static_cast<ncclComm_t>(comm_), s.stream),
+                           "ncclRecv");
+        }
     }
     check_nccl(nccl().GroupEnd(), "ncclGroupEnd");
 }
@@ -168,16 +220,23 @@ void PeerExchange::upload_table(Local& l, const std::vector<PeerPtrs>& peers) {
     B200_CUDA(cudaStreamSynchronize(rt().stream));
 }
 
-void PeerExchange::upload_send(Local& l, const std::vector<std::int64_t>& fmin, const std::vector<std::int64_t>& fmax) {
-    std::vector<std::int64_t> send(2 * static_cast<std::size_t>(world_), 0);
-    const std::int64_t a = l.bufs.row0, b = l.bufs.row0 + l.bufs.rows;
-    for (int r = 0; r < world_; ++r) {
+std::vector<std::int64_t> send_ranges(std::int64_t row0, std::int64_t rows, const std::vector<std::int64_t>& fmin,
+                                      const std::vector<std::int64_t>& fmax) {
+    const std::size_t world = fmin.size();
+    std::vector<std::int64_t> send(2 * world, 0);
+    const std::int64_t a = row0, b = row0 + rows;
+    for (std::size_t r = 0; r < world; ++r) {
         const std::int64_t lo = std::max(a, fmin[r]), hi = std::min(b, fmax[r]);
         if (hi > lo) {
             send[2 * r] = lo - a;
             send[2 * r + 1] = hi - a;
         }
     }
+    return send;
+}
+
+void PeerExchange::upload_send(Local& l, const std::vector<std::int64_t>& fmin, const std::vector<std::int64_t>& fmax) {
+    const std::vector<std::int64_t> send = send_ranges(l.bufs.row0, l.bufs.rows, fmin, fmax);
     l.send.ensure(sizeof(std::int64_t) * send.size());
     B200_CUDA(cudaMemcpyAsync(l.send.ptr, send.data(), sizeof(std::int64_t) * send.size(), cudaMemcpyHostToDevice,
                               rt().stream));

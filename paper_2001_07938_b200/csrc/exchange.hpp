@@ -68,7 +68,11 @@ private:
 // NCCL communicator wrapper (dlopen'ed). One shard (this rank).
 class NcclExchange : public Exchange {
 public:
-    NcclExchange(int rank, int world, const void* unique_id, const std::vector<std::int64_t>& bounds);
+    // fmin/fmax: this shard's column footprint; the communicator all-gathers
+    // every rank's, and a vector exchange then moves only the ranges each rank
+    // reads (grouped send/recv: a halo for banded rows, everything for NPB)
+    NcclExchange(int rank, int world, const void* unique_id, const std::vector<std::int64_t>& bounds,
+                 std::int64_t fmin, std::int64_t fmax);
     ~NcclExchange() override;
     int nshards() const override { return 1; }
     int rank() const { return rank_; }
@@ -80,6 +84,8 @@ private:
     int rank_, world_;
     void* comm_ = nullptr;
     std::vector<std::int64_t> bounds_;
+    std::vector<std::int64_t> send_, recv_;  // world x {lo, hi}: slice-relative ranges to / from each rank
+    bool full_ = true;                       // every rank reads every slice: grouped broadcasts
 };
 
 // Peer-memory exchange (p2p.cu): each shard pushes into its peers' replicas
@@ -132,6 +138,13 @@ private:
     int world_ = 1;
     std::vector<void*> opened_;  // IPC mappings to close
 };
+
+// The part of shard [row0, row0+rows) that each rank r reads: its column
+// footprint [fmin[r], fmax[r]) intersected with the shard, as slice-relative
+// {lo, hi} pairs ({0, 0}: nothing). Host logic shared by the peer exchange and
+// b200_dist_send_ranges (the CPU-checkable exchange plan).
+std::vector<std::int64_t> send_ranges(std::int64_t row0, std::int64_t rows, const std::vector<std::int64_t>& fmin,
+                                      const std::vector<std::int64_t>& fmax);
 
 void nccl_unique_id(void* out128);
 int nccl_version();

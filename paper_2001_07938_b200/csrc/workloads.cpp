@@ -9,6 +9,7 @@
 // order) at O(nnz log row) cost and in parallel across rows.
 
 #include "lilac_b200.h"
+#include "exchange.hpp"
 #include "runtime.hpp"
 
 #include <algorithm>
@@ -177,4 +178,114 @@ extern "C" void b200_partition_rows(std::int64_t rows, const std::int64_t* row_p
         bounds[g] = r;
     }
     bounds[k] = rows;
+}
+
+// Column footprint of a row block: [min col, max col + 1) over its nonzeros
+// ({0, 0} when empty) — the replica entries the block's SpMV reads.
+extern "C" void b200_shard_footprint(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind,
+                                     std::int64_t* fmin, std::int64_t* fmax) {
+    std::int64_t lo = INT64_MAX, hi = -1;
+    if (rows > 0)
+        for (std::int64_t j = row_ptr[0]; j < row_ptr[rows]; ++j) {
+            lo = std::min(lo, col_ind[j]);
+            hi = std::max(hi, col_ind[j]);
+        }
+    *fmin = hi < 0 ? 0 : lo;
+    *fmax = hi < 0 ? 0 : hi + 1;
+}
+
+// The exchange plan of the sharded driver: out[(s * world + r) * 2 + {0, 1}] =
+// the part of shard s's slice (slice-relative [lo, hi)) that rank r reads.
+extern "C" void b200_dist_send_ranges(int world, const std::int64_t* bounds, const std::int64_t* fmin,
+                                      const std::int64_t* fmax, std::int64_t* out) {
+    if (world <= 0) return;
+    const std::vector<std::int64_t> lo(fmin, fmin + world), hi(fmax, fmax + world);
+    for (int s = 0; s < world; ++s) {
+        const std::vector<std::int64_t> r = b200::send_ranges(bounds[s], bounds[s + 1] - bounds[s], lo, hi);
+        std::copy(r.begin(), r.end(), out + static_cast<std::ptrdiff_t>(s) * 2 * world);
+    }
+}
+
+// ---- Graph500 Kronecker generator (SURVEY §8(d) input 4) ---------------------------
+//
+// Edge e's endpoints come from `scale` quadrant choices with probabilities
+// A/B/C/D (Graph500: 0.57/0.19/0.19/0.05): per bit, u1 = U(e, 2 bit), u2 =
+// U(e, 2 bit + 1); i = u1 > A+B; j = u2 > (i ? C/(1-A-B) : A/(A+B)). The
+// uniforms are counter-based (splitmix64 of seed, edge, draw), so edges are
+// generated in parallel and the graph depends only on (scale, edgefactor,
+// seed). Vertex labels are then permuted (Fisher-Yates driven by the same
+// hash), as Graph500 does, and the PageRank operator is built: CSR of the
+// transpose (row = dst), columns ascending per row (duplicate edges kept),
+// val = 1/outdeg(src).
+
+namespace {
+
+inline std::uint64_t mix64(std::uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+inline double unit(std::uint64_t seed, std::uint64_t e, std::uint64_t k) {
+    const std::uint64_t h = mix64(mix64(seed ^ mix64(e)) + k);
+    return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+
+}  // namespace
+
+extern "C" int b200_gen_kronecker(int scale, int edgefactor, std::uint64_t seed, double a, double b, double c,
+                                  std::int64_t* row_ptr, std::int64_t* col_ind, double* val) {
+    return boundary("b200_gen_kronecker", [&] {
+        if (scale < 1 || scale > 30 || edgefactor < 1) throw Error(Errc::DataError, "scale 1..30, edgefactor >= 1");
+        const std::int64_t n = std::int64_t(1) << scale, m = static_cast<std::int64_t>(edgefactor) * n;
+        const double ab = a + b, c_norm = c / (1.0 - ab), a_norm = a / ab;
+        std::vector<std::int64_t> src(static_cast<std::size_t>(m)), dst(static_cast<std::size_t>(m));
+        parallel_for(m, [&](std::int64_t lo, std::int64_t hi) {
+            for (std::int64_t e = lo; e < hi; ++e) {
+                std::int64_t s = 0, d = 0;
+                for (int ib = 0; ib < scale; ++ib) {
+                    const int ii = unit(seed, static_cast<std::uint64_t>(e), 2u * ib) > ab;
+                    const double thr = ii ? c_norm : a_norm;
+                    const int jj = unit(seed, static_cast<std::uint64_t>(e), 2u * ib + 1) > thr;
+                    s |= static_cast<std::int64_t>(ii) << ib;
+                    d |= static_cast<std::int64_t>(jj) << ib;
+                }
+                src[e] = s;
+                dst[e] = d;
+            }
+        });
+        // vertex relabelling: Fisher-Yates with hashed draws
+        std::vector<std::int64_t> perm(static_cast<std::size_t>(n));
+        std::iota(perm.begin(), perm.end(), std::int64_t(0));
+        for (std::int64_t i = n - 1; i > 0; --i) {
+            const std::uint64_t h = mix64(mix64(seed ^ 0x5eedull) + static_cast<std::uint64_t>(i));
+            const std::int64_t j = static_cast<std::int64_t>(h % static_cast<std::uint64_t>(i + 1));
+            std::swap(perm[i], perm[j]);
+        }
+        parallel_for(m, [&](std::int64_t lo, std::int64_t hi) {
+            for (std::int64_t e = lo; e < hi; ++e) {
+                src[e] = perm[src[e]];
+                dst[e] = perm[dst[e]];
+            }
+        });
+        std::vector<std::int64_t> outdeg(static_cast<std::size_t>(n), 0);
+        std::fill(row_ptr, row_ptr + n + 1, 0);
+        for (std::int64_t e = 0; e < m; ++e) {
+            ++outdeg[src[e]];
+            ++row_ptr[dst[e] + 1];
+        }
+        for (std::int64_t i = 0; i < n; ++i) row_ptr[i + 1] += row_ptr[i];
+        {  // bucket by destination row (stable), then sort each row's sources
+            std::vector<std::int64_t> fill(row_ptr, row_ptr + n);
+            for (std::int64_t e = 0; e < m; ++e) col_ind[fill[dst[e]]++] = src[e];
+        }
+        parallel_for(n, [&](std::int64_t lo, std::int64_t hi) {
+            for (std::int64_t r = lo; r < hi; ++r) {
+                std::sort(col_ind + row_ptr[r], col_ind + row_ptr[r + 1]);
+                for (std::int64_t j = row_ptr[r]; j < row_ptr[r + 1]; ++j)
+                    val[j] = 1.0 / static_cast<double>(outdeg[col_ind[j]]);
+            }
+        });
+    });
 }

@@ -101,6 +101,20 @@ class CG:
         N.check(N.lib().b200_cg_result(self._h, C.byref(z), C.byref(r)))
         return z.value, r.value
 
+    def start(self, b_ptr: int = 0, stream: int = 0):
+        """x = b (device array; 0 keeps x), z = 0, r = p = b, rho = r.r."""
+        N.check(N.lib().b200_cg_start(self._h, C.c_void_p(b_ptr or None), C.c_void_p(stream)))
+
+    def finish(self, stream: int = 0):
+        """rnorm = |b - A z| (read it with scalars())."""
+        N.check(N.lib().b200_cg_finish(self._h, C.c_void_p(stream)))
+
+    def scalars(self, stream: int = 0):
+        """(rho, rnorm) on the host; synchronises `stream`."""
+        rho, rn = C.c_double(), C.c_double()
+        N.check(N.lib().b200_cg_scalars(self._h, C.c_void_p(stream), C.byref(rho), C.byref(rn)))
+        return rho.value, rn.value
+
     def solve(self, b_ptr: int, iters: int, z_ptr: int = 0) -> float:
         """Plain CG on A z = b from z = 0 for `iters` steps; returns |b - A z|."""
         r = C.c_double()
@@ -181,6 +195,19 @@ class DistCG:
                                                  N.ptr(row_ptr), N.ptr(col_ind), N.ptr(val)))
         return cls(h, world)
 
+    @classmethod
+    def stencil27_nccl(cls, rank, world, nccl_id: bytes, nx, diag=26.1, offdiag=-1.0):
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        N.check(N.lib().b200_dist_cg_create_stencil27_nccl(C.byref(h), rank, world, idbuf, nx, diag, offdiag))
+        return cls(h, world)
+
+    @classmethod
+    def stencil27_local(cls, k, nx, diag=26.1, offdiag=-1.0):
+        h = C.c_void_p()
+        N.check(N.lib().b200_dist_cg_create_stencil27_local(C.byref(h), k, nx, diag, offdiag))
+        return cls(h, k)
+
     @staticmethod
     def nccl_id() -> bytes:
         buf = C.create_string_buffer(128)
@@ -223,12 +250,25 @@ class DistCG:
         """x of this process's shards from host memory (its owned rows)."""
         N.check(N.lib().b200_dist_cg_load_x(self._h, C.c_void_p(x_host_ptr), C.c_void_p(stream)))
 
-    def solve(self, b_ptr: int, iters: int, z_ptr: int = 0) -> float:
-        """Plain CG on A z = b from z = 0 for `iters` steps; returns |b - A z|."""
-        r = C.c_double()
-        N.check(N.lib().b200_cg_solve(self._h, C.c_void_p(b_ptr), int(iters), C.c_void_p(z_ptr or None),
-                                      C.byref(r)))
-        return r.value
+    def start_rowsum(self, stream: int = 0):
+        """x = b = A 1, z = 0, r = p = b (plain CG, the stencil config)."""
+        N.check(N.lib().b200_dist_cg_start_rowsum(self._h, C.c_void_p(stream)))
+
+    def step(self, stream: int = 0):
+        N.check(N.lib().b200_dist_cg_step(self._h, C.c_void_p(stream)))
+
+    def finish(self, stream: int = 0):
+        N.check(N.lib().b200_dist_cg_finish(self._h, C.c_void_p(stream)))
+
+    def scalars(self, stream: int = 0):
+        rho, rn = C.c_double(), C.c_double()
+        N.check(N.lib().b200_dist_cg_scalars(self._h, C.c_void_p(stream), C.byref(rho), C.byref(rn)))
+        return rho.value, rn.value
+
+    def bounds(self):
+        b = np.zeros(self.world + 1, np.int64)
+        N.check(N.lib().b200_dist_cg_bounds(self._h, N.ptr(b)))
+        return b
 
     def npb(self, niter: int, shift: float):
         z, r = C.c_double(), C.c_double()
@@ -252,3 +292,21 @@ class DistCG:
             self.free()
         except Exception:
             pass
+
+
+def shard_footprint(row_ptr, col_ind):
+    """[min col, max col + 1) of a row block's nonzeros (0, 0 when empty)."""
+    lo, hi = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    N.lib().b200_shard_footprint(len(row_ptr) - 1, N.ptr(row_ptr), N.ptr(col_ind), N.ptr(lo), N.ptr(hi))
+    return int(lo[0]), int(hi[0])
+
+
+def send_ranges(bounds, fmin, fmax):
+    """The sharded driver's exchange plan: out[s, r] = [lo, hi) of shard s's
+    slice (slice-relative) that rank r reads."""
+    world = len(bounds) - 1
+    out = np.zeros((world, world, 2), np.int64)
+    N.lib().b200_dist_send_ranges(world, N.ptr(np.ascontiguousarray(bounds, np.int64)),
+                                  N.ptr(np.ascontiguousarray(fmin, np.int64)),
+                                  N.ptr(np.ascontiguousarray(fmax, np.int64)), N.ptr(out.reshape(-1)))
+    return out

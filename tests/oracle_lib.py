@@ -68,6 +68,9 @@ def oracle() -> C.CDLL:
     L.orc_npb_makea.restype = C.c_int
     L.orc_npb_cg.argtypes = [I64, i64p, i64p, f64p, C.c_int, C.c_double, f64p]
     L.orc_npb_cg.restype = C.c_double
+    L.orc_npb_outer.argtypes = [I64, i64p, i64p, f64p, f64p, f64p, f64p, f64p, f64p, C.c_double, C.c_int, f64p]
+    L.orc_npb_outer.restype = C.c_double
+    L.orc_spmv_jds_mt.argtypes = [I64, f64p, i64p, i64p, f64p, i64p, f64p, i64p, C.c_int]
     _oracle = L
     return L
 
@@ -92,6 +95,10 @@ def ref() -> C.CDLL:
     L.ref_call.restype = C.c_int
     L.ref_output.argtypes = [C.c_void_p, f64p]
     L.ref_free.argtypes = [C.c_void_p]
+    L.ref_set_floats.argtypes = [C.c_void_p, C.c_int, f64p, I64]
+    L.ref_set_floats.restype = C.c_int
+    L.ref_scalar.argtypes = [C.c_void_p]
+    L.ref_scalar.restype = C.c_double
     L.ref_last_error.restype = C.c_char_p
     L.ref_infer_interface.argtypes = [C.c_char_p, C.c_char_p, I64]
     L.ref_infer_interface.restype = C.c_int
@@ -202,6 +209,34 @@ def npb_cg(row_ptr, col_ind, val, niter, shift):
     return z, rn[0]
 
 
+class NpbOuter:
+    """NPB outer iterations of the C restatement from a caller-held x (x = 1
+    initially), SpMV on `nthreads` host threads (0 = all): the native CPU
+    baseline of bench.py and the zeta checker of its e2e leg."""
+
+    def __init__(self, row_ptr, col_ind, val, shift, nthreads=0):
+        self.rp, self.ci, self.val, self.shift, self.nthreads = row_ptr, col_ind, val, shift, nthreads
+        n = len(row_ptr) - 1
+        self.n = n
+        self.x = np.ones(n)
+        self.work = [np.zeros(n) for _ in range(4)]
+
+    def step(self):
+        rn = np.zeros(1)
+        z, p, q, r = self.work
+        zeta = oracle().orc_npb_outer(self.n, ptr(self.rp), ptr(self.ci), ptr(self.val), ptr(self.x), ptr(z),
+                                      ptr(p), ptr(q), ptr(r), self.shift, self.nthreads, ptr(rn))
+        return zeta, rn[0]
+
+
+def spmv_jds_mt(nzcnt, perm, val, jd_ptr, x, col_ind, nthreads=0):
+    rows = len(perm)
+    y = np.zeros(rows, dtype=np.float64)
+    oracle().orc_spmv_jds_mt(rows, ptr(y), ptr(nzcnt), ptr(perm), ptr(val), ptr(jd_ptr), ptr(x), ptr(col_ind),
+                             nthreads)
+    return y
+
+
 def fnv1a(b: bytes) -> int:
     buf = C.create_string_buffer(b, len(b))
     return oracle().orc_fnv1a(buf, len(b))
@@ -253,3 +288,159 @@ def same_bits(a: np.ndarray, b: np.ndarray) -> bool:
     a = np.ascontiguousarray(a, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+# --------------------------------------------------------------------------
+# the reference's own CPU harness driven by a host loop (bench.py's reference
+# arm and the class A zeta test): stock "lilac.spmv_csr" / "lilac.spmv_jds" /
+# "lilac.dotproduct" HarnessFns (interp.cpp:330-389), one prepared call per
+# host thread on an nnz-balanced slice, run concurrently (ctypes releases the
+# GIL; the interpreter has no shared mutable state)
+# --------------------------------------------------------------------------
+
+def host_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def _run_parallel(fns):
+    import threading
+    if len(fns) == 1:
+        fns[0]()
+        return
+    th = [threading.Thread(target=f) for f in fns]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+
+
+class RefCsr:
+    """y = A x through `lilac.spmv_csr`, rows cut into T nnz-balanced slices."""
+
+    def __init__(self, row_ptr, col_ind, val, ncols, threads=None, rows=None):
+        R = ref()
+        self.R = R
+        self.rows = len(row_ptr) - 1 if rows is None else rows
+        T = max(1, min(threads or host_threads(), max(1, self.rows)))
+        rp = row_ptr
+        nnz = int(rp[self.rows] - rp[0])
+        b = [0]
+        for t in range(1, T):
+            b.append(max(b[-1], int(np.searchsorted(rp[: self.rows + 1], rp[0] + nnz * t // T))))
+        b.append(self.rows)
+        self.bounds = b
+        self.ncols = ncols
+        self.h = []
+        x0 = np.zeros(max(ncols, 1))
+        for t in range(T):
+            r0, r1 = b[t], b[t + 1]
+            a, e = int(rp[r0]), int(rp[r1])
+            rpt = np.ascontiguousarray(rp[r0:r1 + 1] - rp[r0])
+            cit = np.ascontiguousarray(col_ind[a:e])
+            vt = np.ascontiguousarray(val[a:e])
+            self.h.append(R.ref_prepare_csr(r1 - r0, ptr(rpt), ptr(vt), ptr(x0), ptr(cit), e - a, ncols))
+
+    def __call__(self, x, y):
+        R = self.R
+
+        def job(t):
+            def f():
+                R.ref_set_floats(self.h[t], 4, ptr(x), self.ncols)
+                if R.ref_call(self.h[t]) != 0:
+                    raise IndexError(R.ref_last_error().decode())
+                R.ref_output(self.h[t], ptr(y[self.bounds[t]:self.bounds[t + 1]]))
+            return f
+        _run_parallel([job(t) for t in range(len(self.h))])
+        return y
+
+    def free(self):
+        for h in self.h:
+            self.R.ref_free(h)
+        self.h = []
+
+
+class RefDot:
+    """a . b through `lilac.dotproduct` on T element slices; the slice partials
+    are summed in slice order."""
+
+    def __init__(self, n, threads=None):
+        R = ref()
+        self.R = R
+        T = max(1, min(threads or host_threads(), max(1, n // 4096)))
+        self.bounds = [n * t // T for t in range(T + 1)]
+        z = np.zeros(max(n, 1))
+        self.h = [R.ref_prepare_dot(self.bounds[t + 1] - self.bounds[t], ptr(z), ptr(z)) for t in range(T)]
+
+    def __call__(self, a, b):
+        R = self.R
+        out = [0.0] * len(self.h)
+
+        def job(t):
+            def f():
+                lo, hi = self.bounds[t], self.bounds[t + 1]
+                R.ref_set_floats(self.h[t], 1, ptr(a[lo:hi]), hi - lo)
+                R.ref_set_floats(self.h[t], 2, ptr(b[lo:hi]), hi - lo)
+                R.ref_call(self.h[t])
+                out[t] = R.ref_scalar(self.h[t])
+            return f
+        _run_parallel([job(t) for t in range(len(self.h))])
+        s = 0.0
+        for v in out:
+            s += v
+        return s
+
+    def free(self):
+        for h in self.h:
+            self.R.ref_free(h)
+        self.h = []
+
+
+class RefNpbCG:
+    """NPB CG outer iterations whose SpMVs and dot products are the reference's
+    HarnessFns (RefCsr / RefDot) and whose vector updates are host loops
+    (numpy): a LiLAC-rewritten NPB CG linked against the reference CPU harness
+    (SURVEY §8(d) input 1). x starts at 1."""
+
+    def __init__(self, row_ptr, col_ind, val, shift, threads=None):
+        n = len(row_ptr) - 1
+        self.n, self.shift = n, shift
+        self.spmv = RefCsr(row_ptr, col_ind, val, n, threads)
+        self.dot = RefDot(n, threads)
+        self.x = np.ones(n)
+        self.z, self.p, self.q, self.r = (np.zeros(n) for _ in range(4))
+        self.spmvs = self.dots = 0
+
+    def step(self, cgitmax=25):
+        x, z, p, q, r = self.x, self.z, self.p, self.q, self.r
+        z[:] = 0.0
+        q[:] = 0.0
+        r[:] = x
+        p[:] = r
+        rho = self.dot(r, r)
+        for _ in range(cgitmax):
+            self.spmv(p, q)
+            d = self.dot(p, q)
+            alpha = rho / d
+            rho0 = rho
+            z += alpha * p
+            r -= alpha * q
+            rho = self.dot(r, r)
+            beta = rho / rho0
+            p *= beta
+            p += r
+        self.spmv(z, r)
+        res = x - r
+        rnorm = float(np.sqrt(self.dot(res, res)))
+        t1 = self.dot(x, z)
+        t2 = 1.0 / np.sqrt(self.dot(z, z))
+        x[:] = t2 * z
+        self.spmvs += cgitmax + 1
+        self.dots += 2 * cgitmax + 4
+        return self.shift + 1.0 / t1, rnorm
+
+    def free(self):
+        self.spmv.free()
+        self.dot.free()

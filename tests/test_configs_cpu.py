@@ -1,4 +1,4 @@
-"""CPU checks of the benchmark input synthesis (tools/bench_configs.py):
+"""CPU checks of the benchmark input synthesis (paper_2001_07938_b200/workloads.py):
 the JDS encoder equals the oracle's jds_from_dense contract bit-for-bit, and
 the stencil/Kronecker generators produce the named shapes."""
 import os
@@ -8,8 +8,7 @@ import numpy as np
 
 import oracle_lib as O
 
-sys.path.insert(0, os.path.join(O.ROOT, "tools"))
-import bench_configs as B  # noqa: E402
+from paper_2001_07938_b200 import workloads as B  # noqa: E402
 
 
 def test_parboil_shape_and_jds_encoder_bit_exact():
@@ -40,3 +39,47 @@ def test_kronecker_column_stochastic():
     colsum = np.bincount(ci, weights=val, minlength=n)
     nz = np.bincount(ci, minlength=n) > 0
     assert np.allclose(colsum[nz], 1.0)
+
+
+def test_stencil_rows_match_whole_and_rowsum():
+    nx = 7
+    rp, ci, val = B.gen_stencil27(nx)
+    r0, r1 = 50, 200
+    srp, sci, sval = B.gen_stencil27_rows(nx, r0, r1)
+    assert np.array_equal(srp, rp[r0:r1 + 1] - rp[r0])
+    assert np.array_equal(sci, ci[rp[r0]:rp[r1]]) and np.array_equal(sval, val[rp[r0]:rp[r1]])
+    y = O.spmv_csr(rp, ci, val, np.ones(nx ** 3))
+    assert np.array_equal(B.stencil27_rowsum(nx, r0, r1), y[r0:r1])
+    assert B.stencil27_nnz(nx) == rp[-1]
+
+
+def test_jds_slices_reproduce_whole_bitwise():
+    rp, ci, val = B.gen_parboil(n=5000, nnz_target=50_000)
+    perm, nzcnt, jd_ptr, jval, jcol = B.csr_to_jds(rp, ci, val)
+    x = np.random.default_rng(3).uniform(-1, 1, 5000)
+    whole = O.spmv_jds(nzcnt, perm, jval, jd_ptr, x, jcol)
+    out = np.full(5000, np.nan)
+    for j0, j1 in ((0, 1234), (1234, 1235), (1235, 5000)):
+        snz, sperm, sv, sptr, sc, orig = B.jds_slice(nzcnt, perm, jval, jd_ptr, jcol, j0, j1)
+        out[orig] = O.spmv_jds(snz, sperm, sv, sptr, x, sc)
+    assert O.same_bits(out, whole)
+    assert O.same_bits(O.spmv_jds_mt(nzcnt, perm, jval, jd_ptr, x, jcol, 4), whole)
+
+
+def test_native_npb_outer_matches_benchmark_loop():
+    rp, ci, val = O.npb_makea(1400, 7, 10.0)
+    ref_zeta, ref_rn = O.npb_cg(rp, ci, val, 15, 10.0)
+    it = O.NpbOuter(rp, ci, val, 10.0, nthreads=3)
+    it.step()
+    it.x[:] = 1.0
+    for _ in range(15):
+        zeta, rn = it.step()
+    assert zeta == ref_zeta and rn == ref_rn
+
+
+def test_kronecker_native_matches_restatement():
+    for scale in (5, 8):
+        got = B.gen_kronecker(scale)
+        want = B.gen_kronecker_reference(scale)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)

@@ -242,7 +242,7 @@ def test_fused_cg_matches_per_step_kernels():
     import sys
     import os
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
-    from bench_configs import gen_stencil27
+    from paper_2001_07938_b200.workloads import gen_stencil27
     nx = 85  # 614,125 rows > 148 x 4096
     rp, ci, val = gen_stencil27(nx)
     n = nx ** 3
@@ -629,7 +629,7 @@ def _stencil27_host(nx):
     import sys
     import os
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
-    from bench_configs import gen_stencil27
+    from paper_2001_07938_b200.workloads import gen_stencil27
     return gen_stencil27(nx)
 
 

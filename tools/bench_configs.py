@@ -64,92 +64,8 @@ def report(name, A, n_in, reps, stream, extra=None, bytes_fn=csr_bytes):
     return line
 
 
-# ---- generators -------------------------------------------------
-
-def gen_parboil(seed=20240817, n=146_000, nnz_target=1_500_000):
-    rng = np.random.default_rng(seed)
-    mean = nnz_target / n
-    lens = np.clip(np.round(rng.lognormal(np.log(mean) - 0.18, 0.6, n)), 1, 64).astype(np.int64)
-    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    band = n // 8
-    rows = np.repeat(np.arange(n), lens)
-    ci = np.clip(rows + rng.integers(-band, band + 1, rp[-1]), 0, n - 1)
-    # ascending columns per row (duplicates allowed, summed by the math)
-    order = np.lexsort((ci, rows))
-    ci = ci[order].astype(np.int64)
-    val = rng.uniform(-2, 2, rp[-1])
-    val[val == 0] = 1.0
-    return rp, ci, val
-
-
-def csr_to_jds(rp, ci, val):
-    """jds_from_dense contract (oracles.hpp:109-144) from CSR: stable sort of
-    rows by nonzero count descending; perm[orig] = jagged; diagonals."""
-    n = len(rp) - 1
-    lens = np.diff(rp)
-    order = np.argsort(-lens, kind="stable")
-    perm = np.empty(n, np.int64)
-    perm[order] = np.arange(n)
-    nzcnt = lens[order].astype(np.int64)
-    max_nz = int(nzcnt[0]) if n else 0
-    counts = np.array([(nzcnt > k).sum() for k in range(max_nz)], np.int64)
-    jd_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    jval = np.empty(rp[-1], np.float64)
-    jcol = np.empty(rp[-1], np.int64)
-    starts = rp[order]
-    for k in range(max_nz):
-        m = counts[k]
-        src = starts[:m] + k
-        jval[jd_ptr[k]:jd_ptr[k + 1]] = val[src]
-        jcol[jd_ptr[k]:jd_ptr[k + 1]] = ci[src]
-    return perm, nzcnt, jd_ptr, jval, jcol
-
-
-def gen_kronecker(scale, edgefactor=16, seed=1, a=0.57, b=0.19, c=0.19):
-    """Graph500 Kronecker edge list -> CSR of the transposed, column-stochastic
-    adjacency (PageRank operator): row = dst, col = src, val = 1/outdeg(src)."""
-    rng = np.random.default_rng(seed)
-    n = 1 << scale
-    m = edgefactor * n
-    src = np.zeros(m, np.int64)
-    dst = np.zeros(m, np.int64)
-    ab = a + b
-    c_norm = c / (1 - ab)
-    a_norm = a / ab
-    for ib in range(scale):
-        r1 = rng.random(m)
-        r2 = rng.random(m)
-        ii = (r1 > ab).astype(np.int64)
-        jj = (r2 > (c_norm * ii + a_norm * (1 - ii))).astype(np.int64)
-        src += ii << ib
-        dst += jj << ib
-    # Graph500 permutes vertex labels
-    p = rng.permutation(n)
-    src, dst = p[src], p[dst]
-    outdeg = np.bincount(src, minlength=n).astype(np.float64)
-    order = np.lexsort((src, dst))
-    src, dst = src[order], dst[order]
-    rp = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
-    val = 1.0 / outdeg[src]
-    return rp, src.astype(np.int64), val
-
-
-def gen_stencil27(nx):
-    """27-point stencil on an nx^3 grid: diag 26.1, off-diag -1 (SPD)."""
-    n = nx ** 3
-    idx = np.arange(n, dtype=np.int64)
-    i, j, k = idx // (nx * nx), (idx // nx) % nx, idx % nx
-    offs = [(di, dj, dk) for di in (-1, 0, 1) for dj in (-1, 0, 1) for dk in (-1, 0, 1)]
-    valid = []
-    for di, dj, dk in offs:
-        valid.append((i + di >= 0) & (i + di < nx) & (j + dj >= 0) & (j + dj < nx) & (k + dk >= 0) & (k + dk < nx))
-    V = np.stack(valid, axis=1)  # n x 27, offsets in increasing linear order
-    lens = V.sum(axis=1)
-    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    lin = np.array([di * nx * nx + dj * nx + dk for di, dj, dk in offs], np.int64)
-    cols = (idx[:, None] + lin[None, :])[V]
-    vals = np.where(lin[None, :] == 0, 26.1, -1.0) * np.ones((n, 27))
-    return rp, cols.astype(np.int64), vals[V]
+from paper_2001_07938_b200.workloads import (csr_to_jds, gen_kronecker, gen_parboil,  # noqa: E402,F401
+                                              gen_stencil27)
 
 
 def main():

@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import oracle_lib as O  # noqa: E402
-from bench_configs import gen_stencil27  # noqa: E402
+from paper_2001_07938_b200.workloads import gen_stencil27  # noqa: E402
 from paper_2001_07938_b200 import _native as N  # noqa: E402
 from paper_2001_07938_b200 import device as D  # noqa: E402
 from paper_2001_07938_b200 import harness as H  # noqa: E402
