@@ -1,0 +1,256 @@
+"""GPU parity at the BASELINE.json config shapes (B200 only), through the C ABI.
+
+* Parboil-shape JDS (n=146000, nnz~1.5M): b200_spmv_jds bit-identical to the
+  oracle restatement and to the reference's own lilac.spmv_jds HarnessFn
+  (oracle/_ref) on the whole matrix.
+* Kronecker scale 22 (skewed rows, a 160k-nonzero row): the split and
+  merge-path kernels within 1e-12 * sum|a x| per row of the oracle; 20
+  PageRank steps on the device against the same iteration on the host.
+* 27-point stencil N=420 (2e9 nonzeros, generated in HBM): sampled row
+  blocks of A x against the oracle on host-generated rows; CG's true
+  residual against the recurrence.
+* NPB class C: the tiled SpMV element-wise against the reference HarnessFn
+  (lilac.spmv_csr) and the oracle; the native generator bit-identical to the
+  oracle's makea.
+* The sharded stencil driver (k local shards): same partition as
+  b200_partition_rows, same CG residual as one GPU.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2001_07938_b200 import _native as N
+from paper_2001_07938_b200 import device as D
+from paper_2001_07938_b200 import harness as H
+from paper_2001_07938_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(autouse=True)
+def _mode():
+    H.set_errors_return(True)
+    N.lib().b200_set_kernel(b"auto")
+    yield
+    N.lib().b200_set_kernel(b"auto")
+
+
+def within(y, ref, bound, tol=TOL):
+    err = np.abs(y - ref)
+    bad = err > tol * bound
+    assert not bad.any(), f"{bad.sum()} rows exceed; worst {np.max(err / np.maximum(bound, 1e-300))}"
+
+
+# ---- Parboil JDS -------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def parboil():
+    rp, ci, val = W.gen_parboil()
+    return (rp, ci, val) + W.csr_to_jds(rp, ci, val)
+
+
+def test_parboil_jds_bit_exact_oracle_and_reference(parboil):
+    rp, ci, val, perm, nzcnt, jd_ptr, jval, jcol = parboil
+    n = len(perm)
+    assert n == 146_000 and abs(len(jval) - 1_500_000) < 30_000
+    x = np.random.default_rng(146).uniform(-2, 2, n)
+    y = np.full(n, np.nan)
+    H.spmv_jds(n, y, nzcnt, perm, jval, jd_ptr, x, jcol)
+    ref = O.spmv_jds(nzcnt, perm, jval, jd_ptr, x, jcol)
+    assert O.same_bits(y, ref)
+    if O.ref_available():
+        R = O.ref()
+        h = R.ref_prepare_jds(n, O.ptr(nzcnt), O.ptr(perm), O.ptr(jval), O.ptr(jd_ptr), O.ptr(x), O.ptr(jcol),
+                              len(jval), len(jd_ptr), n)
+        assert R.ref_call(h) == 0
+        yr = np.zeros(n)
+        R.ref_output(h, O.ptr(yr))
+        R.ref_free(h)
+        assert O.same_bits(y, yr)
+
+
+def test_parboil_jds_device_api_and_repeat(parboil):
+    import torch
+    rp, ci, val, perm, nzcnt, jd_ptr, jval, jcol = parboil
+    n = len(perm)
+    A = D.Matrix.jds(nzcnt, perm, jval, jd_ptr, jcol)
+    try:
+        xs = [np.random.default_rng(s).uniform(-1, 1, n) for s in (1, 2)]
+        for xh in xs:
+            x = torch.from_numpy(xh).cuda()
+            y = torch.empty(n, dtype=torch.float64, device="cuda")
+            A.spmv(x.data_ptr(), y.data_ptr())
+            torch.cuda.synchronize()
+            assert O.same_bits(y.cpu().numpy(), O.spmv_jds(nzcnt, perm, jval, jd_ptr, xh, jcol))
+    finally:
+        A.free()
+
+
+# ---- Kronecker scale 22 ---------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def kron():
+    return W.gen_kronecker(22)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "split", "merge"])
+def test_kron22_spmv_within_tolerance(kron, kernel):
+    import torch
+    rp, ci, val = kron
+    n = len(rp) - 1
+    N.lib().b200_set_kernel(kernel.encode())
+    A = D.Matrix.csr(rp, ci, val)
+    try:
+        info = A.info()
+        if kernel == "auto":
+            assert info["kernel"] == 5, "skewed rows take the split plan"
+        xh = np.random.default_rng(22).uniform(0, 1, n)
+        x = torch.from_numpy(xh).cuda()
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        A.spmv(x.data_ptr(), y.data_ptr())
+        A.spmv(x.data_ptr(), y.data_ptr())  # counters / fix-up state reset between calls
+        torch.cuda.synchronize()
+        ref = O.spmv_csr_mt(rp, ci, val, xh, 0)
+        bound = O.spmv_csr_mt(rp, ci, np.abs(val), np.abs(xh), 0)
+        within(y.cpu().numpy(), ref, bound)
+    finally:
+        A.free()
+
+
+def test_kron22_pagerank_20_steps(kron):
+    import torch
+    rp, ci, val = kron
+    n = len(rp) - 1
+    A = D.Matrix.csr(rp, ci, val)
+    try:
+        x = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+        w = torch.empty_like(x)
+        A.pagerank(0.85, 20, x.data_ptr(), w.data_ptr())
+        torch.cuda.synchronize()
+        xc = np.full(n, 1.0 / n)
+        for _ in range(20):
+            yc = O.spmv_csr_mt(rp, ci, val, xc, 0)
+            xc = 0.85 * yc + 0.15 / n
+        xd = x.cpu().numpy()
+        # a contraction: each step's SpMV error <= 1e-12 sum|a x| stays bounded
+        assert np.max(np.abs(xd - xc) / np.abs(xc)) <= 1e-10
+        assert abs(xd.sum() - xc.sum()) <= 1e-10 * xc.sum()
+    finally:
+        A.free()
+
+
+def test_kron22_harness_entry(kron):
+    rp, ci, val = kron
+    n = len(rp) - 1
+    x = np.random.default_rng(5).uniform(0, 1, n)
+    y = np.full(n, np.nan)
+    H.spmv_csr(n, y, rp, val, x, ci)
+    ref = O.spmv_csr_mt(rp, ci, val, x, 0)
+    bound = O.spmv_csr_mt(rp, ci, np.abs(val), np.abs(x), 0)
+    within(y, ref, bound)
+
+
+# ---- 27-point stencil N=420 --------------------------------------------------------------
+
+def test_stencil420_sampled_rows_and_cg():
+    import torch
+    nx = 420
+    n = nx ** 3
+    A = D.Matrix.stencil27(nx)
+    try:
+        info = A.info()
+        assert info["rows"] == n and info["nnz"] == 1_990_865_512
+        g = torch.Generator("cuda").manual_seed(420)
+        x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+        y = torch.empty_like(x)
+        A.spmv(x.data_ptr(), y.data_ptr())
+        torch.cuda.synchronize()
+        xh = x.cpu().numpy()
+        for r0, r1 in ((0, 200_000), (n // 2 - 100_000, n // 2 + 100_000), (n - 200_000, n)):
+            srp, sci, sval = W.gen_stencil27_rows(nx, r0, r1)
+            ref = O.spmv_csr_mt(srp, sci, sval, xh, 0)
+            bound = O.spmv_csr_mt(srp, sci, np.abs(sval), np.abs(xh), 0)
+            within(y[r0:r1].cpu().numpy(), ref, bound)
+        del x, y
+        # CG on A z = A 1: the true residual agrees with the recurrence
+        cg = D.CG(A)
+        b = torch.from_numpy(W.stencil27_rowsum(nx, 0, n)).cuda()
+        cg.start(b.data_ptr())
+        for _ in range(20):
+            cg.step()
+        cg.finish()
+        rho, rnorm = cg.scalars()
+        bn = float(torch.linalg.norm(b).item())
+        assert rnorm / bn < 1e-2
+        assert abs(rnorm - np.sqrt(rho)) <= 1e-8 * bn
+        cg.free()
+    finally:
+        A.free()
+
+
+# ---- NPB class C ----------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def npb_c():
+    return D.gen_npb(150000, 15, 110.0)
+
+
+def test_npb_c_generator_bit_exact(npb_c):
+    want = O.npb_makea(150000, 15, 110.0)
+    for g, w in zip(npb_c, want):
+        assert np.array_equal(g, w)
+
+
+def test_npb_c_tiled_elementwise_vs_reference_harness(npb_c):
+    rp, ci, val = npb_c
+    n = 150000
+    x = np.random.default_rng(150).uniform(-1, 1, n)
+    y = np.full(n, np.nan)
+    H.spmv_csr(n, y, rp, val, x, ci)
+    ref = O.spmv_csr_mt(rp, ci, val, x, 0)
+    bound = O.spmv_csr_mt(rp, ci, np.abs(val), np.abs(x), 0)
+    within(y, ref, bound)
+    if O.ref_available():
+        A = O.RefCsr(rp, ci, val, n)
+        yr = np.zeros(n)
+        A(x, yr)
+        A.free()
+        assert O.same_bits(yr, ref)  # the reference harness and the oracle agree bitwise
+        within(y, yr, bound)
+    # the tiled layout is what ran
+    M = D.Matrix.csr(rp, ci, val)
+    assert M.info()["kernel"] == 4
+    M.free()
+
+
+# ---- sharded stencil (k local shards on this GPU) ------------------------------------------
+
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_sharded_stencil_matches_single(k):
+    import torch
+    nx = 40
+    n = nx ** 3
+    rp, ci, val = W.gen_stencil27(nx)
+    d = D.DistCG.stencil27_local(k, nx)
+    try:
+        assert np.array_equal(d.bounds(), D.partition_rows(rp, k))
+        d.start_rowsum()
+        for _ in range(15):
+            d.step()
+        d.finish()
+        rho_k, rn_k = d.scalars()
+    finally:
+        d.free()
+    A = D.Matrix.stencil27(nx)
+    cg = D.CG(A)
+    b = torch.from_numpy(W.stencil27_rowsum(nx, 0, n)).cuda()
+    cg.start(b.data_ptr())
+    for _ in range(15):
+        cg.step()
+    cg.finish()
+    rho1, rn1 = cg.scalars()
+    cg.free()
+    A.free()
+    bn = float(torch.linalg.norm(b).item())
+    assert abs(rn_k - rn1) <= 1e-10 * bn and abs(rho_k - rho1) <= 1e-10 * bn * bn

@@ -136,3 +136,22 @@ def test_oracle_gemm_matches_reference_harness_golden():
         g = c["gemm"]
         out = O.gemm(g["n"], g["m"], g["p"], np.array(g["a"], np.float64), np.array(g["b"], np.float64))
         assert O.same_bits(out, np.array(g["c"], np.float64))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_npb_class_a_zeta_through_reference_harness():
+    """SURVEY §8(d) input 1: NPB CG class A whose SpMVs and dot products are
+    the reference's own lilac.spmv_csr / lilac.dotproduct HarnessFns
+    (interp.cpp:330-389, oracle/_ref), host vector updates; zeta verified to
+    NPB's 1e-10 (warm-up iteration + 15, ~40 s on 8 threads)."""
+    rp, ci, val = O.npb_makea(14000, 11, 20.0)
+    cg = O.RefNpbCG(rp, ci, val, 20.0)
+    try:
+        cg.step()
+        cg.x[:] = 1.0
+        for _ in range(15):
+            zeta, rnorm = cg.step()
+    finally:
+        cg.free()
+    assert abs(zeta - 17.130235054029) / 17.130235054029 <= 1e-10
+    assert cg.spmvs == 16 * 26
