@@ -442,7 +442,7 @@ def run_reference(args):
         def one():
             spmv()
             np.multiply(y, DAMPING, out=x)
-            x += (1.0 - DAMPING) / n
+            np.add(x, (1.0 - DAMPING) / n, out=x)
         one()  # a warm-up step (the interpreter has nothing to warm beyond one call)
         steps = []
         for _ in range(args.steps):
@@ -477,11 +477,11 @@ def run_reference(args):
 
         def vec_ops():  # CG vector work of one iteration on the same row sample: 2 dots + 3 axpy-type updates
             float(a @ b)
-            a += 0.5 * b
-            b -= 0.5 * c
+            np.add(a, 0.5 * b, out=a)
+            np.subtract(b, 0.5 * c, out=b)
             float(b @ b)
-            c *= 0.5
-            c += b
+            np.multiply(c, 0.5, out=c)
+            np.add(c, b, out=c)
         spmv()
         vec_ops()
         steps = []
