@@ -258,7 +258,8 @@ def csr_bytes(info):
     return info["nnz"] * (8 + info["col_bytes"]) + 8 * (info["rows"] + 1) + 8 * info["rows"] + 8 * info["cols"]
 
 
-KERNEL_NAMES = {1: "k_csr_vector", 2: "k_spmv_merge", 3: "k_csr_exact", 4: "k_spmv_tiled", 5: "k_csr_split"}
+KERNEL_NAMES = {1: "k_csr_vector", 2: "k_spmv_merge", 3: "k_csr_exact", 4: "k_spmv_tiled", 5: "k_csr_split",
+                6: "k_spmv_lrc"}
 
 
 def base_line(args, config, world, value, ms_step, extra_cfg=None):
@@ -993,7 +994,7 @@ def run_kron(ctx):
                     "bytes_per_call": by, "kernel": kname, "max_row": info["max_row"]}
     line["roofline"] = roofline(by, spmv_ms, kname, "CSR algorithmic bytes per launch / mean of back-to-back launches "
                                 "(CUDA events, bench stream)", "kron")
-    line["gpu_launches"] = args.steps * 3  # work-counter reset, split SpMV, update
+    line["gpu_launches"] = args.steps * {6: 4, 5: 3}.get(info["kernel"], 2)  # (+ hot gather, fix-up | counter reset), update
     line["clocks"] = clk
     line["marshal_first_call"] = {"s": t_marshal, "h2d_bytes": int(nnz * 16 + (n + 1) * 8),
                                   "device_bytes": info["device_bytes"]}

@@ -142,12 +142,13 @@ def build_cpp_tests(force: bool = False, verbose: bool = False):
     if force or _stale(out, deps):
         _run(["g++", "-std=c++17", "-O1", "-g", f"-I{INCLUDE}", "-o", out, src,
               os.path.join(CSRC, "marshal.cpp"), "-lpthread"], verbose)
-    # tests/cpp/test_tcsr: the tiled layout builder replayed on the CPU
-    src = os.path.join(ROOT, "tests", "cpp", "test_tcsr.cpp")
-    out = os.path.join(ROOT, "tests", "cpp", "test_tcsr")
-    if os.path.exists(src) and (force or _stale(out, [src, LIB] + _headers())):
-        _run(["g++", "-std=c++17", "-O2", f"-I{INCLUDE}", f"-I{CSRC}", f"-I{CUDA_HOME}/include", "-o", out, src,
-              f"-L{PKG}", "-llilac_b200", "-Wl,-rpath,$ORIGIN/../../paper_2001_07938_b200", "-lpthread"], verbose)
+    # tests/cpp/test_tcsr, test_lrc: the tiled / lane-range layout builders replayed on the CPU
+    for name in ("test_tcsr", "test_lrc"):
+        src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+        out = os.path.join(ROOT, "tests", "cpp", name)
+        if os.path.exists(src) and (force or _stale(out, [src, LIB] + _headers())):
+            _run(["g++", "-std=c++17", "-O2", f"-I{INCLUDE}", f"-I{CSRC}", f"-I{CUDA_HOME}/include", "-o", out, src,
+                  f"-L{PKG}", "-llilac_b200", "-Wl,-rpath,$ORIGIN/../../paper_2001_07938_b200", "-lpthread"], verbose)
 
 
 def clean():

@@ -82,7 +82,7 @@ void device_quiesce();
 // Resident sparse matrices (device layout)
 // ---------------------------------------------------------------------------
 
-enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3, Tiled = 4, Split = 5 };
+enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3, Tiled = 4, Split = 5, Lane = 6 };
 const char* csr_kernel_name(CsrKernel k);
 CsrKernel parse_csr_kernel(const std::string& s);
 
@@ -162,6 +162,51 @@ struct SplitDev {
     unsigned long long* work = nullptr;       // work-unit counter (zeroed before each launch)
 };
 
+// Lane-range CSR (upload-time cached invariant, lrcsr_build.cpp; kernel in
+// lrcsr.cu) for matrices whose x gathers must go to global memory (skewed
+// graphs): the nonzeros, in CSR order with empty rows compacted away, are cut
+// into units of kLrcUnit = 32 lanes x kLrcChunks chunks x 4; lane l of a unit
+// owns a contiguous range of 4 kLrcChunks nonzeros and chunk i of lane l is
+// stored at unit offset (32 i + l) * 4, so each warp-wide chunk load is a
+// contiguous 1 KB (val) + 512 B (col) burst, independent of row lengths (no
+// row_ptr -> col -> x dependence chain, no per-row imbalance). col is a u32:
+// bit 31 = a row starts here, bit 30 = the column is one of the `hot` most
+// frequent columns and the low bits are its slot in a shared-memory copy of
+// their x values (the gathers that would dominate the L1TEX queue become
+// LDS), else the global column. A lane descriptor holds the compact row of its
+// first nonzero | kLrcCont when that row began before the lane. Rows complete
+// inside a unit are stored directly; the row in progress at each unit's start
+// and end goes to a per-unit carry, summed in unit order by a fix-up pass
+// (deterministic). HBM: 12 bytes per nonzero + 4 per 4 kLrcChunks nonzeros.
+constexpr int kLrcChunks = 8;
+constexpr int kLrcLaneNnz = 4 * kLrcChunks;
+constexpr int kLrcUnit = 32 * kLrcLaneNnz;
+constexpr std::uint32_t kLrcStart = 1u << 31;
+constexpr std::uint32_t kLrcHot = 1u << 30;
+constexpr std::uint32_t kLrcColMask = kLrcHot - 1u;
+constexpr std::uint32_t kLrcCont = 1u << 31;
+constexpr int kLrcHotMax = 27 * 1024 - 1;  // + the zero cell: 216 KB of shared memory
+struct LrcCarry {
+    std::int32_t head_row;  // compact row in progress at the unit's start, -1 none
+    std::int32_t tail_row;  // row begun in the unit and still open at its end, -1 none
+    std::int32_t split;     // some row begins inside the unit
+    std::int32_t pad;
+    double head_val, tail_val;
+};
+struct LrcDev {
+    std::int64_t units = 0, nnz = 0;
+    std::int64_t rows_c = 0;                  // nonempty rows
+    int hot = 0;                              // hot columns (slot `hot` is a zero cell)
+    bool has_empty = false;                   // some rows are empty: y is zeroed first
+    const double* val = nullptr;              // units * kLrcUnit
+    const std::uint32_t* col = nullptr;       // units * kLrcUnit
+    const std::uint32_t* desc = nullptr;      // units * 32
+    const std::int32_t* rmap = nullptr;       // rows_c: compact -> original row (null: identity)
+    const std::int32_t* hot_cols = nullptr;   // hot
+    double* x_hot = nullptr;                  // hot + 1, gathered per call
+    LrcCarry* carry = nullptr;                // units
+};
+
 struct CsrDev {
     std::int64_t rows = 0;      // number of rows computed
     std::int64_t nnz = 0;       // extent of val/col (row_ptr[rows] for the ABI)
@@ -175,6 +220,7 @@ struct CsrDev {
     const TcsrDev* tiled = nullptr;         // present when the tiled layout was built
     const MergeDev* merge = nullptr;        // present when the merge plan was built
     const SplitDev* split = nullptr;        // present when the split plan was built
+    const LrcDev* lrc = nullptr;            // present when the lane-range layout was built
 };
 
 struct JdsDev {
@@ -208,6 +254,8 @@ void launch_merge_plan(const std::int64_t* row_ptr, std::int64_t rows, std::int6
 void launch_spmv_merge(const CsrDev& A, const double* x, double* y, cudaStream_t s);
 // Split kernel (kernels.cu): vector rows + warp-per-chunk long rows in one launch.
 void launch_spmv_split(const CsrDev& A, const double* x, double* y, cudaStream_t s);
+// y = A x on the lane-range layout (lrcsr.cu): hot-x gather, main kernel, carry fix-up.
+void launch_spmv_lrc(const LrcDev& L, std::int64_t rows, const double* x, double* y, cudaStream_t s);
 // p.q of a finished SpMV into the CG scalars (alpha, or the shard partial).
 void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, double* partials, unsigned int* ticket,
                            CgScalars* sc, cudaStream_t s);

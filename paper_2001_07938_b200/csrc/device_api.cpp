@@ -22,6 +22,7 @@ struct b200_matrix {
     TcsrOwner tiled;
     MergeOwner merge;
     SplitOwner split;
+    LrcOwner lrc;
     std::int64_t max_row = 0;
 };
 
@@ -67,8 +68,10 @@ int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int6
         d.monotone = monotone;
         A->max_row = max_row;
         if (A->tiled.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel)) d.tiled = &A->tiled.dev;
-        if (!d.tiled && A->split.refresh(d, row_ptr, rt().kernel)) d.split = &A->split.dev;
-        if (!d.tiled && A->merge.refresh(d, row_ptr, rt().kernel)) d.merge = &A->merge.dev;
+        if (!d.tiled && A->lrc.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel))
+            d.lrc = &A->lrc.dev;
+        if (!d.tiled && !d.lrc && A->split.refresh(d, row_ptr, rt().kernel)) d.split = &A->split.dev;
+        if (!d.tiled && !d.lrc && A->merge.refresh(d, row_ptr, rt().kernel)) d.merge = &A->merge.dev;
         *out = A.release();
     });
 }
@@ -154,6 +157,7 @@ void b200_matrix_free(b200_matrix* A) {
     A->tiled.release();
     A->merge.release();
     A->split.release();
+    A->lrc.release();
     delete A;
 }
 
@@ -169,7 +173,9 @@ int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
             info->nnz = A->csr.nnz;
             info->kernel = static_cast<int32_t>(matrix_kernel(A));
             // column index width the chosen kernel streams (tiled: 16-bit slab-local keys)
-            info->col_bytes = info->kernel == static_cast<int32_t>(CsrKernel::Tiled) ? 2 : (A->csr.col32 ? 4 : 8);
+            info->col_bytes = info->kernel == static_cast<int32_t>(CsrKernel::Tiled)  ? 2
+                              : info->kernel == static_cast<int32_t>(CsrKernel::Lane) ? 4
+                              : (A->csr.col32 ? 4 : 8);
             info->lanes = csr_vector_width(A->csr);
         } else {
             info->rows = A->jds.rows;
@@ -181,7 +187,7 @@ int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
         }
         info->device_bytes = static_cast<std::int64_t>(A->row_ptr.bytes + A->col.bytes + A->val.bytes + A->nzcnt.bytes +
                                                        A->perm.bytes + A->inv_perm.bytes + A->jd_ptr.bytes) +
-                             A->tiled.bytes;
+                             A->tiled.bytes + A->lrc.bytes;
     });
 }
 

@@ -40,6 +40,7 @@ struct Shard {
     TcsrOwner tiled;
     MergeOwner merge;
     SplitOwner split;
+    LrcOwner lrc;
     DevBuf x, q, r, p_full, z_full, partials, scalars, gathered;
     CgVectors v{};
 
@@ -49,6 +50,7 @@ struct Shard {
         tiled.release();
         merge.release();
         split.release();
+        lrc.release();
     }
 };
 
@@ -114,8 +116,12 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
         s.tiled.dev.cols = n;
         A.tiled = &s.tiled.dev;
     } else {
-        if (s.split.refresh(A, lrp.data(), rt().kernel)) A.split = &s.split.dev;
-        if (s.merge.refresh(A, lrp.data(), rt().kernel)) A.merge = &s.merge.dev;
+        if (s.lrc.refresh(rows, lrp.data(), ci + base, val + base, n, monotone, max_row, rt().kernel)) {
+            A.lrc = &s.lrc.dev;
+        } else {
+            if (s.split.refresh(A, lrp.data(), rt().kernel)) A.split = &s.split.dev;
+            if (s.merge.refresh(A, lrp.data(), rt().kernel)) A.merge = &s.merge.dev;
+        }
     }
     init_shard_vectors(s, n, nranks);
 }

@@ -173,6 +173,7 @@ struct spmv_csr_state {
     TcsrOwner tiled;                // derived layouts, rebuilt when the matrix changes
     MergeOwner merge;
     SplitOwner split;
+    LrcOwner lrc;
     std::int64_t tiled_stamp = -1;  // sum of matrix update/construct counters it was built at
     CsrKernel tiled_policy = CsrKernel::Auto;
     bool first_run_done = false;
@@ -421,7 +422,11 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         const std::int64_t stamp = matrix_stamp(state);
         if (stamp != state.tiled_stamp || rt().kernel != state.tiled_policy) {
             state.tiled.refresh(rows, row_ptr, col_ind, val, ci.cols, rp.monotone, rp.max_row, rt().kernel);
-            if (!state.tiled.valid) {
+            if (!state.tiled.valid)
+                state.lrc.refresh(rows, row_ptr, col_ind, val, ci.cols, rp.monotone, rp.max_row, rt().kernel);
+            else
+                state.lrc.release();
+            if (!state.tiled.valid && !state.lrc.valid) {
                 state.split.refresh(A, row_ptr, rt().kernel);
                 state.merge.refresh(A, row_ptr, rt().kernel);
             } else {
@@ -432,6 +437,7 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
             state.tiled_policy = rt().kernel;
         }
         if (state.tiled.valid) A.tiled = &state.tiled.dev;
+        if (state.lrc.valid) A.lrc = &state.lrc.dev;
         if (state.merge.valid) A.merge = &state.merge.dev;
         if (state.split.valid) A.split = &state.split.dev;
         tm.acquired();

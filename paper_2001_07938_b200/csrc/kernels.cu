@@ -717,6 +717,7 @@ const char* csr_kernel_name(CsrKernel k) {
     case CsrKernel::Exact: return "exact";
     case CsrKernel::Tiled: return "tiled";
     case CsrKernel::Split: return "split";
+    case CsrKernel::Lane: return "lane";
     }
     return "?";
 }
@@ -728,7 +729,8 @@ CsrKernel parse_csr_kernel(const std::string& s) {
     if (s == "split") return CsrKernel::Split;
     if (s == "exact") return CsrKernel::Exact;
     if (s == "tiled") return CsrKernel::Tiled;
-    throw Error(Errc::DataError, "unknown CSR kernel '" + s + "' (auto, vector, tiled, exact)");
+    if (s == "lane") return CsrKernel::Lane;
+    throw Error(Errc::DataError, "unknown CSR kernel '" + s + "' (auto, vector, tiled, split, merge, lane, exact)");
 }
 
 int csr_vector_width(const CsrDev& A) {
@@ -745,9 +747,11 @@ CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested) {
     if (requested == CsrKernel::Merge) return A.merge ? CsrKernel::Merge : CsrKernel::Vector;
     if (requested == CsrKernel::Split) return A.split ? CsrKernel::Split : CsrKernel::Vector;
     if (requested == CsrKernel::Tiled) return A.tiled ? CsrKernel::Tiled : CsrKernel::Vector;
+    if (requested == CsrKernel::Lane) return A.lrc ? CsrKernel::Lane : CsrKernel::Vector;
     // Auto: the derived layouts exist only when they were judged to pay at
     // upload (tcsr_wanted / merge_wanted)
     if (A.tiled) return CsrKernel::Tiled;
+    if (A.lrc) return CsrKernel::Lane;
     if (A.split) return CsrKernel::Split;
     if (A.merge) return CsrKernel::Merge;
     return CsrKernel::Vector;
@@ -808,6 +812,10 @@ void launch_spmv_csr(const CsrDev& A, const double* x, double* y, CsrKernel k, c
         launch_spmv_split(A, x, y, s);
         return;
     }
+    if (k == CsrKernel::Lane) {
+        launch_spmv_lrc(*A.lrc, A.rows, x, y, s);
+        return;
+    }
     if (k == CsrKernel::Exact) {
         unsigned g = grid_for(A.rows);
         if (A.col32)
@@ -831,8 +839,10 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
         launch_spmv_tiled(*A.tiled, A.rows, p, q, partials, ticket, sc, s, dot_off);
         return;
     }
-    if (A.split || A.merge) {  // rows finish only after the fix-up: dot in its own pass
-        if (A.split)
+    if (A.lrc || A.split || A.merge) {  // rows finish only after the fix-up: dot in its own pass
+        if (A.lrc)
+            launch_spmv_lrc(*A.lrc, A.rows, p, q, s);
+        else if (A.split)
             launch_spmv_split(A, p, q, s);
         else
             launch_spmv_merge(A, p, q, s);

@@ -1,0 +1,206 @@
+// lrcsr_build.cpp — host builder of the lane-range CSR layout (b200.hpp,
+// kernel lrcsr.cu): an upload-time cached invariant of (row_ptr, col_ind,
+// val), rebuilt only when the marshaling layer re-marshals the matrix.
+//
+// Steps (host threads): column frequencies -> the hot set (the most frequent
+// columns, up to kLrcHotMax, kept only if they cover a useful share of the
+// nonzeros) -> compact rows (nonempty, with the map back) -> every nonzero
+// placed at its unit / lane / chunk slot with its encoded column -> one
+// descriptor per (unit, lane).
+
+#include "runtime.hpp"
+#include "tcsr.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+namespace b200 {
+
+namespace {
+
+template <typename F>
+void par_for(std::int64_t n, F&& f) {
+    unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+    nt = static_cast<unsigned>(std::min<std::int64_t>(nt, std::max<std::int64_t>(1, n / 4096)));
+    if (nt <= 1) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        const std::int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+        th.emplace_back([&f, lo, hi] { f(lo, hi); });
+    }
+    for (auto& t : th) t.join();
+}
+
+// position of nonzero e (CSR order, 0-based) in the layout
+inline std::int64_t lrc_pos(std::int64_t e) {
+    const std::int64_t u = e / kLrcUnit, w = e % kLrcUnit;
+    const std::int64_t l = w / kLrcLaneNnz, k = w % kLrcLaneNnz;
+    return u * kLrcUnit + (32 * (k / 4) + l) * 4 + (k % 4);
+}
+
+}  // namespace
+
+bool lrc_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, std::int64_t cols, bool monotone,
+                bool forced) {
+    if (!monotone || rows <= 0 || nnz <= 0) return false;
+    if (rows >= (std::int64_t(1) << 31) || cols > static_cast<std::int64_t>(kLrcColMask)) return false;
+    if (forced) return true;
+    // skewed rows (the merge_wanted test): a row-parallel kernel is bound by its
+    // longest rows and by its dependence chains
+    const double mean = static_cast<double>(nnz) / static_cast<double>(rows);
+    return max_row >= 4096 && static_cast<double>(max_row) > 32.0 * mean;
+}
+
+void lrc_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* val,
+                    std::int64_t cols, LrcHost& h) {
+    const std::int64_t base = rp[0], nnz = rp[rows] - base;
+    h = LrcHost{};
+    h.nnz = nnz;
+    h.units = (nnz + kLrcUnit - 1) / kLrcUnit;
+    // ---- hot columns ----------------------------------------------------------
+    std::vector<std::atomic<std::uint32_t>> freq(static_cast<std::size_t>(std::max<std::int64_t>(cols, 1)));
+    for (auto& f : freq) f.store(0, std::memory_order_relaxed);
+    par_for(nnz, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t j = lo; j < hi; ++j) freq[ci[base + j]].fetch_add(1, std::memory_order_relaxed);
+    });
+    std::vector<std::int32_t> slot(static_cast<std::size_t>(std::max<std::int64_t>(cols, 1)), -1);
+    {
+        std::vector<std::pair<std::uint32_t, std::int32_t>> cand;
+        for (std::int64_t c = 0; c < cols; ++c) {
+            const std::uint32_t f = freq[c].load(std::memory_order_relaxed);
+            if (f >= 2) cand.emplace_back(f, static_cast<std::int32_t>(c));
+        }
+        const char* e = std::getenv("LILAC_B200_LRC_HOT");  // cap (0 = no shared-memory x cache)
+        const std::int64_t cap = e && *e ? std::min<std::int64_t>(std::atoll(e), kLrcHotMax) : kLrcHotMax;
+        const std::size_t want = static_cast<std::size_t>(std::min<std::int64_t>(cap, static_cast<std::int64_t>(cand.size())));
+        auto by_freq = [](const auto& a, const auto& b) { return a.first != b.first ? a.first > b.first : a.second < b.second; };
+        if (want < cand.size()) std::nth_element(cand.begin(), cand.begin() + static_cast<std::ptrdiff_t>(want), cand.end(), by_freq);
+        cand.resize(want);
+        std::sort(cand.begin(), cand.end(), [](const auto& a, const auto& b) { return a.second < b.second; });
+        std::int64_t covered = 0;
+        for (const auto& c : cand) covered += c.first;
+        // worth a slot only when it moves a real share of the gathers off L1TEX
+        if (nnz > 0 && static_cast<double>(covered) >= 0.05 * static_cast<double>(nnz)) {
+            for (std::size_t i = 0; i < cand.size(); ++i) {
+                slot[cand[i].second] = static_cast<std::int32_t>(i);
+                h.hot_cols.push_back(cand[i].second);
+            }
+            h.hot_covered = covered;
+        }
+    }
+    h.hot = static_cast<int>(h.hot_cols.size());
+    // ---- compact rows ---------------------------------------------------------
+    std::vector<std::int32_t> comp(static_cast<std::size_t>(rows), -1);
+    for (std::int64_t r = 0; r < rows; ++r)
+        if (rp[r + 1] > rp[r]) {
+            comp[r] = static_cast<std::int32_t>(h.rmap.size());
+            h.rmap.push_back(static_cast<std::int32_t>(r));
+        }
+    h.rows_c = static_cast<std::int64_t>(h.rmap.size());
+    h.has_empty = h.rows_c != rows;
+    if (!h.has_empty) h.rmap.clear();  // identity
+    // ---- nonzeros -------------------------------------------------------------
+    const std::int64_t total = h.units * kLrcUnit;
+    h.val.assign(static_cast<std::size_t>(total), 0.0);
+    h.col.assign(static_cast<std::size_t>(total), kLrcHot | static_cast<std::uint32_t>(h.hot));  // padding: zero cell
+    par_for(rows, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t r = lo; r < hi; ++r) {
+            for (std::int64_t j = rp[r]; j < rp[r + 1]; ++j) {
+                const std::int64_t p = lrc_pos(j - base);
+                const std::int64_t c = ci[j];
+                std::uint32_t enc = slot[c] >= 0 ? (kLrcHot | static_cast<std::uint32_t>(slot[c]))
+                                                 : static_cast<std::uint32_t>(c);
+                if (j == rp[r]) enc |= kLrcStart;
+                h.val[p] = val[j];
+                h.col[p] = enc;
+            }
+        }
+    });
+    // ---- lane descriptors -----------------------------------------------------
+    h.desc.assign(static_cast<std::size_t>(h.units * 32), 0u);
+    const std::uint32_t last = static_cast<std::uint32_t>(std::max<std::int64_t>(h.rows_c - 1, 0));
+    par_for(h.units * 32, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t q = lo; q < hi; ++q) {
+            const std::int64_t e0 = (q / 32) * kLrcUnit + (q % 32) * kLrcLaneNnz;
+            if (e0 >= nnz) {  // padding lane: continues the last row with zeros
+                h.desc[q] = last | kLrcCont;
+                continue;
+            }
+            // the row holding nonzero e0: last r with rp[r] <= base + e0 (empty rows skipped)
+            const std::int64_t r = (std::upper_bound(rp, rp + rows + 1, base + e0) - rp) - 1;
+            const bool start = rp[r] == base + e0;
+            h.desc[q] = static_cast<std::uint32_t>(comp[r]) | (start ? 0u : kLrcCont);
+        }
+    });
+}
+
+void LrcOwner::upload(const LrcHost& h) {
+    Runtime& r = rt();
+    auto put = [&](DevBuf& d, const void* src, std::size_t bytes) {
+        d.ensure(std::max<std::size_t>(bytes, 16));
+        if (bytes) B200_CUDA(cudaMemcpyAsync(d.ptr, src, bytes, cudaMemcpyHostToDevice, r.stream));
+    };
+    put(val, h.val.data(), h.val.size() * sizeof(double));
+    put(col, h.col.data(), h.col.size() * sizeof(std::uint32_t));
+    put(desc, h.desc.data(), h.desc.size() * sizeof(std::uint32_t));
+    put(rmap, h.rmap.data(), h.rmap.size() * sizeof(std::int32_t));
+    put(hot_cols, h.hot_cols.data(), h.hot_cols.size() * sizeof(std::int32_t));
+    x_hot.ensure(sizeof(double) * static_cast<std::size_t>(h.hot + 2));
+    B200_CUDA(cudaMemsetAsync(x_hot.ptr, 0, sizeof(double) * static_cast<std::size_t>(h.hot + 2), r.stream));
+    carry.ensure(sizeof(LrcCarry) * static_cast<std::size_t>(std::max<std::int64_t>(h.units, 1)));
+    B200_CUDA(cudaStreamSynchronize(r.stream));
+    dev = LrcDev{};
+    dev.units = h.units;
+    dev.nnz = h.nnz;
+    dev.rows_c = h.rows_c;
+    dev.hot = h.hot;
+    dev.has_empty = h.has_empty;
+    dev.val = val.as<double>();
+    dev.col = col.as<std::uint32_t>();
+    dev.desc = desc.as<std::uint32_t>();
+    dev.rmap = h.has_empty ? rmap.as<std::int32_t>() : nullptr;
+    dev.hot_cols = hot_cols.as<std::int32_t>();
+    dev.x_hot = x_hot.as<double>();
+    dev.carry = carry.as<LrcCarry>();
+    hot_covered = h.hot_covered;
+    bytes = static_cast<std::int64_t>(h.val.size() * 12 + h.desc.size() * 4 + h.rmap.size() * 4);
+    valid = true;
+}
+
+void LrcOwner::release() {
+    for (DevBuf* b : {&val, &col, &desc, &rmap, &hot_cols, &x_hot, &carry}) b->release();
+    dev = LrcDev{};
+    valid = false;
+    bytes = 0;
+    hot_covered = 0;
+}
+
+bool LrcOwner::refresh(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* v,
+                       std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy) {
+    const bool forced = policy == CsrKernel::Lane;
+    if ((policy != CsrKernel::Auto && !forced) || rows <= 0) {
+        release();
+        return false;
+    }
+    host_in(rp, sizeof(std::int64_t) * static_cast<std::size_t>(rows + 1));
+    const std::int64_t nnz = rp[rows] - rp[0];
+    if (!lrc_wanted(rows, nnz, max_row, cols, monotone, forced)) {
+        release();
+        return false;
+    }
+    host_in(ci + rp[0], sizeof(std::int64_t) * static_cast<std::size_t>(nnz));
+    host_in(v + rp[0], sizeof(double) * static_cast<std::size_t>(nnz));
+    LrcHost h;
+    lrc_build_host(rows, rp, ci, v, cols, h);
+    upload(h);
+    return true;
+}
+
+}  // namespace b200

@@ -63,4 +63,31 @@ struct SplitOwner {
     void release();
 };
 
+// Lane-range layout (lrcsr_build.cpp / lrcsr.cu). Built for monotone row_ptr
+// with skewed rows (the merge_wanted test) under Auto, or when forced ("lane").
+bool lrc_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, std::int64_t cols, bool monotone,
+                bool forced);
+
+struct LrcHost {
+    std::int64_t units = 0, nnz = 0, rows_c = 0, hot_covered = 0;
+    int hot = 0;
+    bool has_empty = false;
+    std::vector<double> val;
+    std::vector<std::uint32_t> col, desc;
+    std::vector<std::int32_t> rmap, hot_cols;
+};
+void lrc_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, const double* val,
+                    std::int64_t cols, LrcHost& out);
+
+struct LrcOwner {
+    DevBuf val, col, desc, rmap, hot_cols, x_hot, carry;
+    LrcDev dev;
+    bool valid = false;
+    std::int64_t bytes = 0, hot_covered = 0;
+    void upload(const LrcHost& h);
+    void release();
+    bool refresh(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, const double* val,
+                 std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy);
+};
+
 }  // namespace b200

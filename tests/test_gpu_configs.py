@@ -94,7 +94,7 @@ def kron():
     return W.gen_kronecker(22)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "split", "merge"])
+@pytest.mark.parametrize("kernel", ["auto", "split", "merge", "lane"])
 def test_kron22_spmv_within_tolerance(kron, kernel):
     import torch
     rp, ci, val = kron
@@ -104,7 +104,7 @@ def test_kron22_spmv_within_tolerance(kron, kernel):
     try:
         info = A.info()
         if kernel == "auto":
-            assert info["kernel"] == 5, "skewed rows take the split plan"
+            assert info["kernel"] == 6, "skewed rows take the lane-range layout"
         xh = np.random.default_rng(22).uniform(0, 1, n)
         x = torch.from_numpy(xh).cuda()
         y = torch.empty(n, dtype=torch.float64, device="cuda")

@@ -97,6 +97,14 @@ def test_golden_csr_split_within_tolerance(name, case):
 
 
 @pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_golden_csr_lane_within_tolerance(name, case):
+    c = O.case_arrays(case)
+    N.lib().b200_set_kernel(b"lane")
+    y = run_csr(c["row_ptr"], c["col_ind"], c["val"], c["x"])
+    assert_within(y, c["y_csr"], spmv_bound(c["row_ptr"], c["col_ind"], c["val"], c["x"]))
+
+
+@pytest.mark.parametrize("name,case", O.all_golden_cases(), ids=lambda v: v if isinstance(v, str) else "")
 def test_golden_jds_bitwise(name, case):
     c = O.case_arrays(case)
     y = np.full(c["rows"], np.nan)
@@ -164,7 +172,7 @@ def test_random_csr_vs_oracle(shape):
     y_ref = O.spmv_csr(rp, ci, val, x)
     y = run_csr(rp, ci, val, x)
     assert_within(y, y_ref, spmv_bound(rp, ci, val, x))
-    for kernel in (b"vector", b"tiled", b"merge", b"split"):
+    for kernel in (b"vector", b"tiled", b"merge", b"split", b"lane"):
         N.lib().b200_set_kernel(kernel)
         assert_within(run_csr(rp, ci, val, x), y_ref, spmv_bound(rp, ci, val, x))
     N.lib().b200_set_kernel(b"exact")
@@ -390,7 +398,8 @@ def test_resident_matrix_moves_only_vectors():
 # --------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("cls,kernel", [("S", b"auto"), ("A", b"auto"), ("A", b"tiled"), ("A", b"vector"),
-                                        ("A", b"merge"), ("A", b"split"), ("C", b"auto"), ("C", b"vector")])
+                                        ("A", b"merge"), ("A", b"split"), ("A", b"lane"), ("C", b"auto"),
+                                        ("C", b"vector")])
 def test_npb_cg_zeta_device_driver(cls, kernel):
     na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
     rp, ci, val = D.gen_npb(na, nonzer, shift)
@@ -608,11 +617,11 @@ def test_power_law_rows_choose_split_and_match():
     val = rng.uniform(-1, 1, int(rp[-1]))
     x = rng.uniform(-1, 1, n)
     A = D.Matrix.csr(rp, ci, val)
-    assert A.info()["kernel"] == 5  # split
+    assert A.info()["kernel"] == 6  # lane-range layout for skewed rows
     A.free()
     y_ref = O.spmv_csr(rp, ci, val, x)
     bound = spmv_bound(rp, ci, val, x)
-    for kernel in (b"auto", b"merge"):
+    for kernel in (b"auto", b"merge", b"split", b"lane"):
         N.lib().b200_set_kernel(kernel)
         y1 = run_csr(rp, ci, val, x)
         y2 = run_csr(rp, ci, val, x)

@@ -19,3 +19,16 @@ def test_tiled_layout_builder_replay():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("ok ") == 4, r.stdout
+
+
+def test_lane_range_layout_builder_replay():
+    """tests/cpp/test_lrc: the lane-range layout (csrc/lrcsr_build.cpp) replayed
+    by a CPU restatement of lrcsr.cu — lane walks, warp combine, unit carries
+    and the fix-up — on power-law, short, unit-aligned and single-nonzero
+    matrices: every row written once, y within 1e-12 sum|a x|."""
+    binp = os.path.join(B.ROOT, "tests", "cpp", "test_lrc")
+    if not os.path.exists(binp):
+        pytest.skip("tests/cpp/test_lrc not built")
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("ok ") == 4, r.stdout
