@@ -374,7 +374,7 @@ bool TcsrOwner::refresh(std::int64_t rows, const std::int64_t* rp, const std::in
         host_in(ci, sizeof(std::int64_t) * static_cast<std::size_t>(end));
         host_in(v, sizeof(double) * static_cast<std::size_t>(end));
     }
-    if (policy == CsrKernel::Vector || policy == CsrKernel::Exact ||
+    if ((policy != CsrKernel::Auto && policy != CsrKernel::Tiled) ||
         !tcsr_wanted(rows, rp, ci, cols, monotone, max_row, forced)) {
         release();
         return false;
