@@ -143,12 +143,14 @@ def build_cpp_tests(force: bool = False, verbose: bool = False):
         _run(["g++", "-std=c++17", "-O1", "-g", f"-I{INCLUDE}", "-o", out, src,
               os.path.join(CSRC, "marshal.cpp"), "-lpthread"], verbose)
     # tests/cpp/test_tcsr, test_lrc: the tiled / lane-range layout builders replayed on the CPU
-    for name in ("test_tcsr", "test_lrc"):
+    for name in ("test_tcsr", "test_lrc", "test_lrc_dev"):
         src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
         out = os.path.join(ROOT, "tests", "cpp", name)
         if os.path.exists(src) and (force or _stale(out, [src, LIB] + _headers())):
+            extra = [f"-L{CUDA_HOME}/lib64", "-lcudart"] if name == "test_lrc_dev" else []
             _run(["g++", "-std=c++17", "-O2", f"-I{INCLUDE}", f"-I{CSRC}", f"-I{CUDA_HOME}/include", "-o", out, src,
-                  f"-L{PKG}", "-llilac_b200", "-Wl,-rpath,$ORIGIN/../../paper_2001_07938_b200", "-lpthread"], verbose)
+                  f"-L{PKG}", "-llilac_b200", "-Wl,-rpath,$ORIGIN/../../paper_2001_07938_b200", "-lpthread"] + extra,
+                 verbose)
 
 
 def clean():

@@ -84,6 +84,11 @@ void device_quiesce();
 
 enum class CsrKernel : int { Auto = 0, Vector = 1, Merge = 2, Exact = 3, Tiled = 4, Split = 5, Lane = 6 };
 const char* csr_kernel_name(CsrKernel k);
+// Keep a resident matrix's plain CSR (col / val) once a derived layout (tiled,
+// lane-range) serves it? Default no: the derived layout alone is used and the
+// plain arrays' HBM is freed (NPB class C 0.80 -> 0.42 GB, stencil N=420
+// 48 -> 24 GB). LILAC_B200_KEEP_CSR=1 keeps them (any kernel stays selectable).
+bool keep_plain_csr();
 CsrKernel parse_csr_kernel(const std::string& s);
 
 // Tiled CSR (upload-time cached invariant, tcsr_build.cpp): rows cut into

@@ -28,6 +28,16 @@ struct b200_matrix {
 
 namespace {
 
+// A derived layout serves the matrix: free the plain col / val (keep_plain_csr).
+void drop_plain(b200_matrix& A) {
+    CsrDev& d = A.csr;
+    if (!(d.tiled || d.lrc) || keep_plain_csr()) return;
+    A.col.release();
+    A.val.release();
+    d.col = nullptr;
+    d.val = nullptr;
+}
+
 CsrKernel matrix_kernel(const b200_matrix* A) {
     return choose_csr_kernel(A->csr, rt().kernel);
 }
@@ -68,10 +78,11 @@ int b200_matrix_create_csr(b200_matrix** out, std::int64_t rows, const std::int6
         d.monotone = monotone;
         A->max_row = max_row;
         if (A->tiled.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel)) d.tiled = &A->tiled.dev;
-        if (!d.tiled && A->lrc.refresh(rows, row_ptr, col_ind, val, cols, monotone, max_row, rt().kernel))
+        if (!d.tiled && A->lrc.refresh(d, row_ptr, col_ind, rt().kernel))
             d.lrc = &A->lrc.dev;
         if (!d.tiled && !d.lrc && A->split.refresh(d, row_ptr, rt().kernel)) d.split = &A->split.dev;
         if (!d.tiled && !d.lrc && A->merge.refresh(d, row_ptr, rt().kernel)) d.merge = &A->merge.dev;
+        drop_plain(*A);
         *out = A.release();
     });
 }
@@ -213,6 +224,14 @@ int b200_matrix_create_stencil27(b200_matrix** out, std::int64_t nx, double diag
         d.val = A->val.as<double>();
         d.monotone = true;
         A->max_row = d.max_row;
+        // the lane-range layout streams banded rows at ~0.9 of copy (the
+        // row-parallel kernel ~0.75); built on the device from the generated CSR
+        const CsrKernel pol = rt().kernel;
+        if ((pol == CsrKernel::Auto && d.nnz >= (std::int64_t(16) << 20)) || pol == CsrKernel::Lane) {
+            lrc_build_device(n, d.row_ptr, d.col, true, d.val, d.nnz, n, A->lrc, rt().stream);
+            d.lrc = &A->lrc.dev;
+        }
+        drop_plain(*A);
         *out = A.release();
     });
 }

@@ -79,6 +79,15 @@ namespace {
 
 void init_shard_vectors(Shard& s, std::int64_t n, int nranks);
 
+// A derived layout serves the shard: free its plain col / val (keep_plain_csr).
+void drop_plain(Shard& s) {
+    if (!(s.A.tiled || s.A.lrc) || keep_plain_csr()) return;
+    s.col.release();
+    s.val.release();
+    s.A.col = nullptr;
+    s.A.val = nullptr;
+}
+
 // Upload one row block [row0, row0+rows) given its host arrays (row_ptr with
 // rows+1 entries, absolute offsets into col_ind/val as passed).
 void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, const std::int64_t* rp,
@@ -116,13 +125,14 @@ void load_shard(Shard& s, std::int64_t n, std::int64_t row0, std::int64_t rows, 
         s.tiled.dev.cols = n;
         A.tiled = &s.tiled.dev;
     } else {
-        if (s.lrc.refresh(rows, lrp.data(), ci + base, val + base, n, monotone, max_row, rt().kernel)) {
+        if (s.lrc.refresh(A, lrp.data(), ci + base, rt().kernel)) {
             A.lrc = &s.lrc.dev;
         } else {
             if (s.split.refresh(A, lrp.data(), rt().kernel)) A.split = &s.split.dev;
             if (s.merge.refresh(A, lrp.data(), rt().kernel)) A.merge = &s.merge.dev;
         }
     }
+    drop_plain(s);
     init_shard_vectors(s, n, nranks);
 }
 
@@ -184,6 +194,12 @@ void load_shard_stencil(Shard& s, std::int64_t nx, std::int64_t row0, std::int64
     A.col32 = true;
     A.val = s.val.as<double>();
     A.monotone = true;
+    const CsrKernel pol = rt().kernel;
+    if ((pol == CsrKernel::Auto && s.nnz >= (std::int64_t(16) << 20)) || pol == CsrKernel::Lane) {
+        lrc_build_device(rows, A.row_ptr, A.col, true, A.val, s.nnz, n, s.lrc, rt().stream);
+        A.lrc = &s.lrc.dev;
+    }
+    drop_plain(s);
     init_shard_vectors(s, n, nranks);
 }
 

@@ -176,6 +176,7 @@ struct spmv_csr_state {
     LrcOwner lrc;
     std::int64_t tiled_stamp = -1;  // sum of matrix update/construct counters it was built at
     CsrKernel tiled_policy = CsrKernel::Auto;
+    bool plain_dropped = false;     // col / val device copies freed: a derived layout serves the matrix
     bool first_run_done = false;
 };
 
@@ -419,11 +420,25 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         A.val = dval.data<double>();
         A.monotone = rp.monotone;
         // derived tiled layout: rebuilt only when row_ptr/col_ind/val were re-marshaled
-        const std::int64_t stamp = matrix_stamp(state);
-        if (stamp != state.tiled_stamp || rt().kernel != state.tiled_policy) {
+        std::int64_t stamp = matrix_stamp(state);
+        const bool rebuild = stamp != state.tiled_stamp || rt().kernel != state.tiled_policy;
+        if (rebuild && state.plain_dropped) {
+            // the plain col / val were freed behind the old layout: a rebuild (or
+            // another kernel) needs them again — re-marshal both in full
+            state.m_col_ind.release();
+            state.m_val.release();
+            state.plain_dropped = false;
+            state.m_col_ind.acquire(col_ind, nnz * sizeof(*col_ind), nullptr, ColInd_update, ColInd_destruct);
+            state.m_val.acquire(val, nnz * sizeof(*val), nullptr, B200Read_update, B200Read_destruct);
+            A.col = ci.buf.ptr;
+            A.col32 = ci.col32;
+            A.val = dval.data<double>();
+            stamp = matrix_stamp(state);
+        }
+        if (rebuild) {
             state.tiled.refresh(rows, row_ptr, col_ind, val, ci.cols, rp.monotone, rp.max_row, rt().kernel);
             if (!state.tiled.valid)
-                state.lrc.refresh(rows, row_ptr, col_ind, val, ci.cols, rp.monotone, rp.max_row, rt().kernel);
+                state.lrc.refresh(A, row_ptr, col_ind, rt().kernel);
             else
                 state.lrc.release();
             if (!state.tiled.valid && !state.lrc.valid) {
@@ -435,6 +450,17 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
             }
             state.tiled_stamp = stamp;
             state.tiled_policy = rt().kernel;
+            // only the derived layout is read from now on: free the plain copies
+            // (the marshal objects stay constructed, so change detection goes on)
+            if ((state.tiled.valid || state.lrc.valid) && !keep_plain_csr() && !dval.lent) {
+                ci.buf.release();
+                dval.buf.release();
+                state.plain_dropped = true;
+            }
+        }
+        if (state.plain_dropped) {
+            A.col = nullptr;
+            A.val = nullptr;
         }
         if (state.tiled.valid) A.tiled = &state.tiled.dev;
         if (state.lrc.valid) A.lrc = &state.lrc.dev;

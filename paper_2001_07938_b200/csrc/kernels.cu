@@ -742,6 +742,9 @@ int csr_vector_width(const CsrDev& A) {
 }
 
 CsrKernel choose_csr_kernel(const CsrDev& A, CsrKernel requested) {
+    // the plain arrays were dropped once a derived layout was built (keep_plain_csr)
+    if (!A.val && A.tiled) return CsrKernel::Tiled;
+    if (!A.val && A.lrc) return CsrKernel::Lane;
     if (requested == CsrKernel::Exact) return CsrKernel::Exact;
     if (requested == CsrKernel::Vector) return CsrKernel::Vector;
     if (requested == CsrKernel::Merge) return A.merge ? CsrKernel::Merge : CsrKernel::Vector;

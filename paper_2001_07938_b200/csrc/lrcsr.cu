@@ -20,8 +20,13 @@
 
 #include "b200.hpp"
 #include "ldst.cuh"
+#include "tcsr.hpp"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace b200 {
 
@@ -286,6 +291,226 @@ void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
 }
 
 }  // namespace
+
+// ---- device-side builder (a resident CSR: the device-generated stencil, the
+// harness's uploaded arrays) --------------------------------------------------
+
+namespace {
+
+constexpr int kBT = 256;
+
+unsigned bgrid(std::int64_t n) {
+    return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>((n + kBT - 1) / kBT, 148 * 64)));
+}
+
+#define GS_LOOP(i, n)                                                                                        \
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n);        \
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+
+__device__ __forceinline__ std::int64_t lrc_pos_d(std::int64_t e) {
+    const std::int64_t u = e / kLrcUnit, w = e % kLrcUnit;
+    const std::int64_t l = w / kLrcLaneNnz, k = w % kLrcLaneNnz;
+    return u * kLrcUnit + (32 * (k / 4) + l) * 4 + (k % 4);
+}
+
+template <typename IdxT>
+__global__ void k_lrc_freq(const IdxT* __restrict__ col, std::int64_t nnz, unsigned* __restrict__ freq) {
+    GS_LOOP(j, nnz) atomicAdd(freq + col[j], 1u);
+}
+
+__global__ void k_lrc_iota(std::int32_t* __restrict__ v, std::int64_t n) {
+    GS_LOOP(i, n) v[i] = static_cast<std::int32_t>(i);
+}
+
+// slots for the chosen hot columns (sorted ascending by column)
+__global__ void k_lrc_slots(const std::int32_t* __restrict__ hot_cols, int hot, std::int32_t* __restrict__ slot) {
+    GS_LOOP(i, hot) slot[hot_cols[i]] = static_cast<std::int32_t>(i);
+}
+
+template <typename IdxT>
+__global__ void k_lrc_scatter(const IdxT* __restrict__ col, const double* __restrict__ val, std::int64_t nnz,
+                              std::int64_t total, const std::int32_t* __restrict__ slot, int hot,
+                              double* __restrict__ oval, std::uint32_t* __restrict__ ocol) {
+    GS_LOOP(e, total) {
+        const std::int64_t p = lrc_pos_d(e);
+        if (e < nnz) {
+            const std::int64_t c = static_cast<std::int64_t>(col[e]);
+            const std::int32_t sl = slot ? slot[c] : -1;
+            oval[p] = val[e];
+            ocol[p] = sl >= 0 ? (kLrcHot | static_cast<std::uint32_t>(sl)) : static_cast<std::uint32_t>(c);
+        } else {  // padding: value 0 times the zero cell
+            oval[p] = 0.0;
+            ocol[p] = kLrcHot | static_cast<std::uint32_t>(hot);
+        }
+    }
+}
+
+// row starts, nonempty flags (for the compaction scan)
+__global__ void k_lrc_rows(const std::int64_t* __restrict__ rp, std::int64_t rows, std::uint32_t* __restrict__ ocol,
+                           std::int32_t* __restrict__ nonempty) {
+    GS_LOOP(r, rows) {
+        const std::int64_t a = rp[r] - rp[0], b = rp[r + 1] - rp[0];
+        nonempty[r] = b > a ? 1 : 0;
+        if (b > a) ocol[lrc_pos_d(a)] |= kLrcStart;
+    }
+}
+
+__global__ void k_lrc_rmap(const std::int32_t* __restrict__ comp, const std::int32_t* __restrict__ nonempty,
+                           std::int64_t rows, std::int32_t* __restrict__ rmap) {
+    GS_LOOP(r, rows) if (nonempty[r]) rmap[comp[r]] = static_cast<std::int32_t>(r);
+}
+
+__global__ void k_lrc_desc(const std::int64_t* __restrict__ rp, std::int64_t rows, std::int64_t nnz,
+                           std::int64_t units, const std::int32_t* __restrict__ comp, std::uint32_t last,
+                           std::uint32_t* __restrict__ desc) {
+    GS_LOOP(q, units * 32) {
+        const std::int64_t e0 = (q / 32) * kLrcUnit + (q % 32) * kLrcLaneNnz;
+        if (e0 >= nnz) {
+            desc[q] = last | kLrcCont;
+            continue;
+        }
+        const std::int64_t t = rp[0] + e0;
+        std::int64_t lo = 0, hi = rows + 1;  // first index with rp[idx] > t
+        while (lo < hi) {
+            const std::int64_t mid = (lo + hi) >> 1;
+            if (rp[mid] <= t)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        const std::int64_t r = lo - 1;
+        const std::uint32_t cr = comp ? static_cast<std::uint32_t>(comp[r]) : static_cast<std::uint32_t>(r);
+        desc[q] = cr | (rp[r] == t ? 0u : kLrcCont);
+    }
+}
+
+}  // namespace
+
+int lrc_hot_cap() {
+    const char* e = std::getenv("LILAC_B200_LRC_HOT");
+    // measured on Kronecker scale 22: 0 -> 351 us, 4096 -> 319, 12288 -> 294,
+    // 16384 -> 294, 27647 -> 513 (the cache then leaves L1 too small for the
+    // remaining global gathers)
+    return e && *e ? static_cast<int>(std::min<long>(std::atol(e), kLrcHotMax)) : 12288;
+}
+
+void lrc_build_device(std::int64_t rows, const std::int64_t* rp, const void* col, bool col32, const double* val,
+                      std::int64_t nnz, std::int64_t cols, LrcOwner& o, cudaStream_t s) {
+    o.release();
+    const std::int64_t units = (nnz + kLrcUnit - 1) / kLrcUnit, total = units * kLrcUnit;
+    // ---- hot set: column frequencies, top `cap` by (count desc, column asc) ----
+    const int cap = lrc_hot_cap();
+    int hot = 0;
+    std::int64_t covered = 0;
+    DevBuf slot;
+    if (cap > 0 && cols > 0 && nnz > 0) {
+        DevBuf freq, keys_out, cols_in, cols_out, tmp;
+        freq.ensure(sizeof(unsigned) * cols, false);
+        B200_CUDA(cudaMemsetAsync(freq.ptr, 0, sizeof(unsigned) * cols, s));
+        if (col32)
+            k_lrc_freq<<<bgrid(nnz), kBT, 0, s>>>(static_cast<const std::int32_t*>(col), nnz, freq.as<unsigned>());
+        else
+            k_lrc_freq<<<bgrid(nnz), kBT, 0, s>>>(static_cast<const std::int64_t*>(col), nnz, freq.as<unsigned>());
+        cols_in.ensure(sizeof(std::int32_t) * cols, false);
+        k_lrc_iota<<<bgrid(cols), kBT, 0, s>>>(cols_in.as<std::int32_t>(), cols);
+        keys_out.ensure(sizeof(unsigned) * cols, false);
+        cols_out.ensure(sizeof(std::int32_t) * cols, false);
+        std::size_t tb = 0;
+        B200_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, freq.as<unsigned>(), keys_out.as<unsigned>(),
+                                                            cols_in.as<std::int32_t>(), cols_out.as<std::int32_t>(),
+                                                            static_cast<int>(cols), 0, 32, s));
+        tmp.ensure(tb, false);
+        B200_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.ptr, tb, freq.as<unsigned>(), keys_out.as<unsigned>(),
+                                                            cols_in.as<std::int32_t>(), cols_out.as<std::int32_t>(),
+                                                            static_cast<int>(cols), 0, 32, s));
+        const int want = static_cast<int>(std::min<std::int64_t>(cap, cols));
+        std::vector<unsigned> cnt(static_cast<std::size_t>(want));
+        std::vector<std::int32_t> hc(static_cast<std::size_t>(want));
+        B200_CUDA(cudaMemcpyAsync(cnt.data(), keys_out.ptr, sizeof(unsigned) * want, cudaMemcpyDeviceToHost, s));
+        B200_CUDA(cudaMemcpyAsync(hc.data(), cols_out.ptr, sizeof(std::int32_t) * want, cudaMemcpyDeviceToHost, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        int k = 0;
+        while (k < want && cnt[k] >= 2) covered += cnt[k++];
+        if (static_cast<double>(covered) >= 0.05 * static_cast<double>(nnz)) {
+            hot = k;
+            hc.resize(static_cast<std::size_t>(hot));
+            std::sort(hc.begin(), hc.end());
+            o.hot_cols.ensure(sizeof(std::int32_t) * std::max(hot, 1));
+            B200_CUDA(cudaMemcpyAsync(o.hot_cols.ptr, hc.data(), sizeof(std::int32_t) * hot, cudaMemcpyHostToDevice, s));
+            slot.ensure(sizeof(std::int32_t) * cols, false);
+            B200_CUDA(cudaMemsetAsync(slot.ptr, 0xff, sizeof(std::int32_t) * cols, s));
+            k_lrc_slots<<<bgrid(hot), kBT, 0, s>>>(o.hot_cols.as<std::int32_t>(), hot, slot.as<std::int32_t>());
+        } else {
+            covered = 0;
+        }
+        B200_CUDA(cudaStreamSynchronize(s));
+        for (DevBuf* b : {&freq, &keys_out, &cols_in, &cols_out, &tmp}) b->release();
+    }
+    if (!o.hot_cols.ptr) o.hot_cols.ensure(16);
+    // ---- nonzeros ---------------------------------------------------------------
+    o.val.ensure(sizeof(double) * std::max<std::int64_t>(total, 2), false);
+    o.col.ensure(sizeof(std::uint32_t) * std::max<std::int64_t>(total, 4), false);
+    if (col32)
+        k_lrc_scatter<<<bgrid(total), kBT, 0, s>>>(static_cast<const std::int32_t*>(col) , val, nnz, total,
+                                                   hot ? slot.as<std::int32_t>() : nullptr, hot, o.val.as<double>(),
+                                                   o.col.as<std::uint32_t>());
+    else
+        k_lrc_scatter<<<bgrid(total), kBT, 0, s>>>(static_cast<const std::int64_t*>(col), val, nnz, total,
+                                                   hot ? slot.as<std::int32_t>() : nullptr, hot, o.val.as<double>(),
+                                                   o.col.as<std::uint32_t>());
+    // ---- rows: starts, compaction ---------------------------------------------------
+    DevBuf nonempty, comp;
+    nonempty.ensure(sizeof(std::int32_t) * (rows + 1), false);
+    comp.ensure(sizeof(std::int32_t) * (rows + 1), false);
+    k_lrc_rows<<<bgrid(rows), kBT, 0, s>>>(rp, rows, o.col.as<std::uint32_t>(), nonempty.as<std::int32_t>());
+    B200_CUDA(cudaMemsetAsync(nonempty.as<std::int32_t>() + rows, 0, sizeof(std::int32_t), s));
+    {
+        std::size_t tb = 0;
+        B200_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nonempty.as<std::int32_t>(), comp.as<std::int32_t>(),
+                                                rows + 1, s));
+        DevBuf tmp;
+        tmp.ensure(tb, false);
+        B200_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tb, nonempty.as<std::int32_t>(), comp.as<std::int32_t>(),
+                                                rows + 1, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        tmp.release();
+    }
+    std::int32_t rows_c = 0;
+    B200_CUDA(cudaMemcpy(&rows_c, comp.as<std::int32_t>() + rows, sizeof rows_c, cudaMemcpyDeviceToHost));
+    const bool has_empty = rows_c != rows;
+    if (has_empty) {
+        o.rmap.ensure(sizeof(std::int32_t) * std::max<std::int64_t>(rows_c, 1));
+        k_lrc_rmap<<<bgrid(rows), kBT, 0, s>>>(comp.as<std::int32_t>(), nonempty.as<std::int32_t>(), rows,
+                                               o.rmap.as<std::int32_t>());
+    }
+    o.desc.ensure(sizeof(std::uint32_t) * std::max<std::int64_t>(units * 32, 4), false);
+    k_lrc_desc<<<bgrid(units * 32), kBT, 0, s>>>(rp, rows, nnz, units, has_empty ? comp.as<std::int32_t>() : nullptr,
+                                                 static_cast<std::uint32_t>(std::max(rows_c - 1, 0)),
+                                                 o.desc.as<std::uint32_t>());
+    B200_CUDA(cudaGetLastError());
+    o.x_hot.ensure(sizeof(double) * static_cast<std::size_t>(hot + 2));
+    B200_CUDA(cudaMemsetAsync(o.x_hot.ptr, 0, sizeof(double) * static_cast<std::size_t>(hot + 2), s));
+    o.carry.ensure(sizeof(LrcCarry) * static_cast<std::size_t>(std::max<std::int64_t>(units, 1)));
+    B200_CUDA(cudaStreamSynchronize(s));
+    for (DevBuf* b : {&slot, &nonempty, &comp}) b->release();
+    LrcDev& d = o.dev;
+    d = LrcDev{};
+    d.units = units;
+    d.nnz = nnz;
+    d.rows_c = rows_c;
+    d.hot = hot;
+    d.has_empty = has_empty;
+    d.val = o.val.as<double>();
+    d.col = o.col.as<std::uint32_t>();
+    d.desc = o.desc.as<std::uint32_t>();
+    d.rmap = has_empty ? o.rmap.as<std::int32_t>() : nullptr;
+    d.hot_cols = o.hot_cols.as<std::int32_t>();
+    d.x_hot = o.x_hot.as<double>();
+    d.carry = o.carry.as<LrcCarry>();
+    o.hot_covered = covered;
+    o.bytes = total * 12 + units * 32 * 4 + (has_empty ? rows_c * 4 : 0);
+    o.valid = true;
+}
 
 void launch_spmv_lrc(const LrcDev& L, std::int64_t rows, const double* x, double* y, cudaStream_t s) {
     if (rows <= 0) return;

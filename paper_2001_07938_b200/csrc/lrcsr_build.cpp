@@ -48,14 +48,18 @@ inline std::int64_t lrc_pos(std::int64_t e) {
 }  // namespace
 
 bool lrc_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, std::int64_t cols, bool monotone,
-                bool forced) {
+                bool forced, double locality) {
     if (!monotone || rows <= 0 || nnz <= 0) return false;
     if (rows >= (std::int64_t(1) << 31) || cols > static_cast<std::int64_t>(kLrcColMask)) return false;
     if (forced) return true;
     // skewed rows (the merge_wanted test): a row-parallel kernel is bound by its
     // longest rows and by its dependence chains
     const double mean = static_cast<double>(nnz) / static_cast<double>(rows);
-    return max_row >= 4096 && static_cast<double>(max_row) > 32.0 * mean;
+    if (max_row >= 4096 && static_cast<double>(max_row) > 32.0 * mean) return true;
+    // banded rows at scale: units stream at ~0.9 of copy where the row-parallel
+    // kernel reaches ~0.75 (27-point stencil, 57M nonzeros: 122 vs 142 us);
+    // below ~16 units per warp slot the grid is not filled
+    return locality >= 0.0 && locality <= 0.3 && nnz >= (std::int64_t(16) << 20);
 }
 
 void lrc_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* val,
@@ -77,8 +81,7 @@ void lrc_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64_
             const std::uint32_t f = freq[c].load(std::memory_order_relaxed);
             if (f >= 2) cand.emplace_back(f, static_cast<std::int32_t>(c));
         }
-        const char* e = std::getenv("LILAC_B200_LRC_HOT");  // cap (0 = no shared-memory x cache)
-        const std::int64_t cap = e && *e ? std::min<std::int64_t>(std::atoll(e), kLrcHotMax) : kLrcHotMax;
+        const std::int64_t cap = lrc_hot_cap();  // 0 = no shared-memory x cache
         const std::size_t want = static_cast<std::size_t>(std::min<std::int64_t>(cap, static_cast<std::int64_t>(cand.size())));
         auto by_freq = [](const auto& a, const auto& b) { return a.first != b.first ? a.first > b.first : a.second < b.second; };
         if (want < cand.size()) std::nth_element(cand.begin(), cand.begin() + static_cast<std::ptrdiff_t>(want), cand.end(), by_freq);
@@ -182,24 +185,26 @@ void LrcOwner::release() {
     hot_covered = 0;
 }
 
-bool LrcOwner::refresh(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* v,
-                       std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy) {
+bool LrcOwner::refresh(const CsrDev& A, const std::int64_t* rp, const std::int64_t* ci, CsrKernel policy) {
     const bool forced = policy == CsrKernel::Lane;
-    if ((policy != CsrKernel::Auto && !forced) || rows <= 0) {
+    if ((policy != CsrKernel::Auto && !forced) || A.rows <= 0 || !A.monotone) {
         release();
         return false;
     }
-    host_in(rp, sizeof(std::int64_t) * static_cast<std::size_t>(rows + 1));
-    const std::int64_t nnz = rp[rows] - rp[0];
-    if (!lrc_wanted(rows, nnz, max_row, cols, monotone, forced)) {
+    host_in(rp, sizeof(std::int64_t) * static_cast<std::size_t>(A.rows + 1));
+    const std::int64_t base = rp[0], nnz = rp[A.rows] - base;
+    double loc = -1.0;
+    if (!forced && nnz >= (std::int64_t(16) << 20)) {
+        host_in(ci + base, sizeof(std::int64_t) * static_cast<std::size_t>(nnz));
+        loc = gather_locality(A.rows, rp, ci);
+    }
+    if (!lrc_wanted(A.rows, nnz, A.max_row, A.cols, A.monotone, forced, loc)) {
         release();
         return false;
     }
-    host_in(ci + rp[0], sizeof(std::int64_t) * static_cast<std::size_t>(nnz));
-    host_in(v + rp[0], sizeof(double) * static_cast<std::size_t>(nnz));
-    LrcHost h;
-    lrc_build_host(rows, rp, ci, v, cols, h);
-    upload(h);
+    const std::size_t w = A.col32 ? 4 : 8;
+    lrc_build_device(A.rows, A.row_ptr, static_cast<const char*>(A.col) + w * static_cast<std::size_t>(base), A.col32,
+                     A.val + base, nnz, A.cols, *this, rt().stream);
     return true;
 }
 

@@ -145,6 +145,14 @@ void DevBuf::release() {
     bytes = cap = 0;
 }
 
+bool keep_plain_csr() {
+    static const bool keep = [] {
+        const char* e = std::getenv("LILAC_B200_KEEP_CSR");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return keep;
+}
+
 void device_quiesce() {
     if (rt().inited) (void)cudaDeviceSynchronize();
 }

@@ -25,6 +25,9 @@ struct TcsrHost {
 // skips the size/locality tests.
 bool tcsr_wanted(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, std::int64_t cols,
                  bool monotone, std::int64_t max_row, bool forced);
+// distinct x sectors per nonzero over 64 sampled 32-row windows (1 = no
+// locality at all; -1 = too few nonzeros to tell)
+double gather_locality(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind);
 void tcsr_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind,
                      const double* val, std::int64_t cols, TcsrHost& out);
 
@@ -65,8 +68,11 @@ struct SplitOwner {
 
 // Lane-range layout (lrcsr_build.cpp / lrcsr.cu). Built for monotone row_ptr
 // with skewed rows (the merge_wanted test) under Auto, or when forced ("lane").
+// Auto: skewed rows (the merge_wanted test), or a large matrix whose gathers
+// have locality (locality = gather_locality, <= 0.3: banded / stencil rows),
+// where fixed-size units stream better than row-parallel walks.
 bool lrc_wanted(std::int64_t rows, std::int64_t nnz, std::int64_t max_row, std::int64_t cols, bool monotone,
-                bool forced);
+                bool forced, double locality);
 
 struct LrcHost {
     std::int64_t units = 0, nnz = 0, rows_c = 0, hot_covered = 0;
@@ -86,8 +92,17 @@ struct LrcOwner {
     std::int64_t bytes = 0, hot_covered = 0;
     void upload(const LrcHost& h);
     void release();
-    bool refresh(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, const double* val,
-                 std::int64_t cols, bool monotone, std::int64_t max_row, CsrKernel policy);
+    // A: the resident CSR (device row_ptr / col / val, as uploaded); row_ptr /
+    // col_ind: the caller's host arrays (for the policy tests). Built on the device.
+    bool refresh(const CsrDev& A, const std::int64_t* row_ptr, const std::int64_t* col_ind, CsrKernel policy);
 };
+
+// The same layout built on the device from a resident CSR (row_ptr int64,
+// col int32 or int64, val f64; nnz = row_ptr[rows] - row_ptr[0], columns
+// rebased to row_ptr[0]): the hot set by a device histogram + radix sort with
+// the host builder's tie order, so both builders produce identical arrays.
+void lrc_build_device(std::int64_t rows, const std::int64_t* row_ptr, const void* col, bool col32, const double* val,
+                      std::int64_t nnz, std::int64_t cols, LrcOwner& out, cudaStream_t s);
+int lrc_hot_cap();
 
 }  // namespace b200

@@ -206,8 +206,12 @@ bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* 
     const std::int64_t nslabs = (cols + kSlabW - 1) / kSlabW;
     const std::int64_t tiles = std::max<std::int64_t>(device_sms(), (rows + kMaxTileRows - 1) / kMaxTileRows);
     if (nnz / (tiles * nslabs * kTileWarps) < 256) return false;
-    // gather locality: distinct 32-byte x sectors per nonzero over windows of
-    // 32 consecutive rows (a warp's worth). ~1 = every gather its own sector.
+    return gather_locality(rows, rp, ci) > 0.3;
+}
+
+double gather_locality(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci) {
+    // distinct 32-byte x sectors per nonzero over windows of 32 consecutive
+    // rows (a warp's worth). ~1 = every gather its own sector; -1 = unknown.
     double ratio_sum = 0;
     int windows = 0;
     std::vector<std::int64_t> sec;
@@ -221,7 +225,7 @@ bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* 
         ratio_sum += static_cast<double>(distinct) / static_cast<double>(sec.size());
         ++windows;
     }
-    return windows > 0 && ratio_sum / windows > 0.3;
+    return windows > 0 ? ratio_sum / windows : -1.0;
 }
 
 void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, const double* val,

@@ -32,3 +32,15 @@ def test_lane_range_layout_builder_replay():
     r = subprocess.run([binp], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("ok ") == 4, r.stdout
+
+
+@pytest.mark.gpu
+def test_lane_range_device_builder_matches_host_builder():
+    """tests/cpp/test_lrc_dev: lrc_build_device (hot set by device histogram +
+    radix sort, encoded columns, descriptors, compact-row map) bit-identical to
+    the host builder that test_lrc replays."""
+    binp = os.path.join(B.ROOT, "tests", "cpp", "test_lrc_dev")
+    assert os.path.exists(binp), "tests/cpp/test_lrc_dev not built"
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("ok ") == 4, r.stdout
