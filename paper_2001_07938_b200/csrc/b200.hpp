@@ -202,11 +202,13 @@ struct LrcDev {
     std::int64_t units = 0, nnz = 0;
     std::int64_t rows_c = 0;                  // nonempty rows
     int hot = 0;                              // hot columns (slot `hot` is a zero cell)
-    bool has_empty = false;                   // some rows are empty: y is zeroed first
+    bool has_empty = false;                   // some rows are empty
     const double* val = nullptr;              // units * kLrcUnit
     const std::uint32_t* col = nullptr;       // units * kLrcUnit
     const std::uint32_t* desc = nullptr;      // units * 32
     const std::int32_t* rmap = nullptr;       // rows_c: compact -> original row (null: identity)
+    const std::int32_t* empty = nullptr;      // rows - rows_c empty rows (the fix-up pass zeroes them)
+    std::int64_t nempty = 0;
     const std::int32_t* hot_cols = nullptr;   // hot
     double* x_hot = nullptr;                  // hot + 1, gathered per call
     LrcCarry* carry = nullptr;                // units

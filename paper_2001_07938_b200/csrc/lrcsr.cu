@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kLrcThreads, 1)
                 : "memory");
         }
     }
+    pdl_trigger();  // the fix-up may launch now; its griddepcontrol.wait covers this grid
     bool waited = !HOT;
     for (; u < L.units; u += stride) {
         const std::uint32_t d = __ldg(L.desc + u * 32 + lane);
@@ -241,8 +242,11 @@ __global__ void k_lrc_gather_hot(const std::int32_t* __restrict__ cols, int hot,
 // units it continues into, summing in unit order.
 template <bool RMAP>
 __global__ void k_lrc_fixup(LrcDev L, double* __restrict__ y) {
-    pdl_wait();
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    // empty rows (never in the stream) are zero; nothing else writes them
+    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L.nempty; i += stride)
+        y[__ldg(L.empty + i)] = 0.0;
+    pdl_wait();  // every unit's carry is written
     for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < L.units;
          u += stride) {
         const LrcCarry c = L.carry[u];
@@ -281,12 +285,12 @@ void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
     cfg.numAttrs = HOT ? 1 : 0;
     B200_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_lrc<HOT, RMAP>, L, x, y));
     cudaLaunchConfig_t fc{};
-    const std::int64_t fb = std::min<std::int64_t>((L.units + 255) / 256, 148 * 8);
+    const std::int64_t fb = std::min<std::int64_t>((std::max(L.units, L.nempty) + 255) / 256, 148 * 8);
     fc.gridDim = dim3(static_cast<unsigned>(std::max<std::int64_t>(fb, 1)));
     fc.blockDim = dim3(256);
     fc.stream = s;
     fc.attrs = at;
-    fc.numAttrs = 0;  // the carries are complete only when every unit is: plain stream order
+    fc.numAttrs = 1;  // launched early; zeroes the empty rows, then waits for every carry
     B200_CUDA(cudaLaunchKernelEx(&fc, k_lrc_fixup<RMAP>, L, y));
 }
 
@@ -356,8 +360,13 @@ __global__ void k_lrc_rows(const std::int64_t* __restrict__ rp, std::int64_t row
 }
 
 __global__ void k_lrc_rmap(const std::int32_t* __restrict__ comp, const std::int32_t* __restrict__ nonempty,
-                           std::int64_t rows, std::int32_t* __restrict__ rmap) {
-    GS_LOOP(r, rows) if (nonempty[r]) rmap[comp[r]] = static_cast<std::int32_t>(r);
+                           std::int64_t rows, std::int32_t* __restrict__ rmap, std::int32_t* __restrict__ empty) {
+    GS_LOOP(r, rows) {
+        if (nonempty[r])
+            rmap[comp[r]] = static_cast<std::int32_t>(r);
+        else
+            empty[r - comp[r]] = static_cast<std::int32_t>(r);
+    }
 }
 
 __global__ void k_lrc_desc(const std::int64_t* __restrict__ rp, std::int64_t rows, std::int64_t nnz,
@@ -480,8 +489,9 @@ void lrc_build_device(std::int64_t rows, const std::int64_t* rp, const void* col
     const bool has_empty = rows_c != rows;
     if (has_empty) {
         o.rmap.ensure(sizeof(std::int32_t) * std::max<std::int64_t>(rows_c, 1));
+        o.empty.ensure(sizeof(std::int32_t) * std::max<std::int64_t>(rows - rows_c, 1));
         k_lrc_rmap<<<bgrid(rows), kBT, 0, s>>>(comp.as<std::int32_t>(), nonempty.as<std::int32_t>(), rows,
-                                               o.rmap.as<std::int32_t>());
+                                               o.rmap.as<std::int32_t>(), o.empty.as<std::int32_t>());
     }
     o.desc.ensure(sizeof(std::uint32_t) * std::max<std::int64_t>(units * 32, 4), false);
     k_lrc_desc<<<bgrid(units * 32), kBT, 0, s>>>(rp, rows, nnz, units, has_empty ? comp.as<std::int32_t>() : nullptr,
@@ -504,11 +514,13 @@ void lrc_build_device(std::int64_t rows, const std::int64_t* rp, const void* col
     d.col = o.col.as<std::uint32_t>();
     d.desc = o.desc.as<std::uint32_t>();
     d.rmap = has_empty ? o.rmap.as<std::int32_t>() : nullptr;
+    d.empty = has_empty ? o.empty.as<std::int32_t>() : nullptr;
+    d.nempty = rows - rows_c;
     d.hot_cols = o.hot_cols.as<std::int32_t>();
     d.x_hot = o.x_hot.as<double>();
     d.carry = o.carry.as<LrcCarry>();
     o.hot_covered = covered;
-    o.bytes = total * 12 + units * 32 * 4 + (has_empty ? rows_c * 4 : 0);
+    o.bytes = total * 12 + units * 32 * 4 + (has_empty ? rows * 4 : 0);
     o.valid = true;
 }
 
@@ -519,7 +531,6 @@ void launch_spmv_lrc(const LrcDev& L, std::int64_t rows, const double* x, double
         B200_CUDA(cudaGetDevice(&dev));
         B200_CUDA(cudaDeviceGetAttribute(&g_lrc_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    if (L.has_empty) B200_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * static_cast<std::size_t>(rows), s));
     if (L.units == 0) return;
     // always through the shared-memory cell path: padding entries read its
     // zero cell (never an Inf or NaN of x), whether or not columns are hot

@@ -80,13 +80,13 @@ struct LrcHost {
     bool has_empty = false;
     std::vector<double> val;
     std::vector<std::uint32_t> col, desc;
-    std::vector<std::int32_t> rmap, hot_cols;
+    std::vector<std::int32_t> rmap, hot_cols, empty;
 };
 void lrc_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind, const double* val,
                     std::int64_t cols, LrcHost& out);
 
 struct LrcOwner {
-    DevBuf val, col, desc, rmap, hot_cols, x_hot, carry;
+    DevBuf val, col, desc, rmap, empty, hot_cols, x_hot, carry;
     LrcDev dev;
     bool valid = false;
     std::int64_t bytes = 0, hot_covered = 0;

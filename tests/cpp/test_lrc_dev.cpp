@@ -85,7 +85,10 @@ static void check(std::int64_t rows, std::int64_t cols, int maxlen, double p_emp
     same(back<std::uint32_t>(o.col, total), h.col, "col", name);
     same(back<std::uint32_t>(o.desc, static_cast<std::size_t>(h.units) * 32), h.desc, "desc", name);
     same(back<std::int32_t>(o.hot_cols, static_cast<std::size_t>(h.hot)), h.hot_cols, "hot_cols", name);
-    if (h.has_empty) same(back<std::int32_t>(o.rmap, static_cast<std::size_t>(h.rows_c)), h.rmap, "rmap", name);
+    if (h.has_empty) {
+        same(back<std::int32_t>(o.rmap, static_cast<std::size_t>(h.rows_c)), h.rmap, "rmap", name);
+        same(back<std::int32_t>(o.empty, static_cast<std::size_t>(rows - h.rows_c)), h.empty, "empty", name);
+    }
     o.release();
     drp.release();
     dcol.release();
