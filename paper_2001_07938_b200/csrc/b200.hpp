@@ -181,8 +181,9 @@ struct SplitDev {
 // LDS), else the global column. A lane descriptor holds the compact row of its
 // first nonzero | kLrcCont when that row began before the lane. Rows complete
 // inside a unit are stored directly; the row in progress at each unit's start
-// and end goes to a per-unit carry, summed in unit order by a fix-up pass
-// (deterministic). HBM: 12 bytes per nonzero + 4 per 4 kLrcChunks nonzeros.
+// and end goes to a per-unit carry; a fix-up pass sums every row that crossed
+// units from a structural plan built with the layout (one thread per short
+// crossing, one warp per long one: a fixed order, deterministic). HBM: 12 bytes per nonzero + 4 per 4 kLrcChunks nonzeros.
 constexpr int kLrcChunks = 8;
 constexpr int kLrcLaneNnz = 4 * kLrcChunks;
 constexpr int kLrcUnit = 32 * kLrcLaneNnz;
@@ -191,12 +192,15 @@ constexpr std::uint32_t kLrcHot = 1u << 30;
 constexpr std::uint32_t kLrcColMask = kLrcHot - 1u;
 constexpr std::uint32_t kLrcCont = 1u << 31;
 constexpr int kLrcHotMax = 27 * 1024 - 1;  // + the zero cell: 216 KB of shared memory
+// Per unit, per call: the partial of the row open at the unit's start (when
+// lane 0 continues a row) and of the row open at its end.
 struct LrcCarry {
-    std::int32_t head_row;  // compact row in progress at the unit's start, -1 none
-    std::int32_t tail_row;  // row begun in the unit and still open at its end, -1 none
-    std::int32_t split;     // some row begins inside the unit
-    std::int32_t pad;
     double head_val, tail_val;
+};
+// A row crossing units (structural, built with the layout): it begins in unit
+// u and ends in unit e >= u; y[row] = tail_val[u] + head_val[u+1..e].
+struct LrcFix {
+    std::int32_t u, e, row, pad;
 };
 struct LrcDev {
     std::int64_t units = 0, nnz = 0;
@@ -212,7 +216,10 @@ struct LrcDev {
     const std::int32_t* hot_cols = nullptr;   // hot
     double* x_hot = nullptr;                  // hot + 1, gathered per call
     LrcCarry* carry = nullptr;                // units
+    const LrcFix* fix = nullptr;              // nfix_short entries (e - u <= kLrcFixShort), then nfix_long
+    std::int64_t nfix_short = 0, nfix_long = 0;
 };
+constexpr int kLrcFixShort = 16;  // longer crossings are summed by a warp
 
 struct CsrDev {
     std::int64_t rows = 0;      // number of rows computed

@@ -197,33 +197,13 @@ __global__ void __launch_bounds__(kLrcThreads, 1)
         const int b = sm ? __ffs(static_cast<int>(sm & ~1u)) - 1 : -1;  // first split lane > 0
         const double head0 = __shfl_sync(kFull, w.head, 0);
         const double totb = __shfl_sync(kFull, tot, b < 0 ? 0 : b);
-        const std::uint32_t rowb = __shfl_sync(kFull, rprev, b < 0 ? 0 : b);
         const double S31 = __shfl_sync(kFull, S, 31);
-        const std::uint32_t row31 = __shfl_sync(kFull, w.row, 31);
-        const int seg31 = __shfl_sync(kFull, seg, 31);
         if (lane == 0) {
             LrcCarry c;
-            c.pad = 0;
-            c.split = sm != 0u;
-            c.head_row = -1;
-            c.head_val = 0.0;
-            if (cont0) {
-                const std::uint32_t first = d & ~kLrcCont;
-                if (sm & 1u) {  // lane 0 itself closes it
-                    c.head_row = static_cast<std::int32_t>(first);
-                    c.head_val = w.head;
-                } else if (b >= 0) {  // closed at the first split lane
-                    c.head_row = static_cast<std::int32_t>(rowb);
-                    c.head_val = totb;
-                } else {  // no row begins in this unit: it is all one row's
-                    c.head_row = static_cast<std::int32_t>(first);
-                    c.head_val = S31;
-                }
-            }
-            // the row open at the unit's end, if it began in this unit
-            const bool tail = ((sm >> seg31) & 1u) != 0u;
-            c.tail_row = tail ? static_cast<std::int32_t>(row31) : -1;
-            c.tail_val = tail ? S31 : 0.0;
+            // the row open at the unit's start (lane 0 continues it): closed by
+            // lane 0 itself, at the first split lane, or never (all one row)
+            c.head_val = !cont0 ? 0.0 : (sm & 1u) ? w.head : (b >= 0 ? totb : S31);
+            c.tail_val = S31;  // the row open at the unit's end (used when it began here)
             L.carry[u] = c;
         }
     }
@@ -238,27 +218,29 @@ __global__ void k_lrc_gather_hot(const std::int32_t* __restrict__ cols, int hot,
     pdl_trigger();
 }
 
-// Rows that crossed units: the unit where a row began walks forward over the
-// units it continues into, summing in unit order.
+// Rows that crossed units (the structural plan): a short crossing is summed
+// by one thread in unit order, a long one by a warp (lanes stride the units,
+// then a fixed shuffle tree). Empty rows (never in the stream) are zeroed here.
 template <bool RMAP>
 __global__ void k_lrc_fixup(LrcDev L, double* __restrict__ y) {
+    const std::int64_t tid = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    // empty rows (never in the stream) are zero; nothing else writes them
-    for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L.nempty; i += stride)
-        y[__ldg(L.empty + i)] = 0.0;
+    for (std::int64_t i = tid; i < L.nempty; i += stride) y[__ldg(L.empty + i)] = 0.0;
     pdl_wait();  // every unit's carry is written
-    for (std::int64_t u = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < L.units;
-         u += stride) {
-        const LrcCarry c = L.carry[u];
-        if (c.tail_row < 0) continue;
-        double tot = c.tail_val;
-        for (std::int64_t v = u + 1; v < L.units; ++v) {
-            const int hr = __ldcg(&L.carry[v].head_row);
-            if (hr != c.tail_row) break;
-            tot += __ldcg(&L.carry[v].head_val);
-            if (__ldcg(&L.carry[v].split)) break;
-        }
-        y[out_row<RMAP>(L, static_cast<std::uint32_t>(c.tail_row))] = tot;
+    for (std::int64_t i = tid; i < L.nfix_short; i += stride) {
+        const LrcFix f = L.fix[i];
+        double tot = __ldcg(&L.carry[f.u].tail_val);
+        for (int v = f.u + 1; v <= f.e; ++v) tot += __ldcg(&L.carry[v].head_val);
+        y[out_row<RMAP>(L, static_cast<std::uint32_t>(f.row))] = tot;
+    }
+    const int lane = threadIdx.x & 31;
+    for (std::int64_t i = tid >> 5; i < L.nfix_long; i += stride >> 5) {
+        const LrcFix f = L.fix[L.nfix_short + i];
+        double part = 0.0;
+        for (int v = f.u + 1 + lane; v <= f.e; v += 32) part += __ldcg(&L.carry[v].head_val);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        if (lane == 0) y[out_row<RMAP>(L, static_cast<std::uint32_t>(f.row))] = __ldcg(&L.carry[f.u].tail_val) + part;
     }
 }
 
@@ -285,7 +267,8 @@ void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
     cfg.numAttrs = HOT ? 1 : 0;
     B200_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_lrc<HOT, RMAP>, L, x, y));
     cudaLaunchConfig_t fc{};
-    const std::int64_t fb = std::min<std::int64_t>((std::max(L.units, L.nempty) + 255) / 256, 148 * 8);
+    const std::int64_t work = std::max({L.nfix_short, 32 * L.nfix_long, L.nempty});
+    const std::int64_t fb = std::min<std::int64_t>((work + 255) / 256, 148 * 8);
     fc.gridDim = dim3(static_cast<unsigned>(std::max<std::int64_t>(fb, 1)));
     fc.blockDim = dim3(256);
     fc.stream = s;
@@ -390,6 +373,36 @@ __global__ void k_lrc_desc(const std::int64_t* __restrict__ rp, std::int64_t row
         const std::int64_t r = lo - 1;
         const std::uint32_t cr = comp ? static_cast<std::uint32_t>(comp[r]) : static_cast<std::uint32_t>(r);
         desc[q] = cr | (rp[r] == t ? 0u : kLrcCont);
+    }
+}
+
+// The crossing-row plan: for each unit, the row holding its last nonzero,
+// when that row began inside the unit (else an earlier unit owns it).
+__global__ void k_lrc_plan(const std::int64_t* __restrict__ rp, std::int64_t rows, std::int64_t nnz,
+                           std::int64_t units, const std::int32_t* __restrict__ comp, LrcFix* __restrict__ fix_short,
+                           LrcFix* __restrict__ fix_long, unsigned long long* __restrict__ counts) {
+    GS_LOOP(u, units) {
+        const std::int64_t last = std::min<std::int64_t>((u + 1) * kLrcUnit, nnz) - 1;
+        const std::int64_t t = rp[0] + last;
+        std::int64_t lo = 0, hi = rows + 1;  // first index with rp[idx] > t
+        while (lo < hi) {
+            const std::int64_t mid = (lo + hi) >> 1;
+            if (rp[mid] <= t)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        const std::int64_t r = lo - 1;
+        if (rp[r] - rp[0] < u * kLrcUnit) continue;  // began in an earlier unit
+        LrcFix f;
+        f.u = static_cast<std::int32_t>(u);
+        f.e = static_cast<std::int32_t>((rp[r + 1] - rp[0] - 1) / kLrcUnit);
+        f.row = comp ? comp[r] : static_cast<std::int32_t>(r);
+        f.pad = 0;
+        if (f.e - f.u <= kLrcFixShort)
+            fix_short[atomicAdd(&counts[0], 1ull)] = f;
+        else
+            fix_long[atomicAdd(&counts[1], 1ull)] = f;
     }
 }
 
@@ -498,6 +511,30 @@ void lrc_build_device(std::int64_t rows, const std::int64_t* rp, const void* col
                                                  static_cast<std::uint32_t>(std::max(rows_c - 1, 0)),
                                                  o.desc.as<std::uint32_t>());
     B200_CUDA(cudaGetLastError());
+    // crossing-row plan (short crossings first, then long ones)
+    std::int64_t nshort = 0, nlong = 0;
+    {
+        DevBuf fs, fl, cnt;
+        fs.ensure(sizeof(LrcFix) * std::max<std::int64_t>(units, 1), false);
+        fl.ensure(sizeof(LrcFix) * std::max<std::int64_t>(units, 1), false);
+        cnt.ensure(16, false);
+        B200_CUDA(cudaMemsetAsync(cnt.ptr, 0, 16, s));
+        k_lrc_plan<<<bgrid(units), kBT, 0, s>>>(rp, rows, nnz, units, has_empty ? comp.as<std::int32_t>() : nullptr,
+                                                fs.as<LrcFix>(), fl.as<LrcFix>(), cnt.as<unsigned long long>());
+        unsigned long long c[2] = {0, 0};
+        B200_CUDA(cudaMemcpyAsync(c, cnt.ptr, 16, cudaMemcpyDeviceToHost, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        nshort = static_cast<std::int64_t>(c[0]);
+        nlong = static_cast<std::int64_t>(c[1]);
+        o.fix.ensure(sizeof(LrcFix) * std::max<std::int64_t>(nshort + nlong, 1));
+        if (nshort)
+            B200_CUDA(cudaMemcpyAsync(o.fix.ptr, fs.ptr, sizeof(LrcFix) * nshort, cudaMemcpyDeviceToDevice, s));
+        if (nlong)
+            B200_CUDA(cudaMemcpyAsync(o.fix.as<LrcFix>() + nshort, fl.ptr, sizeof(LrcFix) * nlong,
+                                      cudaMemcpyDeviceToDevice, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        for (DevBuf* b : {&fs, &fl, &cnt}) b->release();
+    }
     o.x_hot.ensure(sizeof(double) * static_cast<std::size_t>(hot + 2));
     B200_CUDA(cudaMemsetAsync(o.x_hot.ptr, 0, sizeof(double) * static_cast<std::size_t>(hot + 2), s));
     o.carry.ensure(sizeof(LrcCarry) * static_cast<std::size_t>(std::max<std::int64_t>(units, 1)));
@@ -519,6 +556,9 @@ void lrc_build_device(std::int64_t rows, const std::int64_t* rp, const void* col
     d.hot_cols = o.hot_cols.as<std::int32_t>();
     d.x_hot = o.x_hot.as<double>();
     d.carry = o.carry.as<LrcCarry>();
+    d.fix = o.fix.as<LrcFix>();
+    d.nfix_short = nshort;
+    d.nfix_long = nlong;
     o.hot_covered = covered;
     o.bytes = total * 12 + units * 32 * 4 + (has_empty ? rows * 4 : 0);
     o.valid = true;

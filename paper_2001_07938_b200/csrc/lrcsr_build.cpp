@@ -146,44 +146,8 @@ void lrc_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64_
     });
 }
 
-void LrcOwner::upload(const LrcHost& h) {
-    Runtime& r = rt();
-    auto put = [&](DevBuf& d, const void* src, std::size_t bytes) {
-        d.ensure(std::max<std::size_t>(bytes, 16));
-        if (bytes) B200_CUDA(cudaMemcpyAsync(d.ptr, src, bytes, cudaMemcpyHostToDevice, r.stream));
-    };
-    put(val, h.val.data(), h.val.size() * sizeof(double));
-    put(col, h.col.data(), h.col.size() * sizeof(std::uint32_t));
-    put(desc, h.desc.data(), h.desc.size() * sizeof(std::uint32_t));
-    put(rmap, h.rmap.data(), h.rmap.size() * sizeof(std::int32_t));
-    put(empty, h.empty.data(), h.empty.size() * sizeof(std::int32_t));
-    put(hot_cols, h.hot_cols.data(), h.hot_cols.size() * sizeof(std::int32_t));
-    x_hot.ensure(sizeof(double) * static_cast<std::size_t>(h.hot + 2));
-    B200_CUDA(cudaMemsetAsync(x_hot.ptr, 0, sizeof(double) * static_cast<std::size_t>(h.hot + 2), r.stream));
-    carry.ensure(sizeof(LrcCarry) * static_cast<std::size_t>(std::max<std::int64_t>(h.units, 1)));
-    B200_CUDA(cudaStreamSynchronize(r.stream));
-    dev = LrcDev{};
-    dev.units = h.units;
-    dev.nnz = h.nnz;
-    dev.rows_c = h.rows_c;
-    dev.hot = h.hot;
-    dev.has_empty = h.has_empty;
-    dev.val = val.as<double>();
-    dev.col = col.as<std::uint32_t>();
-    dev.desc = desc.as<std::uint32_t>();
-    dev.rmap = h.has_empty ? rmap.as<std::int32_t>() : nullptr;
-    dev.empty = h.has_empty ? empty.as<std::int32_t>() : nullptr;
-    dev.nempty = static_cast<std::int64_t>(h.empty.size());
-    dev.hot_cols = hot_cols.as<std::int32_t>();
-    dev.x_hot = x_hot.as<double>();
-    dev.carry = carry.as<LrcCarry>();
-    hot_covered = h.hot_covered;
-    bytes = static_cast<std::int64_t>(h.val.size() * 12 + h.desc.size() * 4 + h.rmap.size() * 4 + h.empty.size() * 4);
-    valid = true;
-}
-
 void LrcOwner::release() {
-    for (DevBuf* b : {&val, &col, &desc, &rmap, &empty, &hot_cols, &x_hot, &carry}) b->release();
+    for (DevBuf* b : {&val, &col, &desc, &rmap, &empty, &hot_cols, &x_hot, &carry, &fix}) b->release();
     dev = LrcDev{};
     valid = false;
     bytes = 0;

@@ -86,11 +86,10 @@ void lrc_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::i
                     std::int64_t cols, LrcHost& out);
 
 struct LrcOwner {
-    DevBuf val, col, desc, rmap, empty, hot_cols, x_hot, carry;
+    DevBuf val, col, desc, rmap, empty, hot_cols, x_hot, carry, fix;
     LrcDev dev;
     bool valid = false;
     std::int64_t bytes = 0, hot_covered = 0;
-    void upload(const LrcHost& h);
     void release();
     // A: the resident CSR (device row_ptr / col / val, as uploaded); row_ptr /
     // col_ind: the caller's host arrays (for the policy tests). Built on the device.

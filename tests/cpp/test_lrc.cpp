@@ -132,43 +132,31 @@ static void replay(const Csr& a, const char* name) {
                     writes[map(w[l - 1].row)]++;
                 }
             }
+        // the unit's carry (lrcsr.cu): head = the row open at its start
         LrcCarry c{};
-        c.split = sm != 0;
-        c.head_row = -1;
         if (cont[0]) {
-            const std::uint32_t first = h.desc[u * 32] & ~kLrcCont;
             int b = -1;
             for (int l = 1; l < 32; ++l)
                 if ((sm >> l) & 1u) {
                     b = l;
                     break;
                 }
-            if (sm & 1u) {
-                c.head_row = static_cast<std::int32_t>(first);
-                c.head_val = w[0].head;
-            } else if (b >= 0) {
-                c.head_row = static_cast<std::int32_t>(w[b - 1].row);
-                c.head_val = S[b - 1] + w[b].head;
-            } else {
-                c.head_row = static_cast<std::int32_t>(first);
-                c.head_val = S[31];
-            }
+            c.head_val = (sm & 1u) ? w[0].head : (b >= 0 ? S[b - 1] + w[b].head : S[31]);
         }
-        const bool tail = (sm >> seg[31]) & 1u;
-        c.tail_row = tail ? static_cast<std::int32_t>(w[31].row) : -1;
-        c.tail_val = tail ? S[31] : 0.0;
+        c.tail_val = S[31];
         carry[u] = c;
     }
+    // the structural crossing plan (k_lrc_plan) and the fix-up sums
+    const std::int64_t base = a.rp[0];
     for (std::int64_t u = 0; u < h.units; ++u) {
-        if (carry[u].tail_row < 0) continue;
+        const std::int64_t last = std::min<std::int64_t>((u + 1) * kLrcUnit, nnz) - 1;
+        const std::int64_t r = (std::upper_bound(a.rp.begin(), a.rp.end(), base + last) - a.rp.begin()) - 1;
+        if (a.rp[r] - base < u * kLrcUnit) continue;
+        const std::int64_t e = (a.rp[r + 1] - base - 1) / kLrcUnit;
         double tot = carry[u].tail_val;
-        for (std::int64_t v = u + 1; v < h.units; ++v) {
-            if (carry[v].head_row != carry[u].tail_row) break;
-            tot += carry[v].head_val;
-            if (carry[v].split) break;
-        }
-        y[map(carry[u].tail_row)] = tot;
-        writes[map(carry[u].tail_row)]++;
+        for (std::int64_t v = u + 1; v <= e; ++v) tot += carry[v].head_val;
+        y[r] = tot;
+        writes[r]++;
     }
     CHECK(stored == nnz, "%s: stored %lld of %lld nonzeros", name, (long long)stored, (long long)nnz);
     for (std::int64_t r = 0; r < a.rows; ++r) {
