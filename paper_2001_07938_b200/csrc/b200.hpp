@@ -249,6 +249,7 @@ struct JdsDev {
     const void* col = nullptr;
     bool col32 = true;
     const double* val = nullptr;
+    double* prod = nullptr;                    // nnz scratch: the products of the two-phase kernel
 };
 
 // ---------------------------------------------------------------------------

@@ -236,6 +236,7 @@ struct spmv_jds_state {
     MarshalObject<DevArray> m_val;
     MarshalObject<DevArray> m_x;
     MarshalObject<DevArray> m_output;
+    DevBuf prod;  // product scratch of the two-phase JDS kernel
     bool validated = false;
     bool first_run_done = false;
 };
@@ -546,6 +547,8 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         A.col = ci.buf.ptr;
         A.col32 = ci.col32;
         A.val = dval.data<double>();
+        state.prod.ensure(sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(nnz, 1)), false);
+        A.prod = state.prod.as<double>();
         timed_launch(hs, [&] { launch_spmv_jds(A, dx.data<double>(), dout.buf.as<double>(), rt().stream); });
         tm.acquired();
 

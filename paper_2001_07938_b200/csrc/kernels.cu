@@ -489,6 +489,74 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
     }
 }
 
+// Two-phase JDS (bijective perm, a product scratch): the rows' sums must be
+// sequential in k order to stay bit-identical, but the products need not be.
+// Phase 1 computes every stored product prod[e] = val[e] * x[col[e]] with
+// all nonzeros in parallel (coalesced val/col, independent gathers: no row
+// waits on its own earlier loads); phase 2 sums each jagged row's products in
+// the reference k order from L2 (addresses known up front, 16 in flight).
+// The longest rows no longer serialise rounds of gathers (Parboil shape: 64
+// diagonals, 4 dependent val/col -> x rounds per row in the one-phase kernel).
+template <typename IdxT>
+__global__ void __launch_bounds__(kThreads) k_jds_products(std::int64_t nnz, const IdxT* __restrict__ col,
+                                                           const double* __restrict__ val,
+                                                           const double* __restrict__ x, double* __restrict__ prod) {
+    pdl_trigger();  // phase 2 may launch; it waits for this grid before reading prod
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
+    std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    constexpr int U = 4;
+    for (; e + (U - 1) * stride < nnz; e += U * stride) {
+        double v[U], xv[U];
+        long long c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + e + u * stride));
+            c[u] = static_cast<long long>(__ldg(col + e + u * stride));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) prod[e + u * stride] = __dmul_rn(v[u], xv[u]);
+    }
+    for (; e < nnz; e += stride) prod[e] = __dmul_rn(val[e], __ldg(x + static_cast<long long>(col[e])));
+}
+
+__global__ void __launch_bounds__(kThreads) k_jds_sum(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
+                                                      const std::int64_t* __restrict__ inv_perm,
+                                                      const std::int64_t* __restrict__ jd_ptr,
+                                                      const double* __restrict__ prod, double* __restrict__ y) {
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
+    std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    // the row's shape does not depend on phase 1
+    std::int64_t len = j < rows ? __ldg(nzcnt + j) : 0, out = j < rows ? __ldg(inv_perm + j) : 0;
+    pdl_wait();
+    for (; j < rows; j += stride) {
+        double acc = 0.0;
+        std::int64_t k = 0;
+        for (; k + kJdsU <= len; k += kJdsU) {
+            double p[kJdsU];
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) p[u] = __ldcg(prod + __ldg(jd_ptr + k + u) + j);
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) acc = __dadd_rn(acc, p[u]);
+        }
+        if (k < len) {
+            double p[kJdsU];
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) p[u] = k + u < len ? __ldcg(prod + __ldg(jd_ptr + k + u) + j) : 0.0;
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u)
+                if (k + u < len) acc = __dadd_rn(acc, p[u]);
+        }
+        y[out] = acc;
+        const std::int64_t nj = j + stride;
+        if (nj < rows) {
+            len = __ldg(nzcnt + nj);
+            out = __ldg(inv_perm + nj);
+        }
+    }
+}
+
 // JDS when perm is not a bijection: thread per original row (uncoalesced,
 // still the reference's semantics and order).
 template <typename IdxT>
@@ -864,6 +932,32 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
     if (A.rows <= 0) return;
     const unsigned g = grid_for(A.rows);
+    static const bool two_phase = [] {  // LILAC_B200_JDS_2P=0: the one-phase kernel
+        const char* e = std::getenv("LILAC_B200_JDS_2P");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (A.inv_perm && A.prod && two_phase) {
+        const unsigned gp = grid_for(A.nnz, kSMs * 8);
+        if (A.col32)
+            k_jds_products<std::int32_t><<<gp, kThreads, 0, s>>>(A.nnz, static_cast<const std::int32_t*>(A.col), A.val,
+                                                                 x, A.prod);
+        else
+            k_jds_products<std::int64_t><<<gp, kThreads, 0, s>>>(A.nnz, static_cast<const std::int64_t*>(A.col), A.val,
+                                                                 x, A.prod);
+        B200_CUDA(cudaGetLastError());
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(g);
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        B200_CUDA(cudaLaunchKernelEx(&cfg, k_jds_sum, A.rows, A.nzcnt, A.inv_perm, A.jd_ptr,
+                                     static_cast<const double*>(A.prod), y));
+        return;
+    }
     if (A.inv_perm) {
         if (A.col32)
             k_jds<std::int32_t><<<g, kThreads, 0, s>>>(A.rows, A.nzcnt, A.inv_perm, A.jd_ptr,
