@@ -74,6 +74,16 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(ptr); }
 };
 void pool_trim();  // return every cached block to CUDA
+// True the first time it is called for the current device (function
+// attributes such as the dynamic shared-memory limit are per device).
+inline bool first_on_device(std::uint64_t& mask) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return false;
+    const std::uint64_t bit = 1ull << (d & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
 // Wait for all work on the current device (errors ignored: teardown paths)
 // before buffers that caller streams may still use go back to the pool.
 void device_quiesce();

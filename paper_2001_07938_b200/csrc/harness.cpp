@@ -379,9 +379,21 @@ std::int64_t sum_h2d(std::initializer_list<std::int64_t> v) {
 // Entry points
 // =================================================================================
 
+namespace b200 {
+// multi_harness.cpp: the same entry points over LILAC_B200_NGPUS devices
+void multi_spmv_csr(std::int64_t rows, double* output, const std::int64_t* row_ptr, const double* val,
+                    const double* x, const std::int64_t* col_ind);
+void multi_dot(double* result, std::int64_t n, const double* a, const double* b);
+void multi_vec2(const char* name, std::int64_t n, double* y, double s, const double* x, bool axpy);
+}  // namespace b200
+
 extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int64_t* row_ptr, const double* val,
                               const double* x, const std::int64_t* col_ind) {
     boundary("b200_spmv_csr", [&] {
+        if (harness_ngpus() > 1) {
+            multi_spmv_csr(rows, output, row_ptr, val, x, col_ind);
+            return;
+        }
         spmv_csr_state& state = csr_state();
         HarnessStats& hs = harness_stats("b200_spmv_csr");
         Timer tm(hs);
@@ -561,6 +573,10 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
 
 extern "C" void b200_dot(double* result, std::int64_t length, const double* a, const double* b) {
     boundary("b200_dot", [&] {
+        if (harness_ngpus() > 1) {
+            multi_dot(result, length, a, b);
+            return;
+        }
         dot_state& state = dot_st();
         HarnessStats& hs = harness_stats("b200_dot");
         Timer tm(hs);
@@ -608,6 +624,10 @@ extern "C" void b200_dot(double* result, std::int64_t length, const double* a, c
 namespace {
 
 void vec2_call(const char* name, std::int64_t n, double* y, double s, const double* x, bool axpy) {
+    if (harness_ngpus() > 1) {
+        multi_vec2(name, n, y, s, x, axpy);
+        return;
+    }
     vec2_state& state = vec2_st(name);
     HarnessStats& hs = harness_stats(name);
     Timer tm(hs);

@@ -248,13 +248,11 @@ int g_lrc_sms = 0;
 
 template <bool HOT, bool RMAP>
 void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
-    static bool attr = false;
+    static std::uint64_t attr = 0;
     const std::size_t smem = HOT ? sizeof(double) * static_cast<std::size_t>(kLrcHotMax + 2) : 0;
-    if (!attr) {
+    if (first_on_device(attr))
         B200_CUDA(cudaFuncSetAttribute(k_spmv_lrc<HOT, RMAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
-        attr = true;
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(std::min<std::int64_t>(g_lrc_sms, (L.units + kLrcWarps - 1) / kLrcWarps)));
     cfg.blockDim = dim3(kLrcThreads);

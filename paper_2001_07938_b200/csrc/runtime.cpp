@@ -165,9 +165,92 @@ void pool_trim() {
 
 // ---- runtime ------------------------------------------------------------------
 
-Runtime& rt() {
+namespace {
+thread_local Runtime* tl_rt = nullptr;  // a DeviceScope's runtime
+Runtime& primary_rt() {
     static Runtime r;
     return r;
+}
+std::map<int, std::unique_ptr<Runtime>>& secondary_rts() {
+    static auto* m = new std::map<int, std::unique_ptr<Runtime>>;  // outlives atexit teardown
+    return *m;
+}
+}  // namespace
+
+Runtime& rt() { return tl_rt ? *tl_rt : primary_rt(); }
+
+int harness_ngpus() {
+    static const int k = [] {
+        const char* e = std::getenv("LILAC_B200_NGPUS");
+        return e && *e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    return k;
+}
+
+int shard_device(int g) {
+    ensure_init();
+    int count = 1;
+    B200_CUDA(cudaGetDeviceCount(&count));
+    return (primary_rt().device + g) % std::max(count, 1);
+}
+
+Runtime& device_runtime(int device) {
+    ensure_init();
+    Runtime& p = primary_rt();
+    if (device == p.device) return p;
+    auto& m = secondary_rts();
+    auto it = m.find(device);
+    if (it != m.end()) return *it->second;
+    auto r = std::make_unique<Runtime>();
+    Runtime* prev = tl_rt;
+    int prev_dev = 0;
+    B200_CUDA(cudaGetDevice(&prev_dev));
+    B200_CUDA(cudaSetDevice(device));
+    r->device = device;
+    B200_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+    B200_CUDA(cudaEventCreate(&r->ev_k0));
+    B200_CUDA(cudaEventCreate(&r->ev_k1));
+    {
+        void* h = nullptr;
+        B200_CUDA(cudaHostAlloc(&h, 128, cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(h, 0, 128);
+        r->h_slot_val = static_cast<double*>(h);
+        r->h_slot_flag = reinterpret_cast<unsigned*>(static_cast<char*>(h) + 64);
+        void* d = nullptr;
+        B200_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+        r->dslot.value = static_cast<double*>(d);
+        r->dslot.flag = reinterpret_cast<unsigned*>(static_cast<char*>(d) + 64);
+    }
+    r->inited = true;
+    tl_rt = r.get();  // the scratch below is allocated on `device`
+    r->partials.ensure(sizeof(double) * kMaxParts * 4);
+    r->scalars.ensure(4096);
+    r->flags.ensure(64);
+    B200_CUDA(cudaMemsetAsync(r->scalars.ptr, 0, 4096, r->stream));
+    B200_CUDA(cudaStreamSynchronize(r->stream));
+    tl_rt = prev;
+    B200_CUDA(cudaSetDevice(prev_dev));
+    Runtime& out = *r;
+    m.emplace(device, std::move(r));
+    return out;
+}
+
+DeviceScope::DeviceScope(int device) : prev(tl_rt) {
+    Runtime& r = device_runtime(device);
+    const Runtime& p = primary_rt();
+    // the primary's settings
+    r.kernel = p.kernel;
+    r.strategy = p.strategy;
+    r.exact_blas = p.exact_blas;
+    r.stage_bytes = p.stage_bytes;
+    B200_CUDA(cudaGetDevice(&prev_dev));
+    B200_CUDA(cudaSetDevice(r.device));
+    tl_rt = &r;
+}
+
+DeviceScope::~DeviceScope() {
+    tl_rt = prev;
+    (void)cudaSetDevice(prev_dev);
 }
 
 static void at_exit_teardown() { shutdown(); }
@@ -246,10 +329,21 @@ double wait_host_slot(unsigned seq) {
 }
 
 void shutdown() {
-    Runtime& r = rt();
+    Runtime& r = primary_rt();
     lilac::marshal::release_all();
     mirrors_clear();
     if (!r.inited) return;
+    for (auto& kv : secondary_rts()) {
+        Runtime& q = *kv.second;
+        (void)cudaSetDevice(q.device);
+        for (DevBuf* b : {&q.partials, &q.scalars, &q.flags, &q.stage}) b->release();
+        if (q.h_slot_val) cudaFreeHost(q.h_slot_val);
+        if (q.ev_k0) cudaEventDestroy(q.ev_k0);
+        if (q.ev_k1) cudaEventDestroy(q.ev_k1);
+        if (q.stream) cudaStreamDestroy(q.stream);
+    }
+    secondary_rts().clear();
+    (void)cudaSetDevice(r.device);
     r.partials.release();
     r.scalars.release();
     r.flags.release();

@@ -79,6 +79,23 @@ struct Runtime {
 };
 
 Runtime& rt();
+// Multi-device harness path (LILAC_B200_NGPUS = k >= 2): every device but
+// the primary gets its own runtime (stream, scratch, result slot) carrying the
+// primary's settings. While a DeviceScope is alive, this thread's rt() is the
+// scope device's runtime and that device is current, so every upload / build /
+// launch helper works on it unchanged.
+Runtime& device_runtime(int device);
+struct DeviceScope {
+    Runtime* prev;
+    int prev_dev = 0;
+    explicit DeviceScope(int device);
+    ~DeviceScope();
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
+// LILAC_B200_NGPUS (>= 1; read once) and the device of shard g (g mod visible)
+int harness_ngpus();
+int shard_device(int g);
 void ensure_init();  // lazy first-call init + atexit teardown
 // Spin until the kernel that was given HostSlot seq `seq` posted its value
 // (checking the stream for errors now and then); returns the value.

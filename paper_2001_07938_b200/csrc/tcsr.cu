@@ -580,13 +580,12 @@ int g_sms = 0;
 template <int MODE>
 void launch_variant(const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
                     CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
-    static bool configured = false;
-    if (!configured) {
+    static std::uint64_t configured = 0;
+    if (first_on_device(configured)) {
         B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<false, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kTileSmemBudget));
         B200_CUDA(cudaFuncSetAttribute(k_spmv_tiled<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kTileSmemBudget));
-        configured = true;
     }
     if (partials)
         launch_pdl(k_spmv_tiled<true, MODE>, dim3(std::min<unsigned>(grid, kMaxParts)), dim3(kTileThreads),
@@ -646,6 +645,9 @@ bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream
         max_grid = coop ? per_sm * sms : 0;
         if (max_grid <= 0) enabled = 0;
     }
+    static std::uint64_t configured = 0;
+    if (enabled && first_on_device(configured))
+        B200_CUDA(cudaFuncSetAttribute(k_cg_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBudget));
     if (!enabled || steps <= 0 || T.ntiles <= 0 || v.row0 != 0 || v.p != v.p_full) return false;
     const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>({T.ntiles, max_grid, kMaxParts}));
     B200_CUDA(cudaMemsetAsync(&v.sc->bar, 0, sizeof(unsigned), s));
