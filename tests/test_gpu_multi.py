@@ -60,7 +60,7 @@ out["spmv_changed"] = bool(np.all(np.abs(y3 - O.spmv_csr(rp, ci, val, x))
 a = rng.uniform(-1, 1, 100003)
 b = rng.uniform(-1, 1, 100003)
 d = H.dotproduct(len(a), a, b)
-out["dot"] = abs(d - O.dot(a, b)) <= 1e-12 * O.dot(np.abs(a), np.abs(b))
+out["dot"] = bool(abs(d - O.dot(a, b)) <= 1e-12 * O.dot(np.abs(a), np.abs(b)))
 yy = b.copy()
 H.axpy(len(a), yy, 0.5, a)
 out["axpy"] = bool(O.same_bits(yy, O.axpy(b, 0.5, a)))
