@@ -405,8 +405,10 @@ void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter) {
     if (bytes == 0) return;
     if (rt().lazy_writeback) {
         PhaseTimer pt(kPhPublish);
-        if (mirror_publish_lazy(host, bytes, d.buf)) {
-            counter.lazy += static_cast<std::int64_t>(bytes);
+        std::size_t eager = 0;  // the partial edge pages of an unaligned output, written now
+        if (mirror_publish_lazy(host, bytes, d.buf, &eager)) {
+            counter.lazy += static_cast<std::int64_t>(bytes - eager);
+            counter.d2h += static_cast<std::int64_t>(eager);
             return;
         }
     }
@@ -467,8 +469,11 @@ std::int64_t g_lazy_deferred = 0, g_lazy_filled = 0;
 void mirror_fill(lilac::marshal::DeferredRange* d) {
     auto* m = static_cast<Mirror*>(d->ctx);
     const std::size_t bytes = d->content_hi - d->content_lo;
+    // the lazy bytes start content_lo - base into the mirror (an unaligned
+    // output defers only its whole interior pages)
+    const std::size_t off = d->content_lo - reinterpret_cast<std::uintptr_t>(m->reg.ref.base);
     Runtime& r = rt();
-    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(d->content_lo), m->buf->ptr, bytes,
+    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(d->content_lo), m->buf->as<const char>() + off, bytes,
                                     cudaMemcpyDeviceToHost, r.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r.stream);
     if (e != cudaSuccess) {
@@ -545,12 +550,19 @@ void mirror_publish(const void* host, std::size_t bytes, DevBuf& src) {
     g_mirrors.emplace(h, std::move(m));
 }
 
-bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src) {
+bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::size_t* eager) {
     const auto h = reinterpret_cast<std::uintptr_t>(host);
     const std::size_t pg = lilac::marshal::page_size();
-    if (!mirrors_enabled() || bytes < kMirrorMin || h % pg != 0) return false;
+    if (eager) *eager = 0;
+    if (!mirrors_enabled() || bytes < kMirrorMin) return false;
+    const bool aligned = h % pg == 0;
+    // an unaligned output (every malloc'd array): its whole interior pages are
+    // deferred; the partial pages at either end hold neighbouring data and are
+    // written eagerly (<= 2 small copies) so nothing but our bytes is PROT_NONE
+    const std::uintptr_t ilo = (h + pg - 1) / pg * pg, ihi = (h + bytes) / pg * pg;
+    if (!aligned && ihi < ilo + pg) return false;  // not one whole page inside
     auto same = g_mirrors.find(h);
-    if (same != g_mirrors.end() && same->second->reg.ref.bytes == bytes && same->second->lazy.active &&
+    if (aligned && same != g_mirrors.end() && same->second->reg.ref.bytes == bytes && same->second->lazy.active &&
         lilac::marshal::reclean_covered(same->second->reg)) {
         // steady state (rewritten before the host looked): swap in the new
         // device bytes; pages stay PROT_NONE, no system call
@@ -563,13 +575,28 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src) {
     }
     drop_overlapping(h, bytes);
     if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
+    std::size_t edges = 0;
+    if (!aligned) {
+        // the edge bytes land first: the Hybrid guard below snapshots them
+        lilac::marshal::supersede_range(host, bytes);
+        Runtime& r = rt();
+        if (ilo > h)
+            B200_CUDA(cudaMemcpyAsync(const_cast<void*>(host), src.ptr, ilo - h, cudaMemcpyDeviceToHost, r.stream));
+        if (h + bytes > ihi)
+            B200_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(ihi), src.as<char>() + (ihi - h), h + bytes - ihi,
+                                      cudaMemcpyDeviceToHost, r.stream));
+        B200_CUDA(cudaStreamSynchronize(r.stream));
+        edges = (ilo - h) + (h + bytes - ihi);
+    }
     auto m = std::make_unique<Mirror>();
     m->reg.ref = {host, bytes, nullptr};
-    m->reg.strategy = lilac::marshal::Strategy::PageProtect;  // whole pages: no edge reads of lazy bytes
-    m->lazy.lo = h;
-    m->lazy.hi = (h + bytes + pg - 1) / pg * pg;
-    m->lazy.content_lo = h;
-    m->lazy.content_hi = h + bytes;
+    // whole pages: PageProtect (no edge reads of lazy bytes); unaligned: Hybrid
+    // guards the interior and snapshots the (eagerly written) edges
+    m->reg.strategy = aligned ? lilac::marshal::Strategy::PageProtect : lilac::marshal::Strategy::Hybrid;
+    m->lazy.lo = aligned ? h : ilo;
+    m->lazy.hi = aligned ? (h + bytes + pg - 1) / pg * pg : ihi;
+    m->lazy.content_lo = aligned ? h : ilo;
+    m->lazy.content_hi = aligned ? h + bytes : ihi;
     m->lazy.fill = mirror_fill;
     m->lazy.ctx = m.get();
     m->buf = steal(src, bytes);  // before defer_range: a fill needs the bytes
@@ -586,9 +613,10 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src) {
         const_cast<DevBuf&>(*m->buf) = DevBuf{};
         return false;
     }
-    g_lazy_deferred += static_cast<std::int64_t>(bytes);
+    g_lazy_deferred += static_cast<std::int64_t>(m->lazy.content_hi - m->lazy.content_lo);
     g_mirror_total += m->buf->cap;
     g_mirrors.emplace(h, std::move(m));
+    if (eager) *eager = edges;
     return true;
 }
 

@@ -209,7 +209,8 @@ def lazy_counters():
 
 def page_aligned(n, dtype=np.float64):
     """A zeroed array whose data starts on a page boundary (lazy write-back
-    applies to page-aligned outputs; numpy's malloc'd arrays are not)."""
+    defers every whole page of an output; on an unaligned array the two
+    partial edge pages are written at once)."""
     import mmap
     dt = np.dtype(dtype)
     nbytes = max(int(n) * dt.itemsize, 1)

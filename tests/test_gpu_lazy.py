@@ -162,3 +162,37 @@ def test_cg_lazy_bit_identical_to_eager_and_device_resident():
     # eager mode moves every vector on every call
     h2d = sum(s1[k] - s0.get(k, 0) for k in s1)
     assert h2d <= 8 * n * 8, h2d
+
+
+@pytest.mark.parametrize("offset", [8, 16, 1000, 4088])
+def test_unaligned_output_defers_interior_pages(offset):
+    """A malloc'd-style output (not page aligned): the whole interior pages are
+    deferred, the two partial edge pages written at once; the values read
+    back equal the oracle's bit for bit, and neighbours on the edge pages are
+    untouched."""
+    rows = 30_000
+    rp, ci, val = rand_csr(rows, rows, 6, 21)
+    x = np.random.default_rng(3).uniform(-1, 1, rows)
+    base = H.page_aligned(rows + 1024)
+    start = offset // 8
+    y = base[start:start + rows]
+    assert y.ctypes.data % 4096 == offset % 4096
+    base[:start] = 7.0
+    base[start + rows:] = 9.0
+    N.lib().b200_set_kernel(b"exact")
+    try:
+        c0 = H.lazy_counters()
+        H.spmv_csr(rows, y, rp, val, x, ci)
+        c1 = H.lazy_counters()
+        assert c1["ranges"] == c0["ranges"] + 1
+        interior = ((y.ctypes.data + rows * 8) // 4096 - (y.ctypes.data + 4095) // 4096) * 4096
+        assert c1["bytes_deferred"] - c0["bytes_deferred"] == interior
+        assert np.all(base[:start] == 7.0) and np.all(base[start + rows:] == 9.0)  # neighbours: no fault, intact
+        ref = O.spmv_csr(rp, ci, val, x, rows)
+        assert O.same_bits(y, ref)
+        # chained: the unaligned output feeds the next call device-to-device
+        z = np.zeros(rows)
+        H.spmv_csr(rows, z, rp, val, y, ci)
+        assert O.same_bits(z, O.spmv_csr(rp, ci, val, ref, rows))
+    finally:
+        N.lib().b200_set_kernel(b"auto")
