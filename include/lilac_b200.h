@@ -168,6 +168,12 @@ void b200_stats_reset(void);
 /* Change-detection cost counters since process start: SIGSEGV traps taken,
  * mprotect calls, bytes hashed; and device bytes currently held as mirrors. */
 int b200_marshal_counters(int64_t* faults, int64_t* mprotects, int64_t* hash_bytes, int64_t* mirror_bytes);
+/* Guarded caller regions found in DMA-reachable host memory (CUDA-pinned,
+ * registered or managed). Page guards see CPU stores only: if another library
+ * writes such an array by DMA or from a kernel, the resident copy would go
+ * stale. Either call b200_host_forget on it after such a write, or run with
+ * LILAC_B200_PINNED=always (those regions are then re-marshaled every call). */
+int64_t b200_dma_visible_regions(void);
 /* Host-side phase accumulators (ns, counts), collected while profiling is on
  * (b200_set_profiling): mirror fetch, mirror poll, D2D, H2D, D2H+sync, mirror
  * publish, publish guard, acquire (axpy/xpay inputs), launch, binding pick,

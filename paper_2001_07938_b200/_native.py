@@ -68,6 +68,7 @@ SIGNATURES = {
     "b200_harness_stats_get": (C.c_int, [C.POINTER(HarnessStats), C.c_int]),
     "b200_stats_reset": (None, []),
     "b200_marshal_counters": (C.c_int, [i64p, i64p, i64p, i64p]),
+    "b200_dma_visible_regions": (i64, []),
     "b200_host_profile": (C.c_int, [i64p, i64p, C.c_int]),
     # 4. resident device API
     "b200_matrix_create_csr": (C.c_int, [C.POINTER(vp), i64, i64p, i64p, f64p]),

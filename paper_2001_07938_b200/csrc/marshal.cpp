@@ -59,6 +59,9 @@ volatile long g_stat_faults = 0, g_stat_mprotect = 0, g_stat_hash_bytes = 0;
 volatile long g_def_n = 0, g_def_fault_fills = 0, g_def_explicit_fills = 0, g_def_cancelled = 0;
 struct sigaction g_prev;
 bool g_prev_valid = false;
+bool (*g_dma_probe)(const void*) = nullptr;  // set_dma_probe
+bool g_dma_always = false;
+long g_dma_regions = 0;
 
 // mprotect(RW) over [lo, hi). A stale range over memory the caller freed may
 // contain unmapped holes (a trimmed heap); mprotect then fails as a whole at
@@ -393,6 +396,11 @@ std::size_t page_size() {
 }
 
 void mark_clean(TrackedRegion& r) {
+    if ((r.strategy == Strategy::PageProtect || r.strategy == Strategy::Hybrid) && g_dma_probe && r.ref.bytes) {
+        const bool v = g_dma_probe(r.ref.base);
+        if (v && !r.dma_visible) g_dma_regions = g_dma_regions + 1;
+        r.dma_visible = v;
+    }
     switch (r.strategy) {
     case Strategy::Naive:
         r.dirty = true;  // untracked: never clean
@@ -464,7 +472,14 @@ void mark_clean(TrackedRegion& r) {
     }
 }
 
+void set_dma_probe(bool (*probe)(const void*)) { g_dma_probe = probe; }
+void set_dma_always_dirty(bool on) { g_dma_always = on; }
+long dma_visible_regions() { return g_dma_regions; }
+
 bool poll_dirty(TrackedRegion& r) {
+    if (r.dma_visible && g_dma_always &&
+        (r.strategy == Strategy::PageProtect || r.strategy == Strategy::Hybrid))
+        return true;  // a DMA / device write would not fault: do not trust the guard
     switch (r.strategy) {
     case Strategy::Naive:
         return true;

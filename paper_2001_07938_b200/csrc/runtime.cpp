@@ -303,6 +303,18 @@ void ensure_init() {
     r.strategy = lilac::marshal::default_strategy(Strategy::Hybrid);
     const char* wb = std::getenv("LILAC_B200_WRITEBACK");
     if (wb && std::strcmp(wb, "lazy") == 0) r.lazy_writeback = true;
+    // page guards see CPU stores only: tell the marshaling layer which host
+    // memory DMA or device stores can reach (pinned / registered / managed)
+    lilac::marshal::set_dma_probe([](const void* p) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+    });
+    const char* pin = std::getenv("LILAC_B200_PINNED");
+    lilac::marshal::set_dma_always_dirty(pin && std::strcmp(pin, "always") == 0);
     // registered after the CUDA runtime initialised, so it runs before the
     // runtime's own teardown (mirrors harnessgen.cpp:98-113)
     std::atexit(at_exit_teardown);
@@ -850,6 +862,8 @@ int b200_marshal_counters(int64_t* faults, int64_t* mprotects, int64_t* hash_byt
     if (mirror_bytes) *mirror_bytes = b200::mirror_bytes();
     return 0;
 }
+
+int64_t b200_dma_visible_regions(void) { return lilac::marshal::dma_visible_regions(); }
 
 void b200_stats_reset(void) {
     for (HarnessStats* h : all_harness_stats()) {

@@ -106,3 +106,49 @@ def test_npb_host_cg_class_a_on_two_gpus():
     harness calls) unchanged, LILAC_B200_NGPUS=2: zeta verifies."""
     out = run(NPB, 2)
     assert out["ok"] is True, out
+
+
+PINNED = """
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, "tests")
+import oracle_lib as O
+from paper_2001_07938_b200 import harness as H, _native as N
+H.set_errors_return(True)
+n = 20000
+rng = np.random.default_rng(8)
+lens = rng.integers(1, 20, n)
+rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+ci = rng.integers(0, n, int(rp[-1])).astype(np.int64)
+val_t = torch.from_numpy(rng.uniform(-1, 1, int(rp[-1]))).pin_memory()
+val = val_t.numpy()                 # a pinned input array
+x = rng.uniform(-1, 1, n)
+y = np.zeros(n)
+H.spmv_csr(n, y, rp, val, x, ci)
+before = N.lib().b200_dma_visible_regions()
+# another library writes the pinned matrix by DMA: no page fault sees it
+src = torch.from_numpy(val * 2.0).cuda()
+val_t.copy_(src)
+torch.cuda.synchronize()
+y2 = np.zeros(n)
+H.spmv_csr(n, y2, rp, val, x, ci)
+ref2 = O.spmv_csr(rp, ci, val, x)
+bound = O.spmv_csr(rp, ci, np.abs(val), np.abs(x))
+print(json.dumps({"detected": int(before), "fresh": bool(np.all(np.abs(y2 - ref2) <= 1e-12 * bound))}))
+"""
+
+
+def test_pinned_inputs_detected_and_always_policy():
+    """A pinned input written by DMA after it was marshaled: the region is
+    counted as DMA-visible, and under LILAC_B200_PINNED=always the next call
+    re-marshals it (fresh result)."""
+    env_old = os.environ.get("LILAC_B200_PINNED")
+    os.environ["LILAC_B200_PINNED"] = "always"
+    try:
+        out = run(PINNED, 1)
+    finally:
+        if env_old is None:
+            os.environ.pop("LILAC_B200_PINNED", None)
+        else:
+            os.environ["LILAC_B200_PINNED"] = env_old
+    assert out["detected"] >= 1 and out["fresh"] is True, out
