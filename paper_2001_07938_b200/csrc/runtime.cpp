@@ -568,13 +568,8 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::
     if (eager) *eager = 0;
     if (!mirrors_enabled() || bytes < kMirrorMin) return false;
     const bool aligned = h % pg == 0;
-    // an unaligned output (every malloc'd array): its whole interior pages are
-    // deferred; the partial pages at either end hold neighbouring data and are
-    // written eagerly (<= 2 small copies) so nothing but our bytes is PROT_NONE
-    const std::uintptr_t ilo = (h + pg - 1) / pg * pg, ihi = (h + bytes) / pg * pg;
-    if (!aligned && ihi < ilo + pg) return false;  // not one whole page inside
     auto same = g_mirrors.find(h);
-    if (aligned && same != g_mirrors.end() && same->second->reg.ref.bytes == bytes && same->second->lazy.active &&
+    if (same != g_mirrors.end() && same->second->reg.ref.bytes == bytes && same->second->lazy.active &&
         lilac::marshal::reclean_covered(same->second->reg)) {
         // steady state (rewritten before the host looked): swap in the new
         // device bytes; pages stay PROT_NONE, no system call
@@ -587,35 +582,27 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::
     }
     drop_overlapping(h, bytes);
     if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
-    std::size_t edges = 0;
-    if (!aligned) {
-        // the edge bytes land first: the Hybrid guard below snapshots them
-        lilac::marshal::supersede_range(host, bytes);
-        Runtime& r = rt();
-        if (ilo > h)
-            B200_CUDA(cudaMemcpyAsync(const_cast<void*>(host), src.ptr, ilo - h, cudaMemcpyDeviceToHost, r.stream));
-        if (h + bytes > ihi)
-            B200_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(ihi), src.as<char>() + (ihi - h), h + bytes - ihi,
-                                      cudaMemcpyDeviceToHost, r.stream));
-        B200_CUDA(cudaStreamSynchronize(r.stream));
-        edges = (ilo - h) + (h + bytes - ihi);
-    }
     auto m = std::make_unique<Mirror>();
     m->reg.ref = {host, bytes, nullptr};
-    // whole pages: PageProtect (no edge reads of lazy bytes); unaligned: Hybrid
-    // guards the interior and snapshots the (eagerly written) edges
+    // Every page the bytes touch is deferred (PROT_NONE); only our bytes are
+    // ever filled, so a neighbour sharing an edge page (an unaligned,
+    // malloc'd array) reads correctly after a one-time fault. Aligned:
+    // PageProtect; unaligned: Hybrid, which guards a lazy edge page whole
+    // instead of snapshotting it.
     m->reg.strategy = aligned ? lilac::marshal::Strategy::PageProtect : lilac::marshal::Strategy::Hybrid;
-    m->lazy.lo = aligned ? h : ilo;
-    m->lazy.hi = aligned ? (h + bytes + pg - 1) / pg * pg : ihi;
-    m->lazy.content_lo = aligned ? h : ilo;
-    m->lazy.content_hi = aligned ? h + bytes : ihi;
+    m->lazy.lo = h / pg * pg;
+    m->lazy.hi = (h + bytes + pg - 1) / pg * pg;
+    m->lazy.content_lo = h;
+    m->lazy.content_hi = h + bytes;
     m->lazy.fill = mirror_fill;
     m->lazy.ctx = m.get();
     m->buf = steal(src, bytes);  // before defer_range: a fill needs the bytes
     try {
         PhaseTimer pt(kPhPublishGuard);
-        lilac::marshal::mark_clean(m->reg);
+        // deferred first: the guard then sees the lazy edge pages and guards
+        // them whole instead of snapshotting (reading) their stale bytes
         lilac::marshal::defer_range(m->lazy);
+        lilac::marshal::mark_clean(m->reg);
     } catch (const Error&) {
         lilac::marshal::retire_deferred(m->lazy, false);
         lilac::marshal::drop_guard(m->reg);
@@ -625,10 +612,9 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::
         const_cast<DevBuf&>(*m->buf) = DevBuf{};
         return false;
     }
-    g_lazy_deferred += static_cast<std::int64_t>(m->lazy.content_hi - m->lazy.content_lo);
+    g_lazy_deferred += static_cast<std::int64_t>(bytes);
     g_mirror_total += m->buf->cap;
     g_mirrors.emplace(h, std::move(m));
-    if (eager) *eager = edges;
     return true;
 }
 

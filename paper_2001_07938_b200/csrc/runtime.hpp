@@ -152,10 +152,9 @@ inline void host_in(const void* p, std::size_t bytes) { lilac::marshal::material
 void upload(DevArray& d, const void* host, std::size_t bytes);
 // download: D2H write-back; then publishes a device mirror of the host region
 // (the mirror takes d's buffer; d gets a fresh one from the pool).
-// Lazy mode (regions >= 8 KiB with at least one whole page): no D2H of the
-// whole pages — the mirror is published with them PROT_NONE and the bytes land
-// on first touch; the partial pages at an unaligned region's ends are written
-// at once.
+// Lazy mode (regions >= 8 KiB): no D2H — the mirror is published with every
+// page the region touches PROT_NONE, and its bytes land on the first touch of
+// any of those pages (a neighbour on an unaligned region's edge page included).
 void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter);
 
 // Device mirrors (the coherence layer of SURVEY §8(f)1): after a write-back the
@@ -164,7 +163,7 @@ void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter);
 // of (a sub-range of) it is served device-to-device. LILAC_B200_MIRRORS=0 off.
 bool mirror_fetch(DevArray& d, const void* host, std::size_t bytes);
 void mirror_publish(const void* host, std::size_t bytes, DevBuf& src);
-// *eager: bytes of an unaligned output's partial edge pages written at once
+// *eager: bytes written back at once (0: all deferred)
 bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::size_t* eager = nullptr);
 void lazy_bytes(std::int64_t* deferred, std::int64_t* filled);
 void mirrors_clear();                                    // lazy bytes filled first

@@ -110,7 +110,9 @@ def test_host_sync_materialises_for_dma():
     assert H.lazy_counters()["fault_fills"] == c1["fault_fills"]  # already real: no fault
 
 
-def test_misaligned_output_falls_back_to_eager():
+def test_misaligned_output_is_lazy():
+    """8 bytes past a page boundary: every page the output touches is lazy,
+    nothing goes back at the call; the values fill on the first touch."""
     rows = 20_000
     rp, ci, val = rand_csr(rows, rows, 4, 15)
     x = np.random.default_rng(5).uniform(-1, 1, rows)
@@ -119,8 +121,10 @@ def test_misaligned_output_falls_back_to_eager():
     c0 = H.lazy_counters()
     s0 = H.harness_stats()["b200_spmv_csr"]
     H.spmv_csr(rows, y, rp, val, x, ci)
-    assert H.lazy_counters()["ranges"] == c0["ranges"]
-    assert H.harness_stats()["b200_spmv_csr"]["bytes_d2h"] - s0["bytes_d2h"] == rows * 8
+    assert H.lazy_counters()["ranges"] == c0["ranges"] + 1
+    assert H.harness_stats()["b200_spmv_csr"]["bytes_d2h"] - s0["bytes_d2h"] == 0
+    ref = O.spmv_csr(rp, ci, val, x, rows)
+    assert (np.abs(y - ref) <= 1e-12 * O.spmv_csr(rp, ci, np.abs(val), np.abs(x), rows)).all()
 
 
 def _host_cg(n, rp, ci, val, alloc, iters=25):
@@ -165,11 +169,11 @@ def test_cg_lazy_bit_identical_to_eager_and_device_resident():
 
 
 @pytest.mark.parametrize("offset", [8, 16, 1000, 4088])
-def test_unaligned_output_defers_interior_pages(offset):
-    """A malloc'd-style output (not page aligned): the whole interior pages are
-    deferred, the two partial edge pages written at once; the values read
-    back equal the oracle's bit for bit, and neighbours on the edge pages are
-    untouched."""
+def test_unaligned_output_neighbours_and_chaining(offset):
+    """A malloc'd-style output (not page aligned): all its pages are lazy
+    (PROT_NONE); a neighbour sharing an edge page reads its own bytes intact
+    after a one-time fault that fills only the output's bytes; the output
+    equals the oracle bit for bit and feeds the next call device-to-device."""
     rows = 30_000
     rp, ci, val = rand_csr(rows, rows, 6, 21)
     x = np.random.default_rng(3).uniform(-1, 1, rows)
@@ -185,14 +189,32 @@ def test_unaligned_output_defers_interior_pages(offset):
         H.spmv_csr(rows, y, rp, val, x, ci)
         c1 = H.lazy_counters()
         assert c1["ranges"] == c0["ranges"] + 1
-        interior = ((y.ctypes.data + rows * 8) // 4096 - (y.ctypes.data + 4095) // 4096) * 4096
-        assert c1["bytes_deferred"] - c0["bytes_deferred"] == interior
-        assert np.all(base[:start] == 7.0) and np.all(base[start + rows:] == 9.0)  # neighbours: no fault, intact
+        assert c1["bytes_deferred"] - c0["bytes_deferred"] == rows * 8
+        assert np.all(base[start + rows:] == 9.0) and np.all(base[:start] == 7.0)  # neighbours intact
         ref = O.spmv_csr(rp, ci, val, x, rows)
         assert O.same_bits(y, ref)
-        # chained: the unaligned output feeds the next call device-to-device
+        # a fresh output chained from the (now filled) one
         z = np.zeros(rows)
         H.spmv_csr(rows, z, rp, val, y, ci)
         assert O.same_bits(z, O.spmv_csr(rp, ci, val, ref, rows))
     finally:
         N.lib().b200_set_kernel(b"auto")
+
+
+def test_unaligned_chain_stays_on_device():
+    """y = A x into an unaligned output, then z = A y without touching y: y is
+    served device-to-device and never filled."""
+    rows = 30_000
+    rp, ci, val = rand_csr(rows, rows, 6, 23)
+    x = np.random.default_rng(4).uniform(-1, 1, rows)
+    y = H.page_aligned(rows + 2)[1:rows + 1]
+    z = H.page_aligned(rows + 2)[1:rows + 1]
+    c0 = H.lazy_counters()
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    H.spmv_csr(rows, z, rp, val, y, ci)
+    c1 = H.lazy_counters()
+    assert c1["bytes_filled"] == c0["bytes_filled"]  # y never came back
+    yr = O.spmv_csr(rp, ci, val, x, rows)
+    zr = O.spmv_csr(rp, ci, val, yr, rows)
+    bound = O.spmv_csr(rp, ci, np.abs(val), np.abs(yr), rows)
+    assert np.all(np.abs(z - zr) <= 1e-11 * bound + 1e-300)
