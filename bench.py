@@ -789,19 +789,19 @@ def run_npb(ctx, cls):
     line["gen_s"] = t_gen
 
     if ctx.world == 1 and not args.no_e2e:
-        lazy = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "lazy", "pageable")
-        lazy_pinned = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "lazy", "pinned")
+        lazy = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "lazy", "pinned")
+        lazy_pageable = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "lazy", "pageable")
         eager = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "eager", "pinned")
         default = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "eager", "pageable")
         line["e2e"] = lazy
-        line["e2e_lazy_pinned"] = lazy_pinned
+        line["e2e_lazy_pageable"] = lazy_pageable
         line["e2e_eager"] = eager
         line["e2e_default"] = default
-        line["e2e"]["note"] = ("headline: plain numpy (malloc'd, unaligned) host vectors with the opt-in lazy "
-                               "write-back (b200_set_writeback: whole pages deferred, edge pages written at once); "
-                               "e2e_default = the reference semantics an unmodified program gets (same vectors, "
-                               "eager write-back, default strategy); e2e_lazy_pinned / e2e_eager: pinned, "
-                               "page-aligned vectors")
+        line["e2e"]["note"] = ("headline: pinned page-aligned host vectors with the opt-in lazy write-back "
+                               "(b200_set_writeback); e2e_lazy_pageable: plain numpy (malloc'd, adjacent) vectors, "
+                               "lazy (an edge page shared with another vector in use is written at once); "
+                               "e2e_eager: pinned, eager; e2e_default = the reference semantics an unmodified "
+                               "program gets (plain numpy vectors, eager write-back, default strategy)")
     elif ctx.world > 1 and not args.no_e2e:
         line["e2e"] = e2e_dist(ctx, cg, shard_rows, shift, args.warmup, args.steps)
 
@@ -828,7 +828,7 @@ def run_npb(ctx, cls):
         # the e2e legs' zeta after W+K iterations from x=1, checked against the oracle's
         if "e2e" in line and zetas:
             zref = zetas[-1]
-            for k in ("e2e", "e2e_lazy_pinned", "e2e_eager", "e2e_default"):
+            for k in ("e2e", "e2e_lazy_pageable", "e2e_eager", "e2e_default"):
                 z = line[k]["zeta"]
                 line[k]["zeta_ref_oracle"] = zref
                 line[k]["zeta_verified"] = abs(z - zref) / abs(zref) <= 1e-10

@@ -472,6 +472,24 @@ void mark_clean(TrackedRegion& r) {
     }
 }
 
+bool page_shared(std::uintptr_t page, std::uintptr_t self_lo, std::uintptr_t self_hi) {
+    const std::uintptr_t pe = page + page_size();
+    // the parts of the page outside our bytes
+    const std::uintptr_t a0 = page, a1 = std::min(pe, std::max(page, self_lo));
+    const std::uintptr_t b0 = std::max(page, std::min(pe, self_hi)), b1 = pe;
+    auto hits = [&](std::uintptr_t lo, std::uintptr_t hi) {
+        return (a0 < a1 && lo < a1 && a0 < hi) || (b0 < b1 && lo < b1 && b0 < hi);
+    };
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (const TrackedRegion* r : g_tracked) {
+        const auto lo = reinterpret_cast<std::uintptr_t>(r->ref.base);
+        if (r->ref.bytes && hits(lo, lo + r->ref.bytes)) return true;
+    }
+    for (const DeferredRange* d : g_deferred)
+        if (d->active && hits(d->content_lo, d->content_hi)) return true;
+    return false;
+}
+
 void set_dma_probe(bool (*probe)(const void*)) { g_dma_probe = probe; }
 void set_dma_always_dirty(bool on) { g_dma_always = on; }
 long dma_visible_regions() { return g_dma_regions; }

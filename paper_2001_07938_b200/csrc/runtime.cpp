@@ -582,18 +582,49 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::
     }
     drop_overlapping(h, bytes);
     if (g_mirror_total + bytes > kMirrorLimit) mirrors_clear();
+    // The pages the bytes touch are deferred (PROT_NONE) and only our bytes are
+    // ever filled, so an unrelated neighbour on an edge page (malloc header,
+    // free space) reads correctly after a one-time fault. An edge page shared
+    // with another array in use (adjacent heap allocations) is written at once
+    // instead: making it lazy would fill this output on every access to the
+    // neighbour. Aligned: PageProtect; unaligned: Hybrid, which guards a lazy
+    // edge page whole and snapshots an eager one.
+    std::uintptr_t lo = h / pg * pg, hi = (h + bytes + pg - 1) / pg * pg;
+    std::uintptr_t clo = h, chi = h + bytes;
+    std::size_t edges = 0;
+    if (!aligned || (h + bytes) % pg) {
+        const std::uintptr_t last = (h + bytes - 1) / pg * pg;
+        const bool head = h % pg && lilac::marshal::page_shared(lo, h, h + bytes);
+        const bool tail = (h + bytes) % pg && lilac::marshal::page_shared(last, h, h + bytes) &&
+                          (last != lo || !head);
+        if (head) {
+            lo += pg;
+            clo = lo;
+        }
+        if (tail) {
+            hi = last;
+            chi = last;
+        }
+        if (hi <= lo || chi <= clo) return false;  // nothing left to defer
+        if (head || tail) {
+            Runtime& r = rt();
+            lilac::marshal::supersede_range(host, bytes);
+            if (head)
+                B200_CUDA(cudaMemcpyAsync(const_cast<void*>(host), src.ptr, clo - h, cudaMemcpyDeviceToHost, r.stream));
+            if (tail)
+                B200_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(chi), src.as<char>() + (chi - h), h + bytes - chi,
+                                          cudaMemcpyDeviceToHost, r.stream));
+            B200_CUDA(cudaStreamSynchronize(r.stream));
+            edges = (clo - h) + (h + bytes - chi);
+        }
+    }
     auto m = std::make_unique<Mirror>();
     m->reg.ref = {host, bytes, nullptr};
-    // Every page the bytes touch is deferred (PROT_NONE); only our bytes are
-    // ever filled, so a neighbour sharing an edge page (an unaligned,
-    // malloc'd array) reads correctly after a one-time fault. Aligned:
-    // PageProtect; unaligned: Hybrid, which guards a lazy edge page whole
-    // instead of snapshotting it.
     m->reg.strategy = aligned ? lilac::marshal::Strategy::PageProtect : lilac::marshal::Strategy::Hybrid;
-    m->lazy.lo = h / pg * pg;
-    m->lazy.hi = (h + bytes + pg - 1) / pg * pg;
-    m->lazy.content_lo = h;
-    m->lazy.content_hi = h + bytes;
+    m->lazy.lo = lo;
+    m->lazy.hi = hi;
+    m->lazy.content_lo = clo;
+    m->lazy.content_hi = chi;
     m->lazy.fill = mirror_fill;
     m->lazy.ctx = m.get();
     m->buf = steal(src, bytes);  // before defer_range: a fill needs the bytes
@@ -612,9 +643,10 @@ bool mirror_publish_lazy(const void* host, std::size_t bytes, DevBuf& src, std::
         const_cast<DevBuf&>(*m->buf) = DevBuf{};
         return false;
     }
-    g_lazy_deferred += static_cast<std::int64_t>(bytes);
+    g_lazy_deferred += static_cast<std::int64_t>(chi - clo);
     g_mirror_total += m->buf->cap;
     g_mirrors.emplace(h, std::move(m));
+    if (eager) *eager = edges;
     return true;
 }
 

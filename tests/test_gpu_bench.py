@@ -43,7 +43,7 @@ def check_line(line, config, steps, warmup):
 def test_bench_npb_a_line():
     line = run_bench("--config", "npb_a", "--steps", "4", "--warmup", "3", "--spmv-reps", "20")
     check_line(line, "npb_a", 4, 3)
-    for k in ("e2e", "e2e_lazy_pinned", "e2e_eager", "e2e_default"):
+    for k in ("e2e", "e2e_lazy_pageable", "e2e_eager", "e2e_default"):
         assert line[k]["zeta_verified"] is True, (k, line[k])
     assert line["e2e_default"]["memory"] == "pageable" and line["e2e_default"]["writeback"] == "eager"
     assert line["marshal_first_call"]["s"] > 0

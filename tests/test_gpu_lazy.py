@@ -218,3 +218,30 @@ def test_unaligned_chain_stays_on_device():
     zr = O.spmv_csr(rp, ci, val, yr, rows)
     bound = O.spmv_csr(rp, ci, np.abs(val), np.abs(yr), rows)
     assert np.all(np.abs(z - zr) <= 1e-11 * bound + 1e-300)
+
+
+def test_adjacent_outputs_share_edge_pages_without_thrashing():
+    """Three vectors packed back to back (as small heap allocations are): the
+    edge page each shares with a neighbour in use is written at once, the
+    rest stays lazy; a CG-style chain over them matches the eager results and
+    does not refill the outputs on every call."""
+    rows = 14_000  # 112 KB: heap-allocated by malloc, adjacent in practice
+    rp, ci, val = rand_csr(rows, rows, 6, 31)
+    buf = H.page_aligned(3 * rows + 64)[3:]
+    x, y, z = buf[:rows], buf[rows:2 * rows], buf[2 * rows:3 * rows]
+    x[:] = np.random.default_rng(9).uniform(-1, 1, rows)
+    c0 = H.lazy_counters()
+    for _ in range(5):
+        H.spmv_csr(rows, y, rp, val, x, ci)
+        H.spmv_csr(rows, z, rp, val, y, ci)
+        d = H.dotproduct(rows, y, z)
+    c1 = H.lazy_counters()
+    yr = O.spmv_csr(rp, ci, val, x, rows)
+    zr = O.spmv_csr(rp, ci, val, yr, rows)
+    b1 = O.spmv_csr(rp, ci, np.abs(val), np.abs(x), rows)
+    assert np.all(np.abs(y - yr) <= 1e-12 * b1)
+    assert abs(d - O.dot(yr, zr)) <= 1e-9 * O.dot(np.abs(yr), np.abs(zr))
+    # the chain stayed on the device: at most the one fill when z's first
+    # write-back meets y's still-lazy tail page (from then on that shared page
+    # is written at once)
+    assert c1["explicit_fills"] - c0["explicit_fills"] <= 1
