@@ -577,13 +577,18 @@ class Ctx:
         return self.max_over_ranks(e0.elapsed_time(e1)), clk
 
     def kernel_ms(self, launch, reps):
-        """Mean CUDA-event time of `reps` back-to-back launches on the bench stream."""
+        """Mean CUDA-event time of `reps` back-to-back launches on the bench
+        stream. A spin kernel ahead of the first event holds the stream until
+        every launch is queued, so the host's per-call cost (ctypes, ~10 us)
+        never shows up as GPU idle time between small kernels."""
         import torch
         for _ in range(5):
             launch()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        with torch.cuda.stream(self.stream):
+            torch.cuda._sleep(int(2e6) + reps * 40000)  # ~1 ms + 20 us per launch at 1.9 GHz
         e0.record(self.stream)
         for _ in range(reps):
             launch()
@@ -874,6 +879,7 @@ def run_parboil(ctx):
     with torch.cuda.stream(ctx.stream):
         for e0, e1 in ev:
             flush.zero_()
+            torch.cuda._sleep(200000)  # holds the stream while the launch is queued (no host gap inside e0..e1)
             e0.record(ctx.stream)
             A.spmv(x.data_ptr(), y.data_ptr(), ctx.sh)
             e1.record(ctx.stream)

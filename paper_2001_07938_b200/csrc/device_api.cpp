@@ -17,7 +17,6 @@ struct b200_matrix {
     int device = -1;
     DevBuf row_ptr, col, val;             // CSR
     DevBuf nzcnt, perm, inv_perm, jd_ptr;  // JDS (+col, val)
-    DevBuf prod;                           // JDS product scratch (two-phase kernel)
     CsrDev csr;
     JdsDev jds;
     TcsrOwner tiled;
@@ -147,8 +146,7 @@ int b200_matrix_create_jds(b200_matrix** out, std::int64_t rows, const std::int6
         d.col = A->col.ptr;
         d.col32 = col32;
         d.val = A->val.as<double>();
-        A->prod.ensure(sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(nnz, 1)), false);
-        d.prod = A->prod.as<double>();
+        d.nlong = jds_long_rows(rows, nzcnt);
         A->max_row = max_nz;
         *out = A.release();
     });
@@ -168,7 +166,6 @@ void b200_matrix_free(b200_matrix* A) {
     A->perm.release();
     A->inv_perm.release();
     A->jd_ptr.release();
-    A->prod.release();
     A->tiled.release();
     A->merge.release();
     A->split.release();

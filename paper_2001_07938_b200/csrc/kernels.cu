@@ -26,6 +26,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kSMs = 148;
 constexpr int kJdsU = 16;  // JDS diagonals in flight per thread
+#ifndef LILAC_JDS_MINB
+#define LILAC_JDS_MINB 4  // 4 CTAs per SM (64 registers): the Parboil shape's 571 CTAs in one wave
+#endif
 
 // ---- load helpers -----------------------------------------------------------
 
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_exact(std::int64_t rows,
 
 // JDS, thread per jagged row j (coalesced over j); y scattered through inv_perm.
 template <typename IdxT>
-__global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
+__global__ void __launch_bounds__(kThreads, LILAC_JDS_MINB) k_jds(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
                                                   const std::int64_t* __restrict__ inv_perm,
                                                   const std::int64_t* __restrict__ jd_ptr,
                                                   const IdxT* __restrict__ col,
@@ -447,28 +450,13 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
     for (std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; j < rows; j += stride) {
         const std::int64_t len = __ldg(nzcnt + j);
         double acc = 0.0;
-        std::int64_t k = 0;
         // kJdsU diagonals in flight: all val/col loads of the group, then all x
-        // gathers, then the sums in the reference k order (two memory round
-        // trips per group; the longest jagged rows set the kernel time)
-        for (; k + kJdsU <= len; k += kJdsU) {
-            double v[kJdsU], xv[kJdsU];
-            long long c[kJdsU];
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u) {
-                const std::int64_t off = __ldg(jd_ptr + k + u) + j;
-                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
-                c[u] = static_cast<long long>(__ldg(col + off));
-            }
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
-        }
-        if (k < len) {  // the last < kJdsU diagonals: one masked group, all loads in flight
+        // gathers (each product overwrites its value: fewer live registers, so
+        // 4 CTAs fit per SM), then the sums in the reference k order
+        for (std::int64_t k = 0; k < len; k += kJdsU) {
             const std::int64_t rem = len - k;
-            double v[kJdsU], xv[kJdsU];
-            long long c[kJdsU];
+            double v[kJdsU];
+            IdxT c[kJdsU];
 #pragma unroll
             for (int u = 0; u < kJdsU; ++u) {
                 v[u] = 0.0;
@@ -476,85 +464,115 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
                 if (u < rem) {
                     const std::int64_t off = __ldg(jd_ptr + k + u) + j;
                     asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
-                    c[u] = static_cast<long long>(__ldg(col + off));
+                    c[u] = __ldg(col + off);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kJdsU; ++u) xv[u] = u < rem ? __ldg(x + c[u]) : 0.0;
+            for (int u = 0; u < kJdsU; ++u)
+                if (u < rem) v[u] = __dmul_rn(v[u], __ldg(x + static_cast<long long>(c[u])));
 #pragma unroll
             for (int u = 0; u < kJdsU; ++u)
-                if (u < rem) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+                if (u < rem) acc = __dadd_rn(acc, v[u]);
         }
         y[__ldg(inv_perm + j)] = acc;
     }
 }
 
-// Two-phase JDS (bijective perm, a product scratch): the rows' sums must be
-// sequential in k order to stay bit-identical, but the products need not be.
-// Phase 1 computes every stored product prod[e] = val[e] * x[col[e]] with
-// all nonzeros in parallel (coalesced val/col, independent gathers: no row
-// waits on its own earlier loads); phase 2 sums each jagged row's products in
-// the reference k order from L2 (addresses known up front, 16 in flight).
-// The longest rows no longer serialise rounds of gathers (Parboil shape: 64
-// diagonals, 4 dependent val/col -> x rounds per row in the one-phase kernel).
-template <typename IdxT>
-__global__ void __launch_bounds__(kThreads) k_jds_products(std::int64_t nnz, const IdxT* __restrict__ col,
-                                                           const double* __restrict__ val,
-                                                           const double* __restrict__ x, double* __restrict__ prod) {
-    pdl_trigger();  // phase 2 may launch; it waits for this grid before reading prod
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
-    std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    constexpr int U = 4;
-    for (; e + (U - 1) * stride < nnz; e += U * stride) {
-        double v[U], xv[U];
-        long long c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + e + u * stride));
-            c[u] = static_cast<long long>(__ldg(col + e + u * stride));
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) prod[e + u * stride] = __dmul_rn(v[u], xv[u]);
-    }
-    for (; e < nnz; e += stride) prod[e] = __dmul_rn(val[e], __ldg(x + static_cast<long long>(col[e])));
-}
+// JDS with the long jagged rows split over a quad of lanes. A row's sum must
+// be sequential in the reference k order (bit-identical), but its products
+// need not be: lane q of the quad loads diagonals [16 q, 16 q + 16) of each
+// 64-diagonal stretch and forms their products in parallel with the others
+// (one val/col round trip, one x round trip), then the quad adds them in k
+// order, passing the running sum from lane to lane (16 dependent adds each).
+// jd_ptr is staged in shared memory once per CTA. Rows of <= 16 diagonals (most
+// of a Parboil-shape matrix) keep one lane each. The long rows are the first
+// `nlong` jagged rows (JDS sorts by length; any order stays correct, the short
+// path loops).
+constexpr int kJdsQuad = 4;
+constexpr int kJdsSmemJd = 2048;
 
-__global__ void __launch_bounds__(kThreads) k_jds_sum(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
-                                                      const std::int64_t* __restrict__ inv_perm,
-                                                      const std::int64_t* __restrict__ jd_ptr,
-                                                      const double* __restrict__ prod, double* __restrict__ y) {
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
-    std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    // the row's shape does not depend on phase 1
-    std::int64_t len = j < rows ? __ldg(nzcnt + j) : 0, out = j < rows ? __ldg(inv_perm + j) : 0;
-    pdl_wait();
-    for (; j < rows; j += stride) {
+template <typename IdxT>
+__global__ void __launch_bounds__(kThreads) k_jds_quad(std::int64_t rows, std::int64_t nlong,
+                                                       const std::int64_t* __restrict__ nzcnt,
+                                                       const std::int64_t* __restrict__ inv_perm,
+                                                       const std::int64_t* __restrict__ jd_ptr, std::int64_t njd,
+                                                       const IdxT* __restrict__ col, const double* __restrict__ val,
+                                                       const double* __restrict__ x, double* __restrict__ y) {
+    __shared__ std::int64_t sjd[kJdsSmemJd];
+    const bool staged = njd <= kJdsSmemJd;
+    if (staged)
+        for (int i = threadIdx.x; i < njd; i += kThreads) sjd[i] = __ldg(jd_ptr + i);
+    __syncthreads();
+    auto jd = [&](std::int64_t k) { return staged ? sjd[k] : __ldg(jd_ptr + k); };
+    const std::int64_t t = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const std::int64_t nquad = nlong * kJdsQuad;
+    if (t < ((nquad + 31) / 32) * 32) {  // long rows: whole warps of quads
+        const int lane = threadIdx.x & 31, q = lane & (kJdsQuad - 1), g0 = lane & ~(kJdsQuad - 1);
+        const std::int64_t j = t / kJdsQuad;
+        const bool live = j < nlong;
+        const std::int64_t len = live ? __ldg(nzcnt + j) : 0;
+        const unsigned gmask = 0xfu << g0;
         double acc = 0.0;
-        std::int64_t k = 0;
-        for (; k + kJdsU <= len; k += kJdsU) {
+        for (std::int64_t kb = 0;; kb += kJdsQuad * kJdsU) {
+            const bool any = __any_sync(0xffffffffu, kb < len);
+            if (!any) break;
+            const std::int64_t k0 = kb + kJdsU * q;
             double p[kJdsU];
+            IdxT c[kJdsU];
 #pragma unroll
-            for (int u = 0; u < kJdsU; ++u) p[u] = __ldcg(prod + __ldg(jd_ptr + k + u) + j);
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u) acc = __dadd_rn(acc, p[u]);
-        }
-        if (k < len) {
-            double p[kJdsU];
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u) p[u] = k + u < len ? __ldcg(prod + __ldg(jd_ptr + k + u) + j) : 0.0;
+            for (int u = 0; u < kJdsU; ++u) {
+                p[u] = 0.0;
+                c[u] = 0;
+                if (k0 + u < len) {
+                    const std::int64_t off = jd(k0 + u) + j;
+                    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(p[u]) : "l"(val + off));
+                    c[u] = __ldg(col + off);
+                }
+            }
 #pragma unroll
             for (int u = 0; u < kJdsU; ++u)
-                if (k + u < len) acc = __dadd_rn(acc, p[u]);
+                if (k0 + u < len) p[u] = __dmul_rn(p[u], __ldg(x + static_cast<long long>(c[u])));
+            // the quad's products in k order: lane q adds its 16 after lane q-1
+#pragma unroll
+            for (int s = 0; s < kJdsQuad; ++s) {
+                if (q == s) {
+#pragma unroll
+                    for (int u = 0; u < kJdsU; ++u)
+                        if (k0 + u < len) acc = __dadd_rn(acc, p[u]);
+                }
+                acc = __shfl_sync(0xffffffffu, acc, g0 + s);
+            }
         }
-        y[out] = acc;
-        const std::int64_t nj = j + stride;
-        if (nj < rows) {
-            len = __ldg(nzcnt + nj);
-            out = __ldg(inv_perm + nj);
-        }
+        (void)gmask;
+        if (live && q == 0) y[__ldg(inv_perm + j)] = acc;
+        return;
     }
+    // short rows: one lane each (a loop covers any length)
+    const std::int64_t j = nlong + (t - ((nquad + 31) / 32) * 32);
+    if (j >= rows) return;
+    const std::int64_t len = __ldg(nzcnt + j);
+    double acc = 0.0;
+    for (std::int64_t k = 0; k < len; k += kJdsU) {
+        double p[kJdsU];
+        IdxT c[kJdsU];
+#pragma unroll
+        for (int u = 0; u < kJdsU; ++u) {
+            p[u] = 0.0;
+            c[u] = 0;
+            if (k + u < len) {
+                const std::int64_t off = jd(k + u) + j;
+                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(p[u]) : "l"(val + off));
+                c[u] = __ldg(col + off);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kJdsU; ++u)
+            if (k + u < len) p[u] = __dmul_rn(p[u], __ldg(x + static_cast<long long>(c[u])));
+#pragma unroll
+        for (int u = 0; u < kJdsU; ++u)
+            if (k + u < len) acc = __dadd_rn(acc, p[u]);
+    }
+    y[__ldg(inv_perm + j)] = acc;
 }
 
 // JDS when perm is not a bijection: thread per original row (uncoalesced,
@@ -932,30 +950,16 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
     if (A.rows <= 0) return;
     const unsigned g = grid_for(A.rows);
-    static const bool two_phase = [] {  // LILAC_B200_JDS_2P=0: the one-phase kernel
-        const char* e = std::getenv("LILAC_B200_JDS_2P");
-        return !(e && std::strcmp(e, "0") == 0);
-    }();
-    if (A.inv_perm && A.prod && two_phase) {
-        const unsigned gp = grid_for(A.nnz, kSMs * 8);
+    if (A.inv_perm && A.nlong >= 0) {
+        const std::int64_t threads = ((A.nlong * kJdsQuad + 31) / 32) * 32 + (A.rows - A.nlong);
+        const unsigned gq = static_cast<unsigned>(std::max<std::int64_t>(1, (threads + kThreads - 1) / kThreads));
         if (A.col32)
-            k_jds_products<std::int32_t><<<gp, kThreads, 0, s>>>(A.nnz, static_cast<const std::int32_t*>(A.col), A.val,
-                                                                 x, A.prod);
+            k_jds_quad<std::int32_t><<<gq, kThreads, 0, s>>>(A.rows, A.nlong, A.nzcnt, A.inv_perm, A.jd_ptr, A.njd,
+                                                             static_cast<const std::int32_t*>(A.col), A.val, x, y);
         else
-            k_jds_products<std::int64_t><<<gp, kThreads, 0, s>>>(A.nnz, static_cast<const std::int64_t*>(A.col), A.val,
-                                                                 x, A.prod);
+            k_jds_quad<std::int64_t><<<gq, kThreads, 0, s>>>(A.rows, A.nlong, A.nzcnt, A.inv_perm, A.jd_ptr, A.njd,
+                                                             static_cast<const std::int64_t*>(A.col), A.val, x, y);
         B200_CUDA(cudaGetLastError());
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(g);
-        cfg.blockDim = dim3(kThreads);
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        B200_CUDA(cudaLaunchKernelEx(&cfg, k_jds_sum, A.rows, A.nzcnt, A.inv_perm, A.jd_ptr,
-                                     static_cast<const double*>(A.prod), y));
         return;
     }
     if (A.inv_perm) {
