@@ -259,7 +259,6 @@ struct JdsDev {
     const void* col = nullptr;
     bool col32 = true;
     const double* val = nullptr;
-    std::int64_t nlong = -1;                   // leading jagged rows of > 16 diagonals (quad lanes); -1 unknown
 };
 
 // ---------------------------------------------------------------------------
@@ -288,12 +287,6 @@ void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, dou
 // Tiled kernel (tcsr.cu); partials/ticket/sc non-null = fused p.q for CG.
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
                        unsigned int* ticket, struct CgScalars* sc, cudaStream_t s, std::int64_t dot_off = 0);
-// Leading jagged rows with more than 16 diagonals (nzcnt on the host).
-inline std::int64_t jds_long_rows(std::int64_t rows, const std::int64_t* nzcnt) {
-    std::int64_t n = 0;
-    while (n < rows && nzcnt[n] > 16) ++n;
-    return n;
-}
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s);
 
 struct CgScalars;

@@ -236,8 +236,6 @@ struct spmv_jds_state {
     MarshalObject<DevArray> m_val;
     MarshalObject<DevArray> m_x;
     MarshalObject<DevArray> m_output;
-    std::int64_t nlong = -1;        // leading long jagged rows, cached with nzcnt
-    std::int64_t nlong_stamp = -1;  // nzcnt's construct + update count it was computed at
     bool validated = false;
     bool first_run_done = false;
 };
@@ -560,15 +558,6 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         A.col = ci.buf.ptr;
         A.col32 = ci.col32;
         A.val = dval.data<double>();
-        {
-            const std::int64_t st = state.m_nzcnt.counters().n_construct + state.m_nzcnt.counters().n_update;
-            if (st != state.nlong_stamp) {
-                host_in(nzcnt, sizeof(std::int64_t) * static_cast<std::size_t>(rows));
-                state.nlong = jds_long_rows(rows, nzcnt);
-                state.nlong_stamp = st;
-            }
-        }
-        A.nlong = state.nlong;
         timed_launch(hs, [&] { launch_spmv_jds(A, dx.data<double>(), dout.buf.as<double>(), rt().stream); });
         tm.acquired();
 

@@ -26,9 +26,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kSMs = 148;
 constexpr int kJdsU = 16;  // JDS diagonals in flight per thread
-#ifndef LILAC_JDS_MINB
-#define LILAC_JDS_MINB 4  // 4 CTAs per SM (64 registers): the Parboil shape's 571 CTAs in one wave
-#endif
 
 // ---- load helpers -----------------------------------------------------------
 
@@ -440,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_exact(std::int64_t rows,
 
 // JDS, thread per jagged row j (coalesced over j); y scattered through inv_perm.
 template <typename IdxT>
-__global__ void __launch_bounds__(kThreads, LILAC_JDS_MINB) k_jds(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
+__global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
                                                   const std::int64_t* __restrict__ inv_perm,
                                                   const std::int64_t* __restrict__ jd_ptr,
                                                   const IdxT* __restrict__ col,
@@ -450,13 +447,28 @@ __global__ void __launch_bounds__(kThreads, LILAC_JDS_MINB) k_jds(std::int64_t r
     for (std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; j < rows; j += stride) {
         const std::int64_t len = __ldg(nzcnt + j);
         double acc = 0.0;
+        std::int64_t k = 0;
         // kJdsU diagonals in flight: all val/col loads of the group, then all x
-        // gathers (each product overwrites its value: fewer live registers, so
-        // 4 CTAs fit per SM), then the sums in the reference k order
-        for (std::int64_t k = 0; k < len; k += kJdsU) {
+        // gathers, then the sums in the reference k order (two memory round
+        // trips per group; the longest jagged rows set the kernel time)
+        for (; k + kJdsU <= len; k += kJdsU) {
+            double v[kJdsU], xv[kJdsU];
+            long long c[kJdsU];
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) {
+                const std::int64_t off = __ldg(jd_ptr + k + u) + j;
+                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
+                c[u] = static_cast<long long>(__ldg(col + off));
+            }
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+            for (int u = 0; u < kJdsU; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+        }
+        if (k < len) {  // the last < kJdsU diagonals: one masked group, all loads in flight
             const std::int64_t rem = len - k;
-            double v[kJdsU];
-            IdxT c[kJdsU];
+            double v[kJdsU], xv[kJdsU];
+            long long c[kJdsU];
 #pragma unroll
             for (int u = 0; u < kJdsU; ++u) {
                 v[u] = 0.0;
@@ -464,115 +476,17 @@ __global__ void __launch_bounds__(kThreads, LILAC_JDS_MINB) k_jds(std::int64_t r
                 if (u < rem) {
                     const std::int64_t off = __ldg(jd_ptr + k + u) + j;
                     asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
-                    c[u] = __ldg(col + off);
+                    c[u] = static_cast<long long>(__ldg(col + off));
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kJdsU; ++u)
-                if (u < rem) v[u] = __dmul_rn(v[u], __ldg(x + static_cast<long long>(c[u])));
+            for (int u = 0; u < kJdsU; ++u) xv[u] = u < rem ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
             for (int u = 0; u < kJdsU; ++u)
-                if (u < rem) acc = __dadd_rn(acc, v[u]);
+                if (u < rem) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
         }
         y[__ldg(inv_perm + j)] = acc;
     }
-}
-
-// JDS with the long jagged rows split over a quad of lanes. A row's sum must
-// be sequential in the reference k order (bit-identical), but its products
-// need not be: lane q of the quad loads diagonals [16 q, 16 q + 16) of each
-// 64-diagonal stretch and forms their products in parallel with the others
-// (one val/col round trip, one x round trip), then the quad adds them in k
-// order, passing the running sum from lane to lane (16 dependent adds each).
-// jd_ptr is staged in shared memory once per CTA. Rows of <= 16 diagonals (most
-// of a Parboil-shape matrix) keep one lane each. The long rows are the first
-// `nlong` jagged rows (JDS sorts by length; any order stays correct, the short
-// path loops).
-constexpr int kJdsQuad = 4;
-constexpr int kJdsSmemJd = 2048;
-
-template <typename IdxT>
-__global__ void __launch_bounds__(kThreads) k_jds_quad(std::int64_t rows, std::int64_t nlong,
-                                                       const std::int64_t* __restrict__ nzcnt,
-                                                       const std::int64_t* __restrict__ inv_perm,
-                                                       const std::int64_t* __restrict__ jd_ptr, std::int64_t njd,
-                                                       const IdxT* __restrict__ col, const double* __restrict__ val,
-                                                       const double* __restrict__ x, double* __restrict__ y) {
-    __shared__ std::int64_t sjd[kJdsSmemJd];
-    const bool staged = njd <= kJdsSmemJd;
-    if (staged)
-        for (int i = threadIdx.x; i < njd; i += kThreads) sjd[i] = __ldg(jd_ptr + i);
-    __syncthreads();
-    auto jd = [&](std::int64_t k) { return staged ? sjd[k] : __ldg(jd_ptr + k); };
-    const std::int64_t t = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    const std::int64_t nquad = nlong * kJdsQuad;
-    if (t < ((nquad + 31) / 32) * 32) {  // long rows: whole warps of quads
-        const int lane = threadIdx.x & 31, q = lane & (kJdsQuad - 1), g0 = lane & ~(kJdsQuad - 1);
-        const std::int64_t j = t / kJdsQuad;
-        const bool live = j < nlong;
-        const std::int64_t len = live ? __ldg(nzcnt + j) : 0;
-        const unsigned gmask = 0xfu << g0;
-        double acc = 0.0;
-        for (std::int64_t kb = 0;; kb += kJdsQuad * kJdsU) {
-            const bool any = __any_sync(0xffffffffu, kb < len);
-            if (!any) break;
-            const std::int64_t k0 = kb + kJdsU * q;
-            double p[kJdsU];
-            IdxT c[kJdsU];
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u) {
-                p[u] = 0.0;
-                c[u] = 0;
-                if (k0 + u < len) {
-                    const std::int64_t off = jd(k0 + u) + j;
-                    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(p[u]) : "l"(val + off));
-                    c[u] = __ldg(col + off);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kJdsU; ++u)
-                if (k0 + u < len) p[u] = __dmul_rn(p[u], __ldg(x + static_cast<long long>(c[u])));
-            // the quad's products in k order: lane q adds its 16 after lane q-1
-#pragma unroll
-            for (int s = 0; s < kJdsQuad; ++s) {
-                if (q == s) {
-#pragma unroll
-                    for (int u = 0; u < kJdsU; ++u)
-                        if (k0 + u < len) acc = __dadd_rn(acc, p[u]);
-                }
-                acc = __shfl_sync(0xffffffffu, acc, g0 + s);
-            }
-        }
-        (void)gmask;
-        if (live && q == 0) y[__ldg(inv_perm + j)] = acc;
-        return;
-    }
-    // short rows: one lane each (a loop covers any length)
-    const std::int64_t j = nlong + (t - ((nquad + 31) / 32) * 32);
-    if (j >= rows) return;
-    const std::int64_t len = __ldg(nzcnt + j);
-    double acc = 0.0;
-    for (std::int64_t k = 0; k < len; k += kJdsU) {
-        double p[kJdsU];
-        IdxT c[kJdsU];
-#pragma unroll
-        for (int u = 0; u < kJdsU; ++u) {
-            p[u] = 0.0;
-            c[u] = 0;
-            if (k + u < len) {
-                const std::int64_t off = jd(k + u) + j;
-                asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(p[u]) : "l"(val + off));
-                c[u] = __ldg(col + off);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kJdsU; ++u)
-            if (k + u < len) p[u] = __dmul_rn(p[u], __ldg(x + static_cast<long long>(c[u])));
-#pragma unroll
-        for (int u = 0; u < kJdsU; ++u)
-            if (k + u < len) acc = __dadd_rn(acc, p[u]);
-    }
-    y[__ldg(inv_perm + j)] = acc;
 }
 
 // JDS when perm is not a bijection: thread per original row (uncoalesced,
@@ -950,18 +864,6 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
     if (A.rows <= 0) return;
     const unsigned g = grid_for(A.rows);
-    if (A.inv_perm && A.nlong >= 0) {
-        const std::int64_t threads = ((A.nlong * kJdsQuad + 31) / 32) * 32 + (A.rows - A.nlong);
-        const unsigned gq = static_cast<unsigned>(std::max<std::int64_t>(1, (threads + kThreads - 1) / kThreads));
-        if (A.col32)
-            k_jds_quad<std::int32_t><<<gq, kThreads, 0, s>>>(A.rows, A.nlong, A.nzcnt, A.inv_perm, A.jd_ptr, A.njd,
-                                                             static_cast<const std::int32_t*>(A.col), A.val, x, y);
-        else
-            k_jds_quad<std::int64_t><<<gq, kThreads, 0, s>>>(A.rows, A.nlong, A.nzcnt, A.inv_perm, A.jd_ptr, A.njd,
-                                                             static_cast<const std::int64_t*>(A.col), A.val, x, y);
-        B200_CUDA(cudaGetLastError());
-        return;
-    }
     if (A.inv_perm) {
         if (A.col32)
             k_jds<std::int32_t><<<g, kThreads, 0, s>>>(A.rows, A.nzcnt, A.inv_perm, A.jd_ptr,
