@@ -434,6 +434,9 @@ extern "C" void b200_spmv_csr(std::int64_t rows, double* output, const std::int6
         // derived tiled layout: rebuilt only when row_ptr/col_ind/val were re-marshaled
         std::int64_t stamp = matrix_stamp(state);
         const bool rebuild = stamp != state.tiled_stamp || rt().kernel != state.tiled_policy;
+        // (the flag alone is not enough: a new matrix identity re-constructs the
+        // bindings, which brings the plain arrays back)
+        state.plain_dropped = state.plain_dropped && (!ci.buf.ptr || (!dval.lent && !dval.buf.ptr));
         if (rebuild && state.plain_dropped) {
             // the plain col / val were freed behind the old layout: a rebuild (or
             // another kernel) needs them again — re-marshal both in full

@@ -329,17 +329,26 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         const std::uint16_t* kb = T.key + base;
         const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
         const std::uint16_t* lr = T.lrow + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps) * 32 + lane;
+        // this warp's run bounds, lane k holding slab k's (one coalesced load
+        // per tile instead of a dependent L1 round trip at every run start)
+        const int wlo = lane < T.nslabs ? __ldg(wo + lane * kTileWarps + warp) : 0;
+        const int whi = lane < T.nslabs ? __ldg(wo + lane * kTileWarps + warp + 1) : 0;
+        auto run_lo = [&](int k) { return k < 32 ? __shfl_sync(kFull, wlo, k) : __ldg(wo + k * kTileWarps + warp); };
+        auto run_hi = [&](int k) {
+            return k < 32 ? __shfl_sync(kFull, whi, k) : __ldg(wo + k * kTileWarps + warp + 1);
+        };
         for (int r = tid; r < nrows; r += kTileThreads) yp[r] = 0.0;
-        if (lane == 0)  // runs stream into L2 kPfAhead slabs ahead of their use
-            for (int k = 0; k < kPfAhead && k < T.nslabs; ++k)
-                prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
+        for (int k = 0; k < kPfAhead && k < T.nslabs; ++k) {  // runs stream into L2 kPfAhead slabs ahead
+            const int plo = run_lo(k), phi = run_hi(k);
+            if (lane == 0) prefetch_run(vb, kb, plo, phi);
+        }
         // lane descriptors and each run's first chunk are loaded one run ahead (registers)
         unsigned dnext = T.nslabs > 0 ? __ldg(lr + warp * 32) : 0u;
         Chunk ca, cb;
         if (T.nslabs > 0) {
             std::uint64_t pol;
             asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            load_head_chunks(ca, cb, vb, kb, wo[warp], wo[warp + 1], lane, pol);
+            load_head_chunks(ca, cb, vb, kb, run_lo(0), run_hi(0), lane, pol);
         }
         if (tid == 0 && gate) {
             unsigned v;
@@ -368,15 +377,16 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             }
             const unsigned dcur = dnext;
             if (k + 1 < T.nslabs) {
-                if (lane == 0 && k + kPfAhead < T.nslabs)
-                    prefetch_run(vb, kb, wo[(k + kPfAhead) * kTileWarps + warp],
-                                 wo[(k + kPfAhead) * kTileWarps + warp + 1]);
+                if (k + kPfAhead < T.nslabs) {
+                    const int plo = run_lo(k + kPfAhead), phi = run_hi(k + kPfAhead);
+                    if (lane == 0) prefetch_run(vb, kb, plo, phi);
+                }
                 dnext = __ldg(lr + ((k + 1) * kTileWarps + warp) * 32);
             }
             const bool more = k + 1 < T.nslabs;
+            const int nlo = more ? run_lo(k + 1) : 0, nhi = more ? run_hi(k + 1) : 0;
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
-                vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1], dcur, ca, cb,
-                more ? wo[(k + 1) * kTileWarps + warp] : 0, more ? wo[(k + 1) * kTileWarps + warp + 1] : 0,
+                vb, kb, run_lo(k), run_hi(k), dcur, ca, cb, nlo, nhi,
                 c.xs_s + 8u * static_cast<unsigned>(buf * c.stride), c.yp_s, lane);
             __syncwarp();
             if (lane == 0) {
