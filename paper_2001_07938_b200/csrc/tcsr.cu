@@ -164,34 +164,36 @@ __device__ __forceinline__ void load_chunk(Chunk& c, const double* vb, const std
     c.k = ld_stream_u16x4(kb + e, pol);
 }
 
-// A lane's walk state over its range: the row being summed, its partial
-// sum, and the head run (the lane's first row, which may have begun in an
-// earlier lane) once a later row starts.
+// A lane's walk state over its range: the row being summed, its partial sum,
+// and whether a row began inside the lane.
 struct Walk {
     unsigned row;
-    double acc, head;
-    bool in_head;
+    double acc;
+    bool split;
 };
 
 // MODE: 0 = the kernel. Timing probes (LILAC_B200_TILED_PROBE, wrong results,
 // never on the CG path; tools/tiled_probes.sh): 1 no x gathers, 2 no row
 // sums, 3 neither (loads only), 5 = 3 without slab copies/waits, 6 = 0
 // without slab copies/waits.
+//
+// At a row start the partial of the row before it is added into the shared y
+// buffer at once (predicated, no branch). That row is either complete inside
+// this lane or the lane's first row, continued from earlier lanes: those
+// lanes' share arrives through the segmented scan after the walk, so no row
+// is written by two lanes at the same time (rows are owned by one warp).
 template <int MODE>
 __device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::uint32_t xb_s, std::uint32_t yp_s) {
-    const double p = (MODE == 1 || MODE == 3) ? v : v * lds_f64(xb_s + 8u * (key & kKeyColMask));
+    const double x = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (key & kKeyColMask));
     if (MODE >= 2) {
-        w.acc += p;
+        w.acc = fma(v, x, w.acc);
         return;
     }
-    // a new row: the previous one is complete (branch-free; the flush of a
-    // row that began and ended in this lane is predicated, exclusive)
     const bool st = (key & kKeyStart) != 0u;
-    if (st && !w.in_head) sts_add_f64(yp_s + 8u * w.row, w.acc);
-    w.head = st && w.in_head ? w.acc : w.head;
-    w.in_head = w.in_head && !st;
+    if (st) sts_add_f64(yp_s + 8u * w.row, w.acc);
+    w.split = w.split || st;
     w.row += st ? 1u : 0u;
-    w.acc = (st ? 0.0 : w.acc) + p;
+    w.acc = fma(v, x, st ? 0.0 : w.acc);
 }
 
 template <int MODE>
@@ -202,14 +204,15 @@ __device__ __forceinline__ void walk_chunk(Walk& w, const Chunk& c, std::uint32_
     walk_one<MODE>(w, c.v1.y, c.k.y >> 16, xb_s, yp_s);
 }
 
-// Combines the lanes' boundary rows once per run: lane l holds its head run
-// (k0, p0, only when split) and its tail run (k1, p1); rows are
-// non-decreasing across lanes. Adds each row's sum into yp[row] (rows are
-// owned by this warp: no atomics, fixed order). `cont`: the lane's first row
-// began in an earlier lane; inactive lanes (no chunks) are segment heads that
-// store nothing.
-__device__ __forceinline__ void reduce_lanes(unsigned k0, double p0, unsigned k1, double p1, bool split, bool cont,
-                                             bool active, int lane, std::uint32_t yp_s) {
+// Combines the lanes' open rows once per run: lane l holds the partial of its
+// last row (row k1, sum p1; the whole lane when no row began in it). Rows are
+// non-decreasing across lanes. A segmented scan over the lanes sums each row
+// continued across lanes, and the segment's last lane adds it into yp[row]
+// (rows are owned by this warp: no atomics, fixed order). `cont`: the lane's
+// first row began in an earlier lane; inactive lanes (no chunks) are segment
+// heads that store nothing.
+__device__ __forceinline__ void reduce_lanes(unsigned k1, double p1, bool split, bool cont, bool active, int lane,
+                                             std::uint32_t yp_s) {
     double s = p1;
     const bool head = lane == 0 || split || !cont || !active;
     const unsigned hm = __ballot_sync(kFull, head);
@@ -221,12 +224,8 @@ __device__ __forceinline__ void reduce_lanes(unsigned k0, double p0, unsigned k1
         const double t = __shfl_up_sync(kFull, s, d);
         if (lane - d >= seg) s += t;
     }
-    // two ordered store passes over distinct rows: (1) every segment's sum at
-    // its last lane; (2) the head run of every split lane (a row running from
-    // lane i-1's tail into lane i's head gets both)
     if (active && (lane == 31 || ((hm >> (lane + 1)) & 1u))) sts_add_f64(yp_s + 8u * k1, s);
     __syncwarp();
-    if (active && split) sts_add_f64(yp_s + 8u * k0, p0);
 }
 
 // Lane `lane`'s chunks 0 and 1 of the run [lo, hi) (those it has: lane l
@@ -253,7 +252,7 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
     const int C = (hi - lo) / kChunk, m = C >> 5, r = C & 31;
     const int cnt = m + (lane < r ? 1 : 0), iters = m + (r > 0 ? 1 : 0);
     const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);  // chunk i at e0 + 128 i
-    Walk w{ld & 0x7fffu, 0.0, 0.0, true};
+    Walk w{ld & 0x7fffu, 0.0, false};
     xb_s = opaque_u32(xb_s);  // one base register: a gather address is one LEA
     // chunks 0 and 1 were loaded during the previous run; each buffer is
     // refilled with the chunk two ahead as soon as it has been walked
@@ -271,7 +270,7 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
         if (w.acc == 12345.678) sts_add_f64(yp_s, w.acc);
         return;
     }
-    reduce_lanes(ld & 0x7fffu, w.head, w.row, w.acc, !w.in_head, (ld & kLaneCont) != 0u, cnt > 0, lane, yp_s);
+    reduce_lanes(w.row, w.acc, w.split, (ld & kLaneCont) != 0u, cnt > 0, lane, yp_s);
 }
 
 // Shared-memory state of a tiled SpMV CTA (slab double buffer, row sums,
