@@ -110,7 +110,7 @@ CsrKernel parse_csr_kernel(const std::string& s);
 // m + 1 of them); chunk i of lane l is stored at run offset (32 i + l) * 4, so
 // every warp-wide chunk load is one contiguous 1 KB burst while each lane
 // walks its own range in order, summing rows in registers. Each nonzero has a
-// 2-byte key = slab-local column | kKeyStart when it opens a row (never set on
+// 2-byte key = slab-local column << 1 | kKeyStart when it opens a row (never set on
 // a lane's first nonzero); each lane has a 2-byte descriptor = tile-local row
 // of its first nonzero | kLaneCont when that row began in an earlier lane.
 // HBM cost: 10 bytes per stored nonzero + 64 bytes per run.
@@ -120,11 +120,17 @@ constexpr int kSlabW = 12288;            // columns per slab: 2 x 96 KB double-b
 constexpr int kSlabStride = kSlabW + 2;  // + a zero cell (column kSlabW) read by padding entries
 constexpr int kMaxTileRows = 4096;       // tile-local rows fit a descriptor and the smem y buffer
 constexpr int kChunk = 4;                // nonzeros per lane per load (one 256-bit val load)
-constexpr std::uint16_t kKeyStart = 1u << 15;
+// key = slab-local column << 1 | start: the gather address is one mask + one
+// shifted add (xs + (key & ~1) * 4), the start bit one test
+constexpr std::uint16_t kKeyStart = 1u;
 constexpr std::uint16_t kKeyColMask = (1u << 14) - 1u;
 constexpr std::uint16_t kLaneCont = 1u << 15;
+constexpr std::uint16_t tcsr_key(int col, bool start) {
+    return static_cast<std::uint16_t>((static_cast<unsigned>(col) << 1) | (start ? kKeyStart : 0u));
+}
+constexpr int tcsr_key_col(unsigned key) { return static_cast<int>((key >> 1) & kKeyColMask); }
 // padding entry: value 0 times the zero cell (never an Inf or NaN of x)
-constexpr std::uint16_t kPadKey = static_cast<std::uint16_t>(kSlabW);
+constexpr std::uint16_t kPadKey = tcsr_key(kSlabW, false);
 static_assert(kSlabW <= static_cast<int>(kKeyColMask), "slab columns and the zero cell must fit the key");
 // The builder widens the slab to what shared memory leaves after the tile's
 // y buffer: 2 (slab_w + 2) + rows_max doubles within kTileSmemBudget (NPB
@@ -146,7 +152,7 @@ struct TcsrDev {
     const std::int32_t* woff = nullptr;       // ntiles x (nslabs*kTileWarps + 1): run element offsets, tile-relative
     const std::uint16_t* lrow = nullptr;      // ntiles x nslabs*kTileWarps x 32 lane descriptors
     const double* val = nullptr;              // stored nonzeros (+ pads), tiled order
-    const std::uint16_t* key = nullptr;       // same: slab-local column | kKeyStart?
+    const std::uint16_t* key = nullptr;       // same: tcsr_key(slab-local column, row start)
 };
 
 // Merge-path plan (merge.cu): per-CTA start coordinates on the merge of row

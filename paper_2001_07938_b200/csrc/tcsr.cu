@@ -184,7 +184,7 @@ struct Walk {
 // is written by two lanes at the same time (rows are owned by one warp).
 template <int MODE>
 __device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::uint32_t xb_s, std::uint32_t yp_s) {
-    const double x = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + 8u * (key & kKeyColMask));
+    const double x = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + ((key & 0xfffeu) << 2));
     if (MODE >= 2) {
         w.acc = fma(v, x, w.acc);
         return;
@@ -198,9 +198,9 @@ __device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::u
 
 template <int MODE>
 __device__ __forceinline__ void walk_chunk(Walk& w, const Chunk& c, std::uint32_t xb_s, std::uint32_t yp_s) {
-    walk_one<MODE>(w, c.v0.x, c.k.x & 0xffffu, xb_s, yp_s);
+    walk_one<MODE>(w, c.v0.x, c.k.x, xb_s, yp_s);  // low key: walk_one masks to 0xfffe / bit 0
     walk_one<MODE>(w, c.v0.y, c.k.x >> 16, xb_s, yp_s);
-    walk_one<MODE>(w, c.v1.x, c.k.y & 0xffffu, xb_s, yp_s);
+    walk_one<MODE>(w, c.v1.x, c.k.y, xb_s, yp_s);
     walk_one<MODE>(w, c.v1.y, c.k.y >> 16, xb_s, yp_s);
 }
 

@@ -156,7 +156,7 @@ void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, con
                 if (i >= cn[l]) continue;
                 const std::int64_t e = (cs[l] + i) * kChunk + sl, at = (i * 32 + l) * kChunk + sl;
                 if (e >= E) {
-                    hk[at] = pad;
+                    hk[at] = tcsr_key(pad, false);
                     hv[at] = 0.0;
                     continue;
                 }
@@ -181,7 +181,7 @@ void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, con
                     }
                     ++cnt[l >> 4][pl[best].first & 15u];
                 }
-                hk[at] = static_cast<std::uint16_t>(pl[best].first | (start ? kKeyStart : 0));
+                hk[at] = tcsr_key(pl[best].first, start);
                 hv[at] = pl[best].second;
                 pl.erase(pl.begin() + static_cast<std::ptrdiff_t>(best));
             }

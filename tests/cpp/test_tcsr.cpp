@@ -95,7 +95,7 @@ static void check_layout(const char* name, const Csr& a) {
                             const std::uint16_t key = h.key[at];
                             if ((key & kKeyStart) && !(i == 0 && e == 0)) ++row;
                             CHECK(!((key & kKeyStart) && i == 0 && e == 0), "%s: start bit on a lane's first", name);
-                            const int col = key & kKeyColMask;
+                            const int col = tcsr_key_col(key);
                             CHECK(col <= h.slab_w, "%s: key column", name);
                             if (col == h.slab_w) {  // the zero cell: padding / empty-row entry
                                 CHECK(h.val[at] == 0.0, "%s: nonzero padding", name);
