@@ -349,6 +349,34 @@ bool edges_changed(const TrackedRegion& r) {
 }
 
 // Is [lo, hi) inside one active lazy range?
+// The two snapshot strategies keep one 64-bit stamp per clean cycle: the
+// FNV-1a hash of the bytes (Checksum) or the interpreter buffer's write
+// version (ExactVersion); `snapshot_of` is what poll_dirty compares against.
+std::uint64_t snapshot_stamp(const TrackedRegion& r) {
+    return r.strategy == Strategy::Checksum ? fnv1a(r.ref.base, r.ref.bytes) : version_of(r);
+}
+
+std::uint64_t& snapshot_of(TrackedRegion& r) {
+    return r.strategy == Strategy::Checksum ? r.last_checksum : r.last_version;
+}
+
+// Naive / Checksum / ExactVersion: record the stamp (Naive: never clean).
+// False for the page-guard strategies.
+bool snapshot_clean(TrackedRegion& r) {
+    switch (r.strategy) {
+    case Strategy::Naive:
+        r.dirty = true;
+        return true;
+    case Strategy::Checksum:
+    case Strategy::ExactVersion:
+        snapshot_of(r) = snapshot_stamp(r);
+        r.dirty = false;
+        return true;
+    default:
+        return false;
+    }
+}
+
 bool covered_by_deferred(std::uintptr_t lo, std::uintptr_t hi) {
     for (const DeferredRange* d : g_deferred)
         if (d->active && d->lo <= lo && hi <= d->hi) return true;
@@ -357,25 +385,33 @@ bool covered_by_deferred(std::uintptr_t lo, std::uintptr_t hi) {
 
 }  // namespace
 
+namespace {
+// The strategy names of the LILAC_MARSHAL_STRATEGY setting, one table for
+// both directions.
+struct StrategyName {
+    Strategy s;
+    const char* name;
+};
+constexpr StrategyName kStrategyNames[] = {{Strategy::PageProtect, "pageprotect"},
+                                           {Strategy::Checksum, "checksum"},
+                                           {Strategy::ExactVersion, "exact"},
+                                           {Strategy::Naive, "naive"},
+                                           {Strategy::Hybrid, "hybrid"}};
+}  // namespace
+
 const char* strategy_name(Strategy s) {
-    switch (s) {
-    case Strategy::PageProtect: return "pageprotect";
-    case Strategy::Checksum: return "checksum";
-    case Strategy::ExactVersion: return "exact";
-    case Strategy::Naive: return "naive";
-    case Strategy::Hybrid: return "hybrid";
-    }
+    for (const StrategyName& e : kStrategyNames)
+        if (e.s == s) return e.name;
     return "?";
 }
 
 Strategy parse_strategy(const std::string& n) {
-    if (n == "pageprotect") return Strategy::PageProtect;
-    if (n == "checksum") return Strategy::Checksum;
-    if (n == "exact") return Strategy::ExactVersion;
-    if (n == "naive") return Strategy::Naive;
-    if (n == "hybrid") return Strategy::Hybrid;
-    throw Error(Errc::DataError, "unknown marshal strategy '" + n +
-                                     "' (expected pageprotect, checksum, exact, naive or hybrid)");
+    std::string known;
+    for (const StrategyName& e : kStrategyNames) {
+        if (n == e.name) return e.s;
+        known += known.empty() ? e.name : std::string(", ") + e.name;
+    }
+    throw Error(Errc::DataError, "marshal strategy '" + n + "' is not one of: " + known);
 }
 
 Strategy default_strategy(Strategy fallback) {
@@ -401,18 +437,8 @@ void mark_clean(TrackedRegion& r) {
         if (v && !r.dma_visible) g_dma_regions = g_dma_regions + 1;
         r.dma_visible = v;
     }
+    if (snapshot_clean(r)) return;  // the snapshot strategies (no page guard)
     switch (r.strategy) {
-    case Strategy::Naive:
-        r.dirty = true;  // untracked: never clean
-        return;
-    case Strategy::Checksum:
-        r.last_checksum = fnv1a(r.ref.base, r.ref.bytes);
-        r.dirty = false;
-        return;
-    case Strategy::ExactVersion:
-        r.last_version = version_of(r);
-        r.dirty = false;
-        return;
     case Strategy::PageProtect: {
         if (r.ref.bytes == 0) {
             r.dirty = false;
@@ -498,22 +524,12 @@ bool poll_dirty(TrackedRegion& r) {
     if (r.dma_visible && g_dma_always &&
         (r.strategy == Strategy::PageProtect || r.strategy == Strategy::Hybrid))
         return true;  // a DMA / device write would not fault: do not trust the guard
-    switch (r.strategy) {
-    case Strategy::Naive:
-        return true;
-    case Strategy::Checksum:
-        if (!r.dirty && r.ref.bytes > 0) r.dirty = fnv1a(r.ref.base, r.ref.bytes) != r.last_checksum;
-        return r.dirty;
-    case Strategy::ExactVersion:
-        if (!r.dirty && r.ref.bytes > 0) r.dirty = version_of(r) != r.last_version;
-        return r.dirty;
-    case Strategy::PageProtect:
-        return r.dirty;
-    case Strategy::Hybrid:
-        if (!r.dirty && r.ref.bytes > 0) r.dirty = edges_changed(r);
-        return r.dirty;
-    }
-    return true;
+    // a fault already recorded a write, or nothing to compare
+    if (r.dirty || r.ref.bytes == 0) return r.dirty || r.strategy == Strategy::Naive;
+    if (r.strategy == Strategy::Naive) return r.dirty = true;
+    if (r.strategy == Strategy::PageProtect) return false;  // clean until a store faults
+    if (r.strategy == Strategy::Hybrid) return r.dirty = edges_changed(r);
+    return r.dirty = snapshot_stamp(r) != snapshot_of(r);  // Checksum / ExactVersion
 }
 
 void drop_guard(TrackedRegion& r) {
@@ -656,8 +672,37 @@ void deferred_counters(long* deferred, long* fault_fills, long* explicit_fills, 
 // ---- MarshalObjectBase --------------------------------------------------------
 
 namespace {
-std::vector<MarshalObjectBase*> g_objects;
-std::mutex g_objects_mu;
+// Every constructed marshal object, in construction order (release_all tears
+// them down in that order, like the reference's registry).
+class ObjectRegistry {
+public:
+    void add(MarshalObjectBase* o) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (std::find(live_.begin(), live_.end(), o) == live_.end()) live_.push_back(o);
+    }
+    void remove(MarshalObjectBase* o) {
+        std::lock_guard<std::mutex> lk(mu_);
+        live_.erase(std::remove(live_.begin(), live_.end(), o), live_.end());
+    }
+    // take (and unregister) every object, or those `pick` selects
+    template <typename P>
+    std::vector<MarshalObjectBase*> take(P pick) {
+        std::lock_guard<std::mutex> lk(mu_);
+        std::vector<MarshalObjectBase*> out, keep;
+        for (MarshalObjectBase* o : live_) (pick(o) ? out : keep).push_back(o);
+        live_.swap(keep);
+        return out;
+    }
+
+private:
+    std::vector<MarshalObjectBase*> live_;
+    std::mutex mu_;
+};
+
+ObjectRegistry& registry() {
+    static ObjectRegistry* r = new ObjectRegistry;  // usable from atexit handlers
+    return *r;
+}
 }  // namespace
 
 MarshalObjectBase::MarshalObjectBase(std::string name, Strategy s)
@@ -673,27 +718,27 @@ void MarshalObjectBase::set_strategy(Strategy s) {
     fell_back_ = false;
 }
 
-void MarshalObjectBase::enroll() {
-    std::lock_guard<std::mutex> lk(g_objects_mu);
-    if (std::find(g_objects.begin(), g_objects.end(), this) == g_objects.end()) g_objects.push_back(this);
-}
+void MarshalObjectBase::enroll() { registry().add(this); }
 
-void MarshalObjectBase::unenroll() {
-    std::lock_guard<std::mutex> lk(g_objects_mu);
-    g_objects.erase(std::remove(g_objects.begin(), g_objects.end(), this), g_objects.end());
-}
+void MarshalObjectBase::unenroll() { registry().remove(this); }
 
+// Snapshot the region as clean. A region the page guard cannot cover (a
+// misaligned base under PageProtect, a refused mprotect) is demoted to the
+// byte hash for the rest of its life — the reference's ProtectionUnsupported
+// rule — and reported through fell_back().
 void MarshalObjectBase::clean_with_fallback() {
     if (streaming_) return;
+    bool demote = false;
     try {
         mark_clean(region_);
     } catch (const Error& e) {
         if (e.code() != Errc::ProtectionUnsupported) throw;
-        strategy_ = Strategy::Checksum;
-        region_.strategy = Strategy::Checksum;
-        fell_back_ = true;
-        mark_clean(region_);
+        demote = true;
     }
+    if (!demote) return;
+    fell_back_ = true;
+    strategy_ = region_.strategy = Strategy::Checksum;
+    mark_clean(region_);
 }
 
 bool MarshalObjectBase::region_dirty() { return streaming_ || poll_dirty(region_); }
@@ -714,18 +759,12 @@ void MarshalObjectBase::note_update_for_streaming(bool was_dirty) {
 }
 
 void MarshalObjectBase::hook_failed(const char* which, const std::exception& e) const {
-    throw Error(Errc::HookFailure,
-                std::string(which) + " hook failed for region '" + name_ + "': " + e.what());
+    throw Error(Errc::HookFailure, "region '" + name_ + "': the " + which + " hook threw: " + e.what());
 }
 
 Diagnostics release_all() {
-    std::vector<MarshalObjectBase*> live;
-    {
-        std::lock_guard<std::mutex> lk(g_objects_mu);
-        live.swap(g_objects);
-    }
     Diagnostics d;
-    for (MarshalObjectBase* o : live) o->force_release(d);
+    for (MarshalObjectBase* o : registry().take([](MarshalObjectBase*) { return true; })) o->force_release(d);
     return d;
 }
 
@@ -734,19 +773,10 @@ Diagnostics forget_range(const void* base, std::size_t bytes) {
     if (bytes == 0) return d;
     const auto lo = reinterpret_cast<std::uintptr_t>(base);
     const std::uintptr_t hi = lo + bytes;
-    std::vector<MarshalObjectBase*> hit;
-    {
-        std::lock_guard<std::mutex> lk(g_objects_mu);
-        for (MarshalObjectBase* o : g_objects) {
-            const auto rlo = reinterpret_cast<std::uintptr_t>(o->region_.ref.base);
-            if (o->constructed_ && rlo < hi && lo < rlo + o->region_.ref.bytes) hit.push_back(o);
-        }
-        g_objects.erase(std::remove_if(g_objects.begin(), g_objects.end(),
-                                       [&](MarshalObjectBase* o) {
-                                           return std::find(hit.begin(), hit.end(), o) != hit.end();
-                                       }),
-                        g_objects.end());
-    }
+    const auto hit = registry().take([&](MarshalObjectBase* o) {
+        const auto rlo = reinterpret_cast<std::uintptr_t>(o->region_.ref.base);
+        return o->constructed_ && rlo < hi && lo < rlo + o->region_.ref.bytes;
+    });
     for (MarshalObjectBase* o : hit) o->force_release(d);
     std::lock_guard<std::mutex> lk(g_mu);
     for (DeferredRange* r : g_deferred) {
@@ -761,10 +791,13 @@ Diagnostics forget_range(const void* base, std::size_t bytes) {
 
 // ---- PageBuffer -----------------------------------------------------------------
 
-PageBuffer::PageBuffer(std::size_t bytes) : bytes_(bytes) {
-    mapped_ = std::max<std::size_t>(ceil_page(bytes), page_size());
+// Whole anonymous pages (at least one), so PageProtect can guard the buffer.
+PageBuffer::PageBuffer(std::size_t bytes)
+    : p_(nullptr), bytes_(bytes), mapped_((bytes + page_size() - 1) / page_size() * page_size()) {
+    if (mapped_ == 0) mapped_ = page_size();
     void* p = mmap(nullptr, mapped_, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-    if (p == MAP_FAILED) throw Error(Errc::DataError, std::string("mmap failed: ") + std::strerror(errno));
+    if (p == MAP_FAILED)
+        throw Error(Errc::DataError, "PageBuffer of " + std::to_string(bytes) + " bytes: " + std::strerror(errno));
     p_ = p;
 }
 
