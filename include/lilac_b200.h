@@ -67,7 +67,7 @@ void b200_dot(double* result, int64_t length, const double* a, const double* b);
 /* gemm (kernels.lilac:14-19; "lilac.gemm"; infer_interface order n, m, c, p,
  * a, b): c[i*m + j] = sum_{k<p} a[i*p + k] * b[k*m + j], row-major f64.
  * b200_set_exact_blas(1): one thread per output in the reference's k order
- * (bit-identical); else cuBLAS DGEMM (dlopen'ed; tolerance). */
+ * (bit-identical); else the FP64 tensor-core (DMMA) kernel (tolerance). */
 void b200_gemm(int64_t n, int64_t m, double* c, int64_t p, const double* a, const double* b);
 void b200_axpy(int64_t n, double* y, double alpha, const double* x);
 void b200_xpay(int64_t n, double* y, double beta, const double* x);

@@ -721,7 +721,8 @@ def test_gemm_exact_bitwise_vs_reference_golden():
         assert O.same_bits(out, np.array(g["c"], np.float64))
 
 
-@pytest.mark.parametrize("n,m,p", [(1, 1, 1), (7, 5, 3), (300, 200, 250), (512, 384, 1024), (33, 1, 0)])
+@pytest.mark.parametrize("n,m,p", [(1, 1, 1), (7, 5, 3), (300, 200, 250), (512, 384, 1024), (33, 1, 0),
+                                   (65, 63, 17), (129, 257, 31)])
 def test_gemm_fast_and_exact_vs_oracle(n, m, p):
     rng = np.random.default_rng(n * 1000 + m + p)
     a = rng.uniform(-2, 2, n * p)
@@ -729,7 +730,7 @@ def test_gemm_fast_and_exact_vs_oracle(n, m, p):
     ref = O.gemm(n, m, p, a, b)
     scale = O.gemm(n, m, p, np.abs(a), np.abs(b))
     out = np.full(n * m, np.nan)
-    H.gemm(n, m, out, p, a, b)  # cuBLAS DGEMM
+    H.gemm(n, m, out, p, a, b)  # the DMMA kernel (FP64 tensor cores)
     assert (np.abs(out - ref) <= TOL * scale + (scale == 0) * 0).all()
     N.lib().b200_set_exact_blas(1)
     out2 = np.full(n * m, np.nan)
