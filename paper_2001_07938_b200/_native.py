@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblilac_b200.so")
+# LILAC_B200_LIB: an experiment build (tools/build_variant.py); default in-tree
+LIB_PATH = os.environ.get("LILAC_B200_LIB") or os.path.join(PKG, "liblilac_b200.so")
 
 i64 = C.c_int64
 i64p = C.POINTER(C.c_int64)

@@ -114,7 +114,13 @@ CsrKernel parse_csr_kernel(const std::string& s);
 // a lane's first nonzero); each lane has a 2-byte descriptor = tile-local row
 // of its first nonzero | kLaneCont when that row began in an earlier lane.
 // HBM cost: 10 bytes per stored nonzero + 64 bytes per run.
-constexpr int kTileThreads = 1024;
+// 16 warps per tile with 4 chunks in flight per lane (116 registers) beat 32
+// warps with 2 (64 registers): NPB C 73.8 -> 71.6 us, 479 -> 502 it/s
+// (sweep: 1024/2, 1024/3, 768/3, 768/4, 512/2, 512/4, 512/5, 384/6, 256/8)
+#ifndef LILAC_TILE_THREADS
+#define LILAC_TILE_THREADS 512
+#endif
+constexpr int kTileThreads = LILAC_TILE_THREADS;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kSlabW = 12288;            // columns per slab: 2 x 96 KB double-buffered in smem
 constexpr int kSlabStride = kSlabW + 2;  // + a zero cell (column kSlabW) read by padding entries

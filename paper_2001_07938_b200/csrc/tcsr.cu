@@ -228,24 +228,31 @@ __device__ __forceinline__ void reduce_lanes(unsigned k1, double p1, bool split,
     __syncwarp();
 }
 
-// Lane `lane`'s chunks 0 and 1 of the run [lo, hi) (those it has: lane l
+#ifndef LILAC_TILE_PIPE
+#define LILAC_TILE_PIPE 4
+#endif
+// chunks in flight per lane: a register ring, chunk i in slot i % kPipe
+constexpr int kPipe = LILAC_TILE_PIPE;
+
+// Lane `lane`'s first kPipe chunks of the run [lo, hi) (those it has: lane l
 // gets m or m + 1 chunks, m = C / 32).
-__device__ __forceinline__ void load_head_chunks(Chunk& c0, Chunk& c1, const double* vb, const std::uint16_t* kb,
+__device__ __forceinline__ void load_head_chunks(Chunk (&ring)[kPipe], const double* vb, const std::uint16_t* kb,
                                                  int lo, int hi, int lane, std::uint64_t pol) {
     const int C = (hi - lo) / kChunk;
     const int cnt = (C >> 5) + (lane < (C & 31) ? 1 : 0);
     const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);
-    if (cnt > 0) load_chunk(c0, vb, kb, e0, pol);
-    if (cnt > 1) load_chunk(c1, vb, kb, e0 + 128u, pol);
+#pragma unroll
+    for (int u = 0; u < kPipe; ++u)
+        if (cnt > u) load_chunk(ring[u], vb, kb, e0 + 128u * u, pol);
 }
 
 // Processes a (slab, warp) run [lo, hi) (tile-relative, multiples of kChunk)
 // with lane descriptor `ld` against the slab in shared memory at xb_s. The
-// run's bytes were prefetched into L2 one slab ahead; the next chunk is
-// loaded while the current one is walked.
+// run's bytes were prefetched into L2 one slab ahead; each ring slot is
+// refilled with the chunk kPipe ahead as soon as it has been walked.
 template <int MODE>
 __device__ __forceinline__ void process_run(const double* vb, const std::uint16_t* kb, int lo, int hi, unsigned ld,
-                                            Chunk& ca, Chunk& cb, int next_lo, int next_hi, std::uint32_t xb_s,
+                                            Chunk (&ring)[kPipe], int next_lo, int next_hi, std::uint32_t xb_s,
                                             std::uint32_t yp_s, int lane) {
     std::uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -254,18 +261,18 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
     const unsigned e0 = static_cast<unsigned>(lo + kChunk * lane);  // chunk i at e0 + 128 i
     Walk w{ld & 0x7fffu, 0.0, false};
     xb_s = opaque_u32(xb_s);  // one base register: a gather address is one LEA
-    // chunks 0 and 1 were loaded during the previous run; each buffer is
-    // refilled with the chunk two ahead as soon as it has been walked
-    for (int i = 0; i < iters; i += 2) {
-        if (cnt > i) walk_chunk<MODE>(w, ca, xb_s, yp_s);
-        if (cnt > i + 2) load_chunk(ca, vb, kb, e0 + 128u * (i + 2), pol);
-        if (i + 1 >= iters) break;
-        if (cnt > i + 1) walk_chunk<MODE>(w, cb, xb_s, yp_s);
-        if (cnt > i + 3) load_chunk(cb, vb, kb, e0 + 128u * (i + 3), pol);
+    // the first kPipe chunks were loaded during the previous run
+    for (int i = 0; i < iters; i += kPipe) {
+#pragma unroll
+        for (int u = 0; u < kPipe; ++u) {
+            if (i + u >= iters) break;
+            if (cnt > i + u) walk_chunk<MODE>(w, ring[u], xb_s, yp_s);
+            if (cnt > i + u + kPipe) load_chunk(ring[u], vb, kb, e0 + 128u * (i + u + kPipe), pol);
+        }
     }
-    // the next run's first two chunks stream in during this run's lane
-    // reduction and the next slab wait (the matrix does not depend on x)
-    load_head_chunks(ca, cb, vb, kb, next_lo, next_hi, lane, pol);
+    // the next run's first chunks stream in during this run's lane reduction
+    // and the next slab wait (the matrix does not depend on x)
+    load_head_chunks(ring, vb, kb, next_lo, next_hi, lane, pol);
     if (MODE >= 2) {  // probe: no row sums
         if (w.acc == 12345.678) sts_add_f64(yp_s, w.acc);
         return;
@@ -343,11 +350,11 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         }
         // lane descriptors and each run's first chunk are loaded one run ahead (registers)
         unsigned dnext = T.nslabs > 0 ? __ldg(lr + warp * 32) : 0u;
-        Chunk ca, cb;
+        Chunk ring[kPipe];
         if (T.nslabs > 0) {
             std::uint64_t pol;
             asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            load_head_chunks(ca, cb, vb, kb, run_lo(0), run_hi(0), lane, pol);
+            load_head_chunks(ring, vb, kb, run_lo(0), run_hi(0), lane, pol);
         }
         if (tid == 0 && gate) {
             unsigned v;
@@ -385,7 +392,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             const bool more = k + 1 < T.nslabs;
             const int nlo = more ? run_lo(k + 1) : 0, nhi = more ? run_hi(k + 1) : 0;
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
-                vb, kb, run_lo(k), run_hi(k), dcur, ca, cb, nlo, nhi,
+                vb, kb, run_lo(k), run_hi(k), dcur, ring, nlo, nhi,
                 c.xs_s + 8u * static_cast<unsigned>(buf * c.stride), c.yp_s, lane);
             __syncwarp();
             if (lane == 0) {
