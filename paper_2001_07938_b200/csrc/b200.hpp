@@ -206,7 +206,13 @@ struct SplitDev {
 // and end goes to a per-unit carry; a fix-up pass sums every row that crossed
 // units from a structural plan built with the layout (one thread per short
 // crossing, one warp per long one: a fixed order, deterministic). HBM: 12 bytes per nonzero + 4 per 4 kLrcChunks nonzeros.
-constexpr int kLrcChunks = 8;
+// units of 32 x 16 x 4 = 2048 nonzeros: Kronecker-22 231 -> 225 us, stencil
+// N=420 SpMV 0.92 -> 0.945 of copy (4: 247 us; 32: 271 us — fewer, longer
+// units under-fill the tail)
+#ifndef LILAC_LRC_CHUNKS
+#define LILAC_LRC_CHUNKS 16
+#endif
+constexpr int kLrcChunks = LILAC_LRC_CHUNKS;
 constexpr int kLrcLaneNnz = 4 * kLrcChunks;
 constexpr int kLrcUnit = 32 * kLrcLaneNnz;
 constexpr std::uint32_t kLrcStart = 1u << 31;

@@ -33,7 +33,10 @@ namespace b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kLrcThreads = 1024;
+#ifndef LILAC_LRC_THREADS
+#define LILAC_LRC_THREADS 1024
+#endif
+constexpr int kLrcThreads = LILAC_LRC_THREADS;
 constexpr int kLrcWarps = kLrcThreads / 32;
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
