@@ -344,6 +344,9 @@ int b200_dist_cg_bounds(const b200_dist_cg* d, int64_t* bounds);
  * updates + the p exchange); finish = |b - A z| (gathers z); scalars copies
  * rho and rnorm to the host on `stream`. */
 int b200_dist_cg_start_rowsum(b200_dist_cg* d, void* stream);
+/* Plain sharded CG from b = the shards' x (e.g. b200_dist_cg_load_x from
+ * host memory): z = 0, r = p = b. */
+int b200_dist_cg_start(b200_dist_cg* d, void* stream);
 int b200_dist_cg_step(b200_dist_cg* d, void* stream);
 int b200_dist_cg_finish(b200_dist_cg* d, void* stream);
 int b200_dist_cg_scalars(b200_dist_cg* d, void* stream, double* rho, double* rnorm);

@@ -115,6 +115,7 @@ SIGNATURES = {
     "b200_dist_cg_create_stencil27_local": (C.c_int, [C.POINTER(vp), C.c_int, i64, C.c_double, C.c_double]),
     "b200_dist_cg_bounds": (C.c_int, [vp, i64p]),
     "b200_dist_cg_start_rowsum": (C.c_int, [vp, vp]),
+    "b200_dist_cg_start": (C.c_int, [vp, vp]),
     "b200_dist_cg_step": (C.c_int, [vp, vp]),
     "b200_dist_cg_finish": (C.c_int, [vp, vp]),
     "b200_dist_cg_scalars": (C.c_int, [vp, vp, f64p, f64p]),

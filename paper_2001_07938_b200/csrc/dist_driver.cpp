@@ -558,6 +558,10 @@ int b200_dist_cg_start_rowsum(b200_dist_cg* d, void* stream) {
     });
 }
 
+int b200_dist_cg_start(b200_dist_cg* d, void* stream) {
+    return boundary("b200_dist_cg_start", [&] { dist_init(d, stream ? static_cast<cudaStream_t>(stream) : d->stream); });
+}
+
 int b200_dist_cg_step(b200_dist_cg* d, void* stream) {
     return boundary("b200_dist_cg_step", [&] { dist_step(d, stream ? static_cast<cudaStream_t>(stream) : d->stream); });
 }

@@ -254,6 +254,10 @@ class DistCG:
         """x = b = A 1, z = 0, r = p = b (plain CG, the stencil config)."""
         N.check(N.lib().b200_dist_cg_start_rowsum(self._h, C.c_void_p(stream)))
 
+    def start(self, stream: int = 0):
+        """b = the shards' x (load_x first), z = 0, r = p = b."""
+        N.check(N.lib().b200_dist_cg_start(self._h, C.c_void_p(stream)))
+
     def step(self, stream: int = 0):
         N.check(N.lib().b200_dist_cg_step(self._h, C.c_void_p(stream)))
 
