@@ -298,3 +298,28 @@ def test_sharded_stencil420_matches_single():
     # barely diagonally dominant operator CG amplifies those roundings (seen:
     # 2e-8 relative after 8 steps) — a missing halo would be O(1)
     assert abs(rn_k - rn1) <= 1e-6 * rn1 and abs(rho_k - rho1) <= 1e-6 * rho1, (rn_k, rn1, rho_k, rho1)
+
+
+def test_sharded_stencil_start_from_host_b():
+    """b200_dist_cg_load_x + b200_dist_cg_start (b from pinned host memory, the
+    bench's N > 1 e2e path) gives the same CG as b = A 1 formed on the device."""
+    import torch
+    nx = 30
+    n = nx ** 3
+    d = D.DistCG.stencil27_local(3, nx)
+    try:
+        d.start_rowsum()
+        for _ in range(10):
+            d.step()
+        d.finish()
+        rho_a, rn_a = d.scalars()
+        bh = torch.from_numpy(W.stencil27_rowsum(nx, 0, n)).pin_memory()
+        d.load_x(bh.data_ptr())
+        d.start()
+        for _ in range(10):
+            d.step()
+        d.finish()
+        rho_b, rn_b = d.scalars()
+    finally:
+        d.free()
+    assert abs(rn_a - rn_b) <= 1e-9 * max(rn_a, 1e-300) and abs(rho_a - rho_b) <= 1e-9 * rho_a
