@@ -93,6 +93,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true", help="skip the NPB zeta gate (profiling runs only)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e legs (profiling runs only)")
+    ap.add_argument("--no-scaling-model", action="store_true",
+                    help="skip the per-shard SpMV timings (npb_c, stencil at N=1)")
     a = ap.parse_args(argv)
     if a.warmup < 3 and not a.dry_run and a.impl == "ours":
         ap.error("--warmup must be >= 3")
@@ -596,6 +598,25 @@ class Ctx:
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
+    def kernel_ms_cold(self, launch, reps, flush):
+        """Mean CUDA-event time of `reps` launches, each after `flush()` (a
+        pass over a buffer larger than L2) and bracketed by its own pair of
+        events."""
+        import torch
+        for _ in range(3):
+            launch()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        torch.cuda.synchronize()
+        with torch.cuda.stream(self.stream):
+            torch.cuda._sleep(int(2e6) + reps * 200000)
+            for e0, e1 in ev:
+                flush()
+                e0.record(self.stream)
+                launch()
+                e1.record(self.stream)
+        torch.cuda.synchronize()
+        return sum(e0.elapsed_time(e1) for e0, e1 in ev) / reps
+
     def finish(self, line):
         if self.rank == 0:
             print(json.dumps(line), flush=True)
@@ -603,6 +624,45 @@ class Ctx:
             import torch.distributed as dist
             dist.destroy_process_group()
         return 0
+
+
+def shard_scaling(ctx, n, full, make_shard, pick, reps, ks=(2, 4, 8)):
+    """Kernel-only SpMV scaling of a row-sharded config, measured on this one
+    GPU: each shard's row block built as its own resident matrix (the layout
+    the sharded driver builds for it) and timed alone over the full x; the
+    parallel SpMV time at k GPUs is the slowest shard's. Cold = L2 flushed
+    before every launch (the shard's matrix re-read from HBM); warm =
+    back-to-back launches (at large k a shard's matrix fits in the 126 MB L2,
+    as it would between the CG steps of a real k-GPU run). The flush reads a
+    256 MB buffer (a write would leave dirty lines whose write-back lands in
+    the timed launch). The p exchange is
+    not in these numbers: every gpurun call gets one GPU."""
+    import torch
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(11))
+    junk = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
+
+    def flush():  # a read, not a write: no dirty lines left to write back during the timed launch
+        torch.sum(junk, dim=0, out=sink)
+
+    def times(M, rows):
+        y = torch.empty(max(rows, 1), dtype=torch.float64, device="cuda")
+        f = lambda: M.spmv(x.data_ptr(), y.data_ptr(), ctx.sh)  # noqa: E731
+        return ctx.kernel_ms_cold(f, reps, flush), ctx.kernel_ms(f, reps)
+    full_cold, full_warm = times(*full)
+    out = {"full_ms_cold": full_cold, "full_ms_warm": full_warm, "exchange": "not included (one GPU per run)"}
+    for k in ks:
+        cold, warm, timed = [], [], list(pick(k))
+        for g in timed:
+            M, rows = make_shard(k, g)
+            c, w = times(M, rows)
+            M.free()
+            cold.append(c)
+            warm.append(w)
+        out[str(k)] = {"shards_timed": timed, "max_shard_ms_cold": max(cold), "max_shard_ms_warm": max(warm),
+                       "efficiency_cold": full_cold / (k * max(cold)), "efficiency_warm": full_warm / (k * max(warm))}
+    del junk, sink
+    return out
 
 
 def harness_bytes(H, st0, st1):
@@ -793,6 +853,13 @@ def run_npb(ctx, cls):
                                           "(b200_matrix_create_csr / the sharded driver's shard upload)"}
     line["gen_s"] = t_gen
 
+    if ctx.world == 1 and cls == "C" and not args.no_scaling_model:
+        def npb_shard(k, g):
+            b = D.partition_rows(rp, k)
+            r0, r1 = int(b[g]), int(b[g + 1])
+            return D.Matrix.csr(np.ascontiguousarray(rp[r0:r1 + 1] - rp[r0]), np.ascontiguousarray(ci[rp[r0]:rp[r1]]),
+                                np.ascontiguousarray(val[rp[r0]:rp[r1]])), r1 - r0
+        line["spmv_shard_scaling"] = shard_scaling(ctx, na, (A, na), npb_shard, lambda k: range(k), 20)
     if ctx.world == 1 and not args.no_e2e:
         lazy = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "lazy", "pinned")
         lazy_pageable = e2e_npb_c_host(rp, ci, val, na, shift, args.warmup, args.steps, "lazy", "pageable")
@@ -1175,6 +1242,11 @@ def run_stencil(ctx):
             del bd
         ys_h = ys.cpu().numpy()
         xs_h = xs.cpu().numpy()
+        if not args.no_scaling_model:
+            def st_shard(k, g):
+                b = W.stencil27_bounds(nx, k)
+                return D.Matrix.stencil27_rows(nx, int(b[g]), int(b[g + 1])), int(b[g + 1] - b[g])
+            line["spmv_shard_scaling"] = shard_scaling(ctx, n, (A, n), st_shard, lambda k: (0, k // 2), 3)
     else:
         line["gpu_launches"] = args.steps * (6 + 1)
         if not args.no_e2e:

@@ -217,6 +217,10 @@ int b200_axpy_device(int64_t n, double* y_device, double alpha, const double* x_
  * `offdiag` elsewhere (26.1 / -1 gives the SPD operator of the config). nx^3
  * must fit int32 columns (nx <= 1290). */
 int b200_matrix_create_stencil27(b200_matrix** out, int64_t nx, double diag, double offdiag);
+/* Rows [r0, r1) of the same operator as a resident matrix of r1 - r0 rows
+ * over the full nx^3 columns (one shard of the row-sharded config). */
+int b200_matrix_create_stencil27_rows(b200_matrix** out, int64_t nx, int64_t r0, int64_t r1, double diag,
+                                      double offdiag);
 /* `iters` PageRank steps on device vectors (SURVEY §8(d) input 4):
  * work = A x; x = damping*work + (1-damping)/n. A is the column-stochastic
  * transposed adjacency; x holds the start vector (e.g. 1/n). */

@@ -80,6 +80,7 @@ SIGNATURES = {
     "b200_dot_device": (C.c_int, [vp, vp, i64, vp, vp]),
     "b200_axpy_device": (C.c_int, [i64, vp, C.c_double, vp, vp]),
     "b200_matrix_create_stencil27": (C.c_int, [C.POINTER(C.c_void_p), i64, C.c_double, C.c_double]),
+    "b200_matrix_create_stencil27_rows": (C.c_int, [C.POINTER(C.c_void_p), i64, i64, i64, C.c_double, C.c_double]),
     "b200_pagerank_device": (C.c_int, [vp, C.c_double, C.c_int, vp, vp, vp]),
     "b200_cg_solve": (C.c_int, [vp, vp, C.c_int, vp, C.POINTER(C.c_double)]),
     "b200_dbuf_alloc": (C.c_int, [C.POINTER(B200Buf), C.c_size_t]),

@@ -159,6 +159,17 @@ struct TcsrDev {
     const std::uint16_t* lrow = nullptr;      // ntiles x nslabs*kTileWarps x 32 lane descriptors
     const double* val = nullptr;              // stored nonzeros (+ pads), tiled order
     const std::uint16_t* key = nullptr;       // same: tcsr_key(slab-local column, row start)
+    // Slab parts: with parts > 1 a tile's slabs are cut into `parts`
+    // contiguous ranges, one CTA each (work item t * parts + part). Each part
+    // stores its row sums in ypart[part * rows + row]; the part that finishes
+    // last (tile_done ticket) adds the parts in part order into y. Fewer,
+    // taller tiles then stage fewer x slabs per CTA (small matrices with
+    // random columns, where re-staging all of x per tile dominates).
+    int parts = 1;
+    std::int64_t rows = 0;
+    double* ypart = nullptr;        // parts x rows (parts > 1)
+    unsigned* tile_done = nullptr;  // ntiles tickets, zero between launches
+    double* tile_pq = nullptr;      // ntiles: each tile's x.y share (DOT), summed in tile order
 };
 
 // Merge-path plan (merge.cu): per-CTA start coordinates on the merge of row

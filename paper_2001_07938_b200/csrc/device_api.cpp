@@ -236,6 +236,39 @@ int b200_matrix_create_stencil27(b200_matrix** out, std::int64_t nx, double diag
     });
 }
 
+int b200_matrix_create_stencil27_rows(b200_matrix** out, std::int64_t nx, std::int64_t r0, std::int64_t r1,
+                                      double diag, double offdiag) {
+    return boundary("b200_matrix_create_stencil27_rows", [&] {
+        ensure_init();
+        if (!out) throw Error(Errc::DataError, "out is NULL");
+        const std::int64_t n = nx * nx * nx;
+        if (nx < 1 || n - 1 > INT32_MAX) throw Error(Errc::DataError, "nx must give int32 column indices");
+        if (r0 < 0 || r1 < r0 || r1 > n) throw Error(Errc::DataError, "row range outside [0, nx^3]");
+        auto A = std::make_unique<b200_matrix>();
+        A->format = 0;
+        A->device = rt().device;
+        gen_stencil27_rows_device(nx, r0, r1, diag, offdiag, A->row_ptr, A->col, A->val, rt().stream);
+        CsrDev& d = A->csr;
+        d.rows = r1 - r0;
+        d.nnz = stencil27_prefix_nnz(nx, r1) - stencil27_prefix_nnz(nx, r0);
+        d.cols = n;  // global columns: the block reads the full x
+        d.max_row = d.rows ? std::min<std::int64_t>(27, n) : 0;
+        d.row_ptr = A->row_ptr.as<std::int64_t>();
+        d.col = A->col.ptr;
+        d.col32 = true;
+        d.val = A->val.as<double>();
+        d.monotone = true;
+        A->max_row = d.max_row;
+        const CsrKernel pol = rt().kernel;
+        if (d.rows && ((pol == CsrKernel::Auto && d.nnz >= (std::int64_t(16) << 20)) || pol == CsrKernel::Lane)) {
+            lrc_build_device(d.rows, d.row_ptr, d.col, true, d.val, d.nnz, n, A->lrc, rt().stream);
+            d.lrc = &A->lrc.dev;
+        }
+        drop_plain(*A);
+        *out = A.release();
+    });
+}
+
 int b200_pagerank_device(const b200_matrix* A, double damping, int iters, double* x, double* work, void* stream) {
     return boundary("b200_pagerank_device", [&] {
         if (!A || A->format != 0) throw Error(Errc::DataError, "PageRank needs a CSR matrix");

@@ -672,6 +672,10 @@ unsigned grid_for(std::int64_t threads, unsigned cap = kSMs * 16) {
     return static_cast<unsigned>(std::max<std::int64_t>(1, std::min<std::int64_t>(b, cap)));
 }
 
+#ifndef LILAC_VEC_U
+#define LILAC_VEC_U 2
+#endif
+
 template <int S, typename IdxT, bool DOT>
 void vector_launch(const CsrDev& A, const double* x, double* y, double* partials, unsigned* ticket,
                    CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off, std::int64_t max_len) {
@@ -691,7 +695,7 @@ void vector_launch(const CsrDev& A, const double* x, double* y, double* partials
                                                                 A.val, x, y, partials, ticket, sc, dot_off);
         return;
     }
-    k_csr_vector<S, 2, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
+    k_csr_vector<S, LILAC_VEC_U, IdxT, DOT><<<grid, kThreads, 0, s>>>(A.rows, A.row_ptr, static_cast<const IdxT*>(A.col),
                                                             A.val, x, y, partials, ticket, sc, dot_off, max_len);
 }
 

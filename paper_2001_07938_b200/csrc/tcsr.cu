@@ -327,7 +327,12 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
     double* xs = c.xs;
     double* yp = c.yp;
     double pq = 0.0;
-    for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+    const int P = T.parts;
+    const std::int64_t items = T.ntiles * P;
+    for (std::int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const std::int64_t t = item / P;
+        const int part = static_cast<int>(item - t * P);
+        const int k0 = part * T.nslabs / P, k1 = (part + 1) * T.nslabs / P;  // this part's slabs
         const std::int64_t row0 = T.tile_row0[t];
         const int nrows = static_cast<int>(T.tile_row0[t + 1] - row0);
         const std::int64_t base = T.tile_base[t];
@@ -344,17 +349,17 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             return k < 32 ? __shfl_sync(kFull, whi, k) : __ldg(wo + k * kTileWarps + warp + 1);
         };
         for (int r = tid; r < nrows; r += kTileThreads) yp[r] = 0.0;
-        for (int k = 0; k < kPfAhead && k < T.nslabs; ++k) {  // runs stream into L2 kPfAhead slabs ahead
+        for (int k = k0; k < k0 + kPfAhead && k < k1; ++k) {  // runs stream into L2 kPfAhead slabs ahead
             const int plo = run_lo(k), phi = run_hi(k);
             if (lane == 0) prefetch_run(vb, kb, plo, phi);
         }
         // lane descriptors and each run's first chunk are loaded one run ahead (registers)
-        unsigned dnext = T.nslabs > 0 ? __ldg(lr + warp * 32) : 0u;
+        unsigned dnext = k1 > k0 ? __ldg(lr + (k0 * kTileWarps + warp) * 32) : 0u;
         Chunk ring[kPipe];
-        if (T.nslabs > 0) {
+        if (k1 > k0) {
             std::uint64_t pol;
             asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            load_head_chunks(ring, vb, kb, run_lo(0), run_hi(0), lane, pol);
+            load_head_chunks(ring, vb, kb, run_lo(k0), run_hi(k0), lane, pol);
         }
         if (tid == 0 && gate) {
             unsigned v;
@@ -363,16 +368,16 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             } while (v < gate_target);
             gate = nullptr;
         }
-        if (tid == 0 && T.nslabs > 0 && MODE < 5) {
+        if (tid == 0 && k1 > k0 && MODE < 5) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
-            issue_slab(T, x, xs, 0, &c.mbar[0]);
-            if (T.nslabs > 1) issue_slab(T, x, xs + c.stride, 1, &c.mbar[1]);
+            issue_slab(T, x, xs, k0, &c.mbar[0]);
+            if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1]);
         }
         __syncthreads();
         // Free-running slabs: a warp moves on as soon as the next slab has
         // landed; the last warp to release a buffer refills it (no CTA barrier).
-        for (int k = 0; k < T.nslabs; ++k) {
-            const int buf = k & 1;
+        for (int k = k0; k < k1; ++k) {
+            const int buf = (k - k0) & 1;
             if (MODE >= 5) {
             } else if (buf == 0) {
                 mbar_wait(&c.mbar[0], c.phase0);
@@ -382,14 +387,14 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                 c.phase1 ^= 1;
             }
             const unsigned dcur = dnext;
-            if (k + 1 < T.nslabs) {
-                if (k + kPfAhead < T.nslabs) {
+            if (k + 1 < k1) {
+                if (k + kPfAhead < k1) {
                     const int plo = run_lo(k + kPfAhead), phi = run_hi(k + kPfAhead);
                     if (lane == 0) prefetch_run(vb, kb, plo, phi);
                 }
                 dnext = __ldg(lr + ((k + 1) * kTileWarps + warp) * 32);
             }
-            const bool more = k + 1 < T.nslabs;
+            const bool more = k + 1 < k1;
             const int nlo = more ? run_lo(k + 1) : 0, nhi = more ? run_hi(k + 1) : 0;
             process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
                 vb, kb, run_lo(k), run_hi(k), dcur, ring, nlo, nhi,
@@ -399,18 +404,53 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                 __threadfence_block();
                 if (atomicAdd(&c.released[buf], 1u) == kTileWarps - 1) {
                     c.released[buf] = 0;
-                    if (k + 2 < T.nslabs && MODE < 5) {
+                    if (k + 2 < k1 && MODE < 5) {
                         if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");
                         issue_slab(T, x, xs + buf * c.stride, k + 2, &c.mbar[buf]);
                     }
                 }
             }
         }
-        __syncthreads();  // every row of the tile is complete
-        for (int r = tid; r < nrows; r += kTileThreads) {
-            const double v = yp[r];
-            y[row0 + r] = v;
-            if (DOT) pq += v * (COHERENT ? __ldcg(x + dot_off + row0 + r) : __ldg(x + dot_off + row0 + r));
+        __syncthreads();  // every row of the tile (this part's slabs) is complete
+        if (P == 1) {
+            for (int r = tid; r < nrows; r += kTileThreads) {
+                const double v = yp[r];
+                y[row0 + r] = v;
+                if (DOT) pq += v * (COHERENT ? __ldcg(x + dot_off + row0 + r) : __ldg(x + dot_off + row0 + r));
+            }
+        } else {
+            // this part's row sums out; the tile's last part adds all parts
+            // in part order (the same bits whichever part finishes last)
+            double* mine = T.ypart + static_cast<std::int64_t>(part) * T.rows + row0;
+            for (int r = tid; r < nrows; r += kTileThreads) __stcg(mine + r, yp[r]);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) c.released[2] = atomicAdd(&T.tile_done[t], 1u) == static_cast<unsigned>(P - 1) ? 1u : 0u;
+            __syncthreads();
+            if (c.released[2]) {  // CTA-uniform
+                __threadfence();
+                double tpq = 0.0;
+                for (int r = tid; r < nrows; r += kTileThreads) {
+                    double v = __ldcg(T.ypart + row0 + r);
+                    for (int q = 1; q < P; ++q) v += __ldcg(T.ypart + static_cast<std::int64_t>(q) * T.rows + row0 + r);
+                    y[row0 + r] = v;
+                    if (DOT) tpq += v * (COHERENT ? __ldcg(x + dot_off + row0 + r) : __ldg(x + dot_off + row0 + r));
+                }
+                if (DOT) {
+                    // the tile's share of x.y by tile (not by CTA: which CTA
+                    // finalises a tile varies run to run), summed later in
+                    // tile order
+                    __shared__ double tred[kTileWarps];
+                    tpq = warp_sum(tpq);
+                    if (lane == 0) tred[warp] = tpq;
+                    __syncthreads();
+                    if (warp == 0) {
+                        tpq = warp_sum(lane < kTileWarps ? tred[lane] : 0.0);
+                        if (lane == 0) T.tile_pq[t] = tpq;
+                    }
+                }
+                if (tid == 0) T.tile_done[t] = 0u;  // next launch
+            }
         }
         __syncthreads();  // yp reused by the next tile
     }
@@ -423,15 +463,18 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                  unsigned int* ticket, CgScalars* sc, std::int64_t dot_off) {
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) std::uint64_t mbar[2];
-    __shared__ unsigned released[2];
+    __shared__ unsigned released[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     TileCta c;
     tile_cta_init(c, T, smem, mbar, released);
     if (DOT) {  // CG step: launched programmatically after update_p
         pdl_trigger();
-        if (lane == 0 && blockIdx.x < T.ntiles && T.nslabs > 0) {  // the matrix does not depend on it
-            const std::int32_t* wo = T.woff + blockIdx.x * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
-            prefetch_run(T.val + T.tile_base[blockIdx.x], T.key + T.tile_base[blockIdx.x], wo[warp], wo[warp + 1]);
+        if (lane == 0 && blockIdx.x < T.ntiles * T.parts && T.nslabs > 0) {  // the matrix does not depend on it
+            const std::int64_t t = blockIdx.x / T.parts;
+            const int k0 = static_cast<int>(blockIdx.x - t * T.parts) * T.nslabs / T.parts;
+            const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1) +
+                                     k0 * kTileWarps;
+            prefetch_run(T.val + T.tile_base[t], T.key + T.tile_base[t], wo[warp], wo[warp + 1]);
         }
         pdl_wait();
     }
@@ -454,8 +497,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         __syncthreads();
         if (last) {
             __threadfence();
+            // per-CTA partials, or with slab parts the per-tile ones (CTA partials are 0)
+            const double* src = T.parts > 1 ? T.tile_pq : partials;
+            const unsigned n = T.parts > 1 ? static_cast<unsigned>(T.ntiles) : gridDim.x;
             double a = 0.0;
-            for (unsigned i = tid; i < gridDim.x; i += kTileThreads) a += __ldcg(partials + i);
+            for (unsigned i = tid; i < n; i += kTileThreads) a += __ldcg(src + i);
             a = warp_sum(a);
             __syncthreads();
             if (lane == 0) red[warp] = a;
@@ -534,7 +580,7 @@ __device__ __forceinline__ double cta_sum_parts(const double* p, int n, double* 
 __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVectors v, int steps) {
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) std::uint64_t mbar[2];
-    __shared__ unsigned released[2];
+    __shared__ unsigned released[3];
     __shared__ double red[kTileWarps + 1];
     const int tid = threadIdx.x;
     TileCta c;
@@ -550,7 +596,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
                                   red);
         if (tid == 0) pq_part[blockIdx.x] = pq;
         grid_sync(bar, target);
-        const double d = cta_sum_parts(pq_part, gridDim.x, red);
+        const double d = T.parts > 1 ? cta_sum_parts(T.tile_pq, static_cast<int>(T.ntiles), red)
+                                     : cta_sum_parts(pq_part, gridDim.x, red);
         const double alpha = rho / d;
         double rr = 0.0;
         for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
@@ -635,7 +682,7 @@ void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, dou
         B200_CUDA(cudaMemcpyAsync(xalign.ptr, x, xb, cudaMemcpyDeviceToDevice, s));
         x = xalign.as<const double>();
     }
-    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(T.ntiles, g_sms));
+    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>(T.ntiles * T.parts, g_sms));
     switch (partials ? 0 : mode) {  // probes never on the fused CG path
     case 1: launch_variant<1>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     case 2: launch_variant<2>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
@@ -665,7 +712,7 @@ bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream
     if (enabled && first_on_device(configured))
         B200_CUDA(cudaFuncSetAttribute(k_cg_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBudget));
     if (!enabled || steps <= 0 || T.ntiles <= 0 || v.row0 != 0 || v.p != v.p_full) return false;
-    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>({T.ntiles, max_grid, kMaxParts}));
+    const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>({T.ntiles * T.parts, max_grid, kMaxParts}));
     B200_CUDA(cudaMemsetAsync(&v.sc->bar, 0, sizeof(unsigned), s));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

@@ -12,6 +12,7 @@ struct TcsrHost {
     std::int64_t ntiles = 0;
     int nslabs = 0;
     int slab_w = kSlabW, rows_max = kMaxTileRows;
+    int parts = 1;  // slab parts per tile (TcsrDev::parts)
     std::int64_t cols = 0;
     std::vector<std::int64_t> tile_row0, tile_base;
     std::vector<std::int32_t> woff;
@@ -28,11 +29,13 @@ bool tcsr_wanted(std::int64_t rows, const std::int64_t* row_ptr, const std::int6
 // distinct x sectors per nonzero over 64 sampled 32-row windows (1 = no
 // locality at all; -1 = too few nonzeros to tell)
 double gather_locality(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind);
+// Slab parts per tile for a matrix (TcsrDev::parts; LILAC_B200_TILE_PARTS overrides).
+int tcsr_parts(std::int64_t rows, std::int64_t nnz, std::int64_t cols, int sms);
 void tcsr_build_host(std::int64_t rows, const std::int64_t* row_ptr, const std::int64_t* col_ind,
                      const double* val, std::int64_t cols, TcsrHost& out);
 
 struct TcsrOwner {
-    DevBuf tile_row0, tile_base, woff, lrow, val, key;
+    DevBuf tile_row0, tile_base, woff, lrow, val, key, ypart, tile_done, tile_pq;
     TcsrDev dev;
     bool valid = false;
     std::int64_t bytes = 0;

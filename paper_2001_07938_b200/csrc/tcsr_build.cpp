@@ -190,6 +190,19 @@ void write_run(const TileRuns& tr, std::int64_t run, const std::int64_t* ci, con
 
 }  // namespace
 
+int tcsr_parts(std::int64_t rows, std::int64_t nnz, std::int64_t cols, int sms) {
+    if (const char* e = std::getenv("LILAC_B200_TILE_PARTS"))  // experiments
+        if (std::atoi(e) >= 1) return std::min(std::atoi(e), 8);
+    (void)rows;
+    if (nnz <= 0) return 1;
+    // R = x bytes staged per CTA / matrix bytes streamed per CTA (P = 1).
+    // Measured on row blocks of NPB class C (profiles/r02_tile_parts.md):
+    // R 0.49 (whole matrix) best at P = 1; 0.98 and 1.48 at P = 2; 1.97 and
+    // up at P = 4 (1/8 block: 26.2 -> 18.5 us); P = 8 loses (more slab edges).
+    const double R = static_cast<double>(cols) * 8.0 * sms / (static_cast<double>(nnz) * 10.0);
+    return R <= 0.7 ? 1 : (R <= 1.5 ? 2 : 4);
+}
+
 bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, std::int64_t cols,
                  bool monotone, std::int64_t max_row, bool forced) {
     if (!monotone || rows <= 0) return false;
@@ -203,8 +216,10 @@ bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* 
     // every tile re-reads all of x slab by slab: each (slab, warp) run must be
     // long enough to amortise a slab (Kronecker scale 22 has ~41 nonzeros per
     // run over 342 slabs and loses 40x; NPB class C has ~590 over 13)
+    const int parts = tcsr_parts(rows, nnz, cols, device_sms());
     const std::int64_t nslabs = (cols + kSlabW - 1) / kSlabW;
-    const std::int64_t tiles = std::max<std::int64_t>(device_sms(), (rows + kMaxTileRows - 1) / kMaxTileRows);
+    const std::int64_t tiles =
+        std::max<std::int64_t>(device_sms() / parts, (rows + kMaxTileRows - 1) / kMaxTileRows);
     if (nnz / (tiles * nslabs * kTileWarps) < 256) return false;
     return gather_locality(rows, rp, ci) > 0.3;
 }
@@ -238,8 +253,12 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     std::vector<std::int64_t> bounds;
     const char* tps = std::getenv("LILAC_B200_TILES_PER_SM");
     const std::int64_t per_sm = (tps && *tps) ? std::max(1, std::atoi(tps)) : 1;
-    const std::int64_t want = std::max<std::int64_t>(sms * per_sm, (rows + kMaxTileRows - 1) / kMaxTileRows);
-    const std::int64_t nt0 = (want + sms - 1) / sms * sms;
+    const std::int64_t min_tiles = (rows + kMaxTileRows - 1) / kMaxTileRows;
+    int parts = tcsr_parts(rows, nnz, cols, sms);
+    if (parts > 1 && min_tiles * parts > sms * per_sm) parts = 1;  // tall enough tiles anyway
+    h.parts = parts;
+    const std::int64_t want = std::max<std::int64_t>((sms * per_sm + parts - 1) / parts, min_tiles);
+    const std::int64_t nt0 = parts > 1 ? want : (want + sms - 1) / sms * sms;
     bounds.push_back(0);
     for (std::int64_t g = 1; g < nt0; ++g) {
         std::int64_t r = lower_bound_rows(rp, 0, rows, base0 + (nnz * g + nt0 - 1) / nt0);
@@ -263,6 +282,18 @@ void tcsr_build_host(std::int64_t rows, const std::int64_t* rp, const std::int64
     if (const char* e = std::getenv("LILAC_B200_SLAB_W"))  // experiments: a narrower slab
         if (std::atoi(e) >= 1024) h.slab_w = std::min(h.slab_w, std::atoi(e) & ~7);
     h.nslabs = static_cast<int>((cols + h.slab_w - 1) / h.slab_w);
+    if (parts > 1) {  // a multiple of `parts` slabs of equal width: parts of equal work
+        const int wmax = h.slab_w;
+        for (int ns = (h.nslabs + parts - 1) / parts * parts;; ns += parts) {
+            const std::int64_t w = ((cols + ns - 1) / ns + 7) / 8 * 8;
+            if (w <= wmax) {
+                h.slab_w = static_cast<int>(w);
+                h.nslabs = static_cast<int>((cols + w - 1) / w);
+                break;
+            }
+        }
+        if (h.nslabs < parts) h.parts = parts = 1;
+    }
     const std::int64_t per_tile = static_cast<std::int64_t>(h.nslabs) * kTileWarps + 1;
     h.woff.assign(static_cast<std::size_t>(h.ntiles * per_tile), 0);
     h.lrow.assign(static_cast<std::size_t>(h.ntiles * (per_tile - 1) * 32), 0);
@@ -349,8 +380,23 @@ void TcsrOwner::upload(const TcsrHost& h) {
     dev.lrow = lrow.as<std::uint16_t>();
     dev.val = val.as<double>();
     dev.key = key.as<std::uint16_t>();
+    dev.parts = h.parts;
+    dev.rows = h.tile_row0.empty() ? 0 : h.tile_row0.back();
+    dev.ypart = nullptr;
+    dev.tile_done = nullptr;
+    dev.tile_pq = nullptr;
+    if (h.parts > 1) {
+        ypart.ensure(static_cast<std::size_t>(h.parts) * static_cast<std::size_t>(dev.rows) * 8);
+        tile_done.ensure(static_cast<std::size_t>(h.ntiles) * 4);
+        tile_pq.ensure(static_cast<std::size_t>(h.ntiles) * 8);
+        B200_CUDA(cudaMemsetAsync(tile_done.ptr, 0, static_cast<std::size_t>(h.ntiles) * 4, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        dev.ypart = ypart.as<double>();
+        dev.tile_done = tile_done.as<unsigned>();
+        dev.tile_pq = tile_pq.as<double>();
+    }
     bytes = static_cast<std::int64_t>(tile_row0.bytes + tile_base.bytes + woff.bytes + lrow.bytes + val.bytes +
-                                      key.bytes);
+                                      key.bytes + ypart.bytes + tile_done.bytes + tile_pq.bytes);
     valid = true;
 }
 
@@ -361,6 +407,9 @@ void TcsrOwner::release() {
     lrow.release();
     val.release();
     key.release();
+    ypart.release();
+    tile_done.release();
+    tile_pq.release();
     dev = TcsrDev{};
     valid = false;
     bytes = 0;

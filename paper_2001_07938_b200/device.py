@@ -39,6 +39,14 @@ class Matrix:
         N.check(N.lib().b200_matrix_create_stencil27(C.byref(h), int(nx), float(diag), float(offdiag)))
         return cls(h)
 
+    @classmethod
+    def stencil27_rows(cls, nx: int, r0: int, r1: int, diag: float = 26.1, offdiag: float = -1.0):
+        """Rows [r0, r1) of `stencil27(nx)` (all nx^3 columns): one row shard."""
+        h = C.c_void_p()
+        N.check(N.lib().b200_matrix_create_stencil27_rows(C.byref(h), int(nx), int(r0), int(r1), float(diag),
+                                                          float(offdiag)))
+        return cls(h)
+
     @property
     def handle(self):
         return self._h

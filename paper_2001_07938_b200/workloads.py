@@ -138,6 +138,45 @@ def stencil27_nnz(nx: int) -> int:
     return a * a * a
 
 
+def stencil27_prefix_nnz(nx: int, r: int) -> int:
+    """Nonzeros in rows [0, r) of the stencil (csrc/workloads_dev.cu's
+    stencil27_prefix_nnz): per axis a point has 1 + (v > 0) + (v < nx - 1)
+    neighbours, so a row's count is the product over its three coordinates."""
+    def span(v):
+        return 1 + (v > 0) + (v < nx - 1)
+
+    def cum(m):  # sum of span(v) for v < m
+        return m + max(m - 1, 0) + min(m, nx - 1)
+    S = cum(nx)
+    i, rem = divmod(r, nx * nx)
+    j, k = divmod(rem, nx)
+    total = cum(i) * S * S
+    if i < nx:
+        total += span(i) * (cum(j) * S + span(j) * cum(k))
+    return total
+
+
+def stencil27_bounds(nx: int, k: int):
+    """The sharded driver's row bounds (dist_driver.cpp stencil_bounds): shard
+    g starts at the first row whose prefix nonzero count reaches
+    ceil(nnz * g / k)."""
+    n = nx ** 3
+    nnz = stencil27_prefix_nnz(nx, n)
+    b = [0] * (k + 1)
+    for g in range(1, k):
+        target = (nnz * g + k - 1) // k
+        lo, hi = b[g - 1], n
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if stencil27_prefix_nnz(nx, mid) < target:
+                lo = mid + 1
+            else:
+                hi = mid
+        b[g] = lo
+    b[k] = n
+    return np.array(b, np.int64)
+
+
 def gen_stencil27_rows(nx: int, r0: int = 0, r1: int | None = None, diag: float = 26.1, offdiag: float = -1.0):
     """Rows [r0, r1) of the 27-point stencil on an nx^3 grid (lexicographic
     rows, neighbours in increasing column order, `diag` on the diagonal): the

@@ -53,6 +53,19 @@ def test_stencil_rows_match_whole_and_rowsum():
     assert B.stencil27_nnz(nx) == rp[-1]
 
 
+def test_stencil_prefix_and_shard_bounds():
+    """The closed-form prefix count (used for the shard bounds) against the
+    generated rows, and the bounds against the oracle's nnz-balanced row
+    partition of the same matrix (the sharded driver's partition)."""
+    for nx in (1, 2, 3, 6):
+        rp, _, _ = B.gen_stencil27(nx)
+        assert [B.stencil27_prefix_nnz(nx, r) for r in range(nx ** 3 + 1)] == list(rp)
+    nx = 12
+    rp, _, _ = B.gen_stencil27(nx)
+    for k in (1, 2, 3, 5, 8):
+        assert np.array_equal(B.stencil27_bounds(nx, k), O.partition_rows(rp, k)), k
+
+
 def test_jds_slices_reproduce_whole_bitwise():
     rp, ci, val = B.gen_parboil(n=5000, nnz_target=50_000)
     perm, nzcnt, jd_ptr, jval, jcol = B.csr_to_jds(rp, ci, val)

@@ -256,6 +256,35 @@ def test_sharded_stencil_matches_single(k):
     assert abs(rn_k - rn1) <= 1e-10 * bn and abs(rho_k - rho1) <= 1e-10 * bn * bn
 
 
+def test_stencil_row_block_matrix():
+    """b200_matrix_create_stencil27_rows: one shard's rows as a resident
+    matrix over the global columns, against the oracle, under the default
+    policy and the lane-range layout."""
+    import torch
+    nx = 30
+    n = nx ** 3
+    x = np.random.default_rng(2).uniform(-1, 1, n)
+    xd = torch.from_numpy(x).cuda()
+    for k, g in ((1, 0), (3, 1), (4, 3)):
+        b = W.stencil27_bounds(nx, k)
+        r0, r1 = int(b[g]), int(b[g + 1])
+        srp, sci, sval = W.gen_stencil27_rows(nx, r0, r1)
+        ref = O.spmv_csr(srp, sci, sval, x)
+        bound = O.spmv_csr(srp, sci, np.abs(sval), np.abs(x))
+        for pol in (b"auto", b"lane"):
+            N.lib().b200_set_kernel(pol)
+            try:
+                M = D.Matrix.stencil27_rows(nx, r0, r1)
+                y = torch.full((r1 - r0,), float("nan"), dtype=torch.float64, device="cuda")
+                M.spmv(xd.data_ptr(), y.data_ptr())
+                torch.cuda.synchronize()
+                assert M.info()["rows"] == r1 - r0 and M.info()["nnz"] == int(srp[-1])
+                M.free()
+            finally:
+                N.lib().b200_set_kernel(b"auto")
+            assert np.all(np.abs(y.cpu().numpy() - ref) <= 1e-12 * bound), (k, g, pol)
+
+
 def test_sharded_stencil420_matches_single():
     """The config-5 operator at full size (N=420, 2.0e9 nonzeros) through the
     sharded driver: 4 local shards, each generating its rows in HBM and

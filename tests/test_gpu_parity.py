@@ -242,6 +242,42 @@ def test_fused_cg_is_deterministic_run_to_run():
     assert abs(got[0][0] - zeta_ref) / zeta_ref <= 1e-10
 
 
+@pytest.mark.parametrize("parts", [1, 2, 3, 4])
+def test_tiled_slab_parts(parts, monkeypatch):
+    """Tiles cut into slab parts (TcsrDev::parts: one CTA per part, the last
+    part of a tile adds the parts in order): SpMV within tolerance of the
+    oracle, and NPB class A CG (the fused kernel's DOT path and the per-step
+    kernels) verifies zeta, for every part count."""
+    monkeypatch.setenv("LILAC_B200_TILE_PARTS", str(parts))
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES["A"]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    N.lib().b200_set_kernel(b"tiled")
+    x = np.random.default_rng(parts).uniform(-1, 1, na)
+    y = run_csr(rp, ci, val, x)
+    assert_within(y, O.spmv_csr(rp, ci, val, x), spmv_bound(rp, ci, val, x))
+    y2 = run_csr(rp, ci, val, x)  # the tickets were reset by the last part
+    assert np.array_equal(y, y2)
+    A = D.Matrix.csr(rp, ci, val)
+    assert A.info()["kernel"] == 4
+    cg = D.CG(A)  # one GPU: the fused persistent kernel
+    zeta, _ = cg.npb(niter, shift)
+    cg.free()
+    A.free()
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10, (parts, zeta)
+    d = D.DistCG.local(2, rp, ci, val)  # shards: the per-step tiled kernel with the p.q partials
+    assert all(d.info(g)["tiled"] for g in range(2))
+    zeta2, _ = d.npb(niter, shift)
+    d.free()
+    assert abs(zeta2 - zeta_ref) / zeta_ref <= 1e-10, (parts, zeta2)
+    # a ragged matrix: empty rows, rows spanning slabs, fewer slabs than parts
+    rng = np.random.default_rng(40 + parts)
+    for cols in (3000, 100_000):
+        rp2, ci2, val2 = random_csr(rng, 20000, cols, rng.integers(0, 120, 20000) * (rng.random(20000) < 0.8))
+        x2 = rng.uniform(-1, 1, cols)
+        y2 = run_csr(rp2, ci2, val2, x2)
+        assert_within(y2, O.spmv_csr(rp2, ci2, val2, x2), spmv_bound(rp2, ci2, val2, x2))
+
+
 def test_fused_cg_matches_per_step_kernels():
     """CG on one GPU with the tiled layout runs its steps in one persistent
     cooperative kernel (k_cg_tiled) — here with more tiles than SMs; the vector

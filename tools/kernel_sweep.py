@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--kernels", default="split,lane")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--shard", default="1:0", help="k:g = row block g of the k-way nnz-balanced partition")
     a = ap.parse_args()
     N.check(N.lib().b200_init(0))
     if a.matrix == "kron":
@@ -43,8 +44,14 @@ def main():
         rp, ci, val = W.gen_parboil()
     else:
         rp, ci, val = W.gen_stencil27(128)
-    n = len(rp) - 1
     cols = int(ci.max()) + 1
+    k, g = (int(v) for v in a.shard.split(":"))
+    if k > 1:
+        b = D.partition_rows(rp, k)
+        r0, r1 = int(b[g]), int(b[g + 1])
+        rp, ci, val = (np.ascontiguousarray(rp[r0:r1 + 1] - rp[r0]), np.ascontiguousarray(ci[rp[r0]:rp[r1]]),
+                       np.ascontiguousarray(val[rp[r0]:rp[r1]]))
+    n = len(rp) - 1
     s = torch.cuda.Stream()
     x = torch.rand(cols, dtype=torch.float64, device="cuda")
     y = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -71,7 +78,7 @@ def main():
         ms = e0.elapsed_time(e1) / a.reps
         by = info["nnz"] * (8 + info["col_bytes"]) + 8 * (info["rows"] + 1) + 16 * info["rows"]
         ok = bool(np.all(np.abs(y.cpu().numpy() - ref) <= 1e-12 * bound))
-        print(json.dumps({"matrix": a.matrix, "requested": k, "kernel": info["kernel"], "us": ms * 1e3,
+        print(json.dumps({"matrix": a.matrix, "shard": a.shard, "requested": k, "kernel": info["kernel"], "us": ms * 1e3,
                           "gbs": by / (ms * 1e-3) / 1e9, "frac": by / (ms * 1e-3) / 1e9 / peak(), "ok": ok,
                           "device_bytes": info["device_bytes"], "hot_env": os.environ.get("LILAC_B200_LRC_HOT")}),
               flush=True)
