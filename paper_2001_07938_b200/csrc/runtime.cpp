@@ -182,7 +182,9 @@ Runtime& rt() { return tl_rt ? *tl_rt : primary_rt(); }
 int harness_ngpus() {
     static const int k = [] {
         const char* e = std::getenv("LILAC_B200_NGPUS");
-        return e && *e ? std::max(1, std::atoi(e)) : 1;
+        // at most 64 shards: multi_dot's per-shard result slots live in the
+        // runtime's 4 KB scalar block (d_result() + g)
+        return e && *e ? std::min(64, std::max(1, std::atoi(e))) : 1;
     }();
     return k;
 }
