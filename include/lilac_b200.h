@@ -116,6 +116,13 @@ int b200_set_writeback(const char* mode);
 void b200_set_profiling(int on);
 /* Materialise lazy write-back bytes in [host, host+bytes) (NULL: all). */
 int b200_host_sync(const void* host, size_t bytes);
+/* A write that does not fault is about to land in [host, host+bytes) — a
+ * system call (read(), recv(), fread() into the buffer) or another library's
+ * DMA — into an array the harness has seen: lazy bytes there are filled, the
+ * change-detection guards over it are lifted (a guarded page would make the
+ * system call fail with EFAULT) and its regions are marked changed, so the
+ * next call re-marshals them; device mirrors of the range are dropped. */
+int b200_host_will_write(void* host, size_t bytes);
 /* The caller is about to free (or hand to an allocator) [host, host+bytes):
  * drop every binding, device mirror, page guard and lazy range over it,
  * without filling (NULL: everything). Guards and lazy pages must not outlive

@@ -62,6 +62,7 @@ SIGNATURES = {
     "b200_set_profiling": (None, [C.c_int]),
     "b200_host_sync": (C.c_int, [vp, C.c_size_t]),
     "b200_host_forget": (C.c_int, [vp, C.c_size_t]),
+    "b200_host_will_write": (C.c_int, [vp, C.c_size_t]),
     "b200_lazy_counters": (C.c_int, [C.POINTER(C.c_int64)] * 6),
     "b200_version": (C.c_char_p, []),
     # 3. counters

@@ -793,6 +793,19 @@ int b200_host_sync(const void* host, size_t bytes) {
     });
 }
 
+int b200_host_will_write(void* host, size_t bytes) {
+    return boundary("b200_host_will_write", [&] {
+        if (!host || bytes == 0) return;
+        // a writer that does not fault (a system call, another library's DMA):
+        // lazy bytes there become real first (a partial write keeps the rest),
+        // guards over the range are lifted and their regions marked changed,
+        // device mirrors of it are dropped
+        lilac::marshal::materialize_range(host, bytes);
+        lilac::marshal::note_host_write(host, bytes);
+        mirrors_forget(host, bytes);
+    });
+}
+
 int b200_host_forget(const void* host, size_t bytes) {
     return boundary("b200_host_forget", [&] {
         if (!host) {

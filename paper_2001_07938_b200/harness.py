@@ -190,6 +190,14 @@ def host_sync(a=None):
         N.check(N.lib().b200_host_sync(N.ptr(a), a.nbytes))
 
 
+def host_will_write(a):
+    """`a` is about to be written by something that does not fault (a system
+    call such as os.readv / file.readinto, or DMA): fill its lazy bytes, lift
+    the change-detection guards (a guarded page makes the system call fail
+    with EFAULT) and mark it changed (include/lilac_b200.h)."""
+    N.check(N.lib().b200_host_will_write(N.ptr(a), a.nbytes))
+
+
 def host_forget(a=None):
     """Drop every binding / mirror / guard / lazy range over `a` (all when
     None) before its memory is freed or recycled (include/lilac_b200.h)."""

@@ -110,6 +110,40 @@ def test_host_sync_materialises_for_dma():
     assert H.lazy_counters()["fault_fills"] == c1["fault_fills"]  # already real: no fault
 
 
+def test_system_call_into_a_guarded_input_after_will_write():
+    """A guarded input (the matrix values, write-protected for change
+    detection) refilled by a system call: without notice the kernel's write
+    fails with EFAULT; after b200_host_will_write it lands, and the next call
+    re-marshals the array (fresh result)."""
+    import os
+    import tempfile
+    rows = 20_000
+    rp, ci, _ = rand_csr(rows, rows, 4, 15)
+    nnz = int(rp[-1])
+    val = H.page_aligned(nnz)
+    val[:] = np.random.default_rng(5).uniform(-1, 1, nnz)
+    x = np.random.default_rng(6).uniform(-1, 1, rows)
+    y = np.zeros(rows)
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    y1 = y.copy()  # fills y (lazy) before anything else
+    new = np.random.default_rng(7).uniform(-1, 1, nnz)
+    with tempfile.TemporaryFile() as f:
+        f.write(new.tobytes())
+        f.flush()
+        f.seek(0)
+        with pytest.raises(OSError):  # EFAULT: the page guards are invisible to the kernel's copy
+            os.readv(f.fileno(), [memoryview(val).cast("B")])
+        f.seek(0)
+        H.host_will_write(val)
+        assert os.readv(f.fileno(), [memoryview(val).cast("B")]) == val.nbytes
+    assert np.array_equal(val, new)
+    y2 = np.zeros(rows)
+    H.spmv_csr(rows, y2, rp, val, x, ci)
+    ref = O.spmv_csr(rp, ci, val, x, rows)
+    assert (np.abs(y2 - ref) <= 1e-12 * O.spmv_csr(rp, ci, np.abs(val), np.abs(x), rows)).all()
+    assert not np.array_equal(y1, y2)
+
+
 def test_misaligned_output_is_lazy():
     """8 bytes past a page boundary: every page the output touches is lazy,
     nothing goes back at the call; the values fill on the first touch."""
