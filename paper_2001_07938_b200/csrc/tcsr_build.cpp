@@ -200,7 +200,13 @@ int tcsr_parts(std::int64_t rows, std::int64_t nnz, std::int64_t cols, int sms) 
     // R 0.49 (whole matrix) best at P = 1; 0.98 and 1.48 at P = 2; 1.97 and
     // up at P = 4 (1/8 block: 26.2 -> 18.5 us); P = 8 loses (more slab edges).
     const double R = static_cast<double>(cols) * 8.0 * sms / (static_cast<double>(nnz) * 10.0);
-    return R <= 0.7 ? 1 : (R <= 1.5 ? 2 : 4);
+    int parts = R <= 0.7 ? 1 : (R <= 1.5 ? 2 : 4);
+    // every part keeps >= 2 slabs: when x is a slab or two (NPB class A,
+    // 14,000 columns) staging it is cheap and parts only add the combine
+    // (class A: 8.2 -> 10.3 us at P = 2)
+    const std::int64_t nslabs = (cols + kSlabW - 1) / kSlabW;
+    while (parts > 1 && nslabs < 2 * parts) parts /= 2;
+    return parts;
 }
 
 bool tcsr_wanted(std::int64_t rows, const std::int64_t* rp, const std::int64_t* ci, std::int64_t cols,
