@@ -26,7 +26,8 @@ def short(name):
     return re.sub(r"\(.*", "", name).replace("void ", "")
 
 
-def launches(path, out, rnd):
+def launches(path, out, rnd, command="python bench.py --steps 3 --warmup 3 --spmv-reps 10 --no-cpu-baseline "
+                                            "--no-verify --no-e2e"):
     text = open(path).read()
     start = text.index('"ID"')
     rows = list(csv.DictReader(io.StringIO(text[start:])))
@@ -44,8 +45,8 @@ def launches(path, out, rnd):
         agg[k][1] += v
     total = sum(v[1] for v in agg.values())
     lines = [f"# Round {rnd}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)",
-             "", "Command: `python bench.py --steps 3 --warmup 3 --spmv-reps 10 --no-cpu-baseline --no-verify --no-e2e`"
-             " (tools/profile_round.sh). Cold-cache, serialised per-launch times: compare shares, not absolutes.",
+             "", f"Command: `ncu --metrics gpu__time_duration.sum --clock-control none {command}`."
+             " Cold-cache, serialised per-launch times: compare shares, not absolutes.",
              "", f"Launches captured: {sum(v[0] for v in agg.values())}, total device time {total/1e6:.3f} ms", "",
              "| kernel | launches | total ms | mean us | share |", "|---|---:|---:|---:|---:|"]
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -125,11 +126,15 @@ def main():
     ap.add_argument("--rep", default=os.path.join(ROOT, "gpurun_out", "prof_top.ncu-rep"))
     ap.add_argument("--algo-bytes", type=float, default=437052704)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--command", default=None, help="the profiled command, for the launch list's header")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     tag = f"r{a.round:02d}{a.tag}"
     if os.path.exists(a.launches):
-        launches(a.launches, os.path.join(PROF, f"{tag}_launches.md"), a.round)
+        if a.command:
+            launches(a.launches, os.path.join(PROF, f"{tag}_launches.md"), a.round, a.command)
+        else:
+            launches(a.launches, os.path.join(PROF, f"{tag}_launches.md"), a.round)
     if os.path.exists(a.rep):
         top_kernel(a.rep, os.path.join(PROF, f"{tag}_top_kernel.md"), a.round, a.algo_bytes)
 
