@@ -577,6 +577,11 @@ __device__ __forceinline__ double cta_sum_parts(const double* p, int n, double* 
 // barrier. Replaces 3 launches per step; dots are deterministic (fixed
 // per-CTA partition, every CTA sums the partials in CTA order), updates use
 // explicitly rounded mul/add like k_cg_update_zr/k_cg_update_p.
+#ifndef LILAC_CG_PREFETCH
+#define LILAC_CG_PREFETCH 1  // 0 / 1 / 2 / 3 slabs: 494.8 / 498.2 / 493.6 / 484.7 NPB C it/s
+#endif
+constexpr int kCgPrefetch = LILAC_CG_PREFETCH;  // slabs of the next step's runs prefetched during the barriers
+
 __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVectors v, int steps) {
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) std::uint64_t mbar[2];
@@ -595,19 +600,63 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c, it > 0 ? bar : nullptr, target),
                                   red);
         if (tid == 0) pq_part[blockIdx.x] = pq;
+        if (kCgPrefetch > 0 && it + 1 < steps && blockIdx.x < T.ntiles * T.parts) {
+            // HBM is idle until the next step's SpMV (barriers, vector
+            // updates, CTAs waiting for the slowest one): pull the runs of
+            // this CTA's first slabs of the next step into L2 now
+            const int lane = tid & 31, warp = tid >> 5;
+            const std::int64_t t = blockIdx.x / T.parts;
+            const int part = static_cast<int>(blockIdx.x - t * T.parts);
+            const int k0 = part * T.nslabs / T.parts, k1 = (part + 1) * T.nslabs / T.parts;
+            const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
+            const double* vb = T.val + T.tile_base[t];
+            const std::uint16_t* kb = T.key + T.tile_base[t];
+            if (lane == 0)
+                for (int k = k0; k < k1 && k < k0 + kCgPrefetch; ++k)
+                    prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
+        }
+        // One tile per CTA: the tile's z, p, r rows are staged into the (now
+        // idle) slab buffers while this CTA waits at the barrier, and q is
+        // still in the y buffer, so the updates below touch no global loads.
+        const bool cached = T.parts == 1 && T.ntiles <= gridDim.x && blockIdx.x < T.ntiles;
+        std::int64_t crow0 = 0;
+        int cn = 0;
+        if (cached) {
+            crow0 = T.tile_row0[blockIdx.x];
+            cn = static_cast<int>(T.tile_row0[blockIdx.x + 1] - crow0);
+            for (int r = tid; r < cn; r += kTileThreads) {
+                c.xs[r] = __ldcg(v.z + crow0 + r);
+                c.xs[cn + r] = __ldcg(v.p + crow0 + r);
+                c.xs[2 * cn + r] = __ldcg(v.r + crow0 + r);
+            }
+        }
         grid_sync(bar, target);
         const double d = T.parts > 1 ? cta_sum_parts(T.tile_pq, static_cast<int>(T.ntiles), red)
                                      : cta_sum_parts(pq_part, gridDim.x, red);
         const double alpha = rho / d;
         double rr = 0.0;
-        for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
-            const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
-            for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads) {
-                const double zi = __dadd_rn(v.z[i], __dmul_rn(alpha, v.p[i]));
-                const double ri = __dsub_rn(v.r[i], __dmul_rn(alpha, v.q[i]));
-                v.z[i] = zi;
-                v.r[i] = ri;
+        if (cached) {
+            double* zs = c.xs;
+            const double* ps = c.xs + cn;
+            double* rs = c.xs + 2 * cn;
+            for (int r = tid; r < cn; r += kTileThreads) {
+                const double zi = __dadd_rn(zs[r], __dmul_rn(alpha, ps[r]));
+                const double ri = __dsub_rn(rs[r], __dmul_rn(alpha, c.yp[r]));
+                v.z[crow0 + r] = zi;
+                v.r[crow0 + r] = ri;
+                rs[r] = ri;
                 rr += ri * ri;
+            }
+        } else {
+            for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+                const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
+                for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads) {
+                    const double zi = __dadd_rn(v.z[i], __dmul_rn(alpha, v.p[i]));
+                    const double ri = __dsub_rn(v.r[i], __dmul_rn(alpha, v.q[i]));
+                    v.z[i] = zi;
+                    v.r[i] = ri;
+                    rr += ri * ri;
+                }
             }
         }
         rr = cta_sum(rr, red);
@@ -622,10 +671,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         grid_sync(bar, target);
         const double rho_new = cta_sum_parts(rr_part, gridDim.x, red);
         const double beta = rho_new / rho;
-        for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
-            const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
-            for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads)
-                v.p[i] = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
+        if (cached) {
+            const double* ps = c.xs + cn;
+            const double* rs = c.xs + 2 * cn;
+            for (int r = tid; r < cn; r += kTileThreads) v.p[crow0 + r] = __dadd_rn(rs[r], __dmul_rn(beta, ps[r]));
+            // the next step's slab copies (async proxy) overwrite these generic writes
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        } else {
+            for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+                const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
+                for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads)
+                    v.p[i] = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
+            }
         }
         if (tid == 0 && blockIdx.x == 0) {
             v.sc->rho = rho_new;
