@@ -63,6 +63,12 @@ static void check_layout(const char* name, const Csr& a) {
     tcsr_build_host(a.rows, a.rp.data(), a.ci.data(), a.val.data(), a.cols, h);
     CHECK(h.slab_w % 8 == 0 && h.slab_w <= kSlabWMax, "%s: slab width %d", name, h.slab_w);
     CHECK(tcsr_smem_bytes(h.slab_w, h.rows_max) <= static_cast<std::size_t>(kTileSmemBudget), "%s: smem", name);
+    // slab parts: equal-width slabs, a multiple of `parts` of them (parts of equal work)
+    CHECK(h.parts >= 1 && (h.parts == 1 || h.nslabs % h.parts == 0), "%s: %d slabs over %d parts", name, h.nslabs,
+          h.parts);
+    CHECK(static_cast<std::int64_t>(h.nslabs) * h.slab_w >= a.cols &&
+              static_cast<std::int64_t>(h.nslabs - 1) * h.slab_w < a.cols,
+          "%s: slabs cover the columns", name);
     std::vector<double> x(a.cols), y(a.rows, 0.0), ref(a.rows, 0.0), scale(a.rows, 0.0);
     std::mt19937_64 g(7);
     std::uniform_real_distribution<double> u(-1, 1);
@@ -121,8 +127,8 @@ static void check_layout(const char* name, const Csr& a) {
     for (std::int64_t r = 0; r < a.rows; ++r)
         CHECK(std::fabs(y[r] - ref[r]) <= 1e-12 * scale[r] + 1e-300, "%s: row %lld %.17g vs %.17g", name,
               (long long)r, y[r], ref[r]);
-    std::printf("ok %-28s rows=%lld nnz=%lld tiles=%lld slabs=%d slab_w=%d\n", name, (long long)a.rows,
-                (long long)real, (long long)h.ntiles, h.nslabs, h.slab_w);
+    std::printf("ok %-28s rows=%lld nnz=%lld tiles=%lld slabs=%d slab_w=%d parts=%d\n", name, (long long)a.rows,
+                (long long)real, (long long)h.ntiles, h.nslabs, h.slab_w, h.parts);
 }
 
 int main() {
