@@ -285,6 +285,26 @@ def test_stencil_row_block_matrix():
             assert np.all(np.abs(y.cpu().numpy() - ref) <= 1e-12 * bound), (k, g, pol)
 
 
+def test_stencil_row_block_edges():
+    """Empty and whole-range blocks; ranges outside [0, nx^3] are errors."""
+    import torch
+    nx = 9
+    n = nx ** 3
+    M = D.Matrix.stencil27_rows(nx, 5, 5)
+    assert M.info()["rows"] == 0 and M.info()["nnz"] == 0
+    M.free()
+    x = torch.ones(n, dtype=torch.float64, device="cuda")
+    M = D.Matrix.stencil27_rows(nx, 0, n)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    M.spmv(x.data_ptr(), y.data_ptr())
+    torch.cuda.synchronize()
+    assert np.allclose(y.cpu().numpy(), W.stencil27_rowsum(nx, 0, n), rtol=1e-14, atol=1e-12)
+    M.free()
+    for r0, r1 in ((-1, 3), (4, 2), (0, n + 1)):
+        with pytest.raises(N.B200Error):
+            D.Matrix.stencil27_rows(nx, r0, r1)
+
+
 def test_sharded_stencil420_matches_single():
     """The config-5 operator at full size (N=420, 2.0e9 nonzeros) through the
     sharded driver: 4 local shards, each generating its rows in HBM and
