@@ -333,6 +333,19 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         const std::int64_t t = item / P;
         const int part = static_cast<int>(item - t * P);
         const int k0 = part * T.nslabs / P, k1 = (part + 1) * T.nslabs / P;  // this part's slabs
+        // Slab parts (small matrices, a few slabs per CTA) with no gate to
+        // wait for: the first two slab copies start before anything else,
+        // their arrival being the longest leg of the part's start (NPB C 1/8
+        // block: 18.4 -> 16.5 us). With one part per tile (large matrices)
+        // they wait behind the head chunk loads instead, which must lead
+        // (whole NPB C: 72.2 vs 73.2 us issued first).
+        bool issued = false;
+        if (tid == 0 && P > 1 && !gate && k1 > k0 && MODE < 5) {
+            if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
+            issue_slab(T, x, xs, k0, &c.mbar[0]);
+            if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1]);
+            issued = true;
+        }
         const std::int64_t row0 = T.tile_row0[t];
         const int nrows = static_cast<int>(T.tile_row0[t + 1] - row0);
         const std::int64_t base = T.tile_base[t];
@@ -368,7 +381,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             } while (v < gate_target);
             gate = nullptr;
         }
-        if (tid == 0 && k1 > k0 && MODE < 5) {
+        if (tid == 0 && !issued && k1 > k0 && MODE < 5) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
             issue_slab(T, x, xs, k0, &c.mbar[0]);
             if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1]);
@@ -423,9 +436,13 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             // in part order (the same bits whichever part finishes last)
             double* mine = T.ypart + static_cast<std::int64_t>(part) * T.rows + row0;
             for (int r = tid; r < nrows; r += kTileThreads) __stcg(mine + r, yp[r]);
-            __threadfence();
             __syncthreads();
-            if (tid == 0) c.released[2] = atomicAdd(&T.tile_done[t], 1u) == static_cast<unsigned>(P - 1) ? 1u : 0u;
+            // one fence after the barrier publishes the whole CTA's stores
+            // (cumulative) before the ticket, as a per-thread fence would
+            if (tid == 0) {
+                __threadfence();
+                c.released[2] = atomicAdd(&T.tile_done[t], 1u) == static_cast<unsigned>(P - 1) ? 1u : 0u;
+            }
             __syncthreads();
             if (c.released[2]) {  // CTA-uniform
                 __threadfence();
