@@ -508,9 +508,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             s = warp_sum(lane < kTileWarps ? red[lane] : 0.0);
             if (lane == 0) partials[blockIdx.x] = s;
         }
-        __threadfence();
         __syncthreads();
-        if (tid == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (tid == 0) {  // thread 0 wrote the partial: its fence orders it before the ticket
+            __threadfence();
+            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
         __syncthreads();
         if (last) {
             __threadfence();
