@@ -218,6 +218,11 @@ int b200_spmv_device(const b200_matrix* A, const double* x_device, double* y_dev
 int b200_dot_device(const double* a_device, const double* b_device, int64_t n,
                     double* result_device, void* stream);
 int b200_axpy_device(int64_t n, double* y_device, double alpha, const double* x_device, void* stream);
+/* c = a b on device buffers (row-major: a n x p, b p x m, c n x m; the
+ * b200_gemm computation). exact = 1: the reference's k order, bit-identical;
+ * 0: the FP64 tensor-core (DMMA) kernel, within the north-star tolerance. */
+int b200_gemm_device(int64_t n, int64_t m, int64_t p, const double* a_device, const double* b_device,
+                     double* c_device, int exact, void* stream);
 /* The 27-point stencil operator on an nx^3 grid (SURVEY §8(d) input 5),
  * generated directly in HBM: rows in lexicographic (i, j, k) order, each
  * row's neighbours in increasing column order, `diag` on the diagonal and

@@ -79,6 +79,7 @@ SIGNATURES = {
     "b200_matrix_info_get": (C.c_int, [vp, C.POINTER(MatrixInfo)]),
     "b200_spmv_device": (C.c_int, [vp, vp, vp, vp]),
     "b200_dot_device": (C.c_int, [vp, vp, i64, vp, vp]),
+    "b200_gemm_device": (C.c_int, [i64, i64, i64, vp, vp, vp, C.c_int, vp]),
     "b200_axpy_device": (C.c_int, [i64, vp, C.c_double, vp, vp]),
     "b200_matrix_create_stencil27": (C.c_int, [C.POINTER(C.c_void_p), i64, C.c_double, C.c_double]),
     "b200_matrix_create_stencil27_rows": (C.c_int, [C.POINTER(C.c_void_p), i64, i64, i64, C.c_double, C.c_double]),

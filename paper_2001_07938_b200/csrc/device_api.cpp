@@ -305,6 +305,15 @@ int b200_dot_device(const double* a, const double* b, std::int64_t n, double* re
     });
 }
 
+int b200_gemm_device(std::int64_t n, std::int64_t m, std::int64_t p, const double* a, const double* b, double* c,
+                     int exact, void* stream) {
+    return boundary("b200_gemm_device", [&] {
+        ensure_init();
+        if (n < 0 || m < 0 || p < 0) throw Error(Errc::DataError, "negative gemm extent");
+        launch_gemm(n, m, p, a, b, c, exact != 0, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int b200_axpy_device(std::int64_t n, double* y, double alpha, const double* x, void* stream) {
     return boundary("b200_axpy_device", [&] { launch_axpy(n, y, alpha, x, static_cast<cudaStream_t>(stream)); });
 }

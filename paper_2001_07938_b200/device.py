@@ -83,6 +83,12 @@ def dot(a_ptr: int, b_ptr: int, n: int, out_ptr: int, stream: int = 0):
                                     C.c_void_p(stream)))
 
 
+def gemm(n: int, m: int, p: int, a_ptr: int, b_ptr: int, c_ptr: int, exact: bool = False, stream: int = 0):
+    """c = a b on device buffers (row-major n x p times p x m)."""
+    N.check(N.lib().b200_gemm_device(n, m, p, C.c_void_p(a_ptr), C.c_void_p(b_ptr), C.c_void_p(c_ptr),
+                                     1 if exact else 0, C.c_void_p(stream)))
+
+
 class CG:
     """NPB CG solver state over a resident CSR matrix."""
 
