@@ -774,6 +774,28 @@ def test_gemm_fast_and_exact_vs_oracle(n, m, p):
     assert O.same_bits(out2, ref)
 
 
+@pytest.mark.parametrize("n,m,p", [(1, 1, 1), (65, 129, 17), (256, 192, 300)])
+def test_gemm_device_api(n, m, p):
+    """b200_gemm_device on device buffers: the DMMA kernel within tolerance,
+    the exact kernel bit-identical to the oracle."""
+    import torch
+    rng = np.random.default_rng(7 + n + m + p)
+    a = rng.uniform(-2, 2, n * p)
+    b = rng.uniform(-2, 2, p * m)
+    ref = O.gemm(n, m, p, a, b)
+    scale = O.gemm(n, m, p, np.abs(a), np.abs(b))
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    for exact in (False, True):
+        dc = torch.full((n * m,), float("nan"), dtype=torch.float64, device="cuda")
+        D.gemm(n, m, p, da.data_ptr(), db.data_ptr(), dc.data_ptr(), exact=exact)
+        torch.cuda.synchronize()
+        out = dc.cpu().numpy()
+        if exact:
+            assert O.same_bits(out, ref)
+        else:
+            assert (np.abs(out - ref) <= TOL * scale).all()
+
+
 def test_gemm_argument_checks():
     with pytest.raises(ValueError):
         H.gemm(4, 4, np.zeros(15), 4, np.zeros(16), np.zeros(16))
