@@ -637,12 +637,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         // One tile per CTA: the tile's z, p, r rows are staged into the (now
         // idle) slab buffers while this CTA waits at the barrier, and q is
         // still in the y buffer, so the updates below touch no global loads.
-        const bool cached = T.parts == 1 && T.ntiles <= gridDim.x && blockIdx.x < T.ntiles;
-        std::int64_t crow0 = 0;
-        int cn = 0;
+        const bool one_tile = T.parts == 1 && T.ntiles <= gridDim.x && blockIdx.x < T.ntiles;
+        const std::int64_t crow0 = one_tile ? T.tile_row0[blockIdx.x] : 0;
+        const int cn = one_tile ? static_cast<int>(T.tile_row0[blockIdx.x + 1] - crow0) : 0;
+        const bool cached = one_tile && 3 * cn <= 2 * c.stride;  // z, p, r rows fit the slab buffers
         if (cached) {
-            crow0 = T.tile_row0[blockIdx.x];
-            cn = static_cast<int>(T.tile_row0[blockIdx.x + 1] - crow0);
             for (int r = tid; r < cn; r += kTileThreads) {
                 c.xs[r] = __ldcg(v.z + crow0 + r);
                 c.xs[cn + r] = __ldcg(v.p + crow0 + r);
