@@ -29,6 +29,23 @@ namespace b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef LILAC_CTA_TRACE
+#define LILAC_CTA_TRACE 0
+#endif
+constexpr int kMaxTrace = 1024;
+#if LILAC_CTA_TRACE
+__device__ unsigned long long g_cta_trace[5 * kMaxTrace];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_mark(int slot, bool cond = true) {
+    if (cond && threadIdx.x == 0 && blockIdx.x < kMaxTrace) g_cta_trace[5 * blockIdx.x + slot] = gtimer();
+}
+#else
+__device__ __forceinline__ void trace_mark(int, bool = true) {}
+#endif
 #ifndef LILAC_PF_AHEAD
 #define LILAC_PF_AHEAD 1
 #endif
@@ -111,8 +128,8 @@ __device__ __forceinline__ int slab_len(const TcsrDev& T, int k) {
 // arrive (release) on the slab's mbarrier, so every consumer's wait (acquire)
 // sees it together with the bulk bytes. x is never read past cols.
 __device__ __forceinline__ void issue_slab(const TcsrDev& T, const double* __restrict__ x, double* xs, int k,
-                                           std::uint64_t* mbar) {
-    const int len = slab_len(T, k);
+                                           std::uint64_t* mbar, bool tiny = false) {
+    const int len = tiny ? 2 : slab_len(T, k);
     const int even = len & ~1;
     const double* src = x + static_cast<std::int64_t>(k) * T.slab_w;
     if (len & 1) xs[even] = __ldcg(src + even);  // L2: x may have been written earlier in this kernel
@@ -175,7 +192,8 @@ struct Walk {
 // MODE: 0 = the kernel. Timing probes (LILAC_B200_TILED_PROBE, wrong results,
 // never on the CG path; tools/tiled_probes.sh): 1 no x gathers, 2 no row
 // sums, 3 neither (loads only), 5 = 3 without slab copies/waits, 6 = 0
-// without slab copies/waits.
+// without slab copies/waits, 8 / 9 = 3 / 0 with 16-byte slab copies, 10 / 11
+// = 1 / 2 without slab copies/waits.
 //
 // At a row start the partial of the row before it is added into the shared y
 // buffer at once (predicated, no branch). That row is either complete inside
@@ -183,9 +201,15 @@ struct Walk {
 // lanes' share arrives through the segmented scan after the walk, so no row
 // is written by two lanes at the same time (rows are owned by one warp).
 template <int MODE>
-__device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::uint32_t xb_s, std::uint32_t yp_s) {
-    const double x = (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + ((key & 0xfffeu) << 2));
-    if (MODE >= 2) {
+__device__ __forceinline__ double gather_x(unsigned key, std::uint32_t xb_s) {
+    if (MODE == 12)  // probe: bank-conflict-free addresses (lane + 32 * start bit)
+        return lds_f64(xb_s + (((threadIdx.x & 31u) + 32u * (key & 1u)) << 3));
+    return (MODE == 1 || MODE == 3) ? 1.0 : lds_f64(xb_s + ((key & 0xfffeu) << 2));
+}
+
+template <int MODE>
+__device__ __forceinline__ void walk_one(Walk& w, double v, double x, unsigned key, std::uint32_t yp_s) {
+    if (MODE >= 2 && MODE != 12) {
         w.acc = fma(v, x, w.acc);
         return;
     }
@@ -198,10 +222,10 @@ __device__ __forceinline__ void walk_one(Walk& w, double v, unsigned key, std::u
 
 template <int MODE>
 __device__ __forceinline__ void walk_chunk(Walk& w, const Chunk& c, std::uint32_t xb_s, std::uint32_t yp_s) {
-    walk_one<MODE>(w, c.v0.x, c.k.x, xb_s, yp_s);  // low key: walk_one masks to 0xfffe / bit 0
-    walk_one<MODE>(w, c.v0.y, c.k.x >> 16, xb_s, yp_s);
-    walk_one<MODE>(w, c.v1.x, c.k.y, xb_s, yp_s);
-    walk_one<MODE>(w, c.v1.y, c.k.y >> 16, xb_s, yp_s);
+    walk_one<MODE>(w, c.v0.x, gather_x<MODE>(c.k.x, xb_s), c.k.x, yp_s);
+    walk_one<MODE>(w, c.v0.y, gather_x<MODE>(c.k.x >> 16, xb_s), c.k.x >> 16, yp_s);
+    walk_one<MODE>(w, c.v1.x, gather_x<MODE>(c.k.y, xb_s), c.k.y, yp_s);
+    walk_one<MODE>(w, c.v1.y, gather_x<MODE>(c.k.y >> 16, xb_s), c.k.y >> 16, yp_s);
 }
 
 // Combines the lanes' open rows once per run: lane l holds the partial of its
@@ -273,7 +297,7 @@ __device__ __forceinline__ void process_run(const double* vb, const std::uint16_
     // the next run's first chunks stream in during this run's lane reduction
     // and the next slab wait (the matrix does not depend on x)
     load_head_chunks(ring, vb, kb, next_lo, next_hi, lane, pol);
-    if (MODE >= 2) {  // probe: no row sums
+    if (MODE >= 2 && MODE != 12) {  // probe: no row sums
         if (w.acc == 12345.678) sts_add_f64(yp_s, w.acc);
         return;
     }
@@ -340,10 +364,10 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         // they wait behind the head chunk loads instead, which must lead
         // (whole NPB C: 72.2 vs 73.2 us issued first).
         bool issued = false;
-        if (tid == 0 && P > 1 && !gate && k1 > k0 && MODE < 5) {
+        if (tid == 0 && P > 1 && !gate && k1 > k0 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
-            issue_slab(T, x, xs, k0, &c.mbar[0]);
-            if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1]);
+            issue_slab(T, x, xs, k0, &c.mbar[0], MODE == 8 || MODE == 9);
+            if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1], MODE == 8 || MODE == 9);
             issued = true;
         }
         const std::int64_t row0 = T.tile_row0[t];
@@ -362,10 +386,10 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             return k < 32 ? __shfl_sync(kFull, whi, k) : __ldg(wo + k * kTileWarps + warp + 1);
         };
         for (int r = tid; r < nrows; r += kTileThreads) yp[r] = 0.0;
-        for (int k = k0; k < k0 + kPfAhead && k < k1; ++k) {  // runs stream into L2 kPfAhead slabs ahead
-            const int plo = run_lo(k), phi = run_hi(k);
-            if (lane == 0) prefetch_run(vb, kb, plo, phi);
-        }
+        // No L2 prefetch of the first runs here (the loop prefetches from
+        // k0 + 1 on): at a launch every CTA's first runs (33 MB on NPB C)
+        // would queue ahead of the slab copies, which land ~2 us later that
+        // way (CTA trace, tools/cta_trace.py; 72.8 -> 72.0 us, 505 -> 507 it/s).
         // lane descriptors and each run's first chunk are loaded one run ahead (registers)
         unsigned dnext = k1 > k0 ? __ldg(lr + (k0 * kTileWarps + warp) * 32) : 0u;
         Chunk ring[kPipe];
@@ -381,17 +405,17 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             } while (v < gate_target);
             gate = nullptr;
         }
-        if (tid == 0 && !issued && k1 > k0 && MODE < 5) {
+        if (tid == 0 && !issued && k1 > k0 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
-            issue_slab(T, x, xs, k0, &c.mbar[0]);
-            if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1]);
+            issue_slab(T, x, xs, k0, &c.mbar[0], MODE == 8 || MODE == 9);
+            if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1], MODE == 8 || MODE == 9);
         }
         __syncthreads();
         // Free-running slabs: a warp moves on as soon as the next slab has
         // landed; the last warp to release a buffer refills it (no CTA barrier).
         for (int k = k0; k < k1; ++k) {
             const int buf = (k - k0) & 1;
-            if (MODE >= 5) {
+            if (MODE == 5 || MODE == 6 || MODE == 10 || MODE == 11) {
             } else if (buf == 0) {
                 mbar_wait(&c.mbar[0], c.phase0);
                 c.phase0 ^= 1;
@@ -399,6 +423,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                 mbar_wait(&c.mbar[1], c.phase1);
                 c.phase1 ^= 1;
             }
+            if (!DOT && !COHERENT && k == k0) trace_mark(2);
             const unsigned dcur = dnext;
             if (k + 1 < k1) {
                 if (k + kPfAhead < k1) {
@@ -409,7 +434,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             }
             const bool more = k + 1 < k1;
             const int nlo = more ? run_lo(k + 1) : 0, nhi = more ? run_hi(k + 1) : 0;
-            process_run<MODE == 5 ? 3 : (MODE == 6 ? 0 : MODE)>(
+            process_run<MODE == 5 || MODE == 8 ? 3 : (MODE == 6 || MODE == 9 ? 0 : (MODE == 10 || MODE == 11 ? MODE - 9 : MODE))>(
                 vb, kb, run_lo(k), run_hi(k), dcur, ring, nlo, nhi,
                 c.xs_s + 8u * static_cast<unsigned>(buf * c.stride), c.yp_s, lane);
             __syncwarp();
@@ -417,14 +442,15 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                 __threadfence_block();
                 if (atomicAdd(&c.released[buf], 1u) == kTileWarps - 1) {
                     c.released[buf] = 0;
-                    if (k + 2 < k1 && MODE < 5) {
+                    if (k + 2 < k1 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
                         if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");
-                        issue_slab(T, x, xs + buf * c.stride, k + 2, &c.mbar[buf]);
+                        issue_slab(T, x, xs + buf * c.stride, k + 2, &c.mbar[buf], MODE == 8 || MODE == 9);
                     }
                 }
             }
         }
         __syncthreads();  // every row of the tile (this part's slabs) is complete
+        if (!DOT && !COHERENT) trace_mark(3);
         if (P == 1) {
             for (int r = tid; r < nrows; r += kTileThreads) {
                 const double v = yp[r];
@@ -483,6 +509,14 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     __shared__ unsigned released[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     TileCta c;
+#if LILAC_CTA_TRACE
+    if (!DOT && tid == 0 && blockIdx.x < kMaxTrace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_cta_trace[5 * blockIdx.x] = smid;
+    }
+    trace_mark(1, !DOT);
+#endif
     tile_cta_init(c, T, smem, mbar, released);
     if (DOT) {  // CG step: launched programmatically after update_p
         pdl_trigger();
@@ -497,6 +531,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
     __syncthreads();
     const double pq = spmv_tiles<DOT, MODE, false>(T, x, y, dot_off, c);
+    trace_mark(4, !DOT);
 
     if (DOT) {
         __shared__ double red[kTileWarps];
@@ -715,6 +750,17 @@ int g_sms = 0;
 
 }  // namespace
 
+#if LILAC_CTA_TRACE
+// Experiment builds only (tools/cta_trace.py): per CTA of the last standalone
+// tiled SpMV launch: SM id, entry, first slab landed, walk done, exit (ns).
+extern "C" int b200_debug_cta_trace(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_cta_trace, sizeof(unsigned long long) * std::min(n, 5 * kMaxTrace)) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}
+#endif
+
 template <int MODE>
 void launch_variant(const TcsrDev& T, const double* x, double* y, double* partials, unsigned int* ticket,
                     CgScalars* sc, unsigned grid, cudaStream_t s, std::int64_t dot_off) {
@@ -763,6 +809,11 @@ void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, dou
     case 2: launch_variant<2>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     case 5: launch_variant<5>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     case 6: launch_variant<6>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 8: launch_variant<8>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 9: launch_variant<9>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 10: launch_variant<10>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 11: launch_variant<11>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
+    case 12: launch_variant<12>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     default: launch_variant<0>(T, x, y, partials, ticket, sc, grid, s, dot_off); break;
     }
     B200_CUDA(cudaGetLastError());
