@@ -43,8 +43,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void trace_mark(int slot, bool cond = true) {
     if (cond && threadIdx.x == 0 && blockIdx.x < kMaxTrace) g_cta_trace[5 * blockIdx.x + slot] = gtimer();
 }
+// fused CG: [step][CTA][8] = step start, gate passed, first slab landed, walk
+// end, after barrier 1, after barrier 2, p.q summed, z/p/r staged
+constexpr int kCgTraceSteps = 32, kCgTraceCtas = 160;
+__device__ unsigned long long g_cg_trace[kCgTraceSteps * kCgTraceCtas * 8];
+__device__ __forceinline__ void cg_mark(int step, int slot) {
+    if (threadIdx.x == 0 && step < kCgTraceSteps && blockIdx.x < kCgTraceCtas)
+        g_cg_trace[(step * kCgTraceCtas + blockIdx.x) * 8 + slot] = gtimer();
+}
 #else
 __device__ __forceinline__ void trace_mark(int, bool = true) {}
+__device__ __forceinline__ void cg_mark(int, int) {}
 #endif
 #ifndef LILAC_PF_AHEAD
 #define LILAC_PF_AHEAD 1
@@ -314,6 +323,7 @@ struct TileCta {
     unsigned* released;
     std::uint32_t xs_s, yp_s;
     unsigned phase0, phase1;
+    int tstep;  // fused CG step (LILAC_CTA_TRACE builds)
 };
 
 __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, double* smem, std::uint64_t* mbar,
@@ -328,6 +338,7 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, doub
     c.xs_s = opaque_u32(smem_addr(c.xs));
     c.yp_s = opaque_u32(smem_addr(c.yp));
     c.phase0 = c.phase1 = 0;
+    c.tstep = 0;
     if (threadIdx.x == 0) {
         released[0] = released[1] = 0;
         c.xs[T.slab_w] = c.xs[c.stride + T.slab_w] = 0.0;  // padding entries read these
@@ -405,6 +416,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             } while (v < gate_target);
             gate = nullptr;
         }
+        if (COHERENT) cg_mark(c.tstep, 1);
         if (tid == 0 && !issued && k1 > k0 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
             issue_slab(T, x, xs, k0, &c.mbar[0], MODE == 8 || MODE == 9);
@@ -424,6 +436,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                 c.phase1 ^= 1;
             }
             if (!DOT && !COHERENT && k == k0) trace_mark(2);
+            if (COHERENT && k == k0) cg_mark(c.tstep, 2);
             const unsigned dcur = dnext;
             if (k + 1 < k1) {
                 if (k + kPfAhead < k1) {
@@ -451,6 +464,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         }
         __syncthreads();  // every row of the tile (this part's slabs) is complete
         if (!DOT && !COHERENT) trace_mark(3);
+        if (COHERENT) cg_mark(c.tstep, 3);
         if (P == 1) {
             for (int r = tid; r < nrows; r += kTileThreads) {
                 const double v = yp[r];
@@ -651,8 +665,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     double* pq_part = v.partials;
     double* rr_part = v.partials + 2 * kMaxParts;
     for (int it = 0; it < steps; ++it) {
+        c.tstep = it;
+        cg_mark(it, 0);
         const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c, it > 0 ? bar : nullptr, target),
                                   red);
+        cg_mark(it, 6);
         if (tid == 0) pq_part[blockIdx.x] = pq;
         if (kCgPrefetch > 0 && it + 1 < steps && blockIdx.x < T.ntiles * T.parts) {
             // HBM is idle until the next step's SpMV (barriers, vector
@@ -683,7 +700,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
                 c.xs[2 * cn + r] = __ldcg(v.r + crow0 + r);
             }
         }
+        cg_mark(it, 7);
         grid_sync(bar, target);
+        cg_mark(it, 4);
         const double d = T.parts > 1 ? cta_sum_parts(T.tile_pq, static_cast<int>(T.ntiles), red)
                                      : cta_sum_parts(pq_part, gridDim.x, red);
         const double alpha = rho / d;
@@ -722,6 +741,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
             }
         }
         grid_sync(bar, target);
+        cg_mark(it, 5);
         const double rho_new = cta_sum_parts(rr_part, gridDim.x, red);
         const double beta = rho_new / rho;
         if (cached) {
@@ -753,6 +773,13 @@ int g_sms = 0;
 #if LILAC_CTA_TRACE
 // Experiment builds only (tools/cta_trace.py): per CTA of the last standalone
 // tiled SpMV launch: SM id, entry, first slab landed, walk done, exit (ns).
+extern "C" int b200_debug_cg_trace(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_cg_trace,
+                                sizeof(unsigned long long) * std::min(n, kCgTraceSteps * kCgTraceCtas * 8)) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}
 extern "C" int b200_debug_cta_trace(unsigned long long* out, int n) {
     return cudaMemcpyFromSymbol(out, g_cta_trace, sizeof(unsigned long long) * std::min(n, 5 * kMaxTrace)) ==
                    cudaSuccess
