@@ -276,6 +276,27 @@ struct CsrDev {
     const LrcDev* lrc = nullptr;            // present when the lane-range layout was built
 };
 
+// Segmented JDS (k_jds_seg): a jagged row of L nonzeros is served by
+// G = ceil(L / kJdsSegD) consecutive lanes of one warp, lane s holding
+// diagonals [s * kJdsSegD, (s + 1) * kJdsSegD); the row's sum is carried lane
+// to lane in k order (bit-identical to the reference). Rows are length-sorted
+// in JDS, so rows of equal G form contiguous zones; zone z packs 32 / G rows
+// per warp. nzones == 0: the layout does not qualify (nzcnt not
+// non-increasing, or a row longer than 32 * kJdsSegD) and k_jds serves it.
+#ifndef LILAC_JDS_SEG_D
+#define LILAC_JDS_SEG_D 10
+#endif
+constexpr int kJdsSegD = LILAC_JDS_SEG_D;
+constexpr int kJdsMaxZones = 32;
+struct JdsSeg {
+    int nzones = 0;
+    int g[kJdsMaxZones] = {};                  // lanes per row in zone z
+    std::int64_t row0[kJdsMaxZones + 1] = {};  // zone z = jagged rows [row0[z], row0[z + 1])
+    std::int64_t warp0[kJdsMaxZones + 1] = {};  // first warp of zone z; warp0[nzones] = warps in all
+};
+// Host: the zone table of a JDS nzcnt (rows entries, jagged order).
+JdsSeg jds_segments(const std::int64_t* nzcnt, std::int64_t rows);
+
 struct JdsDev {
     std::int64_t rows = 0;
     std::int64_t nnz = 0;
@@ -288,6 +309,7 @@ struct JdsDev {
     const void* col = nullptr;
     bool col32 = true;
     const double* val = nullptr;
+    JdsSeg seg;  // k_jds_seg zones (nzones 0: k_jds)
 };
 
 // ---------------------------------------------------------------------------

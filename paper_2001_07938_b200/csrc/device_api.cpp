@@ -146,6 +146,7 @@ int b200_matrix_create_jds(b200_matrix** out, std::int64_t rows, const std::int6
         d.col = A->col.ptr;
         d.col32 = col32;
         d.val = A->val.as<double>();
+        d.seg = jds_segments(nzcnt, rows);
         A->max_row = max_nz;
         *out = A.release();
     });

@@ -236,6 +236,7 @@ struct spmv_jds_state {
     MarshalObject<DevArray> m_val;
     MarshalObject<DevArray> m_x;
     MarshalObject<DevArray> m_output;
+    JdsSeg seg;  // k_jds_seg zones of the marshaled nzcnt
     bool validated = false;
     bool first_run_done = false;
 };
@@ -520,6 +521,8 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         DevArray& dnz = state.m_nzcnt.acquire(nzcnt, rows * sizeof(*nzcnt), nullptr,
                                               [&](const void* in, std::size_t size, DevArray& out) {
                                                   upload(out, in, size);
+                                                  state.seg = jds_segments(static_cast<const std::int64_t*>(in),
+                                                                           rows);
                                                   state.validated = false;
                                               },
                                               B200Read_destruct);
@@ -561,6 +564,7 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         A.col = ci.buf.ptr;
         A.col32 = ci.col32;
         A.val = dval.data<double>();
+        A.seg = state.seg;
         timed_launch(hs, [&] { launch_spmv_jds(A, dx.data<double>(), dout.buf.as<double>(), rt().stream); });
         tm.acquired();
 

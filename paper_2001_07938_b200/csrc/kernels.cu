@@ -439,6 +439,9 @@ __global__ void __launch_bounds__(kThreads) k_csr_exact(std::int64_t rows,
 }
 
 // JDS, thread per jagged row j (coalesced over j); y scattered through inv_perm.
+#if LILAC_CTA_TRACE
+__device__ unsigned long long g_jds_trace[3 * 4096];  // per block: SM, entry, exit (tools/jds_trace.py)
+#endif
 template <typename IdxT>
 __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::int64_t* __restrict__ nzcnt,
                                                   const std::int64_t* __restrict__ inv_perm,
@@ -446,6 +449,10 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
                                                   const IdxT* __restrict__ col,
                                                   const double* __restrict__ val,
                                                   const double* __restrict__ x, double* __restrict__ y) {
+#if LILAC_CTA_TRACE
+    unsigned long long t_in;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_in));
+#endif
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * kThreads;
     for (std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x; j < rows; j += stride) {
         const std::int64_t len = __ldg(nzcnt + j);
@@ -490,6 +497,90 @@ __global__ void __launch_bounds__(kThreads) k_jds(std::int64_t rows, const std::
         }
         y[__ldg(inv_perm + j)] = acc;
     }
+#if LILAC_CTA_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned long long t_out;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_out));
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_jds_trace[3 * blockIdx.x] = smid;
+        g_jds_trace[3 * blockIdx.x + 1] = t_in;
+        g_jds_trace[3 * blockIdx.x + 2] = t_out;
+    }
+#endif
+}
+
+// Segmented JDS (JdsSeg in b200.hpp): every lane loads the val/col of its
+// (at most kJdsSegD) diagonals and gathers x at once, so a row's memory chain
+// is two trips whatever its length; the products are then summed in k order,
+// the running sum passed from lane to lane of the row's group by shuffles
+// (__dmul_rn / __dadd_rn, as the reference: bit-identical). Small register
+// footprint: the grid is about one wave on the Parboil shape.
+#ifndef LILAC_JDS_SEG_BLOCKS
+#define LILAC_JDS_SEG_BLOCKS 6
+#endif
+template <typename IdxT>
+__global__ void __launch_bounds__(kThreads, LILAC_JDS_SEG_BLOCKS)
+    k_jds_seg(const std::int64_t* __restrict__ nzcnt, const std::int64_t* __restrict__ inv_perm,
+              const std::int64_t* __restrict__ jd_ptr, const IdxT* __restrict__ col, const double* __restrict__ val,
+              const double* __restrict__ x, double* __restrict__ y, const JdsSeg sg) {
+#if LILAC_CTA_TRACE
+    unsigned long long t_in;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_in));
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_jds_trace[3 * blockIdx.x + 1] = t_in;
+#endif
+    const std::int64_t gw = (static_cast<std::int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= sg.warp0[sg.nzones]) return;  // warp-uniform
+    int z = 0;
+    while (z + 1 < sg.nzones && gw >= sg.warp0[z + 1]) ++z;
+    const int G = sg.g[z], rpw = 32 / G;
+    const int r = lane / G, seg = lane - r * G;
+    const std::int64_t j = sg.row0[z] + (gw - sg.warp0[z]) * rpw + r;
+    const bool active = r < rpw && j < sg.row0[z + 1];
+    const std::int64_t len = active ? __ldg(nzcnt + j) : 0;
+    const std::int64_t k0 = static_cast<std::int64_t>(seg) * kJdsSegD;
+    const int cnt = static_cast<int>(len - k0 < 0 ? 0 : (len - k0 > kJdsSegD ? kJdsSegD : len - k0));
+    double v[kJdsSegD];
+    long long c[kJdsSegD];
+#pragma unroll
+    for (int u = 0; u < kJdsSegD; ++u) {
+        v[u] = 0.0;
+        c[u] = 0;
+        if (u < cnt) {
+            const std::int64_t off = __ldg(jd_ptr + k0 + u) + j;
+            asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(val + off));
+            c[u] = static_cast<long long>(__ldg(col + off));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kJdsSegD; ++u)
+        if (u < cnt) v[u] = __dmul_rn(v[u], __ldg(x + c[u]));
+    // the row's running sum, segment by segment in k order
+    double acc = 0.0;
+    const int base = r * G;
+    for (int s = 0; s < G; ++s) {
+        if (seg == s) {
+#pragma unroll
+            for (int u = 0; u < kJdsSegD; ++u)
+                if (u < cnt) acc = __dadd_rn(acc, v[u]);
+        }
+        const int src = base + s;
+        acc = __shfl_sync(0xffffffffu, acc, src < 32 ? src : lane);
+    }
+    if (active && seg == 0) y[__ldg(inv_perm + j)] = acc;
+#if LILAC_CTA_TRACE
+    __syncwarp();
+    if (lane == 0 && blockIdx.x < 4096) {  // the block's last warp to finish wins
+        unsigned long long t_out;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_out));
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_jds_trace[3 * blockIdx.x] = smid;
+        atomicMax(&g_jds_trace[3 * blockIdx.x + 2], t_out);
+    }
+#endif
 }
 
 // JDS when perm is not a bijection: thread per original row (uncoalesced,
@@ -868,8 +959,59 @@ void launch_spmv_csr_dot(const CsrDev& A, const double* p, double* q, double* pa
     B200_CUDA(cudaGetLastError());
 }
 
+JdsSeg jds_segments(const std::int64_t* nz, std::int64_t rows) {
+    JdsSeg sg;
+    if (rows <= 0) return sg;
+    for (std::int64_t j = 1; j < rows; ++j)
+        if (nz[j] > nz[j - 1]) return sg;  // not length-sorted
+    if (nz[0] > static_cast<std::int64_t>(32) * kJdsSegD || nz[rows - 1] < 0) return sg;
+    auto groups = [](std::int64_t L) { return L <= kJdsSegD ? 1 : static_cast<int>((L + kJdsSegD - 1) / kJdsSegD); };
+    std::int64_t j = 0, w = 0;
+    int z = 0;
+    while (j < rows) {
+        const int G = groups(nz[j]);
+        // first row of a smaller group count: nz[row] <= kJdsSegD * (G - 1)
+        std::int64_t lo = j, hi = rows;
+        const std::int64_t lim = static_cast<std::int64_t>(kJdsSegD) * (G - 1);
+        while (lo < hi) {
+            const std::int64_t mid = lo + (hi - lo) / 2;
+            if (G > 1 && nz[mid] <= lim) hi = mid; else lo = mid + 1;
+        }
+        const std::int64_t end = G > 1 ? lo : rows;
+        const int rpw = 32 / G;
+        sg.g[z] = G;
+        sg.row0[z] = j;
+        sg.warp0[z] = w;
+        w += (end - j + rpw - 1) / rpw;
+        ++z;
+        j = end;
+    }
+    sg.row0[z] = rows;
+    sg.warp0[z] = w;
+    sg.nzones = z;
+    return sg;
+}
+
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
     if (A.rows <= 0) return;
+    static const bool seg_off = [] {
+        const char* e = std::getenv("LILAC_B200_JDS");
+        return e && std::strcmp(e, "rowthread") == 0;  // experiments: the thread-per-row kernel
+    }();
+    if (A.inv_perm && A.seg.nzones > 0 && !seg_off) {
+        const std::int64_t threads = A.seg.warp0[A.seg.nzones] * 32;
+        const unsigned gs = static_cast<unsigned>((threads + kThreads - 1) / kThreads);
+        if (A.col32)
+            k_jds_seg<std::int32_t><<<gs, kThreads, 0, s>>>(A.nzcnt, A.inv_perm, A.jd_ptr,
+                                                            static_cast<const std::int32_t*>(A.col), A.val, x, y,
+                                                            A.seg);
+        else
+            k_jds_seg<std::int64_t><<<gs, kThreads, 0, s>>>(A.nzcnt, A.inv_perm, A.jd_ptr,
+                                                            static_cast<const std::int64_t*>(A.col), A.val, x, y,
+                                                            A.seg);
+        B200_CUDA(cudaGetLastError());
+        return;
+    }
     const unsigned g = grid_for(A.rows);
     if (A.inv_perm) {
         if (A.col32)
@@ -954,5 +1096,13 @@ void launch_xpay_to(std::int64_t n, double* out, const double* y, double beta, c
     k_vec2<true><<<grid_for(n, kSMs * 8), kThreads, 0, s>>>(n, out, y, beta, x);
     B200_CUDA(cudaGetLastError());
 }
+
+#if LILAC_CTA_TRACE
+extern "C" int b200_debug_jds_trace(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_jds_trace, sizeof(unsigned long long) * std::min(n, 3 * 4096)) == cudaSuccess
+               ? 0
+               : 1;
+}
+#endif
 
 }  // namespace b200

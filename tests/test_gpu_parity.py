@@ -799,3 +799,45 @@ def test_gemm_device_api(n, m, p):
 def test_gemm_argument_checks():
     with pytest.raises(ValueError):
         H.gemm(4, 4, np.zeros(15), 4, np.zeros(16), np.zeros(16))
+
+
+# --------------------------------------------------------------------------------
+# segmented JDS (k_jds_seg: a row's diagonals spread over up to 32 lanes, the
+# running sum carried lane to lane) and its fallbacks
+# --------------------------------------------------------------------------------
+
+def _jds_case(lens, seed):
+    rng = np.random.default_rng(seed)
+    rows = len(lens)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = rng.integers(0, rows, int(rp[-1])).astype(np.int64)
+    val = rng.uniform(-2, 2, int(rp[-1]))
+    x = rng.uniform(-2, 2, rows)
+    return (*O.jds_from_csr(rp, ci, val), x)
+
+
+def _run_jds(perm, nzcnt, jd_ptr, jval, jcol, x):
+    y = np.full(len(perm), np.nan)
+    H.spmv_jds(len(perm), y, nzcnt, perm, jval, jd_ptr, x, jcol)
+    return y
+
+
+@pytest.mark.parametrize("max_len", [1, 10, 11, 64, 320, 321, 700])
+def test_jds_every_lane_group_bitwise(max_len):
+    # every row length 0..max_len (each lanes-per-row zone and its edges);
+    # rows longer than 32 lanes' worth take the thread-per-row kernel
+    lens = np.concatenate([np.arange(max_len + 1), np.random.default_rng(max_len).integers(0, max_len + 1, 3000)])
+    perm, nzcnt, jd_ptr, jval, jcol, x = _jds_case(lens, 7 + max_len)
+    y = _run_jds(perm, nzcnt, jd_ptr, jval, jcol, x)
+    assert O.same_bits(y, O.spmv_jds(nzcnt, perm, jval, jd_ptr, x, jcol))
+
+
+def test_jds_unsorted_nzcnt_bitwise():
+    # a valid JDS whose nzcnt is not non-increasing (row 0 shortened): the
+    # lane groups do not apply; the reference semantics still hold
+    perm, nzcnt, jd_ptr, jval, jcol, x = _jds_case(np.random.default_rng(3).integers(0, 40, 5000), 11)
+    nzcnt = nzcnt.copy()
+    nzcnt[0] = 1
+    nzcnt[7] = 0
+    y = _run_jds(perm, nzcnt, jd_ptr, jval, jcol, x)
+    assert O.same_bits(y, O.spmv_jds(nzcnt, perm, jval, jd_ptr, x, jcol))
