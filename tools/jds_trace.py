@@ -29,6 +29,9 @@ s = torch.cuda.current_stream().cuda_stream
 for _ in range(20):
     A.spmv(x.data_ptr(), y.data_ptr(), s)
 torch.cuda.synchronize()
+if not hasattr(L, "b200_debug_jds_trace"):  # a product build: the launches above are the workload (ncu)
+    print("no trace in this build (-DLILAC_CTA_TRACE=1)")
+    sys.exit(0)
 buf = (C.c_ulonglong * (3 * 4096))()
 assert L.b200_debug_jds_trace(buf, 3 * 4096) == 0
 a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 3).astype(np.int64)
