@@ -965,7 +965,9 @@ def run_parboil(ctx):
     line["spmv"] = {"gflops_cold": value, "gbs_cold": by / (ms_step * 1e-3) / 1e9, "ms_cold": ms_step,
                     "ms_l2_warm": warm_ms, "gflops_l2_warm": 2 * nnz / (warm_ms * 1e-3) / 1e9,
                     "bytes_per_call": by}
-    line["roofline"] = roofline(by, ms_step, "k_jds", "JDS algorithmic bytes nnz*(8+s_i)+16 rows+8(max_nz+1)+8 rows+"
+    jk = "k_jds_seg" if A.info()["kernel"] == 1 else "k_jds"
+    line["spmv"]["kernel"] = jk
+    line["roofline"] = roofline(by, ms_step, jk, "JDS algorithmic bytes nnz*(8+s_i)+16 rows+8(max_nz+1)+8 rows+"
                                 "8 cols per launch / mean cold-L2 launch time (CUDA events per step)", "parboil")
     line["gpu_launches"] = args.steps
     line["clocks"] = clk

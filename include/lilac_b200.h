@@ -198,8 +198,9 @@ typedef struct {
     int64_t rows, cols, nnz, max_row;
     int32_t format;        /* 0 CSR, 1 JDS */
     int32_t col_bytes;     /* column index width the kernel streams: 8, 4 (narrowed) or 2 (tiled keys) */
-    int32_t kernel;        /* CSR kernel chosen: 1 vector, 2 merge, 3 exact, 4 tiled, 5 split */
-    int32_t lanes;         /* vector kernel lanes per row */
+    int32_t kernel;        /* CSR kernel chosen: 1 vector, 2 merge, 3 exact, 4 tiled, 5 split, 6 lane-range;
+                              JDS: 0 thread per jagged row, 1 lane-segmented (k_jds_seg) */
+    int32_t lanes;         /* CSR vector kernel lanes per row; JDS segmented: most lanes per row */
     int64_t device_bytes;  /* resident bytes */
 } b200_matrix_info;
 

@@ -339,6 +339,7 @@ void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, dou
 void launch_spmv_tiled(const TcsrDev& T, std::int64_t rows, const double* x, double* y, double* partials,
                        unsigned int* ticket, struct CgScalars* sc, cudaStream_t s, std::int64_t dot_off = 0);
 void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s);
+bool jds_segmented(const JdsDev& A);  // launch_spmv_jds takes k_jds_seg
 
 struct CgScalars;
 // Fused CG kernel: q = A p and d = p.q in one pass; the last CTA sets

@@ -194,8 +194,8 @@ int b200_matrix_info_get(const b200_matrix* A, b200_matrix_info* info) {
             info->cols = A->jds.cols;
             info->nnz = A->jds.nnz;
             info->col_bytes = A->jds.col32 ? 4 : 8;
-            info->kernel = 0;
-            info->lanes = 1;
+            info->kernel = jds_segmented(A->jds) ? 1 : 0;
+            info->lanes = info->kernel == 1 ? A->jds.seg.g[0] : 1;
         }
         info->device_bytes = static_cast<std::int64_t>(A->row_ptr.bytes + A->col.bytes + A->val.bytes + A->nzcnt.bytes +
                                                        A->perm.bytes + A->inv_perm.bytes + A->jd_ptr.bytes) +

@@ -996,13 +996,17 @@ JdsSeg jds_segments(const std::int64_t* nz, std::int64_t rows) {
     return sg;
 }
 
-void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
-    if (A.rows <= 0) return;
+bool jds_segmented(const JdsDev& A) {
     static const bool seg_off = [] {
         const char* e = std::getenv("LILAC_B200_JDS");
         return e && std::strcmp(e, "rowthread") == 0;  // experiments: the thread-per-row kernel
     }();
-    if (A.inv_perm && A.seg.nzones > 0 && !seg_off) {
+    return A.inv_perm && A.seg.nzones > 0 && !seg_off;
+}
+
+void launch_spmv_jds(const JdsDev& A, const double* x, double* y, cudaStream_t s) {
+    if (A.rows <= 0) return;
+    if (jds_segmented(A)) {
         const std::int64_t threads = A.seg.warp0[A.seg.nzones] * 32;
         const unsigned gs = static_cast<unsigned>((threads + kThreads - 1) / kThreads);
         if (A.col32)
