@@ -1,0 +1,190 @@
+// copy_engine.cpp — device-to-host copies into pageable caller memory.
+//
+// The reference semantics write every output back after each call
+// (marshal.hpp write_back). A LiLAC-rewritten program's arrays are plain
+// malloc'd memory, and a D2H into pageable memory runs at ~11 GB/s here
+// (the driver stages it through its own pinned buffer with one host copy;
+// tools/bus_probe.py: 1.2 MB pageable 11.4 GB/s, pinned 35 GB/s; host memcpy
+// 13 GB/s on one thread, 35 GB/s on four). Here the D2H lands in a pinned
+// double buffer chunk by chunk, and each landed chunk is copied out by the
+// calling thread plus a few worker threads while the next chunk's DMA runs.
+//
+// Workers spin up to 1 ms between jobs (a host CG loop downloads every ~165 us)
+// and park on a condition variable when idle. They only run memcpy, never
+// CUDA. Set LILAC_B200_STAGED_D2H=0 to use the plain cudaMemcpy.
+
+#include "runtime.hpp"
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include <immintrin.h>
+
+namespace b200 {
+
+namespace {
+
+constexpr std::size_t kStagedMin = std::size_t(256) << 10;
+
+std::size_t env_size(const char* name, std::size_t dflt) {
+    const char* e = std::getenv(name);
+    return (e && std::atol(e) > 0) ? static_cast<std::size_t>(std::atol(e)) : dflt;
+}
+// tuning knobs (experiments): chunk KB, copy granule KB, workers, idle spin us
+const std::size_t kStage = env_size("LILAC_B200_D2H_STAGE_KB", 512) << 10;  // bytes per pinned chunk (two)
+const std::size_t kPart = env_size("LILAC_B200_D2H_PART_KB", 64) << 10;     // host-copy granule per grab
+const int kWorkers = static_cast<int>(env_size("LILAC_B200_D2H_WORKERS", 3));
+const int kSpinUs = static_cast<int>(env_size("LILAC_B200_D2H_SPIN_US", 1000));
+
+// A fixed set of memcpy workers sharing one job at a time: the job is split
+// into kPart pieces; a piece is claimed by a CAS on `next_` = job << 32 |
+// piece, so a worker still leaving the previous job can never claim (or
+// lose) a piece of the next one. The poster copies too and waits for all.
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool;  // never destroyed: workers outlive static teardown
+        return *p;
+    }
+
+    void copy(char* dst, const char* src, std::size_t n) {
+        const std::uint32_t parts = static_cast<std::uint32_t>((n + kPart - 1) / kPart);
+        if (workers_ == 0 || parts <= 1) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        dst_ = dst;
+        src_ = src;
+        len_ = n;
+        parts_ = parts;
+        done_.store(0, std::memory_order_relaxed);
+        const std::uint64_t job = ++job_;
+        next_.store(job << 32, std::memory_order_release);  // publishes the fields above
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            posted_.store(job, std::memory_order_release);
+        }
+        cv_.notify_all();
+        run_parts(job);
+        while (done_.load(std::memory_order_acquire) < parts) _mm_pause();
+    }
+
+private:
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        workers_ = hw >= 8 ? kWorkers : (hw >= 4 ? 1 : 0);
+        for (int i = 0; i < workers_; ++i) std::thread([this] { loop(); }).detach();
+    }
+
+    void run_parts(std::uint64_t job) {
+        std::uint64_t x = next_.load(std::memory_order_acquire);
+        for (;;) {
+            if ((x >> 32) != job || static_cast<std::uint32_t>(x) >= parts_) return;
+            if (!next_.compare_exchange_weak(x, x + 1, std::memory_order_acq_rel, std::memory_order_acquire)) continue;
+            const std::size_t off = static_cast<std::size_t>(static_cast<std::uint32_t>(x)) * kPart;
+            std::memcpy(dst_ + off, src_ + off, std::min(kPart, len_ - off));
+            done_.fetch_add(1, std::memory_order_release);
+            x = next_.load(std::memory_order_acquire);
+        }
+    }
+
+    void loop() {
+        std::uint64_t seen = 0;
+        for (;;) {
+            // spin a while (kSpinUs) for the next job, then park
+            const auto t0 = std::chrono::steady_clock::now();
+            int k = 0;
+            while (posted_.load(std::memory_order_acquire) == seen) {
+                _mm_pause();
+                if ((++k & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(kSpinUs)) {
+                    std::unique_lock<std::mutex> lk(m_);
+                    cv_.wait(lk, [&] { return posted_.load(std::memory_order_acquire) != seen; });
+                    break;
+                }
+            }
+            seen = posted_.load(std::memory_order_acquire);
+            run_parts(seen);
+        }
+    }
+
+    int workers_ = 0;
+    std::uint64_t job_ = 0;  // poster only
+    std::atomic<std::uint64_t> posted_{0};
+    std::atomic<std::uint64_t> next_{0};
+    std::atomic<std::uint32_t> done_{0};
+    std::uint32_t parts_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    std::size_t len_ = 0;
+    std::mutex m_;
+    std::condition_variable cv_;
+};
+
+bool staged_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LILAC_B200_STAGED_D2H");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
+struct Staging {
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int device = -1;
+};
+
+}  // namespace
+
+void d2h_copy(void* host, const void* dev, std::size_t bytes, cudaStream_t s) {
+    bool staged = staged_enabled() && bytes >= kStagedMin;
+    if (staged) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+            (void)cudaGetLastError();
+            a.type = cudaMemoryTypeUnregistered;
+        }
+        staged = a.type == cudaMemoryTypeUnregistered;  // pinned / managed memory: direct DMA is faster
+    }
+    if (!staged) {
+        B200_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s));
+        B200_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    static Staging st;  // calls are serialised per process (the harness runtime is single-threaded)
+    int devno = 0;
+    B200_CUDA(cudaGetDevice(&devno));
+    if (st.device != devno) {  // first use (or another device): pinned chunks and events of this context
+        for (int i = 0; i < 2; ++i) {
+            if (!st.buf[i]) B200_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&st.buf[i]), kStage, cudaHostAllocPortable));
+            if (st.ev[i]) (void)cudaEventDestroy(st.ev[i]);
+            B200_CUDA(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming));
+        }
+        st.device = devno;
+    }
+    CopyPool& pool = CopyPool::get();
+    const char* d = static_cast<const char*>(dev);
+    char* h = static_cast<char*>(host);
+    const std::size_t chunks = (bytes + kStage - 1) / kStage;
+    auto issue = [&](std::size_t c) {
+        const std::size_t off = c * kStage, n = std::min(kStage, bytes - off);
+        B200_CUDA(cudaMemcpyAsync(st.buf[c & 1], d + off, n, cudaMemcpyDeviceToHost, s));
+        B200_CUDA(cudaEventRecord(st.ev[c & 1], s));
+    };
+    issue(0);
+    for (std::size_t c = 0; c < chunks; ++c) {
+        // chunk c + 1 lands in the other buffer, whose chunk (c - 1) was copied out
+        if (c + 1 < chunks) issue(c + 1);
+        B200_CUDA(cudaEventSynchronize(st.ev[c & 1]));
+        const std::size_t off = c * kStage, n = std::min(kStage, bytes - off);
+        pool.copy(h + off, st.buf[c & 1], n);
+    }
+}
+
+}  // namespace b200

@@ -429,8 +429,7 @@ void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter) {
     {
         PhaseTimer pt(kPhD2H);
         lilac::marshal::supersede_range(host, bytes);  // lazy bytes under the destination
-        B200_CUDA(cudaMemcpyAsync(host, d.buf.ptr, bytes, cudaMemcpyDeviceToHost, rt().stream));
-        B200_CUDA(cudaStreamSynchronize(rt().stream));
+        d2h_copy(host, d.buf.ptr, bytes, rt().stream);
     }
     PhaseTimer pt(kPhPublish);
     // publish only after the bytes landed (pinned D2H is asynchronous: the

@@ -156,6 +156,10 @@ void upload(DevArray& d, const void* host, std::size_t bytes);
 // page the region touches PROT_NONE, and its bytes land on the first touch of
 // any of those pages (a neighbour on an unaligned region's edge page included).
 void download(void* host, DevArray& d, std::size_t bytes, DevArray& counter);
+// D2H of `bytes` into host memory on stream s, returning once the bytes landed;
+// pageable destinations go through pinned chunks with parallel host copies
+// (copy_engine.cpp).
+void d2h_copy(void* host, const void* dev, std::size_t bytes, cudaStream_t s);
 
 // Device mirrors (the coherence layer of SURVEY §8(f)1): after a write-back the
 // device holds the exact bytes of the host region; the region is guarded like
