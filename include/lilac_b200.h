@@ -390,6 +390,14 @@ int b200_dist_cg_p2p_export(b200_dist_cg* d, void* out208);
 int b200_dist_cg_p2p_attach(b200_dist_cg* d, const void* handles);
 /* 0 local device copies, 1 NCCL, 2 peer memory. */
 int b200_dist_cg_transport(const b200_dist_cg* d);
+/* With the peer-memory exchange and the tiled layout on every shard, the CG
+ * steps of an outer iteration run in one persistent kernel per process
+ * (k_cg_tiled_dist: SpMV, partial publish, flag waits and the p push inside
+ * it; local shards share one cooperative grid). on = 0 keeps the per-step
+ * kernels (default on; LILAC_B200_DIST_FUSED=0 turns it off process-wide).
+ * b200_dist_cg_fused: 1 if the last outer iteration ran the fused kernel. */
+int b200_dist_cg_set_fused(b200_dist_cg* d, int on);
+int b200_dist_cg_fused(const b200_dist_cg* d);
 int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double* rnorm);
 int b200_dist_cg_info(const b200_dist_cg* d, int shard, int64_t* row0, int64_t* rows, int64_t* nnz,
                       int32_t* tiled);

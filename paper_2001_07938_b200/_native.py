@@ -130,6 +130,8 @@ SIGNATURES = {
     "b200_dist_cg_p2p_export": (C.c_int, [vp, vp]),
     "b200_dist_cg_p2p_attach": (C.c_int, [vp, vp]),
     "b200_dist_cg_transport": (C.c_int, [vp]),
+    "b200_dist_cg_set_fused": (C.c_int, [vp, C.c_int]),
+    "b200_dist_cg_fused": (C.c_int, [vp]),
     "b200_dist_npb": (C.c_int, [vp, C.c_int, C.c_double, f64p, f64p]),
     "b200_dist_cg_info": (C.c_int, [vp, C.c_int, i64p, i64p, i64p, C.POINTER(C.c_int32)]),
 }

@@ -422,6 +422,14 @@ void cg_launch_iteration(const CsrDev& A, const CgVectors& v, cudaStream_t s);
 void cg_launch_iterations(const CsrDev& A, const CgVectors& v, int steps, cudaStream_t s);
 // Fused single-GPU CG steps over the tiled layout; false if not available.
 bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream_t s);
+// Sharded fused CG steps over the tiled layout (tcsr.cu k_cg_tiled_dist): a
+// device array of `nslots` slots (dist_slot_fill), each a shard with its
+// peer-memory exchange bound (CgScalars::p2p); false if not available.
+bool launch_cg_tiled_dist(const void* slots_dev, int nslots, std::size_t smem, unsigned* bars, int steps,
+                          cudaStream_t s);
+std::size_t dist_slot_bytes();
+void dist_slot_fill(void* out, const TcsrDev& T, const CgVectors& v, unsigned* bar);
+std::size_t tiled_smem_bytes(const TcsrDev& T);
 void cg_launch_residual(const CsrDev& A, const CgVectors& v, cudaStream_t s);  // r=A z, rnorm
 void cg_launch_outer_update(const CgVectors& v, double shift, cudaStream_t s);  // zeta, x = z/|z|
 void cg_launch_reset_x(const CgVectors& v, cudaStream_t s);

@@ -73,6 +73,13 @@ struct b200_dist_cg {
     cudaStream_t graph_stream = nullptr;
     int graph_cgitmax = -1;
     double graph_shift = 0.0;
+    // the CG steps of every local shard in one persistent kernel
+    // (k_cg_tiled_dist) once the peer-memory exchange is bound
+    DevBuf fused_slots, fused_bars;
+    std::size_t fused_smem = 0;
+    bool fused_ready = false;
+    bool fused_on = true;    // b200_dist_cg_set_fused
+    bool fused_last = false;  // the last outer iteration ran k_cg_tiled_dist
 };
 
 namespace {
@@ -298,9 +305,44 @@ void dist_finish(b200_dist_cg* d, cudaStream_t st) {
     gather_scalars(d, st, 1, CgFin::Rnorm, 0.0);
 }
 
+// The fused sharded CG (k_cg_tiled_dist) needs the peer-memory exchange
+// bound to every shard's producers and the tiled layout on every shard. Its
+// slot table is uploaded here, outside any graph capture.
+// LILAC_B200_DIST_FUSED=0 keeps the six kernels per step.
+void prepare_fused(b200_dist_cg* d) {
+    static const bool on = [] {
+        const char* e = std::getenv("LILAC_B200_DIST_FUSED");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (d->fused_ready || !on || !d->fused_on || d->transport != 2) return;
+    for (auto& s : d->shards)
+        if (!s->A.tiled) return;
+    const std::size_t sb = dist_slot_bytes(), k = d->shards.size();
+    d->fused_bars.ensure(sizeof(unsigned) * k);
+    std::vector<char> host(sb * k);
+    std::size_t smem = 0;
+    for (std::size_t i = 0; i < k; ++i) {
+        const Shard& sh = *d->shards[i];
+        dist_slot_fill(host.data() + i * sb, *sh.A.tiled, sh.v, d->fused_bars.as<unsigned>() + i);
+        smem = std::max(smem, tiled_smem_bytes(*sh.A.tiled));
+    }
+    d->fused_slots.ensure(host.size());
+    B200_CUDA(cudaMemcpy(d->fused_slots.ptr, host.data(), host.size(), cudaMemcpyHostToDevice));
+    d->fused_smem = smem;
+    d->fused_ready = true;
+}
+
+bool dist_fused_steps(b200_dist_cg* d, int steps, cudaStream_t st) {
+    d->fused_last = d->fused_ready && d->fused_on &&
+                    launch_cg_tiled_dist(d->fused_slots.ptr, static_cast<int>(d->shards.size()), d->fused_smem,
+                                         d->fused_bars.as<unsigned>(), steps, st);
+    return d->fused_last;
+}
+
 void dist_outer(b200_dist_cg* d, int cgitmax, double shift, cudaStream_t st) {
     dist_init(d, st);  // q=z=0, r=p=x (owned slices), rho; p exchanged
-    for (int it = 0; it < cgitmax; ++it) dist_step(d, st);
+    if (!dist_fused_steps(d, cgitmax, st))
+        for (int it = 0; it < cgitmax; ++it) dist_step(d, st);
     dist_finish(d, st);  // residual r = A z needs all of z
     for (auto& s : d->shards) cg_launch_norms(s->v, shift, st);
     gather_scalars(d, st, 2, CgFin::Norms, shift);
@@ -482,6 +524,7 @@ PeerExchange::ShardBufs bufs_of(const Shard& s) {
 void drop_graph(b200_dist_cg* d) {
     if (d->graph) cudaGraphExecDestroy(d->graph);
     d->graph = nullptr;
+    d->fused_ready = false;  // the transport changed: the slot table is rebuilt on the next run
 }
 
 void check_peer_errors(b200_dist_cg* d) {
@@ -533,6 +576,16 @@ int b200_dist_cg_p2p_attach(b200_dist_cg* d, const void* handles) {
 
 int b200_dist_cg_transport(const b200_dist_cg* d) { return d ? d->transport : -1; }
 
+int b200_dist_cg_set_fused(b200_dist_cg* d, int on) {
+    return boundary("b200_dist_cg_set_fused", [&] {
+        if (!d) throw Error(Errc::DataError, "NULL solver");
+        d->fused_on = on != 0;
+        drop_graph(d);
+    });
+}
+
+int b200_dist_cg_fused(const b200_dist_cg* d) { return d && d->fused_last ? 1 : 0; }
+
 int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream) {
     return boundary("b200_dist_cg_load_x", [&] {
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->stream;
@@ -548,6 +601,7 @@ int b200_dist_cg_load_x(b200_dist_cg* d, const double* x_host, void* stream) {
 
 int b200_dist_cg_outer(b200_dist_cg* d, int cgitmax, double shift, void* stream) {
     return boundary("b200_dist_cg_outer", [&] {
+        prepare_fused(d);
         dist_outer_graph(d, cgitmax, shift, stream ? static_cast<cudaStream_t>(stream) : d->stream);
     });
 }
@@ -598,6 +652,7 @@ int b200_dist_cg_result(b200_dist_cg* d, double* zeta, double* rnorm) {
 int b200_dist_npb(b200_dist_cg* d, int niter, double shift, double* zeta, double* rnorm) {
     return boundary("b200_dist_npb", [&] {
         cudaStream_t st = d->stream;
+        prepare_fused(d);
         for (auto& s : d->shards) cg_launch_reset_x(s->v, st);
         dist_outer_graph(d, 25, shift, st);  // NPB's untimed warm-up iteration
         for (auto& s : d->shards) cg_launch_reset_x(s->v, st);

@@ -376,6 +376,7 @@ void PeerExchange::bind_producers(const std::vector<CgScalars*>& sc) {
         d.mb = mailbox(l);
         d.world = world_;
         d.rank = l.rank;
+        d.send = l.send.as<std::int64_t>();
         l.desc.ensure(sizeof d);
         B200_CUDA(cudaMemcpyAsync(l.desc.ptr, &d, sizeof d, cudaMemcpyHostToDevice, rt().stream));
         const void* dp = l.desc.ptr;

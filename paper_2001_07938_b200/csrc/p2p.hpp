@@ -46,6 +46,7 @@ struct P2pDesc {
     Mailbox mb;
     int world;
     int rank;
+    const std::int64_t* send;  // world x {lo, hi}: the part of this shard's slice each peer reads
 };
 
 #ifdef __CUDACC__

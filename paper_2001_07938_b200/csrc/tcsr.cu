@@ -355,16 +355,54 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, doub
 // for it only before the first slab copy of x, so the tile prologue (y
 // buffer, L2 prefetch, descriptors, head chunks: nothing that depends on x)
 // overlaps the barrier.
+// A gate on peer flags (the sharded fused CG): every sender's flag must reach
+// `epoch` (p slices pushed into this shard's replica) before x is read; a wait
+// without progress for 5 s sets *err and gives up (a broken link fails the
+// run instead of hanging the GPU).
+struct FlagGate {
+    const unsigned long long* flags;
+    int n;
+    unsigned long long epoch;
+    int* err;
+};
+
+__device__ __forceinline__ unsigned long long gtime_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void wait_flags(const unsigned long long* flags, int n, unsigned long long epoch, int* err) {
+    if (*reinterpret_cast<volatile int*>(err)) return;
+    const unsigned long long t0 = gtime_ns();
+    for (int r = 0; r < n; ++r) {
+        unsigned long long v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
+            if (v >= epoch) break;
+            if (gtime_ns() - t0 > 5000000000ull) {
+                *reinterpret_cast<volatile int*>(err) = 1;
+                return;
+            }
+        }
+    }
+}
+
+// cta / ncta: this CTA's index among the CTAs sharing the matrix (-1: the
+// whole grid; the sharded fused CG runs several shards' CTA groups in one grid)
 template <bool DOT, int MODE, bool COHERENT>
 __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, double* y, std::int64_t dot_off,
-                                             TileCta& c, const unsigned* gate = nullptr, unsigned gate_target = 0) {
+                                             TileCta& c, const unsigned* gate = nullptr, unsigned gate_target = 0,
+                                             const FlagGate* fg = nullptr, int cta = -1, int ncta = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* xs = c.xs;
     double* yp = c.yp;
     double pq = 0.0;
     const int P = T.parts;
     const std::int64_t items = T.ntiles * P;
-    for (std::int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const std::int64_t my_cta = cta < 0 ? static_cast<std::int64_t>(blockIdx.x) : cta;
+    const std::int64_t n_cta = ncta < 0 ? static_cast<std::int64_t>(gridDim.x) : ncta;
+    for (std::int64_t item = my_cta; item < items; item += n_cta) {
         const std::int64_t t = item / P;
         const int part = static_cast<int>(item - t * P);
         const int k0 = part * T.nslabs / P, k1 = (part + 1) * T.nslabs / P;  // this part's slabs
@@ -375,7 +413,7 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         // they wait behind the head chunk loads instead, which must lead
         // (whole NPB C: 72.2 vs 73.2 us issued first).
         bool issued = false;
-        if (tid == 0 && P > 1 && !gate && k1 > k0 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
+        if (tid == 0 && P > 1 && !gate && !fg && k1 > k0 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
             issue_slab(T, x, xs, k0, &c.mbar[0], MODE == 8 || MODE == 9);
             if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1], MODE == 8 || MODE == 9);
@@ -416,6 +454,8 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             } while (v < gate_target);
             gate = nullptr;
         }
+        if (tid == 0 && fg) wait_flags(fg->flags, fg->n, fg->epoch, fg->err);
+        fg = nullptr;
         if (COHERENT) cg_mark(c.tstep, 1);
         if (tid == 0 && !issued && k1 > k0 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
             if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");  // x: generic writes -> bulk reads
@@ -768,6 +808,157 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
 
 int g_sms = 0;
 
+// ---- the sharded CG in one persistent kernel ------------------
+//
+// k_cg_tiled for a row shard whose p replica is filled by its peers over the
+// peer-memory exchange (p2p.hpp): per CG step the tiled SpMV of the shard
+// (gated on every sender's p flag), the p.q partial of the shard published
+// into every peer's mailbox (NVLink stores + a release.sys flag), a wait for
+// all shards' partials and alpha from their rank-order sum; the z/r update
+// with r.r the same way; then the p update, each new value stored locally and
+// into every peer's replica (only the rows in its column footprint), and this
+// shard's flags raised. One launch replaces 6 kernels per CG step. The CTAs
+// of a shard synchronise on a shard-local counter; shards only through the
+// flags, so one process per GPU runs one slot, and k slots in one cooperative
+// grid emulate k shards on one GPU (how it is tested here). Every wait gives
+// up after 5 s and sets the mailbox error flag.
+struct DistSlot {
+    TcsrDev T;
+    CgVectors v;
+    unsigned* bar;  // the slot's barrier counter (zeroed before the launch)
+};
+
+__device__ __forceinline__ void slot_sync(unsigned* bar, unsigned& target, unsigned n, int* err) {
+    __syncthreads();
+    target += n;
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned long long t0 = gtime_ns();
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= target) break;
+            if (gtime_ns() - t0 > 5000000000ull) {
+                *reinterpret_cast<volatile int*>(err) = 1;
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// this shard's partial into slot (e & 1) of every peer's mailbox, then its flags
+__device__ __forceinline__ void dist_publish(const P2pDesc& d, double val, unsigned long long e) {
+    const unsigned long long slot = e & 1ull;
+    for (int r = 0; r < d.world; ++r)
+        d.peers[r].gathered[(slot * kP2pMaxWorld + d.rank) * kP2pMaxPart] = val;
+    __threadfence_system();
+    for (int r = 0; r < d.world; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(d.peers[r].flags + d.rank), "l"(e) : "memory");
+}
+
+// every shard's partial of epoch e, summed in rank order (cg_fin_apply's order)
+__device__ __forceinline__ double dist_gather_sum(const P2pDesc& d, unsigned long long e) {
+    const unsigned long long slot = e & 1ull;
+    double a = 0.0;
+    for (int r = 0; r < d.world; ++r)
+        a += *reinterpret_cast<volatile double*>(d.mb.gathered + (slot * kP2pMaxWorld + r) * kP2pMaxPart);
+    return a;
+}
+
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_cg_tiled_dist(const DistSlot* __restrict__ slots, int nslots, int steps) {
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) std::uint64_t mbar[2];
+    __shared__ unsigned released[3];
+    __shared__ double red[kTileWarps + 1];
+    __shared__ unsigned long long epoch0;
+    const int tid = threadIdx.x;
+    const int cpr = static_cast<int>(gridDim.x) / nslots;
+    const int slot = static_cast<int>(blockIdx.x) / cpr;
+    if (slot >= nslots) return;
+    const int cta = static_cast<int>(blockIdx.x) - slot * cpr;
+    const DistSlot& S = slots[slot];
+    const TcsrDev& T = S.T;
+    const CgVectors& v = S.v;
+    const P2pDesc& d = *static_cast<const P2pDesc*>(v.sc->p2p);
+    TileCta c;
+    tile_cta_init(c, T, smem, mbar, released);
+    if (tid == 0) epoch0 = *d.mb.epoch;  // read by every CTA before any publish (the first needs all CTAs)
+    __syncthreads();
+    unsigned long long e = epoch0;
+    unsigned target = 0;
+    double rho = __ldcg(&v.sc->rho);
+    double* pq_part = v.partials;
+    double* rr_part = v.partials + 2 * kMaxParts;
+    const std::int64_t* send = d.send;
+    for (int it = 0; it < steps; ++it) {
+        // q = A p over the shard once every sender's p slice (epoch e) is in
+        const FlagGate fg{d.mb.flags, d.world, e, d.mb.err};
+        const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, v.row0, c, nullptr, 0, &fg, cta, cpr),
+                                  red);
+        if (tid == 0) pq_part[cta] = pq;
+        slot_sync(S.bar, target, static_cast<unsigned>(cpr), d.mb.err);
+        const double dpart = T.parts > 1 ? cta_sum_parts(T.tile_pq, static_cast<int>(T.ntiles), red)
+                                         : cta_sum_parts(pq_part, cpr, red);
+        ++e;
+        if (cta == 0 && tid == 0) dist_publish(d, dpart, e);
+        if (tid == 0) wait_flags(d.mb.flags, d.world, e, d.mb.err);
+        __syncthreads();
+        const double dsum = dist_gather_sum(d, e);
+        const double alpha = rho / dsum;
+        if (cta == 0 && tid == 0) {
+            v.sc->d = dsum;
+            v.sc->rho0 = rho;
+            v.sc->alpha = alpha;
+        }
+        double rr = 0.0;
+        for (std::int64_t i = static_cast<std::int64_t>(cta) * kTileThreads + tid; i < v.n;
+             i += static_cast<std::int64_t>(cpr) * kTileThreads) {
+            const double zi = __dadd_rn(__ldcg(v.z + i), __dmul_rn(alpha, __ldcg(v.p + i)));
+            const double ri = __dsub_rn(__ldcg(v.r + i), __dmul_rn(alpha, __ldcg(v.q + i)));
+            v.z[i] = zi;
+            v.r[i] = ri;
+            rr += ri * ri;
+        }
+        rr = cta_sum(rr, red);
+        if (tid == 0) rr_part[cta] = rr;
+        slot_sync(S.bar, target, static_cast<unsigned>(cpr), d.mb.err);
+        const double rpart = cta_sum_parts(rr_part, cpr, red);
+        ++e;
+        if (cta == 0 && tid == 0) dist_publish(d, rpart, e);
+        if (tid == 0) wait_flags(d.mb.flags, d.world, e, d.mb.err);
+        __syncthreads();
+        const double rho_new = dist_gather_sum(d, e);
+        const double beta = rho_new / rho;
+        if (cta == 0 && tid == 0) {
+            v.sc->rho = rho_new;
+            v.sc->beta = beta;
+        }
+        rho = rho_new;
+        // p = r + beta p on the owned rows, stored here and into every peer's
+        // replica rows its SpMV reads
+        for (std::int64_t i = static_cast<std::int64_t>(cta) * kTileThreads + tid; i < v.n;
+             i += static_cast<std::int64_t>(cpr) * kTileThreads) {
+            const double pv = __dadd_rn(__ldcg(v.r + i), __dmul_rn(beta, __ldcg(v.p + i)));
+            v.p[i] = pv;
+            for (int r = 0; r < d.world; ++r)
+                if (r != d.rank && i >= send[2 * r] && i < send[2 * r + 1]) d.peers[r].p_full[v.row0 + i] = pv;
+        }
+        __threadfence_system();
+        slot_sync(S.bar, target, static_cast<unsigned>(cpr), d.mb.err);
+        ++e;
+        if (cta == 0 && tid == 0) {
+            __threadfence_system();
+            for (int r = 0; r < d.world; ++r)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(d.peers[r].flags + d.rank), "l"(e)
+                             : "memory");
+        }
+    }
+    if (cta == 0 && tid == 0) *d.mb.epoch = e;  // the host-side exchanges continue the sequence
+}
+
+
 }  // namespace
 
 #if LILAC_CTA_TRACE
@@ -880,5 +1071,52 @@ bool launch_cg_tiled(const TcsrDev& T, const CgVectors& v, int steps, cudaStream
     B200_CUDA(cudaLaunchKernelEx(&cfg, k_cg_tiled, T, v, steps));
     return true;
 }
+
+
+// Host: k slots (device array of DistSlot) in one cooperative launch, each
+// slot's CTAs one per SM; bars: nslots counters. false when the grid cannot
+// give every slot a CTA.
+bool launch_cg_tiled_dist(const void* slots_dev, int nslots, std::size_t smem, unsigned* bars, int steps,
+                          cudaStream_t s) {
+    static int max_grid = -1;
+    if (max_grid < 0) {
+        int dev = 0, coop = 0, per_sm = 0, sms = 0;
+        B200_CUDA(cudaGetDevice(&dev));
+        B200_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        B200_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        B200_CUDA(
+            cudaFuncSetAttribute(k_cg_tiled_dist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBudget));
+        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tiled_dist, kTileThreads,
+                                                                 kTileSmemBudget));
+        max_grid = coop ? per_sm * sms : 0;
+    }
+    static std::uint64_t configured = 0;
+    if (first_on_device(configured))
+        B200_CUDA(
+            cudaFuncSetAttribute(k_cg_tiled_dist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBudget));
+    if (nslots <= 0 || steps <= 0) return false;
+    const int cpr = std::min(max_grid / nslots, kMaxParts);
+    if (cpr <= 0) return false;
+    B200_CUDA(cudaMemsetAsync(bars, 0, sizeof(unsigned) * static_cast<std::size_t>(nslots), s));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(cpr * nslots));
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    B200_CUDA(cudaLaunchKernelEx(&cfg, k_cg_tiled_dist, static_cast<const DistSlot*>(slots_dev), nslots, steps));
+    return true;
+}
+
+std::size_t dist_slot_bytes() { return sizeof(DistSlot); }
+void dist_slot_fill(void* out, const TcsrDev& T, const CgVectors& v, unsigned* bar) {
+    DistSlot d{T, v, bar};
+    std::memcpy(out, &d, sizeof d);
+}
+std::size_t tiled_smem_bytes(const TcsrDev& T) { return tile_smem(T); }
 
 }  // namespace b200

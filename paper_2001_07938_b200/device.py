@@ -256,6 +256,15 @@ class DistCG:
         """All ranks' records, rank-major (world x 208 bytes)."""
         N.check(N.lib().b200_dist_cg_p2p_attach(self._h, C.create_string_buffer(bytes(handles), len(handles))))
 
+    def set_fused(self, on: bool):
+        """The persistent sharded CG kernel (peer memory + tiled shards) on / off."""
+        N.check(N.lib().b200_dist_cg_set_fused(self._h, 1 if on else 0))
+
+    @property
+    def fused(self) -> bool:
+        """The last outer iteration ran the persistent sharded CG kernel."""
+        return N.lib().b200_dist_cg_fused(self._h) == 1
+
     @property
     def transport(self) -> str:
         return {0: "local", 1: "nccl", 2: "p2p"}.get(N.lib().b200_dist_cg_transport(self._h), "?")

@@ -560,10 +560,36 @@ def test_sharded_cg_peer_memory_exchange_local(cls, k):
     d0.free()
     d = D.DistCG.local(k, rp, ci, val)
     d.use_p2p_local()
+    d.set_fused(False)  # the per-step kernels: same partials as the device-copy exchange
     assert d.transport == "p2p"
     z1, r1 = d.npb(niter, shift)
     assert abs(z1 - zeta_ref) / zeta_ref <= 1e-10
     assert z1 == z0 and r1 == r0
+    assert not d.fused
+    d.free()
+
+
+@pytest.mark.parametrize("cls,k", [("A", 1), ("A", 2), ("A", 3), ("A", 8), ("C", 2), ("C", 4), ("C", 8)])
+def test_sharded_cg_fused_persistent_kernel(cls, k):
+    """The sharded CG in one persistent kernel (k_cg_tiled_dist): k local
+    shards as k CTA groups of one cooperative grid, exchanging p slices and
+    the dot partials through each other's peer buffers and epoch flags, as
+    the ranks of a multi-GPU run would over NVLink. zeta must verify and
+    agree with the 1-GPU solver to ~1e-12 (the dot partitions differ)."""
+    na, nonzer, niter, shift, zeta_ref = D.NPB_CLASSES[cls]
+    rp, ci, val = D.gen_npb(na, nonzer, shift)
+    N.lib().b200_set_kernel(b"tiled")  # class A shards are small enough for the vector kernel by default
+    d = D.DistCG.local(k, rp, ci, val)
+    for g in range(k):
+        assert d.info(g)["tiled"] == 1
+    d.use_p2p_local()
+    zeta, rnorm = d.npb(niter, shift)
+    assert d.fused
+    assert abs(zeta - zeta_ref) / zeta_ref <= 1e-10, (zeta, zeta_ref)
+    d.set_fused(False)
+    z_steps, _ = d.npb(niter, shift)
+    assert not d.fused
+    assert abs(zeta - z_steps) <= 1e-12 * abs(z_steps)
     d.free()
 
 

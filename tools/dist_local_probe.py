@@ -1,6 +1,8 @@
 """Outer-iteration time of the sharded CG driver with k shards on one GPU
 (LocalExchange), e.g. to compare LILAC_B200_DIST_GRAPH=0/1.
-    python tools/dist_local_probe.py [k] [class]"""
+    python tools/dist_local_probe.py [k] [class]
+DIST_P2P=1: peer-memory exchange; DIST_FUSED=0: its per-step kernels instead of
+the persistent sharded CG kernel."""
 import os
 import sys
 import time
@@ -19,6 +21,7 @@ rp, ci, val = D.gen_npb(na, nonzer, shift)
 d = D.DistCG.local(k, rp, ci, val)
 if os.environ.get("DIST_P2P", "0") == "1":
     d.use_p2p_local()
+    d.set_fused(os.environ.get("DIST_FUSED", "1") == "1")
 s = torch.cuda.Stream()
 d.reset(s.cuda_stream)
 for _ in range(3):
@@ -32,5 +35,5 @@ for _ in range(10):
 e1.record(s)
 host = (time.perf_counter() - t0) / 10
 torch.cuda.synchronize()
-print(f"k={k} class {cls} transport={d.transport} graph={os.environ.get('LILAC_B200_DIST_GRAPH', '1')}: "
+print(f"k={k} class {cls} transport={d.transport} fused={d.fused} graph={os.environ.get('LILAC_B200_DIST_GRAPH', '1')}: "
       f"{e0.elapsed_time(e1) / 10:.3f} ms/outer (host issue {host * 1e3:.3f} ms)")
