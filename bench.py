@@ -827,7 +827,9 @@ def run_npb(ctx, cls):
                   + ("tiled layout (16-bit slab-local column keys)" if info["kernel"] == 4
                      else f"CSR (int{8 * info['col_bytes']} col_ind)"),
         "parallelism": (f"row-sharded x{ctx.world} ({transport} exchange of p and the dot partials per CG step, "
-                        "CUDA graph per NPB iteration)") if ctx.world > 1 else "single GPU, CUDA graph per NPB iteration",
+                        + ("the CG steps in one persistent kernel per GPU (k_cg_tiled_dist), "
+                           if ctx.world > 1 and getattr(cg, "fused", False) else "")
+                        + "CUDA graph per NPB iteration)") if ctx.world > 1 else "single GPU, CUDA graph per NPB iteration",
         "shard_rows_rank0": list(shard_rows),
         "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % (by / 1e9) if by > 126e6 else
               "matrix smaller than L2 (%.1f MB)" % (by / 1e6),
@@ -842,10 +844,13 @@ def run_npb(ctx, cls):
     line["roofline"] = roofline(by, spmv_ms, kname, f"algorithmic bytes nnz*(8+{info['col_bytes']})+8(rows+1)+8rows+"
                                 f"8cols per launch / mean of {args.spmv_reps} back-to-back launches (CUDA events, "
                                 "bench stream)", cfg)
+    dist_fused = ctx.world > 1 and getattr(cg, "fused", False)
     line["gpu_launches"] = args.steps * (((1 + 1 + 2 + 2) if fused else (1 + 3 * CGITMAX + 2 + 2)) if ctx.world == 1
-                                         else (1 + 6 * CGITMAX + 6 + 2))
+                                         else (4 + 1 + 5 + 3) if dist_fused else (1 + 6 * CGITMAX + 6 + 2))
     line["cg_steps"] = ("one persistent cooperative kernel per NPB iteration (grid barriers)"
-                        if fused and ctx.world == 1 else "3 kernels per CG step (programmatic dependent launch)")
+                        if fused and ctx.world == 1 else
+                        "one persistent kernel per NPB iteration per GPU (shard barriers, peer flags)" if dist_fused
+                        else "3 kernels per CG step (programmatic dependent launch)")
     line["clocks"] = clk
     line["marshal_first_call"] = {"s": t_marshal, "h2d_bytes": int(nnz * 16 + (na + 1) * 8),
                                   "device_bytes": info["device_bytes"],
