@@ -844,6 +844,15 @@ def run_npb(ctx, cls):
     line["roofline"] = roofline(by, spmv_ms, kname, f"algorithmic bytes nnz*(8+{info['col_bytes']})+8(rows+1)+8rows+"
                                 f"8cols per launch / mean of {args.spmv_reps} back-to-back launches (CUDA events, "
                                 "bench stream)", cfg)
+    # the whole timed region against the same peak: an NPB iteration's
+    # algorithmic bytes (26 SpMV + 25 CG steps' 96n vector bytes + ~48n for
+    # the residual and norms) per measured iteration, over all ranks
+    pk, _ = measured_peak()
+    it_bytes = 26 * by * ctx.world + (25 * 96 + 48) * na
+    line["iteration_roofline"] = {"achieved": it_bytes / (ms_step * 1e-3) / 1e9, "peak": pk, "unit": "GB/s",
+                                  "frac": it_bytes / (ms_step * 1e-3) / 1e9 / (pk * ctx.world),
+                                  "how": "(26 SpMV bytes + (25*96+48) n) per NPB iteration / ms_per_step, "
+                                         "peak x n_gpus"}
     dist_fused = ctx.world > 1 and getattr(cg, "fused", False)
     line["gpu_launches"] = args.steps * (((1 + 1 + 2 + 2) if fused else (1 + 3 * CGITMAX + 2 + 2)) if ctx.world == 1
                                          else (4 + 1 + 5 + 3) if dist_fused else (1 + 6 * CGITMAX + 6 + 2))
