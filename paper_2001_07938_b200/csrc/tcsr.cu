@@ -324,7 +324,32 @@ struct TileCta {
     std::uint32_t xs_s, yp_s;
     unsigned phase0, phase1;
     int tstep;  // fused CG step (LILAC_CTA_TRACE builds)
+    // fused CG: the tile's z, p, r rows (global, from st_row0, st_n of them)
+    // are bulk-copied into the slab buffer that goes idle when the
+    // penultimate slab is released, so they land during the last slab's walk
+    // (st_n = 0: no staging)
+    const double *st_z, *st_p, *st_r;
+    std::int64_t st_row0;
+    int st_n;
 };
+
+// Where the staged rows sit in the slab buffer: an array's rows start at an
+// even offset (16-byte copies) plus the row-0 parity shift.
+__device__ __forceinline__ int stage_pitch(int n) { return (n + 3) & ~1; }
+
+// Issued by one thread: the three row ranges into buffer `dst` (a slab
+// buffer no warp reads any more), completion on `mbar`.
+__device__ __forceinline__ void issue_stage(const TileCta& c, double* dst, std::uint64_t* mbar) {
+    const int sh = static_cast<int>(c.st_row0 & 1);
+    const int len = (c.st_n + sh + 1) & ~1;  // even: whole 16-byte granules
+    const int pitch = stage_pitch(c.st_n);
+    const unsigned bytes = static_cast<unsigned>(len) * 8u;
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // rows written by generic stores last step
+    mbar_arrive_tx(mbar, 3u * bytes);
+    bulk_g2s(dst, c.st_z + (c.st_row0 - sh), bytes, mbar);
+    bulk_g2s(dst + pitch, c.st_p + (c.st_row0 - sh), bytes, mbar);
+    bulk_g2s(dst + 2 * pitch, c.st_r + (c.st_row0 - sh), bytes, mbar);
+}
 
 __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, double* smem, std::uint64_t* mbar,
                                               unsigned* released) {
@@ -339,6 +364,9 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, doub
     c.yp_s = opaque_u32(smem_addr(c.yp));
     c.phase0 = c.phase1 = 0;
     c.tstep = 0;
+    c.st_z = c.st_p = c.st_r = nullptr;
+    c.st_row0 = 0;
+    c.st_n = 0;
     if (threadIdx.x == 0) {
         released[0] = released[1] = 0;
         c.xs[T.slab_w] = c.xs[c.stride + T.slab_w] = 0.0;  // padding entries read these
@@ -498,6 +526,8 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
                     if (k + 2 < k1 && (MODE < 5 || MODE == 8 || MODE == 9 || MODE == 12)) {
                         if (COHERENT) asm volatile("fence.proxy.async.global;" ::: "memory");
                         issue_slab(T, x, xs + buf * c.stride, k + 2, &c.mbar[buf], MODE == 8 || MODE == 9);
+                    } else if (COHERENT && c.st_n > 0 && P == 1 && k + 2 == k1) {
+                        issue_stage(c, xs + buf * c.stride, &c.mbar[buf]);
                     }
                 }
             }
@@ -689,6 +719,10 @@ __device__ __forceinline__ double cta_sum_parts(const double* p, int n, double* 
 #define LILAC_CG_PREFETCH 1  // 0 / 1 / 2 / 3 slabs: 494.8 / 498.2 / 493.6 / 484.7 NPB C it/s
 #endif
 constexpr int kCgPrefetch = LILAC_CG_PREFETCH;  // slabs of the next step's runs prefetched during the barriers
+#ifndef LILAC_CG_ASYNC_STAGE
+#define LILAC_CG_ASYNC_STAGE 1
+#endif
+constexpr bool kCgAsyncStage = LILAC_CG_ASYNC_STAGE != 0;  // z, p, r rows staged by bulk copies during the last slab
 
 __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVectors v, int steps) {
     extern __shared__ __align__(128) double smem[];
@@ -704,6 +738,28 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     double rho = __ldcg(&v.sc->rho);
     double* pq_part = v.partials;
     double* rr_part = v.partials + 2 * kMaxParts;
+    // One tile per CTA: the tile's z, p, r rows are staged into a slab buffer
+    // and q stays in the y buffer, so the updates below touch no global loads.
+    // With two or more slabs the staging is three bulk copies issued when the
+    // penultimate slab's buffer is released (they land during the last slab's
+    // walk); otherwise loads after the SpMV.
+    const bool one_tile = T.parts == 1 && T.ntiles <= gridDim.x && blockIdx.x < T.ntiles;
+    const std::int64_t crow0 = one_tile ? T.tile_row0[blockIdx.x] : 0;
+    const int cn = one_tile ? static_cast<int>(T.tile_row0[blockIdx.x + 1] - crow0) : 0;
+    const bool async_stage = kCgAsyncStage && one_tile && T.nslabs >= 2 && 3 * stage_pitch(cn) <= c.stride;
+    const bool cached = async_stage || (one_tile && 3 * cn <= 2 * c.stride);  // z, p, r rows fit the slab buffers
+    const int sbuf = (T.nslabs - 2) & 1;  // the buffer of slab nslabs - 2
+    const int sh = static_cast<int>(crow0 & 1), pitch = stage_pitch(cn);
+    double* zs = async_stage ? c.xs + sbuf * c.stride + sh : c.xs;
+    double* ps = async_stage ? zs + pitch : c.xs + cn;
+    double* rs = async_stage ? zs + 2 * pitch : c.xs + 2 * cn;
+    if (async_stage) {
+        c.st_z = v.z;
+        c.st_p = v.p;
+        c.st_r = v.r;
+        c.st_row0 = crow0;
+        c.st_n = cn;
+    }
     for (int it = 0; it < steps; ++it) {
         c.tstep = it;
         cg_mark(it, 0);
@@ -726,18 +782,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
                 for (int k = k0; k < k1 && k < k0 + kCgPrefetch; ++k)
                     prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
         }
-        // One tile per CTA: the tile's z, p, r rows are staged into the (now
-        // idle) slab buffers while this CTA waits at the barrier, and q is
-        // still in the y buffer, so the updates below touch no global loads.
-        const bool one_tile = T.parts == 1 && T.ntiles <= gridDim.x && blockIdx.x < T.ntiles;
-        const std::int64_t crow0 = one_tile ? T.tile_row0[blockIdx.x] : 0;
-        const int cn = one_tile ? static_cast<int>(T.tile_row0[blockIdx.x + 1] - crow0) : 0;
-        const bool cached = one_tile && 3 * cn <= 2 * c.stride;  // z, p, r rows fit the slab buffers
-        if (cached) {
+        if (async_stage) {  // the staging copies issued during the SpMV
+            if (sbuf == 0) {
+                mbar_wait(&c.mbar[0], c.phase0);
+                c.phase0 ^= 1;
+            } else {
+                mbar_wait(&c.mbar[1], c.phase1);
+                c.phase1 ^= 1;
+            }
+        } else if (cached) {
             for (int r = tid; r < cn; r += kTileThreads) {
-                c.xs[r] = __ldcg(v.z + crow0 + r);
-                c.xs[cn + r] = __ldcg(v.p + crow0 + r);
-                c.xs[2 * cn + r] = __ldcg(v.r + crow0 + r);
+                zs[r] = __ldcg(v.z + crow0 + r);
+                ps[r] = __ldcg(v.p + crow0 + r);
+                rs[r] = __ldcg(v.r + crow0 + r);
             }
         }
         cg_mark(it, 7);
@@ -748,9 +805,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         const double alpha = rho / d;
         double rr = 0.0;
         if (cached) {
-            double* zs = c.xs;
-            const double* ps = c.xs + cn;
-            double* rs = c.xs + 2 * cn;
             for (int r = tid; r < cn; r += kTileThreads) {
                 const double zi = __dadd_rn(zs[r], __dmul_rn(alpha, ps[r]));
                 const double ri = __dsub_rn(rs[r], __dmul_rn(alpha, c.yp[r]));
@@ -785,8 +839,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         const double rho_new = cta_sum_parts(rr_part, gridDim.x, red);
         const double beta = rho_new / rho;
         if (cached) {
-            const double* ps = c.xs + cn;
-            const double* rs = c.xs + 2 * cn;
             for (int r = tid; r < cn; r += kTileThreads) v.p[crow0 + r] = __dadd_rn(rs[r], __dmul_rn(beta, ps[r]));
             // the next step's slab copies (async proxy) overwrite these generic writes
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
