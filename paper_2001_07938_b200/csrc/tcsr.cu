@@ -331,6 +331,8 @@ struct TileCta {
     const double *st_z, *st_p, *st_r;
     std::int64_t st_row0;
     int st_n;
+    int st_buf;            // the slab buffer the rows land in
+    const double* st_ps;   // where the p rows land (shared memory): the p.q epilogue reads them
 };
 
 // Where the staged rows sit in the slab buffer: an array's rows start at an
@@ -367,6 +369,8 @@ __device__ __forceinline__ void tile_cta_init(TileCta& c, const TcsrDev& T, doub
     c.st_z = c.st_p = c.st_r = nullptr;
     c.st_row0 = 0;
     c.st_n = 0;
+    c.st_buf = 0;
+    c.st_ps = nullptr;
     if (threadIdx.x == 0) {
         released[0] = released[1] = 0;
         c.xs[T.slab_w] = c.xs[c.stride + T.slab_w] = 0.0;  // padding entries read these
@@ -536,10 +540,27 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
         if (!DOT && !COHERENT) trace_mark(3);
         if (COHERENT) cg_mark(c.tstep, 3);
         if (P == 1) {
-            for (int r = tid; r < nrows; r += kTileThreads) {
-                const double v = yp[r];
-                y[row0 + r] = v;
-                if (DOT) pq += v * (COHERENT ? __ldcg(x + dot_off + row0 + r) : __ldg(x + dot_off + row0 + r));
+            if (COHERENT && c.st_n > 0) {
+                // the staged rows (issued at the penultimate slab) hold this
+                // tile's p: the dot needs no global round trip
+                if (c.st_buf == 0) {
+                    mbar_wait(&c.mbar[0], c.phase0);
+                    c.phase0 ^= 1;
+                } else {
+                    mbar_wait(&c.mbar[1], c.phase1);
+                    c.phase1 ^= 1;
+                }
+                for (int r = tid; r < nrows; r += kTileThreads) {
+                    const double v = yp[r];
+                    y[row0 + r] = v;
+                    if (DOT) pq += v * c.st_ps[r];
+                }
+            } else {
+                for (int r = tid; r < nrows; r += kTileThreads) {
+                    const double v = yp[r];
+                    y[row0 + r] = v;
+                    if (DOT) pq += v * (COHERENT ? __ldcg(x + dot_off + row0 + r) : __ldg(x + dot_off + row0 + r));
+                }
             }
         } else {
             // this part's row sums out; the tile's last part adds all parts
@@ -759,6 +780,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         c.st_r = v.r;
         c.st_row0 = crow0;
         c.st_n = cn;
+        c.st_buf = sbuf;
+        c.st_ps = ps;
     }
     for (int it = 0; it < steps; ++it) {
         c.tstep = it;
@@ -782,14 +805,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
                 for (int k = k0; k < k1 && k < k0 + kCgPrefetch; ++k)
                     prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
         }
-        if (async_stage) {  // the staging copies issued during the SpMV
-            if (sbuf == 0) {
-                mbar_wait(&c.mbar[0], c.phase0);
-                c.phase0 ^= 1;
-            } else {
-                mbar_wait(&c.mbar[1], c.phase1);
-                c.phase1 ^= 1;
-            }
+        if (async_stage) {
+            // the staging copies landed: waited for in spmv_tiles' epilogue
         } else if (cached) {
             for (int r = tid; r < cn; r += kTileThreads) {
                 zs[r] = __ldcg(v.z + crow0 + r);
