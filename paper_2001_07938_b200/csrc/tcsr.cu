@@ -759,6 +759,27 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     double rho = __ldcg(&v.sc->rho);
     double* pq_part = v.partials;
     double* rr_part = v.partials + 2 * kMaxParts;
+    // the next step's first runs of this CTA's first item, loaded once
+    __shared__ int pf_lo[kCgPrefetch > 0 ? kCgPrefetch : 1][kTileWarps], pf_hi[kCgPrefetch > 0 ? kCgPrefetch : 1][kTileWarps];
+    __shared__ const double* pf_vb;
+    __shared__ const std::uint16_t* pf_kb;
+    const bool pf_on = kCgPrefetch > 0 && blockIdx.x < T.ntiles * T.parts;
+    if (pf_on) {
+        const std::int64_t t = blockIdx.x / T.parts;
+        const int part = static_cast<int>(blockIdx.x - t * T.parts);
+        const int k0 = part * T.nslabs / T.parts, k1 = (part + 1) * T.nslabs / T.parts;
+        const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
+        if (tid == 0) {
+            pf_vb = T.val + T.tile_base[t];
+            pf_kb = T.key + T.tile_base[t];
+        }
+        for (int e = tid; e < (kCgPrefetch > 0 ? kCgPrefetch : 1) * kTileWarps; e += kTileThreads) {
+            const int q = e / kTileWarps, w = e - q * kTileWarps, k = k0 + q;
+            pf_lo[q][w] = k < k1 ? wo[k * kTileWarps + w] : 0;
+            pf_hi[q][w] = k < k1 ? wo[k * kTileWarps + w + 1] : 0;
+        }
+    }
+    __syncthreads();
     // One tile per CTA: the tile's z, p, r rows are staged into a slab buffer
     // and q stays in the y buffer, so the updates below touch no global loads.
     // With two or more slabs the staging is three bulk copies issued when the
@@ -790,20 +811,14 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
                                   red);
         cg_mark(it, 6);
         if (tid == 0) pq_part[blockIdx.x] = pq;
-        if (kCgPrefetch > 0 && it + 1 < steps && blockIdx.x < T.ntiles * T.parts) {
+        if (kCgPrefetch > 0 && it + 1 < steps && pf_on && (tid & 31) == 0) {
             // HBM is idle until the next step's SpMV (barriers, vector
             // updates, CTAs waiting for the slowest one): pull the runs of
-            // this CTA's first slabs of the next step into L2 now
-            const int lane = tid & 31, warp = tid >> 5;
-            const std::int64_t t = blockIdx.x / T.parts;
-            const int part = static_cast<int>(blockIdx.x - t * T.parts);
-            const int k0 = part * T.nslabs / T.parts, k1 = (part + 1) * T.nslabs / T.parts;
-            const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
-            const double* vb = T.val + T.tile_base[t];
-            const std::uint16_t* kb = T.key + T.tile_base[t];
-            if (lane == 0)
-                for (int k = k0; k < k1 && k < k0 + kCgPrefetch; ++k)
-                    prefetch_run(vb, kb, wo[k * kTileWarps + warp], wo[k * kTileWarps + warp + 1]);
+            // this CTA's first slabs of the next step into L2 now (bounds
+            // from shared memory: no global round trip before the barrier)
+            const int warp = tid >> 5;
+            for (int q = 0; q < kCgPrefetch; ++q)
+                if (pf_lo[q][warp] < pf_hi[q][warp]) prefetch_run(pf_vb, pf_kb, pf_lo[q][warp], pf_hi[q][warp]);
         }
         if (async_stage) {
             // the staging copies landed: waited for in spmv_tiles' epilogue

@@ -50,3 +50,10 @@ names = ["gate min", "gate max", "slab0 avg", "slab0 max", "walk end min", "walk
 print(f"grid {grid}, steps traced {steps}; per step (mean over steps 1..{len(rows)}), us from the step's first CTA start:")
 for n, v in zip(names, m):
     print(f"  {n:16s} {v:8.2f}")
+
+# is a CTA's SpMV time systematic across steps (same CTA, same SM, same tile)?
+w = (a[1:steps, :, 3] - a[1:steps, :, 2]).astype(np.float64) / 1e3  # walk: slab 0 landed -> walk end
+c = np.corrcoef(w[::2].mean(axis=0), w[1::2].mean(axis=0))[0, 1]
+print(f"per-CTA walk time, even vs odd steps: correlation {c:.2f}; CTA means min/avg/max "
+      f"{w.mean(axis=0).min():.2f}/{w.mean():.2f}/{w.mean(axis=0).max():.2f} us; per-step spread (max-avg) "
+      f"{(w.max(axis=1) - w.mean(axis=1)).mean():.2f} us")
