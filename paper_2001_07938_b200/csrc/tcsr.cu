@@ -47,6 +47,8 @@ __device__ __forceinline__ void trace_mark(int slot, bool cond = true) {
 // end, after barrier 1, after barrier 2, p.q summed, z/p/r staged
 constexpr int kCgTraceSteps = 32, kCgTraceCtas = 160;
 __device__ unsigned long long g_cg_trace[kCgTraceSteps * kCgTraceCtas * 8];
+__device__ unsigned g_cg_smid[kCgTraceCtas];
+__device__ unsigned g_cg_rot;  // k_cg_tiled: CTA b takes tile (b + rot) % grid (trace builds)
 __device__ __forceinline__ void cg_mark(int step, int slot) {
     if (threadIdx.x == 0 && step < kCgTraceSteps && blockIdx.x < kCgTraceCtas)
         g_cg_trace[(step * kCgTraceCtas + blockIdx.x) * 8 + slot] = gtimer();
@@ -751,6 +753,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     __shared__ unsigned released[3];
     __shared__ double red[kTileWarps + 1];
     const int tid = threadIdx.x;
+#if LILAC_CTA_TRACE
+    const unsigned me = (blockIdx.x + g_cg_rot) % gridDim.x;  // trace builds: which tile a CTA takes can rotate
+#else
+    const unsigned me = blockIdx.x;
+#endif
     TileCta c;
     tile_cta_init(c, T, smem, mbar, released);
     __syncthreads();
@@ -763,10 +770,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     __shared__ int pf_lo[kCgPrefetch > 0 ? kCgPrefetch : 1][kTileWarps], pf_hi[kCgPrefetch > 0 ? kCgPrefetch : 1][kTileWarps];
     __shared__ const double* pf_vb;
     __shared__ const std::uint16_t* pf_kb;
-    const bool pf_on = kCgPrefetch > 0 && blockIdx.x < T.ntiles * T.parts;
+    const bool pf_on = kCgPrefetch > 0 && me < T.ntiles * T.parts;
     if (pf_on) {
-        const std::int64_t t = blockIdx.x / T.parts;
-        const int part = static_cast<int>(blockIdx.x - t * T.parts);
+        const std::int64_t t = me / T.parts;
+        const int part = static_cast<int>(me - t * T.parts);
         const int k0 = part * T.nslabs / T.parts, k1 = (part + 1) * T.nslabs / T.parts;
         const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
         if (tid == 0) {
@@ -785,9 +792,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     // With two or more slabs the staging is three bulk copies issued when the
     // penultimate slab's buffer is released (they land during the last slab's
     // walk); otherwise loads after the SpMV.
-    const bool one_tile = T.parts == 1 && T.ntiles <= gridDim.x && blockIdx.x < T.ntiles;
-    const std::int64_t crow0 = one_tile ? T.tile_row0[blockIdx.x] : 0;
-    const int cn = one_tile ? static_cast<int>(T.tile_row0[blockIdx.x + 1] - crow0) : 0;
+    const bool one_tile = T.parts == 1 && T.ntiles <= gridDim.x && me < T.ntiles;
+    const std::int64_t crow0 = one_tile ? T.tile_row0[me] : 0;
+    const int cn = one_tile ? static_cast<int>(T.tile_row0[me + 1] - crow0) : 0;
     const bool async_stage = kCgAsyncStage && one_tile && T.nslabs >= 2 && 3 * stage_pitch(cn) <= c.stride;
     const bool cached = async_stage || (one_tile && 3 * cn <= 2 * c.stride);  // z, p, r rows fit the slab buffers
     const int sbuf = (T.nslabs - 2) & 1;  // the buffer of slab nslabs - 2
@@ -804,10 +811,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
         c.st_buf = sbuf;
         c.st_ps = ps;
     }
+#if LILAC_CTA_TRACE
+    if (tid == 0 && blockIdx.x < kCgTraceCtas) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cg_smid[blockIdx.x] = smid;
+    }
+#endif
     for (int it = 0; it < steps; ++it) {
         c.tstep = it;
         cg_mark(it, 0);
-        const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c, it > 0 ? bar : nullptr, target),
+        const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, 0, c, it > 0 ? bar : nullptr, target, nullptr,
+                                                            static_cast<int>(me), -1),
                                   red);
         cg_mark(it, 6);
         if (tid == 0) pq_part[blockIdx.x] = pq;
@@ -846,7 +861,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
                 rr += ri * ri;
             }
         } else {
-            for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+            for (std::int64_t t = me; t < T.ntiles; t += gridDim.x) {
                 const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
                 for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads) {
                     const double zi = __dadd_rn(v.z[i], __dmul_rn(alpha, v.p[i]));
@@ -875,7 +890,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
             // the next step's slab copies (async proxy) overwrite these generic writes
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         } else {
-            for (std::int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+            for (std::int64_t t = me; t < T.ntiles; t += gridDim.x) {
                 const std::int64_t row0 = T.tile_row0[t], row1 = T.tile_row0[t + 1];
                 for (std::int64_t i = row0 + tid; i < row1; i += kTileThreads)
                     v.p[i] = __dadd_rn(v.r[i], __dmul_rn(beta, v.p[i]));
@@ -1048,6 +1063,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 #if LILAC_CTA_TRACE
 // Experiment builds only (tools/cta_trace.py): per CTA of the last standalone
 // tiled SpMV launch: SM id, entry, first slab landed, walk done, exit (ns).
+extern "C" int b200_debug_cg_rot(unsigned rot) {
+    return cudaMemcpyToSymbol(g_cg_rot, &rot, sizeof rot) == cudaSuccess ? 0 : 1;
+}
+extern "C" int b200_debug_cg_smid(unsigned* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_cg_smid, sizeof(unsigned) * std::min(n, kCgTraceCtas)) == cudaSuccess ? 0 : 1;
+}
 extern "C" int b200_debug_cg_trace(unsigned long long* out, int n) {
     return cudaMemcpyFromSymbol(out, g_cg_trace,
                                 sizeof(unsigned long long) * std::min(n, kCgTraceSteps * kCgTraceCtas * 8)) ==

@@ -57,3 +57,42 @@ c = np.corrcoef(w[::2].mean(axis=0), w[1::2].mean(axis=0))[0, 1]
 print(f"per-CTA walk time, even vs odd steps: correlation {c:.2f}; CTA means min/avg/max "
       f"{w.mean(axis=0).min():.2f}/{w.mean():.2f}/{w.mean(axis=0).max():.2f} us; per-step spread (max-avg) "
       f"{(w.max(axis=1) - w.mean(axis=1)).mean():.2f} us")
+
+# systematic by SM or by tile? launch A with CTA b on tile b, launch B with
+# CTA b on tile (b + 37) % grid; compare per-SM and per-tile mean walk times
+def launch_walk(rot):
+    assert L.b200_debug_cg_rot(rot) == 0
+    cg.outer(110.0, 25, s)
+    torch.cuda.synchronize()
+    assert L.b200_debug_cg_trace(buf, STEPS * CTAS * 8) == 0
+    sm = (C.c_uint * CTAS)()
+    assert L.b200_debug_cg_smid(sm, CTAS) == 0
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(STEPS, CTAS, 8).astype(np.int64)[1:25, :grid]
+    wk = ((t[:, :, 3] - t[:, :, 2]) / 1e3).mean(axis=0)
+    by_sm = {int(sm[b]): wk[b] for b in range(grid)}
+    by_tile = {(b + rot) % grid: wk[b] for b in range(grid)}
+    return by_sm, by_tile
+sa, ta = launch_walk(0)
+sb, tb = launch_walk(37)
+assert L.b200_debug_cg_rot(0) == 0
+ks = sorted(set(sa) & set(sb))
+print(f"per-SM walk time, launch A vs B (tiles rotated by 37): correlation "
+      f"{np.corrcoef([sa[k] for k in ks], [sb[k] for k in ks])[0, 1]:.2f}; per-tile: "
+      f"{np.corrcoef([ta[k] for k in range(grid)], [tb[k] for k in range(grid)])[0, 1]:.2f}")
+
+# what explains the per-tile part? tile rows (row starts) vs nnz (tiles are nnz-balanced)
+nt = grid
+nnz_total = int(rp[-1])
+bnd = [0]
+for g in range(1, nt):
+    tgt = (nnz_total * g + nt - 1) // nt
+    r = int(np.searchsorted(rp, tgt, side="left"))
+    bnd.append(max(min(r, len(rp) - 1), bnd[-1]))
+bnd.append(len(rp) - 1)
+bnd = np.array(bnd)
+rows_t = np.diff(bnd)
+nnz_t = rp[bnd[1:]] - rp[bnd[:-1]]
+tm = np.array([(ta[k] + tb[k]) / 2 for k in range(nt)])
+print(f"per-tile walk time vs rows: corr {np.corrcoef(tm, rows_t)[0, 1]:.2f}; vs nnz: {np.corrcoef(tm, nnz_t)[0, 1]:.2f}; "
+      f"rows min/max {rows_t.min()}/{rows_t.max()}, nnz min/max {nnz_t.min()}/{nnz_t.max()}; "
+      f"walk by tile index (first/last 10): {np.round(tm[:10], 1)} ... {np.round(tm[-10:], 1)}")
