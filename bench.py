@@ -1068,9 +1068,13 @@ def run_kron(ctx):
     x = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
     w = torch.empty_like(x)
     nsteps = args.warmup + args.steps
-    ms_total, clk = ctx.timed_steps(lambda: A.pagerank(DAMPING, 1, x.data_ptr(), w.data_ptr(), ctx.sh),
-                                    args.warmup, args.steps)
-    x_dev = x.cpu().numpy()
+    bufs = [x, w]  # the iterate ping-pongs: step i reads bufs[i % 2] and writes the other
+
+    def pr_step():
+        A.pagerank_step(DAMPING, bufs[0].data_ptr(), bufs[1].data_ptr(), ctx.sh)
+        bufs.reverse()
+    ms_total, clk = ctx.timed_steps(pr_step, args.warmup, args.steps)
+    x_dev = bufs[0].cpu().numpy()
     ms_step = ms_total / args.steps
     flops = 2 * nnz + 2 * n
     value = flops / (ms_step * 1e-3) / 1e9
@@ -1087,7 +1091,10 @@ def run_kron(ctx):
                     "bytes_per_call": by, "kernel": kname, "max_row": info["max_row"]}
     line["roofline"] = roofline(by, spmv_ms, kname, "CSR algorithmic bytes per launch / mean of back-to-back launches "
                                 "(CUDA events, bench stream)", "kron")
-    line["gpu_launches"] = args.steps * {6: 4, 5: 3}.get(info["kernel"], 2)  # (+ hot gather, fix-up | counter reset), update
+    pr_fused = info["kernel"] == 6 and os.environ.get("LILAC_B200_PAGERANK_FUSED", "1") != "0"
+    # lane-range: hot gather, main, fix-up (the update folded into the row stores); else SpMV (+ counter reset) + update
+    line["gpu_launches"] = args.steps * (3 if pr_fused else {6: 4, 5: 3}.get(info["kernel"], 2))
+    line["pagerank_update"] = "fused into the lane-range row stores" if pr_fused else "separate kernel"
     line["clocks"] = clk
     line["marshal_first_call"] = {"s": t_marshal, "h2d_bytes": int(nnz * 16 + (n + 1) * 8),
                                   "device_bytes": info["device_bytes"]}

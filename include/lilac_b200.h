@@ -239,6 +239,11 @@ int b200_matrix_create_stencil27_rows(b200_matrix** out, int64_t nx, int64_t r0,
  * transposed adjacency; x holds the start vector (e.g. 1/n). */
 int b200_pagerank_device(const b200_matrix* A, double damping, int iters, double* x_device, double* work_device,
                          void* stream);
+/* One PageRank step y = damping*(A x) + (1-damping)/rows into another device
+ * vector (y must not alias x). On the lane-range layout the update is folded
+ * into the SpMV's row stores (one pass, the same bits as SpMV + update). */
+int b200_pagerank_step_device(const b200_matrix* A, double damping, const double* x_device, double* y_device,
+                              void* stream);
 
 /* Device buffers for harness TUs generated from a LiLAC-How spec
  * (paper_2001_07938_b200/specs/b200.lilac, emitted by the reference's own

@@ -84,6 +84,7 @@ SIGNATURES = {
     "b200_matrix_create_stencil27": (C.c_int, [C.POINTER(C.c_void_p), i64, C.c_double, C.c_double]),
     "b200_matrix_create_stencil27_rows": (C.c_int, [C.POINTER(C.c_void_p), i64, i64, i64, C.c_double, C.c_double]),
     "b200_pagerank_device": (C.c_int, [vp, C.c_double, C.c_int, vp, vp, vp]),
+    "b200_pagerank_step_device": (C.c_int, [vp, C.c_double, vp, vp, vp]),
     "b200_cg_solve": (C.c_int, [vp, vp, C.c_int, vp, C.POINTER(C.c_double)]),
     "b200_dbuf_alloc": (C.c_int, [C.POINTER(B200Buf), C.c_size_t]),
     "b200_dbuf_upload": (C.c_int, [C.POINTER(B200Buf), vp, C.c_size_t]),

@@ -331,6 +331,10 @@ void launch_spmv_merge(const CsrDev& A, const double* x, double* y, cudaStream_t
 void launch_spmv_split(const CsrDev& A, const double* x, double* y, cudaStream_t s);
 // y = A x on the lane-range layout (lrcsr.cu): hot-x gather, main kernel, carry fix-up.
 void launch_spmv_lrc(const LrcDev& L, std::int64_t rows, const double* x, double* y, cudaStream_t s);
+// One PageRank step on the lane-range layout, the update fused into the row
+// stores: y = d * (A x) + (1 - d) / rows, the same bits as the SpMV followed by
+// launch_pagerank_update. y must not alias x. false: not applicable (no units).
+bool launch_pagerank_lrc(const LrcDev& L, std::int64_t rows, const double* x, double* y, double d, cudaStream_t s);
 // p.q of a finished SpMV into the CG scalars (alpha, or the shard partial).
 void launch_cg_dot_scalars(const double* p, const double* q, std::int64_t n, double* partials, unsigned int* ticket,
                            CgScalars* sc, cudaStream_t s);

@@ -8,6 +8,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <utility>
 #include <memory>
 
 using namespace b200;
@@ -270,16 +273,57 @@ int b200_matrix_create_stencil27_rows(b200_matrix** out, std::int64_t nx, std::i
     });
 }
 
+// LILAC_B200_PAGERANK_FUSED=0: SpMV + update kernels (experiments)
+static bool fused_pagerank() {
+    static const bool on = [] {
+        const char* e = std::getenv("LILAC_B200_PAGERANK_FUSED");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
 int b200_pagerank_device(const b200_matrix* A, double damping, int iters, double* x, double* work, void* stream) {
     return boundary("b200_pagerank_device", [&] {
         if (!A || A->format != 0) throw Error(Errc::DataError, "PageRank needs a CSR matrix");
         if (A->csr.rows != A->csr.cols && A->csr.cols > A->csr.rows)
             throw Error(Errc::DataError, "PageRank needs a square operator");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
+        // the lane-range layout folds the update into its row stores: the
+        // iterate ping-pongs between x and work (one pass per step instead of
+        // SpMV + update), copied back into x after an odd number of steps
+        const bool fused = A->csr.lrc && iters > 0 && A->csr.lrc->units > 0 && fused_pagerank();
+        double* cur = x;
+        double* nxt = work;
         for (int it = 0; it < iters; ++it) {
+            if (fused && launch_pagerank_lrc(*A->csr.lrc, A->csr.rows, cur, nxt, damping, s)) {
+                std::swap(cur, nxt);
+                continue;
+            }
+            if (cur != x) {  // (not reached: a layout either fuses every step or none)
+                B200_CUDA(cudaMemcpyAsync(x, cur, sizeof(double) * static_cast<std::size_t>(A->csr.rows),
+                                          cudaMemcpyDeviceToDevice, s));
+                cur = x;
+                nxt = work;
+            }
             launch_spmv_csr(A->csr, x, work, rt().kernel, s);
             launch_pagerank_update(A->csr.rows, x, work, damping, s);
         }
+        if (cur != x)
+            B200_CUDA(cudaMemcpyAsync(x, cur, sizeof(double) * static_cast<std::size_t>(A->csr.rows),
+                                      cudaMemcpyDeviceToDevice, s));
+    });
+}
+
+int b200_pagerank_step_device(const b200_matrix* A, double damping, const double* x, double* y, void* stream) {
+    return boundary("b200_pagerank_step_device", [&] {
+        if (!A || A->format != 0) throw Error(Errc::DataError, "PageRank needs a CSR matrix");
+        if (A->csr.rows != A->csr.cols && A->csr.cols > A->csr.rows)
+            throw Error(Errc::DataError, "PageRank needs a square operator");
+        if (x == y) throw Error(Errc::DataError, "PageRank step: y must not alias x");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (A->csr.lrc && fused_pagerank() && launch_pagerank_lrc(*A->csr.lrc, A->csr.rows, x, y, damping, s)) return;
+        launch_spmv_csr(A->csr, x, y, rt().kernel, s);
+        launch_pagerank_update(A->csr.rows, y, y, damping, s);  // elementwise in place
     });
 }
 

@@ -83,6 +83,14 @@ __device__ __forceinline__ std::int64_t out_row(const LrcDev& L, std::uint32_t r
     return RMAP ? static_cast<std::int64_t>(__ldg(L.rmap + r)) : static_cast<std::int64_t>(r);
 }
 
+// The value a finished row stores: the SpMV's sum, or with PR the PageRank
+// update d * sum + (1 - d) / n applied in the same store (exactly
+// k_pagerank_update's operations: the same bits as SpMV + update).
+template <bool PR>
+__device__ __forceinline__ double row_out(double v, double d, double tele) {
+    return PR ? __dadd_rn(__dmul_rn(d, v), tele) : v;
+}
+
 // A lane's walk over its range: the compact row being summed and its partial,
 // the head partial (the lane's first row, begun before the lane) once closed.
 struct LWalk {
@@ -91,21 +99,21 @@ struct LWalk {
     bool in_head;
 };
 
-template <bool RMAP>
+template <bool RMAP, bool PR>
 __device__ __forceinline__ void lwalk_one(LWalk& w, double v, double xv, std::uint32_t c, const LrcDev& L,
-                                          double* __restrict__ y) {
+                                          double* __restrict__ y, double d, double tele) {
     const bool st = (c & kLrcStart) != 0u;
     // a row that began and ended inside this lane is complete: store it
-    if (st && !w.in_head) y[out_row<RMAP>(L, w.row)] = w.acc;
+    if (st && !w.in_head) y[out_row<RMAP>(L, w.row)] = row_out<PR>(w.acc, d, tele);
     w.head = st && w.in_head ? w.acc : w.head;
     w.in_head = w.in_head && !st;
     w.row += st ? 1u : 0u;
     w.acc = fma(v, xv, st ? 0.0 : w.acc);
 }
 
-template <bool HOT, bool RMAP>
+template <bool HOT, bool RMAP, bool PR>
 __global__ void __launch_bounds__(kLrcThreads, 1)
-    k_spmv_lrc(LrcDev L, const double* __restrict__ x, double* __restrict__ y) {
+    k_spmv_lrc(LrcDev L, const double* __restrict__ x, double* __restrict__ y, double pr_d, double pr_tele) {
     extern __shared__ __align__(128) double xs[];
     __shared__ __align__(8) std::uint64_t mbar;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -163,7 +171,7 @@ __global__ void __launch_bounds__(kLrcThreads, 1)
             LChunk na;
             if (i + 2 < kLrcChunks) load_lchunk(na, L, e0 + 128 * (i + 2), pol);
 #pragma unroll
-            for (int s = 0; s < 4; ++s) lwalk_one<RMAP>(w, ca.v[s], xa[s], ca.c[s], L, y);
+            for (int s = 0; s < 4; ++s) lwalk_one<RMAP, PR>(w, ca.v[s], xa[s], ca.c[s], L, y, pr_d, pr_tele);
             ca = cb;
             if (i + 2 < kLrcChunks) cb = na;
         }
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(kLrcThreads, 1)
         const bool closes = lane > 0 && split;
         const bool fresh = ((sm >> segprev) & 1u) != 0u;
         const double tot = Sprev + w.head;  // w.head is 0 for a lane whose first nonzero starts a row
-        if (closes && fresh) y[out_row<RMAP>(L, rprev)] = tot;
+        if (closes && fresh) y[out_row<RMAP>(L, rprev)] = row_out<PR>(tot, pr_d, pr_tele);
         // carries: the row open at the unit's start (lane 0 continues it)
         const bool cont0 = __shfl_sync(kFull, static_cast<int>(cont), 0) != 0;
         const int b = sm ? __ffs(static_cast<int>(sm & ~1u)) - 1 : -1;  // first split lane > 0
@@ -224,17 +232,17 @@ __global__ void k_lrc_gather_hot(const std::int32_t* __restrict__ cols, int hot,
 // Rows that crossed units (the structural plan): a short crossing is summed
 // by one thread in unit order, a long one by a warp (lanes stride the units,
 // then a fixed shuffle tree). Empty rows (never in the stream) are zeroed here.
-template <bool RMAP>
-__global__ void k_lrc_fixup(LrcDev L, double* __restrict__ y) {
+template <bool RMAP, bool PR>
+__global__ void k_lrc_fixup(LrcDev L, double* __restrict__ y, double pr_d, double pr_tele) {
     const std::int64_t tid = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t i = tid; i < L.nempty; i += stride) y[__ldg(L.empty + i)] = 0.0;
+    for (std::int64_t i = tid; i < L.nempty; i += stride) y[__ldg(L.empty + i)] = row_out<PR>(0.0, pr_d, pr_tele);
     pdl_wait();  // every unit's carry is written
     for (std::int64_t i = tid; i < L.nfix_short; i += stride) {
         const LrcFix f = L.fix[i];
         double tot = __ldcg(&L.carry[f.u].tail_val);
         for (int v = f.u + 1; v <= f.e; ++v) tot += __ldcg(&L.carry[v].head_val);
-        y[out_row<RMAP>(L, static_cast<std::uint32_t>(f.row))] = tot;
+        y[out_row<RMAP>(L, static_cast<std::uint32_t>(f.row))] = row_out<PR>(tot, pr_d, pr_tele);
     }
     const int lane = threadIdx.x & 31;
     for (std::int64_t i = tid >> 5; i < L.nfix_long; i += stride >> 5) {
@@ -243,18 +251,21 @@ __global__ void k_lrc_fixup(LrcDev L, double* __restrict__ y) {
         for (int v = f.u + 1 + lane; v <= f.e; v += 32) part += __ldcg(&L.carry[v].head_val);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-        if (lane == 0) y[out_row<RMAP>(L, static_cast<std::uint32_t>(f.row))] = __ldcg(&L.carry[f.u].tail_val) + part;
+        if (lane == 0)
+            y[out_row<RMAP>(L, static_cast<std::uint32_t>(f.row))] =
+                row_out<PR>(__ldcg(&L.carry[f.u].tail_val) + part, pr_d, pr_tele);
     }
 }
 
 int g_lrc_sms = 0;
 
-template <bool HOT, bool RMAP>
-void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
+template <bool HOT, bool RMAP, bool PR = false>
+void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s, double pr_d = 0.0,
+                double pr_tele = 0.0) {
     static std::uint64_t attr = 0;
     const std::size_t smem = HOT ? sizeof(double) * static_cast<std::size_t>(kLrcHotMax + 2) : 0;
     if (first_on_device(attr))
-        B200_CUDA(cudaFuncSetAttribute(k_spmv_lrc<HOT, RMAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B200_CUDA(cudaFuncSetAttribute(k_spmv_lrc<HOT, RMAP, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(std::min<std::int64_t>(g_lrc_sms, (L.units + kLrcWarps - 1) / kLrcWarps)));
@@ -266,7 +277,7 @@ void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = HOT ? 1 : 0;
-    B200_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_lrc<HOT, RMAP>, L, x, y));
+    B200_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_lrc<HOT, RMAP, PR>, L, x, y, pr_d, pr_tele));
     cudaLaunchConfig_t fc{};
     const std::int64_t work = std::max({L.nfix_short, 32 * L.nfix_long, L.nempty});
     const std::int64_t fb = std::min<std::int64_t>((work + 255) / 256, 148 * 8);
@@ -275,7 +286,7 @@ void lrc_launch(const LrcDev& L, const double* x, double* y, cudaStream_t s) {
     fc.stream = s;
     fc.attrs = at;
     fc.numAttrs = 1;  // launched early; zeroes the empty rows, then waits for every carry
-    B200_CUDA(cudaLaunchKernelEx(&fc, k_lrc_fixup<RMAP>, L, y));
+    B200_CUDA(cudaLaunchKernelEx(&fc, k_lrc_fixup<RMAP, PR>, L, y, pr_d, pr_tele));
 }
 
 }  // namespace
@@ -582,6 +593,24 @@ void launch_spmv_lrc(const LrcDev& L, std::int64_t rows, const double* x, double
     else
         lrc_launch<true, false>(L, x, y, s);
     B200_CUDA(cudaGetLastError());
+}
+
+bool launch_pagerank_lrc(const LrcDev& L, std::int64_t rows, const double* x, double* y, double d, cudaStream_t s) {
+    if (rows <= 0 || L.units == 0) return false;  // nothing streamed: the caller's SpMV + update
+    if (!g_lrc_sms) {
+        int dev = 0;
+        B200_CUDA(cudaGetDevice(&dev));
+        B200_CUDA(cudaDeviceGetAttribute(&g_lrc_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const double tele = (1.0 - d) / static_cast<double>(rows);
+    k_lrc_gather_hot<<<(L.hot + 1 + 255) / 256, 256, 0, s>>>(L.hot_cols, L.hot, x, L.x_hot);
+    B200_CUDA(cudaGetLastError());
+    if (L.rmap)
+        lrc_launch<true, true, true>(L, x, y, s, d, tele);
+    else
+        lrc_launch<true, false, true>(L, x, y, s, d, tele);
+    B200_CUDA(cudaGetLastError());
+    return true;
 }
 
 }  // namespace b200

@@ -56,6 +56,11 @@ class Matrix:
         N.check(N.lib().b200_pagerank_device(self._h, float(damping), int(iters), C.c_void_p(x_ptr),
                                              C.c_void_p(work_ptr), C.c_void_p(stream)))
 
+    def pagerank_step(self, damping: float, x_ptr: int, y_ptr: int, stream: int = 0):
+        """y = damping*(A x) + (1-damping)/n into another device vector."""
+        N.check(N.lib().b200_pagerank_step_device(self._h, float(damping), C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                                  C.c_void_p(stream)))
+
     def info(self) -> dict:
         i = N.MatrixInfo()
         N.check(N.lib().b200_matrix_info_get(self._h, C.byref(i)))

@@ -747,6 +747,37 @@ def test_pagerank_device_matches_host_iteration():
     A.free()
 
 
+@pytest.mark.parametrize("steps", [20, 21])
+def test_pagerank_lane_range_fused_update(steps):
+    """The lane-range layout folds the PageRank update into its row stores
+    (rows stored in the main kernel, rows crossing units in the fix-up, empty
+    rows = the teleport term); an odd step count ends with a copy back into x."""
+    import torch
+    rng = np.random.default_rng(9)
+    n = 20000
+    src = rng.integers(0, n, 300000)
+    dst = (rng.pareto(1.2, 300000) * 40).astype(np.int64) % n  # skewed in-degrees, many empty rows
+    outdeg = np.bincount(src, minlength=n).astype(np.float64)
+    order = np.lexsort((src, dst))
+    src, dst = src[order], dst[order]
+    rp = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
+    ci = src.astype(np.int64)
+    val = 1.0 / outdeg[src]
+    N.lib().b200_set_kernel(b"lane")
+    A = D.Matrix.csr(rp, ci, val)
+    assert A.info()["kernel"] == 6
+    x = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    w = torch.empty_like(x)
+    A.pagerank(0.85, steps, x.data_ptr(), w.data_ptr())
+    torch.cuda.synchronize()
+    xr = np.full(n, 1.0 / n)
+    for _ in range(steps):
+        xr = 0.85 * O.spmv_csr(rp, ci, val, xr) + 0.15 / n
+    xd = x.cpu().numpy()
+    assert np.all(np.abs(xd - xr) <= 1e-12 * np.abs(xr) + 1e-18), np.max(np.abs(xd - xr) / np.abs(xr))
+    A.free()
+
+
 def test_cg_solve_on_the_stencil_converges():
     import torch
     nx = 24
