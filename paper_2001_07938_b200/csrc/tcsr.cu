@@ -991,12 +991,56 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     double* pq_part = v.partials;
     double* rr_part = v.partials + 2 * kMaxParts;
     const std::int64_t* send = d.send;
+    // One tile per CTA (one shard per GPU): the tile's z, p, r rows are
+    // bulk-copied into the slab buffer that goes idle at the penultimate slab
+    // (k_cg_tiled's staging), q stays in the y buffer, and the updates below
+    // run from shared memory
+    const bool one_tile = T.parts == 1 && T.ntiles <= cpr && cta < T.ntiles;
+    const std::int64_t crow0 = one_tile ? T.tile_row0[cta] : 0;
+    const int cn = one_tile ? static_cast<int>(T.tile_row0[cta + 1] - crow0) : 0;
+    const bool staged = kCgAsyncStage && one_tile && T.nslabs >= 2 && 3 * stage_pitch(cn) <= c.stride;
+    const int sbuf = (T.nslabs - 2) & 1;
+    double* zs = c.xs + sbuf * c.stride + static_cast<int>(crow0 & 1);
+    double* ps = zs + stage_pitch(cn);
+    double* rs = zs + 2 * stage_pitch(cn);
+    // the next step's first runs of this CTA's first item (L2 prefetch
+    // during the exchanges), bounds loaded once into shared memory
+    __shared__ int pf_lo[kTileWarps], pf_hi[kTileWarps];
+    __shared__ const double* pf_vb;
+    __shared__ const std::uint16_t* pf_kb;
+    const bool pf_on = kCgPrefetch > 0 && cta < T.ntiles * T.parts;
+    if (pf_on) {
+        const std::int64_t t = cta / T.parts;
+        const int part = static_cast<int>(cta - t * T.parts);
+        const int k0 = part * T.nslabs / T.parts, k1 = (part + 1) * T.nslabs / T.parts;
+        const std::int32_t* wo = T.woff + t * (static_cast<std::int64_t>(T.nslabs) * kTileWarps + 1);
+        if (tid == 0) {
+            pf_vb = T.val + T.tile_base[t];
+            pf_kb = T.key + T.tile_base[t];
+        }
+        if (tid < kTileWarps) {
+            pf_lo[tid] = k0 < k1 ? wo[k0 * kTileWarps + tid] : 0;
+            pf_hi[tid] = k0 < k1 ? wo[k0 * kTileWarps + tid + 1] : 0;
+        }
+    }
+    __syncthreads();
+    if (staged) {
+        c.st_z = v.z;
+        c.st_p = v.p;
+        c.st_r = v.r;
+        c.st_row0 = crow0;
+        c.st_n = cn;
+        c.st_buf = sbuf;
+        c.st_ps = ps;
+    }
     for (int it = 0; it < steps; ++it) {
         // q = A p over the shard once every sender's p slice (epoch e) is in
         const FlagGate fg{d.mb.flags, d.world, e, d.mb.err};
         const double pq = cta_sum(spmv_tiles<true, 0, true>(T, v.p_full, v.q, v.row0, c, nullptr, 0, &fg, cta, cpr),
                                   red);
         if (tid == 0) pq_part[cta] = pq;
+        if (pf_on && it + 1 < steps && (tid & 31) == 0 && pf_lo[tid >> 5] < pf_hi[tid >> 5])
+            prefetch_run(pf_vb, pf_kb, pf_lo[tid >> 5], pf_hi[tid >> 5]);
         slot_sync(S.bar, target, static_cast<unsigned>(cpr), d.mb.err);
         const double dpart = T.parts > 1 ? cta_sum_parts(T.tile_pq, static_cast<int>(T.ntiles), red)
                                          : cta_sum_parts(pq_part, cpr, red);
@@ -1012,13 +1056,24 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             v.sc->alpha = alpha;
         }
         double rr = 0.0;
-        for (std::int64_t i = static_cast<std::int64_t>(cta) * kTileThreads + tid; i < v.n;
-             i += static_cast<std::int64_t>(cpr) * kTileThreads) {
-            const double zi = __dadd_rn(__ldcg(v.z + i), __dmul_rn(alpha, __ldcg(v.p + i)));
-            const double ri = __dsub_rn(__ldcg(v.r + i), __dmul_rn(alpha, __ldcg(v.q + i)));
-            v.z[i] = zi;
-            v.r[i] = ri;
-            rr += ri * ri;
+        if (staged) {
+            for (int r = tid; r < cn; r += kTileThreads) {
+                const double zi = __dadd_rn(zs[r], __dmul_rn(alpha, ps[r]));
+                const double ri = __dsub_rn(rs[r], __dmul_rn(alpha, c.yp[r]));
+                v.z[crow0 + r] = zi;
+                v.r[crow0 + r] = ri;
+                rs[r] = ri;
+                rr += ri * ri;
+            }
+        } else {
+            for (std::int64_t i = static_cast<std::int64_t>(cta) * kTileThreads + tid; i < v.n;
+                 i += static_cast<std::int64_t>(cpr) * kTileThreads) {
+                const double zi = __dadd_rn(__ldcg(v.z + i), __dmul_rn(alpha, __ldcg(v.p + i)));
+                const double ri = __dsub_rn(__ldcg(v.r + i), __dmul_rn(alpha, __ldcg(v.q + i)));
+                v.z[i] = zi;
+                v.r[i] = ri;
+                rr += ri * ri;
+            }
         }
         rr = cta_sum(rr, red);
         if (tid == 0) rr_part[cta] = rr;
@@ -1037,14 +1092,36 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         rho = rho_new;
         // p = r + beta p on the owned rows, stored here and into every peer's
         // replica rows its SpMV reads
-        for (std::int64_t i = static_cast<std::int64_t>(cta) * kTileThreads + tid; i < v.n;
-             i += static_cast<std::int64_t>(cpr) * kTileThreads) {
-            const double pv = __dadd_rn(__ldcg(v.r + i), __dmul_rn(beta, __ldcg(v.p + i)));
-            v.p[i] = pv;
-            for (int r = 0; r < d.world; ++r)
-                if (r != d.rank && i >= send[2 * r] && i < send[2 * r + 1]) d.peers[r].p_full[v.row0 + i] = pv;
+        bool pushed = false;  // this thread stored into a peer's replica
+        if (staged) {
+            for (int r = tid; r < cn; r += kTileThreads) {
+                const std::int64_t i = crow0 + r;
+                const double pv = __dadd_rn(rs[r], __dmul_rn(beta, ps[r]));
+                v.p[i] = pv;
+                for (int q = 0; q < d.world; ++q)
+                    if (q != d.rank && i >= send[2 * q] && i < send[2 * q + 1]) {
+                        d.peers[q].p_full[v.row0 + i] = pv;
+                        pushed = true;
+                    }
+            }
+            // the next step's slab copies (async proxy) overwrite the staged rows
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        } else {
+            for (std::int64_t i = static_cast<std::int64_t>(cta) * kTileThreads + tid; i < v.n;
+                 i += static_cast<std::int64_t>(cpr) * kTileThreads) {
+                const double pv = __dadd_rn(__ldcg(v.r + i), __dmul_rn(beta, __ldcg(v.p + i)));
+                v.p[i] = pv;
+                for (int r = 0; r < d.world; ++r)
+                    if (r != d.rank && i >= send[2 * r] && i < send[2 * r + 1]) {
+                        d.peers[r].p_full[v.row0 + i] = pv;
+                        pushed = true;
+                    }
+            }
         }
-        __threadfence_system();
+        // peer stores are made visible system-wide by their own thread before
+        // the shard barrier; local stores are covered by the barrier and the
+        // flag's release
+        if (pushed) __threadfence_system();
         slot_sync(S.bar, target, static_cast<unsigned>(cpr), d.mb.err);
         ++e;
         if (cta == 0 && tid == 0) {

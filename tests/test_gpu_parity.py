@@ -569,7 +569,7 @@ def test_sharded_cg_peer_memory_exchange_local(cls, k):
     d.free()
 
 
-@pytest.mark.parametrize("cls,k", [("A", 1), ("A", 2), ("A", 3), ("A", 8), ("C", 2), ("C", 4), ("C", 8)])
+@pytest.mark.parametrize("cls,k", [("A", 1), ("A", 2), ("A", 3), ("A", 8), ("C", 1), ("C", 2), ("C", 4), ("C", 8)])
 def test_sharded_cg_fused_persistent_kernel(cls, k):
     """The sharded CG in one persistent kernel (k_cg_tiled_dist): k local
     shards as k CTA groups of one cooperative grid, exchanging p slices and
