@@ -496,6 +496,9 @@ __device__ __forceinline__ double spmv_tiles(const TcsrDev& T, const double* x, 
             issue_slab(T, x, xs, k0, &c.mbar[0], MODE == 8 || MODE == 9);
             if (k0 + 1 < k1) issue_slab(T, x, xs + c.stride, k0 + 1, &c.mbar[1], MODE == 8 || MODE == 9);
         }
+        // one slab: buffer 1 idles the whole SpMV, so the fused CG's rows of
+        // this CTA (its own data) are staged there from the start
+        if (COHERENT && tid == 0 && c.st_n > 0 && P == 1 && k1 - k0 == 1) issue_stage(c, xs + c.stride, &c.mbar[1]);
         __syncthreads();
         // Free-running slabs: a warp moves on as soon as the next slab has
         // landed; the last warp to release a buffer refills it (no CTA barrier).
@@ -789,15 +792,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_cg_tiled(TcsrDev T, CgVecto
     __syncthreads();
     // One tile per CTA: the tile's z, p, r rows are staged into a slab buffer
     // and q stays in the y buffer, so the updates below touch no global loads.
-    // With two or more slabs the staging is three bulk copies issued when the
-    // penultimate slab's buffer is released (they land during the last slab's
-    // walk); otherwise loads after the SpMV.
+    // The staging is three bulk copies issued when the penultimate slab's
+    // buffer is released (they land during the last slab's walk), or with a
+    // single slab at the SpMV's start into the idle second buffer; loads after
+    // the SpMV only when the rows do not fit one buffer.
     const bool one_tile = T.parts == 1 && T.ntiles <= gridDim.x && me < T.ntiles;
     const std::int64_t crow0 = one_tile ? T.tile_row0[me] : 0;
     const int cn = one_tile ? static_cast<int>(T.tile_row0[me + 1] - crow0) : 0;
-    const bool async_stage = kCgAsyncStage && one_tile && T.nslabs >= 2 && 3 * stage_pitch(cn) <= c.stride;
+    const bool async_stage = kCgAsyncStage && one_tile && T.nslabs >= 1 && 3 * stage_pitch(cn) <= c.stride;
     const bool cached = async_stage || (one_tile && 3 * cn <= 2 * c.stride);  // z, p, r rows fit the slab buffers
-    const int sbuf = (T.nslabs - 2) & 1;  // the buffer of slab nslabs - 2
+    const int sbuf = T.nslabs >= 2 ? (T.nslabs - 2) & 1 : 1;  // the buffer of slab nslabs - 2 (one slab: buffer 1)
     const int sh = static_cast<int>(crow0 & 1), pitch = stage_pitch(cn);
     double* zs = async_stage ? c.xs + sbuf * c.stride + sh : c.xs;
     double* ps = async_stage ? zs + pitch : c.xs + cn;
@@ -998,8 +1002,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const bool one_tile = T.parts == 1 && T.ntiles <= cpr && cta < T.ntiles;
     const std::int64_t crow0 = one_tile ? T.tile_row0[cta] : 0;
     const int cn = one_tile ? static_cast<int>(T.tile_row0[cta + 1] - crow0) : 0;
-    const bool staged = kCgAsyncStage && one_tile && T.nslabs >= 2 && 3 * stage_pitch(cn) <= c.stride;
-    const int sbuf = (T.nslabs - 2) & 1;
+    const bool staged = kCgAsyncStage && one_tile && T.nslabs >= 1 && 3 * stage_pitch(cn) <= c.stride;
+    const int sbuf = T.nslabs >= 2 ? (T.nslabs - 2) & 1 : 1;
     double* zs = c.xs + sbuf * c.stride + static_cast<int>(crow0 & 1);
     double* ps = zs + stage_pitch(cn);
     double* rs = zs + 2 * stage_pitch(cn);
