@@ -521,6 +521,7 @@ extern "C" void b200_spmv_jds(std::int64_t rows, double* output, const std::int6
         DevArray& dnz = state.m_nzcnt.acquire(nzcnt, rows * sizeof(*nzcnt), nullptr,
                                               [&](const void* in, std::size_t size, DevArray& out) {
                                                   upload(out, in, size);
+                                                  host_in(in, size);  // read on the host below (lazy ranges filled here)
                                                   state.seg = jds_segments(static_cast<const std::int64_t*>(in),
                                                                            rows);
                                                   state.validated = false;
