@@ -67,7 +67,7 @@ def test_partition_rows_bit_exact_vs_oracle(k):
         assert np.array_equal(D.partition_rows(rp, k), O.partition_rows(rp, k))
 
 
-@pytest.mark.parametrize("cls", ["S", "A"])
+@pytest.mark.parametrize("cls", ["S", "A", "C"])
 def test_gen_npb_bit_exact_vs_oracle_makea(cls):
     na, nonzer, _, shift, _ = D.NPB_CLASSES[cls]
     rp, ci, val = D.gen_npb(na, nonzer, shift)
