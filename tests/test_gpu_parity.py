@@ -898,3 +898,62 @@ def test_jds_unsorted_nzcnt_bitwise():
     nzcnt[7] = 0
     y = _run_jds(perm, nzcnt, jd_ptr, jval, jcol, x)
     assert O.same_bits(y, O.spmv_jds(nzcnt, perm, jval, jd_ptr, x, jcol))
+
+
+# --------------------------------------------------------------------------------
+# eager write-back into pageable memory (copy_engine.cpp: pinned chunks +
+# parallel host copies for outputs of 256 KB or more)
+# --------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("rows,offset", [(40000, 0), (200001, 0), (300000, 1), (131072, 3)])
+def test_large_pageable_output_written_back_exactly(rows, offset):
+    """The reference semantics on a plain (malloc'd) output: every element of
+    the output lands, nothing around it changes, whatever the size and the
+    8-byte alignment inside the allocation."""
+    rng = np.random.default_rng(rows + offset)
+    lens = rng.integers(0, 9, rows)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = rng.integers(0, rows, int(rp[-1])).astype(np.int64)
+    for i in range(0, rows, max(1, rows // 64)):  # a few sorted rows suffice for the exact kernel's order
+        ci[rp[i]:rp[i + 1]].sort()
+    val = rng.uniform(-2, 2, int(rp[-1]))
+    x = rng.uniform(-2, 2, rows)
+    N.lib().b200_set_kernel(b"exact")
+    buf = np.full(rows + offset + 5, 7.25)
+    y = buf[offset:offset + rows]
+    H.spmv_csr(rows, y, rp, val, x, ci)
+    assert O.same_bits(y, O.spmv_csr(rp, ci, val, x))
+    assert np.all(buf[:offset] == 7.25) and np.all(buf[offset + rows:] == 7.25)
+
+
+@pytest.mark.parametrize("kernel", [b"auto", b"lane"])
+def test_pagerank_step_api_ping_pong(kernel):
+    """b200_pagerank_step_device: y = d A x + (1-d)/n into another vector, the
+    update folded into the lane-range row stores or run in place after the
+    SpMV on other layouts; alternating buffers reproduces the host iteration."""
+    import torch
+    rng = np.random.default_rng(21)
+    n = 8000
+    src = rng.integers(0, n, 90000)
+    dst = rng.integers(0, n, 90000)
+    outdeg = np.bincount(src, minlength=n).astype(np.float64)
+    order = np.lexsort((src, dst))
+    src, dst = src[order], dst[order]
+    rp = np.concatenate([[0], np.cumsum(np.bincount(dst, minlength=n))]).astype(np.int64)
+    ci = src.astype(np.int64)
+    val = 1.0 / outdeg[src]
+    N.lib().b200_set_kernel(kernel)
+    A = D.Matrix.csr(rp, ci, val)
+    bufs = [torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.float64,
+                                                                                          device="cuda")]
+    for _ in range(7):
+        A.pagerank_step(0.85, bufs[0].data_ptr(), bufs[1].data_ptr())
+        bufs.reverse()
+    torch.cuda.synchronize()
+    xr = np.full(n, 1.0 / n)
+    for _ in range(7):
+        xr = 0.85 * O.spmv_csr(rp, ci, val, xr) + 0.15 / n
+    assert np.allclose(bufs[0].cpu().numpy(), xr, rtol=1e-12, atol=1e-15)
+    with pytest.raises(N.B200Error):
+        A.pagerank_step(0.85, bufs[0].data_ptr(), bufs[0].data_ptr())
+    A.free()
