@@ -38,7 +38,7 @@ std::size_t env_size(const char* name, std::size_t dflt) {
 }
 // tuning knobs (experiments): chunk KB, copy granule KB, workers, idle spin us
 const std::size_t kStage = env_size("LILAC_B200_D2H_STAGE_KB", 512) << 10;  // bytes per pinned chunk (two)
-const std::size_t kPart = env_size("LILAC_B200_D2H_PART_KB", 64) << 10;     // host-copy granule per grab
+const std::size_t kPart = env_size("LILAC_B200_D2H_PART_KB", 32) << 10;     // host-copy granule per grab
 const int kWorkers = static_cast<int>(env_size("LILAC_B200_D2H_WORKERS", 3));
 const int kSpinUs = static_cast<int>(env_size("LILAC_B200_D2H_SPIN_US", 1000));
 
